@@ -1,0 +1,233 @@
+"""Generate the golden fixtures by running the REFERENCE implementation.
+
+Run in the build container only (the reference does not exist on the GPU box):
+
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/make_golden.py
+
+The fixtures pin both the oracle restatement (``tests/test_oracle_golden.py``)
+and, through the oracle, the CUDA path (``tests/test_gpu_parity.py``).  Inputs
+are the seeded Gaussian tensors of ``oracle.htucker_oracle.gaussian_htensor``
+(or the reference's own ``random_htensor`` for the small-case sweep); the same
+host arrays are handed to the reference.  Recorded library versions are stored
+in every file under ``meta``.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+sys.path.insert(0, REF)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
+
+import htucker as ref  # noqa: E402
+from htucker import arith as ref_arith  # noqa: E402
+from htucker import kernels as ref_kernels  # noqa: E402
+
+from oracle import htucker_oracle as orc  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+
+
+def meta():
+    import scipy
+
+    cfg = np.show_config(mode="dicts")
+    blas = cfg.get("Build Dependencies", {}).get("blas", {})
+    return json.dumps({"numpy": np.__version__, "scipy": scipy.__version__,
+                       "blas": f"{blas.get('name')} {blas.get('version')}",
+                       "generator": "tests/golden/make_golden.py"})
+
+
+def to_ref(x: orc.HT):
+    tree = ref.build_balanced_tree(x.tree.d)
+    return ref.HTensor(tree, dict(x.U), dict(x.B), x.root.copy(), orthogonal=x.orthogonal)
+
+
+def pack(prefix: str, x, out: dict):
+    """Flatten an HT (oracle or reference) into npz keys ``prefix/<node>``."""
+    tree_n = 2 * x.tree.d - 1
+    for t in range(tree_n):
+        if t == 0:
+            arr = x.root_matrix if hasattr(x, "root_matrix") else x.root
+        elif (x.leaves if hasattr(x, "leaves") else x.U).get(t) is not None:
+            arr = (x.leaves if hasattr(x, "leaves") else x.U)[t]
+        else:
+            arr = (x.transfer if hasattr(x, "transfer") else x.B)[t]
+        out[f"{prefix}/{t}"] = np.ascontiguousarray(arr)
+
+
+def ref_sigmas(xr):
+    o = ref.orthogonalize(xr)
+    bh = ref.compute_bhat(o)
+    return o, bh, {t: ref_kernels.sym_eig_desc(bh[t])[1] for t in bh}
+
+
+def golden_c1():
+    a, c, x = orc.c1_inputs()
+    ar, cr = to_ref(a), to_ref(c)
+    xr = ref.add(ref.scale(ar, 2.0), ref.scale(cr, 1e-10))
+    ctl = ref.TruncationControl.fixed_rank(10)
+    tr = ref.truncate(xr, ctl)
+    o, bh, lam = ref_sigmas(xr)
+    out = {"meta": meta()}
+    pack("A", a, out)
+    pack("C", c, out)
+    pack("Xorth", o, out)
+    pack("T", tr, out)
+    for t in bh:
+        out[f"bhat/{t}"] = bh[t]
+        out[f"lam/{t}"] = lam[t]
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 15)])
+    out["norm_X"] = ref.norm(xr)
+    out["norm_T"] = ref.norm(tr)
+    out["ip_TT"] = ref.inner_product(tr, tr)
+    # truncation error through the orthogonalised difference (SURVEY finding 0.3.3)
+    out["trunc_err"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(xr, tr)).root_matrix))
+    np.savez_compressed(os.path.join(OUT, "c1.npz"), **out)
+
+
+def golden_small():
+    """The SPEC's intended oracle sweep: d in 2..5, n <= 4, k <= 3,
+    reference ``random_htensor`` inputs, every drop-in operation recorded."""
+    out = {"meta": meta()}
+    case = 0
+    for seed in range(40):
+        rng = np.random.default_rng(1000 + seed)
+        d = int(rng.integers(2, 6))
+        n = [int(v) for v in rng.integers(2, 5, size=d)]
+        tree = ref.build_balanced_tree(d)
+        ka = {t.index: int(min(rng.integers(1, 4), 3)) for t in tree.non_root}
+        # keep the generator's structural bounds (format.py:286-287, 296-299)
+        for leaf in tree.leaves:
+            ka[leaf.index] = min(ka[leaf.index], n[leaf.dim - 1])
+        for lev in reversed(tree.levels_top_down()):
+            for t in lev:
+                node = tree.node(t)
+                if not node.is_leaf and not node.is_root:
+                    s1, s2 = node.sons
+                    ka[t] = min(ka[t], ka[s1] * ka[s2])
+        a = ref.random_htensor(tree, n, ka, seed=2 * seed)
+        c = ref.random_htensor(tree, n, ka, seed=2 * seed + 1)
+        x = ref.add(a, ref.scale(c, 0.5))
+        p = f"case{case}"
+        out[f"{p}/d"] = d
+        out[f"{p}/n"] = np.array(n)
+        pack(f"{p}/A", a, out)
+        pack(f"{p}/C", c, out)
+        o, bh, lam = ref_sigmas(x)
+        pack(f"{p}/Xorth", o, out)
+        for t in bh:
+            out[f"{p}/bhat/{t}"] = bh[t]
+            out[f"{p}/lam/{t}"] = lam[t]
+        eps = 0.3 * ref.norm(x)
+        for tag, ctl in (("fix", ref.TruncationControl.fixed_rank(2)),
+                         ("eps", ref.TruncationControl.accuracy(eps)),
+                         ("both", ref.TruncationControl(eps=eps, max_rank=1))):
+            tr = ref.truncate(x, ctl)
+            out[f"{p}/ranks_{tag}"] = np.array([tr.rank(t) for t in range(1, 2 * d - 1)])
+            out[f"{p}/normT_{tag}"] = ref.norm(tr)
+            out[f"{p}/err_{tag}"] = float(np.linalg.norm(
+                ref.orthogonalize(ref.subtract(x, tr)).root_matrix))
+        out[f"{p}/eps"] = eps
+        out[f"{p}/ip_AC"] = ref.inner_product(a, c)
+        out[f"{p}/dense_X"] = ref.to_dense(x)
+        out[f"{p}/entry"] = np.array([ref.evaluate_entry(x, tuple(0 for _ in range(d))),
+                                      ref.evaluate_entry(x, tuple(v - 1 for v in n))])
+        case += 1
+    out["count"] = case
+    np.savez_compressed(os.path.join(OUT, "small.npz"), **out)
+
+
+def golden_shrink():
+    """Rank shrink in orthogonalize: leaf rank > n and k_t > k1*k2 after add
+    (arith.py:135-141, kernels.py:27-28)."""
+    tree = ref.build_balanced_tree(4)
+    a = ref.random_htensor(tree, [3, 2, 3, 4], {1: 4, 2: 3, 3: 3, 4: 2, 5: 2, 6: 2}, seed=7)
+    c = ref.random_htensor(tree, [3, 2, 3, 4], {1: 3, 2: 2, 3: 2, 4: 2, 5: 1, 6: 2}, seed=8)
+    x = ref.add(a, c)
+    o, bh, lam = ref_sigmas(x)
+    out = {"meta": meta()}
+    pack("A", a, out)
+    pack("C", c, out)
+    pack("Xorth", o, out)
+    for t in bh:
+        out[f"bhat/{t}"] = bh[t]
+        out[f"lam/{t}"] = lam[t]
+    out["ranks_X"] = np.array([x.rank(t) for t in range(1, 7)])
+    out["ranks_Xorth"] = np.array([o.rank(t) for t in range(1, 7)])
+    tr = ref.truncate(x, ref.TruncationControl.fixed_rank(2))
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 7)])
+    out["err_T"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(x, tr)).root_matrix))
+    np.savez_compressed(os.path.join(OUT, "shrink.npz"), **out)
+
+
+def golden_c2_d8():
+    """C2 at d=8 (n=1000, k=50): inputs regenerate from seeds 6/7; store the
+    gauge-invariant outputs only (the tensors are ~9 MB each)."""
+    a, c, x = orc.c2_inputs(8)
+    xr = ref.add(to_ref(a), to_ref(c))
+    tr = ref.truncate(xr, ref.TruncationControl.fixed_rank(50))
+    _, _, lam = ref_sigmas(xr)
+    out = {"meta": meta()}
+    for t in lam:
+        out[f"lam/{t}"] = lam[t]
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 15)])
+    out["ip_TT"] = ref.inner_product(tr, tr)
+    out["norm_X"] = ref.norm(xr)
+    out["trunc_err"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(xr, tr)).root_matrix))
+    np.savez_compressed(os.path.join(OUT, "c2_d8.npz"), **out)
+
+
+def golden_c3_small():
+    """Operator application + truncation (C3 shape, shrunk): d=4, n=6, k=3,
+    Laplace-sum operator, eps 1e-8*||Y|| with cap 3."""
+    tree = ref.build_balanced_tree(4)
+    otr = orc.balanced_tree(4)
+    x = orc.gaussian_htensor(otr, 6, 3, 11)
+    op = orc.laplace_operator(otr, 6)
+    rop = ref.HTOperator(tree, {t: [ref.GeneralizedMatrix.diagonal(w[0].data),
+                                    ref.GeneralizedMatrix.csr(w[1].data)] for t, w in op.W.items()},
+                         dict(op.H), op.root.copy())
+    xr = to_ref(x)
+    y = ref.apply_operator(rop, xr)
+    ctl = ref.TruncationControl(eps=1e-8 * ref.norm(y), max_rank=3)
+    tr = ref.truncate(y, ctl)
+    out = {"meta": meta()}
+    pack("X", x, out)
+    pack("Y", y, out)
+    out["dense_op"] = ref.operator_to_dense_matrix(rop)
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 7)])
+    out["norm_Y"] = ref.norm(y)
+    out["err_T"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(y, tr)).root_matrix))
+    _, _, lam = ref_sigmas(y)
+    for t in lam:
+        out[f"lam/{t}"] = lam[t]
+    np.savez_compressed(os.path.join(OUT, "c3_small.npz"), **out)
+
+
+def golden_spec():
+    """Known answers quoted in the SPEC."""
+    q, r = ref_kernels.reduced_qr(np.array([[3.0], [4.0]]))
+    v, lam = ref_kernels.sym_eig_desc(np.array([[2.0, 1.0], [1.0, 2.0]]))
+    t5 = ref.build_balanced_tree(5)
+    out = {"meta": meta(), "qr_q": q, "qr_r": r, "eig_lam": lam,
+           "tree5_intervals": np.array([n.interval for n in t5.nodes]),
+           "tree5_fathers": np.array([-1 if n.father is None else n.father for n in t5.nodes]),
+           "tree10_levels": np.array([n.level for n in ref.build_balanced_tree(10).nodes]),
+           "tree10_intervals": np.array([n.interval for n in ref.build_balanced_tree(10).nodes])}
+    np.savez_compressed(os.path.join(OUT, "spec.npz"), **out)
+
+
+if __name__ == "__main__":
+    golden_spec()
+    golden_small()
+    golden_shrink()
+    golden_c1()
+    golden_c3_small()
+    golden_c2_d8()
+    print("golden fixtures written to", OUT)
