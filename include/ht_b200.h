@@ -1,0 +1,172 @@
+/*
+ * ht_b200.h -- C ABI of the B200-native hierarchical-Tucker (HT) engine.
+ *
+ * The reference (arXiv 1708.03340, /root/reference/pkg/src/htucker) is a
+ * pure-Python package with no FFI; this header is the binding a
+ * ctypes/cffi/pybind shim would use to put the reference's HT tensor API on
+ * the GPU.  Every entry point names the reference function it replaces.
+ *
+ * Conventions
+ *  - float64 everywhere; all array pointers are DEVICE pointers unless noted.
+ *  - A tensor is described by its dimension d (the tree is the reference's
+ *    balanced dimension tree, tree.py:55-101: BFS node ids, root 0, 2d-1
+ *    nodes), leaf sizes, per-node ranks and one device pointer per node.
+ *    Node arrays are C-order exactly as in the reference HTensor
+ *    (format.py:50-132): root (k_s1 x k_s2), inner (k_t x k_s1 x k_s2),
+ *    leaf (n x k).
+ *  - Functions are asynchronous on `stream` unless documented otherwise; no
+ *    allocation happens inside -- callers pass a workspace sized by the
+ *    matching *_workspace_size query.  Inputs are never modified.
+ *  - Return value: HT_OK or an HT_ERR_* code; ht_last_error() gives the text
+ *    (thread-local).  Python maps codes to the reference exceptions
+ *    (ValueError for shape / orthogonality / symmetry errors).
+ */
+#ifndef HT_B200_H
+#define HT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef void* ht_stream_t; /* cudaStream_t */
+
+enum {
+  HT_OK = 0,
+  HT_ERR_SHAPE = 1,           /* arith.py:398-402, format.py:101-119 */
+  HT_ERR_NOT_ORTHOGONAL = 2,  /* arith.py:306-307 */
+  HT_ERR_NONCONVERGED = 3,
+  HT_ERR_CUDA = 4,
+  HT_ERR_NOT_SYMMETRIC = 5,   /* kernels.py:47-50 */
+  HT_ERR_ARGUMENT = 6,        /* arith.py:47-51 */
+  HT_ERR_UNSUPPORTED = 7
+};
+
+typedef struct {
+  int32_t d;              /* tensor dimension, >= 2 */
+  const int64_t* n;       /* [d] host: leaf sizes by mode (mode mu -> n[mu-1]) */
+  const int64_t* rank;    /* [2d-1] host: rank per node id, rank[0] == 1 */
+  double* const* node;    /* [2d-1] host array of device pointers, BFS node id order */
+  int32_t orthogonal;     /* HTensor.orthogonal (format.py:76) */
+} ht_tensor;
+
+/* TruncationControl (arith.py:32-66). eps <= 0 means "no accuracy bound";
+ * max_rank <= 0 and max_rank_per_node == NULL means "no cap". */
+typedef struct {
+  double eps;
+  int64_t max_rank;
+  const int64_t* max_rank_per_node; /* [2d-1] host or NULL (dict form of max_rank) */
+} ht_trunc_ctl;
+
+/* GeneralizedMatrix (format.py:135-180). kind: 0 dense (row-major rows x cols),
+ * 1 diagonal (values[rows]), 2 CSR (int32 indptr[rows+1], indices[nnz]). */
+typedef struct {
+  int32_t kind;
+  int64_t rows, cols, nnz;
+  const double* values;
+  const int32_t* indptr;
+  const int32_t* indices;
+} ht_gmat;
+
+/* HTOperator (format.py:183-250): leaf node t carries rank[t] columns
+ * leaf_cols[t][0..rank[t]-1]; transfer/root arrays as for ht_tensor. */
+typedef struct {
+  int32_t d;
+  const int64_t* rank;            /* [2d-1] host */
+  const ht_gmat* const* leaf_cols;/* [2d-1] host (NULL entries for non-leaves) */
+  double* const* node;            /* [2d-1] device pointers (leaf entries unused) */
+} ht_operator;
+
+const char* ht_last_error(void);
+const char* ht_version(void);
+
+/* ---- tree-level operations (arith.py drivers) ------------------------- */
+
+/* truncate (arith.py:325-352).  Two-phase form for data-dependent ranks:
+ *  1. ht_truncate_ranks: orthogonalize (if needed) + reduced Gramians + batched
+ *     eigendecomposition + select_rank; SYNCHRONISES the stream and returns the
+ *     kept ranks in out_rank[2d-1] (host);
+ *  2. ht_truncate_project: projection into `out` (allocated with out_rank),
+ *     reusing the state phase 1 left in `ws`.
+ * ht_truncate does both without a host sync when the ranks are fixed by the
+ * shapes (ht_truncate_static_ranks returns 1). */
+int ht_truncate_workspace_size(const ht_tensor* x, size_t* bytes);
+int ht_truncate_static_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, int64_t* out_rank);
+int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
+                      int64_t* out_rank, ht_stream_t stream);
+int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
+                        const ht_tensor* out, ht_stream_t stream);
+int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
+                const ht_tensor* out, ht_stream_t stream);
+
+/* Hierarchical singular values: after ht_truncate_ranks, copy the descending,
+ * clamped eigenvalues lambda_t of every non-root node's reduced Gramian
+ * (sigma_t = sqrt(lambda_t)) into lam (device, concatenated in node-id order). */
+int ht_truncate_eigenvalues(const ht_tensor* x, void* ws, size_t ws_bytes, double* lam, ht_stream_t stream);
+
+/* orthogonalize (arith.py:273-296): out has the orthogonalised ranks
+ * (ht_orth_ranks) and orthogonal = 1. */
+int ht_orth_ranks(const ht_tensor* x, int64_t* out_rank);
+int ht_orthogonalize_workspace_size(const ht_tensor* x, size_t* bytes);
+int ht_orthogonalize(const ht_tensor* x, void* ws, size_t ws_bytes, const ht_tensor* out, ht_stream_t stream);
+
+/* compute_bhat (arith.py:299-322): reduced Gramian of every non-root node t
+ * (rank[t] x rank[t], row-major) at bhat[t]; x must be orthogonal. */
+int ht_gramians_workspace_size(const ht_tensor* x, size_t* bytes);
+int ht_gramians(const ht_tensor* x, void* ws, size_t ws_bytes, double* const* bhat, ht_stream_t stream);
+
+/* add (arith.py:355-365) and subtract (arith.py:374-375, alpha_c = -1):
+ * out ranks are a.rank + c.rank node by node (root 1). No FLOPs (Lemma 3). */
+int ht_add(const ht_tensor* a, const ht_tensor* c, double alpha_c, const ht_tensor* out, ht_stream_t stream);
+
+/* scale (arith.py:368-371): y = alpha * x elementwise (used on the root). */
+int ht_scale(const double* x, double* y, int64_t count, double alpha, ht_stream_t stream);
+
+/* inner_product (arith.py:246-265).  Result written to result_dev (device);
+ * if result_host != NULL the stream is synchronised and the value copied. */
+int ht_inner_product_workspace_size(const ht_tensor* a, const ht_tensor* c, size_t* bytes);
+int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws_bytes,
+                     double* result_dev, double* result_host, ht_stream_t stream);
+
+/* apply_operator (arith.py:378-395): out ranks are op.rank * x.rank. */
+int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream);
+
+/* ---- node kernels (kernels.py primitives, batched) ------------------- */
+
+/* reduced_qr (kernels.py:24-32) on `nodes` m x K matrices A(row,col) =
+ * A[node*a_node + row*a_r + col*a_c]; Q is m x min(m,K), R is min(m,K) x K
+ * row-major (ld r_ld), diag(R) >= 0. */
+int ht_qr_workspace_size(int64_t m, int64_t K, int64_t nodes, size_t* bytes);
+int ht_qr_batched(int64_t m, int64_t K, int64_t nodes, const double* A, int64_t a_r, int64_t a_c, int64_t a_node,
+                  double* Q, int64_t q_r, int64_t q_c, int64_t q_node, double* R, int64_t r_ld, int64_t r_node,
+                  void* ws, size_t ws_bytes, ht_stream_t stream);
+
+/* sym_eig_desc (kernels.py:35-54) on `nodes` K x K row-major matrices:
+ * eigenvectors V (row-major, columns = eigenvectors), lam descending clamped.
+ * Synchronises to report HT_ERR_NOT_SYMMETRIC like the reference. */
+int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double* lam, ht_stream_t stream);
+
+/* Strided batched GEMM C = alpha*A*B + beta*C (the mode_multiply / tensordot
+ * contractions, kernels.py:92-104). */
+int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A, int64_t a_m,
+                    int64_t a_k, int64_t a_b, const double* B, int64_t b_k, int64_t b_n, int64_t b_b, double beta,
+                    double* C, int64_t c_m, int64_t c_n, int64_t c_b, ht_stream_t stream);
+
+/* ---- instrumentation -------------------------------------------------- */
+
+/* Total kernel launches issued by this library since load (always counted). */
+int64_t ht_launch_count(void);
+/* on != 0: record a CUDA event pair on the launching stream around every kernel
+ * launch and attribute algorithmic flops/bytes per kernel; clears the tally. */
+int ht_profile_enable(int on);
+/* Writes {"kernel": {"ms", "launches", "flops", "bytes"}, ...} JSON into buf
+ * (synchronises the recorded events); returns the full JSON length. */
+int ht_profile_report(char* buf, size_t len);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HT_B200_H */

@@ -1,0 +1,314 @@
+"""HT arithmetic on the GPU -- the drop-in for the reference ``htucker.arith``.
+
+Same functions, signatures, semantics and exceptions as the reference
+(arith.py:32-402); every one dispatches to the C ABI of ``libht_b200.so``
+(include/ht_b200.h), whose level-batched sm_100a kernels do all the floating
+point work.  Host code here only sizes workspaces, allocates outputs and reads
+back the values the reference returns to the host (ranks in accuracy mode,
+inner products).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib
+from .format import F64, HTensor, HTOperator, node_shape
+
+
+# ---------------------------------------------------------------------------
+# truncation control (reference arith.py:32-66)
+# ---------------------------------------------------------------------------
+
+
+@dataclass(frozen=True)
+class TruncationControl:
+    """Per-node rank choice: absolute ``eps`` (budget eps^2/(2d-2) per node) and/or
+    a ``max_rank`` cap (int or per-node-id dict).  At least one must be set."""
+
+    eps: float | None = None
+    max_rank: int | dict | None = None
+
+    def __post_init__(self):
+        if self.eps is None and self.max_rank is None:
+            raise ValueError("truncation needs eps and/or max_rank")
+        if self.eps is not None and self.eps <= 0:
+            raise ValueError("eps must be positive")
+
+    @staticmethod
+    def fixed_rank(max_rank) -> "TruncationControl":
+        return TruncationControl(eps=None, max_rank=max_rank)
+
+    @staticmethod
+    def accuracy(eps: float, max_rank=None) -> "TruncationControl":
+        return TruncationControl(eps=eps, max_rank=max_rank)
+
+    @staticmethod
+    def relative(rel: float, norm_value: float, max_rank=None) -> "TruncationControl":
+        """Relative accuracy rel*||Y|| (C3/C4 configs); the reference only has absolute eps."""
+        return TruncationControl(eps=rel * norm_value, max_rank=max_rank)
+
+    def cap_for(self, node_id: int):
+        if self.max_rank is None:
+            return None
+        if isinstance(self.max_rank, dict):
+            return int(self.max_rank[node_id])
+        return int(self.max_rank)
+
+    def _c(self, nn: int):
+        per = None
+        cap = 0
+        if isinstance(self.max_rank, dict):
+            per = _lib.i64_array([0] + [int(self.max_rank[t]) for t in range(1, nn)])
+        elif self.max_rank is not None:
+            cap = int(self.max_rank)
+            if cap <= 0:
+                cap = 1  # select_rank keeps at least one column (arith.py:88)
+        c = _lib.CTruncCtl(float(self.eps) if self.eps is not None else 0.0, cap,
+                           ctypes.cast(per, ctypes.POINTER(ctypes.c_int64)) if per is not None else None)
+        return c, per
+
+
+# ---------------------------------------------------------------------------
+# helpers
+# ---------------------------------------------------------------------------
+
+
+def _ws(nbytes: int, dev) -> torch.Tensor:
+    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+
+
+def _sizes_by_node(x: HTensor) -> dict:
+    return {leaf.index: int(x.node_array(leaf.index).shape[0]) for leaf in x.tree.leaves}
+
+
+def _check_compatible(a: HTensor, c: HTensor) -> None:
+    """arith.py:398-402."""
+    if a.tree.d != c.tree.d:
+        raise ValueError(f"tensor dimensions differ: {a.tree.d} vs {c.tree.d}")
+    if a.shape != c.shape:
+        raise ValueError(f"tensor shapes differ: {a.shape} vs {c.shape}")
+
+
+def _stream():
+    return _lib.stream_handle()
+
+
+# ---------------------------------------------------------------------------
+# drop-in API
+# ---------------------------------------------------------------------------
+
+
+def add(a: HTensor, c: HTensor) -> HTensor:
+    """arith.py:355-365: frames concatenate, transfers embed block-diagonally."""
+    return _add(a, c, 1.0)
+
+
+def subtract(a: HTensor, c: HTensor) -> HTensor:
+    """arith.py:374-375: add(a, scale(c, -1)) in one launch."""
+    return _add(a, c, -1.0)
+
+
+def _add(a: HTensor, c: HTensor, alpha_c: float) -> HTensor:
+    _check_compatible(a, c)
+    lib = _lib.load()
+    tree = a.tree
+    ranks = {t: a.rank(t) + c.rank(t) for t in range(1, len(tree.nodes))}
+    out = HTensor.empty(tree, _sizes_by_node(a), ranks, device=a.device)
+    _lib.check(lib.ht_add(a._c(), c._c(), float(alpha_c), out._c(), _stream()), "add")
+    return out
+
+
+def scale(a: HTensor, alpha: float) -> HTensor:
+    """arith.py:368-371: alpha applied to the root matrix; leaves/transfers shared."""
+    lib = _lib.load()
+    root = a.root_matrix
+    new_root = torch.empty_like(root)
+    _lib.check(lib.ht_scale(root.data_ptr(), new_root.data_ptr(), root.numel(), float(alpha), _stream()), "scale")
+    nodes = dict(a._nodes)
+    nodes[0] = new_root
+    return HTensor._wrap(a.tree, nodes, a.orthogonal)
+
+
+def inner_product(a: HTensor, c: HTensor) -> float:
+    """arith.py:246-265 (returns a host float; one device->host read)."""
+    _check_compatible(a, c)
+    lib = _lib.load()
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.ht_inner_product_workspace_size(a._c(), c._c(), ctypes.byref(nbytes)), "inner_product")
+    ws = _ws(nbytes.value, a.device)
+    res = torch.empty(1, dtype=F64, device=a.device)
+    host = ctypes.c_double(0.0)
+    _lib.check(lib.ht_inner_product(a._c(), c._c(), ws.data_ptr(), ws.numel(), res.data_ptr(),
+                                    ctypes.byref(host), _stream()), "inner_product")
+    return float(host.value)
+
+
+def inner_product_device(a: HTensor, c: HTensor) -> torch.Tensor:
+    """Asynchronous variant: the inner product as a 1-element device tensor."""
+    _check_compatible(a, c)
+    lib = _lib.load()
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.ht_inner_product_workspace_size(a._c(), c._c(), ctypes.byref(nbytes)), "inner_product")
+    ws = _ws(nbytes.value, a.device)
+    res = torch.empty(1, dtype=F64, device=a.device)
+    _lib.check(lib.ht_inner_product(a._c(), c._c(), ws.data_ptr(), ws.numel(), res.data_ptr(), None, _stream()),
+               "inner_product")
+    return res
+
+
+def norm(a: HTensor) -> float:
+    """arith.py:268-270."""
+    return math.sqrt(max(0.0, inner_product(a, a)))
+
+
+def orthogonalize(a: HTensor) -> HTensor:
+    """arith.py:273-296: bottom-up batched Householder QR sweep."""
+    lib = _lib.load()
+    tree = a.tree
+    nn = len(tree.nodes)
+    rbuf = (ctypes.c_int64 * nn)()
+    _lib.check(lib.ht_orth_ranks(a._c(), rbuf), "orthogonalize")
+    ranks = {t: int(rbuf[t]) for t in range(1, nn)}
+    out = HTensor.empty(tree, _sizes_by_node(a), ranks, orthogonal=True, device=a.device)
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.ht_orthogonalize_workspace_size(a._c(), ctypes.byref(nbytes)), "orthogonalize")
+    ws = _ws(nbytes.value, a.device)
+    _lib.check(lib.ht_orthogonalize(a._c(), ws.data_ptr(), ws.numel(), out._c(), _stream()), "orthogonalize")
+    return out
+
+
+def compute_bhat(a: HTensor) -> dict:
+    """arith.py:299-322: reduced Gramians (device tensors) of every non-root node."""
+    if not a.orthogonal:
+        raise ValueError("tensor is not orthogonal; call orthogonalize() first")
+    lib = _lib.load()
+    tree = a.tree
+    nn = len(tree.nodes)
+    G = {t: torch.empty((a.rank(t), a.rank(t)), dtype=F64, device=a.device) for t in range(1, nn)}
+    ptrs = _lib.ptr_array([0] + [G[t].data_ptr() for t in range(1, nn)])
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(lib.ht_gramians_workspace_size(a._c(), ctypes.byref(nbytes)), "compute_bhat")
+    ws = _ws(nbytes.value, a.device)
+    _lib.check(lib.ht_gramians(a._c(), ws.data_ptr(), ws.numel(), ptrs, _stream()), "compute_bhat")
+    return G
+
+
+class _TruncState:
+    """Workspace + ranks after phase 1 of a truncation (orth, Gramians, eig, select)."""
+
+    def __init__(self, a: HTensor, ctl: TruncationControl):
+        lib = _lib.load()
+        self.a = a
+        self.ctl = ctl
+        nn = len(a.tree.nodes)
+        self.cctl, self._keep = ctl._c(nn)
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(lib.ht_truncate_workspace_size(a._c(), ctypes.byref(nbytes)), "truncate")
+        self.ws = _ws(nbytes.value, a.device)
+        rbuf = (ctypes.c_int64 * nn)()
+        self.static = lib.ht_truncate_static_ranks(a._c(), ctypes.byref(self.cctl), rbuf) == 1
+        self.ranks = {t: int(rbuf[t]) for t in range(1, nn)}
+        self.phase1_done = False
+
+    def run_phase1(self):
+        lib = _lib.load()
+        nn = len(self.a.tree.nodes)
+        rbuf = (ctypes.c_int64 * nn)()
+        _lib.check(lib.ht_truncate_ranks(self.a._c(), ctypes.byref(self.cctl), self.ws.data_ptr(), self.ws.numel(),
+                                         rbuf, _stream()), "truncate")
+        self.ranks = {t: int(rbuf[t]) for t in range(1, nn)}
+        self.phase1_done = True
+
+
+def truncate(a: HTensor, ctl: TruncationControl) -> HTensor:
+    """arith.py:325-352: orthogonalize if needed, reduced Gramians, batched
+    eigendecompositions + rank choice, projection.  Result not orthogonal."""
+    lib = _lib.load()
+    st = _TruncState(a, ctl)
+    if st.static:
+        out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
+        _lib.check(lib.ht_truncate(a._c(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
+                                   _stream()), "truncate")
+        return out
+    st.run_phase1()
+    out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
+    _lib.check(lib.ht_truncate_project(a._c(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
+                                       _stream()), "truncate")
+    return out
+
+
+def hierarchical_singular_values(a: HTensor) -> dict:
+    """sigma_t = sqrt(lambda(Bhat_t)) per non-root node, descending (device tensors).
+    The reference computes these inside truncate (arith.py:340-343) and discards them."""
+    lib = _lib.load()
+    st = _TruncState(a, TruncationControl.fixed_rank(1))
+    st.run_phase1()
+    nn = len(a.tree.nodes)
+    rbuf = (ctypes.c_int64 * nn)()
+    _lib.check(lib.ht_orth_ranks(a._c(), rbuf), "orth ranks")
+    ko = {t: (int(rbuf[t]) if not a.orthogonal else a.rank(t)) for t in range(1, nn)}
+    total = sum(ko.values())
+    lam = torch.empty(total, dtype=F64, device=a.device)
+    _lib.check(lib.ht_truncate_eigenvalues(a._c(), st.ws.data_ptr(), st.ws.numel(), lam.data_ptr(), _stream()),
+               "eigenvalues")
+    out, off = {}, 0
+    for t in range(1, nn):
+        out[t] = torch.sqrt(lam[off:off + ko[t]])
+        off += ko[t]
+    return out
+
+
+def apply_operator(op: HTOperator, a: HTensor) -> HTensor:
+    """arith.py:378-395 (Lemma 4): ranks multiply, operator index slow."""
+    tree = a.tree
+    if op.tree.d != tree.d:
+        raise ValueError(f"operator dimension {op.tree.d} != tensor dimension {tree.d}")
+    if op.col_sizes != a.shape:
+        raise ValueError(f"operator column sizes {op.col_sizes} do not match tensor shape {a.shape}")
+    lib = _lib.load()
+    ranks = {t: op.rank(t) * a.rank(t) for t in range(1, len(tree.nodes))}
+    sizes = {leaf.index: int(op.leaf_shape(leaf.index)[0]) for leaf in tree.leaves}
+    out = HTensor.empty(tree, sizes, ranks, device=a.device)
+    _lib.check(lib.ht_apply_operator(ctypes.byref(op._c()), a._c(), out._c(), _stream()), "apply_operator")
+    return out
+
+
+def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, alpha=1.0, beta=0.0) -> torch.Tensor:
+    """C = alpha A B + beta C on the DMMA kernel (row-major 2-D CUDA float64)."""
+    lib = _lib.load()
+    M, K = A.shape
+    K2, N = B.shape
+    if K != K2:
+        raise ValueError("inner dimensions differ")
+    if out is None:
+        out = torch.empty((M, N), dtype=F64, device=A.device)
+    _lib.check(lib.ht_gemm_strided(M, N, K, 1, float(alpha), A.data_ptr(), A.stride(0), A.stride(1), 0,
+                                   B.data_ptr(), B.stride(0), B.stride(1), 0, float(beta), out.data_ptr(),
+                                   out.stride(0), out.stride(1), 0, _stream()), "gemm")
+    return out
+
+
+def leaf_map(x: HTensor, dim: int, matrix) -> HTensor:
+    """Replace the frame of mode ``dim`` by ``matrix @ U`` (solvers.py:58-62)."""
+    leaf = x.tree.leaf_for_dim(dim)
+    M = matrix if isinstance(matrix, torch.Tensor) else torch.as_tensor(np.asarray(matrix, dtype=np.float64))
+    M = M.to(x.device, F64).contiguous()
+    U = x.node_array(leaf.index)
+    nodes = dict(x._nodes)
+    nodes[leaf.index] = gemm(M, U)
+    return HTensor._wrap(x.tree, nodes, False)
+
+
+def _check_all():
+    return _lib.load()
+
+
+__all__ = ["TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
+           "orthogonalize", "compute_bhat", "truncate", "hierarchical_singular_values", "apply_operator",
+           "gemm", "leaf_map"]

@@ -1,0 +1,69 @@
+// Shared definitions for the B200 (sm_100a) HT-arithmetic kernels.
+//
+// All arithmetic is IEEE float64.  On sm_100a the only FP64 tensor-core path is
+// mma.sync DMMA (tcgen05 has no kind::f64); DMMA and DFMA both measure ~37 TF/s
+// on this pool's B200s (profiles/r01_fp64_peak_microbench.jsonl).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <string>
+
+namespace ht {
+
+constexpr int kWarp = 32;
+
+// Status codes shared with include/ht_b200.h.
+enum Status : int {
+  kOk = 0,
+  kErrShape = 1,
+  kErrNotOrthogonal = 2,
+  kErrNonConverged = 3,
+  kErrCuda = 4,
+  kErrNotSymmetric = 5,
+  kErrArgument = 6,
+  kErrUnsupported = 7,
+};
+
+void set_error(const std::string& msg);
+const char* last_error();
+
+#define HT_CUDA_CHECK(expr)                                                     \
+  do {                                                                          \
+    cudaError_t _e = (expr);                                                    \
+    if (_e != cudaSuccess) {                                                    \
+      ::ht::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e));      \
+      return ::ht::kErrCuda;                                                    \
+    }                                                                           \
+  } while (0)
+
+#define HT_LAUNCH_CHECK()                                                       \
+  do {                                                                          \
+    cudaError_t _e = cudaGetLastError();                                        \
+    if (_e != cudaSuccess) {                                                    \
+      ::ht::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      return ::ht::kErrCuda;                                                    \
+    }                                                                           \
+  } while (0)
+
+#define HT_TRY(expr)                        \
+  do {                                      \
+    int _s = (expr);                        \
+    if (_s != ::ht::kOk) return _s;         \
+  } while (0)
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+inline int ceil_div(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+}  // namespace ht

@@ -1,0 +1,1139 @@
+// Level-wise HT drivers behind the C ABI (include/ht_b200.h).
+//
+// The reference walks the dimension tree one node at a time in Python
+// (arith.py:246-395).  Here every phase is one batched launch per tree level
+// (or one launch for all nodes where the phase is order-free), all nodes of a
+// level share each launch, and no host synchronisation happens except where
+// the reference returns a host value (ranks in accuracy mode, inner products).
+#include <algorithm>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "eig.cuh"
+#include "gemm.cuh"
+#include "ht_b200.h"
+#include "misc.cuh"
+#include "qr.cuh"
+
+namespace ht {
+
+namespace {
+thread_local std::string g_err;
+}
+void set_error(const std::string& m) { g_err = m; }
+const char* last_error() { return g_err.c_str(); }
+
+namespace {
+
+constexpr int kSMs = 148;
+
+// ---------------------------------------------------------------------------
+// dimension tree (reference tree.py:55-101): balanced split (mu+nu-1)/2, BFS ids
+// ---------------------------------------------------------------------------
+struct Tree {
+  int d = 0, nn = 0, depth = 0;
+  std::vector<int> lo, hi, father, son1, son2, level;
+  std::vector<std::vector<int>> levels;
+  std::vector<int> leaf_of_dim;  // [d+1]
+  bool leaf(int t) const { return son1[t] < 0; }
+};
+
+Tree build_tree(int d) {
+  Tree T;
+  T.d = d;
+  struct Item { int lo, hi, father, level; };
+  std::vector<Item> q{{1, d, -1, 0}};
+  for (size_t h = 0; h < q.size(); ++h) {
+    const Item it = q[h];
+    const int t = (int)h;
+    T.lo.push_back(it.lo); T.hi.push_back(it.hi); T.father.push_back(it.father); T.level.push_back(it.level);
+    T.son1.push_back(-1); T.son2.push_back(-1);
+    if (it.father >= 0) {
+      if (T.son1[it.father] < 0) T.son1[it.father] = t; else T.son2[it.father] = t;
+    }
+    if (it.lo != it.hi) {
+      const int cut = (it.lo + it.hi - 1) / 2;
+      q.push_back({it.lo, cut, t, it.level + 1});
+      q.push_back({cut + 1, it.hi, t, it.level + 1});
+    }
+  }
+  T.nn = (int)T.lo.size();
+  for (int t = 0; t < T.nn; ++t) T.depth = std::max(T.depth, T.level[t]);
+  T.levels.assign(T.depth + 1, {});
+  for (int t = 0; t < T.nn; ++t) T.levels[T.level[t]].push_back(t);
+  T.leaf_of_dim.assign(d + 1, -1);
+  for (int t = 0; t < T.nn; ++t)
+    if (T.leaf(t)) T.leaf_of_dim[T.lo[t]] = t;
+  return T;
+}
+
+const Tree& tree_for(int d) {
+  static std::mutex mu;
+  static std::map<int, Tree> cache;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = cache.find(d);
+  if (it == cache.end()) it = cache.emplace(d, build_tree(d)).first;
+  return it->second;
+}
+
+// ---------------------------------------------------------------------------
+// tensor views
+// ---------------------------------------------------------------------------
+struct View {
+  const Tree* T = nullptr;
+  std::vector<long long> n;     // per node: leaf size (0 for non-leaves)
+  std::vector<long long> k;     // per node rank (root 1)
+  std::vector<double*> p;
+  bool orth = false;
+  long long k1(int t) const { return k[T->son1[t]]; }
+  long long k2(int t) const { return k[T->son2[t]]; }
+  long long elems(int t) const {
+    if (T->leaf(t)) return n[t] * k[t];
+    if (t == 0) return k1(t) * k2(t);
+    return k[t] * k1(t) * k2(t);
+  }
+};
+
+int make_view(const ht_tensor* x, View& v, bool need_ptrs = true) {
+  if (!x || x->d < 2) {
+    set_error("tensor dimension must be >= 2");
+    return kErrShape;
+  }
+  const Tree& T = tree_for(x->d);
+  v.T = &T;
+  v.n.assign(T.nn, 0);
+  v.k.assign(T.nn, 1);
+  v.p.assign(T.nn, nullptr);
+  v.orth = x->orthogonal != 0;
+  for (int t = 0; t < T.nn; ++t) {
+    v.k[t] = t == 0 ? 1 : x->rank[t];
+    if (v.k[t] < 1) {
+      set_error("rank of node " + std::to_string(t) + " must be >= 1");
+      return kErrShape;
+    }
+    if (T.leaf(t)) {
+      v.n[t] = x->n[T.lo[t] - 1];
+      if (v.n[t] < 1) {
+        set_error("leaf size must be >= 1");
+        return kErrShape;
+      }
+    }
+    if (need_ptrs) {
+      if (!x->node || !x->node[t]) {
+        set_error("missing device pointer for node " + std::to_string(t));
+        return kErrArgument;
+      }
+      v.p[t] = x->node[t];
+    }
+  }
+  return kOk;
+}
+
+// ranks after orthogonalize: rank can only shrink (arith.py:135-141, kernels.py:27-28)
+std::vector<long long> orth_ranks(const View& x) {
+  const Tree& T = *x.T;
+  std::vector<long long> ko(T.nn, 1);
+  for (int l = T.depth; l >= 1; --l)
+    for (int t : T.levels[l]) {
+      if (T.leaf(t)) ko[t] = std::min(x.n[t], x.k[t]);
+      else ko[t] = std::min(x.k[t], ko[T.son1[t]] * ko[T.son2[t]]);
+    }
+  return ko;
+}
+
+// ---------------------------------------------------------------------------
+// bump allocator over the caller's workspace (measure mode when base == null)
+// ---------------------------------------------------------------------------
+struct Arena {
+  char* base = nullptr;
+  size_t off = 0;
+  double* take(long long ndoubles) {
+    off = (off + 255) & ~(size_t)255;
+    double* r = base ? (double*)(base + off) : nullptr;
+    off += (size_t)std::max<long long>(ndoubles, 1) * sizeof(double);
+    return r;
+  }
+  int* take_int(long long n) { return (int*)take((n + 1) / 2); }
+};
+
+// Merge consecutive single-node GEMM descriptors that differ only by constant
+// pointer deltas into one descriptor with an outer batch (nb2).
+void merge_gemms(std::vector<GemmDesc>& v) {
+  std::vector<GemmDesc> out;
+  size_t i = 0;
+  while (i < v.size()) {
+    GemmDesc d = v[i];
+    size_t j = i + 1;
+    if (d.nb2 == 1 && d.splits == 1 && j < v.size()) {
+      const long long dA = v[j].A - d.A, dB = v[j].B - d.B, dC = v[j].C - d.C;
+      while (j < v.size()) {
+        const GemmDesc& e = v[j];
+        const long long c = (long long)(j - i);
+        bool same = e.nb2 == 1 && e.splits == 1 && e.M == d.M && e.N == d.N && e.K == d.K && e.KO == d.KO &&
+                    e.nb1 == d.nb1 && e.a_m == d.a_m && e.a_k == d.a_k && e.a_o == d.a_o && e.a_b1 == d.a_b1 &&
+                    e.b_k == d.b_k && e.b_n == d.b_n && e.b_o == d.b_o && e.b_b1 == d.b_b1 && e.c_m == d.c_m &&
+                    e.c_n == d.c_n && e.c_b1 == d.c_b1 && e.alpha == d.alpha && e.beta == d.beta &&
+                    e.A - d.A == c * dA && e.B - d.B == c * dB && e.C - d.C == c * dC;
+        if (!same) break;
+        ++j;
+      }
+      if (j - i > 1) {
+        d.nb2 = (int)(j - i);
+        d.a_b2 = dA;
+        d.b_b2 = dB;
+        d.c_b2 = dC;
+      } else {
+        j = i + 1;
+      }
+    }
+    out.push_back(d);
+    i = j;
+  }
+  v.swap(out);
+}
+
+void merge_qrs(std::vector<QrProblem>& v) {
+  std::vector<QrProblem> out;
+  size_t i = 0;
+  while (i < v.size()) {
+    QrProblem d = v[i];
+    size_t j = i + 1;
+    if (j < v.size()) {
+      const long long dA = v[j].A - d.A, dQ = v[j].Q - d.Q, dR = v[j].R - d.R;
+      while (j < v.size()) {
+        const QrProblem& e = v[j];
+        const long long c = (long long)(j - i);
+        bool same = e.m == d.m && e.K == d.K && e.a_r == d.a_r && e.a_c == d.a_c && e.q_r == d.q_r &&
+                    e.q_c == d.q_c && e.r_ld == d.r_ld && e.A - d.A == c * dA && e.Q - d.Q == c * dQ &&
+                    e.R - d.R == c * dR && (e.V == nullptr) == (d.V == nullptr) &&
+                    (d.V == nullptr || e.V - d.V == c * (long long)d.m * d.K);
+        if (!same) break;
+        ++j;
+      }
+      if (j - i > 1) {
+        d.nodes = (int)(j - i);
+        d.a_node = dA;
+        d.q_node = dQ;
+        d.r_node = dR;
+      } else {
+        j = i + 1;
+      }
+    }
+    out.push_back(d);
+    i = j;
+  }
+  v.swap(out);
+}
+
+// Plan (and, if arena has a base, bind) the QR workspace of a set of problems.
+int plan_qrs(std::vector<QrProblem>& qs, Arena& ar) {
+  merge_qrs(qs);
+  int total_nodes = 0;
+  for (auto& q : qs) total_nodes += q.nodes;
+  for (auto& q : qs) {
+    q.P = std::max(1, ceil_div(kSMs, std::max(1, total_nodes)));
+    HT_TRY(qr_plan(q, kSMs));
+    const bool own_v = q.V == nullptr;
+    long long need = (long long)q.nodes * (q.tau_node + 2 * q.st_node) + (own_v ? (long long)q.nodes * q.v_node : 0);
+    double* w = ar.take(need);
+    if (ar.base) {
+      double* vkeep = q.V;
+      double* cur = w;
+      if (own_v) {
+        q.V = cur;
+        cur += (long long)q.nodes * q.v_node;
+      } else {
+        q.V = vkeep;
+      }
+      q.tau = cur;
+      cur += (long long)q.nodes * q.tau_node;
+      q.Rst = cur;
+      cur += (long long)q.nodes * q.st_node;
+      q.W = cur;
+    }
+  }
+  return kOk;
+}
+
+// split-K count so a level's reduction GEMMs fill the GPU
+int pick_splits(long long tiles_total, long long reduction) {
+  long long s = std::max<long long>(1, (2 * kSMs + tiles_total - 1) / std::max<long long>(1, tiles_total));
+  s = std::min<long long>(s, std::max<long long>(1, reduction / (kGemmBK * 8)));
+  return (int)std::min<long long>(s, 64);
+}
+
+// ---------------------------------------------------------------------------
+// orthogonalize (arith.py:273-296)
+// ---------------------------------------------------------------------------
+struct OrthPlan {
+  std::vector<long long> ko;
+  std::vector<double*> out;  // orthogonalised node arrays
+  std::vector<double*> R;    // R factors (ko[t] x k[t], row-major)
+};
+
+// Runs (or, in measure mode, sizes) the bottom-up sweep.  `out` pointers may be
+// supplied (ht_orthogonalize) or carved from the arena (truncate).
+int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec) {
+  const Tree& T = *x.T;
+  op.ko = orth_ranks(x);
+  const auto& ko = op.ko;
+  if (op.out.empty()) {
+    op.out.assign(T.nn, nullptr);
+    for (int t = 0; t < T.nn; ++t) {
+      long long e;
+      if (T.leaf(t)) e = x.n[t] * ko[t];
+      else if (t == 0) e = ko[T.son1[t]] * ko[T.son2[t]];
+      else e = ko[t] * ko[T.son1[t]] * ko[T.son2[t]];
+      op.out[t] = ar.take(e);
+    }
+  }
+  op.R.assign(T.nn, nullptr);
+  for (int t = 1; t < T.nn; ++t) op.R[t] = ar.take(ko[t] * x.k[t]);
+
+  const size_t scratch_base = scratch_ar.off;
+  size_t scratch_max = scratch_base;
+  for (int l = T.depth; l >= 1; --l) {
+    scratch_ar.off = scratch_base;
+    std::vector<GemmDesc> g2, g3;
+    std::vector<QrProblem> qs;
+    std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
+    for (int t : T.levels[l])
+      if (!T.leaf(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
+    for (int t : T.levels[l])
+      if (!T.leaf(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
+    for (int t : T.levels[l]) {
+      if (T.leaf(t)) {
+        QrProblem q{};
+        q.A = x.p[t]; q.a_r = x.k[t]; q.a_c = 1;
+        q.Q = op.out[t]; q.q_r = ko[t]; q.q_c = 1;
+        q.R = op.R[t]; q.r_ld = x.k[t];
+        q.m = (int)x.n[t]; q.K = (int)x.k[t]; q.nodes = 1;
+        qs.push_back(q);
+        continue;
+      }
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      const long long kt = x.k[t], k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
+      double* T1 = T1s[t];
+      double* Bp = Bps[t];
+      // mode-2 absorb, per slice i: T1_i (k1o x k2) = R1 (k1o x k1) * B_i (k1 x k2)
+      GemmDesc a = gemm_desc(op.R[s1], k1, 1, x.p[t], k2, 1, T1, k2, 1, (int)k1o, (int)k2, (int)k1);
+      a.nb1 = (int)kt; a.a_b1 = 0; a.b_b1 = k1 * k2; a.c_b1 = k1o * k2;
+      g2.push_back(a);
+      // mode-3 absorb: Bp ((kt k1o) x k2o) = T1 ((kt k1o) x k2) * R2^T
+      g3.push_back(gemm_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
+      // QR of M23(Bp): (k1o k2o) x kt column-major, in place as reflector storage
+      QrProblem q{};
+      q.A = Bp; q.a_r = 1; q.a_c = k1o * k2o;
+      q.V = Bp;
+      q.Q = op.out[t]; q.q_r = 1; q.q_c = k1o * k2o;
+      q.R = op.R[t]; q.r_ld = kt;
+      q.m = (int)(k1o * k2o); q.K = (int)kt; q.nodes = 1;
+      qs.push_back(q);
+    }
+    HT_TRY(plan_qrs(qs, scratch_ar));
+    scratch_max = std::max(scratch_max, scratch_ar.off);
+    if (exec) {
+      merge_gemms(g2);
+      merge_gemms(g3);
+      HT_TRY(gemm_grouped(g2, s));
+      HT_TRY(gemm_grouped(g3, s));
+      HT_TRY(qr_batched(qs, s));
+    }
+  }
+  // root: B_D <- R1 B_D R2^T (arith.py:144-145)
+  scratch_ar.off = scratch_base;
+  {
+    const int s1 = T.son1[0], s2 = T.son2[0];
+    const long long k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
+    double* tmp = scratch_ar.take(k1o * k2);
+    scratch_max = std::max(scratch_max, scratch_ar.off);
+    if (exec) {
+      std::vector<GemmDesc> g{gemm_desc(op.R[s1], k1, 1, x.p[0], k2, 1, tmp, k2, 1, (int)k1o, (int)k2, (int)k1)};
+      HT_TRY(gemm_grouped(g, s));
+      std::vector<GemmDesc> g4{gemm_desc(tmp, k2, 1, op.R[s2], 1, k2, op.out[0], k2o, 1, (int)k1o, (int)k2o, (int)k2)};
+      HT_TRY(gemm_grouped(g4, s));
+    }
+  }
+  scratch_ar.off = scratch_max;
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// reduced Gramians, top-down (arith.py:148-158, 299-322)
+// ---------------------------------------------------------------------------
+int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar, cudaStream_t s, bool exec) {
+  const Tree& T = *o.T;
+  const size_t base = scratch_ar.off;
+  size_t mx = base;
+  // root: G_s1 = B_D B_D^T, G_s2 = B_D^T B_D
+  {
+    scratch_ar.off = base;
+    const int s1 = T.son1[0], s2 = T.son2[0];
+    const long long k1 = o.k[s1], k2 = o.k[s2];
+    double* P1 = scratch_ar.take(k1 * k1);
+    double* P2 = scratch_ar.take(k2 * k2);
+    mx = std::max(mx, scratch_ar.off);
+    if (exec) {
+      std::vector<GemmDesc> g;
+      GemmDesc a = gemm_desc(o.p[0], k2, 1, o.p[0], 1, k2, P1, k1, 1, (int)k1, (int)k1, (int)k2);
+      a.splits = 1;
+      GemmDesc b = gemm_desc(o.p[0], 1, k2, o.p[0], k2, 1, P2, k2, 1, (int)k2, (int)k2, (int)k1);
+      g.push_back(a);
+      g.push_back(b);
+      HT_TRY(gemm_grouped(g, s));
+      std::vector<ReduceDesc> r(2);
+      r[0] = ReduceDesc{P1, G[s1], k1, 1, 0, 0, 1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0};
+      r[1] = ReduceDesc{P2, G[s2], k2, 1, 0, 0, 1, (int)k2, (int)k2, 1, 1, 1, 1.0, 0.0};
+      HT_TRY(reduce_partials(r, s));
+    }
+  }
+  for (int l = 1; l < T.depth; ++l) {
+    scratch_ar.off = base;
+    std::vector<int> inner;
+    for (int t : T.levels[l])
+      if (!T.leaf(t)) inner.push_back(t);
+    if (inner.empty()) continue;
+    std::vector<GemmDesc> g1s, g2s;
+    std::vector<ReduceDesc> rs;
+    long long tiles = 0;
+    for (int t : inner) {
+      const long long k1 = o.k[T.son1[t]], k2 = o.k[T.son2[t]];
+      tiles += (long long)ceil_div(k1, kGemmBM) * ceil_div(k1, kGemmBN) + (long long)ceil_div(k2, kGemmBM) * ceil_div(k2, kGemmBN);
+    }
+    std::vector<double*> t1s(T.nn, nullptr);
+    for (int t : inner) t1s[t] = scratch_ar.take(o.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+    for (int t : inner) {
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      const long long kt = o.k[t], k1 = o.k[s1], k2 = o.k[s2];
+      const long long f = k1 * k2;
+      double* t1 = t1s[t];
+      // t1 (kt x k1k2) = G_t (kt x kt) * M1(B)   (arith.py:155)
+      g1s.push_back(gemm_desc(G[t], kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
+      const int S1 = pick_splits(tiles, kt * k2);
+      const int S2 = pick_splits(tiles, kt * k1);
+      double* P1 = scratch_ar.take(S1 * k1 * k1);
+      double* P2 = scratch_ar.take(S2 * k2 * k2);
+      // g1[p,q] = sum_{i,l} B[i,p,l] t1[i,q,l]   (arith.py:156)
+      GemmDesc a = gemm_desc(o.p[t], k2, 1, t1, 1, k2, P1, k1, 1, (int)k1, (int)k1, (int)k2);
+      a.KO = (int)kt; a.a_o = f; a.b_o = f; a.splits = S1;
+      // g2[p,q] = sum_{i,j} B[i,j,p] t1[i,j,q]   (arith.py:157)
+      GemmDesc b = gemm_desc(o.p[t], 1, k2, t1, k2, 1, P2, k2, 1, (int)k2, (int)k2, (int)(kt * k1));
+      b.splits = S2;
+      g2s.push_back(a);
+      g2s.push_back(b);
+      rs.push_back(ReduceDesc{P1, G[s1], k1, 1, 0, 0, S1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0});
+      rs.push_back(ReduceDesc{P2, G[s2], k2, 1, 0, 0, S2, (int)k2, (int)k2, 1, 1, 1, 1.0, 0.0});
+    }
+    mx = std::max(mx, scratch_ar.off);
+    if (exec) {
+      merge_gemms(g1s);
+      HT_TRY(gemm_grouped(g1s, s));
+      HT_TRY(gemm_grouped(g2s, s));
+      HT_TRY(reduce_partials(rs, s));
+    }
+  }
+  scratch_ar.off = mx;
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// truncate (arith.py:325-352)
+// ---------------------------------------------------------------------------
+struct TruncPlan {
+  OrthPlan op;
+  View o;                       // orthogonal tensor (x itself or op.out)
+  std::vector<double*> G, EV, lam;
+  int* ranks = nullptr;
+  int* status = nullptr;
+  Arena scratch;
+};
+
+int eig_caps(const ht_trunc_ctl* ctl, int t) {
+  if (ctl->max_rank_per_node) return (int)ctl->max_rank_per_node[t];
+  return ctl->max_rank > 0 ? (int)ctl->max_rank : 0;
+}
+
+int check_ctl(const ht_trunc_ctl* ctl) {
+  if (!ctl) {
+    set_error("truncation control is null");
+    return kErrArgument;
+  }
+  if (!(ctl->eps > 0) && ctl->max_rank <= 0 && !ctl->max_rank_per_node) {
+    set_error("truncation needs eps and/or max_rank");
+    return kErrArgument;
+  }
+  return kOk;
+}
+
+// Layout of the truncate workspace (deterministic in the shapes of x).
+int plan_truncate(const View& x, TruncPlan& P, char* base) {
+  const Tree& T = *x.T;
+  Arena ar;
+  ar.base = base;
+  P.o = x;
+  if (!x.orth) {
+    P.op = OrthPlan{};
+    P.op.ko = orth_ranks(x);
+    P.op.out.assign(T.nn, nullptr);
+    const auto& ko = P.op.ko;
+    for (int t = 0; t < T.nn; ++t) {
+      long long e;
+      if (T.leaf(t)) e = x.n[t] * ko[t];
+      else if (t == 0) e = ko[T.son1[t]] * ko[T.son2[t]];
+      else e = ko[t] * ko[T.son1[t]] * ko[T.son2[t]];
+      P.op.out[t] = ar.take(e);
+    }
+    P.o.k = ko;
+    P.o.p = P.op.out;
+    P.o.orth = true;
+  }
+  P.G.assign(T.nn, nullptr);
+  P.EV.assign(T.nn, nullptr);
+  P.lam.assign(T.nn, nullptr);
+  // G / EV / lam of all non-root nodes are contiguous so same-K nodes batch
+  for (int t = 1; t < T.nn; ++t) P.G[t] = ar.take(P.o.k[t] * P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t) P.EV[t] = ar.take(P.o.k[t] * P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t) P.lam[t] = ar.take(P.o.k[t]);
+  P.ranks = ar.take_int(T.nn + 1);
+  P.status = P.ranks + T.nn;
+  P.scratch = ar;  // everything after this point is phase scratch
+  return kOk;
+}
+
+size_t truncate_ws_bytes(const View& x) {
+  TruncPlan P;
+  plan_truncate(x, P, nullptr);
+  Arena sc = P.scratch;
+  const size_t start = sc.off;
+  size_t need = start;
+  if (!x.orth) {
+    Arena a2 = sc;
+    OrthPlan op = P.op;
+    run_orthogonalize(x, op, a2, a2, nullptr, false);
+    need = std::max(need, a2.off);
+  }
+  {
+    Arena a3 = sc;
+    run_gramians(P.o, P.G, a3, nullptr, false);
+    need = std::max(need, a3.off);
+  }
+  {
+    // projection temporaries with the (upper-bound) ranks ko
+    const Tree& T = *x.T;
+    Arena a4 = sc;
+    for (int t = 1; t < T.nn; ++t) {
+      if (T.leaf(t)) continue;
+      const long long kt = P.o.k[t], k1 = P.o.k[T.son1[t]], k2 = P.o.k[T.son2[t]];
+      a4.take(kt * k1 * k2);
+      a4.take(kt * k1 * k2);
+    }
+    a4.take(P.o.k[T.son1[0]] * P.o.k[T.son2[0]]);
+    need = std::max(need, a4.off);
+  }
+  // every Arena::take may pad by up to 255 bytes; planning merges differ between
+  // measure and execute mode, so reserve the worst case per node
+  return need + 4096 * (size_t)x.T->nn + 256;
+}
+
+int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s) {
+  HT_TRY(check_ctl(ctl));
+  const size_t need = truncate_ws_bytes(x);
+  if (!ws || ws_bytes < need) {
+    set_error("truncate workspace too small: need " + std::to_string(need) + " bytes");
+    return kErrArgument;
+  }
+  HT_TRY(plan_truncate(x, P, ws));
+  const Tree& T = *x.T;
+  HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
+  if (!x.orth) {
+    Arena sc = P.scratch;  // R factors live in scratch: needed only during the sweep
+    HT_TRY(run_orthogonalize(x, P.op, sc, sc, s, true));
+  }
+  {
+    Arena sc = P.scratch;
+    HT_TRY(run_gramians(P.o, P.G, sc, s, true));
+  }
+  // batched eigendecomposition + select_rank of all 2d-2 non-root nodes
+  std::vector<EigProblem> eps;
+  for (int t = 1; t < T.nn; ++t) {
+    EigProblem e{};
+    e.S = P.G[t]; e.V = P.EV[t]; e.lam = P.lam[t];
+    e.rank = P.ranks + t; e.status = P.status;
+    e.K = (int)P.o.k[t]; e.nodes = 1;
+    e.eps = ctl->eps > 0 ? ctl->eps : 0.0;
+    e.n_nonroot = T.nn - 1;
+    e.cap = eig_caps(ctl, t);
+    e.s_node = 0; e.v_node = 0; e.l_node = 0;
+    if (!eps.empty()) {
+      EigProblem& b = eps.back();
+      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank) {
+        if (b.nodes == 1) {
+          b.s_node = e.S - b.S; b.v_node = e.V - b.V; b.l_node = e.lam - b.lam;
+          b.nodes = 2;
+          continue;
+        }
+        const long long c = b.nodes;
+        if (b.S + c * b.s_node == e.S && b.V + c * b.v_node == e.V && b.lam + c * b.l_node == e.lam) {
+          b.nodes++;
+          continue;
+        }
+      }
+    }
+    eps.push_back(e);
+  }
+  HT_TRY(eig_batched(eps, s));
+  return kOk;
+}
+
+std::vector<long long> static_ranks(const View& x, const ht_trunc_ctl* ctl, bool& ok) {
+  const Tree& T = *x.T;
+  std::vector<long long> ko = x.orth ? x.k : orth_ranks(x);
+  std::vector<long long> r(T.nn, 1);
+  ok = !(ctl->eps > 0);
+  for (int t = 1; t < T.nn; ++t) {
+    long long v = ko[t];
+    const int cap = eig_caps(ctl, t);
+    if (cap > 0) v = std::min<long long>(v, cap);
+    r[t] = std::max<long long>(1, std::min(v, ko[t]));
+  }
+  return r;
+}
+
+int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View& out, cudaStream_t s) {
+  TruncPlan P;
+  HT_TRY(plan_truncate(x, P, ws));
+  const Tree& T = *x.T;
+  const View& o = P.o;
+  // shape checks of the caller's output
+  for (int t = 1; t < T.nn; ++t)
+    if (out.k[t] > o.k[t]) {
+      set_error("output rank exceeds the orthogonalised rank at node " + std::to_string(t));
+      return kErrShape;
+    }
+  Arena sc = P.scratch;
+  std::vector<GemmDesc> st1, st2, st3;
+  std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
+  for (int t = 1; t < T.nn; ++t)
+    if (!T.leaf(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+  for (int t = 1; t < T.nn; ++t)
+    if (!T.leaf(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
+  for (int t = 1; t < T.nn; ++t) {
+    const long long kt = o.k[t], rt = out.k[t];
+    if (T.leaf(t)) {
+      // U_new (n x r) = Q (n x k) * EV[:, :r]   (arith.py:344)
+      st1.push_back(gemm_desc(o.p[t], kt, 1, P.EV[t], kt, 1, out.p[t], rt, 1, (int)o.n[t], (int)rt, (int)kt));
+      continue;
+    }
+    const int s1 = T.son1[t], s2 = T.son2[t];
+    const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
+    // mode 1: C1 (rt x k1k2) = EV_t^T[:rt] * M1(B)   (arith.py:168)
+    st1.push_back(gemm_desc(P.EV[t], 1, kt, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
+    // mode 2, per slice i: C2_i (r1 x k2) = EV_s1^T[:r1] * C1_i   (arith.py:169)
+    GemmDesc b = gemm_desc(P.EV[s1], 1, k1, C1[t], k2, 1, C2[t], k2, 1, (int)r1, (int)k2, (int)k1);
+    b.nb1 = (int)rt; b.a_b1 = 0; b.b_b1 = k1 * k2; b.c_b1 = r1 * k2;
+    st2.push_back(b);
+    // mode 3: B_new ((rt r1) x r2) = C2 * EV_s2[:, :r2]   (arith.py:170)
+    st3.push_back(gemm_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
+  }
+  {
+    // root: Q1^T B_D Q2   (arith.py:350-351)
+    const int s1 = T.son1[0], s2 = T.son2[0];
+    const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
+    double* tmp = sc.take(r1 * k2);
+    st1.push_back(gemm_desc(P.EV[s1], 1, k1, o.p[0], k2, 1, tmp, k2, 1, (int)r1, (int)k2, (int)k1));
+    st3.push_back(gemm_desc(tmp, k2, 1, P.EV[s2], k2, 1, out.p[0], r2, 1, (int)r1, (int)r2, (int)k2));
+  }
+  merge_gemms(st1);
+  merge_gemms(st2);
+  merge_gemms(st3);
+  HT_TRY(gemm_grouped(st1, s));
+  HT_TRY(gemm_grouped(st2, s));
+  HT_TRY(gemm_grouped(st3, s));
+  return kOk;
+}
+
+int out_view(const ht_tensor* out, const View& x, View& v) {
+  HT_TRY(make_view(out, v));
+  if (out->d != x.T->d) {
+    set_error("output tensor dimension mismatch");
+    return kErrShape;
+  }
+  for (int t = 0; t < x.T->nn; ++t)
+    if (x.T->leaf(t) && v.n[t] != x.n[t]) {
+      set_error("output leaf sizes differ from the input");
+      return kErrShape;
+    }
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// inner product (arith.py:105-123, 246-265)
+// ---------------------------------------------------------------------------
+int run_inner_product(const View& a, const View& c, Arena& ar, double* result, cudaStream_t s, bool exec) {
+  const Tree& T = *a.T;
+  std::vector<double*> phi(T.nn, nullptr);
+  for (int t = 1; t < T.nn; ++t) phi[t] = ar.take(a.k[t] * c.k[t]);
+  const size_t base = ar.off;
+  size_t mx = base;
+  for (int l = T.depth; l >= 1; --l) {
+    ar.off = base;
+    std::vector<GemmDesc> gl, g1, g2, g3;
+    std::vector<ReduceDesc> rs;
+    long long tiles = 0;
+    for (int t : T.levels[l]) tiles += (long long)ceil_div(a.k[t], kGemmBM) * ceil_div(c.k[t], kGemmBN);
+    std::vector<double*> S1s(T.nn, nullptr), S2s(T.nn, nullptr);
+    for (int t : T.levels[l])
+      if (!T.leaf(t)) S1s[t] = ar.take(a.k[t] * a.k[T.son2[t]] * c.k[T.son1[t]]);
+    for (int t : T.levels[l])
+      if (!T.leaf(t)) S2s[t] = ar.take(a.k[t] * c.k[T.son1[t]] * c.k[T.son2[t]]);
+    for (int t : T.levels[l]) {
+      const long long ka = a.k[t], kc = c.k[t];
+      if (T.leaf(t)) {
+        // Phi = U_a^T U_c   (arith.py:105-106)
+        const int S = pick_splits(tiles, a.n[t]);
+        double* Pp = ar.take(S * ka * kc);
+        GemmDesc g = gemm_desc(a.p[t], 1, ka, c.p[t], kc, 1, Pp, kc, 1, (int)ka, (int)kc, (int)a.n[t]);
+        g.splits = S;
+        gl.push_back(g);
+        rs.push_back(ReduceDesc{Pp, phi[t], kc, 1, 0, 0, S, (int)ka, (int)kc, 1, 1, 0, 1.0, 0.0});
+        continue;
+      }
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      const long long ja = a.k[s1], la = a.k[s2], jc = c.k[s1], lc = c.k[s2];
+      double* S1 = S1s[t];
+      double* S2 = S2s[t];
+      // s1[i,l,j'] = sum_j B_a[i,j,l] Phi1[j,j']   (arith.py:116)
+      GemmDesc x1 = gemm_desc(a.p[t], 1, la, phi[s1], jc, 1, S1, jc, 1, (int)la, (int)jc, (int)ja);
+      x1.nb1 = (int)ka; x1.a_b1 = ja * la; x1.b_b1 = 0; x1.c_b1 = la * jc;
+      g1.push_back(x1);
+      // s2[i,j',l'] = sum_l s1[i,l,j'] Phi2[l,l']   (arith.py:117)
+      GemmDesc x2 = gemm_desc(S1, 1, jc, phi[s2], lc, 1, S2, lc, 1, (int)jc, (int)lc, (int)la);
+      x2.nb1 = (int)ka; x2.a_b1 = la * jc; x2.b_b1 = 0; x2.c_b1 = jc * lc;
+      g2.push_back(x2);
+      // Phi_t[i,i'] = sum_{j',l'} s2[i,j',l'] B_c[i',j',l']   (arith.py:118)
+      const int S = pick_splits(tiles, jc * lc);
+      double* Pp = ar.take(S * ka * kc);
+      GemmDesc x3 = gemm_desc(S2, jc * lc, 1, c.p[t], 1, jc * lc, Pp, kc, 1, (int)ka, (int)kc, (int)(jc * lc));
+      x3.splits = S;
+      g3.push_back(x3);
+      rs.push_back(ReduceDesc{Pp, phi[t], kc, 1, 0, 0, S, (int)ka, (int)kc, 1, 1, 0, 1.0, 0.0});
+    }
+    mx = std::max(mx, ar.off);
+    if (exec) {
+      merge_gemms(g1);
+      merge_gemms(g2);
+      HT_TRY(gemm_grouped(gl, s));
+      HT_TRY(gemm_grouped(g1, s));
+      HT_TRY(gemm_grouped(g2, s));
+      HT_TRY(gemm_grouped(g3, s));
+      HT_TRY(reduce_partials(rs, s));
+    }
+  }
+  // root: sum((Phi1^T A Phi2) * C)   (arith.py:121-123)
+  ar.off = base;
+  const int s1 = T.son1[0], s2 = T.son2[0];
+  const long long ka1 = a.k[s1], ka2 = a.k[s2], kc1 = c.k[s1], kc2 = c.k[s2];
+  double* T1 = ar.take(kc1 * ka2);
+  double* T2 = ar.take(kc1 * kc2);
+  mx = std::max(mx, ar.off);
+  if (exec) {
+    std::vector<GemmDesc> g{gemm_desc(phi[s1], 1, kc1, a.p[0], ka2, 1, T1, ka2, 1, (int)kc1, (int)ka2, (int)ka1)};
+    HT_TRY(gemm_grouped(g, s));
+    std::vector<GemmDesc> g4{gemm_desc(T1, ka2, 1, phi[s2], kc2, 1, T2, kc2, 1, (int)kc1, (int)kc2, (int)ka2)};
+    HT_TRY(gemm_grouped(g4, s));
+    HT_TRY(dot(T2, c.p[0], kc1 * kc2, result, s));
+  }
+  ar.off = mx;
+  return kOk;
+}
+
+int check_compatible(const View& a, const View& c) {
+  if (a.T->d != c.T->d) {
+    set_error("tensor dimensions differ: " + std::to_string(a.T->d) + " vs " + std::to_string(c.T->d));
+    return kErrShape;
+  }
+  for (int t = 0; t < a.T->nn; ++t)
+    if (a.T->leaf(t) && a.n[t] != c.n[t]) {
+      set_error("tensor shapes differ");
+      return kErrShape;
+    }
+  return kOk;
+}
+
+}  // namespace
+}  // namespace ht
+
+using namespace ht;
+
+extern "C" {
+
+const char* ht_last_error(void) { return last_error(); }
+const char* ht_version(void) { return "ht_b200 0.1.0 (sm_100a, fp64 DMMA)"; }
+
+int ht_truncate_workspace_size(const ht_tensor* x, size_t* bytes) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  *bytes = truncate_ws_bytes(v);
+  return kOk;
+}
+
+int ht_truncate_static_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, int64_t* out_rank) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  HT_TRY(check_ctl(ctl));
+  bool ok = false;
+  auto r = static_ranks(v, ctl, ok);
+  if (out_rank)
+    for (int t = 0; t < v.T->nn; ++t) out_rank[t] = r[t];
+  return ok ? 1 : 0;
+}
+
+int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int64_t* out_rank,
+                      ht_stream_t stream) {
+  View v;
+  HT_TRY(make_view(x, v));
+  cudaStream_t s = (cudaStream_t)stream;
+  TruncPlan P;
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s));
+  std::vector<int> hr(v.T->nn + 1);
+  HT_CUDA_CHECK(cudaMemcpyAsync(hr.data(), P.ranks, sizeof(int) * (v.T->nn + 1), cudaMemcpyDeviceToHost, s));
+  HT_CUDA_CHECK(cudaStreamSynchronize(s));
+  const int st = hr[v.T->nn];
+  if (st & kEigStatusNotSymmetric) {
+    set_error("matrix is not symmetric within tolerance");
+    return kErrNotSymmetric;
+  }
+  if (st & kEigStatusNonConverged) {
+    set_error("Jacobi eigensolver did not converge");
+    return kErrNonConverged;
+  }
+  out_rank[0] = 1;
+  for (int t = 1; t < v.T->nn; ++t) out_rank[t] = hr[t];
+  return kOk;
+}
+
+int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, const ht_tensor* out,
+                        ht_stream_t stream) {
+  View v, o;
+  HT_TRY(make_view(x, v));
+  HT_TRY(out_view(out, v, o));
+  (void)ctl;
+  if (ws_bytes < truncate_ws_bytes(v)) {
+    set_error("truncate workspace too small");
+    return kErrArgument;
+  }
+  return truncate_phase2(v, ctl, (char*)ws, o, (cudaStream_t)stream);
+}
+
+int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, const ht_tensor* out,
+                ht_stream_t stream) {
+  View v, o;
+  HT_TRY(make_view(x, v));
+  HT_TRY(check_ctl(ctl));
+  bool ok = false;
+  auto r = static_ranks(v, ctl, ok);
+  if (!ok) {
+    set_error("ht_truncate needs shape-determined ranks (fixed-rank control); use ht_truncate_ranks");
+    return kErrArgument;
+  }
+  HT_TRY(out_view(out, v, o));
+  for (int t = 1; t < v.T->nn; ++t)
+    if (o.k[t] != r[t]) {
+      set_error("output ranks do not match the truncation control at node " + std::to_string(t));
+      return kErrShape;
+    }
+  cudaStream_t s = (cudaStream_t)stream;
+  TruncPlan P;
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s));
+  return truncate_phase2(v, ctl, (char*)ws, o, s);
+}
+
+int ht_truncate_eigenvalues(const ht_tensor* x, void* ws, size_t ws_bytes, double* lam, ht_stream_t stream) {
+  View v;
+  HT_TRY(make_view(x, v));
+  if (ws_bytes < truncate_ws_bytes(v)) {
+    set_error("truncate workspace too small");
+    return kErrArgument;
+  }
+  TruncPlan P;
+  HT_TRY(plan_truncate(v, P, (char*)ws));
+  long long off = 0;
+  for (int t = 1; t < v.T->nn; ++t) {
+    HT_CUDA_CHECK(cudaMemcpyAsync(lam + off, P.lam[t], sizeof(double) * P.o.k[t], cudaMemcpyDeviceToDevice,
+                                  (cudaStream_t)stream));
+    off += P.o.k[t];
+  }
+  return kOk;
+}
+
+int ht_orth_ranks(const ht_tensor* x, int64_t* out_rank) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  auto ko = orth_ranks(v);
+  for (int t = 0; t < v.T->nn; ++t) out_rank[t] = ko[t];
+  return kOk;
+}
+
+int ht_orthogonalize_workspace_size(const ht_tensor* x, size_t* bytes) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  OrthPlan op;
+  op.out.assign(v.T->nn, nullptr);
+  Arena ar;
+  HT_TRY(run_orthogonalize(v, op, ar, ar, nullptr, false));
+  *bytes = ar.off + 4096 * (size_t)v.T->nn + 256;
+  return kOk;
+}
+
+int ht_orthogonalize(const ht_tensor* x, void* ws, size_t ws_bytes, const ht_tensor* out, ht_stream_t stream) {
+  View v, o;
+  HT_TRY(make_view(x, v));
+  HT_TRY(out_view(out, v, o));
+  auto ko = orth_ranks(v);
+  for (int t = 1; t < v.T->nn; ++t)
+    if (o.k[t] != ko[t]) {
+      set_error("output ranks must be the orthogonalised ranks");
+      return kErrShape;
+    }
+  size_t need = 0;
+  HT_TRY(ht_orthogonalize_workspace_size(x, &need));
+  if (ws_bytes < need) {
+    set_error("orthogonalize workspace too small");
+    return kErrArgument;
+  }
+  OrthPlan op;
+  op.out = o.p;
+  Arena ar;
+  ar.base = (char*)ws;
+  return run_orthogonalize(v, op, ar, ar, (cudaStream_t)stream, true);
+}
+
+int ht_gramians_workspace_size(const ht_tensor* x, size_t* bytes) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  Arena ar;
+  std::vector<double*> G(v.T->nn, nullptr);
+  HT_TRY(run_gramians(v, G, ar, nullptr, false));
+  *bytes = ar.off + 4096 * (size_t)v.T->nn + 256;
+  return kOk;
+}
+
+int ht_gramians(const ht_tensor* x, void* ws, size_t ws_bytes, double* const* bhat, ht_stream_t stream) {
+  View v;
+  HT_TRY(make_view(x, v));
+  if (!v.orth) {
+    set_error("tensor is not orthogonal; call orthogonalize() first");
+    return kErrNotOrthogonal;
+  }
+  size_t need = 0;
+  HT_TRY(ht_gramians_workspace_size(x, &need));
+  if (ws_bytes < need) {
+    set_error("gramians workspace too small");
+    return kErrArgument;
+  }
+  std::vector<double*> G(bhat, bhat + v.T->nn);
+  Arena ar;
+  ar.base = (char*)ws;
+  return run_gramians(v, G, ar, (cudaStream_t)stream, true);
+}
+
+int ht_add(const ht_tensor* a, const ht_tensor* c, double alpha_c, const ht_tensor* out, ht_stream_t stream) {
+  View va, vc, vo;
+  HT_TRY(make_view(a, va));
+  HT_TRY(make_view(c, vc));
+  HT_TRY(check_compatible(va, vc));
+  HT_TRY(out_view(out, va, vo));
+  const Tree& T = *va.T;
+  for (int t = 1; t < T.nn; ++t)
+    if (vo.k[t] != va.k[t] + vc.k[t]) {
+      set_error("add output ranks must be the sums of the input ranks");
+      return kErrShape;
+    }
+  std::vector<EmbedDesc> ds;
+  for (int t = 0; t < T.nn; ++t) {
+    EmbedDesc e{};
+    e.out = vo.p[t]; e.A = va.p[t]; e.C = vc.p[t];
+    e.alpha_c = t == 0 ? alpha_c : 1.0;
+    if (T.leaf(t)) {
+      // U = [U_a, U_c]   (arith.py:173-174)
+      e.D0 = 1; e.D1 = (int)va.n[t]; e.D2 = (int)vo.k[t];
+      e.a0 = 1; e.a1 = (int)va.n[t]; e.a2 = (int)va.k[t];
+      e.c0 = 1; e.c1 = (int)vc.n[t]; e.c2 = (int)vc.k[t];
+      e.o0 = 0; e.o1 = 0; e.o2 = (int)va.k[t];
+    } else {
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      // block-diagonal embedding   (arith.py:177-192)
+      e.D0 = (int)vo.k[t]; e.D1 = (int)vo.k[s1]; e.D2 = (int)vo.k[s2];
+      e.a0 = (int)va.k[t]; e.a1 = (int)va.k[s1]; e.a2 = (int)va.k[s2];
+      e.c0 = (int)vc.k[t]; e.c1 = (int)vc.k[s1]; e.c2 = (int)vc.k[s2];
+      e.o0 = t == 0 ? 0 : (int)va.k[t]; e.o1 = (int)va.k[s1]; e.o2 = (int)va.k[s2];
+      if (t == 0) { e.D0 = 1; e.a0 = 1; e.c0 = 1; }
+    }
+    ds.push_back(e);
+  }
+  return embed_batched(ds, (cudaStream_t)stream);
+}
+
+int ht_scale(const double* x, double* y, int64_t count, double alpha, ht_stream_t stream) {
+  return scale_copy(x, y, count, alpha, (cudaStream_t)stream);
+}
+
+int ht_inner_product_workspace_size(const ht_tensor* a, const ht_tensor* c, size_t* bytes) {
+  View va, vc;
+  HT_TRY(make_view(a, va, false));
+  HT_TRY(make_view(c, vc, false));
+  HT_TRY(check_compatible(va, vc));
+  Arena ar;
+  HT_TRY(run_inner_product(va, vc, ar, nullptr, nullptr, false));
+  *bytes = ar.off + 4096 * (size_t)va.T->nn + 256;
+  return kOk;
+}
+
+int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws_bytes, double* result_dev,
+                     double* result_host, ht_stream_t stream) {
+  View va, vc;
+  HT_TRY(make_view(a, va));
+  HT_TRY(make_view(c, vc));
+  HT_TRY(check_compatible(va, vc));
+  size_t need = 0;
+  HT_TRY(ht_inner_product_workspace_size(a, c, &need));
+  if (ws_bytes < need || !result_dev) {
+    set_error("inner product workspace too small or no result buffer");
+    return kErrArgument;
+  }
+  Arena ar;
+  ar.base = (char*)ws;
+  cudaStream_t s = (cudaStream_t)stream;
+  HT_TRY(run_inner_product(va, vc, ar, result_dev, s, true));
+  if (result_host) {
+    HT_CUDA_CHECK(cudaMemcpyAsync(result_host, result_dev, sizeof(double), cudaMemcpyDeviceToHost, s));
+    HT_CUDA_CHECK(cudaStreamSynchronize(s));
+  }
+  return kOk;
+}
+
+int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream) {
+  View vx, vo;
+  HT_TRY(make_view(x, vx));
+  if (!op || op->d != x->d) {
+    set_error("operator dimension differs from tensor dimension");
+    return kErrShape;
+  }
+  const Tree& T = *vx.T;
+  HT_TRY(make_view(out, vo));
+  cudaStream_t s = (cudaStream_t)stream;
+  std::vector<KronDesc> kd;
+  std::vector<LeafApplyDesc> ld;
+  std::vector<GemmDesc> gd;
+  for (int t = 0; t < T.nn; ++t) {
+    const long long R = t == 0 ? 1 : op->rank[t];
+    if (t > 0 && vo.k[t] != R * vx.k[t]) {
+      set_error("apply output ranks must be operator rank * tensor rank");
+      return kErrShape;
+    }
+    if (T.leaf(t)) {
+      const ht_gmat* cols = op->leaf_cols[t];
+      const long long k = vx.k[t];
+      for (long long r = 0; r < R; ++r) {
+        const ht_gmat& g = cols[r];
+        if (g.cols != vx.n[t] || g.rows != vo.n[t]) {
+          set_error("operator column sizes do not match tensor shape");
+          return kErrShape;
+        }
+        if (g.kind == 0) {
+          gd.push_back(gemm_desc(g.values, g.cols, 1, vx.p[t], k, 1, vo.p[t] + r * k, R * k, 1, (int)g.rows, (int)k,
+                                 (int)g.cols));
+        } else {
+          LeafApplyDesc e{};
+          e.kind = g.kind; e.vals = g.values; e.indptr = g.indptr; e.indices = g.indices;
+          e.U = vx.p[t]; e.V = vo.p[t]; e.n_out = (int)g.rows; e.k = (int)k; e.ldv = (int)(R * k);
+          e.col0 = (int)(r * k);
+          ld.push_back(e);
+        }
+      }
+      continue;
+    }
+    const int s1 = T.son1[t], s2 = T.son2[t];
+    KronDesc e{};
+    e.out = vo.p[t]; e.H = op->node[t]; e.B = vx.p[t];
+    if (t == 0) {
+      e.kp = 1; e.ki = 1;
+    } else {
+      e.kp = (int)op->rank[t]; e.ki = (int)vx.k[t];
+    }
+    e.kq = (int)op->rank[s1]; e.kr = (int)op->rank[s2];
+    e.kj = (int)vx.k[s1]; e.kl = (int)vx.k[s2];
+    kd.push_back(e);
+  }
+  HT_TRY(kron_batched(kd, s));
+  HT_TRY(leaf_apply_batched(ld, s));
+  HT_TRY(gemm_grouped(gd, s));
+  return kOk;
+}
+
+int ht_qr_workspace_size(int64_t m, int64_t K, int64_t nodes, size_t* bytes) {
+  QrProblem q{};
+  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes; q.P = 0;
+  HT_TRY(qr_plan(q, kSMs));
+  *bytes = (size_t)qr_workspace_doubles(q) * sizeof(double) + 1024;
+  return kOk;
+}
+
+int ht_qr_batched(int64_t m, int64_t K, int64_t nodes, const double* A, int64_t a_r, int64_t a_c, int64_t a_node,
+                  double* Q, int64_t q_r, int64_t q_c, int64_t q_node, double* R, int64_t r_ld, int64_t r_node,
+                  void* ws, size_t ws_bytes, ht_stream_t stream) {
+  QrProblem q{};
+  q.A = A; q.a_r = a_r; q.a_c = a_c; q.a_node = a_node;
+  q.Q = Q; q.q_r = q_r; q.q_c = q_c; q.q_node = q_node;
+  q.R = R; q.r_ld = r_ld; q.r_node = r_node;
+  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes; q.P = 0;
+  HT_TRY(qr_plan(q, kSMs));
+  const size_t need = (size_t)qr_workspace_doubles(q) * sizeof(double);
+  if (ws_bytes < need) {
+    set_error("qr workspace too small");
+    return kErrArgument;
+  }
+  qr_bind_workspace(q, (double*)ws);
+  std::vector<QrProblem> v{q};
+  return qr_batched(v, (cudaStream_t)stream);
+}
+
+int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double* lam, ht_stream_t stream) {
+  int* st = nullptr;
+  HT_CUDA_CHECK(cudaMallocAsync((void**)&st, sizeof(int), (cudaStream_t)stream));
+  HT_CUDA_CHECK(cudaMemsetAsync(st, 0, sizeof(int), (cudaStream_t)stream));
+  EigProblem e{};
+  e.S = S; e.s_node = K * K; e.V = V; e.v_node = K * K; e.lam = lam; e.l_node = K;
+  e.status = st; e.K = (int)K; e.nodes = (int)nodes; e.n_nonroot = 1;
+  std::vector<EigProblem> v{e};
+  int rc = eig_batched(v, (cudaStream_t)stream);
+  int hs = 0;
+  cudaMemcpyAsync(&hs, st, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  cudaFreeAsync(st, (cudaStream_t)stream);
+  HT_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
+  if (rc != kOk) return rc;
+  if (hs & kEigStatusNotSymmetric) {
+    set_error("matrix is not symmetric within tolerance");
+    return kErrNotSymmetric;
+  }
+  if (hs & kEigStatusNonConverged) {
+    set_error("Jacobi eigensolver did not converge");
+    return kErrNonConverged;
+  }
+  return kOk;
+}
+
+int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A, int64_t a_m,
+                    int64_t a_k, int64_t a_b, const double* B, int64_t b_k, int64_t b_n, int64_t b_b, double beta,
+                    double* C, int64_t c_m, int64_t c_n, int64_t c_b, ht_stream_t stream) {
+  GemmDesc g = gemm_desc(A, a_m, a_k, B, b_k, b_n, C, c_m, c_n, (int)M, (int)N, (int)K, alpha, beta);
+  g.nb1 = (int)batch; g.a_b1 = a_b; g.b_b1 = b_b; g.c_b1 = c_b;
+  std::vector<GemmDesc> v{g};
+  return gemm_grouped(v, (cudaStream_t)stream);
+}
+
+}  // extern "C"

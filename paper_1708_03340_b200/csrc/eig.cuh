@@ -1,0 +1,39 @@
+// Batched symmetric eigensolver (parallel cyclic two-sided Jacobi in shared
+// memory) with the reference's post-processing fused in: stable descending
+// order, eigenvalues clamped >= 0 (kernels.py:35-54) and the per-node rank
+// choice of select_rank (arith.py:69-88) -- all on device, no host sync.
+//
+// Jacobi (rather than tridiagonalisation) because the reduced Gramians of the
+// C1 parity case are graded: their small eigenvalues (~1e-20 relative) are only
+// determined to high RELATIVE accuracy by a Jacobi method with the
+// |a_pq| <= eps*sqrt(|a_pp a_qq|) stopping rule (Demmel-Veselic).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ht {
+
+struct EigProblem {
+  const double* S;  // symmetric K x K, row-major (ld K), node stride s_node
+  long long s_node;
+  double* V;        // eigenvectors, row-major K x K: V[i*K + j] = i-th entry of eigenvector j
+  long long v_node;
+  double* lam;      // K eigenvalues, descending, clamped >= 0
+  long long l_node;
+  int* rank;        // selected rank per node (may be null)
+  int* status;      // device int, OR-ed with error bits (may be null)
+  int K, nodes;
+  double eps;       // absolute truncation accuracy; <= 0: none
+  int n_nonroot;    // 2d - 2
+  int cap;          // rank cap; <= 0: none
+};
+
+constexpr int kEigMaxK = 112;
+constexpr int kEigStatusNotSymmetric = 1;
+constexpr int kEigStatusNonConverged = 2;
+
+int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream);
+
+}  // namespace ht

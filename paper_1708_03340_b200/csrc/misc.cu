@@ -1,0 +1,205 @@
+#include <algorithm>
+
+#include "misc.cuh"
+#include "prof.cuh"
+
+namespace ht {
+
+namespace {
+
+constexpr int MAXD = 64;
+
+struct EmbedBatch {
+  int count;
+  int begin[MAXD + 1];
+  EmbedDesc d[MAXD];
+};
+
+struct KronBatch {
+  int count;
+  int begin[MAXD + 1];
+  KronDesc d[MAXD];
+};
+
+struct LeafBatch {
+  int count;
+  int begin[MAXD + 1];
+  LeafApplyDesc d[MAXD];
+};
+
+template <typename B>
+__device__ __forceinline__ int find(const B& b) {
+  int di = 0;
+  while (di + 1 < b.count && (int)blockIdx.x >= b.begin[di + 1]) ++di;
+  return di;
+}
+
+__global__ void embed_kernel(const __grid_constant__ EmbedBatch b) {
+  const int di = find(b);
+  const EmbedDesc& e = b.d[di];
+  const long long total = (long long)e.D0 * e.D1 * e.D2;
+  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
+  for (long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x; x < total; x += stride) {
+    const int i2 = (int)(x % e.D2);
+    const long long r = x / e.D2;
+    const int i1 = (int)(r % e.D1);
+    const int i0 = (int)(r / e.D1);
+    double v = 0.0;
+    if (i0 < e.a0 && i1 < e.a1 && i2 < e.a2) {
+      v = e.A[((long long)i0 * e.a1 + i1) * e.a2 + i2];
+    } else {
+      const int j0 = i0 - e.o0, j1 = i1 - e.o1, j2 = i2 - e.o2;
+      if (j0 >= 0 && j1 >= 0 && j2 >= 0 && j0 < e.c0 && j1 < e.c1 && j2 < e.c2)
+        v = e.alpha_c * e.C[((long long)j0 * e.c1 + j1) * e.c2 + j2];
+    }
+    e.out[x] = v;
+  }
+}
+
+__global__ void kron_kernel(const __grid_constant__ KronBatch b) {
+  const int di = find(b);
+  const KronDesc& k = b.d[di];
+  const long long D1 = (long long)k.kq * k.kj, D2 = (long long)k.kr * k.kl;
+  const long long total = (long long)k.kp * k.ki * D1 * D2;
+  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
+  for (long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x; x < total; x += stride) {
+    const long long i2 = x % D2, rr = x / D2;
+    const long long i1 = rr % D1, i0 = rr / D1;
+    const int p = (int)(i0 / k.ki), i = (int)(i0 % k.ki);
+    const int q = (int)(i1 / k.kj), j = (int)(i1 % k.kj);
+    const int r = (int)(i2 / k.kl), l = (int)(i2 % k.kl);
+    k.out[x] = k.H[((long long)p * k.kq + q) * k.kr + r] * k.B[((long long)i * k.kj + j) * k.kl + l];
+  }
+}
+
+__global__ void leaf_apply_kernel(const __grid_constant__ LeafBatch b) {
+  const int di = find(b);
+  const LeafApplyDesc& e = b.d[di];
+  const long long total = (long long)e.n_out * e.k;
+  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
+  for (long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x; x < total; x += stride) {
+    const int i = (int)(x / e.k), l = (int)(x % e.k);
+    double v;
+    if (e.kind == 1) {
+      v = e.vals[i] * e.U[(long long)i * e.k + l];
+    } else {
+      v = 0.0;
+      for (int z = e.indptr[i]; z < e.indptr[i + 1]; ++z) v = fma(e.vals[z], e.U[(long long)e.indices[z] * e.k + l], v);
+    }
+    e.V[(long long)i * e.ldv + e.col0 + l] = v;
+  }
+}
+
+__global__ void scale_kernel(const double* x, double* y, long long n, double a) {
+  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    y[i] = a * x[i];
+}
+
+__global__ void dot_kernel(const double* a, const double* b, long long n, double* out) {
+  __shared__ double part[32];
+  double s = 0.0;
+  for (long long i = threadIdx.x; i < n; i += blockDim.x) s = fma(a[i], b[i], s);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? part[threadIdx.x] : 0.0;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) *out = v;
+  }
+}
+
+int blocks_for(long long total) { return (int)std::max<long long>(1, std::min<long long>(ceil_div(total, 256), 2048)); }
+
+}  // namespace
+
+int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    EmbedBatch b;
+    b.count = 0;
+    int blocks = 0;
+    while (i < descs.size() && b.count < MAXD) {
+      const EmbedDesc& d = descs[i++];
+      const long long total = (long long)d.D0 * d.D1 * d.D2;
+      if (total == 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += blocks_for(total);
+      b.d[b.count++] = d;
+    }
+    if (!b.count) continue;
+    b.begin[b.count] = blocks;
+    ProfToken tok = prof_begin(stream);
+    embed_kernel<<<blocks, 256, 0, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "embed", stream, 0.0, 0.0);
+  }
+  return kOk;
+}
+
+int kron_batched(const std::vector<KronDesc>& descs, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    KronBatch b;
+    b.count = 0;
+    int blocks = 0;
+    while (i < descs.size() && b.count < MAXD) {
+      const KronDesc& d = descs[i++];
+      const long long total = (long long)d.kp * d.kq * d.kr * d.ki * d.kj * d.kl;
+      if (total == 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += blocks_for(total);
+      b.d[b.count++] = d;
+    }
+    if (!b.count) continue;
+    b.begin[b.count] = blocks;
+    ProfToken tok = prof_begin(stream);
+    kron_kernel<<<blocks, 256, 0, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "kron", stream, 0.0, 0.0);
+  }
+  return kOk;
+}
+
+int leaf_apply_batched(const std::vector<LeafApplyDesc>& descs, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    LeafBatch b;
+    b.count = 0;
+    int blocks = 0;
+    while (i < descs.size() && b.count < MAXD) {
+      const LeafApplyDesc& d = descs[i++];
+      const long long total = (long long)d.n_out * d.k;
+      if (total == 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += blocks_for(total);
+      b.d[b.count++] = d;
+    }
+    if (!b.count) continue;
+    b.begin[b.count] = blocks;
+    ProfToken tok = prof_begin(stream);
+    leaf_apply_kernel<<<blocks, 256, 0, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "leaf_apply", stream, 0.0, 0.0);
+  }
+  return kOk;
+}
+
+int scale_copy(const double* x, double* y, long long n, double alpha, cudaStream_t stream) {
+  if (n <= 0) return kOk;
+  ProfToken tok = prof_begin(stream);
+  scale_kernel<<<blocks_for(n), 256, 0, stream>>>(x, y, n, alpha);
+  HT_LAUNCH_CHECK();
+  prof_end(tok, "scale", stream, 0.0, 16.0 * n);
+  return kOk;
+}
+
+int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream) {
+  ProfToken tok = prof_begin(stream);
+  dot_kernel<<<1, 1024, 0, stream>>>(a, b, n, out);
+  HT_LAUNCH_CHECK();
+  prof_end(tok, "dot", stream, 2.0 * n, 16.0 * n);
+  return kOk;
+}
+
+}  // namespace ht

@@ -1,0 +1,53 @@
+// HBM-bound elementwise kernels of the HT arithmetic: the Lemma-3 block
+// embedding of add (arith.py:173-192), the Kronecker transfer tensors of the
+// operator application (arith.py:204-213), the leaf images W_r U of diagonal /
+// CSR operator columns (arith.py:195-201, format.py:167-173), scaling and dots.
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ht {
+
+// out(i0,i1,i2) over dims D = A placed at 0 (dims a) + C placed at offset o (dims c), 0 elsewhere.
+struct EmbedDesc {
+  double* out;
+  const double* A;
+  const double* C;
+  int D0, D1, D2;
+  int a0, a1, a2;
+  int c0, c1, c2;
+  int o0, o1, o2;
+  double alpha_c;  // scale applied to the C block
+};
+int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream);
+
+// out[(p*ki+i), (q*kj+j), (r*kl+l)] = H[p,q,r] * B[i,j,l]
+struct KronDesc {
+  double* out;
+  const double* H;
+  const double* B;
+  int kp, kq, kr;
+  int ki, kj, kl;
+};
+int kron_batched(const std::vector<KronDesc>& descs, cudaStream_t stream);
+
+// Leaf operator column applied to U (n_in x k row-major), written into columns
+// [col0, col0+k) of V (n_out x ldv row-major).  kind 1: diagonal, kind 2: CSR.
+struct LeafApplyDesc {
+  int kind;
+  const double* vals;
+  const int* indptr;
+  const int* indices;
+  const double* U;
+  double* V;
+  int n_out, k, ldv, col0;
+};
+int leaf_apply_batched(const std::vector<LeafApplyDesc>& descs, cudaStream_t stream);
+
+int scale_copy(const double* x, double* y, long long n, double alpha, cudaStream_t stream);
+// out[0] = sum_i a[i] * b[i]   (single CTA, deterministic order)
+int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream);
+
+}  // namespace ht

@@ -1,0 +1,479 @@
+"""Device-resident HT containers (mirror of the reference ``htucker.format``).
+
+:class:`HTensor` keeps the reference constructor ``HTensor(tree, leaves,
+transfer, root_matrix, orthogonal=False)`` (format.py:50-132) but stores every
+node array in HBM as a float64 CUDA tensor.  Arrays created by this package
+live in one contiguous *arena* per tensor (node arrays in breadth-first id
+order, C-order -- exactly the layout the C ABI expects), so host<->device
+transfer of a whole tensor is a single copy.  Node arrays may also be shared
+between tensors (``scale`` reuses leaves and transfers like arith.py:370-371).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _lib
+from .tree import DimensionTree, build_balanced_tree
+
+F64 = torch.float64
+
+
+def _device(device=None) -> torch.device:
+    if device is not None:
+        return torch.device(device)
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_1708_03340_b200 needs a CUDA device (B200); there is no CPU fallback")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def node_shape(tree: DimensionTree, t: int, sizes: dict, ranks: dict) -> tuple:
+    """C-order shape of node ``t`` given leaf sizes (by node id) and ranks (by node id)."""
+    node = tree.node(t)
+    if node.is_leaf:
+        return (sizes[t], ranks[t])
+    s1, s2 = node.sons
+    if node.is_root:
+        return (ranks[s1], ranks[s2])
+    return (ranks[t], ranks[s1], ranks[s2])
+
+
+class HTensor:
+    """A tensor in hierarchical Tucker format, resident on the GPU.
+
+    ``leaves``/``transfer``/``root_matrix`` accept numpy arrays or torch tensors
+    (copied to the device in one transfer) exactly like the reference
+    constructor; the attributes hold CUDA float64 tensors.
+    """
+
+    def __init__(self, tree: DimensionTree, leaves: dict, transfer: dict, root_matrix,
+                 orthogonal: bool = False, *, device=None):
+        self.tree = tree
+        self.orthogonal = bool(orthogonal)
+        arrays = {}
+        for t, u in leaves.items():
+            arrays[int(t)] = u
+        for t, b in transfer.items():
+            arrays[int(t)] = b
+        arrays[0] = root_matrix
+        if all(isinstance(v, torch.Tensor) and v.is_cuda and v.dtype == F64 for v in arrays.values()):
+            self._nodes = {t: v.contiguous() for t, v in arrays.items()}
+            self._arena = None
+        else:
+            self._nodes, self._arena = _upload(tree, arrays, _device(device))
+        self._cstruct = None
+        self.validate()
+
+    # -- internal constructors -------------------------------------------------
+
+    @classmethod
+    def _wrap(cls, tree, nodes: dict, orthogonal: bool, arena=None) -> "HTensor":
+        obj = cls.__new__(cls)
+        obj.tree = tree
+        obj.orthogonal = bool(orthogonal)
+        obj._nodes = nodes
+        obj._arena = arena
+        obj._cstruct = None
+        return obj
+
+    @classmethod
+    def empty(cls, tree: DimensionTree, sizes_by_node: dict, ranks: dict, orthogonal: bool = False,
+              device=None) -> "HTensor":
+        """Allocate an uninitialised tensor (one arena) with the given leaf sizes / ranks."""
+        dev = _device(device)
+        shapes = {t: node_shape(tree, t, sizes_by_node, ranks) for t in range(len(tree.nodes))}
+        total = sum(math.prod(s) for s in shapes.values())
+        arena = torch.empty(total, dtype=F64, device=dev)
+        nodes, off = {}, 0
+        for t in range(len(tree.nodes)):
+            n = math.prod(shapes[t])
+            nodes[t] = arena[off:off + n].view(shapes[t])
+            off += n
+        return cls._wrap(tree, nodes, orthogonal, arena)
+
+    @classmethod
+    def from_numpy(cls, tree, leaves, transfer, root_matrix, orthogonal=False, device=None) -> "HTensor":
+        return cls(tree, leaves, transfer, root_matrix, orthogonal, device=device)
+
+    # -- reference attributes --------------------------------------------------
+
+    @property
+    def leaves(self) -> dict:
+        return {n.index: self._nodes[n.index] for n in self.tree.nodes if n.is_leaf}
+
+    @property
+    def transfer(self) -> dict:
+        return {n.index: self._nodes[n.index] for n in self.tree.inner_nodes}
+
+    @property
+    def root_matrix(self) -> torch.Tensor:
+        return self._nodes[0]
+
+    def node_array(self, t: int) -> torch.Tensor:
+        return self._nodes[t]
+
+    def rank(self, node_id: int) -> int:
+        node = self.tree.node(node_id)
+        if node.is_root:
+            return 1
+        if node.is_leaf:
+            return int(self._nodes[node_id].shape[1])
+        return int(self._nodes[node_id].shape[0])
+
+    @property
+    def ranks(self) -> dict:
+        return {n.index: self.rank(n.index) for n in self.tree.non_root}
+
+    @property
+    def max_rank(self) -> int:
+        return max(self.ranks.values())
+
+    @property
+    def shape(self) -> tuple:
+        return tuple(int(self._nodes[self.tree.leaf_for_dim(mu).index].shape[0])
+                     for mu in range(1, self.tree.d + 1))
+
+    @property
+    def device(self) -> torch.device:
+        return self._nodes[0].device
+
+    def validate(self) -> None:
+        """format.py:101-119: rank chain along every edge."""
+        tree = self.tree
+        for node in tree.nodes:
+            if node.is_leaf:
+                if node.index not in self._nodes:
+                    raise ValueError(f"missing leaf frame for node {node.index}")
+                if self._nodes[node.index].dim() != 2:
+                    raise ValueError(f"leaf {node.index} must be a matrix")
+                continue
+            s1, s2 = node.sons
+            k1, k2 = self.rank(s1), self.rank(s2)
+            arr = self._nodes.get(node.index)
+            if arr is None:
+                raise ValueError(f"missing array for node {node.index}")
+            got = tuple(arr.shape) if node.is_root else tuple(arr.shape[1:])
+            if got != (k1, k2):
+                raise ValueError(f"rank chain broken at node {node.index}: transfer sees {got}, "
+                                 f"sons have ranks ({k1}, {k2})")
+
+    def copy(self) -> "HTensor":
+        nodes = {t: v.clone() for t, v in self._nodes.items()}
+        return HTensor._wrap(self.tree, nodes, self.orthogonal)
+
+    def storage_size(self) -> int:
+        return int(sum(v.numel() for v in self._nodes.values()))
+
+    # -- host transfer ---------------------------------------------------------
+
+    def to_numpy(self):
+        """(leaves, transfer, root_matrix) as numpy dicts -- one D2H copy when arena-backed."""
+        if self._arena is not None:
+            host = self._arena.cpu().numpy()
+            out, off = {}, 0
+            for t in range(len(self.tree.nodes)):
+                a = self._nodes[t]
+                out[t] = host[off:off + a.numel()].reshape(tuple(a.shape))
+                off += a.numel()
+        else:
+            out = {t: v.cpu().numpy() for t, v in self._nodes.items()}
+        leaves = {n.index: out[n.index] for n in self.tree.nodes if n.is_leaf}
+        transfer = {n.index: out[n.index] for n in self.tree.inner_nodes}
+        return leaves, transfer, out[0]
+
+    # -- pinned host arenas (end-to-end path) ----------------------------------
+
+    @classmethod
+    def from_host_arena(cls, tree: DimensionTree, sizes_by_node: dict, ranks: dict, host: torch.Tensor,
+                        orthogonal: bool = False, device=None) -> "HTensor":
+        """Upload a flat host buffer (node arrays in BFS id order, C-order; ideally
+        pinned) with ONE asynchronous host->device copy."""
+        out = cls.empty(tree, sizes_by_node, ranks, orthogonal, device)
+        if host.numel() != out._arena.numel():
+            raise ValueError("host arena size does not match the tensor shapes")
+        out._arena.copy_(host, non_blocking=True)
+        return out
+
+    def to_host_arena(self, host: torch.Tensor | None = None) -> torch.Tensor:
+        """Copy the whole tensor into a flat (pinned) host buffer with one D2H copy."""
+        if self._arena is None:
+            flat = torch.cat([self._nodes[t].reshape(-1) for t in range(len(self.tree.nodes))])
+        else:
+            flat = self._arena
+        if host is None:
+            host = torch.empty(flat.numel(), dtype=F64, pin_memory=True)
+        host.copy_(flat, non_blocking=True)
+        return host
+
+    def host_layout(self):
+        """(sizes_by_node, ranks) needed to rebuild this tensor from a host arena."""
+        return ({leaf.index: int(self._nodes[leaf.index].shape[0]) for leaf in self.tree.leaves},
+                {t: self.rank(t) for t in range(1, len(self.tree.nodes))})
+
+    # -- C ABI -----------------------------------------------------------------
+
+    def _c(self) -> _lib.CTensor:
+        if self._cstruct is None:
+            tree = self.tree
+            n = _lib.i64_array(self.shape)
+            ranks = _lib.i64_array([1] + [self.rank(t) for t in range(1, len(tree.nodes))])
+            ptrs = _lib.ptr_array([self._nodes[t].data_ptr() for t in range(len(tree.nodes))])
+            cs = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
+                              ctypes.cast(ranks, ctypes.POINTER(ctypes.c_int64)),
+                              ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), int(self.orthogonal))
+            self._cstruct = (cs, n, ranks, ptrs)
+        cs = self._cstruct[0]
+        cs.orthogonal = int(self.orthogonal)
+        return cs
+
+    def __repr__(self) -> str:
+        return (f"HTensor(d={self.tree.d}, shape={self.shape}, max_rank={self.max_rank}, "
+                f"orthogonal={self.orthogonal}, device={self.device})")
+
+
+def _upload(tree: DimensionTree, arrays: dict, dev: torch.device):
+    """Pack node arrays (numpy / torch) into one pinned buffer and copy it to HBM."""
+    host = {}
+    for t, a in arrays.items():
+        if isinstance(a, torch.Tensor):
+            a = a.detach().to("cpu", F64).numpy()
+        host[t] = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    total = sum(a.size for a in host.values())
+    pinned = torch.empty(total, dtype=F64, pin_memory=True)
+    buf = pinned.numpy()
+    off = 0
+    layout = {}
+    for t in range(len(tree.nodes)):
+        if t not in host:
+            raise ValueError(f"missing array for node {t}")
+        a = host[t]
+        buf[off:off + a.size] = a.ravel()
+        layout[t] = (off, a.shape)
+        off += a.size
+    arena = torch.empty(total, dtype=F64, device=dev)
+    arena.copy_(pinned, non_blocking=True)
+    nodes = {t: arena[o:o + math.prod(s)].view(s) for t, (o, s) in layout.items()}
+    # keep the pinned buffer alive until the asynchronous copy has executed
+    _PINNED_KEEPALIVE.append((torch.cuda.current_stream(dev).record_event(), pinned))
+    _trim_keepalive()
+    return nodes, arena
+
+
+_PINNED_KEEPALIVE: list = []
+
+
+def _trim_keepalive():
+    while _PINNED_KEEPALIVE and _PINNED_KEEPALIVE[0][0].query():
+        _PINNED_KEEPALIVE.pop(0)
+
+
+# ---------------------------------------------------------------------------
+# operators (reference format.py:135-250)
+# ---------------------------------------------------------------------------
+
+
+class GeneralizedMatrix:
+    """A linear map R^n -> R^m stored dense, diagonal or CSR (format.py:135-180)."""
+
+    def __init__(self, kind: str, data):
+        if kind not in ("dense", "diagonal", "csr"):
+            raise ValueError(f"unknown kind {kind}")
+        self.kind = kind
+        self.data = data
+        self._dev = None
+
+    @staticmethod
+    def dense(mat) -> "GeneralizedMatrix":
+        return GeneralizedMatrix("dense", np.asarray(mat, dtype=np.float64))
+
+    @staticmethod
+    def diagonal(vec) -> "GeneralizedMatrix":
+        return GeneralizedMatrix("diagonal", np.asarray(vec, dtype=np.float64).ravel())
+
+    @staticmethod
+    def csr(mat) -> "GeneralizedMatrix":
+        import scipy.sparse as sp
+
+        m = sp.csr_matrix(mat, dtype=np.float64)
+        m.sort_indices()
+        return GeneralizedMatrix("csr", m)
+
+    @property
+    def shape(self) -> tuple:
+        if self.kind == "diagonal":
+            n = self.data.shape[0]
+            return (n, n)
+        return tuple(self.data.shape)
+
+    def to_dense(self) -> np.ndarray:
+        if self.kind == "diagonal":
+            return np.diag(self.data)
+        if self.kind == "csr":
+            return self.data.toarray()
+        return np.asarray(self.data)
+
+    def device_struct(self, dev) -> _lib.CGmat:
+        """Upload once; returns the ht_gmat descriptor (keeps the device arrays alive)."""
+        if self._dev is None:
+            rows, cols = self.shape
+            if self.kind == "dense":
+                vals = torch.as_tensor(np.ascontiguousarray(self.data), dtype=F64).to(dev)
+                self._dev = (_lib.CGmat(0, rows, cols, rows * cols, vals.data_ptr(), None, None), vals)
+            elif self.kind == "diagonal":
+                vals = torch.as_tensor(self.data, dtype=F64).to(dev)
+                self._dev = (_lib.CGmat(1, rows, cols, rows, vals.data_ptr(), None, None), vals)
+            else:
+                vals = torch.as_tensor(self.data.data, dtype=F64).to(dev)
+                ip = torch.as_tensor(self.data.indptr.astype(np.int32)).to(dev)
+                ix = torch.as_tensor(self.data.indices.astype(np.int32)).to(dev)
+                self._dev = (_lib.CGmat(2, rows, cols, int(self.data.nnz), vals.data_ptr(), ip.data_ptr(),
+                                        ix.data_ptr()), vals, ip, ix)
+        return self._dev[0]
+
+
+class HTOperator:
+    """Tree-format linear operator (format.py:183-250): leaf columns are
+    :class:`GeneralizedMatrix` lists; transfer tensors / root live on the GPU."""
+
+    def __init__(self, tree: DimensionTree, leaves: dict, transfer: dict, root_matrix, *, device=None):
+        self.tree = tree
+        self.leaves = {int(t): list(cols) for t, cols in leaves.items()}
+        dev = _device(device)
+        self._dev = dev
+        self.transfer = {int(t): torch.as_tensor(np.asarray(b, dtype=np.float64) if not isinstance(b, torch.Tensor)
+                                                 else b, dtype=F64).to(dev).contiguous()
+                         for t, b in transfer.items()}
+        self.root_matrix = torch.as_tensor(np.asarray(root_matrix, dtype=np.float64)
+                                           if not isinstance(root_matrix, torch.Tensor) else root_matrix,
+                                           dtype=F64).to(dev).contiguous()
+        self._cstruct = None
+        self.validate()
+
+    def rank(self, node_id: int) -> int:
+        node = self.tree.node(node_id)
+        if node.is_root:
+            return 1
+        if node.is_leaf:
+            return len(self.leaves[node_id])
+        return int(self.transfer[node_id].shape[0])
+
+    @property
+    def ranks(self) -> dict:
+        return {n.index: self.rank(n.index) for n in self.tree.non_root}
+
+    def leaf_shape(self, node_id: int) -> tuple:
+        return self.leaves[node_id][0].shape
+
+    @property
+    def row_sizes(self) -> tuple:
+        return tuple(self.leaf_shape(self.tree.leaf_for_dim(mu).index)[0] for mu in range(1, self.tree.d + 1))
+
+    @property
+    def col_sizes(self) -> tuple:
+        return tuple(self.leaf_shape(self.tree.leaf_for_dim(mu).index)[1] for mu in range(1, self.tree.d + 1))
+
+    def validate(self) -> None:
+        tree = self.tree
+        for node in tree.nodes:
+            if node.is_leaf:
+                cols = self.leaves.get(node.index)
+                if not cols:
+                    raise ValueError(f"missing leaf columns for node {node.index}")
+                if len({c.shape for c in cols}) != 1:
+                    raise ValueError(f"leaf {node.index} mixes column shapes")
+                continue
+            s1, s2 = node.sons
+            got = tuple(self.root_matrix.shape) if node.is_root else tuple(self.transfer[node.index].shape[1:])
+            if got != (self.rank(s1), self.rank(s2)):
+                raise ValueError(f"rank chain broken at operator node {node.index}")
+
+    def _c(self) -> _lib.COperator:
+        if self._cstruct is None:
+            tree = self.tree
+            nn = len(tree.nodes)
+            ranks = _lib.i64_array([1] + [self.rank(t) for t in range(1, nn)])
+            col_arrays = []
+            leaf_ptrs = (ctypes.POINTER(_lib.CGmat) * nn)()
+            for t in range(nn):
+                if tree.node(t).is_leaf:
+                    arr = (_lib.CGmat * len(self.leaves[t]))(*[g.device_struct(self._dev) for g in self.leaves[t]])
+                    col_arrays.append(arr)
+                    leaf_ptrs[t] = ctypes.cast(arr, ctypes.POINTER(_lib.CGmat))
+            node_ptrs = _lib.ptr_array([self.root_matrix.data_ptr() if t == 0 else
+                                        (self.transfer[t].data_ptr() if t in self.transfer else 0)
+                                        for t in range(nn)])
+            cs = _lib.COperator(tree.d, ctypes.cast(ranks, ctypes.POINTER(ctypes.c_int64)),
+                                ctypes.cast(leaf_ptrs, ctypes.POINTER(ctypes.POINTER(_lib.CGmat))),
+                                ctypes.cast(node_ptrs, ctypes.POINTER(ctypes.c_void_p)))
+            self._cstruct = (cs, ranks, col_arrays, leaf_ptrs, node_ptrs)
+        return self._cstruct[0]
+
+    def __repr__(self) -> str:
+        return f"HTOperator(d={self.tree.d}, rows={self.row_sizes}, cols={self.col_sizes})"
+
+
+# ---------------------------------------------------------------------------
+# constructors (reference format.py:262-336)
+# ---------------------------------------------------------------------------
+
+
+def _uniform_ranks(tree, k) -> dict:
+    if isinstance(k, dict):
+        return {n.index: int(k[n.index]) for n in tree.non_root}
+    return {n.index: int(k) for n in tree.non_root}
+
+
+def _leaf_sizes(tree, n) -> dict:
+    if np.isscalar(n):
+        return {leaf.index: int(n) for leaf in tree.leaves}
+    sizes = list(n)
+    if len(sizes) != tree.d:
+        raise ValueError(f"need {tree.d} leaf sizes, got {len(sizes)}")
+    return {tree.leaf_for_dim(mu).index: int(sizes[mu - 1]) for mu in range(1, tree.d + 1)}
+
+
+def random_htensor(tree: DimensionTree, n, k, seed: int, device=None) -> HTensor:
+    """Uniform [-1, 1] entries from PCG64(seed) in the reference's node order
+    (format.py:271-301): the same seed gives the same tensor as the reference."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    ranks = _uniform_ranks(tree, k)
+    sizes = _leaf_sizes(tree, n)
+    leaves, transfer, root = {}, {}, None
+    for node in tree.nodes:
+        if node.is_leaf:
+            nm, km = sizes[node.index], ranks[node.index]
+            if km > nm:
+                raise ValueError(f"leaf rank {km} exceeds size {nm} at node {node.index}")
+            leaves[node.index] = rng.uniform(-1.0, 1.0, size=(nm, km))
+            continue
+        s1, s2 = node.sons
+        k1, k2 = ranks[s1], ranks[s2]
+        if node.is_root:
+            root = rng.uniform(-1.0, 1.0, size=(k1, k2))
+            continue
+        kt = ranks[node.index]
+        if kt > k1 * k2:
+            raise ValueError(f"rank {kt} at node {node.index} exceeds structural bound {k1 * k2}")
+        transfer[node.index] = rng.uniform(-1.0, 1.0, size=(kt, k1, k2))
+    return HTensor(tree, leaves, transfer, root, device=device)
+
+
+def identity_htoperator(tree: DimensionTree, n) -> HTOperator:
+    """Rank-1 identity operator (format.py:330-336)."""
+    sizes = _leaf_sizes(tree, n)
+    leaves = {leaf.index: [GeneralizedMatrix.diagonal(np.ones(sizes[leaf.index]))] for leaf in tree.leaves}
+    transfer = {node.index: np.ones((1, 1, 1)) for node in tree.inner_nodes}
+    return HTOperator(tree, leaves, transfer, np.ones((1, 1)))
+
+
+def storage_size(tensor: HTensor) -> int:
+    """format.py:459-464: sum n k + sum k_t k1 k2 + k1 k2."""
+    return tensor.storage_size()
+
+
+__all__ = ["HTensor", "HTOperator", "GeneralizedMatrix", "random_htensor", "identity_htoperator",
+           "storage_size", "build_balanced_tree", "DimensionTree"]
