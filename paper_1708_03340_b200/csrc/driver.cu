@@ -177,6 +177,7 @@ void merge_gemms(std::vector<GemmDesc>& v) {
                     e.nb1 == d.nb1 && e.a_m == d.a_m && e.a_k == d.a_k && e.a_o == d.a_o && e.a_b1 == d.a_b1 &&
                     e.b_k == d.b_k && e.b_n == d.b_n && e.b_o == d.b_o && e.b_b1 == d.b_b1 && e.c_m == d.c_m &&
                     e.c_n == d.c_n && e.c_b1 == d.c_b1 && e.alpha == d.alpha && e.beta == d.beta &&
+                    e.a_tri == d.a_tri &&
                     e.A - d.A == c * dA && e.B - d.B == c * dB && e.C - d.C == c * dC;
         if (!same) break;
         ++j;
@@ -232,29 +233,10 @@ void merge_qrs(std::vector<QrProblem>& v) {
 // Plan (and, if arena has a base, bind) the QR workspace of a set of problems.
 int plan_qrs(std::vector<QrProblem>& qs, Arena& ar) {
   merge_qrs(qs);
-  int total_nodes = 0;
-  for (auto& q : qs) total_nodes += q.nodes;
   for (auto& q : qs) {
-    q.P = std::max(1, ceil_div(kSMs, std::max(1, total_nodes)));
-    HT_TRY(qr_plan(q, kSMs));
-    const bool own_v = q.V == nullptr;
-    long long need = (long long)q.nodes * (q.tau_node + 2 * q.st_node) + (own_v ? (long long)q.nodes * q.v_node : 0);
-    double* w = ar.take(need);
-    if (ar.base) {
-      double* vkeep = q.V;
-      double* cur = w;
-      if (own_v) {
-        q.V = cur;
-        cur += (long long)q.nodes * q.v_node;
-      } else {
-        q.V = vkeep;
-      }
-      q.tau = cur;
-      cur += (long long)q.nodes * q.tau_node;
-      q.Rst = cur;
-      cur += (long long)q.nodes * q.st_node;
-      q.W = cur;
-    }
+    HT_TRY(qr_plan(q));
+    double* w = ar.take(qr_workspace_doubles(q));
+    if (ar.base) qr_bind_workspace(q, w);
   }
   return kOk;
 }
@@ -339,8 +321,8 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     if (exec) {
       merge_gemms(g2);
       merge_gemms(g3);
-      HT_TRY(gemm_grouped(g2, s));
-      HT_TRY(gemm_grouped(g3, s));
+      HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
+      HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
       HT_TRY(qr_batched(qs, s));
     }
   }
@@ -431,8 +413,8 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     mx = std::max(mx, scratch_ar.off);
     if (exec) {
       merge_gemms(g1s);
-      HT_TRY(gemm_grouped(g1s, s));
-      HT_TRY(gemm_grouped(g2s, s));
+      HT_TRY(gemm_grouped(g1s, s, "gemm_gram_t1"));
+      HT_TRY(gemm_grouped(g2s, s, "gemm_gram_g"));
       HT_TRY(reduce_partials(rs, s));
     }
   }
@@ -650,9 +632,9 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   merge_gemms(st1);
   merge_gemms(st2);
   merge_gemms(st3);
-  HT_TRY(gemm_grouped(st1, s));
-  HT_TRY(gemm_grouped(st2, s));
-  HT_TRY(gemm_grouped(st3, s));
+  HT_TRY(gemm_grouped(st1, s, "gemm_project"));
+  HT_TRY(gemm_grouped(st2, s, "gemm_project"));
+  HT_TRY(gemm_grouped(st3, s, "gemm_project"));
   return kOk;
 }
 
@@ -1077,8 +1059,8 @@ int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor
 
 int ht_qr_workspace_size(int64_t m, int64_t K, int64_t nodes, size_t* bytes) {
   QrProblem q{};
-  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes; q.P = 0;
-  HT_TRY(qr_plan(q, kSMs));
+  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes;
+  HT_TRY(qr_plan(q));
   *bytes = (size_t)qr_workspace_doubles(q) * sizeof(double) + 1024;
   return kOk;
 }
@@ -1090,8 +1072,8 @@ int ht_qr_batched(int64_t m, int64_t K, int64_t nodes, const double* A, int64_t 
   q.A = A; q.a_r = a_r; q.a_c = a_c; q.a_node = a_node;
   q.Q = Q; q.q_r = q_r; q.q_c = q_c; q.q_node = q_node;
   q.R = R; q.r_ld = r_ld; q.r_node = r_node;
-  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes; q.P = 0;
-  HT_TRY(qr_plan(q, kSMs));
+  q.m = (int)m; q.K = (int)K; q.nodes = (int)nodes;
+  HT_TRY(qr_plan(q));
   const size_t need = (size_t)qr_workspace_doubles(q) * sizeof(double);
   if (ws_bytes < need) {
     set_error("qr workspace too small");

@@ -76,7 +76,15 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_cons
         if (m < g.M && f < k_end) {
           long long o = 0, k = f;
           if (g.KO > 1) { o = f / g.K; k = f - o * g.K; }
-          v = __ldg(A + m * g.a_m + k * g.a_k + o * g.a_o);
+          if (g.a_tri == 0) {
+            v = __ldg(A + m * g.a_m + k * g.a_k + o * g.a_o);
+          } else if (g.a_tri == 3) {
+            v = (m == k) ? 1.0 : 0.0;
+          } else {
+            // implicit unit-diagonal Householder vectors (compact-WY Y factor)
+            const bool stored = g.a_tri == 1 ? (m > k) : (k > m);
+            v = stored ? __ldg(A + m * g.a_m + k * g.a_k + o * g.a_o) : (m == k ? 1.0 : 0.0);
+          }
         }
         ra[q] = v;
       }
@@ -202,7 +210,7 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
 
 }  // namespace
 
-int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream) {
+int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag) {
   size_t i = 0;
   while (i < descs.size()) {
     GemmBatch batch;
@@ -235,12 +243,12 @@ int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream) {
     ProfToken tok = prof_begin(stream);
     gemm_dmma_kernel<<<blocks, THREADS, 0, stream>>>(batch);
     HT_LAUNCH_CHECK();
-    prof_end(tok, "gemm_dmma", stream, flops, bytes);
+    prof_end(tok, tag, stream, flops, bytes);
   }
   return kOk;
 }
 
-int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream) {
+int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, const char* tag) {
   size_t i = 0;
   while (i < descs.size()) {
     ReduceBatch rb;
@@ -262,7 +270,7 @@ int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream) {
     ProfToken tok = prof_begin(stream);
     reduce_partials_kernel<<<blocks, 256, 0, stream>>>(rb);
     HT_LAUNCH_CHECK();
-    prof_end(tok, "reduce_partials", stream, 0.0, bytes);
+    prof_end(tok, tag, stream, 0.0, bytes);
   }
   return kOk;
 }

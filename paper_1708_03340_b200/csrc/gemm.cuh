@@ -27,6 +27,7 @@ struct GemmDesc {
   int splits;
   int tiles_m, tiles_n;
   int block_begin;
+  int a_tri;  // 0 dense; 1 unit-lower in (m,k); 2 unit-upper in (m,k); 3 identity (A not read)
   double alpha, beta;
 };
 
@@ -41,8 +42,8 @@ struct ReduceDesc {
 };
 
 // Launch a set of GEMMs (any number; split into launches of <= kMaxGemmDescs).
-int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream);
-int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream);
+int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag = "gemm_dmma");
+int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, const char* tag = "reduce_partials");
 
 constexpr int kMaxGemmDescs = 48;
 constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;

@@ -1,23 +1,25 @@
-// Batched streaming-TSQR Householder QR, see qr.cuh for the algorithm.
+// Tree-TSQR Householder QR with register-resident blocks and compact-WY Q
+// formation on DMMA GEMMs (see qr.cuh).
 //
-// Reference semantics: kernels.py:24-32 -- Householder QR (dlarfg reflectors as
-// in LAPACK dgeqrf), explicit thin Q (dorgqr), then the sign fix diag(R) >= 0.
-// Wide input (m < K) gives Q m x m and R m x K (kernels.py:27-28).
+// Reference semantics: kernels.py:24-32 -- dlarfg reflectors as in LAPACK
+// dgeqrf, explicit thin Q (dorgqr), sign fix diag(R) >= 0; wide input (m < K)
+// gives Q m x m and R m x K (kernels.py:27-28).
 #include <algorithm>
 
-#include "qr.cuh"
+#include "gemm.cuh"
 #include "prof.cuh"
+#include "qr.cuh"
 
 namespace ht {
 
 namespace {
 
-constexpr int QT = 512;        // threads per CTA
-constexpr int NW = QT / kWarp;  // 16 warps
+constexpr int QT = 512;          // threads per CTA
+constexpr int NW = QT / kWarp;   // 16 warps
+constexpr int RPW = 8;           // rows per warp  -> 128-row blocks
+constexpr int CS = 4;            // column slots per lane -> K <= 128
+constexpr int BR = NW * RPW;     // 128 block rows
 constexpr int MAXD = 32;
-constexpr int MS = 128;        // sub-block rows (4 rows per lane)
-constexpr int NT = MS / kWarp;  // row slots per lane
-constexpr int SMEM_MAX_BYTES = 227 * 1024;
 
 struct QrDev {
   const double* A;
@@ -27,11 +29,10 @@ struct QrDev {
   double* R;
   long long r_ld, r_node;
   double* V;
-  double* tau;
   double* Rst;
-  double* W;
-  long long v_node, tau_node, st_node;
-  int m, K, P, rpc, nsub_pc, nsub_total;
+  double* Tst;
+  long long v_node, st_node, t_node;
+  int m, K, P, rpc;
   int begin, per_node, nodes;
 };
 
@@ -47,550 +48,532 @@ __device__ __forceinline__ int find_desc(const QrBatch& b) {
   return di;
 }
 
-__device__ __forceinline__ int chunk_rows(const QrDev& q, int c) {
-  return c < q.P - 1 ? q.rpc : q.m - (q.P - 1) * q.rpc;
+struct Smem {
+  double* R;    // K x (K+1) heads of the triangular-head mode
+  double* GT;   // K x (K+1): strict upper = G = Y^T Y, strict lower = T^T
+  double* part; // NW x (K+1) per-warp partial dots
+  double* ssp;  // NW partial tail norms
+  double* head; // K: head row of the dense mode
+  double* coef; // K: tau * w_c
+  double* taus; // K
+  double* col;  // 128: broadcast of the active column (tail values, unscaled)
+  int rp;
+};
+
+__device__ __forceinline__ Smem carve(double* sm, int K) {
+  Smem s;
+  s.rp = K + 1;
+  s.R = sm;
+  s.GT = s.R + K * s.rp;
+  s.part = s.GT + K * s.rp;
+  s.ssp = s.part + NW * s.rp;
+  s.head = s.ssp + NW;
+  s.coef = s.head + K;
+  s.taus = s.coef + K;
+  s.col = s.taus + K;
+  return s;
 }
 
-__device__ __forceinline__ int nsub_of(int rows) { return rows <= MS ? 1 : 1 + (rows - MS + MS - 1) / MS; }
-
-__device__ __forceinline__ int round_up32(int v) { return (v + 31) & ~31; }
-
-__device__ __forceinline__ double pick(const double (&r)[NT], int slot) {
-  double v = r[0];
+// The owner lane of column j (lane j&31, slot j>>5) publishes its 8 rows of column j.
+template <int SLOT>
+__device__ __forceinline__ void publish_col(const double (&a)[RPW][CS], double* col, int w) {
 #pragma unroll
-  for (int t = 1; t < NT; ++t)
-    if (slot == t) v = r[t];
-  return v;
+  for (int r = 0; r < RPW; ++r) col[w * RPW + r] = a[r][SLOT];
 }
 
-// Householder factorisation of the column-major shared block As (pitch p).
-//  dense = true : reflector j: head As[j][j], tail rows j+1..nrows-1 (plain dgeqr2)
-//  dense = false: reflector j: head R[j][j] (row-major, pitch rp), tail rows 0..nrows-1
-//                 (QR of [R; As] with R upper triangular: one flat-TSQR step)
-// Writes tau[0..K) (zeros beyond nrefl).  One __syncthreads per reflector: the warp
-// owning column j+1 updates it first and immediately computes reflector j+1.
-__device__ void hh_factor(double* As, int p, int nrows, int K, int nrefl, bool dense, double* R, int rp,
-                          double* taus) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void publish(const double (&a)[RPW][CS], double* col, int w, int js) {
+  switch (js) {
+    case 0: publish_col<0>(a, col, w); break;
+    case 1: publish_col<1>(a, col, w); break;
+    case 2: publish_col<2>(a, col, w); break;
+    default: publish_col<3>(a, col, w); break;
+  }
+}
 
-  auto in_tail = [&](int i, int j) { return i < nrows && (!dense || i > j); };
-  auto head_ptr = [&](int j, int c) -> double* { return dense ? &As[c * p + j] : &R[j * rp + c]; };
+template <int SLOT, bool DENSE>
+__device__ __forceinline__ void store_v(double (&a)[RPW][CS], const double (&u)[RPW], double scal, double beta,
+                                        int w, int j, int nrows) {
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int i = w * RPW + r;
+    if (DENSE && i == j) a[r][SLOT] = beta;
+    else if (i < nrows && (!DENSE || i > j)) a[r][SLOT] = u[r] * scal;
+  }
+}
 
-  auto larfg = [&](int j) {
-    double ss = 0.0;
+// Householder factorisation of the register block a (rows w*8+r, columns lane+32s).
+//  DENSE: reflector j has head a[j][j] and tail rows j+1..nrows-1 (dgeqr2 on the block)
+//  !DENSE: head R[j][j] (shared, upper triangular), tail rows 0..nrows-1 (one TSQR step
+//          on [R; a]).
+// Two CTA barriers per reflector: the partial dots (and tail norm) of reflector j+1 are
+// formed in the same pass that applies reflector j.  Leaves tau in s.taus and the
+// compact-WY T transposed into the strict lower part of GT.
+template <bool DENSE>
+__device__ void factor_core(double (&a)[RPW][CS], int nrows, int K, int nrefl, const Smem& s) {
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int rp = s.rp;
+  for (int j = tid; j < K; j += blockDim.x) s.taus[j] = 0.0;
+  double u[RPW];
+  // phase 1 for reflector j (column j already published in s.col)
+  auto phase1 = [&](int j) {
+    double p[CS], ss = 0.0;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      if (in_tail(i, j)) {
-        const double v = As[j * p + i];
-        ss = fma(v, v, ss);
-      }
-    }
-    ss = warp_sum(ss);
-    const double alpha = *head_ptr(j, j);
-    double tau = 0.0;
-    if (ss > 0.0) {
-      const double beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-      tau = (beta - alpha) / beta;
-      const double scal = 1.0 / (alpha - beta);
+    for (int t = 0; t < CS; ++t) p[t] = 0.0;
 #pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (in_tail(i, j)) As[j * p + i] *= scal;
-      }
-      __syncwarp();
-      if (lane == 0) *head_ptr(j, j) = beta;
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w * RPW + r;
+      const bool tail = i < nrows && (!DENSE || i > j);
+      u[r] = tail ? s.col[i] : 0.0;
+      ss = fma(u[r], u[r], ss);
+#pragma unroll
+      for (int t = 0; t < CS; ++t) p[t] = fma(u[r], a[r][t], p[t]);
     }
-    if (lane == 0) taus[j] = tau;
-    __syncwarp();
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int c = lane + t * kWarp;
+      if (c < K) s.part[w * rp + c] = p[t];
+    }
+    if (lane == 0) s.ssp[w] = ss;  // all lanes of a warp hold the same rows
+    if (DENSE && (j >> 3) == w) {
+      const int rr = j & 7;
+#pragma unroll
+      for (int r = 0; r < RPW; ++r)
+        if (r == rr) {
+#pragma unroll
+          for (int t = 0; t < CS; ++t) {
+            const int c = lane + t * kWarp;
+            if (c < K) s.head[c] = a[r][t];
+          }
+        }
+    }
   };
 
-  for (int j = nrefl + (int)threadIdx.x; j < K; j += blockDim.x) taus[j] = 0.0;
-  if (nrefl > 0 && warp == 0) larfg(0);
-  __syncthreads();
+  if (nrefl > 0) {
+    if (lane == 0) publish(a, s.col, w, 0);
+    __syncwarp();
+    phase1(0);
+  }
   for (int j = 0; j < nrefl; ++j) {
-    const double tj = taus[j];
-    double x[NT];
+    __syncthreads();
+    // ---- phase 2: reflector parameters (dlarfg), coefficients, G column ----
+    double ssum = 0.0;
 #pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      x[t] = in_tail(i, j) ? As[j * p + i] : 0.0;
+    for (int q = 0; q < NW; ++q) ssum += s.ssp[q];
+    const double alpha = DENSE ? s.head[j] : s.R[j * rp + j];
+    double beta = alpha, tau = 0.0, scal = 0.0;
+    if (ssum > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, ssum)), alpha);
+      tau = (beta - alpha) / beta;
+      scal = 1.0 / (alpha - beta);
     }
-    const int c0 = j + 1 + (((warp - (j + 1)) % NW) + NW) % NW;
-    for (int c = c0; c < K; c += NW) {
-      if (tj != 0.0) {
-        double s = 0.0;
+    if (tid < K) {
+      const int c = tid;
+      double dot = 0.0;
 #pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int i = lane + t * kWarp;
-          if (i < nrows) s = fma(x[t], As[c * p + i], s);
-        }
-        double* h = head_ptr(j, c);
-        const double hv = *h;
-        s = warp_sum(s);
-        const double w = tj * (hv + s);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int i = lane + t * kWarp;
-          if (in_tail(i, j)) As[c * p + i] = fma(-w, x[t], As[c * p + i]);
-        }
-        __syncwarp();
-        if (lane == 0) *h = hv - w;
-        __syncwarp();
+      for (int q = 0; q < NW; ++q) dot += s.part[q * rp + c];
+      const double hd = DENSE ? s.head[c] : s.R[j * rp + c];
+      const double wc = fma(scal, dot, hd);
+      if (c > j) {
+        s.coef[c] = tau * wc;
+        if (!DENSE) s.R[j * rp + c] = hd - tau * wc;
+      } else if (c < j) {
+        s.GT[c * rp + j] = wc;  // v_c^T v_j
+      } else {
+        s.taus[j] = tau;
+        if (!DENSE) s.R[j * rp + j] = beta;
       }
-      if (c == j + 1 && c < nrefl) larfg(c);
     }
     __syncthreads();
-  }
-}
-
-// Load rows [row0, row0+nrows) x cols [0, K) of a strided matrix into column-major smem.
-__device__ void load_block(double* As, int p, const double* A, long long a_r, long long a_c, int row0, int nrows,
-                           int K) {
-  const int total = nrows * K;
-  if (a_c == 1) {
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int i = e / K, c = e - i * K;
-      As[c * p + i] = A[(long long)(row0 + i) * a_r + c];
+    // ---- phase 3: apply reflector j (branch-free over rows), store v_j ----
+    double cf[CS];
+#pragma unroll
+    for (int t = 0; t < CS; ++t) {
+      const int c = lane + t * kWarp;
+      cf[t] = (c > j && c < K) ? s.coef[c] : 0.0;
     }
-  } else {
-    for (int e = threadIdx.x; e < total; e += blockDim.x) {
-      const int c = e / nrows, i = e - c * nrows;
-      As[c * p + i] = A[(long long)(row0 + i) * a_r + (long long)c * a_c];
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w * RPW + r;
+      const double vr = u[r] * scal + ((DENSE && i == j) ? 1.0 : 0.0);
+#pragma unroll
+      for (int t = 0; t < CS; ++t) a[r][t] = fma(-cf[t], vr, a[r][t]);
     }
-  }
-}
-
-__global__ void __launch_bounds__(QT, 1) qr_factor_kernel(const __grid_constant__ QrBatch b) {
-  extern __shared__ double sm[];
-  const QrDev& q = b.d[find_desc(b)];
-  const int local = blockIdx.x - q.begin;
-  const int nd = local / q.P, c = local % q.P;
-  const int K = q.K, m = q.m;
-  const int rows = chunk_rows(q, c), r0 = c * q.rpc;
-  const double* A = q.A + nd * q.a_node;
-  double* V = q.V + nd * q.v_node;
-  double* tg = q.tau + nd * q.tau_node + (long long)c * q.nsub_pc * K;
-  double* Rst = q.Rst + nd * q.st_node + (long long)c * K * K;
-  const int rp = K + 1;
-  double* R = sm;
-  double* As = sm + K * rp;
-  double* taus = As + K * (MS + 1);
-
-  // sub-block 0: dense Householder QR (its top K rows become the chunk's R rows)
-  const int n0 = min(rows, MS);
-  const int p0 = round_up32(n0) + 1;
-  const int k0 = min(n0, K);
-  load_block(As, p0, A, q.a_r, q.a_c, r0, n0, K);
-  __syncthreads();
-  hh_factor(As, p0, n0, K, k0, true, R, rp, taus);
-  for (int e = threadIdx.x; e < k0 * n0; e += blockDim.x) {
-    const int col = e / n0, i = e - col * n0;
-    if (i > col) V[(long long)col * m + r0 + i] = As[col * p0 + i];
-  }
-  for (int j = threadIdx.x; j < K; j += blockDim.x) tg[j] = taus[j];
-  if (rows > n0) {
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int j = e / K, cc = e - j * K;
-      R[j * rp + cc] = cc >= j ? As[cc * p0 + j] : 0.0;
+    const int jl = j & 31, js = j >> 5;
+    if (lane == jl) {
+      switch (js) {
+        case 0: store_v<0, DENSE>(a, u, scal, beta, w, j, nrows); break;
+        case 1: store_v<1, DENSE>(a, u, scal, beta, w, j, nrows); break;
+        case 2: store_v<2, DENSE>(a, u, scal, beta, w, j, nrows); break;
+        default: store_v<3, DENSE>(a, u, scal, beta, w, j, nrows); break;
+      }
     }
-  } else {
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int j = e / K, cc = e - j * K;
-      Rst[e] = (j < k0 && cc >= j) ? As[cc * p0 + j] : 0.0;
+    if (j + 1 < nrefl) {
+      if (lane == ((j + 1) & 31)) publish(a, s.col, w, (j + 1) >> 5);
+      __syncwarp();
+      phase1(j + 1);
     }
   }
   __syncthreads();
-
-  // remaining sub-blocks: one flat-TSQR step [R; A_s] each
-  int off = n0, s = 1;
-  while (off < rows) {
-    const int ns = min(MS, rows - off);
-    load_block(As, MS + 1, A, q.a_r, q.a_c, r0 + off, ns, K);
-    __syncthreads();
-    hh_factor(As, MS + 1, ns, K, K, false, R, rp, taus);
-    for (int e = threadIdx.x; e < K * ns; e += blockDim.x) {
-      const int col = e / ns, i = e - col * ns;
-      V[(long long)col * m + r0 + off + i] = As[col * (MS + 1) + i];
-    }
-    for (int j = threadIdx.x; j < K; j += blockDim.x) tg[(long long)s * K + j] = taus[j];
-    __syncthreads();
-    off += ns;
-    ++s;
-  }
-  if (rows > n0) {
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int j = e / K, cc = e - j * K;
-      Rst[e] = R[j * rp + cc];
+  // ---- compact-WY T (dlarft, forward columnwise): T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] G[l][j]
+  // stored transposed: T[i][j] at GT[j][i] (i < j); one barrier per column.
+  {
+    const int i = tid >> 2, seg = tid & 3;
+    for (int j = 1; j < nrefl; ++j) {
+      double acc = 0.0;
+      if (i < j) {
+        const int len = j - i, ch = (len + 3) >> 2;
+        const int l0 = i + seg * ch, l1 = min(j, l0 + ch);
+        for (int l = l0; l < l1; ++l) {
+          const double til = (l == i) ? s.taus[i] : s.GT[l * rp + i];
+          acc = fma(til, s.GT[l * rp + j], acc);
+        }
+      }
+      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+      if (i < j && seg == 0) s.GT[j * rp + i] = -s.taus[j] * acc;
+      __syncthreads();
     }
   }
 }
 
-__device__ __forceinline__ int pairs_in_round(int P, int r) {
-  const int h = 1 << r;
-  return P > h ? (P - h - 1) / (2 * h) + 1 : 0;
+__device__ void store_T(double* T, const Smem& s, int K, int nrefl) {
+  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+    const int i = e / K, j = e - i * K;
+    double v = 0.0;
+    if (j < nrefl) {
+      if (i < j) v = s.GT[j * s.rp + i];
+      else if (i == j) v = s.taus[i];
+    }
+    T[e] = v;
+  }
 }
 
-// Binary-tree combine of chunk R factors: QR of [R_a; R_b] (round r).
-__global__ void __launch_bounds__(QT, 1) qr_combine_kernel(const __grid_constant__ QrBatch b) {
+// mode 0: dense QR of one row block; mode 1: combine step [R_a; R_b] of round `round`.
+__global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ QrBatch b) {
   extern __shared__ double sm[];
   const QrDev& q = b.d[find_desc(b)];
-  const int r = b.round;
   const int local = blockIdx.x - q.begin;
   const int nd = local / q.per_node, k = local % q.per_node;
-  const int a = k << (r + 1), bb = a + (1 << r);
   const int K = q.K;
-  const int rp = K + 1, pb = round_up32(K) + 1;
-  double* R = sm;
-  double* As = sm + K * rp;
-  double* taus = As + K * (MS + 1);
-  double* Ra = q.Rst + nd * q.st_node + (long long)a * K * K;
-  double* Rb = q.Rst + nd * q.st_node + (long long)bb * K * K;
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, cc = e - i * K;
-    R[i * rp + cc] = Ra[e];
-    As[cc * pb + i] = Rb[e];
+  const Smem s = carve(sm, K);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  double a[RPW][CS];
+  double* Rst = q.Rst + nd * q.st_node;
+  double* Tst = q.Tst + nd * q.t_node;
+
+  if (b.round < 0) {
+    // ---- dense block c = k ----
+    const int c = k;
+    const int row0 = c * q.rpc;
+    const int rows = min(q.rpc, q.m - row0);
+    const double* A = q.A + nd * q.a_node;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w * RPW + r;
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int col = lane + t * kWarp;
+        a[r][t] = (i < rows && col < K) ? __ldg(A + (long long)(row0 + i) * q.a_r + (long long)col * q.a_c) : 0.0;
+      }
+    }
+    const int nrefl = min(rows, K);
+    factor_core<true>(a, rows, K, nrefl, s);
+    double* V = q.V + nd * q.v_node;
+    double* Rc = Rst + (long long)c * K * K;
+#pragma unroll
+    for (int r = 0; r < RPW; ++r) {
+      const int i = w * RPW + r;
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int col = lane + t * kWarp;
+        if (col < K) {
+          if (i < rows) V[(long long)col * q.m + row0 + i] = a[r][t];
+          if (i < K) Rc[(long long)i * K + col] = (i < nrefl && col >= i) ? a[r][t] : 0.0;
+        }
+      }
+    }
+    store_T(Tst + (long long)c * K * K, s, K, nrefl);
+  } else {
+    // ---- combine pair (a, b) ----
+    const int r = b.round;
+    const int ia = k << (r + 1), ib = ia + (1 << r);
+    double* Ra = Rst + (long long)ia * K * K;
+    double* Rb = Rst + (long long)ib * K * K;
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+      const int i = e / K, c = e - i * K;
+      s.R[i * s.rp + c] = Ra[e];
+    }
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      const int i = w * RPW + rr;
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int col = lane + t * kWarp;
+        a[rr][t] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
+      }
+    }
+    factor_core<false>(a, K, K, K, s);
+    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
+      const int i = e / K, c = e - i * K;
+      Ra[e] = s.R[i * s.rp + c];
+    }
+    // reflector tails of the R_b rows, column-major K x K, into R_b's slot
+#pragma unroll
+    for (int rr = 0; rr < RPW; ++rr) {
+      const int i = w * RPW + rr;
+#pragma unroll
+      for (int t = 0; t < CS; ++t) {
+        const int col = lane + t * kWarp;
+        if (i < K && col < K) Rb[(long long)col * K + i] = a[rr][t];
+      }
+    }
+    store_T(Tst + (long long)(q.P + ib) * K * K, s, K, K);
   }
-  __syncthreads();
-  hh_factor(As, pb, K, K, K, false, R, rp, taus);
-  double* ctau = q.tau + nd * q.tau_node + (long long)q.nsub_total * K + (long long)bb * K;
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, cc = e - i * K;
-    Ra[e] = R[i * rp + cc];
-    Rb[cc * K + i] = As[cc * pb + i];  // reflector tails, column-major
-  }
-  for (int j = threadIdx.x; j < K; j += blockDim.x) ctau[j] = taus[j];
 }
 
-// Sign fix (kernels.py:31-32) and the seed diag(s) of the backward accumulation.
+// sign fix (kernels.py:31-32): R out, and the seed diag(s) in Q's top rows
 __global__ void qr_finalize_kernel(const __grid_constant__ QrBatch b) {
   const QrDev& q = b.d[find_desc(b)];
   const int nd = blockIdx.x - q.begin;
   const int K = q.K, kq = min(q.m, K);
   const double* Rf = q.Rst + nd * q.st_node;
   double* Ro = q.R + nd * q.r_node;
-  double* W0 = q.W + nd * q.st_node;
+  double* Q = q.Q + nd * q.q_node;
   for (int e = threadIdx.x; e < kq * K; e += blockDim.x) {
     const int j = e / K, c = e - j * K;
-    const double s = Rf[j * K + j] < 0.0 ? -1.0 : 1.0;
-    Ro[(long long)j * q.r_ld + c] = s * Rf[j * K + c];
+    const double sg = Rf[j * K + j] < 0.0 ? -1.0 : 1.0;
+    Ro[(long long)j * q.r_ld + c] = sg * Rf[j * K + c];
   }
-  for (int e = threadIdx.x; e < kq * K; e += blockDim.x) {
-    const int c = e / K, i = e - c * K;
-    W0[(long long)c * K + i] = (i == c) ? (Rf[c * K + c] < 0.0 ? -1.0 : 1.0) : 0.0;
-  }
-}
-
-// Backward accumulation through one combine round: [W_a; 0] -> [W_a'; W_b].
-__global__ void __launch_bounds__(QT, 1) qr_expand_round_kernel(const __grid_constant__ QrBatch b) {
-  extern __shared__ double sm[];
-  const QrDev& q = b.d[find_desc(b)];
-  const int r = b.round;
-  const int local = blockIdx.x - q.begin;
-  const int nd = local / q.per_node, k = local % q.per_node;
-  const int a = k << (r + 1), bb = a + (1 << r);
-  const int K = q.K, kq = min(q.m, K);
-  const int pb = round_up32(K) + 1;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  double* Vs = sm;
-  double* taus = sm + K * pb;
-  const double* Vb = q.Rst + nd * q.st_node + (long long)bb * K * K;
-  const double* ct = q.tau + nd * q.tau_node + (long long)q.nsub_total * K + (long long)bb * K;
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int c = e / K, i = e - c * K;
-    Vs[c * pb + i] = Vb[e];
-  }
-  for (int j = threadIdx.x; j < K; j += blockDim.x) taus[j] = ct[j];
-  __syncthreads();
-  double* Wa = q.W + nd * q.st_node + (long long)a * K * K;
-  double* Wb = q.W + nd * q.st_node + (long long)bb * K * K;
-  for (int c = warp; c < kq; c += NW) {
-    double wa[NT], wb[NT];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      wa[t] = i < K ? Wa[(long long)c * K + i] : 0.0;
-      wb[t] = 0.0;
-    }
-    for (int j = K - 1; j >= 0; --j) {
-      const double tj = taus[j];
-      if (tj == 0.0) continue;
-      double s = 0.0;
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (i < K) s = fma(Vs[j * pb + i], wb[t], s);
-      }
-      const double hv = __shfl_sync(0xffffffffu, pick(wa, j >> 5), j & 31);
-      s = warp_sum(s);
-      const double w = tj * (hv + s);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (t == (j >> 5) && lane == (j & 31)) wa[t] -= w;
-        if (i < K) wb[t] = fma(-w, Vs[j * pb + i], wb[t]);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      if (i < K) {
-        Wa[(long long)c * K + i] = wa[t];
-        Wb[(long long)c * K + i] = wb[t];
-      }
-    }
+  for (int e = threadIdx.x; e < kq * kq; e += blockDim.x) {
+    const int i = e / kq, c = e - i * kq;
+    Q[(long long)i * q.q_r + (long long)c * q.q_c] = (i == c) ? (Rf[c * K + c] < 0.0 ? -1.0 : 1.0) : 0.0;
   }
 }
 
-// Every chunk applies its reflectors in reverse to its seed: rows of the thin Q.
-__global__ void __launch_bounds__(QT, 1) qr_expand_chunk_kernel(const __grid_constant__ QrBatch b) {
-  extern __shared__ double sm[];
-  const QrDev& q = b.d[find_desc(b)];
-  const int local = blockIdx.x - q.begin;
-  const int nd = local / q.P, c = local % q.P;
-  const int K = q.K, m = q.m, kq = min(m, K);
-  const int rows = chunk_rows(q, c), r0 = c * q.rpc;
-  const int n0 = min(rows, MS), p0 = round_up32(n0) + 1, k0 = min(n0, K);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const double* V = q.V + nd * q.v_node;
-  const double* tg = q.tau + nd * q.tau_node + (long long)c * q.nsub_pc * K;
-  double* Wc = q.W + nd * q.st_node + (long long)c * K * K;
-  double* Q = q.Q + nd * q.q_node;
-  double* Vs = sm;
-  double* taus = sm + K * (MS + 1);
-
-  const int nsub = nsub_of(rows);
-  for (int s = nsub - 1; s >= 1; --s) {
-    const int off = n0 + (s - 1) * MS;
-    const int ns = min(MS, rows - off);
-    for (int e = threadIdx.x; e < K * ns; e += blockDim.x) {
-      const int col = e / ns, i = e - col * ns;
-      Vs[col * (MS + 1) + i] = V[(long long)col * m + r0 + off + i];
-    }
-    for (int j = threadIdx.x; j < K; j += blockDim.x) taus[j] = tg[(long long)s * K + j];
-    __syncthreads();
-    for (int cc = warp; cc < kq; cc += NW) {
-      double wr[NT], qv[NT];
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        wr[t] = i < K ? Wc[(long long)cc * K + i] : 0.0;
-        qv[t] = 0.0;
-      }
-      for (int j = K - 1; j >= 0; --j) {
-        const double tj = taus[j];
-        if (tj == 0.0) continue;
-        double sdot = 0.0;
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int i = lane + t * kWarp;
-          if (i < ns) sdot = fma(Vs[j * (MS + 1) + i], qv[t], sdot);
-        }
-        const double hv = __shfl_sync(0xffffffffu, pick(wr, j >> 5), j & 31);
-        sdot = warp_sum(sdot);
-        const double w = tj * (hv + sdot);
-#pragma unroll
-        for (int t = 0; t < NT; ++t) {
-          const int i = lane + t * kWarp;
-          if (t == (j >> 5) && lane == (j & 31)) wr[t] -= w;
-          if (i < ns) qv[t] = fma(-w, Vs[j * (MS + 1) + i], qv[t]);
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (i < ns) Q[(long long)(r0 + off + i) * q.q_r + (long long)cc * q.q_c] = qv[t];
-        if (i < K) Wc[(long long)cc * K + i] = wr[t];
-      }
-    }
-    __syncthreads();
-  }
-
-  // sub-block 0: dense reflectors applied in reverse to [W; 0]
-  for (int e = threadIdx.x; e < k0 * n0; e += blockDim.x) {
-    const int col = e / n0, i = e - col * n0;
-    Vs[col * p0 + i] = V[(long long)col * m + r0 + i];
-  }
-  for (int j = threadIdx.x; j < K; j += blockDim.x) taus[j] = tg[j];
-  __syncthreads();
-  for (int cc = warp; cc < kq; cc += NW) {
-    double qv[NT];
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      qv[t] = (i < k0) ? Wc[(long long)cc * K + i] : 0.0;
-    }
-    for (int j = k0 - 1; j >= 0; --j) {
-      const double tj = taus[j];
-      if (tj == 0.0) continue;
-      double sdot = 0.0;
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (i < n0 && i > j) sdot = fma(Vs[j * p0 + i], qv[t], sdot);
-      }
-      const double hv = __shfl_sync(0xffffffffu, pick(qv, j >> 5), j & 31);
-      sdot = warp_sum(sdot);
-      const double w = tj * (hv + sdot);
-#pragma unroll
-      for (int t = 0; t < NT; ++t) {
-        const int i = lane + t * kWarp;
-        if (t == (j >> 5) && lane == (j & 31)) qv[t] -= w;
-        if (i < n0 && i > j) qv[t] = fma(-w, Vs[j * p0 + i], qv[t]);
-      }
-    }
-#pragma unroll
-    for (int t = 0; t < NT; ++t) {
-      const int i = lane + t * kWarp;
-      if (i < n0) Q[(long long)(r0 + i) * q.q_r + (long long)cc * q.q_c] = qv[t];
-    }
-  }
+size_t smem_bytes(int K) {
+  const int rp = K + 1;
+  return (size_t)(2 * K * rp + NW * rp + NW + 3 * K + BR) * sizeof(double);
 }
-
-int nsub_host(int rows) { return rows <= MS ? 1 : 1 + (rows - MS + MS - 1) / MS; }
 
 int pairs_host(int P, int r) {
   const int h = 1 << r;
   return P > h ? (P - h - 1) / (2 * h) + 1 : 0;
 }
 
-size_t smem_bytes(int K) { return (size_t)(K * (K + 1) + K * (MS + 1) + K) * sizeof(double); }
-
 bool g_attr_done = false;
-
-int ensure_attrs() {
-  if (g_attr_done) return kOk;
-  HT_CUDA_CHECK(cudaFuncSetAttribute(qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX_BYTES));
-  HT_CUDA_CHECK(cudaFuncSetAttribute(qr_combine_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX_BYTES));
-  HT_CUDA_CHECK(
-      cudaFuncSetAttribute(qr_expand_round_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX_BYTES));
-  HT_CUDA_CHECK(
-      cudaFuncSetAttribute(qr_expand_chunk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX_BYTES));
-  g_attr_done = true;
-  return kOk;
-}
 
 QrDev to_dev(const QrProblem& p) {
   QrDev d{};
   d.A = p.A; d.a_r = p.a_r; d.a_c = p.a_c; d.a_node = p.a_node;
   d.Q = p.Q; d.q_r = p.q_r; d.q_c = p.q_c; d.q_node = p.q_node;
   d.R = p.R; d.r_ld = p.r_ld; d.r_node = p.r_node;
-  d.V = p.V; d.tau = p.tau; d.Rst = p.Rst; d.W = p.W;
-  d.v_node = p.v_node; d.tau_node = p.tau_node; d.st_node = p.st_node;
-  d.m = p.m; d.K = p.K; d.P = p.P; d.rpc = p.rpc; d.nsub_pc = p.nsub_pc; d.nsub_total = p.nsub_total;
+  d.V = p.V; d.Rst = p.Rst; d.Tst = p.Tst;
+  d.v_node = p.v_node; d.st_node = p.st_node; d.t_node = p.t_node;
+  d.m = p.m; d.K = p.K; d.P = p.P; d.rpc = p.rpc;
   d.nodes = p.nodes;
   return d;
 }
 
-enum Phase { kFactor, kCombine, kFinalize, kExpandRound, kExpandChunk };
-
-// LAPACK-equivalent algorithmic flops: dgeqrf (factor) / dorgqr (Q formation)
 double qr_flops(int m, int K) {
   const double a = std::max(m, K), b = std::min(m, K);
   return 2.0 * a * b * b - 2.0 / 3.0 * b * b * b;
 }
 
-const char* phase_name(int ph) {
-  static const char* names[] = {"qr_factor", "qr_combine", "qr_finalize", "qr_expand_round", "qr_expand_chunk"};
-  return names[ph];
-}
-
-template <typename KernelT>
-int launch_phase(KernelT kernel, std::vector<QrProblem>& probs, Phase ph, int round, cudaStream_t stream) {
+// round < 0: dense blocks; round >= 0: combine round; round == -2: finalize
+int launch(std::vector<QrProblem>& probs, int round, cudaStream_t stream) {
   size_t i = 0;
   while (i < probs.size()) {
     QrBatch b;
     b.count = 0;
-    b.round = round;
+    b.round = round == -2 ? 0 : round;
     int blocks = 0;
     size_t smem = 0;
+    double flops = 0;
     while (i < probs.size() && b.count < MAXD) {
       const QrProblem& p = probs[i++];
-      int per = 0;
-      switch (ph) {
-        case kFactor:
-        case kExpandChunk: per = p.P; break;
-        case kCombine:
-        case kExpandRound: per = pairs_host(p.P, round); break;
-        case kFinalize: per = 1; break;
-      }
+      int per;
+      if (round == -2) per = 1;
+      else if (round < 0) per = p.P;
+      else per = pairs_host(p.P, round);
       if (per == 0 || p.nodes == 0) continue;
       QrDev d = to_dev(p);
       d.begin = blocks;
       d.per_node = per;
       blocks += per * p.nodes;
       smem = std::max(smem, smem_bytes(p.K));
+      if (round == -1) flops += (double)p.nodes * qr_flops(p.m, p.K);
       b.d[b.count++] = d;
     }
-    if (b.count == 0) continue;
-    if (ph == kFinalize) smem = 0;
-    double flops = 0, bytes = 0;
-    for (int q = 0; q < b.count; ++q) {
-      const QrDev& d = b.d[q];
-      if (ph == kFactor || ph == kExpandChunk) {
-        flops += (double)d.nodes * qr_flops(d.m, d.K);
-        bytes += 16.0 * d.nodes * (double)d.m * d.K;
-      }
-    }
+    if (!b.count) continue;
     ProfToken tok = prof_begin(stream);
-    kernel<<<blocks, ph == kFinalize ? 256 : QT, smem, stream>>>(b);
-    HT_LAUNCH_CHECK();
-    prof_end(tok, phase_name(ph), stream, flops, bytes);
+    if (round == -2) {
+      qr_finalize_kernel<<<blocks, 256, 0, stream>>>(b);
+      HT_LAUNCH_CHECK();
+      prof_end(tok, "qr_finalize", stream, 0.0, 0.0);
+    } else {
+      qr_step_kernel<<<blocks, QT, smem, stream>>>(b);
+      HT_LAUNCH_CHECK();
+      prof_end(tok, round < 0 ? "qr_block_factor" : "qr_tree_combine", stream, flops, 0.0);
+    }
   }
   return kOk;
 }
 
 }  // namespace
 
-int qr_plan(QrProblem& p, int target_ctas) {
+int qr_plan(QrProblem& p) {
   if (p.K < 1 || p.m < 1) {
     set_error("qr_plan: empty matrix");
     return kErrShape;
   }
   if (p.K > kQrMaxK) {
-    set_error("qr_plan: K=" + std::to_string(p.K) + " exceeds the shared-memory QR path (K <= 112)");
+    set_error("qr_plan: K=" + std::to_string(p.K) + " exceeds the register-resident QR path (K <= 112)");
     return kErrUnsupported;
   }
-  int pmax = std::max(1, p.m / std::max(p.K, MS));
-  int want = p.P > 0 ? p.P : std::max(1, ceil_div(target_ctas, std::max(1, p.nodes)));
-  p.P = std::min(want, pmax);
-  p.rpc = p.m / p.P;
-  p.ms0 = MS;
-  p.ms = MS;
-  p.nsub_pc = nsub_host(p.rpc);
-  p.nsub_total = (p.P - 1) * p.nsub_pc + nsub_host(p.m - (p.P - 1) * p.rpc);
+  int P = ceil_div(p.m, BR);
+  int rpc = std::max(ceil_div(p.m, P), std::min(p.K, BR));
+  P = ceil_div(p.m, rpc);
+  p.P = P;
+  p.rpc = rpc;
   p.v_node = (long long)p.m * p.K;
-  p.tau_node = (long long)(p.nsub_total + p.P) * p.K;
-  p.st_node = (long long)p.P * p.K * p.K;
+  p.st_node = (long long)P * p.K * p.K;
+  p.t_node = 2LL * P * p.K * p.K;
+  p.x_node = 3LL * P * p.K * p.K;
+  p.own_v = (p.V == nullptr);
   return kOk;
 }
 
 long long qr_workspace_doubles(const QrProblem& p) {
-  return (long long)p.nodes * (p.v_node + p.tau_node + 2 * p.st_node);
+  return (long long)p.nodes * ((p.own_v ? p.v_node : 0) + p.st_node + p.t_node + p.x_node) + 1024;
 }
 
 void qr_bind_workspace(QrProblem& p, double* ws) {
-  p.V = ws;
-  ws += (long long)p.nodes * p.v_node;
-  p.tau = ws;
-  ws += (long long)p.nodes * p.tau_node;
+  if (p.own_v) {
+    p.V = ws;
+    ws += (long long)p.nodes * p.v_node;
+  }
   p.Rst = ws;
   ws += (long long)p.nodes * p.st_node;
-  p.W = ws;
+  p.Tst = ws;
+  ws += (long long)p.nodes * p.t_node;
+  p.X = ws;
 }
 
 int qr_batched(std::vector<QrProblem>& probs, cudaStream_t stream) {
   if (probs.empty()) return kOk;
-  HT_TRY(ensure_attrs());
+  if (!g_attr_done) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    g_attr_done = true;
+  }
   int maxP = 1;
   for (auto& p : probs) maxP = std::max(maxP, p.P);
   int rounds = 0;
   while ((1 << rounds) < maxP) ++rounds;
-  HT_TRY(launch_phase(qr_factor_kernel, probs, kFactor, 0, stream));
-  for (int r = 0; r < rounds; ++r) HT_TRY(launch_phase(qr_combine_kernel, probs, kCombine, r, stream));
-  HT_TRY(launch_phase(qr_finalize_kernel, probs, kFinalize, 0, stream));
-  for (int r = rounds - 1; r >= 0; --r) HT_TRY(launch_phase(qr_expand_round_kernel, probs, kExpandRound, r, stream));
-  HT_TRY(launch_phase(qr_expand_chunk_kernel, probs, kExpandChunk, 0, stream));
+
+  // ---- factorisation ----
+  HT_TRY(launch(probs, -1, stream));
+  for (int r = 0; r < rounds; ++r) HT_TRY(launch(probs, r, stream));
+  HT_TRY(launch(probs, -2, stream));
+
+  // ---- Q formation on DMMA GEMMs (compact WY) ----
+  // Q(row, col) for row = chunk start + i; W blocks live in Q's top rows of each chunk.
+  auto qptr = [](const QrProblem& p, long long row) { return p.Q + row * p.q_r; };
+  for (int r = rounds - 1; r >= 0; --r) {
+    std::vector<GemmDesc> g1, g2;
+    for (auto& p : probs) {
+      const int np = pairs_host(p.P, r);
+      if (np == 0) continue;
+      const int K = p.K, kq = std::min(p.m, K);
+      const long long KK = (long long)K * K;
+      const long long pair_rows = (long long)p.rpc << (r + 1);
+      const long long hb = 1LL << r;
+      // last chunk may be short: split off the pair whose b is the last chunk
+      const int last_b = (int)((long long)(np - 1) * (2 * hb) + hb);
+      const int rows_lastb = std::min(p.rpc, p.m - last_b * p.rpc);
+      const bool short_last = rows_lastb < K;
+      auto add_pairs = [&](int k0, int cnt, int krb) {
+        if (cnt <= 0) return;
+        const long long ia0 = (long long)k0 * 2 * hb, ib0 = ia0 + hb;
+        double* X = p.X + ia0 * KK;
+        // X = T_ab W_a  (K x kq)
+        GemmDesc x = gemm_desc(p.Tst + (p.P + ib0) * KK, K, 1, qptr(p, ia0 * p.rpc), p.q_r, p.q_c, X, kq, 1, K,
+                               kq, K);
+        x.nb1 = cnt; x.a_b1 = 2 * hb * KK; x.b_b1 = pair_rows * p.q_r; x.c_b1 = 2 * hb * KK;
+        x.nb2 = p.nodes; x.a_b2 = p.t_node; x.b_b2 = p.q_node; x.c_b2 = p.x_node;
+        g1.push_back(x);
+        // W_b = -V_b X   (krb x kq); V_b column-major K x K in R_b's slot
+        GemmDesc wb = gemm_desc(p.Rst + ib0 * KK, 1, K, X, kq, 1, qptr(p, ib0 * p.rpc), p.q_r, p.q_c, krb, kq, K,
+                                -1.0, 0.0);
+        wb.nb1 = cnt; wb.a_b1 = 2 * hb * KK; wb.b_b1 = 2 * hb * KK; wb.c_b1 = pair_rows * p.q_r;
+        wb.nb2 = p.nodes; wb.a_b2 = p.st_node; wb.b_b2 = p.x_node; wb.c_b2 = p.q_node;
+        g2.push_back(wb);
+        // W_a -= X
+        GemmDesc wa = gemm_desc(nullptr, 0, 0, X, kq, 1, qptr(p, ia0 * p.rpc), p.q_r, p.q_c, K, kq, K, -1.0, 1.0);
+        wa.a_tri = 3;
+        wa.nb1 = cnt; wa.b_b1 = 2 * hb * KK; wa.c_b1 = pair_rows * p.q_r;
+        wa.nb2 = p.nodes; wa.b_b2 = p.x_node; wa.c_b2 = p.q_node;
+        g2.push_back(wa);
+      };
+      if (short_last) {
+        add_pairs(0, np - 1, K);
+        add_pairs(np - 1, 1, rows_lastb);
+      } else {
+        add_pairs(0, np, K);
+      }
+    }
+    HT_TRY(gemm_grouped(g1, stream, "gemm_qr_tree"));
+    HT_TRY(gemm_grouped(g2, stream, "gemm_qr_tree"));
+  }
+  {
+    // blocks: X1 = Y_top^T W, X2 = T X1, Q = [W; 0] - Y X2
+    std::vector<GemmDesc> g1, g2, g3;
+    for (auto& p : probs) {
+      const int K = p.K, kq = std::min(p.m, K);
+      const long long KK = (long long)K * K;
+      const int last_rows = p.m - (p.P - 1) * p.rpc;
+      auto add_blocks = [&](int c0, int cnt, int rows) {
+        if (cnt <= 0) return;
+        const int kr = std::min(rows, K);
+        double* X1 = p.X + (long long)p.P * KK + (long long)c0 * KK;
+        double* X2 = p.X + 2LL * p.P * KK + (long long)c0 * KK;
+        const long long row0 = (long long)c0 * p.rpc;
+        // X1 (K x kq) = Y[0:kr, :]^T W (kr x kq): A(m,k) = Y(k,m), unit-upper in (m,k)
+        GemmDesc a = gemm_desc(p.V + row0, p.m, 1, qptr(p, row0), p.q_r, p.q_c, X1, kq, 1, K, kq, kr);
+        a.a_tri = 2;
+        a.nb1 = cnt; a.a_b1 = p.rpc; a.b_b1 = (long long)p.rpc * p.q_r; a.c_b1 = KK;
+        a.nb2 = p.nodes; a.a_b2 = p.v_node; a.b_b2 = p.q_node; a.c_b2 = p.x_node;
+        g1.push_back(a);
+        // X2 = T X1
+        GemmDesc t = gemm_desc(p.Tst + (long long)c0 * KK, K, 1, X1, kq, 1, X2, kq, 1, K, kq, K);
+        t.nb1 = cnt; t.a_b1 = KK; t.b_b1 = KK; t.c_b1 = KK;
+        t.nb2 = p.nodes; t.a_b2 = p.t_node; t.b_b2 = p.x_node; t.c_b2 = p.x_node;
+        g2.push_back(t);
+        // Q rows [0, kr) = W - Y[0:kr] X2  (unit-lower in (m,k))
+        GemmDesc top = gemm_desc(p.V + row0, 1, p.m, X2, kq, 1, qptr(p, row0), p.q_r, p.q_c, kr, kq, K, -1.0, 1.0);
+        top.a_tri = 1;
+        top.nb1 = cnt; top.a_b1 = p.rpc; top.b_b1 = KK; top.c_b1 = (long long)p.rpc * p.q_r;
+        top.nb2 = p.nodes; top.a_b2 = p.v_node; top.b_b2 = p.x_node; top.c_b2 = p.q_node;
+        g3.push_back(top);
+        if (rows > kr) {
+          // Q rows [kr, rows) = -Y[kr:rows] X2  (dense part of Y)
+          GemmDesc bot = gemm_desc(p.V + row0 + kr, 1, p.m, X2, kq, 1, qptr(p, row0 + kr), p.q_r, p.q_c, rows - kr,
+                                   kq, K, -1.0, 0.0);
+          bot.nb1 = cnt; bot.a_b1 = p.rpc; bot.b_b1 = KK; bot.c_b1 = (long long)p.rpc * p.q_r;
+          bot.nb2 = p.nodes; bot.a_b2 = p.v_node; bot.b_b2 = p.x_node; bot.c_b2 = p.q_node;
+          g3.push_back(bot);
+        }
+      };
+      if (last_rows == p.rpc) {
+        add_blocks(0, p.P, p.rpc);
+      } else {
+        add_blocks(0, p.P - 1, p.rpc);
+        add_blocks(p.P - 1, 1, last_rows);
+      }
+    }
+    HT_TRY(gemm_grouped(g1, stream, "gemm_qr_block"));
+    HT_TRY(gemm_grouped(g2, stream, "gemm_qr_block"));
+    HT_TRY(gemm_grouped(g3, stream, "gemm_qr_block"));
+  }
   return kOk;
 }
 

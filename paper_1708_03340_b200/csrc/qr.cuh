@@ -1,18 +1,21 @@
 // Batched tall-skinny Householder QR (sign-fixed, explicit thin Q) for the
-// leaf frames and the M_{2,3} matricised transfer tensors -- the replacement
-// for reference kernels.py:24-32 (numpy dgeqrf+dorgqr, R diagonal >= 0).
+// leaf frames and the M_{2,3}-matricised transfer tensors -- the replacement
+// for reference kernels.py:24-32 (numpy dgeqrf + dorgqr, then diag(R) >= 0).
 //
-// Algorithm (communication-avoiding, all Householder, no Gram/Cholesky step so
-// rank-deficient frames such as add(A, A) stay exactly orthonormal):
-//   1. every node is cut into P row chunks (>= K rows each); one CTA per chunk
-//      factors its first sub-block densely and then streams the remaining
-//      sub-blocks through a "triangular head" Householder step against its
-//      running R (flat TSQR inside the CTA);
-//   2. the P chunk R factors are combined by a binary tree of [R_a; R_b]
-//      Householder steps (one launch per round, all nodes of a level at once);
-//   3. R is sign-fixed (R_jj >= 0) and the sign matrix seeds the backward
-//      accumulation of Q: tree rounds top-down, then every chunk applies its
-//      reflectors in reverse to produce its rows of Q.
+// Algorithm: tree TSQR, Householder everywhere (no Gram / Cholesky step, so
+// exactly rank-deficient frames such as add(A, A) keep an orthonormal Q).
+//   1. Each node is cut into P row blocks of <= 128 rows (all but the last
+//      have >= K rows).  One CTA per block runs dense Householder QR with the
+//      block held in registers (16 warps x 8 rows, lanes x 4 columns), two
+//      CTA barriers per reflector (the dots of reflector j+1 are fused into
+//      the update of reflector j), and builds the compact-WY factor T
+//      (H_0..H_{K-1} = I - Y T Y^T) in shared memory.
+//   2. Block R factors are merged by a binary tree of [R_a; R_b] steps
+//      (reflector heads in R_a rows, tails in R_b), one launch per round for
+//      all nodes of a tree level.
+//   3. R is sign-fixed; diag(sign) seeds Q.  Q is then formed top-down with
+//      batched DMMA GEMMs only: per tree pair X = T W_a, W_b = -V_b X,
+//      W_a -= X; per block Q = [W; 0] - Y T (Y_top^T W).
 #pragma once
 
 #include <vector>
@@ -22,36 +25,35 @@
 namespace ht {
 
 struct QrProblem {
-  // A(row, col) of node `nd`: A + nd*a_node + row*a_r + col*a_c   (m x K), read only
+  // A(row, col) of node nd: A + nd*a_node + row*a_r + col*a_c  (m x K), read only
   const double* A;
   long long a_r, a_c, a_node;
   // Q(row, col) output (m x kq, kq = min(m, K))
   double* Q;
   long long q_r, q_c, q_node;
-  // R output, row-major kq x K with leading dimension r_ld
+  // R output, row-major kq x K (leading dimension r_ld)
   double* R;
   long long r_ld, r_node;
   int m, K, nodes;
-  int P;  // requested row chunks per node (clamped by the planner)
+  // optional: reflector storage (column-major, ld m, node stride m*K).  May alias
+  // A when A is itself column-major scratch (a_r == 1, a_c == m): the kernel reads
+  // a block into registers before writing its reflectors back.
+  double* V;
 
   // --- filled by qr_plan() ---
-  int rpc, ms0, ms, nsub_pc, nsub_total;
-  long long v_node, tau_node, st_node;  // workspace strides per node (doubles)
-  // --- filled by qr_bind_workspace() ---
-  double* V;    // reflector tails, column-major ld = m
-  double* tau;  // [nsub_total*K sub-block taus][P*K combine taus]
-  double* Rst;  // P blocks K*K (chunk R factors, then combine tails)
-  double* W;    // P blocks K*K (backward-accumulation seeds)
+  int P, rpc;
+  long long v_node, st_node, t_node, x_node;
+  double* Rst;  // P x K x K: block R factors, then combine reflector tails
+  double* Tst;  // 2P x K x K: T factors of blocks [0,P) and of combine steps [P + b]
+  double* X;    // 3P x K x K: GEMM scratch of the Q formation
+  bool own_v;
 };
 
-constexpr int kQrMaxK = 112;  // shared-memory resident path
+constexpr int kQrMaxK = 112;  // register/shared-memory resident path
 
-// Choose chunking / sub-block sizes and the per-node workspace footprint.
-int qr_plan(QrProblem& p, int target_ctas);
+int qr_plan(QrProblem& p);
 long long qr_workspace_doubles(const QrProblem& p);
 void qr_bind_workspace(QrProblem& p, double* ws);
-
-// Run all problems (each a group of same-shaped nodes) on `stream`.
 int qr_batched(std::vector<QrProblem>& probs, cudaStream_t stream);
 
 }  // namespace ht
