@@ -177,7 +177,7 @@ void merge_gemms(std::vector<GemmDesc>& v) {
                     e.nb1 == d.nb1 && e.a_m == d.a_m && e.a_k == d.a_k && e.a_o == d.a_o && e.a_b1 == d.a_b1 &&
                     e.b_k == d.b_k && e.b_n == d.b_n && e.b_o == d.b_o && e.b_b1 == d.b_b1 && e.c_m == d.c_m &&
                     e.c_n == d.c_n && e.c_b1 == d.c_b1 && e.alpha == d.alpha && e.beta == d.beta &&
-                    e.a_tri == d.a_tri &&
+                    e.a_tri == d.a_tri && e.b_tri == d.b_tri &&
                     e.A - d.A == c * dA && e.B - d.B == c * dB && e.C - d.C == c * dC;
         if (!same) break;
         ++j;

@@ -97,7 +97,8 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_cons
         if (n < g.N && f < k_end) {
           long long o = 0, k = f;
           if (g.KO > 1) { o = f / g.K; k = f - o * g.K; }
-          v = __ldg(Bp + k * g.b_k + n * g.b_n + o * g.b_o);
+          if (g.b_tri == 0 || k > n) v = __ldg(Bp + k * g.b_k + n * g.b_n + o * g.b_o);
+          else v = (k == n) ? 1.0 : 0.0;
         }
         rb[q] = v;
       }

@@ -28,6 +28,7 @@ struct GemmDesc {
   int tiles_m, tiles_n;
   int block_begin;
   int a_tri;  // 0 dense; 1 unit-lower in (m,k); 2 unit-upper in (m,k); 3 identity (A not read)
+  int b_tri;  // 0 dense; 1 unit-lower in (k,n): stored for k > n, 1 on the diagonal, 0 above
   double alpha, beta;
 };
 

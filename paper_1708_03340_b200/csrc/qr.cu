@@ -16,9 +16,9 @@ namespace {
 
 constexpr int QT = 512;          // threads per CTA
 constexpr int NW = QT / kWarp;   // 16 warps
-constexpr int RPW = 8;           // rows per warp  -> 128-row blocks
-constexpr int CS = 4;            // column slots per lane -> K <= 128
-constexpr int BR = NW * RPW;     // 128 block rows
+constexpr int LR = 4;            // row slots per lane: rows lane + 32 t -> 128-row blocks
+constexpr int MC = 7;            // column slots per warp: columns w + 16 m -> K <= 112
+constexpr int BR = kWarp * LR;   // 128 block rows
 constexpr int MAXD = 32;
 
 struct QrDev {
@@ -49,14 +49,11 @@ __device__ __forceinline__ int find_desc(const QrBatch& b) {
 }
 
 struct Smem {
-  double* R;    // K x (K+1) heads of the triangular-head mode
-  double* GT;   // K x (K+1): strict upper = G = Y^T Y, strict lower = T^T
-  double* part; // NW x (K+1) per-warp partial dots
-  double* ssp;  // NW partial tail norms
-  double* head; // K: head row of the dense mode
-  double* coef; // K: tau * w_c
-  double* taus; // K
-  double* col;  // 128: broadcast of the active column (tail values, unscaled)
+  double* R;     // K x (K+1) heads of the triangular-head mode
+  double* GT;    // K x (K+1): strict upper = G = Y^T Y, strict lower = T^T
+  double* vbuf;  // 2 x 128: the current / next reflector (head 1 and zeros included)
+  double* taus;  // K
+  double* prm;   // 2 x 4: tau of the current / next reflector
   int rp;
 };
 
@@ -65,175 +62,157 @@ __device__ __forceinline__ Smem carve(double* sm, int K) {
   s.rp = K + 1;
   s.R = sm;
   s.GT = s.R + K * s.rp;
-  s.part = s.GT + K * s.rp;
-  s.ssp = s.part + NW * s.rp;
-  s.head = s.ssp + NW;
-  s.coef = s.head + K;
-  s.taus = s.coef + K;
-  s.col = s.taus + K;
+  s.vbuf = s.GT + K * s.rp;
+  s.taus = s.vbuf + 2 * BR;
+  s.prm = s.taus + K;
   return s;
 }
 
-// The owner lane of column j (lane j&31, slot j>>5) publishes its 8 rows of column j.
-template <int SLOT>
-__device__ __forceinline__ void publish_col(const double (&a)[RPW][CS], double* col, int w) {
+__device__ __forceinline__ double warp_allsum(double v) {
 #pragma unroll
-  for (int r = 0; r < RPW; ++r) col[w * RPW + r] = a[r][SLOT];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
 }
 
-__device__ __forceinline__ void publish(const double (&a)[RPW][CS], double* col, int w, int js) {
-  switch (js) {
-    case 0: publish_col<0>(a, col, w); break;
-    case 1: publish_col<1>(a, col, w); break;
-    case 2: publish_col<2>(a, col, w); break;
-    default: publish_col<3>(a, col, w); break;
+// Transposed 8-way warp reduction: afterwards lane L holds the warp total of slot
+// (L >> 2) & 7 (lanes 4m..4m+3 hold slot m).  18 shuffles instead of 40.
+__device__ __forceinline__ double reduce8(const double (&x)[8], int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+  const unsigned F = 0xffffffffu;
+  const double y0 = (b4 ? x[4] : x[0]) + __shfl_xor_sync(F, b4 ? x[0] : x[4], 16);
+  const double y1 = (b4 ? x[5] : x[1]) + __shfl_xor_sync(F, b4 ? x[1] : x[5], 16);
+  const double y2 = (b4 ? x[6] : x[2]) + __shfl_xor_sync(F, b4 ? x[2] : x[6], 16);
+  const double y3 = (b4 ? x[7] : x[3]) + __shfl_xor_sync(F, b4 ? x[3] : x[7], 16);
+  const double z0 = (b3 ? y2 : y0) + __shfl_xor_sync(F, b3 ? y0 : y2, 8);
+  const double z1 = (b3 ? y3 : y1) + __shfl_xor_sync(F, b3 ? y1 : y3, 8);
+  double u = (b2 ? z1 : z0) + __shfl_xor_sync(F, b2 ? z0 : z1, 4);
+  u += __shfl_xor_sync(F, u, 2);
+  u += __shfl_xor_sync(F, u, 1);
+  return u;
+}
+
+// reflector jj (dlarfg) from the owner warp's column registers; publishes v (with its
+// head 1 and zeros) in vbuf[buf] and tau in prm[buf]
+template <bool DENSE>
+__device__ __forceinline__ void gen_reflector(double (&col)[LR], int jj, int buf, int nrows, const Smem& s) {
+  const int lane = threadIdx.x & 31;
+  const int rp = s.rp;
+  double ss = 0.0;
+#pragma unroll
+  for (int t = 0; t < LR; ++t) {
+    const int row = lane + t * kWarp;
+    const bool tail = row < nrows && (!DENSE || row > jj);
+    if (tail) ss = fma(col[t], col[t], ss);
+  }
+  ss = warp_allsum(ss);
+  double alpha;
+  if (DENSE) {
+    double hv = col[0];
+#pragma unroll
+    for (int t = 1; t < LR; ++t)
+      if ((jj >> 5) == t) hv = col[t];
+    alpha = __shfl_sync(0xffffffffu, hv, jj & 31);
+  } else {
+    alpha = s.R[jj * rp + jj];
+  }
+  double beta = alpha, tau = 0.0, scal = 0.0;
+  if (ss > 0.0) {
+    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+    tau = (beta - alpha) / beta;
+    scal = 1.0 / (alpha - beta);
+  }
+#pragma unroll
+  for (int t = 0; t < LR; ++t) {
+    const int row = lane + t * kWarp;
+    const bool tail = row < nrows && (!DENSE || row > jj);
+    if (tail) col[t] *= scal;
+    double vb = tail ? col[t] : 0.0;
+    if (DENSE && row == jj) {
+      col[t] = beta;
+      vb = 1.0;
+    }
+    s.vbuf[buf * BR + row] = vb;
+  }
+  if (lane == 0) {
+    s.prm[buf * 4] = tau;
+    s.taus[jj] = tau;
+    if (!DENSE) s.R[jj * rp + jj] = beta;
   }
 }
 
-template <int SLOT, bool DENSE>
-__device__ __forceinline__ void store_v(double (&a)[RPW][CS], const double (&u)[RPW], double scal, double beta,
-                                        int w, int j, int nrows) {
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int i = w * RPW + r;
-    if (DENSE && i == j) a[r][SLOT] = beta;
-    else if (i < nrows && (!DENSE || i > j)) a[r][SLOT] = u[r] * scal;
-  }
-}
-
-// Householder factorisation of the register block a (rows w*8+r, columns lane+32s).
-//  DENSE: reflector j has head a[j][j] and tail rows j+1..nrows-1 (dgeqr2 on the block)
+// Householder factorisation of a register block held column-wise: warp w owns columns
+// c = w + 16 m (slot m), lane l owns rows l + 32 t (slot t).
+//  DENSE: reflector j has head a[j][j], tail rows j+1..nrows-1 (dgeqr2 on the block).
 //  !DENSE: head R[j][j] (shared, upper triangular), tail rows 0..nrows-1 (one TSQR step
 //          on [R; a]).
-// Two CTA barriers per reflector: the partial dots (and tail norm) of reflector j+1 are
-// formed in the same pass that applies reflector j.  Leaves tau in s.taus and the
-// compact-WY T transposed into the strict lower part of GT.
+// One CTA barrier per reflector: the owner warp of column j+1 updates it first and
+// publishes reflector j+1 in the same interval.  G = Y^T Y (strict upper) and the
+// compact-WY T (dlarft, transposed into the strict lower part of GT) are built in the
+// same intervals.
 template <bool DENSE>
-__device__ void factor_core(double (&a)[RPW][CS], int nrows, int K, int nrefl, const Smem& s) {
+__device__ void factor_core(double (&a)[MC][LR], int nrows, int K, int nrefl, const Smem& s) {
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   const int rp = s.rp;
   for (int j = tid; j < K; j += blockDim.x) s.taus[j] = 0.0;
-  double u[RPW];
-  // phase 1 for reflector j (column j already published in s.col)
-  auto phase1 = [&](int j) {
-    double p[CS], ss = 0.0;
-#pragma unroll
-    for (int t = 0; t < CS; ++t) p[t] = 0.0;
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const int i = w * RPW + r;
-      const bool tail = i < nrows && (!DENSE || i > j);
-      u[r] = tail ? s.col[i] : 0.0;
-      ss = fma(u[r], u[r], ss);
-#pragma unroll
-      for (int t = 0; t < CS; ++t) p[t] = fma(u[r], a[r][t], p[t]);
-    }
-#pragma unroll
-    for (int t = 0; t < CS; ++t) {
-      const int c = lane + t * kWarp;
-      if (c < K) s.part[w * rp + c] = p[t];
-    }
-    if (lane == 0) s.ssp[w] = ss;  // all lanes of a warp hold the same rows
-    if (DENSE && (j >> 3) == w) {
-      const int rr = j & 7;
-#pragma unroll
-      for (int r = 0; r < RPW; ++r)
-        if (r == rr) {
-#pragma unroll
-          for (int t = 0; t < CS; ++t) {
-            const int c = lane + t * kWarp;
-            if (c < K) s.head[c] = a[r][t];
-          }
-        }
-    }
-  };
 
-  if (nrefl > 0) {
-    if (lane == 0) publish(a, s.col, w, 0);
-    __syncwarp();
-    phase1(0);
-  }
+  if (nrefl > 0 && w == 0) gen_reflector<DENSE>(a[0], 0, 0, nrows, s);
+  __syncthreads();
   for (int j = 0; j < nrefl; ++j) {
-    __syncthreads();
-    // ---- phase 2: reflector parameters (dlarfg), coefficients, G column ----
-    double ssum = 0.0;
+    const int buf = j & 1;
+    double vr[LR];
 #pragma unroll
-    for (int q = 0; q < NW; ++q) ssum += s.ssp[q];
-    const double alpha = DENSE ? s.head[j] : s.R[j * rp + j];
-    double beta = alpha, tau = 0.0, scal = 0.0;
-    if (ssum > 0.0) {
-      beta = -copysign(sqrt(fma(alpha, alpha, ssum)), alpha);
-      tau = (beta - alpha) / beta;
-      scal = 1.0 / (alpha - beta);
+    for (int t = 0; t < LR; ++t) vr[t] = s.vbuf[buf * BR + lane + t * kWarp];
+    const double tau = s.prm[buf * 4];
+    double x[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) x[m] = 0.0;
+#pragma unroll
+    for (int m = 0; m < MC; ++m) {
+      const int c = w + NW * m;
+      if (c < K && c != j) {
+#pragma unroll
+        for (int t = 0; t < LR; ++t) x[m] = fma(vr[t], a[m][t], x[m]);
+      }
     }
-    if (tid < K) {
-      const int c = tid;
-      double dot = 0.0;
+    const double tot = reduce8(x, lane);
 #pragma unroll
-      for (int q = 0; q < NW; ++q) dot += s.part[q * rp + c];
-      const double hd = DENSE ? s.head[c] : s.R[j * rp + c];
-      const double wc = fma(scal, dot, hd);
-      if (c > j) {
-        s.coef[c] = tau * wc;
-        if (!DENSE) s.R[j * rp + c] = hd - tau * wc;
-      } else if (c < j) {
-        s.GT[c * rp + j] = wc;  // v_c^T v_j
-      } else {
-        s.taus[j] = tau;
-        if (!DENSE) s.R[j * rp + j] = beta;
+    for (int m = 0; m < MC; ++m) {
+      const int c = w + NW * m;
+      if (c < K && c != j) {
+        const double d = __shfl_sync(0xffffffffu, tot, 4 * m);
+        if (c > j) {
+          const double hd = DENSE ? 0.0 : s.R[j * rp + c];
+          const double coef = tau * (d + hd);
+#pragma unroll
+          for (int t = 0; t < LR; ++t) a[m][t] = fma(-coef, vr[t], a[m][t]);
+          if (!DENSE && lane == 0) s.R[j * rp + c] = hd - coef;
+          if (c == j + 1 && c < nrefl) gen_reflector<DENSE>(a[m], c, buf ^ 1, nrows, s);
+        } else if (lane == 0) {
+          s.GT[c * rp + j] = d;  // G[c][j] = v_c^T v_j
+        }
       }
     }
     __syncthreads();
-    // ---- phase 3: apply reflector j (branch-free over rows), store v_j ----
-    double cf[CS];
-#pragma unroll
-    for (int t = 0; t < CS; ++t) {
-      const int c = lane + t * kWarp;
-      cf[t] = (c > j && c < K) ? s.coef[c] : 0.0;
-    }
-#pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const int i = w * RPW + r;
-      const double vr = u[r] * scal + ((DENSE && i == j) ? 1.0 : 0.0);
-#pragma unroll
-      for (int t = 0; t < CS; ++t) a[r][t] = fma(-cf[t], vr, a[r][t]);
-    }
-    const int jl = j & 31, js = j >> 5;
-    if (lane == jl) {
-      switch (js) {
-        case 0: store_v<0, DENSE>(a, u, scal, beta, w, j, nrows); break;
-        case 1: store_v<1, DENSE>(a, u, scal, beta, w, j, nrows); break;
-        case 2: store_v<2, DENSE>(a, u, scal, beta, w, j, nrows); break;
-        default: store_v<3, DENSE>(a, u, scal, beta, w, j, nrows); break;
+  }
+  // compact-WY T (dlarft): row i solves T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] G[l][j],
+  // T[i][i] = tau_i -- rows are independent: one thread per row, no barriers.
+  // T[i][j] (i < j) is stored transposed at GT[j][i].
+  if (tid < nrefl) {
+    const int i = tid;
+    for (int j = i + 1; j < nrefl; ++j) {
+      double a0 = s.taus[i] * s.GT[i * rp + j], a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int l = i + 1;
+      for (; l + 3 < j; l += 4) {
+        a0 = fma(s.GT[l * rp + i], s.GT[l * rp + j], a0);
+        a1 = fma(s.GT[(l + 1) * rp + i], s.GT[(l + 1) * rp + j], a1);
+        a2 = fma(s.GT[(l + 2) * rp + i], s.GT[(l + 2) * rp + j], a2);
+        a3 = fma(s.GT[(l + 3) * rp + i], s.GT[(l + 3) * rp + j], a3);
       }
-    }
-    if (j + 1 < nrefl) {
-      if (lane == ((j + 1) & 31)) publish(a, s.col, w, (j + 1) >> 5);
-      __syncwarp();
-      phase1(j + 1);
+      for (; l < j; ++l) a0 = fma(s.GT[l * rp + i], s.GT[l * rp + j], a0);
+      s.GT[j * rp + i] = -s.taus[j] * ((a0 + a1) + (a2 + a3));
     }
   }
   __syncthreads();
-  // ---- compact-WY T (dlarft, forward columnwise): T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] G[l][j]
-  // stored transposed: T[i][j] at GT[j][i] (i < j); one barrier per column.
-  {
-    const int i = tid >> 2, seg = tid & 3;
-    for (int j = 1; j < nrefl; ++j) {
-      double acc = 0.0;
-      if (i < j) {
-        const int len = j - i, ch = (len + 3) >> 2;
-        const int l0 = i + seg * ch, l1 = min(j, l0 + ch);
-        for (int l = l0; l < l1; ++l) {
-          const double til = (l == i) ? s.taus[i] : s.GT[l * rp + i];
-          acc = fma(til, s.GT[l * rp + j], acc);
-        }
-      }
-      acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-      acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-      if (i < j && seg == 0) s.GT[j * rp + i] = -s.taus[j] * acc;
-      __syncthreads();
-    }
-  }
 }
 
 __device__ void store_T(double* T, const Smem& s, int K, int nrefl) {
@@ -257,7 +236,7 @@ __global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ 
   const int K = q.K;
   const Smem s = carve(sm, K);
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double a[RPW][CS];
+  double a[MC][LR];
   double* Rst = q.Rst + nd * q.st_node;
   double* Tst = q.Tst + nd * q.t_node;
 
@@ -268,12 +247,12 @@ __global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ 
     const int rows = min(q.rpc, q.m - row0);
     const double* A = q.A + nd * q.a_node;
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const int i = w * RPW + r;
+    for (int m = 0; m < MC; ++m) {
+      const int col = w + NW * m;
 #pragma unroll
-      for (int t = 0; t < CS; ++t) {
-        const int col = lane + t * kWarp;
-        a[r][t] = (i < rows && col < K) ? __ldg(A + (long long)(row0 + i) * q.a_r + (long long)col * q.a_c) : 0.0;
+      for (int t = 0; t < LR; ++t) {
+        const int i = lane + t * kWarp;
+        a[m][t] = (i < rows && col < K) ? __ldg(A + (long long)(row0 + i) * q.a_r + (long long)col * q.a_c) : 0.0;
       }
     }
     const int nrefl = min(rows, K);
@@ -281,15 +260,14 @@ __global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ 
     double* V = q.V + nd * q.v_node;
     double* Rc = Rst + (long long)c * K * K;
 #pragma unroll
-    for (int r = 0; r < RPW; ++r) {
-      const int i = w * RPW + r;
+    for (int m = 0; m < MC; ++m) {
+      const int col = w + NW * m;
+      if (col >= K) continue;
 #pragma unroll
-      for (int t = 0; t < CS; ++t) {
-        const int col = lane + t * kWarp;
-        if (col < K) {
-          if (i < rows) V[(long long)col * q.m + row0 + i] = a[r][t];
-          if (i < K) Rc[(long long)i * K + col] = (i < nrefl && col >= i) ? a[r][t] : 0.0;
-        }
+      for (int t = 0; t < LR; ++t) {
+        const int i = lane + t * kWarp;
+        if (i < rows) V[(long long)col * q.m + row0 + i] = a[m][t];
+        if (i < K) Rc[(long long)i * K + col] = (i < nrefl && col >= i) ? a[m][t] : 0.0;
       }
     }
     store_T(Tst + (long long)c * K * K, s, K, nrefl);
@@ -304,14 +282,15 @@ __global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ 
       s.R[i * s.rp + c] = Ra[e];
     }
 #pragma unroll
-    for (int rr = 0; rr < RPW; ++rr) {
-      const int i = w * RPW + rr;
+    for (int m = 0; m < MC; ++m) {
+      const int col = w + NW * m;
 #pragma unroll
-      for (int t = 0; t < CS; ++t) {
-        const int col = lane + t * kWarp;
-        a[rr][t] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
+      for (int t = 0; t < LR; ++t) {
+        const int i = lane + t * kWarp;
+        a[m][t] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
       }
     }
+    __syncthreads();
     factor_core<false>(a, K, K, K, s);
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
       const int i = e / K, c = e - i * K;
@@ -319,12 +298,13 @@ __global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ 
     }
     // reflector tails of the R_b rows, column-major K x K, into R_b's slot
 #pragma unroll
-    for (int rr = 0; rr < RPW; ++rr) {
-      const int i = w * RPW + rr;
+    for (int m = 0; m < MC; ++m) {
+      const int col = w + NW * m;
+      if (col >= K) continue;
 #pragma unroll
-      for (int t = 0; t < CS; ++t) {
-        const int col = lane + t * kWarp;
-        if (i < K && col < K) Rb[(long long)col * K + i] = a[rr][t];
+      for (int t = 0; t < LR; ++t) {
+        const int i = lane + t * kWarp;
+        if (i < K) Rb[(long long)col * K + i] = a[m][t];
       }
     }
     store_T(Tst + (long long)(q.P + ib) * K * K, s, K, K);
@@ -352,7 +332,7 @@ __global__ void qr_finalize_kernel(const __grid_constant__ QrBatch b) {
 
 size_t smem_bytes(int K) {
   const int rp = K + 1;
-  return (size_t)(2 * K * rp + NW * rp + NW + 3 * K + BR) * sizeof(double);
+  return (size_t)(2 * K * rp + 2 * BR + K + 8) * sizeof(double);
 }
 
 int pairs_host(int P, int r) {
