@@ -1,12 +1,19 @@
-// Tree-TSQR Householder QR with register-resident blocks and compact-WY Q
-// formation on DMMA GEMMs (see qr.cuh).
+// Blocked tree-TSQR Householder QR with DMMA trailing updates (see qr.cuh).
 //
-// Reference semantics: kernels.py:24-32 -- dlarfg reflectors as in LAPACK
-// dgeqrf, explicit thin Q (dorgqr), sign fix diag(R) >= 0; wide input (m < K)
-// gives Q m x m and R m x K (kernels.py:27-28).
+// Reference semantics: kernels.py:24-32 -- dlarfg reflectors as in LAPACK dgeqrf,
+// explicit thin Q (dorgqr), sign fix diag(R) >= 0; wide input (m < K) gives
+// Q m x m and R m x K (kernels.py:27-28).
+//
+// One CTA owns one "step": either a dense row block (<= 128 rows, dgeqrf on the
+// block) or a tree pair [R_a; R_b] (reflector heads in R_a's rows, tails in R_b).
+// The step's K columns are processed in panels of 8: warp 0 factors the panel
+// in registers (warp-synchronous dlarfg + dots, no CTA barrier per reflector),
+// builds the panel's compact-WY T (8 x 8), and all 16 warps apply
+// (I - V T V^T)^T to the trailing columns with mma.sync DMMA tiles on shared
+// memory.  Q is formed the same way in reverse (I - V T V^T per panel, last
+// panel first) by the apply kernel.
 #include <algorithm>
 
-#include "gemm.cuh"
 #include "prof.cuh"
 #include "qr.cuh"
 
@@ -14,12 +21,16 @@ namespace ht {
 
 namespace {
 
-constexpr int QT = 512;          // threads per CTA
-constexpr int NW = QT / kWarp;   // 16 warps
-constexpr int LR = 4;            // row slots per lane: rows lane + 32 t -> 128-row blocks
-constexpr int MC = 7;            // column slots per warp: columns w + 16 m -> K <= 112
-constexpr int BR = kWarp * LR;   // 128 block rows
+constexpr int QT = 512;         // threads per CTA (apply kernel)
+constexpr int QTF = 256;        // threads per CTA (factor kernel: the panel warp needs registers)
+constexpr int NB = 8;           // panel width
+constexpr int LR = 4;           // rows per lane in the panel warp -> 128 rows
+constexpr int BR = kWarp * LR;  // 128 block rows
 constexpr int MAXD = 32;
+constexpr int SMEM_LIMIT = 227 * 1024;
+
+__host__ __device__ __forceinline__ int pitch_rows(int rows) { return ((rows + 15) & ~15) + 4; }
+__host__ __device__ __forceinline__ int npanels(int K) { return (K + NB - 1) / NB; }
 
 struct QrDev {
   const double* A;
@@ -30,8 +41,9 @@ struct QrDev {
   long long r_ld, r_node;
   double* V;
   double* Rst;
-  double* Tst;
-  long long v_node, st_node, t_node;
+  double* Tp;
+  double* tau;
+  long long v_node, st_node, tp_node, tau_node;
   int m, K, P, rpc;
   int begin, per_node, nodes;
 };
@@ -48,34 +60,22 @@ __device__ __forceinline__ int find_desc(const QrBatch& b) {
   return di;
 }
 
-struct Smem {
-  double* R;     // K x (K+1) heads of the triangular-head mode
-  double* GT;    // K x (K+1): strict upper = G = Y^T Y, strict lower = T^T
-  double* vbuf;  // 2 x 128: the current / next reflector (head 1 and zeros included)
-  double* taus;  // K
-  double* prm;   // 2 x 4: tau of the current / next reflector
-  int rp;
-};
-
-__device__ __forceinline__ Smem carve(double* sm, int K) {
-  Smem s;
-  s.rp = K + 1;
-  s.R = sm;
-  s.GT = s.R + K * s.rp;
-  s.vbuf = s.GT + K * s.rp;
-  s.taus = s.vbuf + 2 * BR;
-  s.prm = s.taus + K;
-  return s;
-}
-
 __device__ __forceinline__ double warp_allsum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
-// Transposed 8-way warp reduction: afterwards lane L holds the warp total of slot
-// (L >> 2) & 7 (lanes 4m..4m+3 hold slot m).  18 shuffles instead of 40.
+__device__ __forceinline__ void cp_async8(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
+}
+
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// Transposed 8-way warp reduction: lane L ends with the total of slot (L >> 2) & 7.
 __device__ __forceinline__ double reduce8(const double (&x)[8], int lane) {
   const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
   const unsigned F = 0xffffffffu;
@@ -91,223 +91,475 @@ __device__ __forceinline__ double reduce8(const double (&x)[8], int lane) {
   return u;
 }
 
-// reflector jj (dlarfg) from the owner warp's column registers; publishes v (with its
-// head 1 and zeros) in vbuf[buf] and tau in prm[buf]
-template <bool DENSE>
-__device__ __forceinline__ void gen_reflector(double (&col)[LR], int jj, int buf, int nrows, const Smem& s) {
-  const int lane = threadIdx.x & 31;
-  const int rp = s.rp;
-  double ss = 0.0;
-#pragma unroll
-  for (int t = 0; t < LR; ++t) {
-    const int row = lane + t * kWarp;
-    const bool tail = row < nrows && (!DENSE || row > jj);
-    if (tail) ss = fma(col[t], col[t], ss);
-  }
-  ss = warp_allsum(ss);
-  double alpha;
-  if (DENSE) {
-    double hv = col[0];
-#pragma unroll
-    for (int t = 1; t < LR; ++t)
-      if ((jj >> 5) == t) hv = col[t];
-    alpha = __shfl_sync(0xffffffffu, hv, jj & 31);
-  } else {
-    alpha = s.R[jj * rp + jj];
-  }
-  double beta = alpha, tau = 0.0, scal = 0.0;
-  if (ss > 0.0) {
-    beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-    tau = (beta - alpha) / beta;
-    scal = 1.0 / (alpha - beta);
-  }
-#pragma unroll
-  for (int t = 0; t < LR; ++t) {
-    const int row = lane + t * kWarp;
-    const bool tail = row < nrows && (!DENSE || row > jj);
-    if (tail) col[t] *= scal;
-    double vb = tail ? col[t] : 0.0;
-    if (DENSE && row == jj) {
-      col[t] = beta;
-      vb = 1.0;
+// C(M x N) = Cinit + sum_k A(m,k) B(k,n) on 8x8 DMMA tiles spread over the CTA's warps.
+// ga/gb return operands (0 outside), lc the initial C value, sc stores a result.
+template <typename GA, typename GB, typename LC, typename SC>
+__device__ __forceinline__ void cta_dmma(int M, int N, int K, GA ga, GB gb, LC lc, SC sc) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int tm = (M + 7) >> 3, tn = (N + 7) >> 3;
+  const int r = lane >> 2, q = lane & 3;
+  for (int tile = warp; tile < tm * tn; tile += nw) {
+    const int m0 = (tile / tn) << 3, n0 = (tile % tn) << 3;
+    double c0[2], c1[2];
+    c0[0] = lc(m0 + r, n0 + 2 * q);
+    c0[1] = lc(m0 + r, n0 + 2 * q + 1);
+    c1[0] = 0.0;
+    c1[1] = 0.0;
+    int k = 0;
+    for (; k + 8 <= K; k += 8) {
+      dmma_8x8x4(c0, ga(m0 + r, k + q), gb(k + q, n0 + r));
+      dmma_8x8x4(c1, ga(m0 + r, k + 4 + q), gb(k + 4 + q, n0 + r));
     }
-    s.vbuf[buf * BR + row] = vb;
-  }
-  if (lane == 0) {
-    s.prm[buf * 4] = tau;
-    s.taus[jj] = tau;
-    if (!DENSE) s.R[jj * rp + jj] = beta;
+    for (; k < K; k += 4) dmma_8x8x4(c0, ga(m0 + r, k + q), gb(k + q, n0 + r));
+    sc(m0 + r, n0 + 2 * q, c0[0] + c1[0]);
+    sc(m0 + r, n0 + 2 * q + 1, c0[1] + c1[1]);
   }
 }
 
-// Householder factorisation of a register block held column-wise: warp w owns columns
-// c = w + 16 m (slot m), lane l owns rows l + 32 t (slot t).
-//  DENSE: reflector j has head a[j][j], tail rows j+1..nrows-1 (dgeqr2 on the block).
-//  !DENSE: head R[j][j] (shared, upper triangular), tail rows 0..nrows-1 (one TSQR step
-//          on [R; a]).
-// One CTA barrier per reflector: the owner warp of column j+1 updates it first and
-// publishes reflector j+1 in the same interval.  G = Y^T Y (strict upper) and the
-// compact-WY T (dlarft, transposed into the strict lower part of GT) are built in the
-// same intervals.
-template <bool DENSE>
-__device__ void factor_core(double (&a)[MC][LR], int nrows, int K, int nrefl, const Smem& s) {
-  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  const int rp = s.rp;
-  for (int j = tid; j < K; j += blockDim.x) s.taus[j] = 0.0;
-
-  if (nrefl > 0 && w == 0) gen_reflector<DENSE>(a[0], 0, 0, nrows, s);
-  __syncthreads();
-  for (int j = 0; j < nrefl; ++j) {
-    const int buf = j & 1;
-    double vr[LR];
+// ---------------------------------------------------------------------------
+// panel factorisation by warp 0 (columns j0 .. j0+nbp-1 of the step)
+//  DENSE: head S[j][j], tail rows j+1..nrows-1;  TRI: head R[j][j], tail rows 0..nrows-1.
+// Writes the reflectors back into S, tau into taus[j], R heads (TRI), and T_p (8x8) into Tp.
+// ---------------------------------------------------------------------------
+// One reflector JJ (compile-time) of the panel factorisation.  Panel rows are held
+// shifted: lane l, slot t holds panel row r' = l + 32 t, i.e. block row j0 + r' (DENSE)
+// or block row r' (TRI), so the head row of reflector JJ (DENSE) is lane JJ, slot 0.
+// The tail norm is reduced together with the 7 dot products (one 8-way reduction).
+template <bool DENSE, int JJ>
+__device__ __forceinline__ void panel_reflector(double (&pv)[NB][LR], double (&trow)[NB], int nr, int j0, int nbp,
+                                                double* R, int rp, double* taus) {
+  const int lane = threadIdx.x & 31;
+  if (JJ < nbp) {
+    const int j = j0 + JJ;
+    // u = tail of column JJ (rows after the head)
+    double u[LR];
 #pragma unroll
-    for (int t = 0; t < LR; ++t) vr[t] = s.vbuf[buf * BR + lane + t * kWarp];
-    const double tau = s.prm[buf * 4];
+    for (int t = 0; t < LR; ++t) {
+      const int rr = lane + t * kWarp;
+      u[t] = (rr < nr && (!DENSE || rr > JJ)) ? pv[JJ][t] : 0.0;
+    }
     double x[8];
 #pragma unroll
-    for (int m = 0; m < 8; ++m) x[m] = 0.0;
+    for (int c = 0; c < NB; ++c) {
+      x[c] = 0.0;
+      if (c < nbp) {
 #pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int c = w + NW * m;
-      if (c < K && c != j) {
-#pragma unroll
-        for (int t = 0; t < LR; ++t) x[m] = fma(vr[t], a[m][t], x[m]);
+        for (int t = 0; t < LR; ++t) x[c] = fma(u[t], pv[c][t], x[c]);
       }
     }
     const double tot = reduce8(x, lane);
+    double dsum[NB], head[NB];
 #pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int c = w + NW * m;
-      if (c < K && c != j) {
-        const double d = __shfl_sync(0xffffffffu, tot, 4 * m);
-        if (c > j) {
-          const double hd = DENSE ? 0.0 : s.R[j * rp + c];
-          const double coef = tau * (d + hd);
+    for (int c = 0; c < NB; ++c) {
+      dsum[c] = __shfl_sync(0xffffffffu, tot, 4 * c);
+      head[c] = DENSE ? __shfl_sync(0xffffffffu, pv[c][0], JJ) : ((c < nbp && c >= JJ) ? R[j * rp + j0 + c] : 0.0);
+    }
+    const double ss = dsum[JJ];
+    const double alpha = head[JJ];
+    double beta = alpha, tau = 0.0, scal = 0.0;
+    if (ss > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+      const double r1 = 1.0 / beta, r2 = 1.0 / (alpha - beta);
+      tau = (beta - alpha) * r1;
+      scal = r2;
+    }
+    double wc[NB];
 #pragma unroll
-          for (int t = 0; t < LR; ++t) a[m][t] = fma(-coef, vr[t], a[m][t]);
-          if (!DENSE && lane == 0) s.R[j * rp + c] = hd - coef;
-          if (c == j + 1 && c < nrefl) gen_reflector<DENSE>(a[m], c, buf ^ 1, nrows, s);
-        } else if (lane == 0) {
-          s.GT[c * rp + j] = d;  // G[c][j] = v_c^T v_j
-        }
-      }
+    for (int c = 0; c < NB; ++c) wc[c] = (c == JJ) ? 0.0 : fma(scal, dsum[c], (DENSE || c > JJ) ? head[c] : 0.0);
+    // update the trailing panel columns; store v_JJ (head beta, tail scaled)
+#pragma unroll
+    for (int t = 0; t < LR; ++t) {
+      const int rr = lane + t * kWarp;
+      const double v = (DENSE && t == 0 && lane == JJ) ? 1.0 : u[t] * scal;
+#pragma unroll
+      for (int c = JJ + 1; c < NB; ++c)
+        if (c < nbp) pv[c][t] = fma(-tau * wc[c], v, pv[c][t]);
+      if (DENSE && t == 0 && lane == JJ) pv[JJ][0] = beta;
+      else if (rr < nr && (!DENSE || rr > JJ)) pv[JJ][t] = u[t] * scal;
     }
-    __syncthreads();
+    if (!DENSE && lane == 0) {
+#pragma unroll
+      for (int c = JJ + 1; c < NB; ++c)
+        if (c < nbp) R[j * rp + j0 + c] = head[c] - tau * wc[c];
+      R[j * rp + j] = beta;
+    }
+    if (lane == 0) taus[j] = tau;
+    // T column JJ (dlarft), kept in registers: lane r < 8 holds T row r.
+    //   T[r][JJ] = -tau_JJ sum_{l=r}^{JJ-1} T[r][l] G[l][JJ],  G[l][JJ] = v_l^T v_JJ = wc[l]
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < JJ; ++l)
+      if (l >= lane) acc = fma(trow[l], wc[l], acc);
+    trow[JJ] = (lane == JJ) ? tau : (lane < JJ ? -tau * acc : 0.0);
   }
-  // compact-WY T (dlarft): row i solves T[i][j] = -tau_j sum_{l=i}^{j-1} T[i][l] G[l][j],
-  // T[i][i] = tau_i -- rows are independent: one thread per row, no barriers.
-  // T[i][j] (i < j) is stored transposed at GT[j][i].
-  if (tid < nrefl) {
-    const int i = tid;
-    for (int j = i + 1; j < nrefl; ++j) {
-      double a0 = s.taus[i] * s.GT[i * rp + j], a1 = 0.0, a2 = 0.0, a3 = 0.0;
-      int l = i + 1;
-      for (; l + 3 < j; l += 4) {
-        a0 = fma(s.GT[l * rp + i], s.GT[l * rp + j], a0);
-        a1 = fma(s.GT[(l + 1) * rp + i], s.GT[(l + 1) * rp + j], a1);
-        a2 = fma(s.GT[(l + 2) * rp + i], s.GT[(l + 2) * rp + j], a2);
-        a3 = fma(s.GT[(l + 3) * rp + i], s.GT[(l + 3) * rp + j], a3);
-      }
-      for (; l < j; ++l) a0 = fma(s.GT[l * rp + i], s.GT[l * rp + j], a0);
-      s.GT[j * rp + i] = -s.taus[j] * ((a0 + a1) + (a2 + a3));
+  if constexpr (JJ + 1 < NB) panel_reflector<DENSE, JJ + 1>(pv, trow, nr, j0, nbp, R, rp, taus);
+}
+
+// ---------------------------------------------------------------------------
+// panel factorisation by warp 0 (columns j0 .. j0+nbp-1 of the step)
+//  DENSE: head S[j][j], tail rows j+1..nrows-1;  TRI: head R[j][j], tail rows 0..nrows-1.
+// Writes the reflectors back into S, tau into taus[j], R heads (TRI), and T_p (8x8) into Tp.
+// ---------------------------------------------------------------------------
+template <bool DENSE>
+__device__ void panel_factor(double* S, int ps, int nrows, int j0, int nbp, double* R, int rp, double* taus,
+                             double* Gs, double* Tp) {
+  (void)Gs;
+  const int lane = threadIdx.x & 31;
+  const int off = DENSE ? j0 : 0;   // panel row r' = block row - off
+  const int nr = nrows - off;
+  double pv[NB][LR];
+  double trow[NB];
+#pragma unroll
+  for (int c = 0; c < NB; ++c) {
+    trow[c] = 0.0;
+#pragma unroll
+    for (int t = 0; t < LR; ++t) {
+      const int rr = lane + t * kWarp;
+      pv[c][t] = (c < nbp && rr < nr) ? S[(j0 + c) * ps + off + rr] : 0.0;
     }
   }
+  panel_reflector<DENSE, 0>(pv, trow, nr, j0, nbp, R, rp, taus);
+#pragma unroll
+  for (int c = 0; c < NB; ++c)
+#pragma unroll
+    for (int t = 0; t < LR; ++t) {
+      const int rr = lane + t * kWarp;
+      if (c < nbp && rr < nr) S[(j0 + c) * ps + off + rr] = pv[c][t];
+    }
+  if (lane < NB) {
+#pragma unroll
+    for (int c = 0; c < NB; ++c) Tp[lane * NB + c] = (lane < nbp && c < nbp) ? trow[c] : 0.0;
+  }
+  __syncwarp();
+}
+
+// Masked copy of panel V (columns j0..j0+nbp-1) into Vp[r][row] (zero rows beyond nrows,
+// unit diagonal and zeros above it in the DENSE case).
+template <bool DENSE>
+__device__ __forceinline__ void stage_panel_v(const double* S, int ps, int nrows, int j0, int nbp, double* Vp) {
+  for (int e = threadIdx.x; e < NB * ps; e += blockDim.x) {
+    const int r = e / ps, row = e - r * ps;
+    double v = 0.0;
+    if (r < nbp && row < nrows) {
+      const int col = j0 + r;
+      if (!DENSE || row > col) v = S[col * ps + row];
+      else if (row == col) v = 1.0;
+    }
+    Vp[e] = v;
+  }
+}
+
+// W (8 x nt) = [R head rows] + Vp^T C,  C = S[:, c0:c0+nt]  (all operands zero padded)
+__device__ __forceinline__ void dmma_vt_c(const double* Vp, int pv, const double* C, int pc, int krows, int nt,
+                                          double* W, int pw, const double* Rh, int rp, int nbp) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int ntt = (nt + 7) >> 3;
+  for (int tile = warp; tile < ntt; tile += nw) {
+    const int n0 = tile << 3;
+    double c0[2] = {0.0, 0.0}, c1[2] = {0.0, 0.0};
+    if (Rh) {
+      if (r < nbp && n0 + 2 * q < nt) c0[0] = Rh[r * rp + n0 + 2 * q];
+      if (r < nbp && n0 + 2 * q + 1 < nt) c0[1] = Rh[r * rp + n0 + 2 * q + 1];
+    }
+    const double* a = Vp + r * pv + q;
+    const double* b = C + (n0 + r) * pc + q;
+    int k = 0;
+    for (; k + 8 <= krows; k += 8) {
+      dmma_8x8x4(c0, a[k], b[k]);
+      dmma_8x8x4(c1, a[k + 4], b[k + 4]);
+    }
+    for (; k < krows; k += 4) dmma_8x8x4(c0, a[k], b[k]);
+    W[r * pw + n0 + 2 * q] = c0[0] + c1[0];
+    W[r * pw + n0 + 2 * q + 1] = c0[1] + c1[1];
+  }
+}
+
+// C[:, 0:nt] (rows krows) += Vp * Wn   (Wn = -T-scaled W, 8 x nt, zero padded)
+__device__ __forceinline__ void dmma_c_plus_v_w(const double* Vp, int pv, const double* Wn, int pw, double* C, int pc,
+                                                int krows, int nt) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int r = lane >> 2, q = lane & 3;
+  const int mt = (krows + 7) >> 3, ntt = (nt + 7) >> 3;
+  for (int tile = warp; tile < mt * ntt; tile += nw) {
+    const int m0 = (tile / ntt) << 3, n0 = (tile % ntt) << 3;
+    double acc[2];
+    double* c = C + (n0 + 2 * q) * pc + m0 + r;
+    acc[0] = c[0];
+    acc[1] = c[pc];
+    // A(m = row, k = reflector) = Vp[k][row]; B(k, n) = Wn[k][n]
+    dmma_8x8x4(acc, Vp[q * pv + m0 + r], Wn[q * pw + n0 + r]);
+    dmma_8x8x4(acc, Vp[(q + 4) * pv + m0 + r], Wn[(q + 4) * pw + n0 + r]);
+    c[0] = acc[0];
+    c[pc] = acc[1];
+  }
+}
+
+// Apply (I - V T V^T)^T of panel [j0, j0+nbp) to the trailing columns [j0+nbp, K).
+template <bool DENSE>
+__device__ void trailing_update(double* S, int ps, int nrows, int K, int j0, int nbp, double* R, int rp,
+                                const double* Tp, double* W, double* W2, int pw, double* Vp) {
+  const int c0 = j0 + nbp;
+  const int nt = K - c0;
+  if (nt <= 0) return;
+  const int krows = (nrows + 3) & ~3;
+  dmma_vt_c(Vp, ps, S + c0 * ps, ps, krows, nt, W, pw, DENSE ? nullptr : R + j0 * rp + c0, rp, nbp);
+  __syncthreads();
+  // W2 = -(T^T W)  (T upper triangular: (T^T W)[r][c] = sum_{l<=r} T[l][r] W[l][c]); TRI: R heads -= T^T W
+  const int ntp = (nt + 7) & ~7;
+  for (int e = threadIdx.x; e < NB * ntp; e += blockDim.x) {
+    const int r = e / ntp, c = e - r * ntp;
+    double acc = 0.0;
+    if (r < nbp && c < nt) {
+      for (int l = 0; l <= r; ++l) acc = fma(Tp[l * NB + r], W[l * pw + c], acc);
+      if (!DENSE) R[(j0 + r) * rp + c0 + c] -= acc;
+    }
+    W2[r * pw + c] = -acc;
+  }
+  __syncthreads();
+  dmma_c_plus_v_w(Vp, ps, W2, pw, S + c0 * ps, ps, krows, nt);
   __syncthreads();
 }
 
-__device__ void store_T(double* T, const Smem& s, int K, int nrefl) {
-  for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-    const int i = e / K, j = e - i * K;
-    double v = 0.0;
-    if (j < nrefl) {
-      if (i < j) v = s.GT[j * s.rp + i];
-      else if (i == j) v = s.taus[i];
-    }
-    T[e] = v;
+template <bool DENSE>
+__device__ void factor_step(double* S, int ps, int nrows, int K, int nrefl, double* R, int rp, double* taus,
+                            double* W, double* W2, int pw, double* Gs, double* Tp, double* Tp_out, double* Vp) {
+  for (int j0 = 0; j0 < nrefl; j0 += NB) {
+    const int nbp = min(NB, nrefl - j0);
+    // TRI: R_b stays upper triangular, so panel p only touches its rows < j0 + nbp
+    const int prow = DENSE ? nrows : min(nrows, j0 + nbp);
+    if (threadIdx.x < kWarp) panel_factor<DENSE>(S, ps, prow, j0, nbp, R, rp, taus, Gs, Tp);
+    __syncthreads();
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Tp_out[(j0 / NB) * NB * NB + e] = Tp[e];
+    stage_panel_v<DENSE>(S, ps, prow, j0, nbp, Vp);
+    __syncthreads();
+    trailing_update<DENSE>(S, ps, prow, K, j0, nbp, R, rp, Tp, W, W2, pw, Vp);
   }
 }
 
-// mode 0: dense QR of one row block; mode 1: combine step [R_a; R_b] of round `round`.
-__global__ void __launch_bounds__(QT, 1) qr_step_kernel(const __grid_constant__ QrBatch b) {
+struct FactorSmem {
+  double *S, *R, *W, *W2, *Gs, *Tp, *taus, *Vp;
+  int ps, rp, pw;
+};
+
+__host__ __device__ __forceinline__ int pad8(int v) { return (v + 7) & ~7; }
+
+__host__ __device__ inline size_t factor_smem_doubles(int K, bool dense, int rows) {
+  const int ps = pitch_rows(dense ? rows : K);
+  const int pw = pitch_rows(pad8(K));
+  return (size_t)(pad8(K) + (dense ? 8 : 0)) * ps + (dense ? 0 : (size_t)K * (K + 1)) + 2 * NB * pw + 2 * NB * NB + K + 8 +
+         (size_t)NB * ps;
+}
+
+__device__ FactorSmem carve_factor(double* sm, int K, bool dense, int rows) {
+  FactorSmem f;
+  f.ps = pitch_rows(dense ? rows : K);
+  f.rp = K + 1;
+  f.pw = pitch_rows(pad8(K));
+  f.S = sm;
+  double* p = sm + (size_t)(pad8(K) + (dense ? 8 : 0)) * f.ps;
+  f.R = p;
+  if (!dense) p += (size_t)K * f.rp;
+  f.W = p;
+  p += NB * f.pw;
+  f.W2 = p;
+  p += NB * f.pw;
+  f.Gs = p;
+  p += NB * NB;
+  f.Tp = p;
+  p += NB * NB;
+  f.taus = p;
+  p += K + 8;
+  f.Vp = p;
+  return f;
+}
+
+// round < 0: dense blocks; round >= 0: combine round
+__global__ void __launch_bounds__(QTF, 1) qr_factor_kernel(const __grid_constant__ QrBatch b) {
   extern __shared__ double sm[];
   const QrDev& q = b.d[find_desc(b)];
   const int local = blockIdx.x - q.begin;
   const int nd = local / q.per_node, k = local % q.per_node;
   const int K = q.K;
-  const Smem s = carve(sm, K);
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  double a[MC][LR];
+  const int np = npanels(K);
   double* Rst = q.Rst + nd * q.st_node;
-  double* Tst = q.Tst + nd * q.t_node;
+  double* Tpg = q.Tp + nd * q.tp_node;
+  double* taug = q.tau + nd * q.tau_node;
 
   if (b.round < 0) {
-    // ---- dense block c = k ----
     const int c = k;
     const int row0 = c * q.rpc;
     const int rows = min(q.rpc, q.m - row0);
-    const double* A = q.A + nd * q.a_node;
-#pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int col = w + NW * m;
-#pragma unroll
-      for (int t = 0; t < LR; ++t) {
-        const int i = lane + t * kWarp;
-        a[m][t] = (i < rows && col < K) ? __ldg(A + (long long)(row0 + i) * q.a_r + (long long)col * q.a_c) : 0.0;
-      }
-    }
     const int nrefl = min(rows, K);
-    factor_core<true>(a, rows, K, nrefl, s);
+    FactorSmem f = carve_factor(sm, K, true, BR);
+    const double* A = q.A + nd * q.a_node;
+    // column-major smem block; global loads coalesced along rows for column-major A
+    for (int e = threadIdx.x; e < (pad8(K) + 8) * f.ps; e += blockDim.x) {
+      const int col = e / f.ps, row = e - col * f.ps;
+      const bool ok = row < rows && col < K;
+      cp_async8(f.S + e, ok ? A + (long long)(row0 + row) * q.a_r + (long long)col * q.a_c : A, ok);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    factor_step<true>(f.S, f.ps, rows, K, nrefl, f.R, f.rp, f.taus, f.W, f.W2, f.pw, f.Gs, f.Tp,
+                      Tpg + (long long)c * np * NB * NB, f.Vp);
     double* V = q.V + nd * q.v_node;
     double* Rc = Rst + (long long)c * K * K;
-#pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int col = w + NW * m;
-      if (col >= K) continue;
-#pragma unroll
-      for (int t = 0; t < LR; ++t) {
-        const int i = lane + t * kWarp;
-        if (i < rows) V[(long long)col * q.m + row0 + i] = a[m][t];
-        if (i < K) Rc[(long long)i * K + col] = (i < nrefl && col >= i) ? a[m][t] : 0.0;
-      }
+    for (int e = threadIdx.x; e < K * BR; e += blockDim.x) {
+      const int col = e / BR, row = e - col * BR;
+      const double v = f.S[col * f.ps + row];
+      if (row < rows) V[(long long)col * q.m + row0 + row] = v;
+      if (row < K) Rc[(long long)row * K + col] = (row < nrefl && col >= row) ? v : 0.0;
     }
-    store_T(Tst + (long long)c * K * K, s, K, nrefl);
+    for (int j = threadIdx.x; j < K; j += blockDim.x) taug[(long long)c * K + j] = j < nrefl ? f.taus[j] : 0.0;
   } else {
-    // ---- combine pair (a, b) ----
     const int r = b.round;
     const int ia = k << (r + 1), ib = ia + (1 << r);
+    FactorSmem f = carve_factor(sm, K, false, K);
     double* Ra = Rst + (long long)ia * K * K;
     double* Rb = Rst + (long long)ib * K * K;
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int i = e / K, c = e - i * K;
-      s.R[i * s.rp + c] = Ra[e];
+      const int i = e / K, col = e - i * K;
+      f.R[i * f.rp + col] = Ra[e];
     }
-#pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int col = w + NW * m;
-#pragma unroll
-      for (int t = 0; t < LR; ++t) {
-        const int i = lane + t * kWarp;
-        a[m][t] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
-      }
+    for (int e = threadIdx.x; e < pad8(K) * f.ps; e += blockDim.x) {
+      const int col = e / f.ps, i = e - col * f.ps;
+      f.S[e] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
     }
     __syncthreads();
-    factor_core<false>(a, K, K, K, s);
+    factor_step<false>(f.S, f.ps, K, K, K, f.R, f.rp, f.taus, f.W, f.W2, f.pw, f.Gs, f.Tp,
+                       Tpg + (long long)(q.P + ib) * np * NB * NB, f.Vp);
     for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int i = e / K, c = e - i * K;
-      Ra[e] = s.R[i * s.rp + c];
+      const int i = e / K, col = e - i * K;
+      Ra[e] = f.R[i * f.rp + col];
+      Rb[(long long)col * K + i] = f.S[col * f.ps + i];  // reflector tails, column-major
     }
-    // reflector tails of the R_b rows, column-major K x K, into R_b's slot
-#pragma unroll
-    for (int m = 0; m < MC; ++m) {
-      const int col = w + NW * m;
-      if (col >= K) continue;
-#pragma unroll
-      for (int t = 0; t < LR; ++t) {
-        const int i = lane + t * kWarp;
-        if (i < K) Rb[(long long)col * K + i] = a[m][t];
+    for (int j = threadIdx.x; j < K; j += blockDim.x) taug[(long long)(q.P + ib) * K + j] = f.taus[j];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Q formation: apply the step's panels in reverse (H_p = I - V_p T_p V_p^T, last panel
+// first) to [W; 0] (dense block) or to [H; Z] (tree pair: heads H = W_a, tails Z = 0).
+// ---------------------------------------------------------------------------
+__host__ __device__ inline size_t apply_smem_doubles(int K, bool dense) {
+  const int pw = pitch_rows(pad8(K));
+  if (dense) {
+    const int pc = pitch_rows(BR);
+    return (size_t)(pad8(K) + 8) * pc + (size_t)NB * pc + 2 * NB * pw + NB * NB + 8;
+  }
+  const int pz = pitch_rows(K);
+  return (size_t)K * pw + (size_t)pad8(K) * pz + (size_t)NB * pz + 2 * NB * pw + NB * NB + 8;
+}
+
+// W2 = -(T W) for upper-triangular T (8 x 8), W (8 x ncols); TRI: heads H += W2
+__device__ __forceinline__ void apply_t(const double* Ts, const double* W, double* W2, int pw, int nbp, int ncols,
+                                        double* Hh, int ph) {
+  const int ntp = (ncols + 7) & ~7;
+  for (int e = threadIdx.x; e < NB * ntp; e += blockDim.x) {
+    const int r = e / ntp, c = e - r * ntp;
+    double acc = 0.0;
+    if (r < nbp && c < ncols) {
+      for (int l = r; l < nbp; ++l) acc = fma(Ts[r * NB + l], W[l * pw + c], acc);
+      if (Hh) Hh[r * ph + c] -= acc;
+    }
+    W2[r * pw + c] = -acc;
+  }
+}
+
+template <bool DENSE>
+__device__ void apply_step(double* C, int pc, double* H, int ph, int nrows, int kq, int nrefl, const double* Vg,
+                           long long v_ld, const double* Tpg, double* Vs, double* W, double* W2, int pw, double* Ts) {
+  for (int p = npanels(nrefl) - 1; p >= 0; --p) {
+    const int j0 = p * NB, nbp = min(NB, nrefl - j0);
+    const int prow = DENSE ? nrows : min(nrows, j0 + nbp);  // TRI: tails only in rows < j0 + nbp
+    for (int e = threadIdx.x; e < NB * pc; e += blockDim.x) {
+      const int r = e / pc, row = e - r * pc;
+      double v = 0.0;
+      if (r < nbp && row < prow) {
+        const int col = j0 + r;
+        if (!DENSE || row > col) v = Vg[(long long)col * v_ld + row];
+        else if (row == col) v = 1.0;
       }
+      Vs[e] = v;
     }
-    store_T(Tst + (long long)(q.P + ib) * K * K, s, K, K);
+    for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = Tpg[p * NB * NB + e];
+    __syncthreads();
+    const int krows = (prow + 3) & ~3;
+    dmma_vt_c(Vs, pc, C, pc, krows, kq, W, pw, DENSE ? nullptr : H + j0 * ph, ph, nbp);
+    __syncthreads();
+    apply_t(Ts, W, W2, pw, nbp, kq, DENSE ? nullptr : H + j0 * ph, ph);
+    __syncthreads();
+    dmma_c_plus_v_w(Vs, pc, W2, pw, C, pc, krows, kq);
+    __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(QT, 1) qr_apply_kernel(const __grid_constant__ QrBatch b) {
+  extern __shared__ double sm[];
+  const QrDev& q = b.d[find_desc(b)];
+  const int local = blockIdx.x - q.begin;
+  const int nd = local / q.per_node, k = local % q.per_node;
+  const int K = q.K, kq = min(q.m, K);
+  const int np = npanels(K);
+  const int pw = pitch_rows(pad8(K));
+  double* Q = q.Q + nd * q.q_node;
+  const double* Tpg = q.Tp + nd * q.tp_node;
+  if (b.round < 0) {
+    const int c = k;
+    const int row0 = c * q.rpc;
+    const int rows = min(q.rpc, q.m - row0);
+    const int nrefl = min(rows, K), kr = nrefl;
+    const int pc = pitch_rows(BR);
+    double* C = sm;
+    double* Vs = C + (size_t)(pad8(K) + 8) * pc;
+    double* W = Vs + NB * pc;
+    double* W2 = W + NB * pw;
+    double* Ts = W2 + NB * pw;
+    for (int e = threadIdx.x; e < (pad8(K) + 8) * pc; e += blockDim.x) {
+      const int col = e / pc, row = e - col * pc;
+      const bool ok = row < kr && col < kq;
+      cp_async8(C + e, ok ? Q + (long long)(row0 + row) * q.q_r + (long long)col * q.q_c : Q, ok);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    apply_step<true>(C, pc, nullptr, 0, rows, kq, nrefl, q.V + nd * q.v_node + row0, q.m,
+                     Tpg + (long long)c * np * NB * NB, Vs, W, W2, pw, Ts);
+    for (int e = threadIdx.x; e < kq * pc; e += blockDim.x) {
+      const int col = e / pc, row = e - col * pc;
+      if (row < rows) Q[(long long)(row0 + row) * q.q_r + (long long)col * q.q_c] = C[e];
+    }
+  } else {
+    const int r = b.round;
+    const int ia = k << (r + 1), ib = ia + (1 << r);
+    const int rows_b = min(q.rpc, q.m - ib * q.rpc);
+    const int krb = min(rows_b, K);
+    const int pz = pitch_rows(K), ph = pw;
+    double* H = sm;                             // heads, row-major K x ph
+    double* Z = H + (size_t)K * ph;             // tails, column-major pad8(kq) x pz
+    double* Vs = Z + (size_t)pad8(K) * pz;
+    double* W = Vs + NB * pz;
+    double* W2 = W + NB * pw;
+    double* Ts = W2 + NB * pw;
+    const long long ra = (long long)ia * q.rpc, rb = (long long)ib * q.rpc;
+    for (int e = threadIdx.x; e < K * ph; e += blockDim.x) {
+      const int row = e / ph, col = e - row * ph;
+      const bool ok = col < kq;
+      cp_async8(H + e, ok ? Q + (ra + row) * q.q_r + (long long)col * q.q_c : Q, ok);
+    }
+    for (int e = threadIdx.x; e < pad8(K) * pz; e += blockDim.x) Z[e] = 0.0;
+    cp_async_wait_all();
+    __syncthreads();
+    apply_step<false>(Z, pz, H, ph, K, kq, K, q.Rst + nd * q.st_node + (long long)ib * K * K, K,
+                      Tpg + (long long)(q.P + ib) * np * NB * NB, Vs, W, W2, pw, Ts);
+    for (int e = threadIdx.x; e < kq * K; e += blockDim.x) {
+      const int row = e / kq, col = e - row * kq;
+      Q[(ra + row) * q.q_r + (long long)col * q.q_c] = H[row * ph + col];
+    }
+    for (int e = threadIdx.x; e < kq * pz; e += blockDim.x) {
+      const int col = e / pz, row = e - col * pz;
+      if (row < krb) Q[(rb + row) * q.q_r + (long long)col * q.q_c] = Z[e];
+    }
   }
 }
 
@@ -330,11 +582,6 @@ __global__ void qr_finalize_kernel(const __grid_constant__ QrBatch b) {
   }
 }
 
-size_t smem_bytes(int K) {
-  const int rp = K + 1;
-  return (size_t)(2 * K * rp + 2 * BR + K + 8) * sizeof(double);
-}
-
 int pairs_host(int P, int r) {
   const int h = 1 << r;
   return P > h ? (P - h - 1) / (2 * h) + 1 : 0;
@@ -347,8 +594,8 @@ QrDev to_dev(const QrProblem& p) {
   d.A = p.A; d.a_r = p.a_r; d.a_c = p.a_c; d.a_node = p.a_node;
   d.Q = p.Q; d.q_r = p.q_r; d.q_c = p.q_c; d.q_node = p.q_node;
   d.R = p.R; d.r_ld = p.r_ld; d.r_node = p.r_node;
-  d.V = p.V; d.Rst = p.Rst; d.Tst = p.Tst;
-  d.v_node = p.v_node; d.st_node = p.st_node; d.t_node = p.t_node;
+  d.V = p.V; d.Rst = p.Rst; d.Tp = p.Tst; d.tau = p.X;
+  d.v_node = p.v_node; d.st_node = p.st_node; d.tp_node = p.t_node; d.tau_node = p.x_node;
   d.m = p.m; d.K = p.K; d.P = p.P; d.rpc = p.rpc;
   d.nodes = p.nodes;
   return d;
@@ -359,20 +606,21 @@ double qr_flops(int m, int K) {
   return 2.0 * a * b * b - 2.0 / 3.0 * b * b * b;
 }
 
-// round < 0: dense blocks; round >= 0: combine round; round == -2: finalize
-int launch(std::vector<QrProblem>& probs, int round, cudaStream_t stream) {
+enum Kind { kFactor, kApply, kFinalize };
+
+int launch(std::vector<QrProblem>& probs, Kind kind, int round, cudaStream_t stream) {
   size_t i = 0;
   while (i < probs.size()) {
     QrBatch b;
     b.count = 0;
-    b.round = round == -2 ? 0 : round;
+    b.round = round;
     int blocks = 0;
     size_t smem = 0;
     double flops = 0;
     while (i < probs.size() && b.count < MAXD) {
       const QrProblem& p = probs[i++];
       int per;
-      if (round == -2) per = 1;
+      if (kind == kFinalize) per = 1;
       else if (round < 0) per = p.P;
       else per = pairs_host(p.P, round);
       if (per == 0 || p.nodes == 0) continue;
@@ -380,20 +628,26 @@ int launch(std::vector<QrProblem>& probs, int round, cudaStream_t stream) {
       d.begin = blocks;
       d.per_node = per;
       blocks += per * p.nodes;
-      smem = std::max(smem, smem_bytes(p.K));
-      if (round == -1) flops += (double)p.nodes * qr_flops(p.m, p.K);
+      const bool dense = round < 0;
+      smem = std::max(smem, sizeof(double) * (kind == kFactor ? factor_smem_doubles(p.K, dense, BR)
+                                                              : apply_smem_doubles(p.K, dense)));
+      if (round < 0 && kind != kFinalize) flops += (double)p.nodes * qr_flops(p.m, p.K);
       b.d[b.count++] = d;
     }
     if (!b.count) continue;
     ProfToken tok = prof_begin(stream);
-    if (round == -2) {
+    if (kind == kFinalize) {
       qr_finalize_kernel<<<blocks, 256, 0, stream>>>(b);
       HT_LAUNCH_CHECK();
       prof_end(tok, "qr_finalize", stream, 0.0, 0.0);
-    } else {
-      qr_step_kernel<<<blocks, QT, smem, stream>>>(b);
+    } else if (kind == kFactor) {
+      qr_factor_kernel<<<blocks, QTF, smem, stream>>>(b);
       HT_LAUNCH_CHECK();
-      prof_end(tok, round < 0 ? "qr_block_factor" : "qr_tree_combine", stream, flops, 0.0);
+      prof_end(tok, round < 0 ? "qr_block_factor" : "qr_tree_factor", stream, flops, 0.0);
+    } else {
+      qr_apply_kernel<<<blocks, QT, smem, stream>>>(b);
+      HT_LAUNCH_CHECK();
+      prof_end(tok, round < 0 ? "qr_block_apply" : "qr_tree_apply", stream, flops, 0.0);
     }
   }
   return kOk;
@@ -407,7 +661,7 @@ int qr_plan(QrProblem& p) {
     return kErrShape;
   }
   if (p.K > kQrMaxK) {
-    set_error("qr_plan: K=" + std::to_string(p.K) + " exceeds the register-resident QR path (K <= 112)");
+    set_error("qr_plan: K=" + std::to_string(p.K) + " exceeds the shared-memory QR path (K <= 112)");
     return kErrUnsupported;
   }
   int P = ceil_div(p.m, BR);
@@ -415,10 +669,11 @@ int qr_plan(QrProblem& p) {
   P = ceil_div(p.m, rpc);
   p.P = P;
   p.rpc = rpc;
+  const int np = npanels(p.K);
   p.v_node = (long long)p.m * p.K;
   p.st_node = (long long)P * p.K * p.K;
-  p.t_node = 2LL * P * p.K * p.K;
-  p.x_node = 3LL * P * p.K * p.K;
+  p.t_node = 2LL * P * np * NB * NB;  // per-panel T factors of blocks and tree pairs
+  p.x_node = 2LL * P * p.K;           // taus
   p.own_v = (p.V == nullptr);
   return kOk;
 }
@@ -442,118 +697,19 @@ void qr_bind_workspace(QrProblem& p, double* ws) {
 int qr_batched(std::vector<QrProblem>& probs, cudaStream_t stream) {
   if (probs.empty()) return kOk;
   if (!g_attr_done) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(qr_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(qr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     g_attr_done = true;
   }
   int maxP = 1;
   for (auto& p : probs) maxP = std::max(maxP, p.P);
   int rounds = 0;
   while ((1 << rounds) < maxP) ++rounds;
-
-  // ---- factorisation ----
-  HT_TRY(launch(probs, -1, stream));
-  for (int r = 0; r < rounds; ++r) HT_TRY(launch(probs, r, stream));
-  HT_TRY(launch(probs, -2, stream));
-
-  // ---- Q formation on DMMA GEMMs (compact WY) ----
-  // Q(row, col) for row = chunk start + i; W blocks live in Q's top rows of each chunk.
-  auto qptr = [](const QrProblem& p, long long row) { return p.Q + row * p.q_r; };
-  for (int r = rounds - 1; r >= 0; --r) {
-    std::vector<GemmDesc> g1, g2;
-    for (auto& p : probs) {
-      const int np = pairs_host(p.P, r);
-      if (np == 0) continue;
-      const int K = p.K, kq = std::min(p.m, K);
-      const long long KK = (long long)K * K;
-      const long long pair_rows = (long long)p.rpc << (r + 1);
-      const long long hb = 1LL << r;
-      // last chunk may be short: split off the pair whose b is the last chunk
-      const int last_b = (int)((long long)(np - 1) * (2 * hb) + hb);
-      const int rows_lastb = std::min(p.rpc, p.m - last_b * p.rpc);
-      const bool short_last = rows_lastb < K;
-      auto add_pairs = [&](int k0, int cnt, int krb) {
-        if (cnt <= 0) return;
-        const long long ia0 = (long long)k0 * 2 * hb, ib0 = ia0 + hb;
-        double* X = p.X + ia0 * KK;
-        // X = T_ab W_a  (K x kq)
-        GemmDesc x = gemm_desc(p.Tst + (p.P + ib0) * KK, K, 1, qptr(p, ia0 * p.rpc), p.q_r, p.q_c, X, kq, 1, K,
-                               kq, K);
-        x.nb1 = cnt; x.a_b1 = 2 * hb * KK; x.b_b1 = pair_rows * p.q_r; x.c_b1 = 2 * hb * KK;
-        x.nb2 = p.nodes; x.a_b2 = p.t_node; x.b_b2 = p.q_node; x.c_b2 = p.x_node;
-        g1.push_back(x);
-        // W_b = -V_b X   (krb x kq); V_b column-major K x K in R_b's slot
-        GemmDesc wb = gemm_desc(p.Rst + ib0 * KK, 1, K, X, kq, 1, qptr(p, ib0 * p.rpc), p.q_r, p.q_c, krb, kq, K,
-                                -1.0, 0.0);
-        wb.nb1 = cnt; wb.a_b1 = 2 * hb * KK; wb.b_b1 = 2 * hb * KK; wb.c_b1 = pair_rows * p.q_r;
-        wb.nb2 = p.nodes; wb.a_b2 = p.st_node; wb.b_b2 = p.x_node; wb.c_b2 = p.q_node;
-        g2.push_back(wb);
-        // W_a -= X
-        GemmDesc wa = gemm_desc(nullptr, 0, 0, X, kq, 1, qptr(p, ia0 * p.rpc), p.q_r, p.q_c, K, kq, K, -1.0, 1.0);
-        wa.a_tri = 3;
-        wa.nb1 = cnt; wa.b_b1 = 2 * hb * KK; wa.c_b1 = pair_rows * p.q_r;
-        wa.nb2 = p.nodes; wa.b_b2 = p.x_node; wa.c_b2 = p.q_node;
-        g2.push_back(wa);
-      };
-      if (short_last) {
-        add_pairs(0, np - 1, K);
-        add_pairs(np - 1, 1, rows_lastb);
-      } else {
-        add_pairs(0, np, K);
-      }
-    }
-    HT_TRY(gemm_grouped(g1, stream, "gemm_qr_tree"));
-    HT_TRY(gemm_grouped(g2, stream, "gemm_qr_tree"));
-  }
-  {
-    // blocks: X1 = Y_top^T W, X2 = T X1, Q = [W; 0] - Y X2
-    std::vector<GemmDesc> g1, g2, g3;
-    for (auto& p : probs) {
-      const int K = p.K, kq = std::min(p.m, K);
-      const long long KK = (long long)K * K;
-      const int last_rows = p.m - (p.P - 1) * p.rpc;
-      auto add_blocks = [&](int c0, int cnt, int rows) {
-        if (cnt <= 0) return;
-        const int kr = std::min(rows, K);
-        double* X1 = p.X + (long long)p.P * KK + (long long)c0 * KK;
-        double* X2 = p.X + 2LL * p.P * KK + (long long)c0 * KK;
-        const long long row0 = (long long)c0 * p.rpc;
-        // X1 (K x kq) = Y[0:kr, :]^T W (kr x kq): A(m,k) = Y(k,m), unit-upper in (m,k)
-        GemmDesc a = gemm_desc(p.V + row0, p.m, 1, qptr(p, row0), p.q_r, p.q_c, X1, kq, 1, K, kq, kr);
-        a.a_tri = 2;
-        a.nb1 = cnt; a.a_b1 = p.rpc; a.b_b1 = (long long)p.rpc * p.q_r; a.c_b1 = KK;
-        a.nb2 = p.nodes; a.a_b2 = p.v_node; a.b_b2 = p.q_node; a.c_b2 = p.x_node;
-        g1.push_back(a);
-        // X2 = T X1
-        GemmDesc t = gemm_desc(p.Tst + (long long)c0 * KK, K, 1, X1, kq, 1, X2, kq, 1, K, kq, K);
-        t.nb1 = cnt; t.a_b1 = KK; t.b_b1 = KK; t.c_b1 = KK;
-        t.nb2 = p.nodes; t.a_b2 = p.t_node; t.b_b2 = p.x_node; t.c_b2 = p.x_node;
-        g2.push_back(t);
-        // Q rows [0, kr) = W - Y[0:kr] X2  (unit-lower in (m,k))
-        GemmDesc top = gemm_desc(p.V + row0, 1, p.m, X2, kq, 1, qptr(p, row0), p.q_r, p.q_c, kr, kq, K, -1.0, 1.0);
-        top.a_tri = 1;
-        top.nb1 = cnt; top.a_b1 = p.rpc; top.b_b1 = KK; top.c_b1 = (long long)p.rpc * p.q_r;
-        top.nb2 = p.nodes; top.a_b2 = p.v_node; top.b_b2 = p.x_node; top.c_b2 = p.q_node;
-        g3.push_back(top);
-        if (rows > kr) {
-          // Q rows [kr, rows) = -Y[kr:rows] X2  (dense part of Y)
-          GemmDesc bot = gemm_desc(p.V + row0 + kr, 1, p.m, X2, kq, 1, qptr(p, row0 + kr), p.q_r, p.q_c, rows - kr,
-                                   kq, K, -1.0, 0.0);
-          bot.nb1 = cnt; bot.a_b1 = p.rpc; bot.b_b1 = KK; bot.c_b1 = (long long)p.rpc * p.q_r;
-          bot.nb2 = p.nodes; bot.a_b2 = p.v_node; bot.b_b2 = p.x_node; bot.c_b2 = p.q_node;
-          g3.push_back(bot);
-        }
-      };
-      if (last_rows == p.rpc) {
-        add_blocks(0, p.P, p.rpc);
-      } else {
-        add_blocks(0, p.P - 1, p.rpc);
-        add_blocks(p.P - 1, 1, last_rows);
-      }
-    }
-    HT_TRY(gemm_grouped(g1, stream, "gemm_qr_block"));
-    HT_TRY(gemm_grouped(g2, stream, "gemm_qr_block"));
-    HT_TRY(gemm_grouped(g3, stream, "gemm_qr_block"));
-  }
+  HT_TRY(launch(probs, kFactor, -1, stream));
+  for (int r = 0; r < rounds; ++r) HT_TRY(launch(probs, kFactor, r, stream));
+  HT_TRY(launch(probs, kFinalize, 0, stream));
+  for (int r = rounds - 1; r >= 0; --r) HT_TRY(launch(probs, kApply, r, stream));
+  HT_TRY(launch(probs, kApply, -1, stream));
   return kOk;
 }
 
