@@ -13,7 +13,7 @@ namespace {
 
 constexpr int ET = 512;
 constexpr int MAXD = 48;
-constexpr int MAX_SWEEPS = 60;
+constexpr int MAX_SWEEPS = 40;
 
 struct EigBatch {
   int count;
@@ -35,13 +35,17 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   const int K = e.K;
   const int n = K + (K & 1);
   const int ap = n + 1;
-  double* A = sm;
-  double* V = A + n * ap;
-  double* cs = V + n * ap;       // [n/2] c
-  double* sn = cs + n / 2;       // [n/2] s
-  double* tt = sn + n / 2;       // [n/2] t
-  int* pp = (int*)(tt + n / 2);  // [n/2] p
-  int* qq = pp + n / 2;          // [n/2] q
+  const int half = n / 2;
+  const int nblk = half * (half + 1) / 2;
+  const int vp_pitch = n + 2;      // even: 16-byte aligned rows for double2 rotations
+  double* A = sm;                  // n x ap, symmetric
+  double* Vt = A + ((n * ap + 1) & ~1);  // n x vp_pitch, rows = eigenvectors (V transposed)
+  double* cs = Vt + n * vp_pitch;  // [half]
+  double* sn = cs + half;
+  double* tt = sn + half;
+  int* pp = (int*)(tt + half);     // [half]
+  int* qq = pp + half;
+  unsigned short* blk = (unsigned short*)(qq + half);  // [nblk] packed (bi, bj), bi <= bj
   __shared__ double red[2];
   const int tid = threadIdx.x;
 
@@ -49,7 +53,14 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   for (int x = tid; x < n * n; x += blockDim.x) {
     const int i = x / n, j = x - i * n;
     A[i * ap + j] = (i < K && j < K) ? S[i * K + j] : 0.0;
-    V[i * ap + j] = (i == j) ? 1.0 : 0.0;
+    Vt[i * vp_pitch + j] = (i == j) ? 1.0 : 0.0;
+  }
+  const int tpp = max(1, (int)blockDim.x / half);  // threads per rotation pair in the V update
+  const int vk = tid / tpp, vsub = tid - vk * tpp;
+  for (int x = tid; x < nblk; x += blockDim.x) {
+    int bi = 0, rem = x;
+    while (rem >= half - bi) { rem -= half - bi; ++bi; }
+    blk[x] = (unsigned short)((bi << 8) | (bi + rem));
   }
   __syncthreads();
   // symmetry check (kernels.py:46-50), then symmetrise as eigh((S + S^T)/2)
@@ -82,8 +93,7 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   }
   __syncthreads();
 
-  const int half = n / 2;
-  const int nblk = half * (half + 1) / 2;
+  const double tol = 2.220446049250313e-16 * (double)max(K, 8);
   bool converged = false;
   for (int sweep = 0; sweep < MAX_SWEEPS; ++sweep) {
     int rotated = 0;
@@ -94,7 +104,9 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
         const double apq = A[p * ap + q];
         const double app = A[p * ap + p], aqq = A[q * ap + q];
         double c = 1.0, s = 0.0, t = 0.0;
-        if (fabs(apq) > 2.220446049250313e-16 * sqrt(fabs(app)) * sqrt(fabs(aqq)) && fabs(apq) > 1e-300) {
+        // relative (Demmel-Veselic) threshold tol * sqrt(a_pp a_qq), tol = K eps: the
+        // eigenvalue perturbation from the neglected a_pq is O(tol^2) relative
+        if (fabs(apq) > tol * sqrt(fabs(app)) * sqrt(fabs(aqq)) && fabs(apq) > 1e-300) {
           const double tau = (aqq - app) / (2.0 * apq);
           t = (tau >= 0.0 ? 1.0 : -1.0) / (fabs(tau) + sqrt(1.0 + tau * tau));
           c = 1.0 / sqrt(1.0 + t * t);
@@ -106,10 +118,8 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
       __syncthreads();
       // A' = J^T A J on the (pair_i, pair_j) 2x2 blocks, i <= j, mirrored
       for (int x = tid; x < nblk; x += blockDim.x) {
-        // decode upper-triangular block index x -> (bi, bj), bi <= bj
-        int bi = 0, rem = x;
-        while (rem >= half - bi) { rem -= half - bi; ++bi; }
-        const int bj = bi + rem;
+        const int code = blk[x];
+        const int bi = code >> 8, bj = code & 255;
         const double si = sn[bi], sj = sn[bj];
         if (si == 0.0 && sj == 0.0) continue;
         const int pi = pp[bi], qi = qq[bi];
@@ -134,16 +144,19 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
         A[qi * ap + pj] = z10; A[pj * ap + qi] = z10;
         A[qi * ap + qj] = z11; A[qj * ap + qi] = z11;
       }
-      // V <- V J
-      for (int x = tid; x < n * half; x += blockDim.x) {
-        const int k = x / n, i = x - k * n;
-        const double s = sn[k];
-        if (s == 0.0) continue;
-        const double c = cs[k];
-        const int p = pp[k], q = qq[k];
-        const double vp = V[i * ap + p], vq = V[i * ap + q];
-        V[i * ap + p] = c * vp - s * vq;
-        V[i * ap + q] = s * vp + c * vq;
+      // V <- V J: rotate rows p, q of V^T, two columns per thread-iteration (16-byte)
+      if (vk < half) {
+        const double s = sn[vk];
+        if (s != 0.0) {
+          const double c = cs[vk];
+          double2* vp = reinterpret_cast<double2*>(Vt + pp[vk] * vp_pitch);
+          double2* vq = reinterpret_cast<double2*>(Vt + qq[vk] * vp_pitch);
+          for (int i = vsub; i < n / 2; i += tpp) {
+            const double2 a0 = vp[i], b0 = vq[i];
+            vp[i] = make_double2(c * a0.x - s * b0.x, c * a0.y - s * b0.y);
+            vq[i] = make_double2(s * a0.x + c * b0.x, s * a0.y + c * b0.y);
+          }
+        }
       }
       __syncthreads();
     }
@@ -157,7 +170,8 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   // stable descending order by eigenvalue, clamp >= 0 (kernels.py:51-53)
   double* lam = e.lam + nd * e.l_node;
   double* Vo = e.V + nd * e.v_node;
-  double* lsorted = cs;  // reuse (needs K <= n/2*3 doubles: cs,sn,tt are contiguous)
+  double* lsorted = cs;  // reuse (cs, sn, tt are contiguous: 3*half >= K doubles)
+  int* perm = pp;        // pp, qq contiguous: 2*half >= K ints
   for (int i = tid; i < K; i += blockDim.x) {
     const double li = A[i * ap + i];
     int pos = 0;
@@ -168,7 +182,12 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
     const double lc = fmax(li, 0.0);
     lam[pos] = lc;
     lsorted[pos] = lc;
-    for (int row = 0; row < K; ++row) Vo[(long long)row * K + pos] = V[row * ap + i];
+    perm[pos] = i;
+  }
+  __syncthreads();
+  for (int x = tid; x < K * K; x += blockDim.x) {
+    const int row = x / K, pos = x - row * K;
+    Vo[(long long)row * K + pos] = Vt[perm[pos] * vp_pitch + row];
   }
   __syncthreads();
   if (tid == 0 && e.rank) {
@@ -192,7 +211,9 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
 
 size_t smem_bytes(int K) {
   const int n = K + (K & 1);
-  return (size_t)(2 * n * (n + 1) + 3 * (n / 2)) * sizeof(double) + (size_t)2 * (n / 2) * sizeof(int) + 16;
+  const int half = n / 2;
+  return (size_t)(n * (n + 1) + 1 + n * (n + 2) + 3 * half) * sizeof(double) + (size_t)2 * half * sizeof(int) +
+         (size_t)(half * (half + 1) / 2) * sizeof(unsigned short) + 64;
 }
 
 bool g_attr = false;
