@@ -241,11 +241,12 @@ int plan_qrs(std::vector<QrProblem>& qs, Arena& ar) {
   return kOk;
 }
 
-// split-K count so a level's reduction GEMMs fill the GPU
+// split-K count so a level's reduction GEMMs fill the GPU (>= ~2 CTAs per SM, each
+// split keeping >= 4 k-tiles)
 int pick_splits(long long tiles_total, long long reduction) {
   long long s = std::max<long long>(1, (2 * kSMs + tiles_total - 1) / std::max<long long>(1, tiles_total));
-  s = std::min<long long>(s, std::max<long long>(1, reduction / (kGemmBK * 8)));
-  return (int)std::min<long long>(s, 64);
+  s = std::min<long long>(s, std::max<long long>(1, reduction / (kGemmBK * 4)));
+  return (int)std::min<long long>(s, 160);
 }
 
 // ---------------------------------------------------------------------------
@@ -384,7 +385,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     long long tiles = 0;
     for (int t : inner) {
       const long long k1 = o.k[T.son1[t]], k2 = o.k[T.son2[t]];
-      tiles += (long long)ceil_div(k1, kGemmBM) * ceil_div(k1, kGemmBN) + (long long)ceil_div(k2, kGemmBM) * ceil_div(k2, kGemmBN);
+      tiles += (long long)gemm_tiles((int)k1, (int)k1) + gemm_tiles((int)k2, (int)k2);
     }
     std::vector<double*> t1s(T.nn, nullptr);
     for (int t : inner) t1s[t] = scratch_ar.take(o.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
@@ -666,7 +667,7 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
     std::vector<GemmDesc> gl, g1, g2, g3;
     std::vector<ReduceDesc> rs;
     long long tiles = 0;
-    for (int t : T.levels[l]) tiles += (long long)ceil_div(a.k[t], kGemmBM) * ceil_div(c.k[t], kGemmBN);
+    for (int t : T.levels[l]) tiles += (long long)gemm_tiles((int)a.k[t], (int)c.k[t]);
     std::vector<double*> S1s(T.nn, nullptr), S2s(T.nn, nullptr);
     for (int t : T.levels[l])
       if (!T.leaf(t)) S1s[t] = ar.take(a.k[t] * a.k[T.son2[t]] * c.k[T.son1[t]]);

@@ -1,7 +1,11 @@
-// Grouped FP64 DMMA GEMM (see gemm.cuh).  64x64x16 CTA tile, 8 warps each
-// owning a 32x16 sub-tile as 4x2 mma.sync.m8n8k4.f64 fragments; operands are
-// staged k-major in shared memory (pitch 68 doubles: conflict-free fragment
-// loads), double-buffered with a register prefetch of the next k-tile.
+// Grouped FP64 DMMA GEMM (see gemm.cuh).
+//
+// CTA tiles are shaped for the HT contractions, whose short dimension is a rank
+// (K ~ 100, r ~ 50): 128x104 / 104x128 cover a 100-wide side in one tile
+// (96% useful), 128x56 / 56x128 a 50-wide side, 64x64 everything else.  8 warps,
+// each owning WM x WN mma.sync.m8n8k4.f64 fragments; operands are staged k-major
+// in shared memory (pitch = 4 mod 16 doubles: conflict-free fragment loads)
+// through a 3-stage cp.async pipeline with zero-fill for the ragged edges.
 #include <algorithm>
 
 #include "gemm.cuh"
@@ -11,10 +15,11 @@ namespace ht {
 
 namespace {
 
-constexpr int BM = kGemmBM, BN = kGemmBN, BK = kGemmBK;
-constexpr int PITCH = 68;  // 64 + 4: k-rows land in disjoint 8-byte bank groups
+constexpr int BK = kGemmBK;  // 16
 constexpr int THREADS = 256;
-constexpr int PER_THREAD = BM * BK / THREADS;  // 4
+constexpr int STAGES = 3;
+
+__host__ __device__ constexpr int pitch16(int x) { return ((x + 15) / 16) * 16 + 4; }
 
 struct GemmBatch {
   int count;
@@ -27,9 +32,82 @@ struct ReduceBatch {
   ReduceDesc d[kMaxGemmDescs];
 };
 
-__global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_constant__ GemmBatch batch) {
-  __shared__ __align__(16) double As[2][BK][PITCH];
-  __shared__ __align__(16) double Bs[2][BK][PITCH];
+__device__ __forceinline__ void cp8(double* smem, const double* gmem) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp8z(double* smem, const double* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+// Operand fetch with masks (implicit unit-triangular Householder factors, identity).
+// Returns the global address to copy from, or null with the constant in `val`.
+// (o0, k0): decomposition of the tile's first reduction index f0 = o0*K + k0; within a
+// 16-wide tile the outer index advances at most once when K >= 16 (else: divide).
+__device__ __forceinline__ void split_f(const GemmDesc& g, long long f0, int kk, long long& o, long long& k) {
+  if (g.KO == 1) {
+    o = 0;
+    k = f0 + kk;
+  } else if (g.K >= 16) {
+    const long long o0 = f0 / g.K;
+    k = f0 - o0 * g.K + kk;
+    o = o0;
+    if (k >= g.K) {
+      k -= g.K;
+      ++o;
+    }
+  } else {
+    o = (f0 + kk) / g.K;
+    k = f0 + kk - o * g.K;
+  }
+}
+
+__device__ __forceinline__ const double* a_src(const GemmDesc& g, const double* A, int m, long long f0, int kk,
+                                               long long k_end, double& val) {
+  val = 0.0;
+  if (m >= g.M || f0 + kk >= k_end) return nullptr;
+  long long o, k;
+  split_f(g, f0, kk, o, k);
+  if (g.a_tri == 3) {
+    val = (m == k) ? 1.0 : 0.0;
+    return nullptr;
+  }
+  if (g.a_tri == 1 || g.a_tri == 2) {
+    const bool stored = g.a_tri == 1 ? (m > k) : (k > m);
+    if (!stored) {
+      val = (m == k) ? 1.0 : 0.0;
+      return nullptr;
+    }
+  }
+  return A + m * g.a_m + k * g.a_k + o * g.a_o;
+}
+
+__device__ __forceinline__ const double* b_src(const GemmDesc& g, const double* B, int n, long long f0, int kk,
+                                               long long k_end, double& val) {
+  val = 0.0;
+  if (n >= g.N || f0 + kk >= k_end) return nullptr;
+  long long o, k;
+  split_f(g, f0, kk, o, k);
+  if (g.b_tri == 1 && k <= n) {
+    val = (k == n) ? 1.0 : 0.0;
+    return nullptr;
+  }
+  return B + k * g.b_k + n * g.b_n + o * g.b_o;
+}
+
+template <int WM, int WN, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant__ GemmBatch batch) {
+  constexpr int BM = 8 * WM * WARPS_M, BN = 8 * WN * WARPS_N;
+  constexpr int PA = pitch16(BM), PB = pitch16(BN);
+  extern __shared__ __align__(16) double smem[];
+  double* As = smem;                     // [STAGES][BK][PA]
+  double* Bs = smem + STAGES * BK * PA;  // [STAGES][BK][PB]
 
   int di = 0;
   while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
@@ -43,7 +121,6 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_cons
   const int split = local % g.splits;
   const int b = local / g.splits;
   const int b1 = b % g.nb1, b2 = b / g.nb1;
-
   const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
   const double* Bp = g.B + b1 * g.b_b1 + b2 * g.b_b2;
 
@@ -54,110 +131,152 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_cons
   const long long k_end = min(L, k_begin + per_split);
   const int ntiles = k_end > k_begin ? (int)((k_end - k_begin + BK - 1) / BK) : 0;
 
-  const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-  const int wm = warp >> 2, wn = warp & 3;  // 2 x 4 warps, each 32 x 16
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp / WARPS_N, wn = warp % WARPS_N;
+  const bool a_kc = (g.a_k == 1), b_kc = (g.b_k == 1);
 
-  const bool a_kc = (g.a_k == 1);
-  const bool b_kc = (g.b_k == 1);
-
-  double ra[PER_THREAD], rb[PER_THREAD];
-
-  auto load = [&](int t) {
+  // Fast path (plain operands; two-level reductions with K >= 16): every thread copies
+  // fixed tile slots; per k-tile only the (outer, inner) reduction offset changes.
+  constexpr int NA = (BM * BK + THREADS - 1) / THREADS, NBB = (BN * BK + THREADS - 1) / THREADS;
+  const bool fast = g.a_tri == 0 && g.b_tri == 0 && (g.KO == 1 || g.K >= BK);
+  const double* pa[NA];
+  const double* pb[NBB];
+  int oa[NA], ob[NBB], ka[NA], kb[NBB];
+  if (fast) {
 #pragma unroll
-    for (int q = 0; q < PER_THREAD; ++q) {
+    for (int q = 0; q < NA; ++q) {
       const int e = tid + q * THREADS;
-      {
-        const int kk = a_kc ? (e & (BK - 1)) : (e >> 6);
-        const int mm = a_kc ? (e >> 4) : (e & (BM - 1));
-        const long long f = k_begin + (long long)t * BK + kk;
-        const int m = m0 + mm;
-        double v = 0.0;
-        if (m < g.M && f < k_end) {
-          long long o = 0, k = f;
-          if (g.KO > 1) { o = f / g.K; k = f - o * g.K; }
-          if (g.a_tri == 0) {
-            v = __ldg(A + m * g.a_m + k * g.a_k + o * g.a_o);
-          } else if (g.a_tri == 3) {
-            v = (m == k) ? 1.0 : 0.0;
-          } else {
-            // implicit unit-diagonal Householder vectors (compact-WY Y factor)
-            const bool stored = g.a_tri == 1 ? (m > k) : (k > m);
-            v = stored ? __ldg(A + m * g.a_m + k * g.a_k + o * g.a_o) : (m == k ? 1.0 : 0.0);
-          }
-        }
-        ra[q] = v;
-      }
-      {
-        const int kk = b_kc ? (e & (BK - 1)) : (e >> 6);
-        const int nn = b_kc ? (e >> 4) : (e & (BN - 1));
-        const long long f = k_begin + (long long)t * BK + kk;
-        const int n = n0 + nn;
-        double v = 0.0;
-        if (n < g.N && f < k_end) {
-          long long o = 0, k = f;
-          if (g.KO > 1) { o = f / g.K; k = f - o * g.K; }
-          if (g.b_tri == 0 || k > n) v = __ldg(Bp + k * g.b_k + n * g.b_n + o * g.b_o);
-          else v = (k == n) ? 1.0 : 0.0;
-        }
-        rb[q] = v;
-      }
+      const int kk = a_kc ? (e % BK) : (e / BM);
+      const int mm = a_kc ? (e / BK) : (e % BM);
+      const bool ok = e < BM * BK && m0 + mm < g.M;
+      oa[q] = ok ? kk * PA + mm : -1;
+      ka[q] = kk;
+      pa[q] = A + (long long)(ok ? m0 + mm : 0) * g.a_m;
     }
-  };
-  auto store = [&](int buf) {
 #pragma unroll
-    for (int q = 0; q < PER_THREAD; ++q) {
+    for (int q = 0; q < NBB; ++q) {
       const int e = tid + q * THREADS;
-      const int akk = a_kc ? (e & (BK - 1)) : (e >> 6);
-      const int amm = a_kc ? (e >> 4) : (e & (BM - 1));
-      As[buf][akk][amm] = ra[q];
-      const int bkk = b_kc ? (e & (BK - 1)) : (e >> 6);
-      const int bnn = b_kc ? (e >> 4) : (e & (BN - 1));
-      Bs[buf][bkk][bnn] = rb[q];
+      const int kk = b_kc ? (e % BK) : (e / BN);
+      const int nn = b_kc ? (e / BK) : (e % BN);
+      const bool ok = e < BN * BK && n0 + nn < g.N;
+      ob[q] = ok ? kk * PB + nn : -1;
+      kb[q] = kk;
+      pb[q] = Bp + (long long)(ok ? n0 + nn : 0) * g.b_n;
     }
-  };
-
-  double acc[4][2][2];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-  if (ntiles > 0) {
-    load(0);
-    store(0);
   }
-  __syncthreads();
+
+  auto load_tile = [&](int t, int stage) {
+    double* as = As + stage * BK * PA;
+    double* bs = Bs + stage * BK * PB;
+    const long long fb = k_begin + (long long)t * BK;
+    if (fast) {
+      const long long krem = k_end - fb;
+      long long o0 = 0, k0 = fb;
+      if (g.KO > 1) {
+        o0 = fb / g.K;
+        k0 = fb - o0 * g.K;
+      }
+#pragma unroll
+      for (int q = 0; q < NA; ++q) {
+        if (oa[q] >= 0) {
+          const bool ok = ka[q] < krem;
+          long long k = k0 + ka[q], o = o0;
+          if (k >= g.K) {
+            k -= g.K;
+            ++o;
+          }
+          cp8z(as + oa[q], ok ? pa[q] + k * g.a_k + o * g.a_o : A, ok);
+        } else if (tid + q * THREADS < BM * BK) {
+          const int e = tid + q * THREADS;
+          as[(a_kc ? (e % BK) : (e / BM)) * PA + (a_kc ? (e / BK) : (e % BM))] = 0.0;
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NBB; ++q) {
+        if (ob[q] >= 0) {
+          const bool ok = kb[q] < krem;
+          long long k = k0 + kb[q], o = o0;
+          if (k >= g.K) {
+            k -= g.K;
+            ++o;
+          }
+          cp8z(bs + ob[q], ok ? pb[q] + k * g.b_k + o * g.b_o : Bp, ok);
+        } else if (tid + q * THREADS < BN * BK) {
+          const int e = tid + q * THREADS;
+          bs[(b_kc ? (e % BK) : (e / BN)) * PB + (b_kc ? (e / BK) : (e % BN))] = 0.0;
+        }
+      }
+      return;
+    }
+    for (int e = tid; e < BM * BK; e += THREADS) {
+      const int kk = a_kc ? (e % BK) : (e / BM);
+      const int mm = a_kc ? (e / BK) : (e % BM);
+      double v;
+      const double* src = a_src(g, A, m0 + mm, fb, kk, k_end, v);
+      double* dst = as + kk * PA + mm;
+      if (src) cp8(dst, src);
+      else *dst = v;
+    }
+    for (int e = tid; e < BN * BK; e += THREADS) {
+      const int kk = b_kc ? (e % BK) : (e / BN);
+      const int nn = b_kc ? (e / BK) : (e % BN);
+      double v;
+      const double* src = b_src(g, Bp, n0 + nn, fb, kk, k_end, v);
+      double* dst = bs + kk * PB + nn;
+      if (src) cp8(dst, src);
+      else *dst = v;
+    }
+  };
+
+  double acc[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; ++i)
+#pragma unroll
+    for (int j = 0; j < WN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < ntiles) load_tile(s, s);
+    cp_commit();
+  }
+  const int ar = wm * WM * 8 + (lane >> 2);
+  const int br = wn * WN * 8 + (lane >> 2);
   for (int t = 0; t < ntiles; ++t) {
-    const int buf = t & 1;
-    if (t + 1 < ntiles) load(t + 1);
+    cp_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = t + STAGES - 1;
+      if (nt < ntiles) load_tile(nt, nt % STAGES);
+      cp_commit();
+    }
+    const double* as = As + (t % STAGES) * BK * PA;
+    const double* bs = Bs + (t % STAGES) * BK * PB;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
-      double af[4], bf[2];
+      const int kr = ks + (lane & 3);
+      double af[WM], bf[WN];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) af[i] = As[buf][ks + (lane & 3)][wm * 32 + i * 8 + (lane >> 2)];
+      for (int i = 0; i < WM; ++i) af[i] = as[kr * PA + ar + i * 8];
 #pragma unroll
-      for (int j = 0; j < 2; ++j) bf[j] = Bs[buf][ks + (lane & 3)][wn * 16 + j * 8 + (lane >> 2)];
+      for (int j = 0; j < WN; ++j) bf[j] = bs[kr * PB + br + j * 8];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < WM; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
+        for (int j = 0; j < WN; ++j) dmma_8x8x4(acc[i][j], af[i], bf[j]);
     }
-    if (t + 1 < ntiles) store(buf ^ 1);
-    __syncthreads();
   }
+  cp_wait<0>();
 
-  // epilogue
   if (g.splits == 1) {
     double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < WM; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < WN; ++j)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
-          const int n = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + v;
+          const int m = m0 + wm * WM * 8 + i * 8 + (lane >> 2);
+          const int n = n0 + wn * WN * 8 + j * 8 + 2 * (lane & 3) + v;
           if (m < g.M && n < g.N) {
             double* p = C + m * g.c_m + n * g.c_n;
             double r = g.alpha * acc[i][j][v];
@@ -169,13 +288,13 @@ __global__ void __launch_bounds__(THREADS, 2) gemm_dmma_kernel(const __grid_cons
     const long long nbatch = (long long)g.nb1 * g.nb2;
     double* P = g.C + ((long long)split * nbatch + b) * g.M * g.N;
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < WM; ++i)
 #pragma unroll
-      for (int j = 0; j < 2; ++j)
+      for (int j = 0; j < WN; ++j)
 #pragma unroll
         for (int v = 0; v < 2; ++v) {
-          const int m = m0 + wm * 32 + i * 8 + (lane >> 2);
-          const int n = n0 + wn * 16 + j * 8 + 2 * (lane & 3) + v;
+          const int m = m0 + wm * WM * 8 + i * 8 + (lane >> 2);
+          const int n = n0 + wn * WN * 8 + j * 8 + 2 * (lane & 3) + v;
           if (m < g.M && n < g.N) P[(long long)m * g.N + n] = acc[i][j][v];
         }
   }
@@ -209,42 +328,96 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
   }
 }
 
+// ---- tile configurations ----
+enum Cfg { kC64, kCN104, kCM104, kCN56, kCM56, kNumCfg };
+
+struct CfgInfo {
+  int bm, bn;
+};
+constexpr CfgInfo kCfg[kNumCfg] = {{64, 64}, {128, 104}, {104, 128}, {128, 56}, {56, 128}};
+
+Cfg pick_cfg(const GemmDesc& d) {
+  if (d.N <= 56 && d.M > 56) return kCN56;
+  if (d.M <= 56 && d.N > 56) return kCM56;
+  if (d.N <= 104 && d.M > 104) return kCN104;
+  if (d.M <= 104 && d.N > 104) return kCM104;
+  if (d.M <= 64 && d.N <= 64) return kC64;
+  if (d.N <= 104 && d.M <= 104) return d.N >= d.M ? kCM104 : kCN104;
+  return kCN104;
+}
+
+size_t smem_for(Cfg c) { return (size_t)STAGES * BK * (pitch16(kCfg[c].bm) + pitch16(kCfg[c].bn)) * sizeof(double); }
+
+template <int WM, int WN, int WMW, int WNW>
+int launch_cfg(GemmBatch& batch, int blocks, size_t smem, cudaStream_t stream) {
+  static bool attr = false;
+  if (!attr) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(gemm_kernel<WM, WN, WMW, WNW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+    attr = true;
+  }
+  gemm_kernel<WM, WN, WMW, WNW><<<blocks, THREADS, smem, stream>>>(batch);
+  HT_LAUNCH_CHECK();
+  return kOk;
+}
+
+int launch_batch(Cfg c, GemmBatch& batch, int blocks, cudaStream_t stream) {
+  const size_t smem = smem_for(c);
+  switch (c) {
+    case kC64: return launch_cfg<4, 2, 2, 4>(batch, blocks, smem, stream);     // 64 x 64
+    case kCN104: return launch_cfg<2, 13, 8, 1>(batch, blocks, smem, stream);  // 128 x 104
+    case kCM104: return launch_cfg<13, 2, 1, 8>(batch, blocks, smem, stream);  // 104 x 128
+    case kCN56: return launch_cfg<2, 7, 8, 1>(batch, blocks, smem, stream);    // 128 x 56
+    case kCM56: return launch_cfg<7, 2, 1, 8>(batch, blocks, smem, stream);    // 56 x 128
+    default: break;
+  }
+  set_error("gemm: bad tile config");
+  return kErrArgument;
+}
+
 }  // namespace
 
+int gemm_tiles(int M, int N) {
+  GemmDesc d{};
+  d.M = M;
+  d.N = N;
+  const Cfg c = pick_cfg(d);
+  return ceil_div(M, kCfg[c].bm) * ceil_div(N, kCfg[c].bn);
+}
+
 int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag) {
-  size_t i = 0;
-  while (i < descs.size()) {
-    GemmBatch batch;
-    batch.count = 0;
-    int blocks = 0;
-    while (i < descs.size() && batch.count < kMaxGemmDescs) {
-      GemmDesc d = descs[i++];
-      if (d.M <= 0 || d.N <= 0 || d.nb1 <= 0 || d.nb2 <= 0) continue;
-      if (d.splits < 1) d.splits = 1;
-      if (d.KO < 1) d.KO = 1;
-      d.tiles_m = ceil_div(d.M, BM);
-      d.tiles_n = ceil_div(d.N, BN);
-      d.block_begin = blocks;
-      long long nb = (long long)d.tiles_m * d.tiles_n * d.splits * d.nb1 * d.nb2;
-      if (nb > (1LL << 30)) {
-        set_error("gemm_grouped: grid too large");
-        return kErrArgument;
+  for (int c = 0; c < kNumCfg; ++c) {
+    size_t i = 0;
+    while (i < descs.size()) {
+      GemmBatch batch;
+      batch.count = 0;
+      int blocks = 0;
+      double flops = 0, bytes = 0;
+      while (i < descs.size() && batch.count < kMaxGemmDescs) {
+        GemmDesc d = descs[i++];
+        if (d.M <= 0 || d.N <= 0 || d.nb1 <= 0 || d.nb2 <= 0) continue;
+        if (pick_cfg(d) != (Cfg)c) continue;
+        if (d.splits < 1) d.splits = 1;
+        if (d.KO < 1) d.KO = 1;
+        d.tiles_m = ceil_div(d.M, kCfg[c].bm);
+        d.tiles_n = ceil_div(d.N, kCfg[c].bn);
+        d.block_begin = blocks;
+        const long long nb = (long long)d.tiles_m * d.tiles_n * d.splits * d.nb1 * d.nb2;
+        if (nb > (1LL << 30)) {
+          set_error("gemm_grouped: grid too large");
+          return kErrArgument;
+        }
+        blocks += (int)nb;
+        const double nbt = (double)d.nb1 * d.nb2;
+        flops += 2.0 * d.M * d.N * (double)d.K * d.KO * nbt;
+        bytes += 8.0 * nbt * ((double)d.M * d.K * d.KO + (double)d.K * d.KO * d.N + (double)d.M * d.N * d.splits);
+        batch.d[batch.count++] = d;
       }
-      blocks += (int)nb;
-      batch.d[batch.count++] = d;
+      if (batch.count == 0) continue;
+      ProfToken tok = prof_begin(stream);
+      HT_TRY(launch_batch((Cfg)c, batch, blocks, stream));
+      prof_end(tok, tag, stream, flops, bytes);
     }
-    if (batch.count == 0) continue;
-    double flops = 0, bytes = 0;
-    for (int q = 0; q < batch.count; ++q) {
-      const GemmDesc& d = batch.d[q];
-      const double nb = (double)d.nb1 * d.nb2;
-      flops += 2.0 * d.M * d.N * (double)d.K * d.KO * nb;
-      bytes += 8.0 * nb * ((double)d.M * d.K * d.KO + (double)d.K * d.KO * d.N + (double)d.M * d.N * d.splits);
-    }
-    ProfToken tok = prof_begin(stream);
-    gemm_dmma_kernel<<<blocks, THREADS, 0, stream>>>(batch);
-    HT_LAUNCH_CHECK();
-    prof_end(tok, tag, stream, flops, bytes);
   }
   return kOk;
 }

@@ -44,6 +44,8 @@ struct ReduceDesc {
 
 // Launch a set of GEMMs (any number; split into launches of <= kMaxGemmDescs).
 int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag = "gemm_dmma");
+// CTA tiles one M x N output uses (tile shape chosen per descriptor)
+int gemm_tiles(int M, int N);
 int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, const char* tag = "reduce_partials");
 
 constexpr int kMaxGemmDescs = 48;
