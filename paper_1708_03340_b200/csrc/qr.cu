@@ -237,16 +237,17 @@ __device__ void panel_factor(double* S, int ps, int nrows, int j0, int nbp, doub
 // unit diagonal and zeros above it in the DENSE case).
 template <bool DENSE>
 __device__ __forceinline__ void stage_panel_v(const double* S, int ps, int nrows, int j0, int nbp, double* Vp) {
-  for (int e = threadIdx.x; e < NB * ps; e += blockDim.x) {
-    const int r = e / ps, row = e - r * ps;
-    double v = 0.0;
-    if (r < nbp && row < nrows) {
-      const int col = j0 + r;
-      if (!DENSE || row > col) v = S[col * ps + row];
-      else if (row == col) v = 1.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int r = warp; r < NB; r += nw)
+    for (int row = lane; row < ps; row += kWarp) {
+      double v = 0.0;
+      if (r < nbp && row < nrows) {
+        const int col = j0 + r;
+        if (!DENSE || row > col) v = S[col * ps + row];
+        else if (row == col) v = 1.0;
+      }
+      Vp[r * ps + row] = v;
     }
-    Vp[e] = v;
-  }
 }
 
 // W (8 x nt) = [R head rows] + Vp^T C,  C = S[:, c0:c0+nt]  (all operands zero padded)
@@ -308,7 +309,7 @@ __device__ void trailing_update(double* S, int ps, int nrows, int K, int j0, int
   // W2 = -(T^T W)  (T upper triangular: (T^T W)[r][c] = sum_{l<=r} T[l][r] W[l][c]); TRI: R heads -= T^T W
   const int ntp = (nt + 7) & ~7;
   for (int e = threadIdx.x; e < NB * ntp; e += blockDim.x) {
-    const int r = e / ntp, c = e - r * ntp;
+    const int r = e & (NB - 1), c = e >> 3;
     double acc = 0.0;
     if (r < nbp && c < nt) {
       for (int l = 0; l <= r; ++l) acc = fma(Tp[l * NB + r], W[l * pw + c], acc);
@@ -382,6 +383,7 @@ __global__ void __launch_bounds__(QTF, 1) qr_factor_kernel(const __grid_constant
   const int nd = local / q.per_node, k = local % q.per_node;
   const int K = q.K;
   const int np = npanels(K);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double* Rst = q.Rst + nd * q.st_node;
   double* Tpg = q.Tp + nd * q.tp_node;
   double* taug = q.tau + nd * q.tau_node;
@@ -394,23 +396,23 @@ __global__ void __launch_bounds__(QTF, 1) qr_factor_kernel(const __grid_constant
     FactorSmem f = carve_factor(sm, K, true, BR);
     const double* A = q.A + nd * q.a_node;
     // column-major smem block; global loads coalesced along rows for column-major A
-    for (int e = threadIdx.x; e < (pad8(K) + 8) * f.ps; e += blockDim.x) {
-      const int col = e / f.ps, row = e - col * f.ps;
-      const bool ok = row < rows && col < K;
-      cp_async8(f.S + e, ok ? A + (long long)(row0 + row) * q.a_r + (long long)col * q.a_c : A, ok);
-    }
+    for (int col = warp; col < pad8(K) + 8; col += nwarps)
+      for (int row = lane; row < f.ps; row += kWarp) {
+        const bool ok = row < rows && col < K;
+        cp_async8(f.S + col * f.ps + row, ok ? A + (long long)(row0 + row) * q.a_r + (long long)col * q.a_c : A, ok);
+      }
     cp_async_wait_all();
     __syncthreads();
     factor_step<true>(f.S, f.ps, rows, K, nrefl, f.R, f.rp, f.taus, f.W, f.W2, f.pw, f.Gs, f.Tp,
                       Tpg + (long long)c * np * NB * NB, f.Vp);
     double* V = q.V + nd * q.v_node;
     double* Rc = Rst + (long long)c * K * K;
-    for (int e = threadIdx.x; e < K * BR; e += blockDim.x) {
-      const int col = e / BR, row = e - col * BR;
-      const double v = f.S[col * f.ps + row];
-      if (row < rows) V[(long long)col * q.m + row0 + row] = v;
-      if (row < K) Rc[(long long)row * K + col] = (row < nrefl && col >= row) ? v : 0.0;
-    }
+    for (int col = warp; col < K; col += nwarps)
+      for (int row = lane; row < BR; row += kWarp) {
+        const double v = f.S[col * f.ps + row];
+        if (row < rows) V[(long long)col * q.m + row0 + row] = v;
+        if (row < K) Rc[(long long)row * K + col] = (row < nrefl && col >= row) ? v : 0.0;
+      }
     for (int j = threadIdx.x; j < K; j += blockDim.x) taug[(long long)c * K + j] = j < nrefl ? f.taus[j] : 0.0;
   } else {
     const int r = b.round;
@@ -418,22 +420,18 @@ __global__ void __launch_bounds__(QTF, 1) qr_factor_kernel(const __grid_constant
     FactorSmem f = carve_factor(sm, K, false, K);
     double* Ra = Rst + (long long)ia * K * K;
     double* Rb = Rst + (long long)ib * K * K;
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int i = e / K, col = e - i * K;
-      f.R[i * f.rp + col] = Ra[e];
-    }
-    for (int e = threadIdx.x; e < pad8(K) * f.ps; e += blockDim.x) {
-      const int col = e / f.ps, i = e - col * f.ps;
-      f.S[e] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
-    }
+    for (int i = warp; i < K; i += nwarps)
+      for (int col = lane; col < K; col += kWarp) f.R[i * f.rp + col] = Ra[i * K + col];
+    for (int col = warp; col < pad8(K); col += nwarps)
+      for (int i = lane; i < f.ps; i += kWarp)
+        f.S[col * f.ps + i] = (i < K && col < K) ? Rb[(long long)i * K + col] : 0.0;
     __syncthreads();
     factor_step<false>(f.S, f.ps, K, K, K, f.R, f.rp, f.taus, f.W, f.W2, f.pw, f.Gs, f.Tp,
                        Tpg + (long long)(q.P + ib) * np * NB * NB, f.Vp);
-    for (int e = threadIdx.x; e < K * K; e += blockDim.x) {
-      const int i = e / K, col = e - i * K;
-      Ra[e] = f.R[i * f.rp + col];
-      Rb[(long long)col * K + i] = f.S[col * f.ps + i];  // reflector tails, column-major
-    }
+    for (int i = warp; i < K; i += nwarps)
+      for (int col = lane; col < K; col += kWarp) Ra[i * K + col] = f.R[i * f.rp + col];
+    for (int col = warp; col < K; col += nwarps)
+      for (int i = lane; i < K; i += kWarp) Rb[(long long)col * K + i] = f.S[col * f.ps + i];  // tails
     for (int j = threadIdx.x; j < K; j += blockDim.x) taug[(long long)(q.P + ib) * K + j] = f.taus[j];
   }
 }
@@ -457,7 +455,7 @@ __device__ __forceinline__ void apply_t(const double* Ts, const double* W, doubl
                                         double* Hh, int ph) {
   const int ntp = (ncols + 7) & ~7;
   for (int e = threadIdx.x; e < NB * ntp; e += blockDim.x) {
-    const int r = e / ntp, c = e - r * ntp;
+    const int r = e & (NB - 1), c = e >> 3;
     double acc = 0.0;
     if (r < nbp && c < ncols) {
       for (int l = r; l < nbp; ++l) acc = fma(Ts[r * NB + l], W[l * pw + c], acc);
@@ -473,15 +471,18 @@ __device__ void apply_step(double* C, int pc, double* H, int ph, int nrows, int 
   for (int p = npanels(nrefl) - 1; p >= 0; --p) {
     const int j0 = p * NB, nbp = min(NB, nrefl - j0);
     const int prow = DENSE ? nrows : min(nrows, j0 + nbp);  // TRI: tails only in rows < j0 + nbp
-    for (int e = threadIdx.x; e < NB * pc; e += blockDim.x) {
-      const int r = e / pc, row = e - r * pc;
-      double v = 0.0;
-      if (r < nbp && row < prow) {
-        const int col = j0 + r;
-        if (!DENSE || row > col) v = Vg[(long long)col * v_ld + row];
-        else if (row == col) v = 1.0;
-      }
-      Vs[e] = v;
+    {
+      const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+      for (int r = warp; r < NB; r += nw)
+        for (int row = lane; row < pc; row += kWarp) {
+          double v = 0.0;
+          if (r < nbp && row < prow) {
+            const int col = j0 + r;
+            if (!DENSE || row > col) v = Vg[(long long)col * v_ld + row];
+            else if (row == col) v = 1.0;
+          }
+          Vs[r * pc + row] = v;
+        }
     }
     for (int e = threadIdx.x; e < NB * NB; e += blockDim.x) Ts[e] = Tpg[p * NB * NB + e];
     __syncthreads();
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(QT, 1) qr_apply_kernel(const __grid_constant__
   const int K = q.K, kq = min(q.m, K);
   const int np = npanels(K);
   const int pw = pitch_rows(pad8(K));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   double* Q = q.Q + nd * q.q_node;
   const double* Tpg = q.Tp + nd * q.tp_node;
   if (b.round < 0) {
@@ -516,19 +518,18 @@ __global__ void __launch_bounds__(QT, 1) qr_apply_kernel(const __grid_constant__
     double* W = Vs + NB * pc;
     double* W2 = W + NB * pw;
     double* Ts = W2 + NB * pw;
-    for (int e = threadIdx.x; e < (pad8(K) + 8) * pc; e += blockDim.x) {
-      const int col = e / pc, row = e - col * pc;
-      const bool ok = row < kr && col < kq;
-      cp_async8(C + e, ok ? Q + (long long)(row0 + row) * q.q_r + (long long)col * q.q_c : Q, ok);
-    }
+    for (int col = warp; col < pad8(K) + 8; col += nwarps)
+      for (int row = lane; row < pc; row += kWarp) {
+        const bool ok = row < kr && col < kq;
+        cp_async8(C + col * pc + row, ok ? Q + (long long)(row0 + row) * q.q_r + (long long)col * q.q_c : Q, ok);
+      }
     cp_async_wait_all();
     __syncthreads();
     apply_step<true>(C, pc, nullptr, 0, rows, kq, nrefl, q.V + nd * q.v_node + row0, q.m,
                      Tpg + (long long)c * np * NB * NB, Vs, W, W2, pw, Ts);
-    for (int e = threadIdx.x; e < kq * pc; e += blockDim.x) {
-      const int col = e / pc, row = e - col * pc;
-      if (row < rows) Q[(long long)(row0 + row) * q.q_r + (long long)col * q.q_c] = C[e];
-    }
+    for (int col = warp; col < kq; col += nwarps)
+      for (int row = lane; row < rows; row += kWarp)
+        Q[(long long)(row0 + row) * q.q_r + (long long)col * q.q_c] = C[col * pc + row];
   } else {
     const int r = b.round;
     const int ia = k << (r + 1), ib = ia + (1 << r);
@@ -542,24 +543,20 @@ __global__ void __launch_bounds__(QT, 1) qr_apply_kernel(const __grid_constant__
     double* W2 = W + NB * pw;
     double* Ts = W2 + NB * pw;
     const long long ra = (long long)ia * q.rpc, rb = (long long)ib * q.rpc;
-    for (int e = threadIdx.x; e < K * ph; e += blockDim.x) {
-      const int row = e / ph, col = e - row * ph;
-      const bool ok = col < kq;
-      cp_async8(H + e, ok ? Q + (ra + row) * q.q_r + (long long)col * q.q_c : Q, ok);
-    }
+    for (int row = warp; row < K; row += nwarps)
+      for (int col = lane; col < ph; col += kWarp) {
+        const bool ok = col < kq;
+        cp_async8(H + row * ph + col, ok ? Q + (ra + row) * q.q_r + (long long)col * q.q_c : Q, ok);
+      }
     for (int e = threadIdx.x; e < pad8(K) * pz; e += blockDim.x) Z[e] = 0.0;
     cp_async_wait_all();
     __syncthreads();
     apply_step<false>(Z, pz, H, ph, K, kq, K, q.Rst + nd * q.st_node + (long long)ib * K * K, K,
                       Tpg + (long long)(q.P + ib) * np * NB * NB, Vs, W, W2, pw, Ts);
-    for (int e = threadIdx.x; e < kq * K; e += blockDim.x) {
-      const int row = e / kq, col = e - row * kq;
-      Q[(ra + row) * q.q_r + (long long)col * q.q_c] = H[row * ph + col];
-    }
-    for (int e = threadIdx.x; e < kq * pz; e += blockDim.x) {
-      const int col = e / pz, row = e - col * pz;
-      if (row < krb) Q[(rb + row) * q.q_r + (long long)col * q.q_c] = Z[e];
-    }
+    for (int row = warp; row < K; row += nwarps)
+      for (int col = lane; col < kq; col += kWarp) Q[(ra + row) * q.q_r + (long long)col * q.q_c] = H[row * ph + col];
+    for (int col = warp; col < kq; col += nwarps)
+      for (int row = lane; row < krb; row += kWarp) Q[(rb + row) * q.q_r + (long long)col * q.q_c] = Z[col * pz + row];
   }
 }
 
