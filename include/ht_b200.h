@@ -101,6 +101,23 @@ int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
 int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
                 const ht_tensor* out, ht_stream_t stream);
 
+/* Sharded truncation (the paper's tree-parallel protocol, one subtree per GPU):
+ * runs one phase restricted to the nodes with mask[t] != 0 (host array [2d-1]).
+ *   phase 0 ORTH   : QR sweep of the masked nodes (R factors of unmasked sons must
+ *                    already sit in their workspace slots -- received from the
+ *                    shard owning them)
+ *   phase 1 GRAM   : reduced Gramians of the sons of masked inner nodes / root
+ *   phase 2 EIG    : eigendecomposition + rank choice of masked non-root nodes
+ *   phase 3 PROJECT: projection of masked nodes into `out` (unmasked sons' eigen-
+ *                    vectors must be in their slots)
+ * Node arrays of unowned nodes are never touched (any non-null pointer). */
+int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int32_t phase,
+                        const uint8_t* mask, const ht_tensor* out, ht_stream_t stream);
+/* Device pointer + element count of a per-node workspace slot of the truncation:
+ * kind 0 R factor, 1 Gramian, 2 eigenvectors, 3 eigenvalues, 4 ranks (int32,
+ * all nodes + status word), 5 orthogonalised node array.  Host-only query. */
+int ht_truncate_slot(const ht_tensor* x, void* ws, int32_t kind, int32_t node, void** ptr, int64_t* count);
+
 /* Hierarchical singular values: after ht_truncate_ranks, copy the descending,
  * clamped eigenvalues lambda_t of every non-root node's reduced Gramian
  * (sigma_t = sqrt(lambda_t)) into lam (device, concatenated in node-id order). */

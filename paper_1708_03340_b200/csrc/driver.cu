@@ -89,6 +89,8 @@ struct View {
   std::vector<long long> k;     // per node rank (root 1)
   std::vector<double*> p;
   bool orth = false;
+  std::vector<unsigned char> mask;  // empty: every node (else: nodes this shard processes)
+  bool on(int t) const { return mask.empty() || mask[t] != 0; }
   long long k1(int t) const { return k[T->son1[t]]; }
   long long k2(int t) const { return k[T->son2[t]]; }
   long long elems(int t) const {
@@ -274,8 +276,10 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       op.out[t] = ar.take(e);
     }
   }
-  op.R.assign(T.nn, nullptr);
-  for (int t = 1; t < T.nn; ++t) op.R[t] = ar.take(ko[t] * x.k[t]);
+  if (op.R.empty()) {
+    op.R.assign(T.nn, nullptr);
+    for (int t = 1; t < T.nn; ++t) op.R[t] = ar.take(ko[t] * x.k[t]);
+  }
 
   const size_t scratch_base = scratch_ar.off;
   size_t scratch_max = scratch_base;
@@ -285,10 +289,11 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     std::vector<QrProblem> qs;
     std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
     for (int t : T.levels[l])
-      if (!T.leaf(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
+      if (!T.leaf(t) && x.on(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
     for (int t : T.levels[l])
-      if (!T.leaf(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
+      if (!T.leaf(t) && x.on(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
     for (int t : T.levels[l]) {
+      if (!x.on(t)) continue;
       if (T.leaf(t)) {
         QrProblem q{};
         q.A = x.p[t]; q.a_r = x.k[t]; q.a_c = 1;
@@ -329,7 +334,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   }
   // root: B_D <- R1 B_D R2^T (arith.py:144-145)
   scratch_ar.off = scratch_base;
-  {
+  if (x.on(0)) {
     const int s1 = T.son1[0], s2 = T.son2[0];
     const long long k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
     double* tmp = scratch_ar.take(k1o * k2);
@@ -353,7 +358,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
   const size_t base = scratch_ar.off;
   size_t mx = base;
   // root: G_s1 = B_D B_D^T, G_s2 = B_D^T B_D
-  {
+  if (o.on(0)) {
     scratch_ar.off = base;
     const int s1 = T.son1[0], s2 = T.son2[0];
     const long long k1 = o.k[s1], k2 = o.k[s2];
@@ -378,7 +383,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     scratch_ar.off = base;
     std::vector<int> inner;
     for (int t : T.levels[l])
-      if (!T.leaf(t)) inner.push_back(t);
+      if (!T.leaf(t) && o.on(t)) inner.push_back(t);
     if (inner.empty()) continue;
     std::vector<GemmDesc> g1s, g2s;
     std::vector<ReduceDesc> rs;
@@ -470,6 +475,8 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
       else e = ko[t] * ko[T.son1[t]] * ko[T.son2[t]];
       P.op.out[t] = ar.take(e);
     }
+    P.op.R.assign(T.nn, nullptr);
+    for (int t = 1; t < T.nn; ++t) P.op.R[t] = ar.take(ko[t] * x.k[t]);
     P.o.k = ko;
     P.o.p = P.op.out;
     P.o.orth = true;
@@ -522,27 +529,35 @@ size_t truncate_ws_bytes(const View& x) {
   return need + 4096 * (size_t)x.T->nn + 256;
 }
 
-int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s) {
-  HT_TRY(check_ctl(ctl));
+// Sub-phases of truncate (each restricted to x.mask for the sharded protocol).
+enum TruncPhase { kPhaseOrth = 0, kPhaseGram = 1, kPhaseEig = 2, kPhaseProject = 3 };
+
+int check_ws(const View& x, char* ws, size_t ws_bytes) {
   const size_t need = truncate_ws_bytes(x);
   if (!ws || ws_bytes < need) {
     set_error("truncate workspace too small: need " + std::to_string(need) + " bytes");
     return kErrArgument;
   }
-  HT_TRY(plan_truncate(x, P, ws));
+  return kOk;
+}
+
+int phase_orth(const View& x, TruncPlan& P, cudaStream_t s) {
+  if (x.orth) return kOk;
+  Arena sc = P.scratch;
+  return run_orthogonalize(x, P.op, sc, sc, s, true);
+}
+
+int phase_gram(TruncPlan& P, cudaStream_t s) {
+  Arena sc = P.scratch;
+  return run_gramians(P.o, P.G, sc, s, true);
+}
+
+// batched eigendecomposition + select_rank of the (masked) non-root nodes
+int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t s) {
   const Tree& T = *x.T;
-  HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
-  if (!x.orth) {
-    Arena sc = P.scratch;  // R factors live in scratch: needed only during the sweep
-    HT_TRY(run_orthogonalize(x, P.op, sc, sc, s, true));
-  }
-  {
-    Arena sc = P.scratch;
-    HT_TRY(run_gramians(P.o, P.G, sc, s, true));
-  }
-  // batched eigendecomposition + select_rank of all 2d-2 non-root nodes
   std::vector<EigProblem> eps;
   for (int t = 1; t < T.nn; ++t) {
+    if (!x.on(t)) continue;
     EigProblem e{};
     e.S = P.G[t]; e.V = P.EV[t]; e.lam = P.lam[t];
     e.rank = P.ranks + t; e.status = P.status;
@@ -568,8 +583,17 @@ int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_
     }
     eps.push_back(e);
   }
-  HT_TRY(eig_batched(eps, s));
-  return kOk;
+  return eig_batched(eps, s);
+}
+
+int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s) {
+  HT_TRY(check_ctl(ctl));
+  HT_TRY(check_ws(x, ws, ws_bytes));
+  HT_TRY(plan_truncate(x, P, ws));
+  HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
+  HT_TRY(phase_orth(x, P, s));
+  HT_TRY(phase_gram(P, s));
+  return phase_eig(x, ctl, P, s);
 }
 
 std::vector<long long> static_ranks(const View& x, const ht_trunc_ctl* ctl, bool& ok) {
@@ -593,7 +617,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   const View& o = P.o;
   // shape checks of the caller's output
   for (int t = 1; t < T.nn; ++t)
-    if (out.k[t] > o.k[t]) {
+    if (x.on(t) && out.k[t] > o.k[t]) {
       set_error("output rank exceeds the orthogonalised rank at node " + std::to_string(t));
       return kErrShape;
     }
@@ -601,10 +625,11 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   std::vector<GemmDesc> st1, st2, st3;
   std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
   for (int t = 1; t < T.nn; ++t)
-    if (!T.leaf(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+    if (!T.leaf(t) && x.on(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
   for (int t = 1; t < T.nn; ++t)
-    if (!T.leaf(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
+    if (!T.leaf(t) && x.on(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
   for (int t = 1; t < T.nn; ++t) {
+    if (!x.on(t)) continue;
     const long long kt = o.k[t], rt = out.k[t];
     if (T.leaf(t)) {
       // U_new (n x r) = Q (n x k) * EV[:, :r]   (arith.py:344)
@@ -622,7 +647,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     // mode 3: B_new ((rt r1) x r2) = C2 * EV_s2[:, :r2]   (arith.py:170)
     st3.push_back(gemm_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
   }
-  {
+  if (x.on(0)) {
     // root: Q1^T B_D Q2   (arith.py:350-351)
     const int s1 = T.son1[0], s2 = T.son2[0];
     const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
@@ -833,6 +858,79 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
   TruncPlan P;
   HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s));
   return truncate_phase2(v, ctl, (char*)ws, o, s);
+}
+
+int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int32_t phase,
+                        const uint8_t* mask, const ht_tensor* out, ht_stream_t stream) {
+  View v;
+  HT_TRY(make_view(x, v));
+  HT_TRY(check_ctl(ctl));
+  HT_TRY(check_ws(v, (char*)ws, ws_bytes));
+  if (mask) v.mask.assign(mask, mask + v.T->nn);
+  cudaStream_t s = (cudaStream_t)stream;
+  if (phase == kPhaseProject) {
+    View o;
+    HT_TRY(out_view(out, v, o));
+    return truncate_phase2(v, ctl, (char*)ws, o, s);
+  }
+  TruncPlan P;
+  HT_TRY(plan_truncate(v, P, (char*)ws));
+  switch (phase) {
+    case kPhaseOrth:
+      HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
+      return phase_orth(v, P, s);
+    case kPhaseGram: return phase_gram(P, s);
+    case kPhaseEig: return phase_eig(v, ctl, P, s);
+    default: break;
+  }
+  set_error("unknown truncate phase");
+  return kErrArgument;
+}
+
+int ht_truncate_slot(const ht_tensor* x, void* ws, int32_t kind, int32_t node, void** ptr, int64_t* count) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  if (node < 0 || node >= v.T->nn) {
+    set_error("node id out of range");
+    return kErrArgument;
+  }
+  TruncPlan P;
+  HT_TRY(plan_truncate(v, P, (char*)ws));
+  const long long k = P.o.k[node];
+  switch (kind) {
+    case 0:  // R factor (orthogonalised rank x input rank)
+      if (v.orth || node == 0) break;
+      *ptr = P.op.R[node];
+      *count = k * v.k[node];
+      return kOk;
+    case 1:  // reduced Gramian
+      if (node == 0) break;
+      *ptr = P.G[node];
+      *count = k * k;
+      return kOk;
+    case 2:  // eigenvectors
+      if (node == 0) break;
+      *ptr = P.EV[node];
+      *count = k * k;
+      return kOk;
+    case 3:  // eigenvalues
+      if (node == 0) break;
+      *ptr = P.lam[node];
+      *count = k;
+      return kOk;
+    case 4:  // selected rank (int32) of every node + status
+      *ptr = P.ranks;
+      *count = v.T->nn + 1;
+      return kOk;
+    case 5:  // orthogonalised node array
+      *ptr = P.o.p[node];
+      *count = node == 0 ? P.o.k1(0) * P.o.k2(0)
+               : v.T->leaf(node) ? v.n[node] * k : k * P.o.k1(node) * P.o.k2(node);
+      return kOk;
+    default: break;
+  }
+  set_error("no such workspace slot for this node");
+  return kErrArgument;
 }
 
 int ht_truncate_eigenvalues(const ht_tensor* x, void* ws, size_t ws_bytes, double* lam, ht_stream_t stream) {
