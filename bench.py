@@ -7,9 +7,11 @@ eigendecompositions, projection -- reference arith.py:325-352.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
-Prints ONE JSON line (rank 0).  Under torchrun (N > 1) every rank truncates its
-own replica tensor (independent objects, no collective on the data path);
-``value`` is the whole-job rate, the step time is the max over ranks.
+Prints ONE JSON line (rank 0).  Under torchrun (N > 1) the tensor is sharded
+over the dimension tree (GPU g owns the subtree under the g-th node of level
+log2 N, GPU0 also the N-1 nodes above; three NCCL point-to-point waves per
+truncation) -- strong scaling of one d=64 truncation; ``--replicas`` runs
+independent replica tensors instead.  The step time is the max over ranks.
 """
 
 from __future__ import annotations
@@ -160,6 +162,16 @@ def parity_summary(T, t_ref, x):
     return {"rel_err_vs_oracle": err, "ranks_equal": got.ranks == t_ref.ranks, "tol": 1e-10}
 
 
+def measured_traffic():
+    """Per-launch DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum) of each profiled
+    kernel from the committed ncu --set full summary, if one exists."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
 def cpu_model():
     try:
         for line in open("/proc/cpuinfo"):
@@ -200,24 +212,98 @@ def run_reference(args, rank, world):
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": len(times), "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian, SURVEY §8(d))",
-        "config": config_dict(args),
+        "scaling": "strong" if world > 1 and not args.replicas else "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Gaussian, SURVEY §8(d))",
+        "config": config_dict(args, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
 
 
-def config_dict(args):
+def config_dict(args, world=1):
+    sharded = world > 1 and not args.replicas
+    par = (f"tree-sharded over {world} GPUs: subtree per GPU at level {int(math.log2(world))}, top {world - 1} "
+           f"nodes on GPU0, NCCL P2P waves R-up/G-down/EV-up" if sharded
+           else ("replica per GPU" if world > 1 else "1 GPU"))
     return {"workload": f"C2: truncate(add(A,C)) d={args.d} n={args.n} rank {2 * args.k}->{args.k}",
             "d": args.d, "n": args.n, "k": args.k, "pre_truncation_rank": 2 * args.k,
             "seeds": [2 * int(round(math.log2(args.d))), 2 * int(round(math.log2(args.d))) + 1],
             "l2_policy": f"inputs {8 * storage(args.d, args.n, 2 * args.k) / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-            "parallelism": "replica per GPU"}
+            "parallelism": par}
 
 
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
+
+
+class _Single:
+    """1 GPU (or one replica per GPU): the public drop-in API on a resident HTensor."""
+
+    def __init__(self, htb, tree, fa, fc, ctl):
+        self.htb, self.tree, self.ctl = htb, tree, ctl
+        ad, cd = htb.HTensor(tree, *fa), htb.HTensor(tree, *fc)
+        self.x = htb.add(ad, cd)  # X resident in HBM (547 MB at d=64: larger than L2)
+        self.sizes, self.ranks = self.x.host_layout()
+        self.host_x = None
+        self.out_host = None
+
+    def step(self):
+        return self.htb.truncate(self.x, self.ctl)
+
+    def prepare_e2e(self):
+        self.host_x = self.x.to_host_arena()  # pinned
+
+    def e2e_step(self):
+        xh = self.htb.HTensor.from_host_arena(self.tree, self.sizes, self.ranks, self.host_x)
+        t = self.htb.truncate(xh, self.ctl)
+        self.out_host = t.to_host_arena(self.out_host)
+        return t
+
+    def e2e_bytes(self):
+        return self.host_x.numel() * 8, self.out_host.numel() * 8
+
+
+class _Sharded:
+    """N GPUs, tree-parallel: this rank's subtree (+ the top nodes on rank 0)."""
+
+    def __init__(self, htb, tree, fa, fc, ctl):
+        from paper_1708_03340_b200 import dist as hd
+
+        self.hd, self.ctl = hd, ctl
+        self.comm = hd.TorchComm()
+        self.smap = hd.ShardMap.build(tree, self.comm.world)
+        owned = self.smap.owned(self.comm.rank)
+        a = hd.ShardedHTensor.from_host(tree, *fa, owned)
+        c = hd.ShardedHTensor.from_host(tree, *fc, owned)
+        self.x = hd.sharded_add(a, c)  # communication-free
+        del a, c
+        self.engine = hd.GpuShardEngine(self.x, ctl)
+        self.orth = self.x.orth_ranks()
+        self.host_x = self.out_host = None
+
+    def step(self):
+        return self.hd.sharded_truncate(self.engine, self.comm, self.smap, self.ctl, self.orth)
+
+    def prepare_e2e(self):
+        import torch
+
+        self.host_x = {t: a.cpu().pin_memory() for t, a in self.x.arrays.items()}
+
+    def e2e_step(self):
+        import torch
+
+        for t, h in self.host_x.items():  # this step's inputs: pinned host -> HBM
+            self.x.arrays[t].copy_(h, non_blocking=True)
+        out = self.step()
+        if self.out_host is None:
+            self.out_host = {t: torch.empty(a.shape, dtype=a.dtype).pin_memory() for t, a in out.arrays.items()}
+        for t, a in out.arrays.items():
+            self.out_host[t].copy_(a, non_blocking=True)
+        return out
+
+    def e2e_bytes(self):
+        return (sum(h.numel() * 8 for h in self.host_x.values()), sum(h.numel() * 8 for h in self.out_host.values()))
 
 
 def run_ours(args, rank, world, local_rank):
@@ -226,25 +312,31 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_1708_03340_b200 as htb
     from paper_1708_03340_b200 import _lib
-    from oracle import htucker_oracle as orc
 
     torch.cuda.set_device(local_rank)
     lib = _lib.load()
-    # every rank: its own replica (seed offset by rank) -- independent objects
-    a, c, x = orc.c2_inputs(args.d, args.n, args.k, seed_base=2 * int(round(math.log2(args.d))) + 2 * rank)
+    sharded = world > 1 and not args.replicas
+    p = int(round(math.log2(args.d)))
+    seed = 2 * p + (0 if sharded else 2 * rank)  # replicas: independent objects per rank
     tree = htb.build_balanced_tree(args.d)
-    ad = htb.HTensor(tree, a.U, a.B, a.root)
-    cd = htb.HTensor(tree, c.U, c.B, c.root)
-    xd = htb.add(ad, cd)  # X resident in HBM (547 MB at d=64: larger than L2)
-    del ad, cd
+    fa = htb.gaussian_factors(tree, args.n, args.k, seed)
+    fc = htb.gaussian_factors(tree, args.n, args.k, seed + 1)
     ctl = htb.TruncationControl.fixed_rank(args.k)
+    work = (_Sharded if sharded else _Single)(htb, tree, fa, fc, ctl)
     for _ in range(args.warmup):
-        htb.truncate(xd, ctl)
+        work.step()
     torch.cuda.synchronize()
 
     def barrier():
         if world > 1:
             dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
     stream = torch.cuda.current_stream()
     with ClockSampler(local_rank) as clk:
@@ -254,95 +346,96 @@ def run_ours(args, rank, world, local_rank):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(args.steps):
-            T = htb.truncate(xd, ctl)
+            T = work.step()
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         launches = lib.ht_launch_count() - n0
-    ms = e0.elapsed_time(e1) / args.steps
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    truncs_per_step = 1 if sharded else world
+    value = truncs_per_step * 1e3 / ms
     if world > 1:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-    value = world * 1e3 / ms
+        lt = torch.tensor([float(launches)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(lt)
+        launches = int(lt.item())
 
-    # per-kernel event timing (separate instrumented steps right after the timed region)
+    # per-kernel event timing (separate instrumented steps right after the timed region; rank 0's kernels)
     lib.ht_profile_enable(1)
     prof_steps = 2
     for _ in range(prof_steps):
-        htb.truncate(xd, ctl)
+        work.step()
     torch.cuda.synchronize()
     prof = _lib.profile_report()
     lib.ht_profile_enable(0)
 
     # end-to-end through the public API: pinned host X -> H2D -> truncate -> D2H of T
-    host_x = xd.to_host_arena()
-    sizes, ranks = xd.host_layout()
-    out_host = None
+    work.prepare_e2e()
+    work.e2e_step()
     torch.cuda.synchronize()
     e2e_steps = max(1, min(args.steps, 5))
-    for _ in range(1):
-        xh = htb.HTensor.from_host_arena(tree, sizes, ranks, host_x)
-        out_host = htb.truncate(xh, ctl).to_host_arena(out_host)
-    torch.cuda.synchronize()
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
+    torch.cuda.synchronize()
     f0.record(stream)
     for _ in range(e2e_steps):
-        xh = htb.HTensor.from_host_arena(tree, sizes, ranks, host_x)
-        Th = htb.truncate(xh, ctl)
-        out_host = Th.to_host_arena(out_host)
+        work.e2e_step()
     f1.record(stream)
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1) / e2e_steps
+    barrier()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1) / e2e_steps)
+    h2d, d2h = work.e2e_bytes()
     if world > 1:
-        t = torch.tensor([e2e_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    h2d = host_x.numel() * 8
-    d2h = out_host.numel() * 8
+        bt = torch.tensor([float(h2d), float(d2h)], dtype=torch.float64, device="cuda")
+        dist.all_reduce(bt)
+        h2d, d2h = int(bt[0].item()), int(bt[1].item())
 
     if rank != 0:
         return None
 
     peak64 = dgemm_peak_tflops()
     peaks = measured_peaks()
+    traffic = measured_traffic()
     # dominant kernel roofline (algorithmic flops / event-timed duration on the launching stream)
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     step_ms_prof = sum(v["ms"] for v in prof.values()) / prof_steps
     if dom["flops"] > 0:
         ach = dom["flops"] / (dom["ms"] * 1e-3) / 1e12
         roof = {"kernel": dom_name, "bound": "tensor", "achieved": ach, "peak": peak64, "unit": "TFLOP/s",
-                "frac": ach / peak64, "traffic": None,
-                "peak_source": "cuBLAS DGEMM 4096^3 measured in this run (FP64; DMMA/DFMA microbench 37.1 TF, "
-                               "profiles/r01_fp64_peak_microbench.jsonl)",
+                "frac": ach / peak64, "traffic": traffic.get(dom_name),
+                "peak_source": "cuBLAS DGEMM 4096^3 measured in this run (FP64 has no tcgen05 path; "
+                               "DMMA/DFMA microbench 37.1 TF, profiles/r01_fp64_peak_microbench.jsonl)",
+                "algorithmic_flops_per_launch": dom["flops"] / max(1, dom["launches"]),
                 "launches_per_step": dom["launches"] / prof_steps,
                 "share_of_step": dom["ms"] / prof_steps / step_ms_prof}
     else:
         bw = dom["bytes"] / (dom["ms"] * 1e-3) / 1e9
         roof = {"kernel": dom_name, "bound": "hbm", "achieved": bw, "peak": peaks.get("hbm_gbs", 6521.1),
-                "unit": "GB/s", "frac": bw / peaks.get("hbm_gbs", 6521.1), "traffic": None}
+                "unit": "GB/s", "frac": bw / peaks.get("hbm_gbs", 6521.1), "traffic": traffic.get(dom_name)}
     flops = algorithmic_flops(args.d, args.n, 2 * args.k, args.k)
-    step_tf = flops / (ms * 1e-3) / 1e12
+    step_tf = truncs_per_step * flops / (ms * 1e-3) / 1e12
     kernels = {k: {"ms_per_step": v["ms"] / prof_steps, "launches_per_step": v["launches"] / prof_steps,
                    "tflops": (v["flops"] / (v["ms"] * 1e-3) / 1e12) if v["flops"] else None}
                for k, v in sorted(prof.items(), key=lambda kv: -kv[1]["ms"])}
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong" if sharded else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian factors, SURVEY §8(d))",
-        "config": config_dict(args),
+        "config": config_dict(args, world),
         "roofline": roof,
-        "roofline_step": {"bound": "tensor", "achieved": step_tf, "peak": peak64, "unit": "TFLOP/s",
-                          "frac": step_tf / peak64, "flops_per_truncation": flops},
+        "roofline_step": {"bound": "tensor", "achieved": step_tf, "peak": peak64 * world, "unit": "TFLOP/s",
+                          "frac": step_tf / (peak64 * world), "flops_per_truncation": flops},
         "kernels": kernels,
-        "e2e": {"value": world * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "ms_per_step": e2e_ms},
+        "e2e": {"value": truncs_per_step * 1e3 / e2e_ms, "unit": UNIT, "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
     if world == 1 and not args.no_cpu_baseline:
+        from oracle import htucker_oracle as orc  # checker / CPU baseline only
+
+        x = orc.add(orc.HT(orc.balanced_tree(args.d), *fa), orc.HT(orc.balanced_tree(args.d), *fc))
         threads = cpu_threads()
         t_ref, dt = cpu_truncation(x, args.k, threads)
         line["cpu_baseline"] = {"value": 1.0 / dt, "unit": UNIT, "cores": threads, "kind": "port",
@@ -362,6 +455,8 @@ def main():
     ap.add_argument("--n", type=int, default=1000)
     ap.add_argument("--k", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N>1: independent replica tensors per GPU instead of one tree-sharded tensor")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))

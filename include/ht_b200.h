@@ -137,6 +137,10 @@ int ht_gramians(const ht_tensor* x, void* ws, size_t ws_bytes, double* const* bh
 /* add (arith.py:355-365) and subtract (arith.py:374-375, alpha_c = -1):
  * out ranks are a.rank + c.rank node by node (root 1). No FLOPs (Lemma 3). */
 int ht_add(const ht_tensor* a, const ht_tensor* c, double alpha_c, const ht_tensor* out, ht_stream_t stream);
+/* Sharded add: only nodes with mask[t] != 0 are read or written (the other node
+ * pointers may be placeholders).  Add needs no communication (dist.py add protocol). */
+int ht_add_sharded(const ht_tensor* a, const ht_tensor* c, double alpha_c, const uint8_t* mask,
+                   const ht_tensor* out, ht_stream_t stream);
 
 /* scale (arith.py:368-371): y = alpha * x elementwise (used on the root). */
 int ht_scale(const double* x, double* y, int64_t count, double alpha, ht_stream_t stream);

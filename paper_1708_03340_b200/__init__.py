@@ -27,6 +27,8 @@ from .format import (
     GeneralizedMatrix,
     HTensor,
     HTOperator,
+    gaussian_factors,
+    gaussian_htensor,
     identity_htoperator,
     random_htensor,
     storage_size,
@@ -43,6 +45,8 @@ __all__ = [
     "apply_operator",
     "build_balanced_tree",
     "compute_bhat",
+    "gaussian_factors",
+    "gaussian_htensor",
     "gemm",
     "hierarchical_singular_values",
     "identity_htoperator",

@@ -32,7 +32,7 @@ EXPORTS = (
     "ht_truncate_project", "ht_truncate", "ht_truncate_eigenvalues",
     "ht_orth_ranks", "ht_orthogonalize_workspace_size", "ht_orthogonalize",
     "ht_gramians_workspace_size", "ht_gramians",
-    "ht_add", "ht_scale",
+    "ht_add", "ht_add_sharded", "ht_scale",
     "ht_inner_product_workspace_size", "ht_inner_product",
     "ht_apply_operator",
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
@@ -88,6 +88,7 @@ def _declare(lib):
         "ht_gramians_workspace_size": ([t, sz], ctypes.c_int),
         "ht_gramians": ([t, _vp, ctypes.c_size_t, P(ctypes.c_void_p), _vp], ctypes.c_int),
         "ht_add": ([t, t, ctypes.c_double, t, _vp], ctypes.c_int),
+        "ht_add_sharded": ([t, t, ctypes.c_double, _vp, t, _vp], ctypes.c_int),
         "ht_scale": ([_vp, _vp, ctypes.c_int64, ctypes.c_double, _vp], ctypes.c_int),
         "ht_inner_product_workspace_size": ([t, t, sz], ctypes.c_int),
         "ht_inner_product": ([t, t, _vp, ctypes.c_size_t, _vp, P(ctypes.c_double), _vp], ctypes.c_int),

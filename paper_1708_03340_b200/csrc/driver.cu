@@ -1023,6 +1023,11 @@ int ht_gramians(const ht_tensor* x, void* ws, size_t ws_bytes, double* const* bh
 }
 
 int ht_add(const ht_tensor* a, const ht_tensor* c, double alpha_c, const ht_tensor* out, ht_stream_t stream) {
+  return ht_add_sharded(a, c, alpha_c, nullptr, out, stream);
+}
+
+int ht_add_sharded(const ht_tensor* a, const ht_tensor* c, double alpha_c, const uint8_t* mask,
+                   const ht_tensor* out, ht_stream_t stream) {
   View va, vc, vo;
   HT_TRY(make_view(a, va));
   HT_TRY(make_view(c, vc));
@@ -1036,6 +1041,7 @@ int ht_add(const ht_tensor* a, const ht_tensor* c, double alpha_c, const ht_tens
     }
   std::vector<EmbedDesc> ds;
   for (int t = 0; t < T.nn; ++t) {
+    if (mask && !mask[t]) continue;  // node owned by another shard: add is communication-free
     EmbedDesc e{};
     e.out = vo.p[t]; e.A = va.p[t]; e.C = vc.p[t];
     e.alpha_c = t == 0 ? alpha_c : 1.0;

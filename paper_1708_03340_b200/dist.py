@@ -102,12 +102,45 @@ class ShardedHTensor:
         self._cs = None
 
     @classmethod
+    def from_host(cls, tree: DimensionTree, leaves: dict, transfer: dict, root, nodes, device=None,
+                  pin: bool = False) -> "ShardedHTensor":
+        """Upload only the owned nodes' host arrays (numpy or torch) to this rank's GPU."""
+        dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+        sizes = {t: int(a.shape[0]) for t, a in leaves.items()}
+        ranks = {t: int(a.shape[1]) for t, a in leaves.items()}
+        ranks.update({t: int(a.shape[0]) for t, a in transfer.items()})
+        host = dict(leaves)
+        host.update(transfer)
+        host[0] = root
+        arrays = {}
+        for t in sorted(nodes):
+            h = torch.as_tensor(np.ascontiguousarray(host[t]), dtype=F64)
+            arrays[t] = h.to(dev, non_blocking=False)
+        return cls(tree, sizes, ranks, arrays, False)
+
+    @classmethod
     def from_htensor(cls, x: HTensor, nodes) -> "ShardedHTensor":
         sizes, ranks = x.host_layout()
         return cls(x.tree, sizes, ranks, {t: x.node_array(t) for t in nodes}, x.orthogonal)
 
     def shape(self, t: int) -> tuple:
         return node_shape(self.tree, t, self.sizes, self.ranks)
+
+    @property
+    def device(self) -> torch.device:
+        return self._dummy.device
+
+    def nbytes(self) -> int:
+        return sum(a.numel() * 8 for a in self.arrays.values())
+
+    def orth_ranks(self) -> dict:
+        """Ranks after orthogonalisation (shape-only; arith.py:280-297 rank shrink)."""
+        nn = len(self.tree.nodes)
+        if self.orthogonal:
+            return dict(self.ranks)
+        rbuf = (ctypes.c_int64 * nn)()
+        _lib.check(_lib.load().ht_orth_ranks(self._c(), rbuf), "orth ranks")
+        return {t: int(rbuf[t]) for t in range(1, nn)}
 
     def _c(self):
         if self._cs is None:
@@ -122,6 +155,23 @@ class ShardedHTensor:
                               ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), int(self.orthogonal))
             self._cs = (cs, n, r, ptrs)
         return self._cs[0]
+
+
+def sharded_add(a: ShardedHTensor, c: ShardedHTensor, alpha_c: float = 1.0) -> ShardedHTensor:
+    """Owned-node HT add (arith.py:160-193); communication-free (reference dist.py add
+    protocol sends no messages).  Nodes owned here must be the same in a and c."""
+    if set(a.arrays) != set(c.arrays):
+        raise ValueError("sharded add: operands own different nodes")
+    lib = _lib.load()
+    ranks = {t: a.ranks[t] + c.ranks[t] for t in a.ranks}
+    arrays = {t: torch.empty(node_shape(a.tree, t, a.sizes, ranks), dtype=F64, device=a.device)
+              for t in a.arrays}
+    out = ShardedHTensor(a.tree, a.sizes, ranks, arrays, False)
+    mask = np.zeros(len(a.tree.nodes), dtype=np.uint8)
+    mask[list(a.arrays)] = 1
+    _lib.check(lib.ht_add_sharded(a._c(), c._c(), float(alpha_c), mask.ctypes.data_as(ctypes.c_void_p), out._c(),
+                                  _lib.stream_handle()), "sharded add")
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -341,5 +391,5 @@ def fake_shard_truncate(x: HTensor, ctl: TruncationControl, world: int):
     return HTensor._wrap(tree, nodes, False)
 
 
-__all__ = ["ShardMap", "ShardedHTensor", "GpuShardEngine", "TorchComm", "LocalComm", "sharded_truncate",
+__all__ = ["ShardMap", "ShardedHTensor", "GpuShardEngine", "TorchComm", "LocalComm", "sharded_truncate", "sharded_add",
            "fake_shard_truncate", "static_ranks"]

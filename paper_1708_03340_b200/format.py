@@ -436,10 +436,9 @@ def _leaf_sizes(tree, n) -> dict:
     return {tree.leaf_for_dim(mu).index: int(sizes[mu - 1]) for mu in range(1, tree.d + 1)}
 
 
-def random_htensor(tree: DimensionTree, n, k, seed: int, device=None) -> HTensor:
-    """Uniform [-1, 1] entries from PCG64(seed) in the reference's node order
-    (format.py:271-301): the same seed gives the same tensor as the reference."""
-    rng = np.random.default_rng(np.random.PCG64(seed))
+def _draw_factors(tree: DimensionTree, n, k, draw, leaf_scale=None, core_scale=None):
+    """Factors in the reference's node order (format.py:271-301), one ``draw(shape)``
+    per node; optional exact power-of-two rescales of leaves / transfer tensors."""
     ranks = _uniform_ranks(tree, k)
     sizes = _leaf_sizes(tree, n)
     leaves, transfer, root = {}, {}, None
@@ -448,17 +447,51 @@ def random_htensor(tree: DimensionTree, n, k, seed: int, device=None) -> HTensor
             nm, km = sizes[node.index], ranks[node.index]
             if km > nm:
                 raise ValueError(f"leaf rank {km} exceeds size {nm} at node {node.index}")
-            leaves[node.index] = rng.uniform(-1.0, 1.0, size=(nm, km))
+            leaves[node.index] = draw((nm, km))
+            if leaf_scale:
+                leaves[node.index] *= leaf_scale(nm)
             continue
         s1, s2 = node.sons
         k1, k2 = ranks[s1], ranks[s2]
         if node.is_root:
-            root = rng.uniform(-1.0, 1.0, size=(k1, k2))
+            root = draw((k1, k2))
+            if core_scale:
+                root *= core_scale(max(k1, k2))
             continue
         kt = ranks[node.index]
         if kt > k1 * k2:
             raise ValueError(f"rank {kt} at node {node.index} exceeds structural bound {k1 * k2}")
-        transfer[node.index] = rng.uniform(-1.0, 1.0, size=(kt, k1, k2))
+        transfer[node.index] = draw((kt, k1, k2))
+        if core_scale:
+            transfer[node.index] *= core_scale(kt)
+    return leaves, transfer, root
+
+
+def random_htensor(tree: DimensionTree, n, k, seed: int, device=None) -> HTensor:
+    """Uniform [-1, 1] entries from PCG64(seed) in the reference's node order
+    (format.py:271-301): the same seed gives the same tensor as the reference."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    leaves, transfer, root = _draw_factors(tree, n, k, lambda shp: rng.uniform(-1.0, 1.0, size=shp))
+    return HTensor(tree, leaves, transfer, root, device=device)
+
+
+def _pow2(x: float) -> float:
+    return 2.0 ** -round(math.log2(x))
+
+
+def gaussian_factors(tree: DimensionTree, n, k, seed: int, scaled: bool = True):
+    """Host (numpy) factors of the benchmark tensors: N(0,1) from
+    PCG64(seed) in the reference's node order; with ``scaled`` leaves x 2^-round(log2 sqrt n)
+    and transfer/root tensors x 2^-round(log2 k) (exact, keeps large-d sums finite).
+    Returns (leaves, transfer, root) dicts keyed by node id."""
+    rng = np.random.default_rng(np.random.PCG64(seed))
+    return _draw_factors(tree, n, k, rng.standard_normal,
+                         (lambda nm: _pow2(math.sqrt(nm))) if scaled else None,
+                         _pow2 if scaled else None)
+
+
+def gaussian_htensor(tree: DimensionTree, n, k, seed: int, scaled: bool = True, device=None) -> HTensor:
+    leaves, transfer, root = gaussian_factors(tree, n, k, seed, scaled)
     return HTensor(tree, leaves, transfer, root, device=device)
 
 
@@ -475,5 +508,6 @@ def storage_size(tensor: HTensor) -> int:
     return tensor.storage_size()
 
 
-__all__ = ["HTensor", "HTOperator", "GeneralizedMatrix", "random_htensor", "identity_htoperator",
+__all__ = ["HTensor", "HTOperator", "GeneralizedMatrix", "random_htensor", "gaussian_htensor", "gaussian_factors",
+           "identity_htoperator",
            "storage_size", "build_balanced_tree", "DimensionTree"]

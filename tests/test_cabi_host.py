@@ -119,3 +119,15 @@ def test_static_ranks_and_workspace_queries_without_gpu():
     ko = (ctypes.c_int64 * 7)()
     assert lib.ht_orth_ranks(ctypes.byref(t2), ko) == 0
     assert list(ko) == [1, 6, 5, 3, 2, 3, 3]
+
+
+def test_gaussian_factors_match_oracle_generator():
+    import paper_1708_03340_b200 as htb
+    from oracle import htucker_oracle as orc
+
+    for d, n, k, seed in [(8, 30, 5, 7), (5, 12, 3, 2)]:
+        lv, tf, root = htb.gaussian_factors(htb.build_balanced_tree(d), n, k, seed)
+        o = orc.gaussian_htensor(orc.balanced_tree(d), n, k, seed)
+        assert all(np.array_equal(lv[t], o.U[t]) for t in o.U)
+        assert all(np.array_equal(tf[t], o.B[t]) for t in o.B)
+        assert np.array_equal(root, o.root)

@@ -38,3 +38,24 @@ def test_fake_shard_accuracy_mode(cuda_ok):
     ref = orc.truncate(x, orc.Ctl(eps=eps))
     assert tg.ranks == ref.ranks
     assert rel_err(tg, ref) <= 1e-10
+
+
+def test_sharded_add_equals_add(cuda_ok):
+    import torch
+
+    import paper_1708_03340_b200 as htb
+    from paper_1708_03340_b200 import dist
+
+    tree = htb.build_balanced_tree(8)
+    fa = htb.gaussian_factors(tree, 30, 4, 5)
+    fc = htb.gaussian_factors(tree, 30, 3, 6)
+    full = htb.subtract(htb.HTensor(tree, *fa), htb.HTensor(tree, *fc))
+    smap = dist.ShardMap.build(tree, 4)
+    for g in range(4):
+        own = smap.owned(g)
+        a = dist.ShardedHTensor.from_host(tree, *fa, own)
+        c = dist.ShardedHTensor.from_host(tree, *fc, own)
+        s = dist.sharded_add(a, c, -1.0)
+        assert set(s.arrays) == set(own)
+        for t in own:
+            assert torch.equal(s.arrays[t], full.node_array(t))
