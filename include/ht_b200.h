@@ -90,8 +90,9 @@ const char* ht_version(void);
  *     kept ranks in out_rank[2d-1] (host);
  *  2. ht_truncate_project: projection into `out` (allocated with out_rank),
  *     reusing the state phase 1 left in `ws`.
- * ht_truncate does both without a host sync when the ranks are fixed by the
- * shapes (ht_truncate_static_ranks returns 1). */
+ * ht_truncate does both without a rank read-back when the ranks are fixed by
+ * the shapes (ht_truncate_static_ranks returns 1); see ht_set_qr_mode for the
+ * one synchronisation of the Cholesky-QR2 check. */
 int ht_truncate_workspace_size(const ht_tensor* x, size_t* bytes);
 int ht_truncate_static_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, int64_t* out_rank);
 int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
@@ -174,6 +175,17 @@ int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double
 int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha, const double* A, int64_t a_m,
                     int64_t a_k, int64_t a_b, const double* B, int64_t b_k, int64_t b_n, int64_t b_b, double beta,
                     double* C, int64_t c_m, int64_t c_n, int64_t c_b, ht_stream_t stream);
+
+/* QR policy of the orthogonalisation sweep (process-wide).
+ *   0 (default): Cholesky-QR2 on DMMA GEMMs for frames with m >= 2K, K <= 128;
+ *      the sweep then synchronises the stream ONCE to read a device red flag
+ *      (pivot loss > 10 digits, non-finite values, or Q1^T Q1 not within 0.1 of I)
+ *      and, if set, recomputes the whole sweep with Householder QR;
+ *   1: Householder tree-TSQR only (no synchronisation).
+ * Both give the unique QR with diag(R) >= 0 of kernels.py:24-32 up to rounding. */
+int ht_set_qr_mode(int mode);
+/* Number of Cholesky-QR2 sweeps that were re-run with Householder QR. */
+int64_t ht_qr_fallback_count(void);
 
 /* ---- instrumentation -------------------------------------------------- */
 

@@ -13,13 +13,16 @@ from .arith import (
     apply_operator,
     compute_bhat,
     gemm,
+    get_qr_mode,
     hierarchical_singular_values,
     inner_product,
     inner_product_device,
     leaf_map,
     norm,
     orthogonalize,
+    qr_fallback_count,
     scale,
+    set_qr_mode,
     subtract,
     truncate,
 )
@@ -48,6 +51,7 @@ __all__ = [
     "gaussian_factors",
     "gaussian_htensor",
     "gemm",
+    "get_qr_mode",
     "hierarchical_singular_values",
     "identity_htoperator",
     "inner_product",
@@ -57,7 +61,9 @@ __all__ = [
     "norm",
     "orthogonalize",
     "random_htensor",
+    "qr_fallback_count",
     "scale",
+    "set_qr_mode",
     "storage_size",
     "subtract",
     "truncate",

@@ -279,6 +279,32 @@ def apply_operator(op: HTOperator, a: HTensor) -> HTensor:
     return out
 
 
+_QR_MODES = {"auto": 0, "householder": 1}
+_qr_mode = "auto"
+
+
+def set_qr_mode(mode: str) -> None:
+    """QR policy of the orthogonalisation sweep (process-wide): ``"auto"`` (default)
+    runs Cholesky-QR2 on DMMA GEMMs where eligible and re-runs the sweep with
+    Householder QR when its device-side check fails; ``"householder"`` always uses
+    the Householder tree-TSQR.  Both return the reference's sign-fixed QR
+    (kernels.py:24-32) up to rounding."""
+    global _qr_mode
+    if mode not in _QR_MODES:
+        raise ValueError(f"qr mode must be one of {sorted(_QR_MODES)}")
+    _lib.check(_lib.load().ht_set_qr_mode(_QR_MODES[mode]), "set_qr_mode")
+    _qr_mode = mode
+
+
+def get_qr_mode() -> str:
+    return _qr_mode
+
+
+def qr_fallback_count() -> int:
+    """How many Cholesky-QR2 sweeps were recomputed with Householder QR."""
+    return int(_lib.load().ht_qr_fallback_count())
+
+
 def gemm(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, alpha=1.0, beta=0.0) -> torch.Tensor:
     """C = alpha A B + beta C on the DMMA kernel (row-major 2-D CUDA float64)."""
     lib = _lib.load()

@@ -1,0 +1,230 @@
+// Cholesky-QR2 (see cholqr.cuh).  The GEMMs run on the grouped DMMA kernel of
+// gemm.cu; this file holds the batched Cholesky / triangular-inverse kernel and
+// the launch sequence.
+#include <cmath>
+
+#include "cholqr.cuh"
+#include "gemm.cuh"
+#include "prof.cuh"
+
+namespace ht {
+namespace {
+
+constexpr int kCholThreads = 512;
+constexpr int kCholMaxDescs = 48;
+// pivot / column-norm^2 below this => kappa(A) ~> 1e5: leave it to Householder
+constexpr double kPivotTol = 1e-10;
+constexpr double kIdentityTol = 0.1;
+
+struct CholDesc {
+  const double* W;  // nodes x K x K row-major (only the upper triangle is read)
+  double* Rf;       // nodes x K x K: upper Cholesky factor (zeros below)
+  double* Ri;       // nodes x K x K: its inverse (upper, zeros below)
+  int K, nodes;
+  int check_identity;
+};
+
+struct CholBatch {
+  CholDesc d[kCholMaxDescs];
+  int block_begin[kCholMaxDescs + 1];
+  int count;
+  int* fail;
+};
+
+// One CTA per K x K Gram matrix.  Symmetric Gaussian elimination on the upper
+// triangle (W = L D L^T, U = D L^T), carrying L^{-1} in the strictly lower
+// triangle of the same shared array: at step j every row i > j does
+//   U[i][c]    -= m_i U[j][c]     (c >= i)          m_i = U[j][i] / U[j][j]
+//   Linv[i][c] -= m_i Linv[j][c]  (c <  j),  Linv[i][j] = -m_i
+// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.  One barrier per column.
+__global__ void __launch_bounds__(kCholThreads) chol_kernel(const __grid_constant__ CholBatch cb) {
+  int di = 0;
+  while (di + 1 < cb.count && (int)blockIdx.x >= cb.block_begin[di + 1]) ++di;
+  const CholDesc& c = cb.d[di];
+  const int node = blockIdx.x - cb.block_begin[di];
+  const int K = c.K, pitch = K + 1;
+  extern __shared__ double sm[];
+  double* W = sm;                 // K x pitch
+  double* dorig = sm + K * pitch; // K
+  double* piv = dorig + K;        // K
+  __shared__ double red[kCholThreads / kWarp];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kCholThreads / kWarp;
+  const long long off = (long long)node * K * K;
+  const double* Wg = c.W + off;
+
+  double dev = 0.0;
+  bool nonfinite = false;
+  for (int e = tid; e < K * K; e += kCholThreads) {
+    const int i = e / K, l = e - i * K;
+    const double v = Wg[e];
+    W[i * pitch + l] = v;
+    if (l >= i) {
+      dev = fmax(dev, fabs(v - (i == l ? 1.0 : 0.0)));
+      nonfinite |= !isfinite(v);
+    }
+  }
+  const int any_nonfinite = __syncthreads_or(nonfinite);
+  for (int j = tid; j < K; j += kCholThreads) dorig[j] = W[j * pitch + j];
+  // block max of the identity deviation (checked in pass 2)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if (lane == 0) red[warp] = dev;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w]);
+    bad = any_nonfinite || (c.check_identity && !(m <= kIdentityTol)) ? 1 : 0;
+  }
+
+  for (int j = 0; j < K; ++j) {
+    const double d0 = dorig[j];
+    double p = W[j * pitch + j];
+    const bool ok = d0 > 1e-290 && isfinite(d0) && p > kPivotTol * d0 && isfinite(p);
+    if (!ok) p = (d0 > 1e-290 && isfinite(d0)) ? d0 : 1.0;  // keep going; the node is flagged
+    if (tid == 0) {
+      piv[j] = p;
+      if (!ok) bad = 1;
+    }
+    const double ip = 1.0 / p;
+    for (int i = j + 1 + warp; i < K; i += nwarps) {
+      const double mi = W[j * pitch + i] * ip;
+      double* Wi = W + i * pitch;
+      const double* Wj = W + j * pitch;
+      // Linv part c <= j
+      for (int cc = lane; cc <= j; cc += 32) Wi[cc] = (cc == j ? 0.0 : Wi[cc]) - mi * (cc == j ? 1.0 : Wj[cc]);
+      // upper part c >= i
+      for (int cc = i + lane; cc < K; cc += 32) Wi[cc] -= mi * Wj[cc];
+    }
+    __syncthreads();
+  }
+
+  for (int j = tid; j < K; j += kCholThreads) piv[j] = sqrt(piv[j]);
+  __syncthreads();
+  // R[i][l] = U[i][l] / sqrt(D_i)  (l >= i)
+  double* Rf = c.Rf + off;
+  double* Ri = c.Ri + off;
+  for (int e = tid; e < K * K; e += kCholThreads) {
+    const int i = e / K, l = e - i * K;
+    Rf[e] = l >= i ? W[i * pitch + l] / piv[i] : 0.0;
+    // element (i, l) of R^{-1} = L^{-T} D^{-1/2}: Linv[l][i] / sqrt(D_l) for i <= l
+    Ri[e] = i <= l ? (i == l ? 1.0 : W[l * pitch + i]) / piv[l] : 0.0;
+  }
+  if (tid == 0 && bad) atomicOr(cb.fail, 1);
+}
+
+size_t chol_smem(int K) { return sizeof(double) * ((size_t)K * (K + 1) + 2 * (size_t)K); }
+
+int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)chol_smem(kCholMaxK)));
+    attr = true;
+  }
+  size_t i = 0;
+  while (i < ds.size()) {
+    CholBatch b{};
+    b.fail = fail;
+    int blocks = 0, kmax = 1;
+    while (i < ds.size() && b.count < kCholMaxDescs) {
+      b.d[b.count] = ds[i];
+      b.block_begin[b.count] = blocks;
+      blocks += ds[i].nodes;
+      kmax = std::max(kmax, ds[i].K);
+      ++b.count;
+      ++i;
+    }
+    b.block_begin[b.count] = blocks;
+    double flops = 0;
+    for (int q = 0; q < b.count; ++q) flops += (double)b.d[q].nodes * b.d[q].K * b.d[q].K * b.d[q].K / 1.5;
+    ProfToken tok = prof_begin(s);
+    chol_kernel<<<blocks, kCholThreads, chol_smem(kmax), s>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "cholqr_factor", s, flops, 0.0);
+  }
+  return kOk;
+}
+
+}  // namespace
+
+bool cholqr_eligible(const QrProblem& q) { return q.K >= 1 && q.K <= kCholMaxK && q.m >= 2 * q.K; }
+
+long long cholqr_workspace_doubles(const CholQr& c) {
+  const long long K = c.q.K, n = c.q.nodes, m = c.q.m;
+  const long long kk = K * K * n;
+  return (c.S > 1 ? c.S * kk : 0) + kk + m * K * n + 4 * kk + 5 * 32;
+}
+
+void cholqr_bind(CholQr& c, double* ws) {
+  const long long K = c.q.K, n = c.q.nodes, m = c.q.m;
+  const long long kk = K * K * n;
+  auto al = [](double* p) { return (double*)(((uintptr_t)p + 255) & ~(uintptr_t)255); };
+  double* p = al(ws);
+  if (c.S > 1) {
+    c.P = p;
+    p = al(p + c.S * kk);
+  }
+  c.W = p; p = al(p + kk);
+  c.Q1 = p; p = al(p + m * K * n);
+  c.R1 = p; p = al(p + kk);
+  c.R2 = p; p = al(p + kk);
+  c.Ri = p;
+}
+
+int cholqr_run(std::vector<CholQr>& cs, int* fail, cudaStream_t s) {
+  if (cs.empty()) return kOk;
+  // Gram GEMM of X (m x K, element (r, i) at X + r*xr + i*xc, node stride xn) into W
+  auto gram = [&](std::vector<GemmDesc>& g, std::vector<ReduceDesc>& r, const CholQr& c, const double* X,
+                  long long xr, long long xc, long long xn) {
+    const int K = c.q.K, m = c.q.m, n = c.q.nodes;
+    GemmDesc d = gemm_desc(X, xc, xr, X, xr, xc, c.S > 1 ? c.P : c.W, K, 1, K, K, m);
+    d.nb1 = n; d.a_b1 = xn; d.b_b1 = xn; d.c_b1 = (long long)K * K;
+    d.splits = c.S;
+    g.push_back(d);
+    if (c.S > 1) r.push_back(ReduceDesc{c.P, c.W, K, 1, (long long)K * K, 0, c.S, K, K, n, 1, 0, 1.0, 0.0});
+  };
+  auto chol = [&](std::vector<CholDesc>& v, const CholQr& c, double* Rf, int check) {
+    v.push_back(CholDesc{c.W, Rf, c.Ri, c.q.K, c.q.nodes, check});
+  };
+  std::vector<GemmDesc> g;
+  std::vector<ReduceDesc> r;
+  std::vector<CholDesc> ch;
+  // pass 1
+  for (auto& c : cs) gram(g, r, c, c.q.A, c.q.a_r, c.q.a_c, c.q.a_node);
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_gram"));
+  HT_TRY(reduce_partials(r, s));
+  for (auto& c : cs) chol(ch, c, c.R1, 0);
+  HT_TRY(launch_chol(ch, fail, s));
+  g.clear(); r.clear(); ch.clear();
+  for (auto& c : cs) {  // Q1 = A Ri  (row-major m x K scratch)
+    const int K = c.q.K, m = c.q.m;
+    GemmDesc d = gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.Q1, K, 1, m, K, K);
+    d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K; d.c_b1 = (long long)m * K;
+    g.push_back(d);
+  }
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_q"));
+  g.clear();
+  // pass 2
+  for (auto& c : cs) gram(g, r, c, c.Q1, c.q.K, 1, (long long)c.q.m * c.q.K);
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_gram"));
+  HT_TRY(reduce_partials(r, s));
+  for (auto& c : cs) chol(ch, c, c.R2, 1);
+  HT_TRY(launch_chol(ch, fail, s));
+  g.clear();
+  for (auto& c : cs) {
+    const int K = c.q.K, m = c.q.m;
+    // Q = Q1 Ri into the caller's layout
+    GemmDesc d = gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+    d.nb1 = c.q.nodes; d.a_b1 = (long long)m * K; d.b_b1 = (long long)K * K; d.c_b1 = c.q.q_node;
+    g.push_back(d);
+    // R = R2 R1 (row-major, ld r_ld)
+    GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
+    e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
+    g.push_back(e);
+  }
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_q"));
+  return kOk;
+}
+
+}  // namespace ht

@@ -1,0 +1,42 @@
+// Tall-skinny QR by Cholesky-QR2 on DMMA GEMMs -- the fast path of the
+// orthogonalisation sweep (replaces reference kernels.py:24-32 reduced_qr for
+// well-conditioned frames; the Householder path of qr.cuh is the fallback).
+//
+//   W1 = A^T A          (split-K DMMA GEMM)      R1 = chol(W1), Ri = R1^{-1}
+//   Q1 = A Ri           (DMMA GEMM)
+//   W2 = Q1^T Q1                                 R2 = chol(W2), Ri = R2^{-1}
+//   Q  = Q1 Ri,  R = R2 R1
+//
+// For full-column-rank A the QR factorisation with diag(R) > 0 is unique, so the
+// result is the sign-fixed Householder QR of the reference up to rounding.
+// CholeskyQR2 is accurate to O(u) in orthogonality and residual while
+// kappa(A) << u^{-1/2}; the factor kernel flags a node (atomicOr on `fail`) when
+// a pivot loses more than 10 digits against its column norm, when anything is
+// non-finite, or when W2 is not within 0.1 of the identity.  The caller then
+// re-runs the whole sweep with Householder QR (exactly rank-deficient frames such
+// as add(A, A) always take that route).
+#pragma once
+
+#include <vector>
+
+#include "common.cuh"
+#include "qr.cuh"
+
+namespace ht {
+
+constexpr int kCholMaxK = 128;  // K x (K+1) doubles resident in shared memory
+
+struct CholQr {
+  QrProblem q;  // addressing of A / Q / R (m, K, nodes, strides); q.V unused
+  int S = 1;    // split-K of the two Gram GEMMs
+  double *P = nullptr, *W = nullptr, *Q1 = nullptr, *R1 = nullptr, *R2 = nullptr, *Ri = nullptr;
+};
+
+bool cholqr_eligible(const QrProblem& q);
+long long cholqr_workspace_doubles(const CholQr& c);
+void cholqr_bind(CholQr& c, double* ws);
+// Launch the 8-kernel sequence for all problems; *fail (device int) is OR-ed with 1
+// on any numerical red flag.  No host synchronisation.
+int cholqr_run(std::vector<CholQr>& cs, int* fail, cudaStream_t stream);
+
+}  // namespace ht

@@ -12,6 +12,7 @@
 #include <string>
 #include <vector>
 
+#include "cholqr.cuh"
 #include "common.cuh"
 #include "eig.cuh"
 #include "gemm.cuh"
@@ -262,8 +263,15 @@ struct OrthPlan {
 
 // Runs (or, in measure mode, sizes) the bottom-up sweep.  `out` pointers may be
 // supplied (ht_orthogonalize) or carved from the arena (truncate).
-int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec) {
+// QR policy: 0 = Cholesky-QR2 where eligible, validated, Householder re-run on a red
+// flag; 1 = Householder only.
+int g_qr_mode = 0;
+long long g_qr_fallbacks = 0;
+
+int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec,
+                      bool chol = false, int* fail = nullptr, int* n_chol = nullptr) {
   const Tree& T = *x.T;
+  if (n_chol) *n_chol = 0;
   op.ko = orth_ranks(x);
   const auto& ko = op.ko;
   if (op.out.empty()) {
@@ -322,14 +330,35 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       q.m = (int)(k1o * k2o); q.K = (int)kt; q.nodes = 1;
       qs.push_back(q);
     }
-    HT_TRY(plan_qrs(qs, scratch_ar));
+    merge_qrs(qs);
+    std::vector<QrProblem> hh;
+    std::vector<CholQr> cq;
+    for (const auto& q : qs) {
+      if (chol && cholqr_eligible(q)) {
+        CholQr c;
+        c.q = q;
+        cq.push_back(c);
+      } else {
+        hh.push_back(q);
+      }
+    }
+    long long ctiles = 0;
+    for (const auto& c : cq) ctiles += (long long)gemm_tiles(c.q.K, c.q.K) * c.q.nodes;
+    for (auto& c : cq) {
+      c.S = pick_splits(ctiles, c.q.m);
+      double* w = scratch_ar.take(cholqr_workspace_doubles(c));
+      if (scratch_ar.base) cholqr_bind(c, w);
+    }
+    if (n_chol) *n_chol += (int)cq.size();
+    HT_TRY(plan_qrs(hh, scratch_ar));
     scratch_max = std::max(scratch_max, scratch_ar.off);
     if (exec) {
       merge_gemms(g2);
       merge_gemms(g3);
       HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
-      HT_TRY(qr_batched(qs, s));
+      HT_TRY(cholqr_run(cq, fail, s));
+      HT_TRY(qr_batched(hh, s));
     }
   }
   // root: B_D <- R1 B_D R2^T (arith.py:144-145)
@@ -348,6 +377,33 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   }
   scratch_ar.off = scratch_max;
   return kOk;
+}
+
+// The orthogonalisation sweep as executed: Cholesky-QR2 first (if enabled), one
+// host synchronisation to read the red flag, Householder re-run if it is set.
+int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch, cudaStream_t s, int* fail) {
+  if (g_qr_mode == 0 && fail) {
+    HT_CUDA_CHECK(cudaMemsetAsync(fail, 0, sizeof(int), s));
+    Arena a = scratch;
+    int n_chol = 0;
+    HT_TRY(run_orthogonalize(x, op, a, a, s, true, true, fail, &n_chol));
+    if (n_chol == 0) return kOk;
+    int h = 0;
+    HT_CUDA_CHECK(cudaMemcpyAsync(&h, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+    HT_CUDA_CHECK(cudaStreamSynchronize(s));
+    if (!h) return kOk;
+    ++g_qr_fallbacks;
+  }
+  Arena a = scratch;
+  return run_orthogonalize(x, op, a, a, s, true, false, nullptr);
+}
+
+// scratch bytes of the sweep: the larger of the Cholesky-QR2 and Householder plans
+size_t orth_scratch_need(const View& x, OrthPlan op, const Arena& scratch) {
+  Arena a = scratch, b = scratch;
+  run_orthogonalize(x, op, a, a, nullptr, false, true);
+  run_orthogonalize(x, op, b, b, nullptr, false, false);
+  return std::max(a.off, b.off);
 }
 
 // ---------------------------------------------------------------------------
@@ -437,6 +493,7 @@ struct TruncPlan {
   std::vector<double*> G, EV, lam;
   int* ranks = nullptr;
   int* status = nullptr;
+  int* qr_fail = nullptr;
   Arena scratch;
 };
 
@@ -488,8 +545,9 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   for (int t = 1; t < T.nn; ++t) P.G[t] = ar.take(P.o.k[t] * P.o.k[t]);
   for (int t = 1; t < T.nn; ++t) P.EV[t] = ar.take(P.o.k[t] * P.o.k[t]);
   for (int t = 1; t < T.nn; ++t) P.lam[t] = ar.take(P.o.k[t]);
-  P.ranks = ar.take_int(T.nn + 1);
+  P.ranks = ar.take_int(T.nn + 2);
   P.status = P.ranks + T.nn;
+  P.qr_fail = P.ranks + T.nn + 1;
   P.scratch = ar;  // everything after this point is phase scratch
   return kOk;
 }
@@ -500,12 +558,7 @@ size_t truncate_ws_bytes(const View& x) {
   Arena sc = P.scratch;
   const size_t start = sc.off;
   size_t need = start;
-  if (!x.orth) {
-    Arena a2 = sc;
-    OrthPlan op = P.op;
-    run_orthogonalize(x, op, a2, a2, nullptr, false);
-    need = std::max(need, a2.off);
-  }
+  if (!x.orth) need = std::max(need, orth_scratch_need(x, P.op, sc));
   {
     Arena a3 = sc;
     run_gramians(P.o, P.G, a3, nullptr, false);
@@ -543,8 +596,7 @@ int check_ws(const View& x, char* ws, size_t ws_bytes) {
 
 int phase_orth(const View& x, TruncPlan& P, cudaStream_t s) {
   if (x.orth) return kOk;
-  Arena sc = P.scratch;
-  return run_orthogonalize(x, P.op, sc, sc, s, true);
+  return orth_sweep(x, P.op, P.scratch, s, P.qr_fail);
 }
 
 int phase_gram(TruncPlan& P, cudaStream_t s) {
@@ -965,8 +1017,8 @@ int ht_orthogonalize_workspace_size(const ht_tensor* x, size_t* bytes) {
   OrthPlan op;
   op.out.assign(v.T->nn, nullptr);
   Arena ar;
-  HT_TRY(run_orthogonalize(v, op, ar, ar, nullptr, false));
-  *bytes = ar.off + 4096 * (size_t)v.T->nn + 256;
+  ar.take_int(2);  // Cholesky-QR2 red flag
+  *bytes = orth_scratch_need(v, op, ar) + 4096 * (size_t)v.T->nn + 256;
   return kOk;
 }
 
@@ -990,8 +1042,20 @@ int ht_orthogonalize(const ht_tensor* x, void* ws, size_t ws_bytes, const ht_ten
   op.out = o.p;
   Arena ar;
   ar.base = (char*)ws;
-  return run_orthogonalize(v, op, ar, ar, (cudaStream_t)stream, true);
+  int* fail = ar.take_int(2);
+  return orth_sweep(v, op, ar, (cudaStream_t)stream, fail);
 }
+
+int ht_set_qr_mode(int mode) {
+  if (mode != 0 && mode != 1) {
+    set_error("qr mode must be 0 (Cholesky-QR2 with Householder fallback) or 1 (Householder)");
+    return kErrArgument;
+  }
+  g_qr_mode = mode;
+  return kOk;
+}
+
+int64_t ht_qr_fallback_count(void) { return g_qr_fallbacks; }
 
 int ht_gramians_workspace_size(const ht_tensor* x, size_t* bytes) {
   View v;

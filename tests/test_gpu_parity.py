@@ -16,11 +16,15 @@ SIGMA_RTOL = 1e-10
 ERR_TOL = 1e-10
 
 
-@pytest.fixture(scope="module")
-def htb(cuda_ok):
+@pytest.fixture(scope="module", params=["auto", "householder"])
+def htb(cuda_ok, request):
+    """Every parity test runs under both QR policies: Cholesky-QR2 with the
+    validated Householder fallback (default) and Householder only."""
     import paper_1708_03340_b200 as m
 
-    return m
+    m.set_qr_mode(request.param)
+    yield m
+    m.set_qr_mode("auto")
 
 
 def _sig_host(sig):
@@ -130,9 +134,17 @@ def test_rank_deficient_add_a_a(htb):
     tr = orc.balanced_tree(8)
     a = orc.gaussian_htensor(tr, 64, 10, 5)
     ad = to_dev(a)
-    T = htb.truncate(htb.add(ad, ad), htb.TruncationControl.fixed_rank(10))
+    n_fb = htb.qr_fallback_count()
+    x2 = htb.add(ad, ad)
+    T = htb.truncate(x2, htb.TruncationControl.fixed_rank(10))
     two_a = orc.scale(a, 2.0)
     assert rel_err(to_host(T), two_a) <= 1e-12
+    o = to_host(htb.orthogonalize(x2))
+    for t, u in o.U.items():  # frames stay orthonormal although [U, U] has rank k
+        np.testing.assert_allclose(u.T @ u, np.eye(u.shape[1]), atol=1e-13)
+    if htb.get_qr_mode() == "auto":
+        # the Cholesky-QR2 red flag must have fired (both sweeps re-run with Householder)
+        assert htb.qr_fallback_count() == n_fb + 2
 
 
 def test_c3_small_operator_then_truncate(htb):
@@ -174,10 +186,12 @@ def test_c2_d8_against_reference(htb):
     z = load("c2_d8.npz")
     a, c, x = orc.c2_inputs(8)
     xd = htb.add(to_dev(a), to_dev(c))
+    n_fb = htb.qr_fallback_count()
     sig = _sig_host(htb.hierarchical_singular_values(xd))
     for t, lam in node_dict(z, "lam", x.tree).items():
         np.testing.assert_allclose(sig[t], np.sqrt(lam), rtol=SIGMA_RTOL)
     T = htb.truncate(xd, htb.TruncationControl.fixed_rank(50))
+    assert htb.qr_fallback_count() == n_fb  # well-conditioned: the Cholesky-QR2 path is kept
     assert [T.rank(t) for t in range(1, 15)] == list(z["ranks_T"])
     np.testing.assert_allclose(htb.inner_product(T, T), float(z["ip_TT"]), rtol=1e-10)
     t_ref = orc.truncate(x, orc.Ctl(max_rank=50))
@@ -189,7 +203,9 @@ def test_c2_d64_headline_shape(htb):
     """BASELINE config C2 at the headline size (d=64, n=1000, k=50 -> rank 100 -> 50)."""
     a, c, x = orc.c2_inputs(64)
     xd = htb.add(to_dev(a), to_dev(c))
+    n_fb = htb.qr_fallback_count()
     T = htb.truncate(xd, htb.TruncationControl.fixed_rank(50))
+    assert htb.qr_fallback_count() == n_fb
     assert all(T.rank(t) == 50 for t in range(1, 127))
     t_ref = orc.truncate(x, orc.Ctl(max_rank=50))
     assert rel_err(to_host(T), t_ref) <= ERR_TOL
