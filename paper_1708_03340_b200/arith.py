@@ -11,6 +11,7 @@ inner products).
 from __future__ import annotations
 
 import ctypes
+import os
 import math
 from dataclasses import dataclass
 
@@ -79,8 +80,14 @@ class TruncationControl:
 # ---------------------------------------------------------------------------
 
 
+_POISON_WS = os.environ.get("HT_POISON_WORKSPACE") == "1"
+
+
 def _ws(nbytes: int, dev) -> torch.Tensor:
-    return torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+    w = torch.empty(max(int(nbytes), 256), dtype=torch.uint8, device=dev)
+    if _POISON_WS:  # debugging aid: NaN-fill so reads of unwritten workspace show up
+        w.fill_(0xFF)
+    return w
 
 
 def _sizes_by_node(x: HTensor) -> dict:

@@ -268,10 +268,10 @@ struct OrthPlan {
 int g_qr_mode = 0;
 long long g_qr_fallbacks = 0;
 
-int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec,
-                      bool chol = false, int* fail = nullptr, int* n_chol = nullptr) {
+// Node arrays of the orthogonalised tensor and the R factors, carved from `ar`
+// unless the caller supplied them (ht_orthogonalize / truncate plans).
+void orth_slots(const View& x, OrthPlan& op, Arena& ar) {
   const Tree& T = *x.T;
-  if (n_chol) *n_chol = 0;
   op.ko = orth_ranks(x);
   const auto& ko = op.ko;
   if (op.out.empty()) {
@@ -288,6 +288,14 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     op.R.assign(T.nn, nullptr);
     for (int t = 1; t < T.nn; ++t) op.R[t] = ar.take(ko[t] * x.k[t]);
   }
+}
+
+int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec,
+                      bool chol = false, int* fail = nullptr, int* n_chol = nullptr) {
+  const Tree& T = *x.T;
+  if (n_chol) *n_chol = 0;
+  orth_slots(x, op, ar);
+  const auto& ko = op.ko;
 
   const size_t scratch_base = scratch_ar.off;
   size_t scratch_max = scratch_base;
@@ -381,7 +389,9 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
 
 // The orthogonalisation sweep as executed: Cholesky-QR2 first (if enabled), one
 // host synchronisation to read the red flag, Householder re-run if it is set.
-int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch, cudaStream_t s, int* fail) {
+int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_t s, int* fail) {
+  Arena scratch = scratch_in;
+  orth_slots(x, op, scratch);  // fixed before either run: the re-run must not reuse their bytes
   if (g_qr_mode == 0 && fail) {
     HT_CUDA_CHECK(cudaMemsetAsync(fail, 0, sizeof(int), s));
     Arena a = scratch;
@@ -399,7 +409,9 @@ int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch, cudaStream_t s
 }
 
 // scratch bytes of the sweep: the larger of the Cholesky-QR2 and Householder plans
-size_t orth_scratch_need(const View& x, OrthPlan op, const Arena& scratch) {
+size_t orth_scratch_need(const View& x, OrthPlan op, const Arena& scratch_in) {
+  Arena scratch = scratch_in;
+  orth_slots(x, op, scratch);
   Arena a = scratch, b = scratch;
   run_orthogonalize(x, op, a, a, nullptr, false, true);
   run_orthogonalize(x, op, b, b, nullptr, false, false);

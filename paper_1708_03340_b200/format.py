@@ -13,11 +13,14 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 
 import numpy as np
 import torch
 
 from . import _lib
+
+_POISON = os.environ.get("HT_POISON_WORKSPACE") == "1"
 from .tree import DimensionTree, build_balanced_tree
 
 F64 = torch.float64
@@ -88,6 +91,8 @@ class HTensor:
         shapes = {t: node_shape(tree, t, sizes_by_node, ranks) for t in range(len(tree.nodes))}
         total = sum(math.prod(s) for s in shapes.values())
         arena = torch.empty(total, dtype=F64, device=dev)
+        if _POISON:  # debugging aid (HT_POISON_WORKSPACE=1): outputs start as NaN
+            arena.fill_(float("nan"))
         nodes, off = {}, 0
         for t in range(len(tree.nodes)):
             n = math.prod(shapes[t])

@@ -4,6 +4,8 @@ import sys
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+# NaN-fill every workspace and output arena so reads of unwritten memory fail tests
+os.environ.setdefault("HT_POISON_WORKSPACE", "1")
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
