@@ -524,6 +524,54 @@ def orth_difference_norm(x: HT, y: HT) -> float:
 
 
 # ---------------------------------------------------------------------------
+# CG with truncation (solvers.py:172-231): the direct caller of the hot path
+# ---------------------------------------------------------------------------
+
+
+def ones_htensor(tr: Tree, n: int) -> HT:
+    """Rank-1 all-ones tensor (the reference's constant right-hand side shape)."""
+    U = {t: np.ones((n, 1)) for t in tr.leaves_by_dim()}
+    B = {t: np.ones((1, 1, 1)) for t in tr.inner_ids()}
+    return HT(tr, U, B, np.ones((1, 1)))
+
+
+def cg_solve(op: HTOp, rhs: HT, ctl: Ctl, eps_stop: float, max_steps: int):
+    """solvers.py:183-231 (_cg_loop with trace): X0 = rhs, truncation after every
+    add / apply, stop on sqrt(<R,R>) <= eps_stop or max_steps, abort on <D,AD> <= 0.
+    Returns (X, internal residuals, true relative residuals)."""
+    b = rhs
+    b_neg = scale(b, -1.0)
+    norm_b = norm(b)
+
+    def true_res(x):  # solvers.py:163-170
+        ax = truncate(apply_operator(op, x), ctl)
+        return norm(add(ax, b_neg)) / norm_b
+
+    x = b
+    r = truncate(add(b, scale(apply_operator(op, x), -1.0)), ctl)
+    d = r
+    rr = inner_product(r, r)
+    internal, true = [math.sqrt(max(0.0, rr))], [true_res(x)]
+    j = 0
+    while math.sqrt(max(0.0, rr)) > eps_stop and j < max_steps:
+        z = truncate(apply_operator(op, d), ctl)
+        dz = inner_product(d, z)
+        if dz <= 0.0:
+            break
+        alpha = rr / dz
+        x = truncate(add(x, scale(d, alpha)), ctl)
+        r_new = truncate(add(r, scale(z, -alpha)), ctl)
+        rr_new = inner_product(r_new, r_new)
+        beta = rr_new / rr
+        d = truncate(add(scale(d, beta), r_new), ctl)
+        r, rr = r_new, rr_new
+        j += 1
+        internal.append(math.sqrt(max(0.0, rr)))
+        true.append(true_res(x))
+    return x, internal, true
+
+
+# ---------------------------------------------------------------------------
 # seeded generators (SURVEY §8(d))
 # ---------------------------------------------------------------------------
 

@@ -210,6 +210,29 @@ def golden_c3_small():
     np.savez_compressed(os.path.join(OUT, "c3_small.npz"), **out)
 
 
+def golden_cg():
+    """The reference's own CG (solvers.cg_solve, SerialBackend) on a small Laplace
+    problem: d=4, n=16, rhs = all-ones rank 1, eps 1e-7 absolute + cap 6, 8 steps."""
+    from htucker import solvers as ref_solvers
+
+    tree = ref.build_balanced_tree(4)
+    otr = orc.balanced_tree(4)
+    op = orc.laplace_operator(otr, 16)
+    rop = ref.HTOperator(tree, {t: [ref.GeneralizedMatrix.diagonal(w[0].data),
+                                    ref.GeneralizedMatrix.csr(w[1].data)] for t, w in op.W.items()},
+                         dict(op.H), op.root.copy())
+    rhs = to_ref(orc.ones_htensor(otr, 16))
+    cfg = ref_solvers.SolverConfig(truncation=ref.TruncationControl(eps=1e-7, max_rank=6), eps_stop=1e-10,
+                                   max_cg_steps=8)
+    x, trace = ref_solvers.cg_solve(rop, rhs, cfg)
+    out = {"meta": meta()}
+    pack("Xcg", x, out)
+    out["ranks_X"] = np.array([x.rank(t) for t in range(1, 7)])
+    out["internal"] = np.array([e.internal_residual for e in trace.entries])
+    out["true_rel"] = np.array([e.true_rel_residual for e in trace.entries])
+    np.savez_compressed(os.path.join(OUT, "cg.npz"), **out)
+
+
 def golden_spec():
     """Known answers quoted in the SPEC."""
     q, r = ref_kernels.reduced_qr(np.array([[3.0], [4.0]]))
@@ -230,4 +253,5 @@ if __name__ == "__main__":
     golden_c1()
     golden_c3_small()
     golden_c2_d8()
+    golden_cg()
     print("golden fixtures written to", OUT)

@@ -164,3 +164,17 @@ def test_c2_d8_sigmas():
     t_ = orc.truncate(x, orc.Ctl(max_rank=50))
     assert [t_.rank(t) for t in range(1, 15)] == list(z["ranks_T"])
     np.testing.assert_allclose(orc.inner_product(t_, t_), float(z["ip_TT"]), rtol=1e-10)
+
+
+def test_oracle_cg_matches_reference_cg():
+    """The oracle's CG (solvers.py:172-231 restated) against the reference's own
+    cg_solve run in the build container (tests/golden/cg.npz)."""
+    z = load("cg.npz")
+    tr = orc.balanced_tree(4)
+    x, internal, true = orc.cg_solve(orc.laplace_operator(tr, 16), orc.ones_htensor(tr, 16),
+                                     orc.Ctl(eps=1e-7, max_rank=6), 1e-10, 8)
+    np.testing.assert_allclose(internal, z["internal"], rtol=1e-12)
+    np.testing.assert_allclose(true, z["true_rel"], rtol=1e-12)
+    assert [x.rank(t) for t in range(1, 7)] == list(z["ranks_X"])
+    ref = unpack(z, "Xcg", tr)
+    assert orc.orth_difference_norm(x, ref) <= 1e-12 * orc.norm(ref)
