@@ -31,107 +31,127 @@ struct CholBatch {
   int* fail;
 };
 
-// One CTA per K x K Gram matrix.  Symmetric Gaussian elimination on the upper
-// triangle (W = L D L^T, U = D L^T), carrying L^{-1} in the strictly lower
-// triangle of the same shared array: at step j every row i > j does
+// One CTA per K x K Gram matrix (K <= 128).  Symmetric Gaussian elimination
+// (W = L D L^T, U = D L^T) with L^{-1} carried in the strictly lower triangle:
+// at step j every row i > j does
 //   U[i][c]    -= m_i U[j][c]     (c >= i)          m_i = U[j][i] / U[j][j]
 //   Linv[i][c] -= m_i Linv[j][c]  (c <  j),  Linv[i][j] = -m_i
-// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.  One barrier per column.
-__global__ void __launch_bounds__(kCholThreads) chol_kernel(const __grid_constant__ CholBatch cb) {
+// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.
+// Register-resident: thread (row i = tid/4, sub = tid%4) keeps W[i][sub + 4q],
+// q < 32, in registers; row j is broadcast through a double-buffered shared row,
+// so each step is one barrier plus 32 independent FMAs per thread.
+constexpr int kCholTPR = 4;                  // threads per row
+constexpr int kCholCPT = kCholMaxK / kCholTPR;  // columns per thread
+
+__global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_constant__ CholBatch cb) {
   int di = 0;
   while (di + 1 < cb.count && (int)blockIdx.x >= cb.block_begin[di + 1]) ++di;
   const CholDesc& c = cb.d[di];
   const int node = blockIdx.x - cb.block_begin[di];
-  const int K = c.K, pitch = K + 1;
-  extern __shared__ double sm[];
-  double* W = sm;                 // K x pitch
-  double* dorig = sm + K * pitch; // K
-  double* piv = dorig + K;        // K
+  const int K = c.K;
+  __shared__ double rowbuf[2][kCholMaxK];
+  __shared__ double dorig[kCholMaxK];
+  __shared__ double sqd[kCholMaxK];
   __shared__ double red[kCholThreads / kWarp];
   __shared__ int bad;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kCholThreads / kWarp;
+  const int i = tid / kCholTPR, sub = tid % kCholTPR;
+  const bool row_ok = i < K;
   const long long off = (long long)node * K * K;
   const double* Wg = c.W + off;
 
+  double w[kCholCPT];
   double dev = 0.0;
   bool nonfinite = false;
-  for (int e = tid; e < K * K; e += kCholThreads) {
-    const int i = e / K, l = e - i * K;
-    const double v = Wg[e];
-    W[i * pitch + l] = v;
-    if (l >= i) {
-      dev = fmax(dev, fabs(v - (i == l ? 1.0 : 0.0)));
-      nonfinite |= !isfinite(v);
+#pragma unroll
+  for (int q = 0; q < kCholCPT; ++q) {
+    const int cc = sub + kCholTPR * q;
+    double v = 0.0;
+    if (row_ok && cc < K) {
+      v = Wg[(long long)i * K + cc];
+      if (cc >= i) {
+        dev = fmax(dev, fabs(v - (cc == i ? 1.0 : 0.0)));
+        nonfinite |= !isfinite(v);
+      }
+      if (cc == i) dorig[i] = v;
     }
+    w[q] = v;
   }
   const int any_nonfinite = __syncthreads_or(nonfinite);
-  for (int j = tid; j < K; j += kCholThreads) dorig[j] = W[j * pitch + j];
-  // block max of the identity deviation (checked in pass 2)
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
   if (lane == 0) red[warp] = dev;
   __syncthreads();
   if (tid == 0) {
     double m = 0.0;
-    for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w]);
+    for (int q = 0; q < nwarps; ++q) m = fmax(m, red[q]);
     bad = any_nonfinite || (c.check_identity && !(m <= kIdentityTol)) ? 1 : 0;
   }
 
   for (int j = 0; j < K; ++j) {
+    double* rb = rowbuf[j & 1];
+    if (i == j) {
+#pragma unroll
+      for (int q = 0; q < kCholCPT; ++q) rb[sub + kCholTPR * q] = w[q];
+    }
+    __syncthreads();
     const double d0 = dorig[j];
-    double p = W[j * pitch + j];
+    double p = rb[j];
     const bool ok = d0 > 1e-290 && isfinite(d0) && p > kPivotTol * d0 && isfinite(p);
     if (!ok) p = (d0 > 1e-290 && isfinite(d0)) ? d0 : 1.0;  // keep going; the node is flagged
     if (tid == 0) {
-      piv[j] = p;
+      sqd[j] = p;
       if (!ok) bad = 1;
     }
-    const double ip = 1.0 / p;
-    for (int i = j + 1 + warp; i < K; i += nwarps) {
-      const double mi = W[j * pitch + i] * ip;
-      double* Wi = W + i * pitch;
-      const double* Wj = W + j * pitch;
-      // Linv part c <= j
-      for (int cc = lane; cc <= j; cc += 32) Wi[cc] = (cc == j ? 0.0 : Wi[cc]) - mi * (cc == j ? 1.0 : Wj[cc]);
-      // upper part c >= i
-      for (int cc = i + lane; cc < K; cc += 32) Wi[cc] -= mi * Wj[cc];
+    if (row_ok && i > j) {
+      const double mi = rb[i] * __drcp_rn(p);
+#pragma unroll
+      for (int q0 = 0; q0 < kCholCPT; q0 += 8) {
+        double r[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) r[u] = rb[sub + kCholTPR * (q0 + u)];  // independent loads
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          // Every column is updated: c < j (Linv) and c >= i (U) need it; columns
+          // j < c < i hold not-yet-defined Linv[i][c] and are overwritten at step c;
+          // c >= K stays 0 (zero buffer entries).  Only c == j is special.
+          const int q = q0 + u, cc = sub + kCholTPR * q;
+          const double t = fma(-mi, r[u], w[q]);
+          w[q] = cc == j ? -mi : t;
+        }
+      }
     }
-    __syncthreads();
   }
-
-  for (int j = tid; j < K; j += kCholThreads) piv[j] = sqrt(piv[j]);
   __syncthreads();
-  // R[i][l] = U[i][l] / sqrt(D_i)  (l >= i)
+  for (int j = tid; j < K; j += kCholThreads) sqd[j] = sqrt(sqd[j]);
+  __syncthreads();
   double* Rf = c.Rf + off;
   double* Ri = c.Ri + off;
-  for (int e = tid; e < K * K; e += kCholThreads) {
-    const int i = e / K, l = e - i * K;
-    Rf[e] = l >= i ? W[i * pitch + l] / piv[i] : 0.0;
-    // element (i, l) of R^{-1} = L^{-T} D^{-1/2}: Linv[l][i] / sqrt(D_l) for i <= l
-    Ri[e] = i <= l ? (i == l ? 1.0 : W[l * pitch + i]) / piv[l] : 0.0;
+  if (row_ok) {
+    const double si = sqd[i];
+#pragma unroll
+    for (int q = 0; q < kCholCPT; ++q) {
+      const int cc = sub + kCholTPR * q;
+      if (cc >= K) continue;
+      // R[i][cc] = U[i][cc] / sqrt(D_i) (cc >= i)
+      Rf[(long long)i * K + cc] = cc >= i ? w[q] / si : 0.0;
+      // R^{-1}(cc, i) = Linv[i][cc] / sqrt(D_i) for cc <= i; zeros below the diagonal
+      Ri[(long long)cc * K + i] = cc < i ? w[q] / si : (cc == i ? 1.0 / si : 0.0);
+    }
   }
   if (tid == 0 && bad) atomicOr(cb.fail, 1);
 }
 
-size_t chol_smem(int K) { return sizeof(double) * ((size_t)K * (K + 1) + 2 * (size_t)K); }
-
 int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)chol_smem(kCholMaxK)));
-    attr = true;
-  }
   size_t i = 0;
   while (i < ds.size()) {
     CholBatch b{};
     b.fail = fail;
-    int blocks = 0, kmax = 1;
+    int blocks = 0;
     while (i < ds.size() && b.count < kCholMaxDescs) {
       b.d[b.count] = ds[i];
       b.block_begin[b.count] = blocks;
       blocks += ds[i].nodes;
-      kmax = std::max(kmax, ds[i].K);
       ++b.count;
       ++i;
     }
@@ -139,7 +159,7 @@ int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s) {
     double flops = 0;
     for (int q = 0; q < b.count; ++q) flops += (double)b.d[q].nodes * b.d[q].K * b.d[q].K * b.d[q].K / 1.5;
     ProfToken tok = prof_begin(s);
-    chol_kernel<<<blocks, kCholThreads, chol_smem(kmax), s>>>(b);
+    chol_kernel<<<blocks, kCholThreads, 0, s>>>(b);
     HT_LAUNCH_CHECK();
     prof_end(tok, "cholqr_factor", s, flops, 0.0);
   }

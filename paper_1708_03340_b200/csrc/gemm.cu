@@ -136,22 +136,34 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant_
   const bool a_kc = (g.a_k == 1), b_kc = (g.b_k == 1);
 
   // Fast path (plain operands; two-level reductions with K >= 16): every thread copies
-  // fixed tile slots; per k-tile only the (outer, inner) reduction offset changes.
+  // fixed tile slots.  Each slot keeps a running global pointer that advances by BK
+  // reduction steps per tile (plus the outer-index jump when the inner index wraps),
+  // so the steady-state loader is one predicated cp.async and a 64-bit add per slot.
   constexpr int NA = (BM * BK + THREADS - 1) / THREADS, NBB = (BN * BK + THREADS - 1) / THREADS;
   const bool fast = g.a_tri == 0 && g.b_tri == 0 && (g.KO == 1 || g.K >= BK);
+  const int gK = g.K;
+  const bool two_level = g.KO > 1;
+  const long long a_step = (long long)BK * g.a_k, b_step = (long long)BK * g.b_k;
+  const long long a_wrap = g.a_o - (long long)gK * g.a_k, b_wrap = g.b_o - (long long)gK * g.b_k;
   const double* pa[NA];
   const double* pb[NBB];
-  int oa[NA], ob[NBB], ka[NA], kb[NBB];
+  int kia[NA], kib[NBB];  // current inner reduction index of each slot (two-level case)
   if (fast) {
+    const long long o_b = two_level ? k_begin / gK : 0;
+    const long long k_b = two_level ? k_begin - o_b * gK : k_begin;
 #pragma unroll
     for (int q = 0; q < NA; ++q) {
       const int e = tid + q * THREADS;
       const int kk = a_kc ? (e % BK) : (e / BM);
       const int mm = a_kc ? (e / BK) : (e % BM);
       const bool ok = e < BM * BK && m0 + mm < g.M;
-      oa[q] = ok ? kk * PA + mm : -1;
-      ka[q] = kk;
-      pa[q] = A + (long long)(ok ? m0 + mm : 0) * g.a_m;
+      long long k = k_b + kk, o = o_b;
+      if (two_level && k >= gK) {
+        k -= gK;
+        ++o;
+      }
+      kia[q] = ok ? (int)k : -1;
+      pa[q] = A + (long long)(ok ? m0 + mm : 0) * g.a_m + k * g.a_k + o * g.a_o;
     }
 #pragma unroll
     for (int q = 0; q < NBB; ++q) {
@@ -159,9 +171,28 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant_
       const int kk = b_kc ? (e % BK) : (e / BN);
       const int nn = b_kc ? (e / BK) : (e % BN);
       const bool ok = e < BN * BK && n0 + nn < g.N;
-      ob[q] = ok ? kk * PB + nn : -1;
-      kb[q] = kk;
-      pb[q] = Bp + (long long)(ok ? n0 + nn : 0) * g.b_n;
+      long long k = k_b + kk, o = o_b;
+      if (two_level && k >= gK) {
+        k -= gK;
+        ++o;
+      }
+      kib[q] = ok ? (int)k : -1;
+      pb[q] = Bp + (long long)(ok ? n0 + nn : 0) * g.b_n + k * g.b_k + o * g.b_o;
+    }
+    // rows / columns beyond the matrix edge are zero in every stage, once
+#pragma unroll
+    for (int q = 0; q < NA; ++q) {
+      const int e = tid + q * THREADS;
+      if (kia[q] < 0 && e < BM * BK)
+        for (int st = 0; st < STAGES; ++st)
+          As[st * BK * PA + (a_kc ? (e % BK) : (e / BM)) * PA + (a_kc ? (e / BK) : (e % BM))] = 0.0;
+    }
+#pragma unroll
+    for (int q = 0; q < NBB; ++q) {
+      const int e = tid + q * THREADS;
+      if (kib[q] < 0 && e < BN * BK)
+        for (int st = 0; st < STAGES; ++st)
+          Bs[st * BK * PB + (b_kc ? (e % BK) : (e / BN)) * PB + (b_kc ? (e / BK) : (e % BN))] = 0.0;
     }
   }
 
@@ -170,40 +201,42 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant_
     double* bs = Bs + stage * BK * PB;
     const long long fb = k_begin + (long long)t * BK;
     if (fast) {
-      const long long krem = k_end - fb;
-      long long o0 = 0, k0 = fb;
-      if (g.KO > 1) {
-        o0 = fb / g.K;
-        k0 = fb - o0 * g.K;
-      }
+      const long long krem_l = k_end - fb;
+      const int krem = krem_l < BK ? (int)krem_l : BK;
 #pragma unroll
       for (int q = 0; q < NA; ++q) {
-        if (oa[q] >= 0) {
-          const bool ok = ka[q] < krem;
-          long long k = k0 + ka[q], o = o0;
-          if (k >= g.K) {
-            k -= g.K;
-            ++o;
-          }
-          cp8z(as + oa[q], ok ? pa[q] + k * g.a_k + o * g.a_o : A, ok);
-        } else if (tid + q * THREADS < BM * BK) {
+        if (kia[q] >= 0) {
           const int e = tid + q * THREADS;
-          as[(a_kc ? (e % BK) : (e / BM)) * PA + (a_kc ? (e / BK) : (e % BM))] = 0.0;
+          const int kk = a_kc ? (e % BK) : (e / BM);
+          const int mm = a_kc ? (e / BK) : (e % BM);
+          const bool ok = kk < krem;
+          cp8z(as + kk * PA + mm, ok ? pa[q] : A, ok);
+          pa[q] += a_step;
+          if (two_level) {
+            kia[q] += BK;
+            if (kia[q] >= gK) {
+              kia[q] -= gK;
+              pa[q] += a_wrap;
+            }
+          }
         }
       }
 #pragma unroll
       for (int q = 0; q < NBB; ++q) {
-        if (ob[q] >= 0) {
-          const bool ok = kb[q] < krem;
-          long long k = k0 + kb[q], o = o0;
-          if (k >= g.K) {
-            k -= g.K;
-            ++o;
-          }
-          cp8z(bs + ob[q], ok ? pb[q] + k * g.b_k + o * g.b_o : Bp, ok);
-        } else if (tid + q * THREADS < BN * BK) {
+        if (kib[q] >= 0) {
           const int e = tid + q * THREADS;
-          bs[(b_kc ? (e % BK) : (e / BN)) * PB + (b_kc ? (e / BK) : (e % BN))] = 0.0;
+          const int kk = b_kc ? (e % BK) : (e / BN);
+          const int nn = b_kc ? (e / BK) : (e % BN);
+          const bool ok = kk < krem;
+          cp8z(bs + kk * PB + nn, ok ? pb[q] : Bp, ok);
+          pb[q] += b_step;
+          if (two_level) {
+            kib[q] += BK;
+            if (kib[q] >= gK) {
+              kib[q] -= gK;
+              pb[q] += b_wrap;
+            }
+          }
         }
       }
       return;
@@ -269,21 +302,41 @@ __global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant_
 
   if (g.splits == 1) {
     double* C = g.C + b1 * g.c_b1 + b2 * g.c_b2;
+    const double alpha = g.alpha, beta = g.beta;
+    const long long c_m = g.c_m, c_n = g.c_n;
+    const int M = g.M, N = g.N;
+    // paired 16-byte stores when the row is contiguous and 16-byte aligned
+    const bool pair = c_n == 1 && (c_m & 1) == 0 && (((uintptr_t)C) & 15) == 0;
 #pragma unroll
-    for (int i = 0; i < WM; ++i)
+    for (int i = 0; i < WM; ++i) {
+      const int m = m0 + wm * WM * 8 + i * 8 + (lane >> 2);
+      if (m >= M) continue;
+      double* row = C + (long long)m * c_m;
 #pragma unroll
-      for (int j = 0; j < WN; ++j)
+      for (int j = 0; j < WN; ++j) {
+        const int n = n0 + wn * WN * 8 + j * 8 + 2 * (lane & 3);
+        if (pair && n + 1 < N) {
+          double2 r = make_double2(alpha * acc[i][j][0], alpha * acc[i][j][1]);
+          double2* p = reinterpret_cast<double2*>(row + n);
+          if (beta != 0.0) {
+            const double2 o = *p;
+            r.x += beta * o.x;
+            r.y += beta * o.y;
+          }
+          *p = r;
+        } else {
 #pragma unroll
-        for (int v = 0; v < 2; ++v) {
-          const int m = m0 + wm * WM * 8 + i * 8 + (lane >> 2);
-          const int n = n0 + wn * WN * 8 + j * 8 + 2 * (lane & 3) + v;
-          if (m < g.M && n < g.N) {
-            double* p = C + m * g.c_m + n * g.c_n;
-            double r = g.alpha * acc[i][j][v];
-            if (g.beta != 0.0) r += g.beta * *p;
-            *p = r;
+          for (int v = 0; v < 2; ++v) {
+            if (n + v < N) {
+              double* p = row + (long long)(n + v) * c_n;
+              double r = alpha * acc[i][j][v];
+              if (beta != 0.0) r += beta * *p;
+              *p = r;
+            }
           }
         }
+      }
+    }
   } else {
     const long long nbatch = (long long)g.nb1 * g.nb2;
     double* P = g.C + ((long long)split * nbatch + b) * g.M * g.N;
