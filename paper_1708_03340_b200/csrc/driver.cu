@@ -244,12 +244,24 @@ int plan_qrs(std::vector<QrProblem>& qs, Arena& ar) {
   return kOk;
 }
 
-// split-K count so a level's reduction GEMMs fill the GPU (>= ~2 CTAs per SM, each
-// split keeping >= 4 k-tiles)
+// split-K count for a level's reduction GEMMs.  The GEMM runs one 256-thread CTA per
+// SM, so the launch takes ceil(tiles*S / 148) waves of ceil(L / (S*BK)) k-tiles plus
+// a fill/drain overhead of ~3 k-tiles per CTA; pick the S that minimises that.
 int pick_splits(long long tiles_total, long long reduction) {
-  long long s = std::max<long long>(1, (2 * kSMs + tiles_total - 1) / std::max<long long>(1, tiles_total));
-  s = std::min<long long>(s, std::max<long long>(1, reduction / (kGemmBK * 4)));
-  return (int)std::min<long long>(s, 160);
+  const long long T = std::max<long long>(1, tiles_total);
+  const long long ktiles = std::max<long long>(1, (reduction + kGemmBK - 1) / kGemmBK);
+  const long long smax = std::min<long long>(160, std::max<long long>(1, ktiles / 4));
+  long long best_s = 1;
+  double best = 1e300;
+  for (long long S = 1; S <= smax; ++S) {
+    const long long waves = (T * S + kSMs - 1) / kSMs;
+    const double cost = (double)waves * ((double)((ktiles + S - 1) / S) + 3.0) + 0.02 * S;  // + reduce cost
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_s = S;
+    }
+  }
+  return (int)best_s;
 }
 
 // ---------------------------------------------------------------------------
