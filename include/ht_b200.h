@@ -187,6 +187,16 @@ int ht_set_qr_mode(int mode);
 /* Number of Cholesky-QR2 sweeps that were re-run with Householder QR. */
 int64_t ht_qr_fallback_count(void);
 
+/* Eigensolver policy of the truncation (process-wide).
+ *   0 (default): Householder tridiagonalisation + multisection bisection +
+ *      twisted-factorisation eigenvectors of the kept eigenpairs; nodes with a
+ *      graded spectrum (min|lambda| < 1e-6 max|lambda|) or near-degenerate kept
+ *      eigenvalues are redone by the Jacobi kernel in the same stream (no sync);
+ *   1: parallel cyclic Jacobi for every node.
+ * Both return dsyevd's eigenpairs (kernels.py:35-54) up to rounding / eigenvector
+ * sign.  (ht_syev_batched always uses Jacobi.) */
+int ht_set_eig_mode(int mode);
+
 /* ---- instrumentation -------------------------------------------------- */
 
 /* Total kernel launches issued by this library since load (always counted). */

@@ -13,6 +13,7 @@ from .arith import (
     apply_operator,
     compute_bhat,
     gemm,
+    get_eig_mode,
     get_qr_mode,
     hierarchical_singular_values,
     inner_product,
@@ -22,6 +23,7 @@ from .arith import (
     orthogonalize,
     qr_fallback_count,
     scale,
+    set_eig_mode,
     set_qr_mode,
     subtract,
     truncate,
@@ -51,6 +53,7 @@ __all__ = [
     "gaussian_factors",
     "gaussian_htensor",
     "gemm",
+    "get_eig_mode",
     "get_qr_mode",
     "hierarchical_singular_values",
     "identity_htoperator",
@@ -63,6 +66,7 @@ __all__ = [
     "random_htensor",
     "qr_fallback_count",
     "scale",
+    "set_eig_mode",
     "set_qr_mode",
     "storage_size",
     "subtract",

@@ -307,6 +307,25 @@ def get_qr_mode() -> str:
     return _qr_mode
 
 
+_EIG_MODES = {"auto": 0, "jacobi": 1}
+_eig_mode = "auto"
+
+
+def set_eig_mode(mode: str) -> None:
+    """Eigensolver policy of truncate (process-wide): ``"auto"`` (default) runs the
+    tridiagonal fast path and redoes graded / near-degenerate nodes with Jacobi;
+    ``"jacobi"`` uses Jacobi everywhere.  Both match sym_eig_desc (kernels.py:35-54)."""
+    global _eig_mode
+    if mode not in _EIG_MODES:
+        raise ValueError(f"eig mode must be one of {sorted(_EIG_MODES)}")
+    _lib.check(_lib.load().ht_set_eig_mode(_EIG_MODES[mode]), "set_eig_mode")
+    _eig_mode = mode
+
+
+def get_eig_mode() -> str:
+    return _eig_mode
+
+
 def qr_fallback_count() -> int:
     """How many Cholesky-QR2 sweeps were recomputed with Householder QR."""
     return int(_lib.load().ht_qr_fallback_count())

@@ -518,6 +518,7 @@ struct TruncPlan {
   int* ranks = nullptr;
   int* status = nullptr;
   int* qr_fail = nullptr;
+  int* eigflag = nullptr;  // per node: redo with Jacobi (set by the tridiagonal fast path)
   Arena scratch;
 };
 
@@ -572,6 +573,7 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   P.ranks = ar.take_int(T.nn + 2);
   P.status = P.ranks + T.nn;
   P.qr_fail = P.ranks + T.nn + 1;
+  P.eigflag = ar.take_int(T.nn);
   P.scratch = ar;  // everything after this point is phase scratch
   return kOk;
 }
@@ -637,6 +639,7 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     EigProblem e{};
     e.S = P.G[t]; e.V = P.EV[t]; e.lam = P.lam[t];
     e.rank = P.ranks + t; e.status = P.status;
+    e.fallback = P.eigflag + t;
     e.K = (int)P.o.k[t]; e.nodes = 1;
     e.eps = ctl->eps > 0 ? ctl->eps : 0.0;
     e.n_nonroot = T.nn - 1;
@@ -644,7 +647,7 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     e.s_node = 0; e.v_node = 0; e.l_node = 0;
     if (!eps.empty()) {
       EigProblem& b = eps.back();
-      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank) {
+      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback) {
         if (b.nodes == 1) {
           b.s_node = e.S - b.S; b.v_node = e.V - b.V; b.l_node = e.lam - b.lam;
           b.nodes = 2;
@@ -1080,6 +1083,15 @@ int ht_set_qr_mode(int mode) {
 }
 
 int64_t ht_qr_fallback_count(void) { return g_qr_fallbacks; }
+
+int ht_set_eig_mode(int mode) {
+  if (mode != 0 && mode != 1) {
+    set_error("eig mode must be 0 (tridiagonal fast path with Jacobi fallback) or 1 (Jacobi)");
+    return kErrArgument;
+  }
+  g_eig_mode = mode;
+  return kOk;
+}
 
 int ht_gramians_workspace_size(const ht_tensor* x, size_t* bytes) {
   View v;

@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   while (di + 1 < b.count && (int)blockIdx.x >= b.begin[di + 1]) ++di;
   const EigProblem& e = b.d[di];
   const int nd = blockIdx.x - b.begin[di];
+  if (e.fallback && e.fallback[nd] == 0) return;  // served by the tridiagonal fast path
   const int K = e.K;
   const int n = K + (K & 1);
   const int ap = n + 1;
@@ -220,7 +221,14 @@ bool g_attr = false;
 
 }  // namespace
 
+int g_eig_mode = 0;
+
 int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
+  bool tri = g_eig_mode == 0;
+  for (const auto& p : probs) tri = tri && p.fallback != nullptr && p.K <= kEigMaxK;
+  if (tri) HT_TRY(eig_tri_batched(probs, stream));
+  else
+    for (auto& p : probs) p.fallback = nullptr;
   if (!g_attr) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     g_attr = true;

@@ -3,10 +3,11 @@
 // order, eigenvalues clamped >= 0 (kernels.py:35-54) and the per-node rank
 // choice of select_rank (arith.py:69-88) -- all on device, no host sync.
 //
-// Jacobi (rather than tridiagonalisation) because the reduced Gramians of the
-// C1 parity case are graded: their small eigenvalues (~1e-20 relative) are only
-// determined to high RELATIVE accuracy by a Jacobi method with the
-// |a_pq| <= eps*sqrt(|a_pp a_qq|) stopping rule (Demmel-Veselic).
+// Two kernels: the tridiagonal fast path (eig_tri.cu) and parallel cyclic Jacobi.
+// Jacobi is kept for graded Gramians -- e.g. the C1 parity case, whose small
+// eigenvalues (~1e-20 relative) are only determined to high RELATIVE accuracy by a
+// Jacobi method with the |a_pq| <= eps*sqrt(|a_pp a_qq|) stopping rule
+// (Demmel-Veselic) -- and for near-degenerate kept eigenvalues.
 #pragma once
 
 #include <vector>
@@ -28,12 +29,19 @@ struct EigProblem {
   double eps;       // absolute truncation accuracy; <= 0: none
   int n_nonroot;    // 2d - 2
   int cap;          // rank cap; <= 0: none
+  int* fallback;    // per-node flags (node stride 1): set by the tridiagonal fast path for
+                    // nodes the Jacobi kernel must redo; null = Jacobi for every node
 };
 
 constexpr int kEigMaxK = 112;
 constexpr int kEigStatusNotSymmetric = 1;
 constexpr int kEigStatusNonConverged = 2;
 
+// Eigensolver policy (process-wide): 0 = tridiagonal fast path with Jacobi for the
+// nodes it flags (needs EigProblem::fallback), 1 = Jacobi only.
+extern int g_eig_mode;
+
 int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream);
+int eig_tri_batched(std::vector<EigProblem>& probs, cudaStream_t stream);
 
 }  // namespace ht

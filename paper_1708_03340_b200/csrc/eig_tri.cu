@@ -1,0 +1,442 @@
+// Batched symmetric eigensolver, fast path: one CTA per K x K matrix (K <= 112),
+// everything in shared memory.
+//
+//   1. Householder tridiagonalisation A = Q T Q^T (lower, dsytd2 order): per column
+//      one reflector, the symmetric mat-vec p = tau A22 v by 4 threads per row, and
+//      the rank-2 update A22 -= v w^T + w v^T.  Reflectors stay in the lower triangle.
+//   2. All K eigenvalues of T by multisection bisection: 4 threads per eigenvalue
+//      evaluate Sturm counts at 4 points per round (sign changes of the scaled
+//      leading-minor recurrence p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2}).
+//   3. select_rank (arith.py:69-88) on the device, then eigenvectors of T for the
+//      kept ranks only, by twisted factorisation (stationary + progressive LDL^T,
+//      twist at min |gamma_k|), four O(K) passes held in the output row itself;
+//      close pairs (gap < 1e-5 ||T||) are re-orthogonalised (MGS) in T-space.
+//   4. Back-transformation by the reflectors, 4 threads per eigenvector.
+//
+// Nodes the fast path cannot serve to the reference's accuracy are flagged for the
+// Jacobi kernel (eig.cu), which runs next and only on flagged nodes: graded spectra
+// (min |lambda| < 1e-6 max |lambda|: the small hierarchical singular values need
+// relative accuracy) and near-degenerate kept eigenvalues (gap < 1e-12 ||T||).
+#include <cmath>
+
+#include "eig.cuh"
+#include "prof.cuh"
+
+namespace ht {
+namespace {
+
+constexpr int TT = 512;
+constexpr int MAXD = 48;
+constexpr int kGroup = 4;  // threads per eigenvalue / eigenvector / mat-vec row
+constexpr double kGradedTol = 1e-6;
+constexpr double kDegenTol = 1e-12;
+constexpr double kClusterTol = 1e-5;
+
+struct TriBatch {
+  int count;
+  int begin[MAXD + 1];
+  EigProblem d[MAXD];
+};
+
+__device__ __forceinline__ double quad_sum(double v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  return v;
+}
+
+// number of eigenvalues of T (d, e2 = e^2) strictly below x
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int K, double x, double pivmin) {
+  double pm2 = 1.0;        // p_{k-2}
+  double pm1 = d[0] - x;   // p_{k-1}
+  if (fabs(pm1) < pivmin) pm1 = -pivmin;
+  int c = pm1 < 0.0;
+  for (int k = 1; k < K; ++k) {
+    double p = fma(d[k] - x, pm1, -e2[k - 1] * pm2);
+    if (fabs(p) < pivmin * fabs(pm1)) p = -pivmin * pm1;  // q_k = p_k / p_{k-1} -> -pivmin
+    c += (p < 0.0) != (pm1 < 0.0);
+    pm2 = pm1;
+    pm1 = p;
+    const double a = fabs(p);
+    if (a > 0x1p+500 || a < 0x1p-500) {  // exact power-of-two rescale
+      const int ex = ilogb(a);
+      pm1 = scalbn(pm1, -ex);
+      pm2 = scalbn(pm2, -ex);
+    }
+  }
+  return c;
+}
+
+__global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ TriBatch b) {
+  extern __shared__ double sm[];
+  int di = 0;
+  while (di + 1 < b.count && (int)blockIdx.x >= b.begin[di + 1]) ++di;
+  const EigProblem& e = b.d[di];
+  const int nd = blockIdx.x - b.begin[di];
+  const int K = e.K;
+  const int ap = K | 1;            // odd pitch
+  const int zp = (K + 1) | 1;
+  double* A = sm;                  // K x ap
+  double* Z = A + K * ap;          // r x zp: eigenvectors of T, one row per kept eigenpair
+  double* dd = Z + K * zp;         // [K] diagonal of T
+  double* ee = dd + K;             // [K] off-diagonal
+  double* e2 = ee + K;             // [K] squares
+  double* tau = e2 + K;            // [K]
+  double* vb = tau + K;            // [K] current reflector
+  double* pb = vb + K;             // [K] p / w
+  double* lam = pb + K;            // [K] ascending eigenvalues
+  __shared__ double red[TT / 32][2];
+  __shared__ double sh[4];
+  __shared__ int flags[2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // ---- load, symmetry check (kernels.py:46-50), symmetrise -------------------
+  const double* S = e.S + nd * e.s_node;
+  double asym = 0.0, amax = 0.0;
+  for (int x = tid; x < K * K; x += TT) {
+    const int i = x / K, j = x - i * K;
+    const double a = S[x], at = S[j * K + i];
+    asym = fmax(asym, fabs(a - at));
+    amax = fmax(amax, fabs(a));
+    A[i * ap + j] = 0.5 * (a + at);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    asym = fmax(asym, __shfl_xor_sync(0xffffffffu, asym, o));
+    amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+  }
+  if (lane == 0) { red[warp][0] = asym; red[warp][1] = amax; }
+  __syncthreads();
+  if (tid == 0) {
+    double s0 = 0.0, s1 = 0.0;
+    for (int w = 0; w < TT / 32; ++w) { s0 = fmax(s0, red[w][0]); s1 = fmax(s1, red[w][1]); }
+    if (e.status && s0 > 1e-12 * fmax(1.0, s1)) atomicOr(e.status, kEigStatusNotSymmetric);
+    flags[0] = 0;
+  }
+
+  // ---- 1. tridiagonalisation --------------------------------------------------
+  for (int j = 0; j + 2 < K; ++j) {
+    const int m = K - j - 1;       // reflector length (rows j+1 .. K-1)
+    if (warp == 0) {
+      double ss = 0.0;
+      for (int k = 1 + lane; k < m; k += 32) {
+        const double x = A[(j + 1 + k) * ap + j];
+        ss = fma(x, x, ss);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+      const double alpha = A[(j + 1) * ap + j];
+      double t = 0.0, beta = alpha, scale = 0.0;
+      if (ss > 0.0) {
+        beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+        t = (beta - alpha) / beta;
+        scale = 1.0 / (alpha - beta);
+      }
+      for (int k = lane; k < m; k += 32) {
+        const double v = k == 0 ? 1.0 : A[(j + 1 + k) * ap + j] * scale;
+        vb[k] = v;
+        if (k > 0) A[(j + 1 + k) * ap + j] = v;  // reflector tail kept in the lower triangle
+      }
+      if (lane == 0) {
+        dd[j] = A[j * ap + j];
+        ee[j] = beta;
+        tau[j] = t;
+      }
+    }
+    __syncthreads();
+    const double tj = tau[j];
+    if (tj != 0.0) {
+      // p = tau * A22 v, 4 threads per row
+      {
+        const int i = tid / kGroup, part = tid % kGroup;
+        double acc = 0.0;
+        if (i < m) {
+          const double* row = A + (j + 1 + i) * ap + (j + 1);
+          for (int k = part; k < m; k += kGroup) acc = fma(row[k], vb[k], acc);
+        }
+        acc = quad_sum(acc);
+        if (i < m && part == 0) pb[i] = tj * acc;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double s = 0.0;
+        for (int k = lane; k < m; k += 32) s = fma(pb[k], vb[k], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double c = -0.5 * tj * s;
+        __syncwarp();
+        for (int k = lane; k < m; k += 32) pb[k] = fma(c, vb[k], pb[k]);  // w = p - tau/2 (p.v) v
+      }
+      __syncthreads();
+      for (int x = tid; x < m * m; x += TT) {
+        const int r = x / m, c = x - r * m;
+        double* a = A + (j + 1 + r) * ap + (j + 1 + c);
+        *a -= fma(vb[r], pb[c], pb[r] * vb[c]);
+      }
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    if (K >= 2) {
+      dd[K - 2] = A[(K - 2) * ap + K - 2];
+      ee[K - 2] = A[(K - 1) * ap + K - 2];
+    }
+    dd[K - 1] = A[(K - 1) * ap + K - 1];
+    ee[K - 1] = 0.0;
+  }
+  __syncthreads();
+  for (int k = tid; k < K; k += TT) e2[k] = ee[k] * ee[k];
+  // Gershgorin bounds, pivmin
+  if (warp == 0) {
+    double gl = INFINITY, gu = -INFINITY, em = 0.0;
+    for (int k = lane; k < K; k += 32) {
+      const double r = (k > 0 ? fabs(ee[k - 1]) : 0.0) + (k + 1 < K ? fabs(ee[k]) : 0.0);
+      gl = fmin(gl, dd[k] - r);
+      gu = fmax(gu, dd[k] + r);
+      if (k + 1 < K) em = fmax(em, ee[k] * ee[k]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      gl = fmin(gl, __shfl_xor_sync(0xffffffffu, gl, o));
+      gu = fmax(gu, __shfl_xor_sync(0xffffffffu, gu, o));
+      em = fmax(em, __shfl_xor_sync(0xffffffffu, em, o));
+    }
+    if (lane == 0) {
+      const double tn = fmax(fabs(gl), fabs(gu));
+      const double pad = 2.0 * 2.220446049250313e-16 * tn * K + 1e-300;
+      sh[0] = gl - pad;
+      sh[1] = gu + pad;
+      sh[2] = 2.2250738585072014e-308 * fmax(1.0, em);
+      sh[3] = tn;
+    }
+  }
+  __syncthreads();
+
+  // ---- 2. eigenvalues: multisection bisection, 4 threads per eigenvalue ---------
+  {
+    const int i = tid / kGroup, part = tid % kGroup;
+    const double pivmin = sh[2];
+    const double atol = 4.0 * 2.220446049250313e-16 * sh[3] + pivmin;  // absolute accuracy of the reduction
+    double lo = sh[0], hi = sh[1];
+    const bool act = i < K;
+    for (int it = 0; it < 64; ++it) {
+      const double w = hi - lo;
+      const bool done = !(w > 2.220446049250313e-16 * 2.0 * fmax(fabs(lo), fabs(hi)) + atol);
+      if (__all_sync(0xffffffffu, done || !act)) break;
+      const double x = lo + w * (double)(part + 1) / (double)(kGroup + 1);
+      const int c = act ? sturm_count(dd, e2, K, x, pivmin) : 0;
+      // smallest point with count > i becomes hi; the point before it lo
+      const unsigned base = (unsigned)(lane & ~(kGroup - 1));
+      double nlo = lo, nhi = hi;
+      bool found = false;
+#pragma unroll
+      for (int g = 0; g < kGroup; ++g) {
+        const int cg = __shfl_sync(0xffffffffu, c, base + g);
+        const double xg = __shfl_sync(0xffffffffu, x, base + g);
+        if (!found) {
+          if (cg > i) {
+            nhi = xg;
+            found = true;
+          } else {
+            nlo = xg;
+          }
+        }
+      }
+      if (!done) {
+        lo = nlo;
+        hi = nhi;
+      }
+    }
+    if (act && part == 0) lam[i] = 0.5 * (lo + hi);
+  }
+  __syncthreads();
+
+  // ---- outputs: eigenvalues (descending, clamped), rank, fallback decision ------
+  double* lamo = e.lam + nd * e.l_node;
+  for (int k = tid; k < K; k += TT) lamo[k] = fmax(lam[K - 1 - k], 0.0);
+  __shared__ int rsel;
+  if (tid == 0) {
+    int r = K;
+    if (e.eps > 0.0) {
+      const double budget = e.eps * e.eps / e.n_nonroot;
+      double tail = 0.0;
+      for (int k = K - 1; k >= 0; --k) {  // descending index k <-> ascending K-1-k
+        tail += fmax(lam[K - 1 - k], 0.0);
+        if (tail <= budget) r = k;
+        else break;
+      }
+    }
+    if (e.cap > 0) r = min(r, e.cap);
+    r = max(1, min(r, K));
+    if (e.rank) e.rank[nd] = r;
+    rsel = r;
+    const double tn = fmax(fabs(lam[0]), fabs(lam[K - 1]));
+    int fb = 0;
+    for (int k = 0; k < K; ++k)
+      if (fabs(lam[k]) < kGradedTol * tn) fb = 1;  // graded: relative accuracy needed
+    // kept eigenpairs (ascending K-r .. K-1) and the boundary pair must be separated
+    for (int k = max(0, K - r - 1); k + 1 < K; ++k)
+      if (lam[k + 1] - lam[k] < kDegenTol * tn) fb = 1;
+    if (!(tn > 0.0) || !isfinite(tn)) fb = 1;  // zero / non-finite matrix: Jacobi
+    flags[1] = fb;
+    if (e.fallback) e.fallback[nd] = fb;
+  }
+  __syncthreads();
+  if (flags[1]) return;  // the Jacobi kernel takes this node
+  const int r = rsel;
+
+  // ---- 3. eigenvectors of T (twisted factorisation), one thread per vector ----------
+  for (int v = tid; v < r; v += TT) {
+    const double sig = lam[K - 1 - v];  // descending order: vector v <-> eigenvalue K-1-v
+    double* z = Z + v * zp;
+    const double pivmin = sh[2];
+    if (K == 1) {
+      z[0] = 1.0;
+      continue;
+    }
+    // pass 1: stationary D+_k into z[k]
+    double dp = dd[0] - sig;
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    z[0] = dp;
+    for (int k = 0; k + 1 < K; ++k) {
+      dp = (dd[k + 1] - sig) - e2[k] / dp;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      z[k + 1] = dp;
+    }
+    // pass 2: progressive D-_k, U_k into z[k+1], gamma_k = D+_k + D-_k - (d_k - sig)
+    double dm = dd[K - 1] - sig;
+    if (fabs(dm) < pivmin) dm = -pivmin;
+    int twist = K - 1;
+    double gmin = fabs(z[K - 1]);  // gamma_{K-1} = D+_{K-1}
+    for (int k = K - 2; k >= 0; --k) {
+      const double u = ee[k] / dm;          // U_k
+      const double dmk = (dd[k] - sig) - ee[k] * u;
+      const double g = z[k] + dmk - (dd[k] - sig);
+      z[k + 1] = u;
+      dm = fabs(dmk) < pivmin ? -pivmin : dmk;
+      if (fabs(g) < gmin) {
+        gmin = fabs(g);
+        twist = k;
+      }
+    }
+    // pass 3: L_k = e_k / D+_k for k < twist into z[k]
+    dp = dd[0] - sig;
+    if (fabs(dp) < pivmin) dp = -pivmin;
+    for (int k = 0; k < twist; ++k) {
+      z[k] = ee[k] / dp;
+      dp = (dd[k + 1] - sig) - e2[k] / dp;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+    }
+    // pass 4/5: z_twist = 1, z_k = -L_k z_{k+1} (k < twist), z_{k+1} = -U_k z_k (k >= twist)
+    z[twist] = 1.0;
+    double nrm = 1.0;
+    for (int k = twist - 1; k >= 0; --k) {
+      z[k] = -z[k] * z[k + 1];
+      nrm = fma(z[k], z[k], nrm);
+    }
+    for (int k = twist; k + 1 < K; ++k) {
+      z[k + 1] = -z[k + 1] * z[k];
+      nrm = fma(z[k + 1], z[k + 1], nrm);
+    }
+    const double inv = 1.0 / sqrt(nrm);
+    for (int k = 0; k < K; ++k) z[k] *= inv;
+  }
+  __syncthreads();
+  // re-orthogonalise close kept pairs (MGS within runs of gap < kClusterTol ||T||), warp 0
+  if (warp == 0) {
+    const double tn = sh[3];
+    int v0 = 0;
+    while (v0 < r) {
+      int v1 = v0 + 1;
+      while (v1 < r && lam[K - 1 - (v1 - 1)] - lam[K - 1 - v1] < kClusterTol * tn) ++v1;
+      for (int a = v0 + 1; a < v1; ++a) {
+        double* za = Z + a * zp;
+        for (int bq = v0; bq < a; ++bq) {
+          const double* zb = Z + bq * zp;
+          double s = 0.0;
+          for (int k = lane; k < K; k += 32) s = fma(za[k], zb[k], s);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          for (int k = lane; k < K; k += 32) za[k] = fma(-s, zb[k], za[k]);
+          __syncwarp();
+        }
+        double s = 0.0;
+        for (int k = lane; k < K; k += 32) s = fma(za[k], za[k], s);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const double inv = 1.0 / sqrt(s);
+        for (int k = lane; k < K; k += 32) za[k] *= inv;
+        __syncwarp();
+      }
+      v0 = v1;
+    }
+  }
+  __syncthreads();
+
+  // ---- 4. back-transformation y = H_0 ... H_{K-3} z, 4 threads per vector --------------
+  {
+    const int v = tid / kGroup, part = tid % kGroup;
+    const bool act = v < r;
+    double* z = Z + (act ? v : 0) * zp;
+    for (int j = K - 3; j >= 0; --j) {
+      const double tj = tau[j];
+      if (tj == 0.0) continue;
+      const int m = K - j - 1;
+      // v_j: 1 at row j+1, A[(j+1+k)*ap + j] below
+      double s = 0.0;
+      if (act)
+        for (int k = part; k < m; k += kGroup) s = fma(k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k], s);
+      s = quad_sum(s) * tj;  // all lanes shuffle
+      if (act)
+        for (int k = part; k < m; k += kGroup) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k]);
+    }
+  }
+  __syncthreads();
+  double* Vo = e.V + nd * e.v_node;
+  for (int x = tid; x < K * r; x += TT) {
+    const int row = x / r, c = x - row * r;
+    Vo[(long long)row * K + c] = Z[c * zp + row];
+  }
+}
+
+size_t tri_smem(int K) {
+  const int ap = K | 1, zp = (K + 1) | 1;
+  return sizeof(double) * ((size_t)K * ap + (size_t)K * zp + 7 * (size_t)K) + 64;
+}
+
+bool g_tri_attr = false;
+
+}  // namespace
+
+int eig_tri_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
+  if (!g_tri_attr) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(tri_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)tri_smem(kEigMaxK)));
+    g_tri_attr = true;
+  }
+  size_t i = 0;
+  while (i < probs.size()) {
+    TriBatch b;
+    b.count = 0;
+    int blocks = 0;
+    size_t smem = 0;
+    while (i < probs.size() && b.count < MAXD) {
+      const EigProblem& p = probs[i++];
+      if (p.nodes == 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += p.nodes;
+      smem = std::max(smem, tri_smem(p.K));
+      b.d[b.count++] = p;
+    }
+    if (b.count == 0) continue;
+    b.begin[b.count] = blocks;
+    double flops = 0;
+    for (int q = 0; q < b.count; ++q) flops += 9.0 * b.d[q].nodes * (double)b.d[q].K * b.d[q].K * b.d[q].K;
+    ProfToken tok = prof_begin(stream);
+    tri_eig_kernel<<<blocks, TT, smem, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "tridiag_eig", stream, flops, 0.0);
+  }
+  return kOk;
+}
+
+}  // namespace ht

@@ -16,15 +16,17 @@ SIGMA_RTOL = 1e-10
 ERR_TOL = 1e-10
 
 
-@pytest.fixture(scope="module", params=["auto", "householder"])
+@pytest.fixture(scope="module", params=[("auto", "auto"), ("householder", "jacobi")], ids=["fast", "fallback"])
 def htb(cuda_ok, request):
-    """Every parity test runs under both QR policies: Cholesky-QR2 with the
-    validated Householder fallback (default) and Householder only."""
+    """Every parity test runs under both kernel policies: the fast paths (Cholesky-QR2,
+    tridiagonal eigensolver; default) and their fallbacks (Householder QR, Jacobi)."""
     import paper_1708_03340_b200 as m
 
-    m.set_qr_mode(request.param)
+    m.set_qr_mode(request.param[0])
+    m.set_eig_mode(request.param[1])
     yield m
     m.set_qr_mode("auto")
+    m.set_eig_mode("auto")
 
 
 def _sig_host(sig):
