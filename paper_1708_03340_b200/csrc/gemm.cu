@@ -102,7 +102,7 @@ __device__ __forceinline__ const double* b_src(const GemmDesc& g, const double* 
 }
 
 template <int WM, int WN, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(THREADS, 1) gemm_kernel(const __grid_constant__ GemmBatch batch) {
+__global__ void __launch_bounds__(THREADS, (WM * WN == 13 ? 2 : 1)) gemm_kernel(const __grid_constant__ GemmBatch batch) {
   constexpr int BM = 8 * WM * WARPS_M, BN = 8 * WN * WARPS_N;
   constexpr int PA = pitch16(BM), PB = pitch16(BN);
   extern __shared__ __align__(16) double smem[];
@@ -382,20 +382,29 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
 }
 
 // ---- tile configurations ----
-enum Cfg { kC64, kCN104, kCM104, kCN56, kCM56, kNumCfg };
+int g_half_tiles = 1;
+enum Cfg { kC64, kCN104, kCM104, kCN56, kCM56, kCN104h, kCM104h, kNumCfg };
 
 struct CfgInfo {
   int bm, bn;
 };
-constexpr CfgInfo kCfg[kNumCfg] = {{64, 64}, {128, 104}, {104, 128}, {128, 56}, {56, 128}};
+// *h: half-height tiles with 8 warps x (8 x 104) fragments, <= 128 registers, two CTAs
+// per SM (one CTA's pipeline fill / epilogue overlaps the other's DMMA main loop)
+constexpr CfgInfo kCfg[kNumCfg] = {{64, 64}, {128, 104}, {104, 128}, {128, 56}, {56, 128}, {64, 104}, {104, 64}};
 
 Cfg pick_cfg(const GemmDesc& d) {
+  // half-height tiles only pay off for short reductions (the rank-sized K of the mode
+  // products and Q = A R^-1); long (split-K) reductions keep the full tiles
+  const bool half = g_half_tiles && (long long)d.K * std::max(d.KO, 1) <= 512;
   if (d.N <= 56 && d.M > 56) return kCN56;
   if (d.M <= 56 && d.N > 56) return kCM56;
-  if (d.N <= 104 && d.M > 104) return kCN104;
-  if (d.M <= 104 && d.N > 104) return kCM104;
+  if (d.N <= 104 && d.M > 104) return half ? kCN104h : kCN104;
+  if (d.M <= 104 && d.N > 104) return half ? kCM104h : kCM104;
   if (d.M <= 64 && d.N <= 64) return kC64;
-  if (d.N <= 104 && d.M <= 104) return d.N >= d.M ? kCM104 : kCN104;
+  if (d.N <= 104 && d.M <= 104) {
+    if (half) return d.N >= d.M ? kCM104h : kCN104h;
+    return d.N >= d.M ? kCM104 : kCN104;
+  }
   return kCN104;
 }
 
@@ -422,6 +431,8 @@ int launch_batch(Cfg c, GemmBatch& batch, int blocks, cudaStream_t stream) {
     case kCM104: return launch_cfg<13, 2, 1, 8>(batch, blocks, smem, stream);  // 104 x 128
     case kCN56: return launch_cfg<2, 7, 8, 1>(batch, blocks, smem, stream);    // 128 x 56
     case kCM56: return launch_cfg<7, 2, 1, 8>(batch, blocks, smem, stream);    // 56 x 128
+    case kCN104h: return launch_cfg<1, 13, 8, 1>(batch, blocks, smem, stream); // 64 x 104
+    case kCM104h: return launch_cfg<13, 1, 1, 8>(batch, blocks, smem, stream); // 104 x 64
     default: break;
   }
   set_error("gemm: bad tile config");
@@ -430,10 +441,12 @@ int launch_batch(Cfg c, GemmBatch& batch, int blocks, cudaStream_t stream) {
 
 }  // namespace
 
-int gemm_tiles(int M, int N) {
+int gemm_tiles(int M, int N) {  // tiles of a long-reduction (split-K planned) GEMM
   GemmDesc d{};
   d.M = M;
   d.N = N;
+  d.K = 1 << 20;
+  d.KO = 1;
   const Cfg c = pick_cfg(d);
   return ceil_div(M, kCfg[c].bm) * ceil_div(N, kCfg[c].bn);
 }
