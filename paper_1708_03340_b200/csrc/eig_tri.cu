@@ -57,10 +57,12 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     pm2 = pm1;
     pm1 = p;
     const double a = fabs(p);
-    if (a > 0x1p+500 || a < 0x1p-500) {  // exact power-of-two rescale
-      const int ex = ilogb(a);
-      pm1 = scalbn(pm1, -ex);
-      pm2 = scalbn(pm2, -ex);
+    if (a > 0x1p+400) {  // exact power-of-two rescales keep the minors in range
+      pm1 *= 0x1p-400;
+      pm2 *= 0x1p-400;
+    } else if (a < 0x1p-400) {
+      pm1 *= 0x1p+400;
+      pm2 *= 0x1p+400;
     }
   }
   return c;
@@ -81,8 +83,8 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   double* ee = dd + K;             // [K] off-diagonal
   double* e2 = ee + K;             // [K] squares
   double* tau = e2 + K;            // [K]
-  double* vb = tau + K;            // [K] current reflector
-  double* pb = vb + K;             // [K] p / w
+  double* vb = tau + K;            // [2][kEigMaxK] reflectors (double-buffered)
+  double* pb = vb + 2 * kEigMaxK;  // [K] p
   double* lam = pb + K;            // [K] ascending eigenvalues
   __shared__ double red[TT / 32][2];
   __shared__ double sh[4];
@@ -114,64 +116,81 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
 
   // ---- 1. tridiagonalisation --------------------------------------------------
+  // Reflector j from column j (rows j+1..K-1), computed by warp 0 into vbuf[j & 1]
+  // while the other warps finish the previous rank-2 update: two barriers per column.
+  double* vbuf = vb;
+  auto reflector = [&](int j, double* v) {
+    const int m = K - j - 1;
+    double ss = 0.0;
+    for (int k = 1 + lane; k < m; k += 32) {
+      const double x = A[(j + 1 + k) * ap + j];
+      ss = fma(x, x, ss);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    const double alpha = A[(j + 1) * ap + j];
+    double t = 0.0, beta = alpha, scale = 0.0;
+    if (ss > 0.0) {
+      beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
+      t = (beta - alpha) / beta;
+      scale = 1.0 / (alpha - beta);
+    }
+    for (int k = lane; k < m; k += 32) {
+      const double x = k == 0 ? 1.0 : A[(j + 1 + k) * ap + j] * scale;
+      v[k] = x;
+      if (k > 0) A[(j + 1 + k) * ap + j] = x;  // reflector tail kept in the lower triangle
+    }
+    if (lane == 0) {
+      dd[j] = A[j * ap + j];
+      ee[j] = beta;
+      tau[j] = t;
+    }
+  };
+  if (K > 2 && warp == 0) reflector(0, vbuf);
+  __syncthreads();
   for (int j = 0; j + 2 < K; ++j) {
     const int m = K - j - 1;       // reflector length (rows j+1 .. K-1)
-    if (warp == 0) {
-      double ss = 0.0;
-      for (int k = 1 + lane; k < m; k += 32) {
-        const double x = A[(j + 1 + k) * ap + j];
-        ss = fma(x, x, ss);
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-      const double alpha = A[(j + 1) * ap + j];
-      double t = 0.0, beta = alpha, scale = 0.0;
-      if (ss > 0.0) {
-        beta = -copysign(sqrt(fma(alpha, alpha, ss)), alpha);
-        t = (beta - alpha) / beta;
-        scale = 1.0 / (alpha - beta);
-      }
-      for (int k = lane; k < m; k += 32) {
-        const double v = k == 0 ? 1.0 : A[(j + 1 + k) * ap + j] * scale;
-        vb[k] = v;
-        if (k > 0) A[(j + 1 + k) * ap + j] = v;  // reflector tail kept in the lower triangle
-      }
-      if (lane == 0) {
-        dd[j] = A[j * ap + j];
-        ee[j] = beta;
-        tau[j] = t;
-      }
-    }
-    __syncthreads();
+    const double* v = vbuf + (j & 1) * kEigMaxK;
+    double* vn = vbuf + ((j + 1) & 1) * kEigMaxK;
     const double tj = tau[j];
     if (tj != 0.0) {
-      // p = tau * A22 v, 4 threads per row
+      // p = tau * A22 v (4 threads per row) and the per-warp partial of p.v
       {
         const int i = tid / kGroup, part = tid % kGroup;
         double acc = 0.0;
         if (i < m) {
           const double* row = A + (j + 1 + i) * ap + (j + 1);
-          for (int k = part; k < m; k += kGroup) acc = fma(row[k], vb[k], acc);
+          for (int k = part; k < m; k += kGroup) acc = fma(row[k], v[k], acc);
         }
-        acc = quad_sum(acc);
-        if (i < m && part == 0) pb[i] = tj * acc;
-      }
-      __syncthreads();
-      if (warp == 0) {
-        double s = 0.0;
-        for (int k = lane; k < m; k += 32) s = fma(pb[k], vb[k], s);
+        acc = quad_sum(acc) * tj;
+        double pv = (i < m && part == 0) ? acc * v[i] : 0.0;
+        if (i < m && part == 0) pb[i] = acc;
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const double c = -0.5 * tj * s;
-        __syncwarp();
-        for (int k = lane; k < m; k += 32) pb[k] = fma(c, vb[k], pb[k]);  // w = p - tau/2 (p.v) v
+        for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
+        if (lane == 0) red[warp][0] = pv;
       }
       __syncthreads();
-      for (int x = tid; x < m * m; x += TT) {
-        const int r = x / m, c = x - r * m;
-        double* a = A + (j + 1 + r) * ap + (j + 1 + c);
-        *a -= fma(vb[r], pb[c], pb[r] * vb[c]);
+      double sv = 0.0;
+#pragma unroll
+      for (int w = 0; w < TT / 32; ++w) sv += red[w][0];  // fixed order: deterministic
+      const double c = -0.5 * tj * sv;                     // w = p + c v
+      if (warp == 0) {
+        // column j+1 (A22 column 0), then the next reflector from it
+        for (int r = lane; r < m; r += 32) {
+          const double wr = fma(c, v[r], pb[r]), w0 = fma(c, v[0], pb[0]);
+          A[(j + 1 + r) * ap + (j + 1)] -= fma(v[r], w0, wr * v[0]);
+        }
+        __syncwarp();
+        if (j + 3 < K) reflector(j + 1, vn);
+      } else {
+        for (int r = warp - 1; r < m; r += TT / 32 - 1) {
+          const double vr = v[r], wr = fma(c, vr, pb[r]);
+          double* ar = A + (j + 1 + r) * ap + (j + 1);
+          for (int cc = 1 + lane; cc < m; cc += 32) ar[cc] -= fma(vr, fma(c, v[cc], pb[cc]), wr * v[cc]);
+        }
       }
+    } else if (warp == 0 && j + 3 < K) {
+      reflector(j + 1, vn);
     }
     __syncthreads();
   }
@@ -184,7 +203,23 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     ee[K - 1] = 0.0;
   }
   __syncthreads();
-  for (int k = tid; k < K; k += TT) e2[k] = ee[k] * ee[k];
+  // exact power-of-two normalisation of T (eigenvalues O(1): the Sturm recurrence
+  // stays in range); lam is scaled back on output
+  if (warp == 0) {
+    double mx = 0.0;
+    for (int k = lane; k < K; k += 32) mx = fmax(mx, fmax(fabs(dd[k]), fabs(ee[k])));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if (lane == 0) sh[3] = (mx > 0.0 && isfinite(mx)) ? exp2(-(double)ilogb(mx)) : 1.0;
+  }
+  __syncthreads();
+  const double tscale = sh[3];
+  for (int k = tid; k < K; k += TT) {
+    dd[k] *= tscale;
+    ee[k] *= tscale;
+    e2[k] = ee[k] * ee[k];
+  }
+  __syncthreads();
   // Gershgorin bounds, pivmin
   if (warp == 0) {
     double gl = INFINITY, gu = -INFINITY, em = 0.0;
@@ -249,10 +284,11 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     if (act && part == 0) lam[i] = 0.5 * (lo + hi);
   }
   __syncthreads();
+  const double unscale = 1.0 / tscale;  // exact (power of two)
 
   // ---- outputs: eigenvalues (descending, clamped), rank, fallback decision ------
   double* lamo = e.lam + nd * e.l_node;
-  for (int k = tid; k < K; k += TT) lamo[k] = fmax(lam[K - 1 - k], 0.0);
+  for (int k = tid; k < K; k += TT) lamo[k] = fmax(lam[K - 1 - k] * unscale, 0.0);
   __shared__ int rsel;
   if (tid == 0) {
     int r = K;
@@ -260,7 +296,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       const double budget = e.eps * e.eps / e.n_nonroot;
       double tail = 0.0;
       for (int k = K - 1; k >= 0; --k) {  // descending index k <-> ascending K-1-k
-        tail += fmax(lam[K - 1 - k], 0.0);
+        tail += fmax(lam[K - 1 - k] * unscale, 0.0);
         if (tail <= budget) r = k;
         else break;
       }
@@ -400,7 +436,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
 
 size_t tri_smem(int K) {
   const int ap = K | 1, zp = (K + 1) | 1;
-  return sizeof(double) * ((size_t)K * ap + (size_t)K * zp + 7 * (size_t)K) + 64;
+  return sizeof(double) * ((size_t)K * ap + (size_t)K * zp + 6 * (size_t)K + 2 * (size_t)kEigMaxK) + 64;
 }
 
 bool g_tri_attr = false;
