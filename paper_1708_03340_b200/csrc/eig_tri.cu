@@ -44,25 +44,30 @@ __device__ __forceinline__ double quad_sum(double v) {
   return v;
 }
 
-// number of eigenvalues of T (d, e2 = e^2) strictly below x
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int K, double x, double pivmin) {
-  double pm2 = 1.0;        // p_{k-2}
-  double pm1 = d[0] - x;   // p_{k-1}
-  if (fabs(pm1) < pivmin) pm1 = -pivmin;
-  int c = pm1 < 0.0;
-  for (int k = 1; k < K; ++k) {
-    double p = fma(d[k] - x, pm1, -e2[k - 1] * pm2);
-    if (fabs(p) < pivmin * fabs(pm1)) p = -pivmin * pm1;  // q_k = p_k / p_{k-1} -> -pivmin
-    c += (p < 0.0) != (pm1 < 0.0);
-    pm2 = pm1;
-    pm1 = p;
-    const double a = fabs(p);
-    if (a > 0x1p+400) {  // exact power-of-two rescales keep the minors in range
-      pm1 *= 0x1p-400;
-      pm2 *= 0x1p-400;
-    } else if (a < 0x1p-400) {
-      pm1 *= 0x1p+400;
-      pm2 *= 0x1p+400;
+// Number of eigenvalues of T (d, e2 = e^2) strictly below x: sign changes of the
+// leading minors p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2} (T normalised to
+// ||T|| ~ 1).  Three FP64 ops per step; the sign test runs on the integer pipe and
+// the exact power-of-two rescale is checked every 8 steps (|p| changes by at most
+// 2^16 up / 2^-424 down in 8 steps).  A zero minor counts as positive.
+__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int K, double x) {
+  double pm2 = 1.0, pm1 = d[0] - x;
+  int c = __double_as_longlong(pm1) < 0;
+  int k = 1;
+  while (k < K) {
+    const int kend = min(K, k + 8);
+    for (; k < kend; ++k) {
+      const double p = fma(d[k] - x, pm1, -e2[k - 1] * pm2);
+      c += (__double_as_longlong(p) ^ __double_as_longlong(pm1)) < 0;
+      pm2 = pm1;
+      pm1 = p;
+    }
+    const double a = fmax(fabs(pm1), fabs(pm2));
+    if (a > 0x1p+300) {
+      pm1 *= 0x1p-300;
+      pm2 *= 0x1p-300;
+    } else if (a < 0x1p-300) {
+      pm1 *= 0x1p+300;
+      pm2 *= 0x1p+300;
     }
   }
   return c;
@@ -170,9 +175,9 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
         if (lane == 0) red[warp][0] = pv;
       }
       __syncthreads();
-      double sv = 0.0;
+      double sv = red[lane & (TT / 32 - 1)][0];  // same shuffle tree in every warp: deterministic
 #pragma unroll
-      for (int w = 0; w < TT / 32; ++w) sv += red[w][0];  // fixed order: deterministic
+      for (int o = TT / 64; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
       const double c = -0.5 * tj * sv;                     // w = p + c v
       if (warp == 0) {
         // column j+1 (A22 column 0), then the next reflector from it
@@ -258,7 +263,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       const bool done = !(w > 2.220446049250313e-16 * 2.0 * fmax(fabs(lo), fabs(hi)) + atol);
       if (__all_sync(0xffffffffu, done || !act)) break;
       const double x = lo + w * (double)(part + 1) / (double)(kGroup + 1);
-      const int c = act ? sturm_count(dd, e2, K, x, pivmin) : 0;
+      const int c = act ? sturm_count(dd, e2, K, x) : 0;
       // smallest point with count > i becomes hi; the point before it lo
       const unsigned base = (unsigned)(lane & ~(kGroup - 1));
       double nlo = lo, nhi = hi;
@@ -408,9 +413,10 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
   __syncthreads();
 
-  // ---- 4. back-transformation y = H_0 ... H_{K-3} z, 4 threads per vector --------------
+  // ---- 4. back-transformation y = H_0 ... H_{K-3} z, G = 8 (r <= 64) or 4 threads per vector
   {
-    const int v = tid / kGroup, part = tid % kGroup;
+    const int G = r <= TT / 8 ? 8 : kGroup;
+    const int v = tid / G, part = tid % G;
     const bool act = v < r;
     double* z = Z + (act ? v : 0) * zp;
     for (int j = K - 3; j >= 0; --j) {
@@ -420,10 +426,13 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       // v_j: 1 at row j+1, A[(j+1+k)*ap + j] below
       double s = 0.0;
       if (act)
-        for (int k = part; k < m; k += kGroup) s = fma(k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k], s);
-      s = quad_sum(s) * tj;  // all lanes shuffle
+        for (int k = part; k < m; k += G) s = fma(k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k], s);
+      s += __shfl_xor_sync(0xffffffffu, s, 1);  // all lanes shuffle
+      s += __shfl_xor_sync(0xffffffffu, s, 2);
+      if (G == 8) s += __shfl_xor_sync(0xffffffffu, s, 4);
+      s *= tj;
       if (act)
-        for (int k = part; k < m; k += kGroup) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k]);
+        for (int k = part; k < m; k += G) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k]);
     }
   }
   __syncthreads();
