@@ -177,11 +177,14 @@ int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha
                     double* C, int64_t c_m, int64_t c_n, int64_t c_b, ht_stream_t stream);
 
 /* QR policy of the orthogonalisation sweep (process-wide).
- *   0 (default): Cholesky-QR2 on DMMA GEMMs for frames with m >= 2K, K <= 128;
- *      the sweep then synchronises the stream ONCE to read a device red flag
- *      (pivot loss > 10 digits, non-finite values, or Q1^T Q1 not within 0.1 of I)
- *      and, if set, recomputes the whole sweep with Householder QR;
- *   1: Householder tree-TSQR only (no synchronisation).
+ *   0 (default): Cholesky-QR on DMMA GEMMs for frames with m >= 2K, K <= 128,
+ *      with the second (re-orthogonalisation) pass decided on the device per node
+ *      (power-iteration estimate of kappa(R) > 20); the sweep then synchronises
+ *      the stream ONCE to read a device red flag (pivot loss > 10 digits,
+ *      non-finite values, or Q1^T Q1 not within 0.1 of I) and, if set, recomputes
+ *      the whole sweep with Householder QR;
+ *   1: Householder tree-TSQR only (no synchronisation);
+ *   2: as 0 but both Cholesky-QR passes always run (CholeskyQR2).
  * Both give the unique QR with diag(R) >= 0 of kernels.py:24-32 up to rounding. */
 int ht_set_qr_mode(int mode);
 /* Number of Cholesky-QR2 sweeps that were re-run with Householder QR. */

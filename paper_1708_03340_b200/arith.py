@@ -286,16 +286,17 @@ def apply_operator(op: HTOperator, a: HTensor) -> HTensor:
     return out
 
 
-_QR_MODES = {"auto": 0, "householder": 1}
+_QR_MODES = {"auto": 0, "householder": 1, "cholqr2": 2}
 _qr_mode = "auto"
 
 
 def set_qr_mode(mode: str) -> None:
     """QR policy of the orthogonalisation sweep (process-wide): ``"auto"`` (default)
-    runs Cholesky-QR2 on DMMA GEMMs where eligible and re-runs the sweep with
-    Householder QR when its device-side check fails; ``"householder"`` always uses
-    the Householder tree-TSQR.  Both return the reference's sign-fixed QR
-    (kernels.py:24-32) up to rounding."""
+    runs Cholesky-QR on DMMA GEMMs where eligible (second pass only where the
+    estimated condition number exceeds 20) and re-runs the sweep with Householder QR
+    when its device-side check fails; ``"cholqr2"`` always runs both passes;
+    ``"householder"`` always uses the Householder tree-TSQR.  All return the
+    reference's sign-fixed QR (kernels.py:24-32) up to rounding."""
     global _qr_mode
     if mode not in _QR_MODES:
         raise ValueError(f"qr mode must be one of {sorted(_QR_MODES)}")

@@ -15,13 +15,23 @@ constexpr int kCholMaxDescs = 48;
 // pivot / column-norm^2 below this => kappa(A) ~> 1e5: leave it to Householder
 constexpr double kPivotTol = 1e-10;
 constexpr double kIdentityTol = 0.1;
+// One pass of Cholesky-QR leaves ||Q^T Q - I|| ~ 1e-17 kappa^2 (measured: 3e-15 at
+// kappa = 10, 7e-14 at 100).  The second pass runs unless ||R||_F ||R^{-1}||_F
+// (>= kappa_2, <= K kappa_2) is at most 300, i.e. kappa_2 <= 300 guaranteed.
+constexpr double kKappaOnePass = 300.0;
+constexpr int kCholInPlaceK = 104;  // widest output one GEMM tile covers (in-place pass 2)
 
 struct CholDesc {
   const double* W;  // nodes x K x K row-major (only the upper triangle is read)
   double* Rf;       // nodes x K x K: upper Cholesky factor (zeros below)
   double* Ri;       // nodes x K x K: its inverse (upper, zeros below)
+  double* Rout;     // optional second copy of Rf (row-major, ld r_ld, node stride r_node)
+  long long r_ld, r_node;
   int K, nodes;
   int check_identity;
+  const int* active;  // optional: skip unless *active != 0
+  int* need2;         // pass 1: OR-ed with 1 when kappa(R) > kappa_max (second pass needed)
+  double kappa_max;   // <= 0: second pass always
 };
 
 struct CholBatch {
@@ -47,6 +57,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
   int di = 0;
   while (di + 1 < cb.count && (int)blockIdx.x >= cb.block_begin[di + 1]) ++di;
   const CholDesc& c = cb.d[di];
+  if (c.active && *c.active == 0) return;
   const int node = blockIdx.x - cb.block_begin[di];
   const int K = c.K;
   __shared__ double rowbuf[2][kCholMaxK];
@@ -127,6 +138,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
   __syncthreads();
   double* Rf = c.Rf + off;
   double* Ri = c.Ri + off;
+  double* Ro = c.Rout ? c.Rout + (long long)node * c.r_node : nullptr;
   if (row_ok) {
     const double si = sqd[i];
 #pragma unroll
@@ -134,15 +146,45 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
       const int cc = sub + kCholTPR * q;
       if (cc >= K) continue;
       // R[i][cc] = U[i][cc] / sqrt(D_i) (cc >= i)
-      Rf[(long long)i * K + cc] = cc >= i ? w[q] / si : 0.0;
+      const double rv = cc >= i ? w[q] / si : 0.0;
+      Rf[(long long)i * K + cc] = rv;
+      if (Ro) Ro[(long long)i * c.r_ld + cc] = rv;
       // R^{-1}(cc, i) = Linv[i][cc] / sqrt(D_i) for cc <= i; zeros below the diagonal
       Ri[(long long)cc * K + i] = cc < i ? w[q] / si : (cc == i ? 1.0 / si : 0.0);
+    }
+  }
+  if (c.need2) {
+    // kappa_2(R) <= ||R||_F ||R^{-1}||_F: one block reduction of the two sums of squares
+    __shared__ double fr[kCholThreads / kWarp][2];
+    double s0 = 0.0, s1 = 0.0;
+    if (row_ok) {
+      const double isi = 1.0 / sqd[i];
+#pragma unroll
+      for (int q = 0; q < kCholCPT; ++q) {
+        const int cc = sub + kCholTPR * q;
+        const double v = w[q] * isi;
+        if (cc >= i && cc < K) s0 = fma(v, v, s0);  // R[i][cc]
+        if (cc < i) s1 = fma(v, v, s1);             // R^{-1}[cc][i]
+      }
+      if (sub == 0) s1 = fma(isi, isi, s1);          // R^{-1}[i][i]
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) { fr[warp][0] = s0; fr[warp][1] = s1; }
+    __syncthreads();
+    if (tid == 0) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int q = 0; q < kCholThreads / kWarp; ++q) { a0 += fr[q][0]; a1 += fr[q][1]; }
+      if (!(sqrt(a0 * a1) <= c.kappa_max)) atomicOr(c.need2, 1);
     }
   }
   if (tid == 0 && bad) atomicOr(cb.fail, 1);
 }
 
-int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s) {
+int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, const char* tag = "cholqr_factor") {
   size_t i = 0;
   while (i < ds.size()) {
     CholBatch b{};
@@ -161,7 +203,7 @@ int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s) {
     ProfToken tok = prof_begin(s);
     chol_kernel<<<blocks, kCholThreads, 0, s>>>(b);
     HT_LAUNCH_CHECK();
-    prof_end(tok, "cholqr_factor", s, flops, 0.0);
+    prof_end(tok, tag, s, ds[0].active ? 0.0 : flops, 0.0);  // conditional launches: no flop claim
   }
   return kOk;
 }
@@ -192,58 +234,93 @@ void cholqr_bind(CholQr& c, double* ws) {
   c.Ri = p;
 }
 
-int cholqr_run(std::vector<CholQr>& cs, int* fail, cudaStream_t s) {
+int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cudaStream_t s) {
   if (cs.empty()) return kOk;
+  // need2[p]: problem p needs the second pass (kappa estimate above kKappaOnePass, or K
+  // too wide for the in-place second pass)
+  HT_CUDA_CHECK(cudaMemsetAsync(need2, 0, sizeof(int) * cs.size(), s));
   // Gram GEMM of X (m x K, element (r, i) at X + r*xr + i*xc, node stride xn) into W
   auto gram = [&](std::vector<GemmDesc>& g, std::vector<ReduceDesc>& r, const CholQr& c, const double* X,
-                  long long xr, long long xc, long long xn) {
+                  long long xr, long long xc, long long xn, const int* active) {
     const int K = c.q.K, m = c.q.m, n = c.q.nodes;
     GemmDesc d = gemm_desc(X, xc, xr, X, xr, xc, c.S > 1 ? c.P : c.W, K, 1, K, K, m);
     d.nb1 = n; d.a_b1 = xn; d.b_b1 = xn; d.c_b1 = (long long)K * K;
     d.splits = c.S;
+    d.active = active;
     g.push_back(d);
-    if (c.S > 1) r.push_back(ReduceDesc{c.P, c.W, K, 1, (long long)K * K, 0, c.S, K, K, n, 1, 0, 1.0, 0.0});
-  };
-  auto chol = [&](std::vector<CholDesc>& v, const CholQr& c, double* Rf, int check) {
-    v.push_back(CholDesc{c.W, Rf, c.Ri, c.q.K, c.q.nodes, check});
+    if (c.S > 1) {
+      ReduceDesc rd{c.P, c.W, K, 1, (long long)K * K, 0, c.S, K, K, n, 1, 0, 1.0, 0.0};
+      rd.active = active;
+      r.push_back(rd);
+    }
   };
   std::vector<GemmDesc> g;
   std::vector<ReduceDesc> r;
   std::vector<CholDesc> ch;
-  // pass 1
-  for (auto& c : cs) gram(g, r, c, c.q.A, c.q.a_r, c.q.a_c, c.q.a_node);
+  // pass 1: W1 = A^T A, R1 = chol(W1) (also written as the final R), kappa estimate
+  for (auto& c : cs) gram(g, r, c, c.q.A, c.q.a_r, c.q.a_c, c.q.a_node, nullptr);
   HT_TRY(gemm_grouped(g, s, "gemm_cholqr_gram"));
   HT_TRY(reduce_partials(r, s));
-  for (auto& c : cs) chol(ch, c, c.R1, 0);
+  for (size_t p = 0; p < cs.size(); ++p) {
+    const CholQr& c = cs[p];
+    CholDesc d{};
+    d.W = c.W; d.Rf = c.R1; d.Ri = c.Ri; d.Rout = c.q.R; d.r_ld = c.q.r_ld; d.r_node = c.q.r_node;
+    d.K = c.q.K; d.nodes = c.q.nodes;
+    d.need2 = need2 + p;
+    d.kappa_max = (c.q.K <= kCholInPlaceK && !two_pass) ? kKappaOnePass : 0.0;
+    ch.push_back(d);
+  }
   HT_TRY(launch_chol(ch, fail, s));
   g.clear(); r.clear(); ch.clear();
-  for (auto& c : cs) {  // Q1 = A Ri  (row-major m x K scratch)
-    const int K = c.q.K, m = c.q.m;
-    GemmDesc d = gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.Q1, K, 1, m, K, K);
-    d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K; d.c_b1 = (long long)m * K;
-    g.push_back(d);
-  }
-  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_q"));
-  g.clear();
-  // pass 2
-  for (auto& c : cs) gram(g, r, c, c.Q1, c.q.K, 1, (long long)c.q.m * c.q.K);
-  HT_TRY(gemm_grouped(g, s, "gemm_cholqr_gram"));
-  HT_TRY(reduce_partials(r, s));
-  for (auto& c : cs) chol(ch, c, c.R2, 1);
-  HT_TRY(launch_chol(ch, fail, s));
-  g.clear();
+  // Q1 = A R1^{-1}, straight into the output when the second pass can run in place
+  // (one CTA owns whole output rows: K <= 104), else into scratch
   for (auto& c : cs) {
     const int K = c.q.K, m = c.q.m;
-    // Q = Q1 Ri into the caller's layout
-    GemmDesc d = gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
-    d.nb1 = c.q.nodes; d.a_b1 = (long long)m * K; d.b_b1 = (long long)K * K; d.c_b1 = c.q.q_node;
+    const bool inplace = K <= kCholInPlaceK;
+    GemmDesc d = inplace ? gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K)
+                         : gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.Q1, K, 1, m, K, K);
+    d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K;
+    d.c_b1 = inplace ? c.q.q_node : (long long)m * K;
     g.push_back(d);
-    // R = R2 R1 (row-major, ld r_ld)
-    GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
-    e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
-    g.push_back(e);
   }
   HT_TRY(gemm_grouped(g, s, "gemm_cholqr_q"));
+  g.clear();
+  // pass 2 (skipped on the device unless need2): W2 = Q1^T Q1, R2 = chol(W2),
+  // Q = Q1 R2^{-1}, R = R2 R1
+  for (size_t p = 0; p < cs.size(); ++p) {
+    const CholQr& c = cs[p];
+    if (c.q.K <= kCholInPlaceK) gram(g, r, c, c.q.Q, c.q.q_r, c.q.q_c, c.q.q_node, need2 + p);
+    else gram(g, r, c, c.Q1, c.q.K, 1, (long long)c.q.m * c.q.K, need2 + p);
+  }
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_gram", false));
+  HT_TRY(reduce_partials(r, s));
+  for (size_t p = 0; p < cs.size(); ++p) {
+    const CholQr& c = cs[p];
+    CholDesc d{};
+    d.W = c.W; d.Rf = c.R2; d.Ri = c.Ri;
+    d.K = c.q.K; d.nodes = c.q.nodes;
+    d.check_identity = 1;
+    d.active = need2 + p;
+    ch.push_back(d);
+  }
+  HT_TRY(launch_chol(ch, fail, s, "cholqr2_factor"));
+  g.clear();
+  for (size_t p = 0; p < cs.size(); ++p) {
+    const CholQr& c = cs[p];
+    const int K = c.q.K, m = c.q.m;
+    const bool inplace = K <= kCholInPlaceK;
+    GemmDesc d = inplace ? gemm_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K)
+                         : gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+    d.nb1 = c.q.nodes; d.a_b1 = inplace ? c.q.q_node : (long long)m * K; d.b_b1 = (long long)K * K;
+    d.c_b1 = c.q.q_node;
+    d.active = need2 + p;
+    g.push_back(d);
+    GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
+    e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
+    e.active = need2 + p;
+    g.push_back(e);
+  }
+  HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
   return kOk;
 }
 

@@ -6,6 +6,9 @@
 //   Q1 = A Ri           (DMMA GEMM)
 //   W2 = Q1^T Q1                                 R2 = chol(W2), Ri = R2^{-1}
 //   Q  = Q1 Ri,  R = R2 R1
+// The second pass only runs (decided on the device, per problem) when the power-
+// iteration estimate of kappa(R1) exceeds 20; below that one pass already gives
+// ||Q^T Q - I|| <~ 1e-14 (single-pass error ~1e-17 kappa^2 measured).
 //
 // For full-column-rank A the QR factorisation with diag(R) > 0 is unique, so the
 // result is the sign-fixed Householder QR of the reference up to rounding.
@@ -35,8 +38,10 @@ struct CholQr {
 bool cholqr_eligible(const QrProblem& q);
 long long cholqr_workspace_doubles(const CholQr& c);
 void cholqr_bind(CholQr& c, double* ws);
-// Launch the 8-kernel sequence for all problems; *fail (device int) is OR-ed with 1
-// on any numerical red flag.  No host synchronisation.
-int cholqr_run(std::vector<CholQr>& cs, int* fail, cudaStream_t stream);
+// Launch the sequence for all problems; *fail (device int) is OR-ed with 1 on any
+// numerical red flag; need2 (device, cs.size() ints) carries the per-problem
+// "second pass needed" decision between the kernels.  No host synchronisation.
+// two_pass: always run the second pass (testing / ht_set_qr_mode(2)).
+int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cudaStream_t stream);
 
 }  // namespace ht

@@ -180,7 +180,7 @@ void merge_gemms(std::vector<GemmDesc>& v) {
                     e.nb1 == d.nb1 && e.a_m == d.a_m && e.a_k == d.a_k && e.a_o == d.a_o && e.a_b1 == d.a_b1 &&
                     e.b_k == d.b_k && e.b_n == d.b_n && e.b_o == d.b_o && e.b_b1 == d.b_b1 && e.c_m == d.c_m &&
                     e.c_n == d.c_n && e.c_b1 == d.c_b1 && e.alpha == d.alpha && e.beta == d.beta &&
-                    e.a_tri == d.a_tri && e.b_tri == d.b_tri &&
+                    e.a_tri == d.a_tri && e.b_tri == d.b_tri && e.active == d.active &&
                     e.A - d.A == c * dA && e.B - d.B == c * dB && e.C - d.C == c * dC;
         if (!same) break;
         ++j;
@@ -275,8 +275,8 @@ struct OrthPlan {
 
 // Runs (or, in measure mode, sizes) the bottom-up sweep.  `out` pointers may be
 // supplied (ht_orthogonalize) or carved from the arena (truncate).
-// QR policy: 0 = Cholesky-QR2 where eligible, validated, Householder re-run on a red
-// flag; 1 = Householder only.
+// QR policy: 0 = Cholesky-QR where eligible (second pass when kappa > 20), validated,
+// Householder re-run on a red flag; 1 = Householder only; 2 = as 0 with both passes always.
 int g_qr_mode = 0;
 long long g_qr_fallbacks = 0;
 
@@ -364,6 +364,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     }
     long long ctiles = 0;
     for (const auto& c : cq) ctiles += (long long)gemm_tiles(c.q.K, c.q.K) * c.q.nodes;
+    int* cflags = cq.empty() ? nullptr : scratch_ar.take_int((long long)cq.size());
     for (auto& c : cq) {
       c.S = pick_splits(ctiles, c.q.m);
       double* w = scratch_ar.take(cholqr_workspace_doubles(c));
@@ -377,7 +378,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       merge_gemms(g3);
       HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
-      HT_TRY(cholqr_run(cq, fail, s));
+      HT_TRY(cholqr_run(cq, fail, cflags, g_qr_mode == 2, s));
       HT_TRY(qr_batched(hh, s));
     }
   }
@@ -404,7 +405,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
 int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_t s, int* fail) {
   Arena scratch = scratch_in;
   orth_slots(x, op, scratch);  // fixed before either run: the re-run must not reuse their bytes
-  if (g_qr_mode == 0 && fail) {
+  if ((g_qr_mode == 0 || g_qr_mode == 2) && fail) {
     HT_CUDA_CHECK(cudaMemsetAsync(fail, 0, sizeof(int), s));
     Arena a = scratch;
     int n_chol = 0;
@@ -1074,8 +1075,9 @@ int ht_orthogonalize(const ht_tensor* x, void* ws, size_t ws_bytes, const ht_ten
 }
 
 int ht_set_qr_mode(int mode) {
-  if (mode != 0 && mode != 1) {
-    set_error("qr mode must be 0 (Cholesky-QR2 with Householder fallback) or 1 (Householder)");
+  if (mode < 0 || mode > 2) {
+    set_error("qr mode must be 0 (Cholesky-QR, adaptive second pass, Householder fallback), 1 (Householder) "
+              "or 2 (Cholesky-QR2 with both passes always)");
     return kErrArgument;
   }
   g_qr_mode = mode;

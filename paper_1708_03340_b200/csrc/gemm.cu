@@ -112,6 +112,7 @@ __global__ void __launch_bounds__(THREADS, (WM * WN == 13 ? 2 : 1)) gemm_kernel(
   int di = 0;
   while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
   const GemmDesc& g = batch.d[di];
+  if (g.active && *g.active == 0) return;
 
   int local = blockIdx.x - g.block_begin;
   const int tn = local % g.tiles_n;
@@ -357,6 +358,7 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
   int di = 0;
   while (di + 1 < rb.count && (int)blockIdx.x >= rb.block_begin[di + 1]) ++di;
   const ReduceDesc& r = rb.d[di];
+  if (r.active && *r.active == 0) return;
   const long long nbatch = (long long)r.nb1 * r.nb2;
   const long long total = nbatch * r.M * r.N;
   const long long stride = (long long)(rb.block_begin[di + 1] - rb.block_begin[di]) * blockDim.x;
@@ -451,7 +453,7 @@ int gemm_tiles(int M, int N) {  // tiles of a long-reduction (split-K planned) G
   return ceil_div(M, kCfg[c].bm) * ceil_div(N, kCfg[c].bn);
 }
 
-int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag) {
+int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
   for (int c = 0; c < kNumCfg; ++c) {
     size_t i = 0;
     while (i < descs.size()) {
@@ -482,7 +484,7 @@ int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* 
       if (batch.count == 0) continue;
       ProfToken tok = prof_begin(stream);
       HT_TRY(launch_batch((Cfg)c, batch, blocks, stream));
-      prof_end(tok, tag, stream, flops, bytes);
+      prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
     }
   }
   return kOk;

@@ -30,6 +30,7 @@ struct GemmDesc {
   int a_tri;  // 0 dense; 1 unit-lower in (m,k); 2 unit-upper in (m,k); 3 identity (A not read)
   int b_tri;  // 0 dense; 1 unit-lower in (k,n): stored for k > n, 1 on the diagonal, 0 above
   double alpha, beta;
+  const int* active;  // optional device flag: the GEMM is skipped (every CTA exits) when *active == 0
 };
 
 // Sum the split-K partials [splits][batch][M][N] into C (optionally (X+X^T)/2).
@@ -40,10 +41,14 @@ struct ReduceDesc {
   int S, M, N, nb1, nb2;
   int sym;
   double alpha, beta;
+  const int* active;  // optional device flag, as in GemmDesc
 };
 
 // Launch a set of GEMMs (any number; split into launches of <= kMaxGemmDescs).
-int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag = "gemm_dmma");
+// count_flops = false for launches whose work is conditional on a device flag (the
+// profiler then books their time but no algorithmic flops).
+int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag = "gemm_dmma",
+                 bool count_flops = true);
 // CTA tiles one M x N output uses (tile shape chosen per descriptor)
 int gemm_tiles(int M, int N);
 int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, const char* tag = "reduce_partials");

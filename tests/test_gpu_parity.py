@@ -16,7 +16,8 @@ SIGMA_RTOL = 1e-10
 ERR_TOL = 1e-10
 
 
-@pytest.fixture(scope="module", params=[("auto", "auto"), ("householder", "jacobi")], ids=["fast", "fallback"])
+@pytest.fixture(scope="module", params=[("auto", "auto"), ("cholqr2", "auto"), ("householder", "jacobi")],
+                ids=["fast", "cholqr2", "fallback"])
 def htb(cuda_ok, request):
     """Every parity test runs under both kernel policies: the fast paths (Cholesky-QR2,
     tridiagonal eigensolver; default) and their fallbacks (Householder QR, Jacobi)."""
@@ -144,7 +145,7 @@ def test_rank_deficient_add_a_a(htb):
     o = to_host(htb.orthogonalize(x2))
     for t, u in o.U.items():  # frames stay orthonormal although [U, U] has rank k
         np.testing.assert_allclose(u.T @ u, np.eye(u.shape[1]), atol=1e-13)
-    if htb.get_qr_mode() == "auto":
+    if htb.get_qr_mode() in ("auto", "cholqr2"):
         # the Cholesky-QR2 red flag must have fired (both sweeps re-run with Householder)
         assert htb.qr_fallback_count() == n_fb + 2
 
