@@ -203,6 +203,14 @@ class HTensor:
         out._arena.copy_(host, non_blocking=True)
         return out
 
+    def load_host_arena(self, host: torch.Tensor) -> "HTensor":
+        """Overwrite this tensor's values from a flat host buffer (one async H2D copy on
+        the current stream; shapes must match).  Lets pipelines reuse device buffers."""
+        if self._arena is None or host.numel() != self._arena.numel():
+            raise ValueError("host arena size does not match the tensor shapes")
+        self._arena.copy_(host, non_blocking=True)
+        return self
+
     def to_host_arena(self, host: torch.Tensor | None = None) -> torch.Tensor:
         """Copy the whole tensor into a flat (pinned) host buffer with one D2H copy."""
         if self._arena is None:
