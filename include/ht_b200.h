@@ -204,9 +204,13 @@ int ht_set_eig_mode(int mode);
 
 /* Total kernel launches issued by this library since load (always counted). */
 int64_t ht_launch_count(void);
-/* on != 0: record a CUDA event pair on the launching stream around every kernel
- * launch and attribute algorithmic flops/bytes per kernel; clears the tally. */
+/* Bit 0: record a CUDA event pair on the launching stream around every kernel
+ * launch and attribute algorithmic flops/bytes per kernel; bit 1: keep a
+ * launch-order log of kernel tags (no events; for matching ncu launch lists).
+ * Clears the tally and the log. */
 int ht_profile_enable(int on);
+/* The launch-order log as JSON [["tag", flops, bytes], ...]; returns its length. */
+int ht_profile_log(char* buf, size_t len);
 /* Writes {"kernel": {"ms", "launches", "flops", "bytes"}, ...} JSON into buf
  * (synchronises the recorded events); returns the full JSON length. */
 int ht_profile_report(char* buf, size_t len);

@@ -36,7 +36,7 @@ EXPORTS = (
     "ht_inner_product_workspace_size", "ht_inner_product",
     "ht_apply_operator",
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
-    "ht_launch_count", "ht_profile_enable", "ht_profile_report",
+    "ht_launch_count", "ht_profile_enable", "ht_profile_report", "ht_profile_log",
     "ht_truncate_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_qr_fallback_count", "ht_set_eig_mode",
 )
 
@@ -104,6 +104,7 @@ def _declare(lib):
         "ht_set_eig_mode": ([ctypes.c_int], ctypes.c_int),
         "ht_profile_enable": ([ctypes.c_int], ctypes.c_int),
         "ht_profile_report": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
+        "ht_profile_log": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
         "ht_syev_batched": ([ctypes.c_int64, ctypes.c_int64, _vp, _vp, _vp, _vp], ctypes.c_int),
         "ht_gemm_strided": ([ctypes.c_int64] * 4 + [ctypes.c_double, _vp] + [ctypes.c_int64] * 3 + [_vp]
                             + [ctypes.c_int64] * 3 + [ctypes.c_double, _vp] + [ctypes.c_int64] * 3 + [_vp],
@@ -154,6 +155,17 @@ def profile_report() -> dict:
     n = lib.ht_profile_report(None, 0)
     buf = ctypes.create_string_buffer(n + 1)
     lib.ht_profile_report(buf, n + 1)
+    return json.loads(buf.value.decode())
+
+
+def profile_log() -> list:
+    """Launch-order kernel tags recorded while ht_profile_enable(2) was on."""
+    import json
+
+    lib = load()
+    n = lib.ht_profile_log(None, 0)
+    buf = ctypes.create_string_buffer(n + 1)
+    lib.ht_profile_log(buf, n + 1)
     return json.loads(buf.value.decode())
 
 

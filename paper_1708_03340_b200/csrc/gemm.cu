@@ -102,7 +102,7 @@ __device__ __forceinline__ const double* b_src(const GemmDesc& g, const double* 
 }
 
 template <int WM, int WN, int WARPS_M, int WARPS_N>
-__global__ void __launch_bounds__(THREADS, (WM * WN == 13 ? 2 : 1)) gemm_kernel(const __grid_constant__ GemmBatch batch) {
+__global__ void __launch_bounds__(THREADS, ((WM * WN == 13 || WM * WN == 14) ? 2 : 1)) gemm_kernel(const __grid_constant__ GemmBatch batch) {
   constexpr int BM = 8 * WM * WARPS_M, BN = 8 * WN * WARPS_N;
   constexpr int PA = pitch16(BM), PB = pitch16(BN);
   extern __shared__ __align__(16) double smem[];

@@ -29,6 +29,12 @@ bool g_on = false;
 std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_pool;
 std::map<std::string, Entry> g_acc;
+bool g_log_on = false;
+struct LogEntry {
+  std::string name;
+  double flops, bytes;
+};
+std::vector<LogEntry> g_log;  // launch-order tag log (ht_profile_enable bit 1)
 
 cudaEvent_t get_event() {
   if (!g_pool.empty()) {
@@ -71,6 +77,10 @@ ProfToken prof_begin(cudaStream_t s) {
 
 void prof_end(const ProfToken& tok, const char* name, cudaStream_t s, double flops, double bytes) {
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (g_log_on) {
+    std::lock_guard<std::mutex> g(g_mu);
+    g_log.push_back({name, flops, bytes});
+  }
   if (!tok.a) return;
   std::lock_guard<std::mutex> g(g_mu);
   cudaEvent_t b = get_event();
@@ -89,8 +99,28 @@ int ht_profile_enable(int on) {
   std::lock_guard<std::mutex> g(ht::g_mu);
   ht::drain_locked();
   ht::g_acc.clear();
-  ht::g_on = on != 0;
+  ht::g_log.clear();
+  ht::g_on = (on & 1) != 0;
+  ht::g_log_on = (on & 2) != 0;
   return 0;
+}
+
+int ht_profile_log(char* buf, size_t len) {
+  std::lock_guard<std::mutex> g(ht::g_mu);
+  std::string s = "[";
+  for (size_t i = 0; i < ht::g_log.size(); ++i) {
+    char tmp[256];
+    snprintf(tmp, sizeof(tmp), "%s[\"%s\", %.6e, %.6e]", i ? ", " : "", ht::g_log[i].name.c_str(),
+             ht::g_log[i].flops, ht::g_log[i].bytes);
+    s += tmp;
+  }
+  s += "]";
+  if (buf && len) {
+    size_t n = s.size() < len - 1 ? s.size() : len - 1;
+    memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return (int)s.size();
 }
 
 int ht_profile_report(char* buf, size_t len) {

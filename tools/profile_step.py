@@ -1,5 +1,9 @@
 """One C2 truncation step between cudaProfilerStart/Stop, for ncu
-(--profile-from-start off).  Usage: python tools/profile_step.py [d]"""
+(--profile-from-start off).  Also writes the launch-order kernel tags of that step
+to gpurun_out/tags.json so ncu launch lists can be attributed to pipeline stages.
+
+    python tools/profile_step.py [d]"""
+import json
 import os
 import sys
 
@@ -7,6 +11,7 @@ import torch
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_1708_03340_b200 as htb  # noqa: E402
+from paper_1708_03340_b200 import _lib  # noqa: E402
 
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 tree = htb.build_balanced_tree(d)
@@ -17,8 +22,15 @@ ctl = htb.TruncationControl.fixed_rank(50)
 for _ in range(2):
     htb.truncate(x, ctl)
 torch.cuda.synchronize()
+lib = _lib.load()
+lib.ht_profile_enable(2)
 torch.cuda.profiler.start()
 htb.truncate(x, ctl)
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("ok")
+tags = _lib.profile_log()
+lib.ht_profile_enable(0)
+os.makedirs("gpurun_out", exist_ok=True)
+with open("gpurun_out/tags.json", "w") as f:
+    json.dump(tags, f)
+print("ok", len(tags), "launches")
