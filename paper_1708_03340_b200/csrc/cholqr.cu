@@ -6,6 +6,7 @@
 #include "cholqr.cuh"
 #include "gemm.cuh"
 #include "prof.cuh"
+#include "ssgemm.cuh"
 
 namespace ht {
 namespace {
@@ -273,18 +274,25 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   HT_TRY(launch_chol(ch, fail, s));
   g.clear(); r.clear(); ch.clear();
   // Q1 = A R1^{-1}, straight into the output when the second pass can run in place
-  // (one CTA owns whole output rows: K <= 104), else into scratch
+  // (one CTA owns whole output rows: K <= 104), else into scratch.  R1^{-1} is the
+  // stationary operand of the streaming GEMM.
+  std::vector<SsDesc> sd;
   for (auto& c : cs) {
     const int K = c.q.K, m = c.q.m;
-    const bool inplace = K <= kCholInPlaceK;
-    GemmDesc d = inplace ? gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K)
-                         : gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.Q1, K, 1, m, K, K);
-    d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K;
-    d.c_b1 = inplace ? c.q.q_node : (long long)m * K;
+    if (K <= kCholInPlaceK) {
+      SsDesc d = ss_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+      d.jobs = c.q.nodes; d.x_job = c.q.a_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+      sd.push_back(d);
+      continue;
+    }
+    GemmDesc d = gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.Q1, K, 1, m, K, K);
+    d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K; d.c_b1 = (long long)m * K;
     g.push_back(d);
   }
+  HT_TRY(ss_gemm(sd, s, "ss_cholqr_q"));
   HT_TRY(gemm_grouped(g, s, "gemm_cholqr_q"));
   g.clear();
+  sd.clear();
   // pass 2 (skipped on the device unless need2): W2 = Q1^T Q1, R2 = chol(W2),
   // Q = Q1 R2^{-1}, R = R2 R1
   for (size_t p = 0; p < cs.size(); ++p) {
@@ -308,18 +316,24 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   for (size_t p = 0; p < cs.size(); ++p) {
     const CholQr& c = cs[p];
     const int K = c.q.K, m = c.q.m;
-    const bool inplace = K <= kCholInPlaceK;
-    GemmDesc d = inplace ? gemm_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K)
-                         : gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
-    d.nb1 = c.q.nodes; d.a_b1 = inplace ? c.q.q_node : (long long)m * K; d.b_b1 = (long long)K * K;
-    d.c_b1 = c.q.q_node;
-    d.active = need2 + p;
-    g.push_back(d);
+    if (K <= kCholInPlaceK) {  // Q <- Q R2^{-1} in place (each CTA owns whole rows)
+      SsDesc d = ss_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+      d.jobs = c.q.nodes; d.x_job = c.q.q_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+      d.active = need2 + p;
+      sd.push_back(d);
+    } else {
+      GemmDesc d = gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+      d.nb1 = c.q.nodes; d.a_b1 = (long long)m * K; d.b_b1 = (long long)K * K;
+      d.c_b1 = c.q.q_node;
+      d.active = need2 + p;
+      g.push_back(d);
+    }
     GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
     e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
     e.active = need2 + p;
     g.push_back(e);
   }
+  HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
   HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
   return kOk;
 }

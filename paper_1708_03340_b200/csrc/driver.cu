@@ -16,6 +16,7 @@
 #include "common.cuh"
 #include "eig.cuh"
 #include "gemm.cuh"
+#include "ssgemm.cuh"
 #include "ht_b200.h"
 #include "misc.cuh"
 #include "qr.cuh"
@@ -200,6 +201,44 @@ void merge_gemms(std::vector<GemmDesc>& v) {
   v.swap(out);
 }
 
+// Merge consecutive single-job stationary-operand GEMMs that differ only by constant
+// pointer deltas into one multi-job descriptor.
+void merge_ss(std::vector<SsDesc>& v) {
+  std::vector<SsDesc> out;
+  size_t i = 0;
+  while (i < v.size()) {
+    SsDesc d = v[i];
+    size_t j = i + 1;
+    if (d.jobs == 1 && j < v.size()) {
+      const long long dX = v[j].X - d.X, dS = v[j].S - d.S, dC = v[j].C - d.C;
+      while (j < v.size()) {
+        const SsDesc& e = v[j];
+        const long long c = (long long)(j - i);
+        const bool same = e.jobs == 1 && e.M == d.M && e.M_lo == d.M_lo && e.N == d.N && e.K == d.K &&
+                          e.x_hi == d.x_hi && e.x_lo == d.x_lo && e.x_k == d.x_k && e.s_k == d.s_k &&
+                          e.s_n == d.s_n && e.c_hi == d.c_hi && e.c_lo == d.c_lo && e.c_n == d.c_n &&
+                          e.alpha == d.alpha && e.beta == d.beta && e.active == d.active &&
+                          e.X - d.X == c * dX && e.S - d.S == c * dS && e.C - d.C == c * dC;
+        if (!same) break;
+        ++j;
+      }
+      if (j - i > 1) {
+        d.jobs = (int)(j - i);
+        d.x_job = dX;
+        d.s_job = dS;
+        d.c_job = dC;
+      } else {
+        j = i + 1;
+      }
+    }
+    out.push_back(d);
+    i = j;
+  }
+  v.swap(out);
+}
+
+bool ss_fits(long long N, long long K) { return N >= 1 && N <= kSsMaxN && K >= 1 && K <= kSsMaxK; }
+
 void merge_qrs(std::vector<QrProblem>& v) {
   std::vector<QrProblem> out;
   size_t i = 0;
@@ -314,6 +353,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   for (int l = T.depth; l >= 1; --l) {
     scratch_ar.off = scratch_base;
     std::vector<GemmDesc> g2, g3;
+    std::vector<SsDesc> sa2, sa3;
     std::vector<QrProblem> qs;
     std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
     for (int t : T.levels[l])
@@ -336,11 +376,21 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       double* T1 = T1s[t];
       double* Bp = Bps[t];
       // mode-2 absorb, per slice i: T1_i (k1o x k2) = R1 (k1o x k1) * B_i (k1 x k2)
-      GemmDesc a = gemm_desc(op.R[s1], k1, 1, x.p[t], k2, 1, T1, k2, 1, (int)k1o, (int)k2, (int)k1);
-      a.nb1 = (int)kt; a.a_b1 = 0; a.b_b1 = k1 * k2; a.c_b1 = k1o * k2;
-      g2.push_back(a);
+      if (ss_fits(k1o, k1)) {
+        // streamed as T1_i^T = B_i^T R1^T over the rows (i, l): R1^T stays in shared memory
+        SsDesc d = ss_desc(x.p[t], 1, k2, op.R[s1], 1, k1, T1, 1, k2, (int)(kt * k2), (int)k1o, (int)k1);
+        d.M_lo = (int)k2; d.x_hi = k1 * k2; d.c_hi = k1o * k2;
+        sa2.push_back(d);
+      } else {
+        GemmDesc a = gemm_desc(op.R[s1], k1, 1, x.p[t], k2, 1, T1, k2, 1, (int)k1o, (int)k2, (int)k1);
+        a.nb1 = (int)kt; a.a_b1 = 0; a.b_b1 = k1 * k2; a.c_b1 = k1o * k2;
+        g2.push_back(a);
+      }
       // mode-3 absorb: Bp ((kt k1o) x k2o) = T1 ((kt k1o) x k2) * R2^T
-      g3.push_back(gemm_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
+      if (ss_fits(k2o, k2))
+        sa3.push_back(ss_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
+      else
+        g3.push_back(gemm_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
       // QR of M23(Bp): (k1o k2o) x kt column-major, in place as reflector storage
       QrProblem q{};
       q.A = Bp; q.a_r = 1; q.a_c = k1o * k2o;
@@ -376,8 +426,12 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     if (exec) {
       merge_gemms(g2);
       merge_gemms(g3);
+      merge_ss(sa2);
+      merge_ss(sa3);
       HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
+      HT_TRY(ss_gemm(sa2, s, "ss_absorb"));
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
+      HT_TRY(ss_gemm(sa3, s, "ss_absorb"));
       HT_TRY(cholqr_run(cq, fail, cflags, g_qr_mode == 2, s));
       HT_TRY(qr_batched(hh, s));
     }
@@ -400,17 +454,71 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   return kOk;
 }
 
-// The orthogonalisation sweep as executed: Cholesky-QR2 first (if enabled), one
-// host synchronisation to read the red flag, Householder re-run if it is set.
-int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_t s, int* fail) {
+// Deferred read of the Cholesky-QR red flag: the flag is copied into pinned host
+// memory behind the sweep and an event recorded; the host only waits on that event
+// after it has enqueued the rest of the truncation, so the GPU never idles on it.
+struct OrthCheck {
+  int* host = nullptr;
+  cudaEvent_t ev = nullptr;
+  bool used = false;
+};
+
+std::mutex g_check_mu;
+std::vector<int*> g_check_slots;
+std::vector<cudaEvent_t> g_check_events;
+
+int check_acquire(OrthCheck& c) {
+  std::lock_guard<std::mutex> g(g_check_mu);
+  if (g_check_slots.empty()) {
+    int* block = nullptr;
+    HT_CUDA_CHECK(cudaHostAlloc((void**)&block, 64 * 64, cudaHostAllocDefault));
+    for (int i = 0; i < 64; ++i) g_check_slots.push_back(block + 16 * i);  // 64-byte apart
+  }
+  c.host = g_check_slots.back();
+  g_check_slots.pop_back();
+  if (g_check_events.empty()) {
+    cudaEvent_t e;
+    HT_CUDA_CHECK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    g_check_events.push_back(e);
+  }
+  c.ev = g_check_events.back();
+  g_check_events.pop_back();
+  return kOk;
+}
+
+// true when the flag reports a failed Cholesky-QR sweep (waits for the event)
+int check_result(OrthCheck& c, bool& failed) {
+  failed = false;
+  if (!c.used) return kOk;
+  HT_CUDA_CHECK(cudaEventSynchronize(c.ev));
+  failed = *(volatile int*)c.host != 0;
+  std::lock_guard<std::mutex> g(g_check_mu);
+  g_check_slots.push_back(c.host);
+  g_check_events.push_back(c.ev);
+  c = OrthCheck{};
+  return kOk;
+}
+
+// The orthogonalisation sweep as executed: Cholesky-QR first (if enabled) with a red
+// flag; Householder re-run if it is set.  With `deferred` the flag is only queued for
+// reading (check_result) and the caller re-runs what depends on the sweep.
+int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_t s, int* fail,
+               OrthCheck* deferred = nullptr, bool force_householder = false) {
   Arena scratch = scratch_in;
   orth_slots(x, op, scratch);  // fixed before either run: the re-run must not reuse their bytes
-  if ((g_qr_mode == 0 || g_qr_mode == 2) && fail) {
+  if ((g_qr_mode == 0 || g_qr_mode == 2) && fail && !force_householder) {
     HT_CUDA_CHECK(cudaMemsetAsync(fail, 0, sizeof(int), s));
     Arena a = scratch;
     int n_chol = 0;
     HT_TRY(run_orthogonalize(x, op, a, a, s, true, true, fail, &n_chol));
     if (n_chol == 0) return kOk;
+    if (deferred) {
+      HT_TRY(check_acquire(*deferred));
+      HT_CUDA_CHECK(cudaMemcpyAsync(deferred->host, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
+      HT_CUDA_CHECK(cudaEventRecord(deferred->ev, s));
+      deferred->used = true;
+      return kOk;
+    }
     int h = 0;
     HT_CUDA_CHECK(cudaMemcpyAsync(&h, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
     HT_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -621,9 +729,9 @@ int check_ws(const View& x, char* ws, size_t ws_bytes) {
   return kOk;
 }
 
-int phase_orth(const View& x, TruncPlan& P, cudaStream_t s) {
+int phase_orth(const View& x, TruncPlan& P, cudaStream_t s, OrthCheck* deferred = nullptr, bool force_hh = false) {
   if (x.orth) return kOk;
-  return orth_sweep(x, P.op, P.scratch, s, P.qr_fail);
+  return orth_sweep(x, P.op, P.scratch, s, P.qr_fail, deferred, force_hh);
 }
 
 int phase_gram(TruncPlan& P, cudaStream_t s) {
@@ -666,12 +774,13 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
   return eig_batched(eps, s);
 }
 
-int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s) {
+int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s,
+                    OrthCheck* deferred = nullptr, bool force_hh = false) {
   HT_TRY(check_ctl(ctl));
   HT_TRY(check_ws(x, ws, ws_bytes));
   HT_TRY(plan_truncate(x, P, ws));
   HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
-  HT_TRY(phase_orth(x, P, s));
+  HT_TRY(phase_orth(x, P, s, deferred, force_hh));
   HT_TRY(phase_gram(P, s));
   return phase_eig(x, ctl, P, s);
 }
@@ -886,7 +995,14 @@ int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, siz
   HT_TRY(make_view(x, v));
   cudaStream_t s = (cudaStream_t)stream;
   TruncPlan P;
-  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s));
+  OrthCheck chk;
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk));
+  bool failed = false;
+  HT_TRY(check_result(chk, failed));
+  if (failed) {  // Cholesky-QR red flag: redo the phase on the Householder path
+    ++g_qr_fallbacks;
+    HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, nullptr, true));
+  }
   std::vector<int> hr(v.T->nn + 1);
   HT_CUDA_CHECK(cudaMemcpyAsync(hr.data(), P.ranks, sizeof(int) * (v.T->nn + 1), cudaMemcpyDeviceToHost, s));
   HT_CUDA_CHECK(cudaStreamSynchronize(s));
@@ -936,7 +1052,16 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
     }
   cudaStream_t s = (cudaStream_t)stream;
   TruncPlan P;
-  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s));
+  OrthCheck chk;
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk));
+  HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s));
+  // the speculative result stands unless the Cholesky-QR flag was raised; then the
+  // whole truncation is recomputed on the Householder path (stream order overwrites)
+  bool failed = false;
+  HT_TRY(check_result(chk, failed));
+  if (!failed) return kOk;
+  ++g_qr_fallbacks;
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, nullptr, true));
   return truncate_phase2(v, ctl, (char*)ws, o, s);
 }
 
