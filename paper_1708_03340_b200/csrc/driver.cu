@@ -575,6 +575,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       if (!T.leaf(t) && o.on(t)) inner.push_back(t);
     if (inner.empty()) continue;
     std::vector<GemmDesc> g1s, g2s;
+    std::vector<SsDesc> s1s;
     std::vector<ReduceDesc> rs;
     long long tiles = 0;
     for (int t : inner) {
@@ -588,8 +589,12 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       const long long kt = o.k[t], k1 = o.k[s1], k2 = o.k[s2];
       const long long f = k1 * k2;
       double* t1 = t1s[t];
-      // t1 (kt x k1k2) = G_t (kt x kt) * M1(B)   (arith.py:155)
-      g1s.push_back(gemm_desc(G[t], kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
+      // t1 (kt x k1k2) = G_t (kt x kt) * M1(B)   (arith.py:155); streamed as
+      // t1^T = M1(B)^T G_t^T with G_t resident in shared memory
+      if (ss_fits(kt, kt))
+        s1s.push_back(ss_desc(o.p[t], 1, f, G[t], 1, kt, t1, 1, f, (int)f, (int)kt, (int)kt));
+      else
+        g1s.push_back(gemm_desc(G[t], kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
       const int S1 = pick_splits(tiles, kt * k2);
       const int S2 = pick_splits(tiles, kt * k1);
       double* P1 = scratch_ar.take(S1 * k1 * k1);
@@ -608,7 +613,9 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     mx = std::max(mx, scratch_ar.off);
     if (exec) {
       merge_gemms(g1s);
+      merge_ss(s1s);
       HT_TRY(gemm_grouped(g1s, s, "gemm_gram_t1"));
+      HT_TRY(ss_gemm(s1s, s, "ss_gram_t1"));
       HT_TRY(gemm_grouped(g2s, s, "gemm_gram_g"));
       HT_TRY(reduce_partials(rs, s));
     }
@@ -812,6 +819,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     }
   Arena sc = P.scratch;
   std::vector<GemmDesc> st1, st2, st3;
+  std::vector<SsDesc> ss1, ss2, ss3;
   std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
   for (int t = 1; t < T.nn; ++t)
     if (!T.leaf(t) && x.on(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
@@ -822,19 +830,35 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     const long long kt = o.k[t], rt = out.k[t];
     if (T.leaf(t)) {
       // U_new (n x r) = Q (n x k) * EV[:, :r]   (arith.py:344)
-      st1.push_back(gemm_desc(o.p[t], kt, 1, P.EV[t], kt, 1, out.p[t], rt, 1, (int)o.n[t], (int)rt, (int)kt));
+      if (ss_fits(rt, kt))
+        ss1.push_back(ss_desc(o.p[t], kt, 1, P.EV[t], kt, 1, out.p[t], rt, 1, (int)o.n[t], (int)rt, (int)kt));
+      else
+        st1.push_back(gemm_desc(o.p[t], kt, 1, P.EV[t], kt, 1, out.p[t], rt, 1, (int)o.n[t], (int)rt, (int)kt));
       continue;
     }
     const int s1 = T.son1[t], s2 = T.son2[t];
     const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
-    // mode 1: C1 (rt x k1k2) = EV_t^T[:rt] * M1(B)   (arith.py:168)
-    st1.push_back(gemm_desc(P.EV[t], 1, kt, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
-    // mode 2, per slice i: C2_i (r1 x k2) = EV_s1^T[:r1] * C1_i   (arith.py:169)
-    GemmDesc b = gemm_desc(P.EV[s1], 1, k1, C1[t], k2, 1, C2[t], k2, 1, (int)r1, (int)k2, (int)k1);
-    b.nb1 = (int)rt; b.a_b1 = 0; b.b_b1 = k1 * k2; b.c_b1 = r1 * k2;
-    st2.push_back(b);
+    // mode 1: C1 (rt x k1k2) = EV_t^T[:rt] * M1(B)   (arith.py:168); streamed as C1^T = M1(B)^T EV_t
+    if (ss_fits(rt, kt))
+      ss1.push_back(ss_desc(o.p[t], 1, k1 * k2, P.EV[t], kt, 1, C1[t], 1, k1 * k2, (int)(k1 * k2), (int)rt, (int)kt));
+    else
+      st1.push_back(gemm_desc(P.EV[t], 1, kt, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
+    // mode 2, per slice i: C2_i (r1 x k2) = EV_s1^T[:r1] * C1_i   (arith.py:169);
+    // streamed as C2_i^T = C1_i^T EV_s1 over the rows (i, l)
+    if (ss_fits(r1, k1)) {
+      SsDesc d = ss_desc(C1[t], 1, k2, P.EV[s1], k1, 1, C2[t], 1, k2, (int)(rt * k2), (int)r1, (int)k1);
+      d.M_lo = (int)k2; d.x_hi = k1 * k2; d.c_hi = r1 * k2;
+      ss2.push_back(d);
+    } else {
+      GemmDesc b = gemm_desc(P.EV[s1], 1, k1, C1[t], k2, 1, C2[t], k2, 1, (int)r1, (int)k2, (int)k1);
+      b.nb1 = (int)rt; b.a_b1 = 0; b.b_b1 = k1 * k2; b.c_b1 = r1 * k2;
+      st2.push_back(b);
+    }
     // mode 3: B_new ((rt r1) x r2) = C2 * EV_s2[:, :r2]   (arith.py:170)
-    st3.push_back(gemm_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
+    if (ss_fits(r2, k2))
+      ss3.push_back(ss_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
+    else
+      st3.push_back(gemm_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
   }
   if (x.on(0)) {
     // root: Q1^T B_D Q2   (arith.py:350-351)
@@ -847,9 +871,15 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   merge_gemms(st1);
   merge_gemms(st2);
   merge_gemms(st3);
+  merge_ss(ss1);
+  merge_ss(ss2);
+  merge_ss(ss3);
   HT_TRY(gemm_grouped(st1, s, "gemm_project"));
+  HT_TRY(ss_gemm(ss1, s, "ss_project"));
   HT_TRY(gemm_grouped(st2, s, "gemm_project"));
+  HT_TRY(ss_gemm(ss2, s, "ss_project"));
   HT_TRY(gemm_grouped(st3, s, "gemm_project"));
+  HT_TRY(ss_gemm(ss3, s, "ss_project"));
   return kOk;
 }
 
