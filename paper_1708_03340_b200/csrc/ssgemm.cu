@@ -9,8 +9,8 @@ namespace {
 
 constexpr int SST = 256;     // 8 warps
 constexpr int SBM = 128;     // rows per output tile (16 per warp: two m8 fragments)
-constexpr int NQ = SBM * 16 / SST;  // X elements each thread copies per stage (8)
 constexpr int SBK = 16;      // k-chunk per pipeline stage
+constexpr int NQ = SBM * SBK / SST;  // X elements each thread copies per stage
 constexpr int SSTAGES = 4;
 constexpr int kSsMaxDescs = 32;
 constexpr int kSMs = 148;
@@ -86,7 +86,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       ld_tile = mt;
 #pragma unroll
       for (int q = 0; q < NQ; ++q) {
-        const int r = kcontig ? (tid >> 4) + (SST / 16) * q : (tid & 127);
+        const int r = kcontig ? (tid / SBK) + (SST / SBK) * q : (tid & 127);
         const int m = mt * SBM + r;
         rowok[q] = m < M;
         const int mm = rowok[q] ? m : 0;
@@ -103,11 +103,11 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
         double* xs = Xs + (s % SSTAGES) * SBK * PX;
         const int kb = kc * SBK;
         if (kcontig) {
-          const int kk = tid & 15;
+          const int kk = tid % SBK;
           const bool kok = kb + kk < K;
 #pragma unroll
           for (int q = 0; q < NQ; ++q) {
-            const int r = (tid >> 4) + (SST / 16) * q;
+            const int r = tid / SBK + (SST / SBK) * q;
             const bool ok = kok && rowok[q];
             cp8z(xs + kk * PX + r, ok ? rowp[q] + (kb + kk) : X, ok);
           }
@@ -126,12 +126,11 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
 #pragma unroll
     for (int s = 0; s < SSTAGES - 1; ++s) issue(s);  // S travels with the first group
 
-    double acc[2][NF][2];
+    double acc[NF][4];  // m16n8 accumulators: rows g, g+8 of the warp's 16, cols 2t, 2t+1
 #pragma unroll
-    for (int f = 0; f < 2; ++f)
-#pragma unroll
-      for (int j = 0; j < NF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
-    const int ar = warp * 16 + (lane >> 2), kl = lane & 3, bc = lane >> 2;
+    for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    const int g8 = lane >> 2, t4 = lane & 3;
+    const int ar = warp * 16 + g8;
     const double alpha = g.alpha, beta = g.beta;
     for (int s = 0; s < nsteps; ++s) {
       cp_wait<SSTAGES - 2>();
@@ -140,14 +139,48 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       const double* xs = Xs + (s % SSTAGES) * SBK * PX;
       const int kc = s % KT;
       const double* ss = Ss + kc * SBK * PS;
+      const int krem = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
 #pragma unroll
-      for (int k4 = 0; k4 < SBK; k4 += 4) {
-        const double a0 = xs[(k4 + kl) * PX + ar], a1 = xs[(k4 + kl) * PX + ar + 8];
+      for (int k16 = 0; k16 < SBK; k16 += 16) {
+        const int kv = krem - k16;
+        if (kv <= 0) break;
+        const double* xk = xs + k16 * PX;
+        const double* sk = ss + k16 * PS;
+        if (kv >= 12) {  // m16n8k16 (k rows beyond K are zero in shared memory)
+          double a[8];
 #pragma unroll
-        for (int j = 0; j < NF; ++j) {
-          const double bv = ss[(k4 + kl) * PS + j * 8 + bc];
-          dmma_8x8x4(acc[0][j], a0, bv);
-          dmma_8x8x4(acc[1][j], a1, bv);
+          for (int i = 0; i < 8; ++i) a[i] = xk[(t4 + 4 * (i >> 1)) * PX + ar + 8 * (i & 1)];
+#pragma unroll
+          for (int j = 0; j < NF; ++j) {
+            double bq[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) bq[i] = sk[(t4 + 4 * i) * PS + j * 8 + g8];
+            dmma_16x8x16(acc[j], a, bq);
+          }
+        } else {  // tail: k8 and/or k4 steps
+          int k0 = 0;
+          if (kv > 4) {
+            double a[4], bq[2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) a[i] = xk[(t4 + 4 * (i >> 1)) * PX + ar + 8 * (i & 1)];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+              bq[0] = sk[t4 * PS + j * 8 + g8];
+              bq[1] = sk[(t4 + 4) * PS + j * 8 + g8];
+              dmma_16x8x8(acc[j], a, bq);
+            }
+            k0 = 8;
+          }
+          if (kv > k0) {
+            double a[2], bq[1];
+            a[0] = xk[(k0 + t4) * PX + ar];
+            a[1] = xk[(k0 + t4) * PX + ar + 8];
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+              bq[0] = sk[(k0 + t4) * PS + j * 8 + g8];
+              dmma_16x8x4(acc[j], a, bq);
+            }
+          }
         }
       }
       if (kc == KT - 1) {  // tile done: epilogue, then restart the accumulators
@@ -160,9 +193,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
             const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
-              const int n = j * 8 + 2 * kl;
+              const int n = j * 8 + 2 * t4;
+              const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
               if (pair && n + 1 < N) {
-                double2 r = make_double2(alpha * acc[f][j][0], alpha * acc[f][j][1]);
+                double2 r = make_double2(alpha * v0, alpha * v1);
                 double2* p = reinterpret_cast<double2*>(crow + n);
                 if (beta != 0.0) {
                   const double2 o = *p;
@@ -171,22 +205,20 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
                 }
                 *p = r;
               } else {
-#pragma unroll
-                for (int v = 0; v < 2; ++v)
-                  if (n + v < N) {
-                    double* p = crow + (long long)(n + v) * g.c_n;
-                    double r = alpha * acc[f][j][v];
-                    if (beta != 0.0) r += beta * *p;
-                    *p = r;
-                  }
+                if (n < N) {
+                  double* p = crow + (long long)n * g.c_n;
+                  *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
+                }
+                if (n + 1 < N) {
+                  double* p = crow + (long long)(n + 1) * g.c_n;
+                  *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
+                }
               }
             }
           }
         }
 #pragma unroll
-        for (int f = 0; f < 2; ++f)
-#pragma unroll
-          for (int j = 0; j < NF; ++j) acc[f][j][0] = acc[f][j][1] = 0.0;
+        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
       }
     }
     cp_wait<0>();
