@@ -14,6 +14,12 @@ constexpr int NQ = SBM * SBK / SST;  // X elements each thread copies per stage
 constexpr int SSTAGES = 4;
 constexpr int kSsMaxDescs = 32;
 constexpr int kSMs = 148;
+#ifndef SS_DEBUG_NO_EPILOGUE
+#define SS_DEBUG_NO_EPILOGUE 0
+#endif
+#ifndef SS_DEBUG_NO_XLOAD
+#define SS_DEBUG_NO_XLOAD 0
+#endif
 
 __host__ __device__ constexpr int ss_pitch(int x) { return ((x + 15) / 16) * 16 + 4; }  // 4 mod 16 doubles
 constexpr int PX = ss_pitch(SBM);
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     };
     const int nsteps = seg * KT;
     auto issue = [&](int s) {
-      if (s < nsteps) {
+      if (s < nsteps && !(SS_DEBUG_NO_XLOAD && s >= SSTAGES)) {
         const int mt = mt0 + s / KT, kc = s - (s / KT) * KT;
         if (mt != ld_tile) set_rows(mt);
         double* xs = Xs + (s % SSTAGES) * SBK * PX;
@@ -183,7 +189,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           }
         }
       }
-      if (kc == KT - 1) {  // tile done: epilogue, then restart the accumulators
+      if (SS_DEBUG_NO_EPILOGUE && kc == KT - 1 && alpha == 12345.0) {  // keep the MMAs alive
+        for (int j = 0; j < NF; ++j) C[j] = acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+      }
+      if (kc == KT - 1 && !SS_DEBUG_NO_EPILOGUE) {  // tile done: epilogue, then restart the accumulators
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
           const int m = (mt0 + s / KT) * SBM + ar + 8 * f;
@@ -220,6 +229,8 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
 #pragma unroll
         for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
       }
+      if (SS_DEBUG_NO_EPILOGUE && kc == KT - 1)
+        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
     }
     cp_wait<0>();
     t += seg;
