@@ -28,8 +28,8 @@ struct SsBatch {
   int count;
   int tile_begin[kSsMaxDescs + 1];  // prefix sums of jobs * tiles_m
   int tiles_m[kSsMaxDescs];
-  int chunk;                         // tiles per CTA
   int kp;                            // K rounded up to SBK (smem rows of S)
+  unsigned char vec[kSsMaxDescs];    // 16-byte X copies are legal for this descriptor
   SsDesc d[kSsMaxDescs];
 };
 
@@ -43,17 +43,30 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int NF>
+__device__ __forceinline__ void cp16z(double* smem, const double* gmem, int valid_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid_bytes));
+}
+
+constexpr int PK = SBK + 4;  // [m][k] layout pitch (4 mod 16 doubles: conflict-free fragments)
+constexpr int XSTAGE = (SBK * PX > SBM * PK) ? SBK * PX : SBM * PK;  // doubles per stage
+
+// LAYOUT 0: X m-contiguous (x_lo == 1), staged [k][m]; copies are row pairs (m, m+1).
+// LAYOUT 1: X k-contiguous (x_k == 1), staged [m][k]; copies are k pairs.
+// VEC: pairs are 16-byte aligned and never straddle an M_lo boundary -> one 16-byte
+// cp.async per pair, else two 8-byte ones.
+template <int NF, int LAYOUT>
 __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBatch b) {
   constexpr int NP = NF * 8;
   constexpr int PS = ss_pitch(NP);
   extern __shared__ __align__(16) double smem[];
-  double* Xs = smem;                        // [SSTAGES][SBK][PX]
-  double* Ss = smem + SSTAGES * SBK * PX;   // [kp][PS]
+  double* Xs = smem;                    // [SSTAGES][XSTAGE]
+  double* Ss = smem + SSTAGES * XSTAGE;  // [kp][PS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int total = b.tile_begin[b.count];
-  int t = blockIdx.x * b.chunk;
-  const int t_end = min(total, t + b.chunk);
+  const int G = gridDim.x;
+  int t = (int)((long long)blockIdx.x * total / G);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * total / G);
 
   while (t < t_end) {
     int di = 0;
@@ -72,7 +85,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     const double* X = g.X + job * g.x_job;
     const double* S = g.S + job * g.s_job;
     double* C = g.C + job * g.c_job;
-    const bool kcontig = g.x_k == 1;
+    const bool vec = b.vec[di];
     __syncthreads();  // the previous segment is done with the shared buffers
 
     // stationary operand: S(k, n) for k < KT*SBK, n < NP (zero padded)
@@ -82,23 +95,32 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       cp8z(Ss + k * PS + n, ok ? S + k * g.s_k + n * g.s_n : S, ok);
     }
 
-    // loader state: rows this thread copies for the tile currently being loaded
-    // k-contiguous X: element e = tid + SST*q -> row e/16 = tid/16 + 16q, kk = tid%16
-    // m-contiguous X: element e -> kk = e/128 = tid/128 + 2q, row = tid%128
+    // loader: LAYOUT 0 -> pair of rows (2*mp, 2*mp+1) with mp = tid%64, kk = tid/64 + 4q
+    //         LAYOUT 1 -> rows tid/8 + 32q, k pair (2*(tid%8), +1)
+    constexpr int NR = LAYOUT == 0 ? 2 : 4;
     int ld_tile = -1;
-    const double* rowp[NQ];
-    bool rowok[NQ];
+    const double* rowp[NR];
+    int rowv[NR];  // LAYOUT 0: valid rows of the pair (0..2); LAYOUT 1: row valid (0/1)
     auto set_rows = [&](int mt) {
       ld_tile = mt;
+      if (LAYOUT == 0) {
+        const int m = mt * SBM + 2 * (tid & 63);
 #pragma unroll
-      for (int q = 0; q < NQ; ++q) {
-        const int r = kcontig ? (tid / SBK) + (SST / SBK) * q : (tid & 127);
-        const int m = mt * SBM + r;
-        rowok[q] = m < M;
-        const int mm = rowok[q] ? m : 0;
-        const int hi = mm / M_lo, lo = mm - hi * M_lo;
-        rowp[q] = X + hi * g.x_hi + lo * g.x_lo;
-        if (!kcontig) break;
+        for (int u = 0; u < 2; ++u) {
+          const int mm = min(m + u, M - 1);
+          const int hi = mm / M_lo, lo = mm - hi * M_lo;
+          rowp[u] = X + hi * g.x_hi + lo * g.x_lo;
+        }
+        rowv[0] = max(0, min(2, M - m));
+      } else {
+#pragma unroll
+        for (int q = 0; q < NR; ++q) {
+          const int m = mt * SBM + (tid >> 3) + 32 * q;
+          rowv[q] = m < M;
+          const int mm = rowv[q] ? m : 0;
+          const int hi = mm / M_lo, lo = mm - hi * M_lo;
+          rowp[q] = X + hi * g.x_hi + lo * g.x_lo;
+        }
       }
     };
     const int nsteps = seg * KT;
@@ -106,24 +128,37 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       if (s < nsteps && !(SS_DEBUG_NO_XLOAD && s >= SSTAGES)) {
         const int mt = mt0 + s / KT, kc = s - (s / KT) * KT;
         if (mt != ld_tile) set_rows(mt);
-        double* xs = Xs + (s % SSTAGES) * SBK * PX;
+        double* xs = Xs + (s % SSTAGES) * XSTAGE;
         const int kb = kc * SBK;
-        if (kcontig) {
-          const int kk = tid % SBK;
-          const bool kok = kb + kk < K;
+        if (LAYOUT == 0) {
+          const int r = 2 * (tid & 63);
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const int r = tid / SBK + (SST / SBK) * q;
-            const bool ok = kok && rowok[q];
-            cp8z(xs + kk * PX + r, ok ? rowp[q] + (kb + kk) : X, ok);
+          for (int q = 0; q < 4; ++q) {
+            const int kk = (tid >> 6) + 4 * q;
+            const int nv = kb + kk < K ? rowv[0] : 0;
+            double* dst = xs + kk * PX + r;
+            const long long ko = (long long)(kb + kk) * g.x_k;
+            if (vec) {
+              cp16z(dst, nv ? rowp[0] + ko : X, 8 * nv);
+            } else {
+              cp8z(dst, nv > 0 ? rowp[0] + ko : X, nv > 0);
+              cp8z(dst + 1, nv > 1 ? rowp[1] + ko : X, nv > 1);
+            }
           }
         } else {
-          const int r = tid & 127;
+          const int kk = 2 * (tid & 7);
+          const int kv = max(0, min(2, K - (kb + kk)));
 #pragma unroll
-          for (int q = 0; q < NQ; ++q) {
-            const int kk = (tid >> 7) + (SST / 128) * q;
-            const bool ok = rowok[0] && kb + kk < K;
-            cp8z(xs + kk * PX + r, ok ? rowp[0] + (long long)(kb + kk) * g.x_k : X, ok);
+          for (int q = 0; q < NR; ++q) {
+            const int r = (tid >> 3) + 32 * q;
+            const int nv = rowv[q] ? kv : 0;
+            double* dst = xs + r * PK + kk;
+            if (vec) {
+              cp16z(dst, nv ? rowp[q] + kb + kk : X, 8 * nv);
+            } else {
+              cp8z(dst, nv > 0 ? rowp[q] + kb + kk : X, nv > 0);
+              cp8z(dst + 1, nv > 1 ? rowp[q] + kb + kk + 1 : X, nv > 1);
+            }
           }
         }
       }
@@ -138,11 +173,15 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     const int g8 = lane >> 2, t4 = lane & 3;
     const int ar = warp * 16 + g8;
     const double alpha = g.alpha, beta = g.beta;
+    // fragment element (row ar + 8*rs, k) of the current stage
+    auto xa = [&](const double* xs, int rs, int k) -> double {
+      return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
+    };
     for (int s = 0; s < nsteps; ++s) {
       cp_wait<SSTAGES - 2>();
       __syncthreads();
       issue(s + SSTAGES - 1);
-      const double* xs = Xs + (s % SSTAGES) * SBK * PX;
+      const double* xs = Xs + (s % SSTAGES) * XSTAGE;
       const int kc = s % KT;
       const double* ss = Ss + kc * SBK * PS;
       const int krem = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
@@ -150,12 +189,11 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       for (int k16 = 0; k16 < SBK; k16 += 16) {
         const int kv = krem - k16;
         if (kv <= 0) break;
-        const double* xk = xs + k16 * PX;
         const double* sk = ss + k16 * PS;
         if (kv >= 12) {  // m16n8k16 (k rows beyond K are zero in shared memory)
           double a[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = xk[(t4 + 4 * (i >> 1)) * PX + ar + 8 * (i & 1)];
+          for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, k16 + t4 + 4 * (i >> 1));
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
             double bq[4];
@@ -168,7 +206,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           if (kv > 4) {
             double a[4], bq[2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xk[(t4 + 4 * (i >> 1)) * PX + ar + 8 * (i & 1)];
+            for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, k16 + t4 + 4 * (i >> 1));
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
               bq[0] = sk[t4 * PS + j * 8 + g8];
@@ -179,8 +217,8 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           }
           if (kv > k0) {
             double a[2], bq[1];
-            a[0] = xk[(k0 + t4) * PX + ar];
-            a[1] = xk[(k0 + t4) * PX + ar + 8];
+            a[0] = xa(xs, 0, k16 + k0 + t4);
+            a[1] = xa(xs, 1, k16 + k0 + t4);
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
               bq[0] = sk[(k0 + t4) * PS + j * 8 + g8];
@@ -237,27 +275,37 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
   }
 }
 
-size_t ss_smem(int nf, int kp) { return sizeof(double) * ((size_t)SSTAGES * SBK * PX + (size_t)kp * ss_pitch(nf * 8)); }
+size_t ss_smem(int nf, int kp) { return sizeof(double) * ((size_t)SSTAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8)); }
 
-template <int NF>
+template <int NF, int LAYOUT>
 int launch_ss(SsBatch& b, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ss_smem(NF, kSsMaxK)));
     attr = true;
   }
   const int total = b.tile_begin[b.count];
-  const int grid = (total + b.chunk - 1) / b.chunk;
-  ss_kernel<NF><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
+  const int grid = std::min(total, kSMs);  // persistent: balanced contiguous tile ranges
+  ss_kernel<NF, LAYOUT><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
   HT_LAUNCH_CHECK();
   return kOk;
+}
+
+// 16-byte copies of X pairs are legal when every pair start is 16-byte aligned and
+// (LAYOUT 0) a row pair never straddles an M_lo boundary.
+bool ss_vec_ok(const SsDesc& d, int layout) {
+  auto even = [](long long v) { return (v & 1) == 0; };
+  if (((uintptr_t)d.X & 15) != 0 || !even(d.x_job) || !even(d.x_hi)) return false;
+  if (layout == 0) return even(d.M_lo) && even(d.x_k);
+  return even(d.x_lo);
 }
 
 }  // namespace
 
 int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
-  for (int variant = 0; variant < 2; ++variant) {
+  for (int variant = 0; variant < 4; ++variant) {  // (N <= 56 | N <= 104) x (LAYOUT 0 | 1)
+    const int nclass = variant >> 1, layout = variant & 1;
     size_t i = 0;
     while (i < descs.size()) {
       SsBatch b;
@@ -268,13 +316,15 @@ int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bo
       while (i < descs.size() && b.count < kSsMaxDescs) {
         const SsDesc& d = descs[i++];
         if (d.M <= 0 || d.N <= 0 || d.jobs <= 0) continue;
-        if (d.K > kSsMaxK || d.N > kSsMaxN || d.K < 1) {
-          set_error("ss_gemm: K or N outside the stationary-operand kernel");
+        if (d.K > kSsMaxK || d.N > kSsMaxN || d.K < 1 || (d.x_k != 1 && d.x_lo != 1)) {
+          set_error("ss_gemm: operand outside the stationary-operand kernel (K, N or X strides)");
           return kErrUnsupported;
         }
-        if ((d.N <= 56 ? 0 : 1) != variant) continue;
+        const int dl = d.x_lo == 1 && d.x_k != 1 ? 0 : 1;  // m-contiguous -> LAYOUT 0
+        if ((d.N <= 56 ? 0 : 1) != nclass || dl != layout) continue;
         const int tm = (d.M + SBM - 1) / SBM;
         b.tiles_m[b.count] = tm;
+        b.vec[b.count] = ss_vec_ok(d, layout) ? 1 : 0;
         b.d[b.count] = d;
         b.tile_begin[b.count + 1] = b.tile_begin[b.count] + tm * d.jobs;
         kmax = std::max(kmax, d.K);
@@ -283,11 +333,12 @@ int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bo
         ++b.count;
       }
       if (b.count == 0) continue;
-      const int total = b.tile_begin[b.count];
-      b.chunk = std::max(1, (total + kSMs - 1) / kSMs);
       b.kp = (kmax + SBK - 1) / SBK * SBK;
       ProfToken tok = prof_begin(stream);
-      HT_TRY(variant == 0 ? launch_ss<7>(b, stream) : launch_ss<13>(b, stream));
+      int rc;
+      if (nclass == 0) rc = layout == 0 ? launch_ss<7, 0>(b, stream) : launch_ss<7, 1>(b, stream);
+      else rc = layout == 0 ? launch_ss<13, 0>(b, stream) : launch_ss<13, 1>(b, stream);
+      HT_TRY(rc);
       prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
     }
   }
