@@ -282,6 +282,7 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
     if (K <= kCholInPlaceK) {
       SsDesc d = ss_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
       d.jobs = c.q.nodes; d.x_job = c.q.a_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+      d.s_tri = 2;  // R^{-1} upper triangular
       sd.push_back(d);
       continue;
     }
@@ -319,6 +320,7 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
     if (K <= kCholInPlaceK) {  // Q <- Q R2^{-1} in place (each CTA owns whole rows)
       SsDesc d = ss_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
       d.jobs = c.q.nodes; d.x_job = c.q.q_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+      d.s_tri = 2;
       d.active = need2 + p;
       sd.push_back(d);
     } else {

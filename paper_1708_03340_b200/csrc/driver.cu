@@ -217,7 +217,7 @@ void merge_ss(std::vector<SsDesc>& v) {
         const bool same = e.jobs == 1 && e.M == d.M && e.M_lo == d.M_lo && e.N == d.N && e.K == d.K &&
                           e.x_hi == d.x_hi && e.x_lo == d.x_lo && e.x_k == d.x_k && e.s_k == d.s_k &&
                           e.s_n == d.s_n && e.c_hi == d.c_hi && e.c_lo == d.c_lo && e.c_n == d.c_n &&
-                          e.alpha == d.alpha && e.beta == d.beta && e.active == d.active &&
+                          e.alpha == d.alpha && e.beta == d.beta && e.active == d.active && e.s_tri == d.s_tri &&
                           e.X - d.X == c * dX && e.S - d.S == c * dS && e.C - d.C == c * dC;
         if (!same) break;
         ++j;
@@ -380,6 +380,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
         // streamed as T1_i^T = B_i^T R1^T over the rows (i, l): R1^T stays in shared memory
         SsDesc d = ss_desc(x.p[t], 1, k2, op.R[s1], 1, k1, T1, 1, k2, (int)(kt * k2), (int)k1o, (int)k1);
         d.M_lo = (int)k2; d.x_hi = k1 * k2; d.c_hi = k1o * k2;
+        d.s_tri = 1;  // S = R1^T: R1 upper triangular
         sa2.push_back(d);
       } else {
         GemmDesc a = gemm_desc(op.R[s1], k1, 1, x.p[t], k2, 1, T1, k2, 1, (int)k1o, (int)k2, (int)k1);
@@ -387,8 +388,11 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
         g2.push_back(a);
       }
       // mode-3 absorb: Bp ((kt k1o) x k2o) = T1 ((kt k1o) x k2) * R2^T
-      if (ss_fits(k2o, k2))
-        sa3.push_back(ss_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
+      if (ss_fits(k2o, k2)) {
+        SsDesc d = ss_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2);
+        d.s_tri = 1;  // S = R2^T
+        sa3.push_back(d);
+      }
       else
         g3.push_back(gemm_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
       // QR of M23(Bp): (k1o k2o) x kt column-major, in place as reflector storage

@@ -173,6 +173,11 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     const int g8 = lane >> 2, t4 = lane & 3;
     const int ar = warp * 16 + g8;
     const double alpha = g.alpha, beta = g.beta;
+    const int s_tri = g.s_tri;
+    // the (k-range [k_lo, k_hi], fragment j) MMA block is structurally zero
+    auto zero_block = [&](int k_lo, int k_hi, int j) {
+      return (s_tri == 1 && k_hi < 8 * j) || (s_tri == 2 && k_lo > 8 * j + 7);
+    };
     // fragment element (row ar + 8*rs, k) of the current stage
     auto xa = [&](const double* xs, int rs, int k) -> double {
       return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
@@ -194,8 +199,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           double a[8];
 #pragma unroll
           for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, k16 + t4 + 4 * (i >> 1));
+          const int kg = kc * SBK + k16;  // global k of this block
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
+            if (zero_block(kg, kg + 15, j)) continue;
             double bq[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) bq[i] = sk[(t4 + 4 * i) * PS + j * 8 + g8];

@@ -30,6 +30,8 @@ struct SsDesc {
   int M, M_lo, N, K, jobs;
   double alpha, beta;
   const int* active;  // optional device flag: skip when *active == 0
+  int s_tri;          // 0 dense S; 1: S(k, n) = 0 for k < n; 2: S(k, n) = 0 for k > n
+                      // (triangular factors: the zero (k16 x n8) MMA blocks are skipped)
 };
 
 constexpr int kSsMaxK = 128;
