@@ -75,6 +75,16 @@ __device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8
       : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
         "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
+// predicated form: no-op when !p (branch-free skipping of structurally zero blocks)
+__device__ __forceinline__ void dmma_16x8x16_if(bool p, double (&c)[4], const double (&a)[8], const double (&b)[4]) {
+  asm volatile(
+      "{\n .reg .pred q;\n setp.ne.b32 q, %16, 0;\n"
+      " @q mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
+      "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n}\n"
+      : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
+      : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(a[4]), "d"(a[5]), "d"(a[6]), "d"(a[7]), "d"(b[0]),
+        "d"(b[1]), "d"(b[2]), "d"(b[3]), "r"((int)p));
+}
 __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double* a, const double* b) {
   asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])

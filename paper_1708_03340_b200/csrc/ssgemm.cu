@@ -55,7 +55,7 @@ constexpr int XSTAGE = (SBK * PX > SBM * PK) ? SBK * PX : SBM * PK;  // doubles 
 // LAYOUT 1: X k-contiguous (x_k == 1), staged [m][k]; copies are k pairs.
 // VEC: pairs are 16-byte aligned and never straddle an M_lo boundary -> one 16-byte
 // cp.async per pair, else two 8-byte ones.
-template <int NF, int LAYOUT>
+template <int NF, int LAYOUT, int TRI>
 __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBatch b) {
   constexpr int NP = NF * 8;
   constexpr int PS = ss_pitch(NP);
@@ -124,12 +124,14 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       }
     };
     const int nsteps = seg * KT;
-    auto issue = [&](int s) {
-      if (s < nsteps && !(SS_DEBUG_NO_XLOAD && s >= SSTAGES)) {
-        const int mt = mt0 + s / KT, kc = s - (s / KT) * KT;
-        if (mt != ld_tile) set_rows(mt);
-        double* xs = Xs + (s % SSTAGES) * XSTAGE;
-        const int kb = kc * SBK;
+    // loader cursor (step ld_s = (tile ld_mt, chunk ld_kc) into stage ld_st), advanced
+    // incrementally: no divisions in the steady state
+    int ld_s = 0, ld_mt = mt0, ld_kc = 0, ld_st = 0;
+    auto issue = [&]() {
+      if (ld_s < nsteps && !(SS_DEBUG_NO_XLOAD && ld_s >= SSTAGES)) {
+        if (ld_mt != ld_tile) set_rows(ld_mt);
+        double* xs = Xs + ld_st * XSTAGE;
+        const int kb = ld_kc * SBK;
         if (LAYOUT == 0) {
           const int r = 2 * (tid & 63);
 #pragma unroll
@@ -163,9 +165,15 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
         }
       }
       cp_commit();
+      ++ld_s;
+      if (++ld_kc == KT) {
+        ld_kc = 0;
+        ++ld_mt;
+      }
+      if (++ld_st == SSTAGES) ld_st = 0;
     };
 #pragma unroll
-    for (int s = 0; s < SSTAGES - 1; ++s) issue(s);  // S travels with the first group
+    for (int s = 0; s < SSTAGES - 1; ++s) issue();  // S travels with the first group
 
     double acc[NF][4];  // m16n8 accumulators: rows g, g+8 of the warp's 16, cols 2t, 2t+1
 #pragma unroll
@@ -173,21 +181,21 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     const int g8 = lane >> 2, t4 = lane & 3;
     const int ar = warp * 16 + g8;
     const double alpha = g.alpha, beta = g.beta;
-    const int s_tri = g.s_tri;
-    // the (k-range [k_lo, k_hi], fragment j) MMA block is structurally zero
+    // the (k-range [k_lo, k_hi], fragment j) MMA block is structurally zero (TRI is the
+    // batch's triangular pattern of S, a template parameter: dense batches have no branches)
     auto zero_block = [&](int k_lo, int k_hi, int j) {
-      return (s_tri == 1 && k_hi < 8 * j) || (s_tri == 2 && k_lo > 8 * j + 7);
+      return (TRI == 1 && k_hi < 8 * j) || (TRI == 2 && k_lo > 8 * j + 7);
     };
     // fragment element (row ar + 8*rs, k) of the current stage
     auto xa = [&](const double* xs, int rs, int k) -> double {
       return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
     };
+    int st = 0, kc = 0, mt = mt0;  // compute cursor
     for (int s = 0; s < nsteps; ++s) {
       cp_wait<SSTAGES - 2>();
       __syncthreads();
-      issue(s + SSTAGES - 1);
-      const double* xs = Xs + (s % SSTAGES) * XSTAGE;
-      const int kc = s % KT;
+      issue();
+      const double* xs = Xs + st * XSTAGE;
       const double* ss = Ss + kc * SBK * PS;
       const int krem = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
 #pragma unroll
@@ -202,11 +210,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           const int kg = kc * SBK + k16;  // global k of this block
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
-            if (zero_block(kg, kg + 15, j)) continue;
             double bq[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) bq[i] = sk[(t4 + 4 * i) * PS + j * 8 + g8];
-            dmma_16x8x16(acc[j], a, bq);
+            if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
           }
         } else {  // tail: k8 and/or k4 steps
           int k0 = 0;
@@ -240,7 +247,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       if (kc == KT - 1 && !SS_DEBUG_NO_EPILOGUE) {  // tile done: epilogue, then restart the accumulators
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
-          const int m = (mt0 + s / KT) * SBM + ar + 8 * f;
+          const int m = mt * SBM + ar + 8 * f;
           if (m < M) {
             const int hi = m / M_lo, lo = m - hi * M_lo;
             double* crow = C + hi * g.c_hi + lo * g.c_lo;
@@ -276,6 +283,11 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       }
       if (SS_DEBUG_NO_EPILOGUE && kc == KT - 1)
         for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+      if (++st == SSTAGES) st = 0;
+      if (++kc == KT) {
+        kc = 0;
+        ++mt;
+      }
     }
     cp_wait<0>();
     t += seg;
@@ -284,17 +296,17 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
 
 size_t ss_smem(int nf, int kp) { return sizeof(double) * ((size_t)SSTAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8)); }
 
-template <int NF, int LAYOUT>
+template <int NF, int LAYOUT, int TRI>
 int launch_ss(SsBatch& b, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF, LAYOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF, LAYOUT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ss_smem(NF, kSsMaxK)));
     attr = true;
   }
   const int total = b.tile_begin[b.count];
   const int grid = std::min(total, kSMs);  // persistent: balanced contiguous tile ranges
-  ss_kernel<NF, LAYOUT><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
+  ss_kernel<NF, LAYOUT, TRI><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
   HT_LAUNCH_CHECK();
   return kOk;
 }
@@ -311,8 +323,8 @@ bool ss_vec_ok(const SsDesc& d, int layout) {
 }  // namespace
 
 int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
-  for (int variant = 0; variant < 4; ++variant) {  // (N <= 56 | N <= 104) x (LAYOUT 0 | 1)
-    const int nclass = variant >> 1, layout = variant & 1;
+  for (int variant = 0; variant < 12; ++variant) {  // (N <= 56 | N <= 104) x LAYOUT x TRI
+    const int nclass = variant / 6, layout = (variant / 3) % 2, tri = variant % 3;
     size_t i = 0;
     while (i < descs.size()) {
       SsBatch b;
@@ -328,7 +340,7 @@ int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bo
           return kErrUnsupported;
         }
         const int dl = d.x_lo == 1 && d.x_k != 1 ? 0 : 1;  // m-contiguous -> LAYOUT 0
-        if ((d.N <= 56 ? 0 : 1) != nclass || dl != layout) continue;
+        if ((d.N <= 56 ? 0 : 1) != nclass || dl != layout || d.s_tri != tri) continue;
         const int tm = (d.M + SBM - 1) / SBM;
         b.tiles_m[b.count] = tm;
         b.vec[b.count] = ss_vec_ok(d, layout) ? 1 : 0;
@@ -342,9 +354,13 @@ int ss_gemm(std::vector<SsDesc>& descs, cudaStream_t stream, const char* tag, bo
       if (b.count == 0) continue;
       b.kp = (kmax + SBK - 1) / SBK * SBK;
       ProfToken tok = prof_begin(stream);
-      int rc;
-      if (nclass == 0) rc = layout == 0 ? launch_ss<7, 0>(b, stream) : launch_ss<7, 1>(b, stream);
-      else rc = layout == 0 ? launch_ss<13, 0>(b, stream) : launch_ss<13, 1>(b, stream);
+      int rc = kErrArgument;
+#define HT_SS_CASE(NFv, Lv, Tv) \
+  if (nclass == (NFv == 7 ? 0 : 1) && layout == Lv && tri == Tv) rc = launch_ss<NFv, Lv, Tv>(b, stream);
+      HT_SS_CASE(7, 0, 0) HT_SS_CASE(7, 0, 1) HT_SS_CASE(7, 0, 2) HT_SS_CASE(7, 1, 0) HT_SS_CASE(7, 1, 1)
+      HT_SS_CASE(7, 1, 2) HT_SS_CASE(13, 0, 0) HT_SS_CASE(13, 0, 1) HT_SS_CASE(13, 0, 2) HT_SS_CASE(13, 1, 0)
+      HT_SS_CASE(13, 1, 1) HT_SS_CASE(13, 1, 2)
+#undef HT_SS_CASE
       HT_TRY(rc);
       prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
     }

@@ -11,7 +11,7 @@ __device__ __forceinline__ void mma16(double (&c)[4], const double (&a)[8], cons
                  "d"(b[0]), "d"(b[1]), "d"(b[2]), "d"(b[3]));
 }
 
-template <int NF, bool LDSB, bool BAR>
+template <int NF, bool LDSB, bool BAR, bool LDSA = false>
 __global__ void kern(double* out, int iters) {
   __shared__ double sb[16 * 116];
   for (int i = threadIdx.x; i < 16 * 116; i += blockDim.x) sb[i] = 1.0 + i * 1e-9;
@@ -22,12 +22,16 @@ __global__ void kern(double* out, int iters) {
   for (int j = 0; j < NF; ++j) c[j][0] = c[j][1] = c[j][2] = c[j][3] = 0.0;
   double breg[4] = {1.0, 1.0, 1.0, 1.0};
   for (int it = 0; it < iters; ++it) {
+    if (LDSA) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) a[i] = sb[(t + 4 * (i >> 1)) * 116 + g + 8 * (i & 1) + (it & 1) * 4];
+    }
 #pragma unroll
     for (int j = 0; j < NF; ++j) {
       double b[4];
       if (LDSB) {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) b[i] = sb[(t + 4 * i) * 116 + j * 8 + g];
+        for (int i = 0; i < 4; ++i) b[i] = sb[(t + 4 * i) * 116 + j * 8 + g + (it & 1) * 2];
       } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) b[i] = breg[i];
@@ -41,15 +45,15 @@ __global__ void kern(double* out, int iters) {
   if (s == 12345.0) out[0] = s;
 }
 
-template <int NF, bool LDSB, bool BAR>
+template <int NF, bool LDSB, bool BAR, bool LDSA = false>
 void run(const char* name, int warps, double* out) {
   int iters = 2000;
   const int grid = 148;
-  kern<NF, LDSB, BAR><<<grid, warps * 32>>>(out, 10);
+  kern<NF, LDSB, BAR, LDSA><<<grid, warps * 32>>>(out, 10);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0); cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  kern<NF, LDSB, BAR><<<grid, warps * 32>>>(out, iters);
+  kern<NF, LDSB, BAR, LDSA><<<grid, warps * 32>>>(out, iters);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms; cudaEventElapsedTime(&ms, e0, e1);
@@ -59,10 +63,11 @@ void run(const char* name, int warps, double* out) {
 
 int main() {
   double* out; cudaMalloc(&out, 8);
-  for (int w : {4, 8, 16}) {
+  for (int w : {4, 8}) {
     run<13, false, false>("regs B, no barrier", w, out);
-    run<13, true, false>("LDS B, no barrier", w, out);
-    run<13, true, true>("LDS B, barrier/13 MMAs", w, out);
+    run<13, true, false>("LDS B (moving), no barrier", w, out);
+    run<13, true, true>("LDS B (moving), barrier", w, out);
+    run<13, true, true, true>("LDS A+B (moving), barrier", w, out);
   }
   return 0;
 }
