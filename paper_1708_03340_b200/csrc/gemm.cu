@@ -275,16 +275,19 @@ __global__ void __launch_bounds__(THREADS, ((WM * WN == 13 || WM * WN == 14) ? 2
   }
   const int ar = wm * WM * 8 + (lane >> 2);
   const int br = wn * WN * 8 + (lane >> 2);
+  int cst = 0, lst = STAGES - 1;  // compute / load stage (rotating, no divisions)
   for (int t = 0; t < ntiles; ++t) {
     cp_wait<STAGES - 2>();
     __syncthreads();
     {
       const int nt = t + STAGES - 1;
-      if (nt < ntiles) load_tile(nt, nt % STAGES);
+      if (nt < ntiles) load_tile(nt, lst);
       cp_commit();
+      if (++lst == STAGES) lst = 0;
     }
-    const double* as = As + (t % STAGES) * BK * PA;
-    const double* bs = Bs + (t % STAGES) * BK * PB;
+    const double* as = As + cst * BK * PA;
+    const double* bs = Bs + cst * BK * PB;
+    if (++cst == STAGES) cst = 0;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += 4) {
       const int kr = ks + (lane & 3);
