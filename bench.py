@@ -196,7 +196,7 @@ def run_reference(args, rank, world):
     threads = cpu_threads()
     _, _, x = orc.c2_inputs(args.d, args.n, args.k)
     times = []
-    budget_s = 150.0
+    budget_s = 60.0
     warm = min(args.warmup, 1)
     for _ in range(warm):
         cpu_truncation(x, args.k, threads)
@@ -494,8 +494,8 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
-    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=50)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--d", type=int, default=64)
     ap.add_argument("--n", type=int, default=1000)
