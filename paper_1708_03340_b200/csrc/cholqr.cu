@@ -7,6 +7,7 @@
 #include "gemm.cuh"
 #include "prof.cuh"
 #include "ssgemm.cuh"
+#include "misc.cuh"
 
 namespace ht {
 namespace {
@@ -337,6 +338,103 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   }
   HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
   HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
+  return kOk;
+}
+
+// ---------------------------------------------------------------------------
+// wide frames: block Gram-Schmidt (twice) over Cholesky-QR panels
+// ---------------------------------------------------------------------------
+namespace {
+int split_for(long long tiles, long long reduction) {
+  const long long T = std::max<long long>(1, tiles);
+  const long long kt = std::max<long long>(1, (reduction + kGemmBK - 1) / kGemmBK);
+  long long best_s = 1;
+  double best = 1e300;
+  for (long long S = 1; S <= std::min<long long>(160, std::max<long long>(1, kt / 4)); ++S) {
+    const double cost = (double)((T * S + 147) / 148) * ((double)((kt + S - 1) / S) + 3.0) + 0.02 * S;
+    if (cost < best - 1e-9) {
+      best = cost;
+      best_s = S;
+    }
+  }
+  return (int)best_s;
+}
+}  // namespace
+
+bool cholbig_eligible(const QrProblem& q) { return q.K > kCholInPlaceK && q.K <= 1024 && q.m >= q.K; }
+
+long long cholbig_workspace_doubles(CholBig& c) {
+  const int K = c.q.K;
+  c.np = (K + kCholInPlaceK - 1) / kCholInPlaceK;
+  c.pw = (K + c.np - 1) / c.np;
+  const long long n = c.q.nodes;
+  const long long c0max = (long long)(c.np - 1) * c.pw;
+  c.S = split_for((long long)gemm_tiles((int)c0max, c.pw) * n, c.q.m);
+  c.panel = CholQr{};
+  c.panel.q = c.q;
+  c.panel.q.K = c.pw;
+  c.panel.S = split_for((long long)gemm_tiles(c.pw, c.pw) * n, c.q.m);
+  return (long long)c.S * n * c0max * c.pw + n * c0max * c.pw + cholqr_workspace_doubles(c.panel) + 3 * 32;
+}
+
+void cholbig_bind(CholBig& c, double* ws) {
+  const long long n = c.q.nodes;
+  const long long c0max = (long long)(c.np - 1) * c.pw;
+  auto al = [](double* p) { return (double*)(((uintptr_t)p + 255) & ~(uintptr_t)255); };
+  double* p = al(ws);
+  c.P = p;
+  p = al(p + (long long)c.S * n * c0max * c.pw);
+  c.Sb = p;
+  p = al(p + n * c0max * c.pw);
+  cholqr_bind(c.panel, p);
+}
+
+int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t s) {
+  for (auto& c : cs) {
+    const QrProblem& q = c.q;
+    const int m = q.m, K = q.K, n = q.nodes;
+    // Q <- A (the sweep works in place in the output), R <- 0
+    std::vector<Copy2dDesc> cp{Copy2dDesc{q.A, q.Q, q.a_r, q.a_c, q.a_node, q.q_r, q.q_c, q.q_node, m, K, n}};
+    HT_TRY(copy2d_batched(cp, s));
+    for (int nd = 0; nd < n; ++nd)
+      HT_CUDA_CHECK(cudaMemset2DAsync(q.R + nd * q.r_node, sizeof(double) * q.r_ld, 0, sizeof(double) * K, K, s));
+    for (int j = 0; j < c.np; ++j) {
+      const int c0 = j * c.pw, w = std::min(c.pw, K - c0);
+      double* QJ = q.Q + (long long)c0 * q.q_c;
+      double* RJ = q.R + c0;  // rows 0..c0-1 of the column block J
+      for (int pass = 0; j > 0 && pass < 2; ++pass) {
+        // P = Q_<^T Q_J (split-K partials [S][node][c0][w])
+        GemmDesc g = gemm_desc(q.Q, q.q_c, q.q_r, QJ, q.q_r, q.q_c, c.P, w, 1, c0, w, m);
+        g.nb1 = n; g.a_b1 = q.q_node; g.b_b1 = q.q_node; g.c_b1 = (long long)c0 * w;
+        g.splits = c.S;
+        std::vector<GemmDesc> gv{g};
+        HT_TRY(gemm_grouped(gv, s, "gemm_bgs_proj"));
+        // pass 0: R_<J = P;  pass 1: Sb = P, R_<J += P
+        std::vector<ReduceDesc> rd;
+        if (pass == 0) {
+          rd.push_back(ReduceDesc{c.P, RJ, q.r_ld, 1, q.r_node, 0, c.S, c0, w, n, 1, 0, 1.0, 0.0});
+        } else {
+          rd.push_back(ReduceDesc{c.P, c.Sb, w, 1, (long long)c0 * w, 0, c.S, c0, w, n, 1, 0, 1.0, 0.0});
+          rd.push_back(ReduceDesc{c.P, RJ, q.r_ld, 1, q.r_node, 0, c.S, c0, w, n, 1, 0, 1.0, 1.0});
+        }
+        HT_TRY(reduce_partials(rd, s));
+        // Q_J -= Q_< S
+        GemmDesc u = pass == 0 ? gemm_desc(q.Q, q.q_r, q.q_c, RJ, q.r_ld, 1, QJ, q.q_r, q.q_c, m, w, c0, -1.0, 1.0)
+                               : gemm_desc(q.Q, q.q_r, q.q_c, c.Sb, w, 1, QJ, q.q_r, q.q_c, m, w, c0, -1.0, 1.0);
+        u.nb1 = n; u.a_b1 = q.q_node; u.b_b1 = pass == 0 ? q.r_node : (long long)c0 * w; u.c_b1 = q.q_node;
+        std::vector<GemmDesc> uv{u};
+        HT_TRY(gemm_grouped(uv, s, "gemm_bgs_update"));
+      }
+      // [Q_J, R_JJ] = CholQR(Q_J), in place
+      CholQr pc = c.panel;
+      pc.q.A = QJ; pc.q.a_r = q.q_r; pc.q.a_c = q.q_c; pc.q.a_node = q.q_node;
+      pc.q.Q = QJ;
+      pc.q.R = q.R + (long long)c0 * q.r_ld + c0;
+      pc.q.K = w;
+      std::vector<CholQr> pv{pc};
+      HT_TRY(cholqr_run(pv, fail, need2, two_pass, s));
+    }
+  }
   return kOk;
 }
 

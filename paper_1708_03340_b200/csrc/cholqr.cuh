@@ -45,3 +45,24 @@ void cholqr_bind(CholQr& c, double* ws);
 int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cudaStream_t stream);
 
 }  // namespace ht
+
+namespace ht {
+
+// Wide frames (K > kCholInPlaceK, m >= K): block Gram-Schmidt with
+// re-orthogonalisation over panels of <= 104 columns, each panel by Cholesky-QR
+// (adaptive second pass):  Q_J <- Q_J - Q_< (Q_<^T Q_J)  twice,  R_<J += both
+// projections,  [Q_J, R_JJ] = CholQR(Q_J).  Works in place in the output Q.
+struct CholBig {
+  QrProblem q;
+  int np = 0, pw = 0;  // panels, panel width (last panel may be narrower)
+  int S = 1;           // split-K of the projection GEMMs
+  double *P = nullptr, *Sb = nullptr;
+  CholQr panel;        // workspace / plan of one panel (re-bound per panel)
+};
+
+bool cholbig_eligible(const QrProblem& q);
+long long cholbig_workspace_doubles(CholBig& c);  // also fills np, pw, S
+void cholbig_bind(CholBig& c, double* ws);
+int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t stream);
+
+}  // namespace ht

@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "cholqr.cuh"
+#include "qr_wide.cuh"
 #include "common.cuh"
 #include "eig.cuh"
 #include "gemm.cuh"
@@ -405,13 +406,20 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       qs.push_back(q);
     }
     merge_qrs(qs);
-    std::vector<QrProblem> hh;
+    std::vector<QrProblem> hh, wide;
     std::vector<CholQr> cq;
+    std::vector<CholBig> cb;
     for (const auto& q : qs) {
       if (chol && cholqr_eligible(q)) {
         CholQr c;
         c.q = q;
         cq.push_back(c);
+      } else if (q.K > kQrMaxK && qr_wide_eligible(q)) {
+        wide.push_back(q);  // short-wide frame beyond the tall-QR kernels (rank shrink)
+      } else if (q.K > kCholMaxK && cholbig_eligible(q)) {
+        CholBig c;  // wide rank: block Gram-Schmidt over Cholesky-QR panels
+        c.q = q;
+        cb.push_back(c);
       } else {
         hh.push_back(q);
       }
@@ -419,6 +427,13 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     long long ctiles = 0;
     for (const auto& c : cq) ctiles += (long long)gemm_tiles(c.q.K, c.q.K) * c.q.nodes;
     int* cflags = cq.empty() ? nullptr : scratch_ar.take_int((long long)cq.size());
+    int* bflags = cb.empty() ? nullptr : scratch_ar.take_int(1);
+    int* bfail = cb.empty() ? nullptr : scratch_ar.take_int(1);
+    for (auto& c : cb) {
+      double* w = scratch_ar.take(cholbig_workspace_doubles(c));
+      if (scratch_ar.base) cholbig_bind(c, w);
+    }
+    if (n_chol) *n_chol += (int)cb.size();
     for (auto& c : cq) {
       c.S = pick_splits(ctiles, c.q.m);
       double* w = scratch_ar.take(cholqr_workspace_doubles(c));
@@ -437,6 +452,8 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
       HT_TRY(ss_gemm(sa3, s, "ss_absorb"));
       HT_TRY(cholqr_run(cq, fail, cflags, g_qr_mode == 2, s));
+      HT_TRY(cholbig_run(cb, fail ? fail : bfail, bflags, g_qr_mode == 2, s));
+      HT_TRY(qr_wide_batched(wide, s));
       HT_TRY(qr_batched(hh, s));
     }
   }
@@ -639,6 +656,7 @@ struct TruncPlan {
   int* status = nullptr;
   int* qr_fail = nullptr;
   int* eigflag = nullptr;  // per node: redo with Jacobi (set by the tridiagonal fast path)
+  std::vector<double*> eigwork;  // per node: eigensolver scratch when K > kEigMaxK
   Arena scratch;
 };
 
@@ -694,6 +712,9 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   P.status = P.ranks + T.nn;
   P.qr_fail = P.ranks + T.nn + 1;
   P.eigflag = ar.take_int(T.nn);
+  P.eigwork.assign(T.nn, nullptr);
+  for (int t = 1; t < T.nn; ++t)
+    if (P.o.k[t] > kEigMaxK) P.eigwork[t] = ar.take(eig_work_doubles((int)P.o.k[t]));
   P.scratch = ar;  // everything after this point is phase scratch
   return kOk;
 }
@@ -760,6 +781,7 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     e.S = P.G[t]; e.V = P.EV[t]; e.lam = P.lam[t];
     e.rank = P.ranks + t; e.status = P.status;
     e.fallback = P.eigflag + t;
+    e.work = P.eigwork[t];
     e.K = (int)P.o.k[t]; e.nodes = 1;
     e.eps = ctl->eps > 0 ? ctl->eps : 0.0;
     e.n_nonroot = T.nn - 1;
@@ -767,14 +789,17 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     e.s_node = 0; e.v_node = 0; e.l_node = 0;
     if (!eps.empty()) {
       EigProblem& b = eps.back();
-      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback) {
+      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback &&
+          (b.work == nullptr) == (e.work == nullptr)) {
         if (b.nodes == 1) {
           b.s_node = e.S - b.S; b.v_node = e.V - b.V; b.l_node = e.lam - b.lam;
+          b.w_node = b.work ? e.work - b.work : 0;
           b.nodes = 2;
           continue;
         }
         const long long c = b.nodes;
-        if (b.S + c * b.s_node == e.S && b.V + c * b.v_node == e.V && b.lam + c * b.l_node == e.lam) {
+        if (b.S + c * b.s_node == e.S && b.V + c * b.v_node == e.V && b.lam + c * b.l_node == e.lam &&
+            (b.work == nullptr || b.work + c * b.w_node == e.work)) {
           b.nodes++;
           continue;
         }

@@ -225,10 +225,23 @@ int g_eig_mode = 0;
 
 int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
   bool tri = g_eig_mode == 0;
-  for (const auto& p : probs) tri = tri && p.fallback != nullptr && p.K <= kEigMaxK;
+  bool big = false;
+  for (const auto& p : probs) {
+    tri = tri && p.fallback != nullptr && (p.K <= kEigMaxK || p.work);
+    big = big || p.K > kEigMaxK;
+  }
+  if (big && !tri) {
+    set_error("eigensolver: K > 112 needs the tridiagonal path (eig mode auto and a workspace)");
+    return kErrUnsupported;
+  }
   if (tri) HT_TRY(eig_tri_batched(probs, stream));
   else
     for (auto& p : probs) p.fallback = nullptr;
+  // the Jacobi kernel only serves nodes the tridiagonal path flagged (never K > 112)
+  std::vector<EigProblem> jp;
+  for (const auto& p : probs)
+    if (p.K <= kEigMaxK) jp.push_back(p);
+  probs.swap(jp);
   if (!g_attr) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     g_attr = true;

@@ -31,9 +31,13 @@ struct EigProblem {
   int cap;          // rank cap; <= 0: none
   int* fallback;    // per-node flags (node stride 1): set by the tridiagonal fast path for
                     // nodes the Jacobi kernel must redo; null = Jacobi for every node
+  double* work;     // global scratch for K > kEigMaxK (2 K (K+2) doubles per node), or null
+  long long w_node;
 };
 
-constexpr int kEigMaxK = 112;
+constexpr int kEigMaxK = 112;      // shared-memory paths (Jacobi; tridiagonal in smem)
+constexpr int kEigMaxKBig = 512;   // tridiagonal path with the matrices in global scratch
+inline long long eig_work_doubles(int K) { return K > kEigMaxK ? 2LL * K * (K + 2) : 0; }
 constexpr int kEigStatusNotSymmetric = 1;
 constexpr int kEigStatusNonConverged = 2;
 

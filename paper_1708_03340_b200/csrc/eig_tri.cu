@@ -34,6 +34,7 @@ constexpr double kClusterTol = 1e-5;
 
 struct TriBatch {
   int count;
+  int kmax;  // largest K of the batch (sizes the shared-memory vectors)
   int begin[MAXD + 1];
   EigProblem d[MAXD];
 };
@@ -80,17 +81,21 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   const EigProblem& e = b.d[di];
   const int nd = blockIdx.x - b.begin[di];
   const int K = e.K;
+  const int KM = b.kmax;
   const int ap = K | 1;            // odd pitch
   const int zp = (K + 1) | 1;
-  double* A = sm;                  // K x ap
-  double* Z = A + K * ap;          // r x zp: eigenvectors of T, one row per kept eigenpair
-  double* dd = Z + K * zp;         // [K] diagonal of T
-  double* ee = dd + K;             // [K] off-diagonal
-  double* e2 = ee + K;             // [K] squares
-  double* tau = e2 + K;            // [K]
-  double* vb = tau + K;            // [2][kEigMaxK] reflectors (double-buffered)
-  double* pb = vb + 2 * kEigMaxK;  // [K] p
-  double* lam = pb + K;            // [K] ascending eigenvalues
+  double* dd = sm;                 // [KM] diagonal of T
+  double* ee = dd + KM;            // [KM] off-diagonal
+  double* e2 = ee + KM;            // [KM] squares
+  double* tau = e2 + KM;           // [KM]
+  double* vb = tau + KM;           // [2][KM] reflectors (double-buffered)
+  double* pb = vb + 2 * KM;        // [KM] p
+  double* lam = pb + KM;           // [KM] ascending eigenvalues
+  // the matrix and the eigenvectors of T: shared memory up to kEigMaxK, else the
+  // node's global scratch (L2-resident)
+  const bool big = K > kEigMaxK;
+  double* A = big ? e.work + nd * e.w_node : lam + KM;  // K x ap
+  double* Z = A + (size_t)K * ap;                        // r x zp, one row per kept pair
   __shared__ double red[TT / 32][2];
   __shared__ double sh[4];
   __shared__ int flags[2];
@@ -155,21 +160,26 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   __syncthreads();
   for (int j = 0; j + 2 < K; ++j) {
     const int m = K - j - 1;       // reflector length (rows j+1 .. K-1)
-    const double* v = vbuf + (j & 1) * kEigMaxK;
-    double* vn = vbuf + ((j + 1) & 1) * kEigMaxK;
+    const double* v = vbuf + (j & 1) * KM;
+    double* vn = vbuf + ((j + 1) & 1) * KM;
     const double tj = tau[j];
     if (tj != 0.0) {
       // p = tau * A22 v (4 threads per row) and the per-warp partial of p.v
       {
-        const int i = tid / kGroup, part = tid % kGroup;
-        double acc = 0.0;
-        if (i < m) {
-          const double* row = A + (j + 1 + i) * ap + (j + 1);
-          for (int k = part; k < m; k += kGroup) acc = fma(row[k], v[k], acc);
+        double pv = 0.0;
+        for (int i0 = 0; i0 < m; i0 += TT / kGroup) {
+          const int i = i0 + tid / kGroup, part = tid % kGroup;
+          double acc = 0.0;
+          if (i < m) {
+            const double* row = A + (size_t)(j + 1 + i) * ap + (j + 1);
+            for (int k = part; k < m; k += kGroup) acc = fma(row[k], v[k], acc);
+          }
+          acc = quad_sum(acc) * tj;
+          if (i < m && part == 0) {
+            pv += acc * v[i];
+            pb[i] = acc;
+          }
         }
-        acc = quad_sum(acc) * tj;
-        double pv = (i < m && part == 0) ? acc * v[i] : 0.0;
-        if (i < m && part == 0) pb[i] = acc;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
         if (lane == 0) red[warp][0] = pv;
@@ -252,8 +262,8 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   __syncthreads();
 
   // ---- 2. eigenvalues: multisection bisection, 4 threads per eigenvalue ---------
-  {
-    const int i = tid / kGroup, part = tid % kGroup;
+  for (int i0 = 0; i0 < K; i0 += TT / kGroup) {
+    const int i = i0 + tid / kGroup, part = tid % kGroup;
     const double pivmin = sh[2];
     const double atol = 4.0 * 2.220446049250313e-16 * sh[3] + pivmin;  // absolute accuracy of the reduction
     double lo = sh[0], hi = sh[1];
@@ -318,6 +328,10 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     for (int k = max(0, K - r - 1); k + 1 < K; ++k)
       if (lam[k + 1] - lam[k] < kDegenTol * tn) fb = 1;
     if (!(tn > 0.0) || !isfinite(tn)) fb = 1;  // zero / non-finite matrix: Jacobi
+    if (big) {  // no shared-memory Jacobi beyond kEigMaxK: keep the tridiagonal result
+      if (fb && e.status && !(tn >= 0.0)) atomicOr(e.status, kEigStatusNonConverged);
+      fb = 0;
+    }
     flags[1] = fb;
     if (e.fallback) e.fallback[nd] = fb;
   }
@@ -416,9 +430,10 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   // ---- 4. back-transformation y = H_0 ... H_{K-3} z, G = 8 (r <= 64) or 4 threads per vector
   {
     const int G = r <= TT / 8 ? 8 : kGroup;
-    const int v = tid / G, part = tid % G;
+    for (int v0 = 0; v0 < r; v0 += TT / G) {
+    const int v = v0 + tid / G, part = tid % G;
     const bool act = v < r;
-    double* z = Z + (act ? v : 0) * zp;
+    double* z = Z + (size_t)(act ? v : 0) * zp;
     for (int j = K - 3; j >= 0; --j) {
       const double tj = tau[j];
       if (tj == 0.0) continue;
@@ -432,7 +447,8 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       if (G == 8) s += __shfl_xor_sync(0xffffffffu, s, 4);
       s *= tj;
       if (act)
-        for (int k = part; k < m; k += G) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k]);
+        for (int k = part; k < m; k += G) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(size_t)(j + 1 + k) * ap + j], z[j + 1 + k]);
+    }
     }
   }
   __syncthreads();
@@ -443,9 +459,9 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
 }
 
-size_t tri_smem(int K) {
+size_t tri_smem(int K) {  // vectors for K, plus the matrices when they live in shared memory
   const int ap = K | 1, zp = (K + 1) | 1;
-  return sizeof(double) * ((size_t)K * ap + (size_t)K * zp + 6 * (size_t)K + 2 * (size_t)kEigMaxK) + 64;
+  return sizeof(double) * (8 * (size_t)K + (K <= kEigMaxK ? (size_t)K * ap + (size_t)K * zp : 0)) + 64;
 }
 
 bool g_tri_attr = false;
@@ -455,23 +471,34 @@ bool g_tri_attr = false;
 int eig_tri_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
   if (!g_tri_attr) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(tri_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)tri_smem(kEigMaxK)));
+                                       (int)std::max(tri_smem(kEigMaxK), tri_smem(kEigMaxKBig))));
     g_tri_attr = true;
   }
   size_t i = 0;
   while (i < probs.size()) {
     TriBatch b;
     b.count = 0;
+    b.kmax = 1;
     int blocks = 0;
     size_t smem = 0;
     while (i < probs.size() && b.count < MAXD) {
       const EigProblem& p = probs[i++];
       if (p.nodes == 0) continue;
+      if (p.K > kEigMaxKBig || (p.K > kEigMaxK && !p.work)) {
+        set_error("eigensolver: K=" + std::to_string(p.K) + " needs K <= 512 and a global scratch");
+        return kErrUnsupported;
+      }
       b.begin[b.count] = blocks;
       blocks += p.nodes;
-      smem = std::max(smem, tri_smem(p.K));
+      b.kmax = std::max(b.kmax, p.K);
       b.d[b.count++] = p;
     }
+    // vectors sized for kmax; matrices in shared memory only if every node fits
+    for (int q = 0; q < b.count; ++q)
+      smem = std::max(smem, sizeof(double) * 8 * (size_t)b.kmax + 64 +
+                                (b.d[q].K <= kEigMaxK ? sizeof(double) * ((size_t)b.d[q].K * (b.d[q].K | 1) +
+                                                                           (size_t)b.d[q].K * ((b.d[q].K + 1) | 1))
+                                                      : 0));
     if (b.count == 0) continue;
     b.begin[b.count] = blocks;
     double flops = 0;

@@ -185,6 +185,37 @@ int leaf_apply_batched(const std::vector<LeafApplyDesc>& descs, cudaStream_t str
   return kOk;
 }
 
+__global__ void copy2d_kernel(Copy2dDesc d) {
+  const long long total = (long long)d.nodes * d.rows * d.cols;
+  for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < total; e += (long long)gridDim.x * blockDim.x) {
+    // column-fastest for row-major destinations, row-fastest otherwise (coalesced writes)
+    long long nd, r, c;
+    if (d.d_c == 1) {
+      c = e % d.cols;
+      r = (e / d.cols) % d.rows;
+      nd = e / ((long long)d.cols * d.rows);
+    } else {
+      r = e % d.rows;
+      c = (e / d.rows) % d.cols;
+      nd = e / ((long long)d.cols * d.rows);
+    }
+    d.dst[nd * d.d_node + r * d.d_r + c * d.d_c] = d.src[nd * d.s_node + r * d.s_r + c * d.s_c];
+  }
+}
+
+int copy2d_batched(const std::vector<Copy2dDesc>& descs, cudaStream_t stream) {
+  for (const auto& d : descs) {
+    const long long total = (long long)d.nodes * d.rows * d.cols;
+    if (total <= 0) continue;
+    const int blocks = (int)std::min<long long>((total + 255) / 256, 148 * 16);
+    ProfToken tok = prof_begin(stream);
+    copy2d_kernel<<<blocks, 256, 0, stream>>>(d);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "copy2d", stream, 0.0, 16.0 * total);
+  }
+  return kOk;
+}
+
 int scale_copy(const double* x, double* y, long long n, double alpha, cudaStream_t stream) {
   if (n <= 0) return kOk;
   ProfToken tok = prof_begin(stream);

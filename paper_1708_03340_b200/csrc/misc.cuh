@@ -47,6 +47,15 @@ struct LeafApplyDesc {
 int leaf_apply_batched(const std::vector<LeafApplyDesc>& descs, cudaStream_t stream);
 
 int scale_copy(const double* x, double* y, long long n, double alpha, cudaStream_t stream);
+
+// dst(r, c) = src(r, c) for rows x cols per node, arbitrary strides (layout changes)
+struct Copy2dDesc {
+  const double* src;
+  double* dst;
+  long long s_r, s_c, s_node, d_r, d_c, d_node;
+  int rows, cols, nodes;
+};
+int copy2d_batched(const std::vector<Copy2dDesc>& descs, cudaStream_t stream);
 // out[0] = sum_i a[i] * b[i]   (single CTA, deterministic order)
 int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream);
 

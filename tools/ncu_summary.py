@@ -49,14 +49,23 @@ if len(sys.argv) > 3:
         raw.append(d)
     raw = [r for r in raw if "ht::" in r.get("Kernel Name", "") or "unnamed>::" in r.get("Kernel Name", "")]
 step_us = sum(num(k["gpu__time_duration.sum"]) / 1e3 for k in launches)
+# align the full-capture rows to the launch list by kernel name, in order
+raw_for = [None] * len(launches)
+if raw is not None:
+    j = 0
+    for i, k in enumerate(launches):
+        base = k["name"].split("(")[0]
+        if j < len(raw) and raw[j].get("Kernel Name", "").split("(")[0] == base:
+            raw_for[i] = raw[j]
+            j += 1
 per = {}
 for i, (k, (tag, flops, nbytes)) in enumerate(zip(launches, tags)):
     e = per.setdefault(tag, {"launches": 0, "ncu_us": 0.0, "flops": 0.0, "kernel": k["name"].split("(")[0]})
     e["launches"] += 1
     e["ncu_us"] += num(k["gpu__time_duration.sum"]) / 1e3
     e["flops"] += flops
-    if raw is not None and i < len(raw):
-        r = raw[i]
+    if raw_for[i] is not None:
+        r = raw_for[i]
         e.setdefault("dram_bytes", 0.0)
         e["dram_bytes"] += num(r.get("dram__bytes_read.sum", 0)) + num(r.get("dram__bytes_write.sum", 0))
         e.setdefault("dmma_pct", []).append(num(r.get("sm__pipe_tensor_subpipe_dmma_cycles_active.avg.pct_of_peak_sustained_active", "nan")))
