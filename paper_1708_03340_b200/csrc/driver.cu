@@ -433,6 +433,13 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       double* w = scratch_ar.take(cholbig_workspace_doubles(c));
       if (scratch_ar.base) cholbig_bind(c, w);
     }
+    for (auto& q : wide) {
+      const long long wn = qr_wide_ws_doubles(q);
+      if (wn > 0) {
+        q.wide_ws_node = (wn + 31) / 32 * 32;
+        q.wide_ws = scratch_ar.take(q.wide_ws_node * q.nodes);
+      }
+    }
     if (n_chol) *n_chol += (int)cb.size();
     for (auto& c : cq) {
       c.S = pick_splits(ctiles, c.q.m);

@@ -47,6 +47,9 @@ struct QrProblem {
   double* Tst;  // 2P x K x K: T factors of blocks [0,P) and of combine steps [P + b]
   double* X;    // 3P x K x K: GEMM scratch of the Q formation
   bool own_v;
+  // wide-frame QR (qr_wide.cu) with the block in global memory: scratch per node
+  double* wide_ws = nullptr;
+  long long wide_ws_node = 0;
 };
 
 constexpr int kQrMaxK = 112;  // register/shared-memory resident path

@@ -1,9 +1,10 @@
 // QR of short-wide frames (m < K, the rank-shrink case of reference
 // arith.py:280-297 / kernels.py:24-32: Q is m x m, R is m x K, diag(R) >= 0).
-// One CTA per node holds the whole m x K block in shared memory (m <= 64,
-// m*K <= 24k doubles), so K is not limited to the tall-QR kernels' 112.
-// Unblocked Householder: reflector j by one warp (m - j <= 64 rows), then every
-// thread updates whole columns; Q accumulated backwards from I_m.
+// One CTA per node holds the whole m x K block -- in shared memory when it fits
+// (<= 200 KB), else in a global scratch (L2-resident) -- so neither K nor m (<= 1024)
+// is limited to the tall-QR kernels' 112.  Unblocked Householder: reflector j by one
+// warp, then every thread updates whole columns; Q accumulated backwards from I_m.
+// A rare path (rank shrink at wide ranks): latency, not throughput, matters.
 #include <cmath>
 
 #include "prof.cuh"
@@ -28,7 +29,8 @@ __global__ void __launch_bounds__(WT) qr_wide_kernel(const __grid_constant__ Wid
   const QrProblem& q = b.d[di];
   const int nd = blockIdx.x - b.begin[di];
   const int m = q.m, K = q.K, ap = K + 1;
-  double* A = sm;                 // m x ap (row-major)
+  // the block lives in shared memory when it fits, else in the node's global scratch
+  double* A = q.wide_ws ? q.wide_ws + nd * q.wide_ws_node : sm;  // m x ap (row-major)
   double* V = A + (size_t)m * ap;  // m x m: reflector j in column j (rows j..m-1), 1 on the diagonal
   double* tau = V + m * m;        // m
   double* Qs = tau + m;           // m x m
@@ -98,13 +100,16 @@ __global__ void __launch_bounds__(WT) qr_wide_kernel(const __grid_constant__ Wid
 }
 
 size_t wide_smem(int m, int K) { return sizeof(double) * ((size_t)m * (K + 1) + 2 * (size_t)m * m + m); }
+constexpr size_t kWideSmem = 200 * 1024;
 
 bool g_attr = false;
 
 }  // namespace
 
-bool qr_wide_eligible(const QrProblem& q) {
-  return q.m >= 1 && q.m < q.K && q.m <= 64 && wide_smem(q.m, q.K) <= 200 * 1024;
+bool qr_wide_eligible(const QrProblem& q) { return q.m >= 1 && q.m < q.K && q.m <= 1024; }
+
+long long qr_wide_ws_doubles(const QrProblem& q) {
+  return wide_smem(q.m, q.K) <= kWideSmem ? 0 : (long long)(wide_smem(q.m, q.K) / sizeof(double)) + 32;
 }
 
 int qr_wide_batched(std::vector<QrProblem>& probs, cudaStream_t stream) {
@@ -120,13 +125,13 @@ int qr_wide_batched(std::vector<QrProblem>& probs, cudaStream_t stream) {
     size_t smem = 0;
     while (i < probs.size() && b.count < MAXD) {
       const QrProblem& p = probs[i++];
-      if (!qr_wide_eligible(p)) {
-        set_error("qr_wide: frame outside the shared-memory wide QR (m < K, m <= 64)");
+      if (!qr_wide_eligible(p) || (wide_smem(p.m, p.K) > kWideSmem && !p.wide_ws)) {
+        set_error("qr_wide: frame outside the wide QR (m < K, m <= 1024, scratch for large blocks)");
         return kErrUnsupported;
       }
       b.begin[b.count] = blocks;
       blocks += p.nodes;
-      smem = std::max(smem, wide_smem(p.m, p.K));
+      if (!p.wide_ws) smem = std::max(smem, wide_smem(p.m, p.K));
       b.d[b.count++] = p;
     }
     if (!b.count) continue;
