@@ -535,35 +535,39 @@ def ones_htensor(tr: Tree, n: int) -> HT:
     return HT(tr, U, B, np.ones((1, 1)))
 
 
-def cg_solve(op: HTOp, rhs: HT, ctl: Ctl, eps_stop: float, max_steps: int):
+def cg_solve(op: HTOp, rhs: HT, ctl, eps_stop: float, max_steps: int):
     """solvers.py:183-231 (_cg_loop with trace): X0 = rhs, truncation after every
     add / apply, stop on sqrt(<R,R>) <= eps_stop or max_steps, abort on <D,AD> <= 0.
+    ``ctl`` is a Ctl or a callable y -> Ctl (per-call control, e.g. relative eps).
     Returns (X, internal residuals, true relative residuals)."""
+    def trunc(y):
+        return truncate(y, ctl(y) if callable(ctl) else ctl)
+
     b = rhs
     b_neg = scale(b, -1.0)
     norm_b = norm(b)
 
     def true_res(x):  # solvers.py:163-170
-        ax = truncate(apply_operator(op, x), ctl)
+        ax = trunc(apply_operator(op, x))
         return norm(add(ax, b_neg)) / norm_b
 
     x = b
-    r = truncate(add(b, scale(apply_operator(op, x), -1.0)), ctl)
+    r = trunc(add(b, scale(apply_operator(op, x), -1.0)))
     d = r
     rr = inner_product(r, r)
     internal, true = [math.sqrt(max(0.0, rr))], [true_res(x)]
     j = 0
     while math.sqrt(max(0.0, rr)) > eps_stop and j < max_steps:
-        z = truncate(apply_operator(op, d), ctl)
+        z = trunc(apply_operator(op, d))
         dz = inner_product(d, z)
         if dz <= 0.0:
             break
         alpha = rr / dz
-        x = truncate(add(x, scale(d, alpha)), ctl)
-        r_new = truncate(add(r, scale(z, -alpha)), ctl)
+        x = trunc(add(x, scale(d, alpha)))
+        r_new = trunc(add(r, scale(z, -alpha)))
         rr_new = inner_product(r_new, r_new)
         beta = rr_new / rr
-        d = truncate(add(scale(d, beta), r_new), ctl)
+        d = trunc(add(scale(d, beta), r_new))
         r, rr = r_new, rr_new
         j += 1
         internal.append(math.sqrt(max(0.0, rr)))

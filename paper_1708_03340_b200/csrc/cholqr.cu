@@ -374,7 +374,13 @@ long long cholbig_workspace_doubles(CholBig& c) {
   c.panel.q = c.q;
   c.panel.q.K = c.pw;
   c.panel.S = split_for((long long)gemm_tiles(c.pw, c.pw) * n, c.q.m);
-  return (long long)c.S * n * c0max * c.pw + n * c0max * c.pw + cholqr_workspace_doubles(c.panel) + 3 * 32;
+  c.hpanel = c.q;
+  c.hpanel.K = c.pw;
+  c.hpanel.V = nullptr;
+  c.hpanel.wide_ws = nullptr;
+  qr_plan(c.hpanel);
+  return (long long)c.S * n * c0max * c.pw + n * c0max * c.pw + n * (long long)c.pw * c.pw +
+         std::max(cholqr_workspace_doubles(c.panel), qr_workspace_doubles(c.hpanel)) + 4 * 32;
 }
 
 void cholbig_bind(CholBig& c, double* ws) {
@@ -386,10 +392,13 @@ void cholbig_bind(CholBig& c, double* ws) {
   p = al(p + (long long)c.S * n * c0max * c.pw);
   c.Sb = p;
   p = al(p + n * c0max * c.pw);
-  cholqr_bind(c.panel, p);
+  c.Rp = p;
+  p = al(p + n * (long long)c.pw * c.pw);
+  cholqr_bind(c.panel, p);  // the two panel plans share one workspace (used one at a time)
+  c.hws = p;
 }
 
-int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t s) {
+int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t s, bool householder) {
   for (auto& c : cs) {
     const QrProblem& q = c.q;
     const int m = q.m, K = q.K, n = q.nodes;
@@ -425,14 +434,56 @@ int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, 
         std::vector<GemmDesc> uv{u};
         HT_TRY(gemm_grouped(uv, s, "gemm_bgs_update"));
       }
-      // [Q_J, R_JJ] = CholQR(Q_J), in place
-      CholQr pc = c.panel;
-      pc.q.A = QJ; pc.q.a_r = q.q_r; pc.q.a_c = q.q_c; pc.q.a_node = q.q_node;
-      pc.q.Q = QJ;
-      pc.q.R = q.R + (long long)c0 * q.r_ld + c0;
-      pc.q.K = w;
-      std::vector<CholQr> pv{pc};
-      HT_TRY(cholqr_run(pv, fail, need2, two_pass, s));
+      if (!householder) {
+        // [Q_J, R_JJ] = CholQR(Q_J), in place
+        CholQr pc = c.panel;
+        pc.q.A = QJ; pc.q.a_r = q.q_r; pc.q.a_c = q.q_c; pc.q.a_node = q.q_node;
+        pc.q.Q = QJ;
+        pc.q.R = q.R + (long long)c0 * q.r_ld + c0;
+        pc.q.K = w;
+        std::vector<CholQr> pv{pc};
+        HT_TRY(cholqr_run(pv, fail, need2, two_pass, s));
+        continue;
+      }
+      // [Q_J, R_JJ] = TSQR(Q_J) in place (Householder: rank-deficient panels stay orthonormal)
+      QrProblem hp = c.hpanel;
+      hp.A = QJ; hp.a_r = q.q_r; hp.a_c = q.q_c; hp.a_node = q.q_node;
+      hp.Q = QJ; hp.q_r = q.q_r; hp.q_c = q.q_c; hp.q_node = q.q_node;
+      hp.R = q.R + (long long)c0 * q.r_ld + c0; hp.r_ld = q.r_ld; hp.r_node = q.r_node;
+      hp.K = w;
+      hp.V = nullptr;
+      HT_TRY(qr_plan(hp));
+      qr_bind_workspace(hp, c.hws);  // w <= pw: fits the workspace planned for pw
+      std::vector<QrProblem> hv{hp};
+      HT_TRY(qr_batched(hv, s));
+      if (j == 0) continue;
+      // completion directions of a deficient panel: project once more and re-factor,
+      // R_<J += S R_JJ and R_JJ <- R' R_JJ
+      GemmDesc g = gemm_desc(q.Q, q.q_c, q.q_r, QJ, q.q_r, q.q_c, c.P, w, 1, c0, w, m);
+      g.nb1 = n; g.a_b1 = q.q_node; g.b_b1 = q.q_node; g.c_b1 = (long long)c0 * w;
+      g.splits = c.S;
+      std::vector<GemmDesc> gv{g};
+      HT_TRY(gemm_grouped(gv, s, "gemm_bgs_proj"));
+      std::vector<ReduceDesc> rd{ReduceDesc{c.P, c.Sb, w, 1, (long long)c0 * w, 0, c.S, c0, w, n, 1, 0, 1.0, 0.0}};
+      HT_TRY(reduce_partials(rd, s));
+      GemmDesc u = gemm_desc(q.Q, q.q_r, q.q_c, c.Sb, w, 1, QJ, q.q_r, q.q_c, m, w, c0, -1.0, 1.0);
+      u.nb1 = n; u.a_b1 = q.q_node; u.b_b1 = (long long)c0 * w; u.c_b1 = q.q_node;
+      // R_<J += S R_JJ  (R_JJ upper triangular, row-major at (c0, c0))
+      const double* RJJ = q.R + (long long)c0 * q.r_ld + c0;
+      GemmDesc ra = gemm_desc(c.Sb, w, 1, RJJ, q.r_ld, 1, RJ, q.r_ld, 1, c0, w, w, 1.0, 1.0);
+      ra.nb1 = n; ra.a_b1 = (long long)c0 * w; ra.b_b1 = q.r_node; ra.c_b1 = q.r_node;
+      std::vector<GemmDesc> uv{u, ra};
+      HT_TRY(gemm_grouped(uv, s, "gemm_bgs_update"));
+      // R' from the re-factorisation into scratch, then R_JJ <- R' R_JJ
+      hp.R = c.Rp; hp.r_ld = w; hp.r_node = (long long)w * w;
+      std::vector<QrProblem> hv2{hp};
+      HT_TRY(qr_batched(hv2, s));
+      std::vector<Copy2dDesc> cr{Copy2dDesc{RJJ, c.Sb, q.r_ld, 1, q.r_node, w, 1, (long long)w * w, w, w, n}};
+      HT_TRY(copy2d_batched(cr, s));
+      GemmDesc rr = gemm_desc(c.Rp, w, 1, c.Sb, w, 1, q.R + (long long)c0 * q.r_ld + c0, q.r_ld, 1, w, w, w);
+      rr.nb1 = n; rr.a_b1 = (long long)w * w; rr.b_b1 = (long long)w * w; rr.c_b1 = q.r_node;
+      std::vector<GemmDesc> rv{rr};
+      HT_TRY(gemm_grouped(rv, s, "gemm_bgs_update"));
     }
   }
   return kOk;

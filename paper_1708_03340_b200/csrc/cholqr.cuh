@@ -56,13 +56,19 @@ struct CholBig {
   QrProblem q;
   int np = 0, pw = 0;  // panels, panel width (last panel may be narrower)
   int S = 1;           // split-K of the projection GEMMs
-  double *P = nullptr, *Sb = nullptr;
-  CholQr panel;        // workspace / plan of one panel (re-bound per panel)
+  double *P = nullptr, *Sb = nullptr, *Rp = nullptr;
+  CholQr panel;        // workspace / plan of one Cholesky-QR panel (re-bound per panel)
+  QrProblem hpanel;    // plan of one Householder-TSQR panel (re-planned per panel width)
+  double* hws = nullptr;  // its workspace
 };
 
 bool cholbig_eligible(const QrProblem& q);
 long long cholbig_workspace_doubles(CholBig& c);  // also fills np, pw, S
 void cholbig_bind(CholBig& c, double* ws);
-int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t stream);
+// householder: panels by Householder tree-TSQR (exactly rank-deficient panels keep an
+// orthonormal Q), each followed by one more projection + TSQR so that the completion
+// directions of deficient panels are orthogonal to the earlier panels too.
+int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, cudaStream_t stream,
+                bool householder = false);
 
 }  // namespace ht

@@ -41,7 +41,8 @@ const char* last_error();
   do {                                                                          \
     cudaError_t _e = cudaGetLastError();                                        \
     if (_e != cudaSuccess) {                                                    \
-      ::ht::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+      ::ht::set_error(std::string("kernel launch (") + __FILE__ + ":" +         \
+                      std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \
       return ::ht::kErrCuda;                                                    \
     }                                                                           \
   } while (0)

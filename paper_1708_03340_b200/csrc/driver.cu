@@ -416,7 +416,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
         cq.push_back(c);
       } else if (q.K > kQrMaxK && qr_wide_eligible(q)) {
         wide.push_back(q);  // short-wide frame beyond the tall-QR kernels (rank shrink)
-      } else if (q.K > kCholMaxK && cholbig_eligible(q)) {
+      } else if (q.K > kQrMaxK && cholbig_eligible(q)) {
         CholBig c;  // wide rank: block Gram-Schmidt over Cholesky-QR panels
         c.q = q;
         cb.push_back(c);
@@ -459,7 +459,9 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
       HT_TRY(ss_gemm(sa3, s, "ss_absorb"));
       HT_TRY(cholqr_run(cq, fail, cflags, g_qr_mode == 2, s));
-      HT_TRY(cholbig_run(cb, fail ? fail : bfail, bflags, g_qr_mode == 2, s));
+      // Cholesky-QR panels on the fast sweep; Householder-TSQR panels on the fallback
+      // sweep and under the Householder policy (rank-deficient wide frames)
+      HT_TRY(cholbig_run(cb, fail ? fail : bfail, bflags, g_qr_mode == 2, s, !chol));
       HT_TRY(qr_wide_batched(wide, s));
       HT_TRY(qr_batched(hh, s));
     }

@@ -49,7 +49,8 @@ __device__ __forceinline__ double quad_sum(double v) {
 // leading minors p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2} (T normalised to
 // ||T|| ~ 1).  Three FP64 ops per step; the sign test runs on the integer pipe and
 // the exact power-of-two rescale is checked every 8 steps (|p| changes by at most
-// 2^16 up / 2^-424 down in 8 steps).  A zero minor counts as positive.
+// 2^16 up / 2^-424 down in 8 steps: inside a block |e_k| > eps ||T||, and splits
+// restart the recurrence).  A zero minor counts as positive.
 __device__ __forceinline__ int sturm_count(const double* d, const double* e2, int K, double x) {
   double pm2 = 1.0, pm1 = d[0] - x;
   int c = __double_as_longlong(pm1) < 0;
@@ -57,9 +58,13 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
   while (k < K) {
     const int kend = min(K, k + 8);
     for (; k < kend; ++k) {
-      const double p = fma(d[k] - x, pm1, -e2[k - 1] * pm2);
-      c += (__double_as_longlong(p) ^ __double_as_longlong(pm1)) < 0;
-      pm2 = pm1;
+      // a split (e_{k-1} = 0) restarts the recurrence for the next block with
+      // p_{k-1} = 1: the count adds up over blocks and |p| cannot decay across it
+      const double e2k = e2[k - 1];
+      const double q = e2k == 0.0 ? 1.0 : pm1;
+      const double p = fma(d[k] - x, q, -e2k * pm2);
+      c += (__double_as_longlong(p) ^ __double_as_longlong(q)) < 0;
+      pm2 = q;
       pm1 = p;
     }
     const double a = fmax(fabs(pm1), fabs(pm2));
@@ -260,6 +265,16 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     }
   }
   __syncthreads();
+  // split T at negligible off-diagonals (|e_k| <= eps ||T||, a perturbation inside the
+  // absolute accuracy of the reduction): graded Gramians leave long runs of tiny
+  // e_k whose products would underflow the Sturm recurrence, and the twisted
+  // vectors of eigenvalues shared by several blocks stay confined to their block
+  for (int k = tid; k + 1 < K; k += TT)
+    if (fabs(ee[k]) <= 2.220446049250313e-16 * sh[3]) {
+      ee[k] = 0.0;
+      e2[k] = 0.0;
+    }
+  __syncthreads();
 
   // ---- 2. eigenvalues: multisection bisection, 4 threads per eigenvalue ---------
   for (int i0 = 0; i0 < K; i0 += TT / kGroup) {
@@ -396,31 +411,91 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     for (int k = 0; k < K; ++k) z[k] *= inv;
   }
   __syncthreads();
-  // re-orthogonalise close kept pairs (MGS within runs of gap < kClusterTol ||T||), warp 0
+  // Close kept pairs (runs of gap < kClusterTol ||T||), warp 0.  Exactly or nearly
+  // degenerate eigenvalues (symmetric problems: T numerically split into blocks
+  // sharing an eigenvalue) give (near-)identical twisted vectors, so vector a of a
+  // run is refined by two steps of inverse iteration with T - lam_a I, each followed
+  // by two Gram-Schmidt passes against the run's earlier vectors; a vector that
+  // vanishes under the projection restarts from a pseudo-random one (the solve then
+  // pulls it into the cluster's invariant subspace).  Singletons only get a
+  // finiteness check.
   if (warp == 0) {
     const double tn = sh[3];
-    int v0 = 0;
-    while (v0 < r) {
-      int v1 = v0 + 1;
-      while (v1 < r && lam[K - 1 - (v1 - 1)] - lam[K - 1 - v1] < kClusterTol * tn) ++v1;
-      for (int a = v0 + 1; a < v1; ++a) {
-        double* za = Z + a * zp;
+    const double piv = 2.220446049250313e-16 * tn + sh[2];
+    double* Dl = vb;  // LDL^T pivots of T - sig I (the reflector buffers are free now)
+    auto wsum = [&](double s) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      return s;
+    };
+    auto nrm2 = [&](const double* z) {
+      double s = 0.0;
+      for (int k = lane; k < K; k += 32) s = fma(z[k], z[k], s);
+      return wsum(s);
+    };
+    auto project_out = [&](double* za, int v0, int a) {
+      for (int pass = 0; pass < 2; ++pass)
         for (int bq = v0; bq < a; ++bq) {
           const double* zb = Z + bq * zp;
           double s = 0.0;
           for (int k = lane; k < K; k += 32) s = fma(za[k], zb[k], s);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+          s = wsum(s);
           for (int k = lane; k < K; k += 32) za[k] = fma(-s, zb[k], za[k]);
           __syncwarp();
         }
-        double s = 0.0;
-        for (int k = lane; k < K; k += 32) s = fma(za[k], za[k], s);
+    };
+    int v0 = 0;
+    while (v0 < r) {
+      int v1 = v0 + 1;
+      while (v1 < r && lam[K - 1 - (v1 - 1)] - lam[K - 1 - v1] < kClusterTol * tn) ++v1;
+      for (int a = v0; a < v1; ++a) {
+        double* za = Z + a * zp;
+        const double s0 = nrm2(za);
+        if (v1 == v0 + 1 && isfinite(s0) && s0 > 0.0) break;  // singleton, twisted vector fine
+        const double sig = lam[K - 1 - a];
+        for (int it = 0; it < 3; ++it) {
+          // scale to max |z| = 1 first (inverse iteration grows the vector by 1/gap)
+          double mx = 0.0;
+          for (int k = lane; k < K; k += 32) mx = fmax(mx, fabs(za[k]));
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        const double inv = 1.0 / sqrt(s);
-        for (int k = lane; k < K; k += 32) za[k] *= inv;
-        __syncwarp();
+          for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          const bool bad = !(mx > 0.0) || !isfinite(mx);
+          for (int k = lane; k < K; k += 32) za[k] = bad ? 0.0 : za[k] / mx;
+          __syncwarp();
+          const double sb = bad ? 0.0 : nrm2(za);
+          project_out(za, v0, a);
+          double s = nrm2(za);
+          if (!(s > 1e-16 * sb)) {  // nothing left outside the earlier vectors: restart
+            for (int k = lane; k < K; k += 32) {
+              unsigned h = (unsigned)k * 2654435761u ^ (unsigned)(a * 40503 + it * 7919 + 12345);
+              h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+              za[k] = (double)(h & 0xffffu) / 65536.0 - 0.5;
+            }
+            __syncwarp();
+            project_out(za, v0, a);
+            s = nrm2(za);
+          }
+          const double inv = s > 0.0 ? 1.0 / sqrt(s) : 0.0;
+          for (int k = lane; k < K; k += 32) za[k] *= inv;
+          __syncwarp();
+          if (it == 2) break;
+          // za <- (T - sig I)^{-1} za by LDL^T (pivots guarded at eps ||T||), lane 0
+          if (lane == 0) {
+            double dk = dd[0] - sig;
+            if (fabs(dk) < piv) dk = dk < 0.0 ? -piv : piv;
+            Dl[0] = dk;
+            for (int k = 1; k < K; ++k) {
+              const double l = ee[k - 1] / Dl[k - 1];
+              dk = (dd[k] - sig) - l * ee[k - 1];
+              if (fabs(dk) < piv) dk = dk < 0.0 ? -piv : piv;
+              Dl[k] = dk;
+              za[k] = fma(-l, za[k - 1], za[k]);
+            }
+            za[K - 1] /= Dl[K - 1];
+            for (int k = K - 2; k >= 0; --k) za[k] = (za[k] - ee[k] * za[k + 1]) / Dl[k];
+          }
+          __syncwarp();
+        }
       }
       v0 = v1;
     }
@@ -459,46 +534,50 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
 }
 
-size_t tri_smem(int K) {  // vectors for K, plus the matrices when they live in shared memory
-  const int ap = K | 1, zp = (K + 1) | 1;
-  return sizeof(double) * (8 * (size_t)K + (K <= kEigMaxK ? (size_t)K * ap + (size_t)K * zp : 0)) + 64;
-}
-
 bool g_tri_attr = false;
 
 }  // namespace
 
 int eig_tri_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
+  constexpr size_t kSmemMax = 226 * 1024;  // + the kernel's static shared memory
   if (!g_tri_attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(tri_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)std::max(tri_smem(kEigMaxK), tri_smem(kEigMaxKBig))));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(tri_eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kSmemMax));
     g_tri_attr = true;
   }
+  // vectors are sized for the batch's largest K; matrices sit in shared memory only
+  // for K <= kEigMaxK -- a problem that would push the batch past the limit starts
+  // the next batch
+  auto mat_bytes = [](int K) {
+    return K <= kEigMaxK ? sizeof(double) * ((size_t)K * (K | 1) + (size_t)K * ((K + 1) | 1)) : 0;
+  };
   size_t i = 0;
   while (i < probs.size()) {
     TriBatch b;
     b.count = 0;
     b.kmax = 1;
     int blocks = 0;
-    size_t smem = 0;
+    size_t mats = 0;
     while (i < probs.size() && b.count < MAXD) {
-      const EigProblem& p = probs[i++];
-      if (p.nodes == 0) continue;
+      const EigProblem& p = probs[i];
+      if (p.nodes == 0) {
+        ++i;
+        continue;
+      }
       if (p.K > kEigMaxKBig || (p.K > kEigMaxK && !p.work)) {
         set_error("eigensolver: K=" + std::to_string(p.K) + " needs K <= 512 and a global scratch");
         return kErrUnsupported;
       }
+      const int kmax = std::max(b.kmax, p.K);
+      const size_t m = std::max(mats, mat_bytes(p.K));
+      if (b.count > 0 && sizeof(double) * 8 * (size_t)kmax + 64 + m > kSmemMax) break;
+      ++i;
       b.begin[b.count] = blocks;
       blocks += p.nodes;
-      b.kmax = std::max(b.kmax, p.K);
+      b.kmax = kmax;
+      mats = m;
       b.d[b.count++] = p;
     }
-    // vectors sized for kmax; matrices in shared memory only if every node fits
-    for (int q = 0; q < b.count; ++q)
-      smem = std::max(smem, sizeof(double) * 8 * (size_t)b.kmax + 64 +
-                                (b.d[q].K <= kEigMaxK ? sizeof(double) * ((size_t)b.d[q].K * (b.d[q].K | 1) +
-                                                                           (size_t)b.d[q].K * ((b.d[q].K + 1) | 1))
-                                                      : 0));
+    const size_t smem = sizeof(double) * 8 * (size_t)b.kmax + 64 + mats;
     if (b.count == 0) continue;
     b.begin[b.count] = blocks;
     double flops = 0;

@@ -17,10 +17,20 @@ from .backend import GpuBackend
 
 
 @dataclass
+class RelativeTruncation:
+    """Truncation to a RELATIVE accuracy: every truncate call uses
+    eps = rel * ||Y|| for its own input Y (the reference takes an
+    absolute eps, solvers.py:196), optionally capped."""
+
+    rel: float
+    max_rank: int | None = None
+
+
+@dataclass
 class SolverConfig:
     """solvers.py:110-135 (the fields the CG loop uses)."""
 
-    truncation: TruncationControl
+    truncation: object  # TruncationControl or RelativeTruncation
     eps_stop: float = 1e-8
     max_cg_steps: int = 25
 
@@ -100,4 +110,4 @@ def _cg_loop(a, b, cfg: SolverConfig, backend, trace):
     return x
 
 
-__all__ = ["SolverConfig", "ConvergenceTrace", "TraceEntry", "cg_solve"]
+__all__ = ["SolverConfig", "RelativeTruncation", "ConvergenceTrace", "TraceEntry", "cg_solve"]

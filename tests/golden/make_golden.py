@@ -233,6 +233,64 @@ def golden_cg():
     np.savez_compressed(os.path.join(OUT, "cg.npz"), **out)
 
 
+def golden_c4_operator():
+    """The reference's affine operator builder (cookie.build_ht_operator, compressed)
+    on small P1 subdomain matrices: pins problems.affine_operator."""
+    from htucker import cookie
+
+    from paper_1708_03340_b200 import problems
+
+    mats, load = problems.p1_diffusion_matrices(cells=6)
+    import scipy.sparse as sp
+
+    zero = sp.csr_matrix(mats[0].shape)
+    grids = [np.linspace(0.1, 1.0, 4) for _ in range(9)]
+    op = cookie.build_ht_operator([zero] + mats, grids)
+    out = {"meta": meta(), "load": load}
+    for t, a in op.transfer.items():
+        out[f"B/{t}"] = np.asarray(a)
+    out["root"] = np.asarray(op.root_matrix)
+    for t, cols in op.leaves.items():
+        for j, g in enumerate(cols):
+            out[f"W/{t}/{j}/kind"] = np.array(g.kind)
+            out[f"W/{t}/{j}/dense"] = np.asarray(g.to_dense() if hasattr(g, "to_dense") else g.data.toarray())
+    for j, m in enumerate(mats):
+        out[f"K/{j}"] = m.toarray()
+    np.savez_compressed(os.path.join(OUT, "c4_operator.npz"), **out)
+
+
+def golden_c4_cg():
+    """BASELINE C4 at full size through the REFERENCE: cookie.build_ht_operator on the
+    64 x 64 P1 subdomain matrices, build_rhs_htensor, and solvers.cg_solve for 20
+    steps on a SerialBackend whose truncate uses eps = 1e-6 * ||Y|| (cap 50) -- the
+    relative-tolerance wrapper C4 asks for (the reference takes an absolute eps).
+    Takes a few minutes; writes c4_cg.npz (the residual traces and max ranks)."""
+    import scipy.sparse as sp
+    from htucker import arith as ref_ar
+    from htucker import cookie
+    from htucker import solvers as ref_solvers
+
+    from paper_1708_03340_b200 import problems
+
+    class RelBackend(ref_solvers.SerialBackend):
+        def truncate(self, x, ctl):
+            return ref_ar.truncate(x, ref.TruncationControl(eps=1e-6 * ref_ar.norm(x), max_rank=50))
+
+    mats, load = problems.p1_diffusion_matrices(cells=64)
+    grids = problems.parameter_grids(points=16)
+    op = cookie.build_ht_operator([sp.csr_matrix(mats[0].shape)] + mats, grids)
+    rhs = cookie.build_rhs_htensor(load, grids)
+    cfg = ref_solvers.SolverConfig(truncation=ref.TruncationControl(eps=1.0, max_rank=50), eps_stop=1e-12,
+                                   max_cg_steps=20)
+    x, trace = ref_solvers.cg_solve(op, rhs, cfg, backend=RelBackend())
+    out = {"meta": meta(),
+           "internal": np.array([e.internal_residual for e in trace.entries]),
+           "true_rel": np.array([e.true_rel_residual for e in trace.entries]),
+           "max_rank": np.array([e.max_rank for e in trace.entries]),
+           "ranks_X": np.array([x.rank(t) for t in range(1, 19)])}
+    np.savez_compressed(os.path.join(OUT, "c4_cg.npz"), **out)
+
+
 def golden_spec():
     """Known answers quoted in the SPEC."""
     q, r = ref_kernels.reduced_qr(np.array([[3.0], [4.0]]))
@@ -254,4 +312,7 @@ if __name__ == "__main__":
     golden_c3_small()
     golden_c2_d8()
     golden_cg()
+    golden_c4_operator()
+    if "--c4" in sys.argv:  # minutes of CPU time
+        golden_c4_cg()
     print("golden fixtures written to", OUT)

@@ -213,3 +213,24 @@ def test_c2_d64_headline_shape(htb):
     t_ref = orc.truncate(x, orc.Ctl(max_rank=50))
     assert rel_err(to_host(T), t_ref) <= ERR_TOL
     np.testing.assert_allclose(htb.inner_product(T, T), orc.inner_product(t_ref, t_ref), rtol=1e-10)
+
+
+def test_c3_full_size(htb):
+    """BASELINE config C3 at its full size: d=16, n=256, X rank 30 (Gaussian), the
+    Laplace-sum operator (ranks 2) -> Y rank 60, truncated with eps = 1e-8 ||Y|| and
+    cap 30 ("whichever comes first")."""
+    tr = orc.balanced_tree(16)
+    x = orc.gaussian_htensor(tr, 256, 30, 16)
+    op = orc.laplace_operator(tr, 256)
+    ttr = htb.build_balanced_tree(16)
+    dop = htb.HTOperator(ttr, {t: [htb.GeneralizedMatrix.diagonal(w[0].data), htb.GeneralizedMatrix.csr(w[1].data)]
+                                for t, w in op.W.items()}, dict(op.H), op.root)
+    y = htb.apply_operator(dop, to_dev(x))
+    assert y.max_rank == 60
+    yr = orc.apply_operator(op, x)
+    ny = htb.norm(y)
+    np.testing.assert_allclose(ny, orc.norm(yr), rtol=1e-12)
+    T = htb.truncate(y, htb.TruncationControl(eps=1e-8 * ny, max_rank=30))
+    ref = orc.truncate(yr, orc.Ctl(eps=1e-8 * orc.norm(yr), max_rank=30))
+    assert to_host(T).ranks == ref.ranks
+    assert rel_err(to_host(T), ref) <= 1e-10
