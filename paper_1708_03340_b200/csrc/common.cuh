@@ -60,7 +60,7 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(c[0]), "+d"(c[1])
                : "d"(a), "d"(b));
 }
@@ -69,7 +69,7 @@ __device__ __forceinline__ void dmma_8x8x4(double (&c)[2], double a, double b) {
 // g = lane/4, t = lane%4:  a[i] = A[g + 8*(i&1)][t + 4*(i>>1)],  b[i] = B[t + 4i][g],
 // c = {C[g][2t], C[g][2t+1], C[g+8][2t], C[g+8][2t+1]}.
 __device__ __forceinline__ void dmma_16x8x16(double (&c)[4], const double (&a)[8], const double (&b)[4]) {
-  asm volatile(
+  asm(
       "mma.sync.aligned.m16n8k16.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7,%8,%9,%10,%11}, "
       "{%12,%13,%14,%15}, {%0,%1,%2,%3};\n"
       : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
@@ -87,12 +87,12 @@ __device__ __forceinline__ void dmma_16x8x16_if(bool p, double (&c)[4], const do
         "d"(b[1]), "d"(b[2]), "d"(b[3]), "r"((int)p));
 }
 __device__ __forceinline__ void dmma_16x8x8(double (&c)[4], const double* a, const double* b) {
-  asm volatile("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+  asm("mma.sync.aligned.m16n8k8.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 __device__ __forceinline__ void dmma_16x8x4(double (&c)[4], const double* a, const double* b) {
-  asm volatile("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
+  asm("mma.sync.aligned.m16n8k4.row.col.f64.f64.f64.f64 {%0,%1,%2,%3}, {%4,%5}, {%6}, {%0,%1,%2,%3};\n"
                : "+d"(c[0]), "+d"(c[1]), "+d"(c[2]), "+d"(c[3])
                : "d"(a[0]), "d"(a[1]), "d"(b[0]));
 }

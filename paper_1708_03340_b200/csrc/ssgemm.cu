@@ -127,6 +127,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     // loader cursor (step ld_s = (tile ld_mt, chunk ld_kc) into stage ld_st), advanced
     // incrementally: no divisions in the steady state
     int ld_s = 0, ld_mt = mt0, ld_kc = 0, ld_st = 0;
+    long long ld_koff = 0;  // LAYOUT 0: ld_kc * SBK * x_k
+    long long qoff[4];      // LAYOUT 0: k offset of each of the thread's four k rows
+#pragma unroll
+    for (int q = 0; q < 4; ++q) qoff[q] = (long long)((tid >> 6) + 4 * q) * g.x_k;
     auto issue = [&]() {
       if (ld_s < nsteps && !(SS_DEBUG_NO_XLOAD && ld_s >= SSTAGES)) {
         if (ld_mt != ld_tile) set_rows(ld_mt);
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
             const int kk = (tid >> 6) + 4 * q;
             const int nv = kb + kk < K ? rowv[0] : 0;
             double* dst = xs + kk * PX + r;
-            const long long ko = (long long)(kb + kk) * g.x_k;
+            const long long ko = ld_koff + qoff[q];
             if (vec) {
               cp16z(dst, nv ? rowp[0] + ko : X, 8 * nv);
             } else {
@@ -166,8 +170,10 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
       }
       cp_commit();
       ++ld_s;
+      ld_koff += (long long)SBK * g.x_k;
       if (++ld_kc == KT) {
         ld_kc = 0;
+        ld_koff = 0;
         ++ld_mt;
       }
       if (++ld_st == SSTAGES) ld_st = 0;
@@ -176,8 +182,6 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     for (int s = 0; s < SSTAGES - 1; ++s) issue();  // S travels with the first group
 
     double acc[NF][4];  // m16n8 accumulators: rows g, g+8 of the warp's 16, cols 2t, 2t+1
-#pragma unroll
-    for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
     const int g8 = lane >> 2, t4 = lane & 3;
     const int ar = warp * 16 + g8;
     const double alpha = g.alpha, beta = g.beta;
@@ -190,29 +194,31 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
     auto xa = [&](const double* xs, int rs, int k) -> double {
       return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
     };
-    int st = 0, kc = 0, mt = mt0;  // compute cursor
-    for (int s = 0; s < nsteps; ++s) {
-      cp_wait<SSTAGES - 2>();
-      __syncthreads();
-      issue();
-      const double* xs = Xs + st * XSTAGE;
-      const double* ss = Ss + kc * SBK * PS;
-      const int krem = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
+    // tiles outer, k-chunks inner: the accumulators live in fixed registers through the
+    // chunk loop (no epilogue branch inside it) while the loader cursor runs ahead
+    // across tile boundaries
+    int st = 0;
+    for (int mt = mt0; mt < mt0 + seg; ++mt) {
 #pragma unroll
-      for (int k16 = 0; k16 < SBK; k16 += 16) {
-        const int kv = krem - k16;
-        if (kv <= 0) break;
-        const double* sk = ss + k16 * PS;
+      for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+      for (int kc = 0; kc < KT; ++kc) {
+        cp_wait<SSTAGES - 2>();
+        __syncthreads();
+        issue();
+        const double* xs = Xs + st * XSTAGE;
+        const double* ss = Ss + kc * SBK * PS;
+        if (++st == SSTAGES) st = 0;
+        const int kv = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
+        const int kg = kc * SBK;      // global k of the chunk
         if (kv >= 12) {  // m16n8k16 (k rows beyond K are zero in shared memory)
           double a[8];
 #pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, k16 + t4 + 4 * (i >> 1));
-          const int kg = kc * SBK + k16;  // global k of this block
+          for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
 #pragma unroll
           for (int j = 0; j < NF; ++j) {
             double bq[4];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) bq[i] = sk[(t4 + 4 * i) * PS + j * 8 + g8];
+            for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
             if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
           }
         } else {  // tail: k8 and/or k4 steps
@@ -220,73 +226,64 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
           if (kv > 4) {
             double a[4], bq[2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, k16 + t4 + 4 * (i >> 1));
+            for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
-              bq[0] = sk[t4 * PS + j * 8 + g8];
-              bq[1] = sk[(t4 + 4) * PS + j * 8 + g8];
+              bq[0] = ss[t4 * PS + j * 8 + g8];
+              bq[1] = ss[(t4 + 4) * PS + j * 8 + g8];
               dmma_16x8x8(acc[j], a, bq);
             }
             k0 = 8;
           }
           if (kv > k0) {
             double a[2], bq[1];
-            a[0] = xa(xs, 0, k16 + k0 + t4);
-            a[1] = xa(xs, 1, k16 + k0 + t4);
+            a[0] = xa(xs, 0, k0 + t4);
+            a[1] = xa(xs, 1, k0 + t4);
 #pragma unroll
             for (int j = 0; j < NF; ++j) {
-              bq[0] = sk[(k0 + t4) * PS + j * 8 + g8];
+              bq[0] = ss[(k0 + t4) * PS + j * 8 + g8];
               dmma_16x8x4(acc[j], a, bq);
             }
           }
         }
       }
-      if (SS_DEBUG_NO_EPILOGUE && kc == KT - 1 && alpha == 12345.0) {  // keep the MMAs alive
-        for (int j = 0; j < NF; ++j) C[j] = acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+      if (SS_DEBUG_NO_EPILOGUE) {
+        if (alpha == 12345.0)  // keep the MMAs alive
+          for (int j = 0; j < NF; ++j) C[j] = acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+        continue;
       }
-      if (kc == KT - 1 && !SS_DEBUG_NO_EPILOGUE) {  // tile done: epilogue, then restart the accumulators
 #pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          const int m = mt * SBM + ar + 8 * f;
-          if (m < M) {
-            const int hi = m / M_lo, lo = m - hi * M_lo;
-            double* crow = C + hi * g.c_hi + lo * g.c_lo;
-            const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
+      for (int f = 0; f < 2; ++f) {
+        const int m = mt * SBM + ar + 8 * f;
+        if (m < M) {
+          const int hi = m / M_lo, lo = m - hi * M_lo;
+          double* crow = C + hi * g.c_hi + lo * g.c_lo;
+          const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
 #pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              const int n = j * 8 + 2 * t4;
-              const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
-              if (pair && n + 1 < N) {
-                double2 r = make_double2(alpha * v0, alpha * v1);
-                double2* p = reinterpret_cast<double2*>(crow + n);
-                if (beta != 0.0) {
-                  const double2 o = *p;
-                  r.x += beta * o.x;
-                  r.y += beta * o.y;
-                }
-                *p = r;
-              } else {
-                if (n < N) {
-                  double* p = crow + (long long)n * g.c_n;
-                  *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
-                }
-                if (n + 1 < N) {
-                  double* p = crow + (long long)(n + 1) * g.c_n;
-                  *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
-                }
+          for (int j = 0; j < NF; ++j) {
+            const int n = j * 8 + 2 * t4;
+            const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
+            if (pair && n + 1 < N) {
+              double2 r = make_double2(alpha * v0, alpha * v1);
+              double2* p = reinterpret_cast<double2*>(crow + n);
+              if (beta != 0.0) {
+                const double2 o = *p;
+                r.x += beta * o.x;
+                r.y += beta * o.y;
+              }
+              *p = r;
+            } else {
+              if (n < N) {
+                double* p = crow + (long long)n * g.c_n;
+                *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
+              }
+              if (n + 1 < N) {
+                double* p = crow + (long long)(n + 1) * g.c_n;
+                *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
               }
             }
           }
         }
-#pragma unroll
-        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-      }
-      if (SS_DEBUG_NO_EPILOGUE && kc == KT - 1)
-        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-      if (++st == SSTAGES) st = 0;
-      if (++kc == KT) {
-        kc = 0;
-        ++mt;
       }
     }
     cp_wait<0>();
