@@ -7,6 +7,7 @@
 // in shared memory (pitch = 4 mod 16 doubles: conflict-free fragment loads)
 // through a 3-stage cp.async pipeline with zero-fill for the ragged edges.
 #include <algorithm>
+#include <cstdlib>
 
 #include "gemm.cuh"
 #include "prof.cuh"
@@ -386,6 +387,232 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
   }
 }
 
+
+// ---- long-reduction kernel ---------------------------------------------------
+// C (M x N <= 112 x 112) = sum over a long (split-K) reduction f = (o, k) of
+// A(f, m) B(f, n): the reduced-Gramian contractions and the Cholesky-QR Gram
+// matrices.  14 warps (7 x 2) each own a 16 x 56 block of one 112 x 112 tile as
+// seven m16n8k16 fragments (A fragment reused seven times: 36 LDS per 56 DMMA);
+// ~100 registers, so 14 warps per SM hide the operand latency the 8-warp generic
+// tile could not.  Both operands are staged through a 4-stage pipeline of 16-byte
+// cp.async pairs: LM = 1 -> pairs along m/n (a_m == b_n == 1, staged [k][m]),
+// LM = 0 -> pairs along k (a_k == b_k == 1, staged [m][k]).
+constexpr int LR_THREADS = 448;
+constexpr int LR_T = 112;        // tile edge
+constexpr int LR_BK = 16;
+constexpr int LR_STAGES = 4;
+constexpr int LR_PM = LR_T + 4;  // [k][m] pitch (4 mod 16 doubles: conflict-free fragments)
+constexpr int LR_PK = LR_BK + 4; // [m][k] pitch
+constexpr int LR_OPD = (LR_BK * LR_PM > LR_T * LR_PK) ? LR_BK * LR_PM : LR_T * LR_PK;  // doubles per operand-stage
+
+__device__ __forceinline__ void cp16z(double* smem, const double* gmem, int valid_bytes) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid_bytes));
+}
+
+template <int LM>
+__global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant__ GemmBatch batch) {
+  extern __shared__ __align__(16) double smem[];
+  int di = 0;
+  while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
+  const GemmDesc& g = batch.d[di];
+  if (g.active && *g.active == 0) return;
+  int local = blockIdx.x - g.block_begin;
+  const int split = local % g.splits;
+  const int b = local / g.splits;
+  const int b1 = b % g.nb1, b2 = b / g.nb1;
+  const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
+  const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2;
+  const int M = g.M, N = g.N, K = g.K;
+  const long long L = (long long)K * g.KO;
+  const long long per_split = ((L + g.splits - 1) / g.splits + LR_BK - 1) / LR_BK * LR_BK;
+  const long long f_begin = split * per_split;
+  const long long f_end = min(L, f_begin + per_split);
+  const int nst = f_end > f_begin ? (int)((f_end - f_begin + LR_BK - 1) / LR_BK) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  // loader slots: two 16-byte pairs per operand per stage
+  //   LM = 1: pair p = tid + 448 q -> k row p / 56 (= tid / 56 + 8 q), m pair 2 (p % 56)
+  //   LM = 0: pair p = tid + 448 q -> row p / 8 (= tid / 8 + 56 q), k pair 2 (tid % 8)
+  const double* arow[2];
+  const double* brow[2];
+  int avb[2], bvb[2];  // valid bytes of the pair (rows beyond M / N read nothing)
+  int kk[2];           // reduction offset of each slot within a stage
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    if (LM) {
+      const int m = 2 * (tid % 56);
+      kk[q] = tid / 56 + 8 * q;
+      avb[q] = 8 * max(0, min(2, M - m));
+      bvb[q] = 8 * max(0, min(2, N - m));
+      arow[q] = A + (long long)min(m, M - 1) * g.a_m;
+      brow[q] = B + (long long)min(m, N - 1) * g.b_n;
+    } else {
+      const int r = tid / 8 + 56 * q;
+      kk[q] = 2 * (tid % 8);
+      avb[q] = r < M ? 16 : 0;
+      bvb[q] = r < N ? 16 : 0;
+      arow[q] = A + (long long)min(r, M - 1) * g.a_m;
+      brow[q] = B + (long long)min(r, N - 1) * g.b_n;
+    }
+  }
+  const long long a_wrap = g.a_o - (long long)K * g.a_k, b_wrap = g.b_o - (long long)K * g.b_k;
+  // loader cursor: stage start f = (o, k), advanced by LR_BK (K >= 16 or KO == 1)
+  long long ld_o = f_begin / K;
+  int ld_k = (int)(f_begin - ld_o * K);
+  int ld_s = 0, ld_st = 0;
+  auto issue = [&]() {
+    if (ld_s < nst) {
+      double* as = smem + ld_st * 2 * LR_OPD;
+      double* bs = as + LR_OPD;
+      const long long f0 = f_begin + (long long)ld_s * LR_BK;
+      const long long abase = ld_o * g.a_o + (long long)ld_k * g.a_k;
+      const long long bbase = ld_o * g.b_o + (long long)ld_k * g.b_k;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const bool fin = f0 + kk[q] < f_end;
+        const bool wrap = ld_k + kk[q] >= K;  // slot crosses into the next outer index
+        const long long ao = abase + (long long)kk[q] * g.a_k + (wrap ? a_wrap : 0);
+        const long long bo = bbase + (long long)kk[q] * g.b_k + (wrap ? b_wrap : 0);
+        const int av = fin ? avb[q] : 0, bv = fin ? bvb[q] : 0;
+        double* ad = LM ? as + kk[q] * LR_PM + 2 * (tid % 56) : as + (tid / 8 + 56 * q) * LR_PK + kk[q];
+        double* bd = LM ? bs + kk[q] * LR_PM + 2 * (tid % 56) : bs + (tid / 8 + 56 * q) * LR_PK + kk[q];
+        cp16z(ad, av ? arow[q] + ao : A, av);
+        cp16z(bd, bv ? brow[q] + bo : B, bv);
+      }
+    }
+    cp_commit();
+    ++ld_s;
+    ld_k += LR_BK;
+    while (ld_k >= K) {
+      ld_k -= K;
+      ++ld_o;
+    }
+    if (++ld_st == LR_STAGES) ld_st = 0;
+  };
+#pragma unroll
+  for (int st = 0; st < LR_STAGES - 1; ++st) issue();
+
+  const int wm = warp >> 1, wn = warp & 1;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int ar = wm * 16 + g8, bc = wn * 56 + g8;
+  double acc[7][4];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  int st = 0;
+  for (int s = 0; s < nst; ++s) {
+    cp_wait<LR_STAGES - 2>();
+    __syncthreads();
+    issue();
+    const double* as = smem + st * 2 * LR_OPD;
+    const double* bs = as + LR_OPD;
+    if (++st == LR_STAGES) st = 0;
+    double a[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = ar + 8 * (i & 1), k = t4 + 4 * (i >> 1);
+      a[i] = LM ? as[k * LR_PM + m] : as[m * LR_PK + k];
+    }
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+      double bq[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int n = bc + 8 * j, k = t4 + 4 * i;
+        bq[i] = LM ? bs[k * LR_PM + n] : bs[n * LR_PK + k];
+      }
+      dmma_16x8x16(acc[j], a, bq);
+    }
+  }
+  cp_wait<0>();
+
+  const long long nbatch = (long long)g.nb1 * g.nb2;
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int m = ar + 8 * f;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 7; ++j) {
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int n = wn * 56 + 8 * j + 2 * t4 + v;
+        if (n >= N) continue;
+        const double r = acc[j][2 * f + v];
+        if (g.splits == 1) {
+          double* p = g.C + b1 * g.c_b1 + b2 * g.c_b2 + (long long)m * g.c_m + (long long)n * g.c_n;
+          *p = g.beta != 0.0 ? g.alpha * r + g.beta * *p : g.alpha * r;
+        } else {
+          g.C[((long long)split * nbatch + b) * M * N + (long long)m * N + n] = r;
+        }
+      }
+    }
+  }
+}
+
+// descriptors the long-reduction kernel takes: plain operands, M, N <= 112 (not both
+// <= 56), reduction >= 256, and 16-byte pairs: layout 1 (a_m == b_n == 1) or 0
+// (a_k == b_k == 1, even K); -1 otherwise
+int lr_layout(const GemmDesc& d) {
+  if (d.a_tri || d.b_tri || d.M > LR_T || d.N > LR_T || (d.M <= 56 && d.N <= 56)) return -1;
+  const int KO = std::max(d.KO, 1);
+  if ((long long)d.K * KO < 256 || (KO > 1 && d.K < LR_BK)) return -1;
+  auto even = [](long long v) { return (v & 1) == 0; };
+  const bool al = (((uintptr_t)d.A | (uintptr_t)d.B) & 15) == 0 && even(d.a_b1) && even(d.a_b2) && even(d.b_b1) &&
+                  even(d.b_b2) && even(d.a_o) && even(d.b_o);
+  if (!al) return -1;
+  if (d.a_m == 1 && d.b_n == 1 && even(d.a_k) && even(d.b_k) && even(d.M) && even(d.N)) return 1;
+  if (d.a_k == 1 && d.b_k == 1 && even(d.K) && even(d.a_m) && even(d.b_n)) return 0;
+  return -1;
+}
+
+size_t lr_smem() { return sizeof(double) * (size_t)LR_STAGES * 2 * LR_OPD; }
+
+int lr_grouped(std::vector<GemmDesc>& descs, int layout, cudaStream_t stream, const char* tag, bool count_flops) {
+  static bool attr[2] = {false, false};
+  size_t i = 0;
+  while (i < descs.size()) {
+    GemmBatch batch;
+    batch.count = 0;
+    int blocks = 0;
+    double flops = 0, bytes = 0;
+    while (i < descs.size() && batch.count < kMaxGemmDescs) {
+      GemmDesc d = descs[i++];
+      if (d.splits < 1) d.splits = 1;
+      if (d.KO < 1) d.KO = 1;
+      d.tiles_m = d.tiles_n = 1;
+      d.block_begin = blocks;
+      blocks += d.splits * d.nb1 * d.nb2;
+      const double nbt = (double)d.nb1 * d.nb2;
+      flops += 2.0 * d.M * d.N * (double)d.K * d.KO * nbt;
+      bytes += 8.0 * nbt * ((double)d.M * d.K * d.KO + (double)d.K * d.KO * d.N + (double)d.M * d.N * d.splits);
+      batch.d[batch.count++] = d;
+    }
+    if (batch.count == 0) continue;
+    ProfToken tok = prof_begin(stream);
+    if (layout == 1) {
+      if (!attr[1]) {
+        HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
+        attr[1] = true;
+      }
+      lr_kernel<1><<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
+    } else {
+      if (!attr[0]) {
+        HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
+        attr[0] = true;
+      }
+      lr_kernel<0><<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
+    }
+    HT_LAUNCH_CHECK();
+    prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
+  }
+  return kOk;
+}
+// HT_GEMM_LR=0 routes everything through the generic tiles (A/B comparisons)
+const int g_lr_enabled = [] {
+  const char* e = std::getenv("HT_GEMM_LR");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
 // ---- tile configurations ----
 int g_half_tiles = 1;
 enum Cfg { kC64, kCN104, kCM104, kCN56, kCM56, kCN104h, kCM104h, kNumCfg };
@@ -456,7 +683,16 @@ int gemm_tiles(int M, int N) {  // tiles of a long-reduction (split-K planned) G
   return ceil_div(M, kCfg[c].bm) * ceil_div(N, kCfg[c].bn);
 }
 
-int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
+int gemm_grouped(std::vector<GemmDesc>& descs_in, cudaStream_t stream, const char* tag, bool count_flops) {
+  std::vector<GemmDesc> lr[2], descs;
+  for (const auto& d : descs_in) {
+    if (d.M <= 0 || d.N <= 0 || d.nb1 <= 0 || d.nb2 <= 0) continue;
+    const int l = g_lr_enabled ? lr_layout(d) : -1;
+    if (l >= 0) lr[l].push_back(d);
+    else descs.push_back(d);
+  }
+  for (int l = 0; l < 2; ++l)
+    if (!lr[l].empty()) HT_TRY(lr_grouped(lr[l], l, stream, tag, count_flops));
   for (int c = 0; c < kNumCfg; ++c) {
     size_t i = 0;
     while (i < descs.size()) {
