@@ -393,17 +393,26 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
 // A(f, m) B(f, n): the reduced-Gramian contractions and the Cholesky-QR Gram
 // matrices.  14 warps (7 x 2) each own a 16 x 56 block of one 112 x 112 tile as
 // seven m16n8k16 fragments (A fragment reused seven times: 36 LDS per 56 DMMA);
-// ~100 registers, so 14 warps per SM hide the operand latency the 8-warp generic
-// tile could not.  Both operands are staged through a 4-stage pipeline of 16-byte
-// cp.async pairs: LM = 1 -> pairs along m/n (a_m == b_n == 1, staged [k][m]),
-// LM = 0 -> pairs along k (a_k == b_k == 1, staged [m][k]).
+// ~130 registers, so 14 warps per SM hide the operand latency the 8-warp generic
+// tile could not.  Both operands are staged through a 3-stage pipeline of 32-deep
+// k-chunks (one barrier per 112 DMMA per warp) in 16-byte cp.async pairs, per
+// descriptor either along m/n (lm = 1: a_m == b_n == 1, staged [k][m]) or along k
+// (lm = 0: a_k == b_k == 1, staged [m][k]); both layouts share one launch so a level's
+// two son Gramians fill the machine together.
 constexpr int LR_THREADS = 448;
 constexpr int LR_T = 112;        // tile edge
-constexpr int LR_BK = 16;
-constexpr int LR_STAGES = 4;
+constexpr int LR_BK = 32;
+constexpr int LR_STAGES = 3;
 constexpr int LR_PM = LR_T + 4;  // [k][m] pitch (4 mod 16 doubles: conflict-free fragments)
 constexpr int LR_PK = LR_BK + 4; // [m][k] pitch
 constexpr int LR_OPD = (LR_BK * LR_PM > LR_T * LR_PK) ? LR_BK * LR_PM : LR_T * LR_PK;  // doubles per operand-stage
+constexpr int LR_Q = LR_T * LR_BK / 2 / LR_THREADS;  // 16-byte pairs per thread per operand-stage (4)
+
+struct LrBatch {
+  int count;
+  unsigned char lm[kMaxGemmDescs];
+  GemmDesc d[kMaxGemmDescs];
+};
 
 __device__ __forceinline__ void cp16z(double* smem, const double* gmem, int valid_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -411,13 +420,7 @@ __device__ __forceinline__ void cp16z(double* smem, const double* gmem, int vali
 }
 
 template <int LM>
-__global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant__ GemmBatch batch) {
-  extern __shared__ __align__(16) double smem[];
-  int di = 0;
-  while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
-  const GemmDesc& g = batch.d[di];
-  if (g.active && *g.active == 0) return;
-  int local = blockIdx.x - g.block_begin;
+__device__ __forceinline__ void lr_body(const GemmDesc& g, int local, double* smem) {
   const int split = local % g.splits;
   const int b = local / g.splits;
   const int b1 = b % g.nb1, b2 = b / g.nb1;
@@ -431,33 +434,31 @@ __global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant
   const int nst = f_end > f_begin ? (int)((f_end - f_begin + LR_BK - 1) / LR_BK) : 0;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // loader slots: two 16-byte pairs per operand per stage
-  //   LM = 1: pair p = tid + 448 q -> k row p / 56 (= tid / 56 + 8 q), m pair 2 (p % 56)
-  //   LM = 0: pair p = tid + 448 q -> row p / 8 (= tid / 8 + 56 q), k pair 2 (tid % 8)
-  const double* arow[2];
-  const double* brow[2];
-  int avb[2], bvb[2];  // valid bytes of the pair (rows beyond M / N read nothing)
-  int kk[2];           // reduction offset of each slot within a stage
+  // loader slots, LR_Q 16-byte pairs per operand per stage:
+  //   LM = 1: pair p = tid + 448 q -> k row p / 56 (= tid / 56 + 8 q), m pair 2 (tid % 56)
+  //   LM = 0: pair p = tid + 448 q -> row p / 16 (= tid / 16 + 28 q), k pair 2 (tid % 16)
+  const double* arow[LM ? 1 : LR_Q];
+  const double* brow[LM ? 1 : LR_Q];
+  int avb[LM ? 1 : LR_Q], bvb[LM ? 1 : LR_Q];  // valid bytes (rows beyond M / N read nothing)
+  if (LM) {
+    const int m = 2 * (tid % 56);
+    avb[0] = 8 * max(0, min(2, M - m));
+    bvb[0] = 8 * max(0, min(2, N - m));
+    arow[0] = A + (long long)min(m, M - 1) * g.a_m;
+    brow[0] = B + (long long)min(m, N - 1) * g.b_n;
+  } else {
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {
-    if (LM) {
-      const int m = 2 * (tid % 56);
-      kk[q] = tid / 56 + 8 * q;
-      avb[q] = 8 * max(0, min(2, M - m));
-      bvb[q] = 8 * max(0, min(2, N - m));
-      arow[q] = A + (long long)min(m, M - 1) * g.a_m;
-      brow[q] = B + (long long)min(m, N - 1) * g.b_n;
-    } else {
-      const int r = tid / 8 + 56 * q;
-      kk[q] = 2 * (tid % 8);
+    for (int q = 0; q < LR_Q; ++q) {
+      const int r = tid / 16 + 28 * q;
       avb[q] = r < M ? 16 : 0;
       bvb[q] = r < N ? 16 : 0;
       arow[q] = A + (long long)min(r, M - 1) * g.a_m;
       brow[q] = B + (long long)min(r, N - 1) * g.b_n;
     }
   }
+  auto kk_of = [&](int q) { return LM ? tid / 56 + 8 * q : 2 * (tid % 16); };
   const long long a_wrap = g.a_o - (long long)K * g.a_k, b_wrap = g.b_o - (long long)K * g.b_k;
-  // loader cursor: stage start f = (o, k), advanced by LR_BK (K >= 16 or KO == 1)
+  // loader cursor: stage start f = (o, k), advanced by LR_BK (K >= LR_BK or KO == 1)
   long long ld_o = f_begin / K;
   int ld_k = (int)(f_begin - ld_o * K);
   int ld_s = 0, ld_st = 0;
@@ -469,16 +470,17 @@ __global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant
       const long long abase = ld_o * g.a_o + (long long)ld_k * g.a_k;
       const long long bbase = ld_o * g.b_o + (long long)ld_k * g.b_k;
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const bool fin = f0 + kk[q] < f_end;
-        const bool wrap = ld_k + kk[q] >= K;  // slot crosses into the next outer index
-        const long long ao = abase + (long long)kk[q] * g.a_k + (wrap ? a_wrap : 0);
-        const long long bo = bbase + (long long)kk[q] * g.b_k + (wrap ? b_wrap : 0);
-        const int av = fin ? avb[q] : 0, bv = fin ? bvb[q] : 0;
-        double* ad = LM ? as + kk[q] * LR_PM + 2 * (tid % 56) : as + (tid / 8 + 56 * q) * LR_PK + kk[q];
-        double* bd = LM ? bs + kk[q] * LR_PM + 2 * (tid % 56) : bs + (tid / 8 + 56 * q) * LR_PK + kk[q];
-        cp16z(ad, av ? arow[q] + ao : A, av);
-        cp16z(bd, bv ? brow[q] + bo : B, bv);
+      for (int q = 0; q < LR_Q; ++q) {
+        const int kk = kk_of(q);
+        const bool fin = f0 + kk < f_end;
+        const bool wrap = ld_k + kk >= K;  // slot crosses into the next outer index
+        const long long ao = abase + (long long)kk * g.a_k + (wrap ? a_wrap : 0);
+        const long long bo = bbase + (long long)kk * g.b_k + (wrap ? b_wrap : 0);
+        const int av = fin ? avb[LM ? 0 : q] : 0, bv = fin ? bvb[LM ? 0 : q] : 0;
+        double* ad = LM ? as + kk * LR_PM + 2 * (tid % 56) : as + (tid / 16 + 28 * q) * LR_PK + kk;
+        double* bd = LM ? bs + kk * LR_PM + 2 * (tid % 56) : bs + (tid / 16 + 28 * q) * LR_PK + kk;
+        cp16z(ad, av ? arow[LM ? 0 : q] + ao : A, av);
+        cp16z(bd, bv ? brow[LM ? 0 : q] + bo : B, bv);
       }
     }
     cp_commit();
@@ -507,21 +509,24 @@ __global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant
     const double* as = smem + st * 2 * LR_OPD;
     const double* bs = as + LR_OPD;
     if (++st == LR_STAGES) st = 0;
-    double a[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int m = ar + 8 * (i & 1), k = t4 + 4 * (i >> 1);
-      a[i] = LM ? as[k * LR_PM + m] : as[m * LR_PK + k];
-    }
+    for (int k16 = 0; k16 < LR_BK; k16 += 16) {
+      double a[8];
 #pragma unroll
-    for (int j = 0; j < 7; ++j) {
-      double bq[4];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const int n = bc + 8 * j, k = t4 + 4 * i;
-        bq[i] = LM ? bs[k * LR_PM + n] : bs[n * LR_PK + k];
+      for (int i = 0; i < 8; ++i) {
+        const int m = ar + 8 * (i & 1), k = k16 + t4 + 4 * (i >> 1);
+        a[i] = LM ? as[k * LR_PM + m] : as[m * LR_PK + k];
       }
-      dmma_16x8x16(acc[j], a, bq);
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        double bq[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int n = bc + 8 * j, k = k16 + t4 + 4 * i;
+          bq[i] = LM ? bs[k * LR_PM + n] : bs[n * LR_PK + k];
+        }
+        dmma_16x8x16(acc[j], a, bq);
+      }
     }
   }
   cp_wait<0>();
@@ -549,6 +554,17 @@ __global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant
   }
 }
 
+__global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant__ LrBatch batch) {
+  extern __shared__ __align__(16) double smem[];
+  int di = 0;
+  while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
+  const GemmDesc& g = batch.d[di];
+  if (g.active && *g.active == 0) return;
+  const int local = blockIdx.x - g.block_begin;
+  if (batch.lm[di]) lr_body<1>(g, local, smem);
+  else lr_body<0>(g, local, smem);
+}
+
 // descriptors the long-reduction kernel takes: plain operands, M, N <= 112 (not both
 // <= 56), reduction >= 256, and 16-byte pairs: layout 1 (a_m == b_n == 1) or 0
 // (a_k == b_k == 1, even K); -1 otherwise
@@ -567,16 +583,22 @@ int lr_layout(const GemmDesc& d) {
 
 size_t lr_smem() { return sizeof(double) * (size_t)LR_STAGES * 2 * LR_OPD; }
 
-int lr_grouped(std::vector<GemmDesc>& descs, int layout, cudaStream_t stream, const char* tag, bool count_flops) {
-  static bool attr[2] = {false, false};
+int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
+  static bool attr = false;
+  if (!attr) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
+    attr = true;
+  }
   size_t i = 0;
   while (i < descs.size()) {
-    GemmBatch batch;
+    LrBatch batch;
     batch.count = 0;
     int blocks = 0;
     double flops = 0, bytes = 0;
     while (i < descs.size() && batch.count < kMaxGemmDescs) {
-      GemmDesc d = descs[i++];
+      GemmDesc d = descs[i].first;
+      batch.lm[batch.count] = (unsigned char)descs[i].second;
+      ++i;
       if (d.splits < 1) d.splits = 1;
       if (d.KO < 1) d.KO = 1;
       d.tiles_m = d.tiles_n = 1;
@@ -589,19 +611,7 @@ int lr_grouped(std::vector<GemmDesc>& descs, int layout, cudaStream_t stream, co
     }
     if (batch.count == 0) continue;
     ProfToken tok = prof_begin(stream);
-    if (layout == 1) {
-      if (!attr[1]) {
-        HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
-        attr[1] = true;
-      }
-      lr_kernel<1><<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
-    } else {
-      if (!attr[0]) {
-        HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
-        attr[0] = true;
-      }
-      lr_kernel<0><<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
-    }
+    lr_kernel<<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
     HT_LAUNCH_CHECK();
     prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
   }
@@ -684,15 +694,15 @@ int gemm_tiles(int M, int N) {  // tiles of a long-reduction (split-K planned) G
 }
 
 int gemm_grouped(std::vector<GemmDesc>& descs_in, cudaStream_t stream, const char* tag, bool count_flops) {
-  std::vector<GemmDesc> lr[2], descs;
+  std::vector<std::pair<GemmDesc, int>> lr;
+  std::vector<GemmDesc> descs;
   for (const auto& d : descs_in) {
     if (d.M <= 0 || d.N <= 0 || d.nb1 <= 0 || d.nb2 <= 0) continue;
     const int l = g_lr_enabled ? lr_layout(d) : -1;
-    if (l >= 0) lr[l].push_back(d);
+    if (l >= 0) lr.emplace_back(d, l);
     else descs.push_back(d);
   }
-  for (int l = 0; l < 2; ++l)
-    if (!lr[l].empty()) HT_TRY(lr_grouped(lr[l], l, stream, tag, count_flops));
+  if (!lr.empty()) HT_TRY(lr_grouped(lr, stream, tag, count_flops));
   for (int c = 0; c < kNumCfg; ++c) {
     size_t i = 0;
     while (i < descs.size()) {
