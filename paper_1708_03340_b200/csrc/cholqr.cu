@@ -12,7 +12,7 @@
 namespace ht {
 namespace {
 
-constexpr int kCholThreads = 512;
+constexpr int kCholThreads = 1024;
 constexpr int kCholMaxDescs = 48;
 // pivot / column-norm^2 below this => kappa(A) ~> 1e5: leave it to Householder
 constexpr double kPivotTol = 1e-10;
@@ -48,12 +48,17 @@ struct CholBatch {
 // at step j every row i > j does
 //   U[i][c]    -= m_i U[j][c]     (c >= i)          m_i = U[j][i] / U[j][j]
 //   Linv[i][c] -= m_i Linv[j][c]  (c <  j),  Linv[i][j] = -m_i
-// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.
-// Register-resident: thread (row i = tid/4, sub = tid%4) keeps W[i][sub + 4q],
-// q < 32, in registers; row j is broadcast through a double-buffered shared row,
-// so each step is one barrier plus 32 independent FMAs per thread.
-constexpr int kCholTPR = 4;                  // threads per row
-constexpr int kCholCPT = kCholMaxK / kCholTPR;  // columns per thread
+// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.  (U[j][i] is the Schur
+// complement's (i, j) entry by symmetry, so only row j is ever broadcast.)
+// Register-resident 2-D blocks: warp bi, lane bc keeps W[4bi .. 4bi+3][4bc .. 4bc+3]
+// in registers, so a warp owns four whole rows.  Pivots are eliminated four at a
+// time: warp J factors its own 4-row panel (pivot and multipliers by shuffles from
+// the diagonal-block lane; row values are lane-local), publishes it to a
+// double-buffered shared panel, and after ONE barrier every lower warp applies the
+// four eliminations from the panel -- K/4 barriers instead of K.
+constexpr int kCholB = 4;                      // block edge
+constexpr int kCholGrid = kCholMaxK / kCholB;  // 32 x 32 thread grid
+static_assert(kCholGrid * kCholGrid == kCholThreads && kCholGrid == kWarp, "one warp per 4-row block");
 
 __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_constant__ CholBatch cb) {
   int di = 0;
@@ -62,75 +67,107 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
   if (c.active && *c.active == 0) return;
   const int node = blockIdx.x - cb.block_begin[di];
   const int K = c.K;
-  __shared__ double rowbuf[2][kCholMaxK];
+  __shared__ __align__(16) double panel[2][kCholB][kCholMaxK];
   __shared__ double dorig[kCholMaxK];
   __shared__ double sqd[kCholMaxK];
-  __shared__ double red[kCholThreads / kWarp];
+  __shared__ double red[kCholThreads / kWarp][2];
   __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarps = kCholThreads / kWarp;
-  const int i = tid / kCholTPR, sub = tid % kCholTPR;
-  const bool row_ok = i < K;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int bi = warp, bc = lane;
+  const int i0 = kCholB * bi, c0 = kCholB * bc;
+  const bool act = i0 < K;  // the warp has rows
   const long long off = (long long)node * K * K;
   const double* Wg = c.W + off;
 
-  double w[kCholCPT];
+  double w[kCholB][kCholB];
   double dev = 0.0;
   bool nonfinite = false;
 #pragma unroll
-  for (int q = 0; q < kCholCPT; ++q) {
-    const int cc = sub + kCholTPR * q;
-    double v = 0.0;
-    if (row_ok && cc < K) {
-      v = Wg[(long long)i * K + cc];
-      if (cc >= i) {
-        dev = fmax(dev, fabs(v - (cc == i ? 1.0 : 0.0)));
-        nonfinite |= !isfinite(v);
+  for (int u = 0; u < kCholB; ++u)
+#pragma unroll
+    for (int v = 0; v < kCholB; ++v) {
+      const int i = i0 + u, cc = c0 + v;
+      double x = 0.0;
+      if (i < K && cc < K) {
+        x = Wg[(long long)i * K + cc];
+        if (cc >= i) {
+          dev = fmax(dev, fabs(x - (cc == i ? 1.0 : 0.0)));
+          nonfinite |= !isfinite(x);
+        }
+        if (cc == i) dorig[i] = x;
       }
-      if (cc == i) dorig[i] = v;
+      w[u][v] = x;
     }
-    w[q] = v;
-  }
   const int any_nonfinite = __syncthreads_or(nonfinite);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
-  if (lane == 0) red[warp] = dev;
+  if (lane == 0) red[warp][0] = dev;
   __syncthreads();
   if (tid == 0) {
     double m = 0.0;
-    for (int q = 0; q < nwarps; ++q) m = fmax(m, red[q]);
+    for (int q = 0; q < kCholThreads / kWarp; ++q) m = fmax(m, red[q][0]);
     bad = any_nonfinite || (c.check_identity && !(m <= kIdentityTol)) ? 1 : 0;
   }
 
-  for (int j = 0; j < K; ++j) {
-    double* rb = rowbuf[j & 1];
-    if (i == j) {
+  const int nblk = (K + kCholB - 1) / kCholB;
+  for (int J = 0; J < nblk; ++J) {
+    const int j0 = kCholB * J;
+    double(*P)[kCholMaxK] = panel[J & 1];
+    if (warp == J) {
+      // factor the panel: rows j0 .. j0+3 against pivots j0 .. j0+3 (lane J holds the
+      // diagonal block)
+      bool flag = false;
 #pragma unroll
-      for (int q = 0; q < kCholCPT; ++q) rb[sub + kCholTPR * q] = w[q];
+      for (int u = 0; u < kCholB; ++u) {
+        const int r = j0 + u;
+        if (r >= K) break;
+        double p = __shfl_sync(0xffffffffu, w[u][u], J);
+        const double d0 = dorig[r];
+        const bool ok = d0 > 1e-290 && isfinite(d0) && p > kPivotTol * d0 && isfinite(p);
+        if (!ok) {
+          p = (d0 > 1e-290 && isfinite(d0)) ? d0 : 1.0;  // keep going; the node is flagged
+          flag = true;
+        }
+        if (lane == 0) sqd[r] = p;
+        const double rp = __drcp_rn(p);
+#pragma unroll
+        for (int u2 = u + 1; u2 < kCholB; ++u2) {
+          const double mi = __shfl_sync(0xffffffffu, w[u][u2], J) * rp;  // U[r][r2] / p
+#pragma unroll
+          for (int v = 0; v < kCholB; ++v) {
+            const double t = fma(-mi, w[u][v], w[u2][v]);
+            w[u2][v] = c0 + v == r ? -mi : t;
+          }
+        }
+      }
+      if (flag && lane == 0) bad = 1;
+#pragma unroll
+      for (int u = 0; u < kCholB; ++u) {
+        *reinterpret_cast<double2*>(&P[u][c0]) = make_double2(w[u][0], w[u][1]);
+        *reinterpret_cast<double2*>(&P[u][c0 + 2]) = make_double2(w[u][2], w[u][3]);
+      }
     }
     __syncthreads();
-    const double d0 = dorig[j];
-    double p = rb[j];
-    const bool ok = d0 > 1e-290 && isfinite(d0) && p > kPivotTol * d0 && isfinite(p);
-    if (!ok) p = (d0 > 1e-290 && isfinite(d0)) ? d0 : 1.0;  // keep going; the node is flagged
-    if (tid == 0) {
-      sqd[j] = p;
-      if (!ok) bad = 1;
-    }
-    if (row_ok && i > j) {
-      const double mi = rb[i] * __drcp_rn(p);
+    if (act && warp > J) {
 #pragma unroll
-      for (int q0 = 0; q0 < kCholCPT; q0 += 8) {
-        double r[8];
+      for (int u = 0; u < kCholB; ++u) {
+        const int r = j0 + u;
+        if (r >= K) break;
+        const double rp = __drcp_rn(sqd[r]);
+        const double2 r01 = *reinterpret_cast<const double2*>(&P[u][c0]);
+        const double2 r23 = *reinterpret_cast<const double2*>(&P[u][c0 + 2]);
+        const double2 m01 = *reinterpret_cast<const double2*>(&P[u][i0]);
+        const double2 m23 = *reinterpret_cast<const double2*>(&P[u][i0 + 2]);
+        const double rr[4] = {r01.x, r01.y, r23.x, r23.y};
+        const double mr[4] = {m01.x, m01.y, m23.x, m23.y};
 #pragma unroll
-        for (int u = 0; u < 8; ++u) r[u] = rb[sub + kCholTPR * (q0 + u)];  // independent loads
+        for (int uu = 0; uu < kCholB; ++uu) {
+          const double mi = mr[uu] * rp;
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          // Every column is updated: c < j (Linv) and c >= i (U) need it; columns
-          // j < c < i hold not-yet-defined Linv[i][c] and are overwritten at step c;
-          // c >= K stays 0 (zero buffer entries).  Only c == j is special.
-          const int q = q0 + u, cc = sub + kCholTPR * q;
-          const double t = fma(-mi, r[u], w[q]);
-          w[q] = cc == j ? -mi : t;
+          for (int v = 0; v < kCholB; ++v) {
+            const double t = fma(-mi, rr[v], w[uu][v]);
+            w[uu][v] = c0 + v == r ? -mi : t;
+          }
         }
       }
     }
@@ -141,45 +178,42 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
   double* Rf = c.Rf + off;
   double* Ri = c.Ri + off;
   double* Ro = c.Rout ? c.Rout + (long long)node * c.r_node : nullptr;
-  if (row_ok) {
-    const double si = sqd[i];
+  double s0 = 0.0, s1 = 0.0;  // ||R||_F^2, ||R^{-1}||_F^2
+  if (act) {
 #pragma unroll
-    for (int q = 0; q < kCholCPT; ++q) {
-      const int cc = sub + kCholTPR * q;
-      if (cc >= K) continue;
-      // R[i][cc] = U[i][cc] / sqrt(D_i) (cc >= i)
-      const double rv = cc >= i ? w[q] / si : 0.0;
-      Rf[(long long)i * K + cc] = rv;
-      if (Ro) Ro[(long long)i * c.r_ld + cc] = rv;
-      // R^{-1}(cc, i) = Linv[i][cc] / sqrt(D_i) for cc <= i; zeros below the diagonal
-      Ri[(long long)cc * K + i] = cc < i ? w[q] / si : (cc == i ? 1.0 / si : 0.0);
+    for (int u = 0; u < kCholB; ++u) {
+      const int i = i0 + u;
+      if (i >= K) continue;
+      const double isi = 1.0 / sqd[i];
+#pragma unroll
+      for (int v = 0; v < kCholB; ++v) {
+        const int cc = c0 + v;
+        if (cc >= K) continue;
+        const double x = w[u][v] * isi;
+        // R[i][cc] = U[i][cc] / sqrt(D_i) (cc >= i)
+        const double rv = cc >= i ? x : 0.0;
+        Rf[(long long)i * K + cc] = rv;
+        if (Ro) Ro[(long long)i * c.r_ld + cc] = rv;
+        // R^{-1}(cc, i) = Linv[i][cc] / sqrt(D_i) for cc <= i; zeros below the diagonal
+        const double iv = cc < i ? x : (cc == i ? isi : 0.0);
+        Ri[(long long)cc * K + i] = iv;
+        s0 = fma(rv, rv, s0);
+        s1 = fma(iv, iv, s1);
+      }
     }
   }
   if (c.need2) {
     // kappa_2(R) <= ||R||_F ||R^{-1}||_F: one block reduction of the two sums of squares
-    __shared__ double fr[kCholThreads / kWarp][2];
-    double s0 = 0.0, s1 = 0.0;
-    if (row_ok) {
-      const double isi = 1.0 / sqd[i];
-#pragma unroll
-      for (int q = 0; q < kCholCPT; ++q) {
-        const int cc = sub + kCholTPR * q;
-        const double v = w[q] * isi;
-        if (cc >= i && cc < K) s0 = fma(v, v, s0);  // R[i][cc]
-        if (cc < i) s1 = fma(v, v, s1);             // R^{-1}[cc][i]
-      }
-      if (sub == 0) s1 = fma(isi, isi, s1);          // R^{-1}[i][i]
-    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s0 += __shfl_xor_sync(0xffffffffu, s0, o);
       s1 += __shfl_xor_sync(0xffffffffu, s1, o);
     }
-    if (lane == 0) { fr[warp][0] = s0; fr[warp][1] = s1; }
+    if (lane == 0) { red[warp][0] = s0; red[warp][1] = s1; }
     __syncthreads();
     if (tid == 0) {
       double a0 = 0.0, a1 = 0.0;
-      for (int q = 0; q < kCholThreads / kWarp; ++q) { a0 += fr[q][0]; a1 += fr[q][1]; }
+      for (int q = 0; q < kCholThreads / kWarp; ++q) { a0 += red[q][0]; a1 += red[q][1]; }
       if (!(sqrt(a0 * a1) <= c.kappa_max)) atomicOr(c.need2, 1);
     }
   }

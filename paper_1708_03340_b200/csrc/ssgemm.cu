@@ -10,7 +10,6 @@ namespace {
 constexpr int SST = 256;     // 8 warps
 constexpr int SBM = 128;     // rows per output tile (16 per warp: two m8 fragments)
 constexpr int SBK = 16;      // k-chunk per pipeline stage
-constexpr int NQ = SBM * SBK / SST;  // X elements each thread copies per stage
 constexpr int SSTAGES = 4;
 constexpr int kSsMaxDescs = 32;
 constexpr int kSMs = 148;
