@@ -101,6 +101,13 @@ int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
                         const ht_tensor* out, ht_stream_t stream);
 int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes,
                 const ht_tensor* out, ht_stream_t stream);
+/* CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on;
+ * env HT_GRAPHS=0 turns it off at start-up).  The second ht_truncate call with the
+ * same shapes, device pointers, control and kernel policies captures the truncation
+ * as two graphs (ORTH; GRAM + EIG + PROJECT) and later calls replay them.  Results
+ * are identical to the eager launches (same kernels, same arguments). */
+int ht_set_graph_mode(int on);
+int ht_graph_stats(int64_t* captures, int64_t* replays);
 
 /* Sharded truncation (the paper's tree-parallel protocol, one subtree per GPU):
  * runs one phase restricted to the nodes with mask[t] != 0 (host array [2d-1]).

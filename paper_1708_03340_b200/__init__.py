@@ -24,6 +24,8 @@ from .arith import (
     qr_fallback_count,
     scale,
     set_eig_mode,
+    set_graph_mode,
+    graph_stats,
     set_qr_mode,
     subtract,
     truncate,
@@ -67,6 +69,8 @@ __all__ = [
     "qr_fallback_count",
     "scale",
     "set_eig_mode",
+    "set_graph_mode",
+    "graph_stats",
     "set_qr_mode",
     "storage_size",
     "subtract",

@@ -327,6 +327,19 @@ def get_eig_mode() -> str:
     return _eig_mode
 
 
+def set_graph_mode(on: bool) -> None:
+    """CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on).
+    Same kernels and arguments as the eager launches, so results are identical."""
+    _lib.check(_lib.load().ht_set_graph_mode(1 if on else 0), "set_graph_mode")
+
+
+def graph_stats() -> tuple:
+    """(captures, replays) of the truncation graph cache."""
+    c, r = ctypes.c_int64(0), ctypes.c_int64(0)
+    _lib.check(_lib.load().ht_graph_stats(ctypes.byref(c), ctypes.byref(r)), "graph_stats")
+    return int(c.value), int(r.value)
+
+
 def qr_fallback_count() -> int:
     """How many Cholesky-QR2 sweeps were recomputed with Householder QR."""
     return int(_lib.load().ht_qr_fallback_count())

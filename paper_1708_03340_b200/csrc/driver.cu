@@ -21,6 +21,7 @@
 #include "ht_b200.h"
 #include "misc.cuh"
 #include "qr.cuh"
+#include "prof.cuh"
 
 namespace ht {
 
@@ -491,6 +492,8 @@ struct OrthCheck {
   int* host = nullptr;
   cudaEvent_t ev = nullptr;
   bool used = false;
+  bool capture = false;  // inside a CUDA-graph capture: `host` is the graph's own pinned
+                         // flag, only the copy is recorded (the caller owns the event)
 };
 
 std::mutex g_check_mu;
@@ -543,9 +546,9 @@ int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_
     HT_TRY(run_orthogonalize(x, op, a, a, s, true, true, fail, &n_chol));
     if (n_chol == 0) return kOk;
     if (deferred) {
-      HT_TRY(check_acquire(*deferred));
+      if (!deferred->capture) HT_TRY(check_acquire(*deferred));
       HT_CUDA_CHECK(cudaMemcpyAsync(deferred->host, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
-      HT_CUDA_CHECK(cudaEventRecord(deferred->ev, s));
+      if (!deferred->capture) HT_CUDA_CHECK(cudaEventRecord(deferred->ev, s));
       deferred->used = true;
       return kOk;
     }
@@ -1029,6 +1032,220 @@ int check_compatible(const View& a, const View& c) {
   return kOk;
 }
 
+// ---------------------------------------------------------------------------
+// CUDA-graph replay of the fixed-rank truncation.  A truncation is ~90 launches whose
+// arguments depend only on the shapes, the device pointers, the control and the
+// kernel policies; the second call with the same key captures it as two graphs --
+// ORTH (ending with the copy of the Cholesky-QR red flag into the graph's own pinned
+// word) and GRAM + EIG + PROJECT -- and every later call replays them: two launches,
+// no per-kernel host cost, and the host waits only on the ORTH graph's completion
+// (as the eager path does) before reading the flag.
+// ---------------------------------------------------------------------------
+struct TruncGraph {
+  std::vector<long long> key;
+  cudaGraphExec_t orth = nullptr, rest = nullptr;
+  int* flag = nullptr;  // pinned
+  cudaEvent_t ev = nullptr;
+  bool chol = false;    // the ORTH graph ran Cholesky-QR and wrote the flag
+  long long n_orth = 0, n_rest = 0;
+  unsigned long long used = 0;
+  long long replays = 0;
+};
+
+std::mutex g_graph_mu;
+std::vector<TruncGraph*> g_graphs;
+std::map<std::vector<long long>, int> g_graph_seen;
+unsigned long long g_graph_clock = 0;
+int g_graph_mode = -1;  // -1: from HT_GRAPHS (default on)
+long long g_graph_captures = 0, g_graph_replays = 0;
+// graphs evicted after fewer than two replays: the caller's buffers rotate faster than
+// the cache holds them, so capturing only adds host work -- stop capturing new ones
+long long g_graph_waste = 0;
+constexpr size_t kMaxGraphs = 16;
+constexpr long long kMaxGraphWaste = 8;
+
+bool graphs_on() {
+  if (g_graph_mode < 0) {
+    const char* e = getenv("HT_GRAPHS");
+    g_graph_mode = (e && e[0] == '0') ? 0 : 1;
+  }
+  return g_graph_mode == 1;
+}
+
+std::vector<long long> graph_key(const View& v, const View& o, const ht_trunc_ctl* ctl, const void* ws,
+                                 size_t ws_bytes) {
+  std::vector<long long> k;
+  const int nn = v.T->nn;
+  k.reserve(8 + 6 * nn);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  long long eps_bits;
+  memcpy(&eps_bits, &ctl->eps, sizeof(eps_bits));
+  k.insert(k.end(), {(long long)dev, (long long)v.T->d, (long long)v.orth, (long long)(uintptr_t)ws,
+                     (long long)ws_bytes, eps_bits, (long long)ctl->max_rank, (long long)g_qr_mode,
+                     (long long)g_eig_mode});
+  for (int t = 0; t < nn; ++t) {
+    k.push_back(v.n[t]);
+    k.push_back(v.k[t]);
+    k.push_back((long long)(uintptr_t)v.p[t]);
+    k.push_back(o.k[t]);
+    k.push_back((long long)(uintptr_t)o.p[t]);
+    k.push_back(ctl->max_rank_per_node ? ctl->max_rank_per_node[t] : -1);
+  }
+  return k;
+}
+
+// Pinned flag words of the graphs, recycled (never freed: cudaFreeHost would
+// synchronise the device, and an evicted graph may still be in flight).
+std::vector<int*> g_graph_flags;
+
+int* graph_flag() {
+  if (g_graph_flags.empty()) {
+    int* block = nullptr;
+    if (cudaHostAlloc((void**)&block, 64 * 64, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+    for (int i = 0; i < 64; ++i) g_graph_flags.push_back(block + 16 * i);
+  }
+  int* f = g_graph_flags.back();
+  g_graph_flags.pop_back();
+  return f;
+}
+
+void destroy_graph(TruncGraph* g) {
+  // executable graphs and events still in flight are released by the driver on completion
+  if (g->orth) cudaGraphExecDestroy(g->orth);
+  if (g->rest) cudaGraphExecDestroy(g->rest);
+  if (g->ev) cudaEventDestroy(g->ev);
+  if (g->flag) g_graph_flags.push_back(g->flag);
+  delete g;
+}
+
+// Capture one part of the truncation on `s`; on error the capture is ended and discarded.
+template <class F>
+int capture_part(cudaStream_t s, cudaGraphExec_t* exec, long long* launches, F&& body) {
+  const long long l0 = prof_launches();
+  HT_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  int rc = body();
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(s, &g);
+  if (rc == kOk && ce != cudaSuccess) {
+    set_error(std::string("graph capture: ") + cudaGetErrorString(ce));
+    rc = kErrCuda;
+  }
+  if (rc == kOk) {
+    ce = cudaGraphInstantiate(exec, g, 0);
+    if (ce != cudaSuccess) {
+      set_error(std::string("graph instantiate: ") + cudaGetErrorString(ce));
+      rc = kErrCuda;
+    }
+  }
+  if (g) cudaGraphDestroy(g);
+  cudaGetLastError();
+  // the launches recorded during capture did not run; replays add them back
+  *launches = prof_launches() - l0;
+  prof_add_launches(-*launches);
+  return rc;
+}
+
+// Captures run on a library-owned stream per device: the caller's stream may be the
+// legacy default stream, which cannot be captured.  The graphs launch on the caller's.
+cudaStream_t capture_stream() {
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  streams[dev] = cs;
+  return cs;
+}
+
+int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
+                       cudaStream_t s_caller, TruncGraph* G) {
+  (void)s_caller;
+  cudaStream_t s = capture_stream();
+  if (!s) {
+    set_error("cannot create the graph-capture stream");
+    return kErrCuda;
+  }
+  G->flag = graph_flag();
+  if (!G->flag) {
+    set_error("cannot allocate the graph's pinned flag");
+    return kErrCuda;
+  }
+  *G->flag = 0;
+  HT_CUDA_CHECK(cudaEventCreateWithFlags(&G->ev, cudaEventDisableTiming));
+  TruncPlan P;
+  OrthCheck chk;
+  chk.host = G->flag;
+  chk.capture = true;
+  HT_TRY(capture_part(s, &G->orth, &G->n_orth, [&]() -> int {
+    HT_TRY(plan_truncate(v, P, ws));
+    HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
+    return phase_orth(v, P, s, &chk);
+  }));
+  G->chol = chk.used;
+  HT_TRY(capture_part(s, &G->rest, &G->n_rest, [&]() -> int {
+    HT_TRY(phase_gram(P, s));
+    HT_TRY(phase_eig(v, ctl, P, s));
+    return truncate_phase2(v, ctl, ws, o, s);
+  }));
+  return kOk;
+}
+
+// ran = true when the graph path ran the truncation (else the caller runs it eagerly).
+int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
+                   cudaStream_t s, bool& ran, bool& failed) {
+  ran = false;
+  failed = false;
+  if (!graphs_on() || g_qr_mode == 1 || prof_active()) return kOk;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
+    cudaGetLastError();
+    return kOk;  // the caller is capturing: record the eager launches into its graph
+  }
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  auto key = graph_key(v, o, ctl, ws, ws_bytes);
+  TruncGraph* G = nullptr;
+  for (auto* g : g_graphs)
+    if (g->key == key) G = g;
+  if (!G) {
+    if (g_graph_seen.size() > 1024) g_graph_seen.clear();
+    if (++g_graph_seen[key] < 2 || g_graph_waste > kMaxGraphWaste) return kOk;  // one-off keys stay eager
+    if (g_graphs.size() >= kMaxGraphs) {
+      auto it = std::min_element(g_graphs.begin(), g_graphs.end(),
+                                 [](TruncGraph* a, TruncGraph* b) { return a->used < b->used; });
+      if ((*it)->replays < 2) ++g_graph_waste;
+      // an in-flight executable graph is released by the driver when it completes
+      destroy_graph(*it);
+      g_graphs.erase(it);
+    }
+    G = new TruncGraph;
+    G->key = key;
+    if (capture_truncation(v, ctl, ws, ws_bytes, o, s, G) != kOk) {
+      cudaGetLastError();
+      destroy_graph(G);
+      g_graph_seen.erase(key);
+      return kOk;  // fall back to the eager path (its own errors are authoritative)
+    }
+    g_graphs.push_back(G);
+    ++g_graph_captures;
+  }
+  G->used = ++g_graph_clock;
+  HT_CUDA_CHECK(cudaGraphLaunch(G->orth, s));
+  if (G->chol) HT_CUDA_CHECK(cudaEventRecord(G->ev, s));
+  HT_CUDA_CHECK(cudaGraphLaunch(G->rest, s));
+  prof_add_launches(G->n_orth + G->n_rest);
+  ++g_graph_replays;
+  ++G->replays;
+  ran = true;
+  if (G->chol) {
+    HT_CUDA_CHECK(cudaEventSynchronize(G->ev));
+    failed = *(volatile int*)G->flag != 0;
+  }
+  return kOk;
+}
+
 }  // namespace
 }  // namespace ht
 
@@ -1118,15 +1335,19 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
       set_error("output ranks do not match the truncation control at node " + std::to_string(t));
       return kErrShape;
     }
+  HT_TRY(check_ws(v, (char*)ws, ws_bytes));
   cudaStream_t s = (cudaStream_t)stream;
   TruncPlan P;
-  OrthCheck chk;
-  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk));
-  HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s));
-  // the speculative result stands unless the Cholesky-QR flag was raised; then the
-  // whole truncation is recomputed on the Householder path (stream order overwrites)
-  bool failed = false;
-  HT_TRY(check_result(chk, failed));
+  bool failed = false, ran = false;
+  HT_TRY(truncate_graph(v, ctl, (char*)ws, ws_bytes, o, s, ran, failed));
+  if (!ran) {
+    OrthCheck chk;
+    HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk));
+    HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s));
+    // the speculative result stands unless the Cholesky-QR flag was raised; then the
+    // whole truncation is recomputed on the Householder path (stream order overwrites)
+    HT_TRY(check_result(chk, failed));
+  }
   if (!failed) return kOk;
   ++g_qr_fallbacks;
   HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, nullptr, true));
@@ -1278,6 +1499,29 @@ int ht_set_qr_mode(int mode) {
 }
 
 int64_t ht_qr_fallback_count(void) { return g_qr_fallbacks; }
+
+int ht_set_graph_mode(int on) {
+  if (on != 0 && on != 1) {
+    set_error("graph mode must be 0 (eager launches) or 1 (CUDA-graph replay of repeated truncations)");
+    return kErrArgument;
+  }
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  g_graph_mode = on;
+  if (!on) {
+    cudaDeviceSynchronize();
+    for (auto* g : g_graphs) destroy_graph(g);
+    g_graphs.clear();
+    g_graph_seen.clear();
+    g_graph_waste = 0;
+  }
+  return kOk;
+}
+
+int ht_graph_stats(int64_t* captures, int64_t* replays) {
+  if (captures) *captures = g_graph_captures;
+  if (replays) *replays = g_graph_replays;
+  return kOk;
+}
 
 int ht_set_eig_mode(int mode) {
   if (mode != 0 && mode != 1) {

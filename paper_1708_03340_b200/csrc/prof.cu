@@ -89,6 +89,15 @@ void prof_end(const ProfToken& tok, const char* name, cudaStream_t s, double flo
   if (g_pending.size() > 4096) drain_locked();
 }
 
+bool prof_active() {
+  std::lock_guard<std::mutex> g(g_mu);
+  return g_on || g_log_on;
+}
+
+void prof_add_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+long long prof_launches() { return g_launches.load(); }
+
 }  // namespace ht
 
 extern "C" {

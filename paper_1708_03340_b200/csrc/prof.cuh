@@ -15,4 +15,10 @@ struct ProfToken {
 ProfToken prof_begin(cudaStream_t s);
 void prof_end(const ProfToken& tok, const char* name, cudaStream_t s, double flops, double bytes);
 
+// true while per-launch timing or the tag log is on (CUDA-graph replay is bypassed then)
+bool prof_active();
+// launches replayed inside a CUDA graph count like direct ones
+void prof_add_launches(long long n);
+long long prof_launches();
+
 }  // namespace ht
