@@ -150,3 +150,21 @@ def constant_rhs(load, grids, device=None) -> HTensor:
 
 
 __all__ = ["p1_diffusion_matrices", "parameter_grids", "affine_operator", "constant_rhs", "N_PARAMS", "SPATIAL_DIM"]
+
+
+def laplace_sum_operator(tree, n: int, device=None) -> HTOperator:
+    """BASELINE config C3's operator: sum_mu I (x) .. (x) L_mu (x) .. (x) I with
+    L = tridiag(-1, 2, -1) of size n, in HT format of ranks 2 (root 1) -- the
+    same construction the reference's tests use for Laplace-like operators
+    (format.py:183-250 layout): leaf columns [I, L]; every transfer tensor
+    H[0,0,0] = H[1,1,0] = H[1,0,1] = 1; root [[0, 1], [1, 0]]."""
+    import scipy.sparse as sp
+
+    lap = sp.diags([-np.ones(n - 1), 2 * np.ones(n), -np.ones(n - 1)], [-1, 0, 1], format="csr")
+    lap.sort_indices()
+    leaves = {leaf.index: [GeneralizedMatrix.diagonal(np.ones(n)), GeneralizedMatrix.csr(lap)]
+              for leaf in tree.leaves}
+    h = np.zeros((2, 2, 2))
+    h[0, 0, 0] = h[1, 1, 0] = h[1, 0, 1] = 1.0
+    transfer = {node.index: h.copy() for node in tree.nodes if not node.is_leaf and not node.is_root}
+    return HTOperator(tree, leaves, transfer, np.array([[0.0, 1.0], [1.0, 0.0]]), device=device)
