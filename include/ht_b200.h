@@ -58,7 +58,15 @@ typedef struct {
   double eps;
   int64_t max_rank;
   const int64_t* max_rank_per_node; /* [2d-1] host or NULL (dict form of max_rank) */
+  int32_t flags;                    /* HT_CTL_* bits (0: truncation only) */
 } ht_trunc_ctl;
+
+/* The caller reads the hierarchical singular values themselves (every sigma to
+ * relative accuracy, also the tiny ones of graded spectra): nodes with graded
+ * Gramians go to the Jacobi eigensolver.  Without it, truncation needs only the kept
+ * eigenpairs and the tail sums, which the tridiagonal path delivers to the
+ * reference's (LAPACK dsyevd) absolute accuracy. */
+#define HT_CTL_RELATIVE_SIGMA 1
 
 /* GeneralizedMatrix (format.py:135-180). kind: 0 dense (row-major rows x cols),
  * 1 diagonal (values[rows]), 2 CSR (int32 indptr[rows+1], indices[nnz]). */

@@ -51,7 +51,11 @@ class CTensor(ctypes.Structure):
 
 
 class CTruncCtl(ctypes.Structure):
-    _fields_ = [("eps", ctypes.c_double), ("max_rank", ctypes.c_int64), ("max_rank_per_node", _i64p)]
+    _fields_ = [("eps", ctypes.c_double), ("max_rank", ctypes.c_int64), ("max_rank_per_node", _i64p),
+                ("flags", ctypes.c_int32)]
+
+
+CTL_RELATIVE_SIGMA = 1
 
 
 class CGmat(ctypes.Structure):

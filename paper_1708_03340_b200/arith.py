@@ -255,6 +255,7 @@ def hierarchical_singular_values(a: HTensor) -> dict:
     The reference computes these inside truncate (arith.py:340-343) and discards them."""
     lib = _lib.load()
     st = _TruncState(a, TruncationControl.fixed_rank(1))
+    st.cctl.flags = _lib.CTL_RELATIVE_SIGMA  # every sigma to relative accuracy (Jacobi on graded nodes)
     st.run_phase1()
     nn = len(a.tree.nodes)
     rbuf = (ctypes.c_int64 * nn)()

@@ -798,10 +798,11 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     e.eps = ctl->eps > 0 ? ctl->eps : 0.0;
     e.n_nonroot = T.nn - 1;
     e.cap = eig_caps(ctl, t);
+    e.graded_fallback = (ctl->flags & HT_CTL_RELATIVE_SIGMA) ? 1 : 0;
     e.s_node = 0; e.v_node = 0; e.l_node = 0;
     if (!eps.empty()) {
       EigProblem& b = eps.back();
-      if (b.K == e.K && b.cap == e.cap && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback &&
+      if (b.K == e.K && b.cap == e.cap && b.graded_fallback == e.graded_fallback && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback &&
           (b.work == nullptr) == (e.work == nullptr)) {
         if (b.nodes == 1) {
           b.s_node = e.S - b.S; b.v_node = e.V - b.V; b.l_node = e.lam - b.lam;
@@ -1082,8 +1083,8 @@ std::vector<long long> graph_key(const View& v, const View& o, const ht_trunc_ct
   long long eps_bits;
   memcpy(&eps_bits, &ctl->eps, sizeof(eps_bits));
   k.insert(k.end(), {(long long)dev, (long long)v.T->d, (long long)v.orth, (long long)(uintptr_t)ws,
-                     (long long)ws_bytes, eps_bits, (long long)ctl->max_rank, (long long)g_qr_mode,
-                     (long long)g_eig_mode});
+                     (long long)ws_bytes, eps_bits, (long long)ctl->max_rank, (long long)ctl->flags,
+                     (long long)g_qr_mode, (long long)g_eig_mode});
   for (int t = 0; t < nn; ++t) {
     k.push_back(v.n[t]);
     k.push_back(v.k[t]);
@@ -1735,6 +1736,7 @@ int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double
   EigProblem e{};
   e.S = S; e.s_node = K * K; e.V = V; e.v_node = K * K; e.lam = lam; e.l_node = K;
   e.status = st; e.K = (int)K; e.nodes = (int)nodes; e.n_nonroot = 1;
+  e.graded_fallback = 1;
   std::vector<EigProblem> v{e};
   int rc = eig_batched(v, (cudaStream_t)stream);
   int hs = 0;

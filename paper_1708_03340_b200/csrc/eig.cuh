@@ -33,6 +33,7 @@ struct EigProblem {
                     // nodes the Jacobi kernel must redo; null = Jacobi for every node
   double* work;     // global scratch for K > kEigMaxK (2 K (K+2) doubles per node), or null
   long long w_node;
+  int graded_fallback;  // graded spectra go to Jacobi (relative accuracy of every sigma)
 };
 
 constexpr int kEigMaxK = 112;      // shared-memory paths (Jacobi; tridiagonal in smem)

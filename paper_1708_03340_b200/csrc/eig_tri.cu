@@ -337,8 +337,9 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     rsel = r;
     const double tn = fmax(fabs(lam[0]), fabs(lam[K - 1]));
     int fb = 0;
-    for (int k = 0; k < K; ++k)
-      if (fabs(lam[k]) < kGradedTol * tn) fb = 1;  // graded: relative accuracy needed
+    if (e.graded_fallback)
+      for (int k = 0; k < K; ++k)
+        if (fabs(lam[k]) < kGradedTol * tn) fb = 1;  // graded: relative accuracy needed
     // kept eigenpairs (ascending K-r .. K-1) and the boundary pair must be separated
     for (int k = max(0, K - r - 1); k + 1 < K; ++k)
       if (lam[k + 1] - lam[k] < kDegenTol * tn) fb = 1;
