@@ -283,6 +283,7 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
     d.nb1 = n; d.a_b1 = xn; d.b_b1 = xn; d.c_b1 = (long long)K * K;
     d.splits = c.S;
     d.active = active;
+    d.sym = 1;
     g.push_back(d);
     if (c.S > 1) {
       ReduceDesc rd{c.P, c.W, K, 1, (long long)K * K, 0, c.S, K, K, n, 1, 0, 1.0, 0.0};

@@ -183,7 +183,7 @@ void merge_gemms(std::vector<GemmDesc>& v) {
                     e.nb1 == d.nb1 && e.a_m == d.a_m && e.a_k == d.a_k && e.a_o == d.a_o && e.a_b1 == d.a_b1 &&
                     e.b_k == d.b_k && e.b_n == d.b_n && e.b_o == d.b_o && e.b_b1 == d.b_b1 && e.c_m == d.c_m &&
                     e.c_n == d.c_n && e.c_b1 == d.c_b1 && e.alpha == d.alpha && e.beta == d.beta &&
-                    e.a_tri == d.a_tri && e.b_tri == d.b_tri && e.active == d.active &&
+                    e.a_tri == d.a_tri && e.b_tri == d.b_tri && e.active == d.active && e.sym == d.sym &&
                     e.A - d.A == c * dA && e.B - d.B == c * dB && e.C - d.C == c * dC;
         if (!same) break;
         ++j;
@@ -634,10 +634,10 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       double* P2 = scratch_ar.take(S2 * k2 * k2);
       // g1[p,q] = sum_{i,l} B[i,p,l] t1[i,q,l]   (arith.py:156)
       GemmDesc a = gemm_desc(o.p[t], k2, 1, t1, 1, k2, P1, k1, 1, (int)k1, (int)k1, (int)k2);
-      a.KO = (int)kt; a.a_o = f; a.b_o = f; a.splits = S1;
+      a.KO = (int)kt; a.a_o = f; a.b_o = f; a.splits = S1; a.sym = 1;
       // g2[p,q] = sum_{i,j} B[i,j,p] t1[i,j,q]   (arith.py:157)
       GemmDesc b = gemm_desc(o.p[t], 1, k2, t1, k2, 1, P2, k2, 1, (int)k2, (int)k2, (int)(kt * k1));
-      b.splits = S2;
+      b.splits = S2; b.sym = 1;
       g2s.push_back(a);
       g2s.push_back(b);
       rs.push_back(ReduceDesc{P1, G[s1], k1, 1, 0, 0, S1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0});

@@ -565,6 +565,248 @@ __global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant
   else lr_body<0>(g, local, smem);
 }
 
+
+// ---- long-reduction kernel, warp-specialised mbarrier pipeline -----------------
+// Same tile and MMA schedule as lr_body (14 consumer warps, 112 x 112, m16n8k16),
+// but one producer warp stages the operands (16-byte cp.async, completion counted on
+// a per-stage `full` mbarrier) and the consumers release each stage on an `empty`
+// mbarrier: no CTA-wide barrier per k-chunk, consumer warps drift independently and
+// the producer runs up to LR_STAGES chunks ahead.
+constexpr int LRT_CONSUMERS = 14;
+// upper-triangle block pairs of the symmetric variant: warp w computes blocks
+// (kBI[2w], kBJ[2w]) and (kBI[2w+1], kBJ[2w+1])
+__constant__ unsigned char kBI[28] = {0, 0, 0, 0, 0, 0, 1, 1, 1, 1, 1, 1, 2, 2, 2, 2, 3, 3, 3, 3, 4, 4, 5, 5, 0, 2, 4, 6};
+__constant__ unsigned char kBJ[28] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 5, 6, 2, 3, 4, 5, 3, 4, 5, 6, 4, 5, 5, 6, 6, 6, 6, 6};
+constexpr int LRT_PRODUCERS = 2;
+constexpr int LRT_THREADS = (LRT_CONSUMERS + LRT_PRODUCERS) * 32;
+
+template <int LM>
+__device__ __forceinline__ void lrt_body(const GemmDesc& g, int local, double* smem, unsigned long long* full,
+                                         unsigned long long* empty) {
+  const int split = local % g.splits;
+  const int b = local / g.splits;
+  const int b1 = b % g.nb1, b2 = b / g.nb1;
+  const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
+  const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2;
+  const int M = g.M, N = g.N, K = g.K;
+  const long long L = (long long)K * g.KO;
+  const long long per_split = ((L + g.splits - 1) / g.splits + LR_BK - 1) / LR_BK * LR_BK;
+  const long long f_begin = split * per_split;
+  const long long f_end = min(L, f_begin + per_split);
+  const int nst = f_end > f_begin ? (int)((f_end - f_begin + LR_BK - 1) / LR_BK) : 0;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+
+  if (warp >= LRT_CONSUMERS) {
+    // ---------------- producer warps ----------------
+    // 16-byte cp.async pairs (zero-filled past the k-tail and beyond M / N), their
+    // completion signalled to full[st] by cp.async.mbarrier.arrive (one per lane)
+    long long o = f_begin / K;
+    int k = (int)(f_begin - o * K);
+    for (int s = 0; s < nst; ++s) {
+      const int st = s % LR_STAGES;
+      mbar_wait(&empty[st], ((s / LR_STAGES) & 1) ^ 1);
+      double* as = smem + st * 2 * LR_OPD;
+      double* bs = as + LR_OPD;
+      const long long f0 = f_begin + (long long)s * LR_BK;
+      const int nv = (int)min((long long)LR_BK, f_end - f0);  // valid k of this chunk
+      const int pw = warp - LRT_CONSUMERS;
+      if (LM) {
+        // k-rows kk = pw, pw + P, ...: lane covers m pairs 2 lane and 2 (lane + 32)
+#pragma unroll 4
+        for (int kq = 0; kq < LR_BK / LRT_PRODUCERS; ++kq) {
+          const int kk = kq * LRT_PRODUCERS + pw;
+          const bool fin = kk < nv;
+          const bool wrap = k + kk >= K;
+          const long long oo = wrap ? o + 1 : o;
+          const long long kx = wrap ? k + kk - K : k + kk;
+          const double* arow = A + oo * g.a_o + kx * g.a_k;
+          const double* brow = B + oo * g.b_o + kx * g.b_k;
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int r = 2 * (lane + 32 * h);
+            if (r < LR_T) {
+              const int av = fin ? 8 * max(0, min(2, M - r)) : 0;
+              const int bv = fin ? 8 * max(0, min(2, N - r)) : 0;
+              cp16z(as + kk * LR_PM + r, av ? arow + r : A, av);
+              cp16z(bs + kk * LR_PM + r, bv ? brow + r : B, bv);
+            }
+          }
+        }
+      } else {
+        // lane covers k pair kk = 2 (lane % 16) of rows lane / 16 + 2 q (this warp's half)
+        const int kk = 2 * (lane & 15);
+        const bool fin = kk < nv;
+        const bool wrap = k + kk >= K;
+        const long long oo = wrap ? o + 1 : o;
+        const long long kx = wrap ? k + kk - K : k + kk;
+        const int r0 = (lane >> 4) + LR_T / LRT_PRODUCERS * pw;
+        const double* ap = A + oo * g.a_o + kx + (long long)r0 * g.a_m;
+        const double* bp = B + oo * g.b_o + kx + (long long)r0 * g.b_n;
+        double* ad = as + r0 * LR_PK + kk;
+        double* bd = bs + r0 * LR_PK + kk;
+#pragma unroll 4
+        for (int q = 0; q < LR_T / LRT_PRODUCERS / 2; ++q) {
+          const int r = r0 + 2 * q;
+          const int av = fin && r < M ? 16 : 0;
+          const int bv = fin && r < N ? 16 : 0;
+          cp16z(ad, av ? ap : A, av);
+          cp16z(bd, bv ? bp : B, bv);
+          ap += 2 * g.a_m;
+          bp += 2 * g.b_n;
+          ad += 2 * LR_PK;
+          bd += 2 * LR_PK;
+        }
+      }
+      cp_async_mbar_arrive(&full[st]);
+      k += LR_BK;
+      while (k >= K) {
+        k -= K;
+        ++o;
+      }
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    return;
+  }
+
+  // ---------------- consumer warps ----------------
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const long long nbatch = (long long)g.nb1 * g.nb2;
+  auto store = [&](int m, int n, double r) {
+    if (g.splits == 1) {
+      double* p = g.C + b1 * g.c_b1 + b2 * g.c_b2 + (long long)m * g.c_m + (long long)n * g.c_n;
+      *p = g.beta != 0.0 ? g.alpha * r + g.beta * *p : g.alpha * r;
+    } else {
+      g.C[((long long)split * nbatch + b) * M * N + (long long)m * N + n] = r;
+    }
+  };
+  auto frag_a = [&](const double* as, int row0, int k16, double (&a)[8]) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int m = row0 + g8 + 8 * (i & 1), k = k16 + t4 + 4 * (i >> 1);
+      a[i] = LM ? as[k * LR_PM + m] : as[m * LR_PK + k];
+    }
+  };
+  auto frag_b = [&](const double* bs, int col0, int k16, double (&bq)[4]) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int n = col0 + g8, k = k16 + t4 + 4 * i;
+      bq[i] = LM ? bs[k * LR_PM + n] : bs[n * LR_PK + k];
+    }
+  };
+  if (g.sym) {
+    // Upper-triangle 16 x 16 blocks (I <= J) of the 112 x 112 tile: 28 blocks, two per
+    // warp, paired along a block row (A fragment shared) where possible.
+    const int I0 = kBI[2 * warp], J0 = kBJ[2 * warp], I1 = kBI[2 * warp + 1], J1 = kBJ[2 * warp + 1];
+    const bool same_row = I0 == I1;
+    double acc[4][4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    for (int s = 0; s < nst; ++s) {
+      const int st = s % LR_STAGES;
+      mbar_wait(&full[st], (s / LR_STAGES) & 1);
+      const double* as = smem + st * 2 * LR_OPD;
+      const double* bs = as + LR_OPD;
+#pragma unroll
+      for (int k16 = 0; k16 < LR_BK; k16 += 16) {
+        double a[8], bq[4];
+        frag_a(as, 16 * I0, k16, a);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          frag_b(bs, 16 * J0 + 8 * j, k16, bq);
+          dmma_16x8x16(acc[j], a, bq);
+        }
+        if (!same_row) frag_a(as, 16 * I1, k16, a);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          frag_b(bs, 16 * J1 + 8 * j, k16, bq);
+          dmma_16x8x16(acc[2 + j], a, bq);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const int I = q ? I1 : I0, J = q ? J1 : J0;
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int f = 0; f < 2; ++f)
+#pragma unroll
+          for (int v = 0; v < 2; ++v) {
+            const int m = 16 * I + g8 + 8 * f, n = 16 * J + 8 * j + 2 * t4 + v;
+            if (m > n || n >= N) continue;
+            const double r = acc[2 * q + j][2 * f + v];
+            store(m, n, r);
+            if (m != n) store(n, m, r);
+          }
+    }
+    return;
+  }
+  const int wm = warp >> 1, wn = warp & 1;
+  const int ar = wm * 16, bc = wn * 56;
+  double acc[7][4];
+#pragma unroll
+  for (int j = 0; j < 7; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+  for (int s = 0; s < nst; ++s) {
+    const int st = s % LR_STAGES;
+    mbar_wait(&full[st], (s / LR_STAGES) & 1);
+    const double* as = smem + st * 2 * LR_OPD;
+    const double* bs = as + LR_OPD;
+#pragma unroll
+    for (int k16 = 0; k16 < LR_BK; k16 += 16) {
+      double a[8];
+      frag_a(as, ar, k16, a);
+#pragma unroll
+      for (int j = 0; j < 7; ++j) {
+        double bq[4];
+        frag_b(bs, bc + 8 * j, k16, bq);
+        dmma_16x8x16(acc[j], a, bq);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[st]);
+  }
+#pragma unroll
+  for (int f = 0; f < 2; ++f) {
+    const int m = ar + g8 + 8 * f;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 7; ++j)
+#pragma unroll
+      for (int v = 0; v < 2; ++v) {
+        const int n = bc + 8 * j + 2 * t4 + v;
+        if (n < N) store(m, n, acc[j][2 * f + v]);
+      }
+  }
+}
+
+__global__ void __launch_bounds__(LRT_THREADS, 1) lrt_kernel(const __grid_constant__ LrBatch batch) {
+  extern __shared__ __align__(128) double smem[];
+  __shared__ unsigned long long full[LR_STAGES], empty[LR_STAGES];
+  int di = 0;
+  while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
+  const GemmDesc& g = batch.d[di];
+  if (g.active && *g.active == 0) return;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < LR_STAGES; ++i) {
+      mbar_init(&full[i], 32 * LRT_PRODUCERS);  // the producer lanes' cp.async arrivals
+      mbar_init(&empty[i], LRT_CONSUMERS);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const int local = blockIdx.x - g.block_begin;
+  if (batch.lm[di]) lrt_body<1>(g, local, smem, full, empty);
+  else lrt_body<0>(g, local, smem, full, empty);
+}
+
+// HT_LR_TMA=0: the cp.async / __syncthreads pipeline (A/B comparisons)
+const int g_lr_tma = [] {
+  const char* e = std::getenv("HT_LR_TMA");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
 // descriptors the long-reduction kernel takes: plain operands, M, N <= 112 (not both
 // <= 56), reduction >= 256, and 16-byte pairs: layout 1 (a_m == b_n == 1) or 0
 // (a_k == b_k == 1, even K); -1 otherwise
@@ -587,6 +829,7 @@ int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream
   static bool attr = false;
   if (!attr) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(lrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
     attr = true;
   }
   size_t i = 0;
@@ -601,17 +844,20 @@ int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream
       ++i;
       if (d.splits < 1) d.splits = 1;
       if (d.KO < 1) d.KO = 1;
+      if (d.M != d.N || !g_lr_tma) d.sym = 0;
       d.tiles_m = d.tiles_n = 1;
       d.block_begin = blocks;
       blocks += d.splits * d.nb1 * d.nb2;
       const double nbt = (double)d.nb1 * d.nb2;
-      flops += 2.0 * d.M * d.N * (double)d.K * d.KO * nbt;
+      // symmetric outputs: the flops of the upper triangle (the mirrored half is not computed)
+      flops += (d.sym ? 1.0 * d.M * (d.N + 1) : 2.0 * d.M * d.N) * (double)d.K * d.KO * nbt;
       bytes += 8.0 * nbt * ((double)d.M * d.K * d.KO + (double)d.K * d.KO * d.N + (double)d.M * d.N * d.splits);
       batch.d[batch.count++] = d;
     }
     if (batch.count == 0) continue;
     ProfToken tok = prof_begin(stream);
-    lr_kernel<<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
+    if (g_lr_tma) lrt_kernel<<<blocks, LRT_THREADS, lr_smem(), stream>>>(batch);
+    else lr_kernel<<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
     HT_LAUNCH_CHECK();
     prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
   }

@@ -31,6 +31,8 @@ struct GemmDesc {
   int b_tri;  // 0 dense; 1 unit-lower in (k,n): stored for k > n, 1 on the diagonal, 0 above
   double alpha, beta;
   const int* active;  // optional device flag: the GEMM is skipped (every CTA exits) when *active == 0
+  int sym;  // C is symmetric (M == N; e.g. A^T A or a reduced Gramian): the long-reduction
+            // kernel computes the upper-triangle 16 x 16 blocks only and mirrors them
 };
 
 // Sum the split-K partials [splits][batch][M][N] into C (optionally (X+X^T)/2).
