@@ -1,5 +1,6 @@
 // Stationary-operand streaming GEMM (see ssgemm.cuh).
 #include <algorithm>
+#include <cstdlib>
 
 #include "prof.cuh"
 #include "ssgemm.cuh"
@@ -290,6 +291,252 @@ __global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBa
   }
 }
 
+
+// ---- warp-specialised variant --------------------------------------------------
+// Same tiles and MMA schedule as ss_kernel (8 consumer warps x 16 rows, S resident),
+// but two producer warps stage the X chunks (cp.async, completion counted on a
+// per-stage `full` mbarrier) and the consumers release each stage on an `empty`
+// mbarrier: no CTA-wide barrier per 16-deep k-chunk, so consumer warps drift and the
+// producers run up to SS2_STAGES chunks ahead, across tile boundaries.  The only CTA
+// barriers left are at job (segment) boundaries, where S is reloaded.
+constexpr int SS2_CONS = 8;
+constexpr int SS2_PROD = 2;
+constexpr int SS2_T = (SS2_CONS + SS2_PROD) * 32;
+constexpr int SS2_STAGES = 5;
+
+template <int NF, int LAYOUT, int TRI>
+__global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ SsBatch b) {
+  constexpr int NP = NF * 8;
+  constexpr int PS = ss_pitch(NP);
+  extern __shared__ __align__(16) double smem[];
+  __shared__ unsigned long long full[SS2_STAGES], empty[SS2_STAGES];
+  double* Xs = smem;                       // [SS2_STAGES][XSTAGE]
+  double* Ss = smem + SS2_STAGES * XSTAGE;  // [kp][PS]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int total = b.tile_begin[b.count];
+  const int G = gridDim.x;
+  int t = (int)((long long)blockIdx.x * total / G);
+  const int t_end = (int)((long long)(blockIdx.x + 1) * total / G);
+  if (tid == 0) {
+    for (int i = 0; i < SS2_STAGES; ++i) {
+      mbar_init(&full[i], 32 * SS2_PROD);
+      mbar_init(&empty[i], SS2_CONS);
+    }
+    mbar_fence_init();
+  }
+  unsigned gs = 0;  // ring position: steps issued / consumed so far (both roles agree)
+
+  while (t < t_end) {
+    int di = 0;
+    while (di + 1 < b.count && t >= b.tile_begin[di + 1]) ++di;
+    const SsDesc& g = b.d[di];
+    const int tm = b.tiles_m[di];
+    const int local = t - b.tile_begin[di];
+    const int job = local / tm, mt0 = local - job * tm;
+    const int seg = min(t_end - t, tm - mt0);  // tiles of this (desc, job) in this CTA
+    if (g.active && *g.active == 0) {
+      t += seg;
+      continue;
+    }
+    const int K = g.K, N = g.N, M = g.M, M_lo = g.M_lo;
+    const int KT = (K + SBK - 1) / SBK;
+    const double* X = g.X + job * g.x_job;
+    const double* S = g.S + job * g.s_job;
+    double* C = g.C + job * g.c_job;
+    const bool vec = b.vec[di];
+    __syncthreads();  // the previous segment is done with S (and the barriers are initialised)
+    for (int e = tid; e < KT * SBK * NP; e += SS2_T) {
+      const int k = e / NP, n = e - k * NP;
+      const bool ok = k < K && n < N;
+      cp8z(Ss + k * PS + n, ok ? S + k * g.s_k + n * g.s_n : S, ok);
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+    const int nsteps = seg * KT;
+
+    if (warp >= SS2_CONS) {
+      // ---------------- producers ----------------
+      const int pl = tid - SS2_CONS * 32;  // 0 .. 63
+      int mt = mt0, kc = 0;
+      // LAYOUT 0: pair (2 mp, 2 mp + 1), mp = pl, k rows kk = 0..15 (all)
+      // LAYOUT 1: rows pl / 8 + 8 q (q < 16), k pair 2 (pl % 8)
+      const double* rowp[LAYOUT == 0 ? 2 : 16];
+      int rv = 0;             // LAYOUT 0: valid rows of the pair; LAYOUT 1: bit q = row valid
+      auto set_rows = [&](int mtile) {
+        if (LAYOUT == 0) {
+          const int m = mtile * SBM + 2 * pl;
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int mm = min(m + u, M - 1);
+            const int hi = mm / M_lo, lo = mm - hi * M_lo;
+            rowp[u] = X + hi * g.x_hi + lo * g.x_lo;
+          }
+          rv = max(0, min(2, M - m));
+        } else {
+          rv = 0;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int m = mtile * SBM + (pl >> 3) + 8 * q;
+            const int mm = m < M ? m : 0;
+            if (m < M) rv |= 1 << q;
+            const int hi = mm / M_lo, lo = mm - hi * M_lo;
+            rowp[q] = X + hi * g.x_hi + lo * g.x_lo;
+          }
+        }
+      };
+      set_rows(mt);
+      for (int s = 0; s < nsteps; ++s, ++gs) {
+        const int st = gs % SS2_STAGES;
+        mbar_wait(&empty[st], ((gs / SS2_STAGES) & 1) ^ 1);
+        double* xs = Xs + st * XSTAGE;
+        const int kb = kc * SBK;
+        if (LAYOUT == 0) {
+          const int r = 2 * pl;
+#pragma unroll
+          for (int kk = 0; kk < SBK; ++kk) {
+            const int nv = kb + kk < K ? rv : 0;
+            const long long ko = (long long)(kb + kk) * g.x_k;
+            double* dst = xs + kk * PX + r;
+            if (vec) {
+              cp16z(dst, nv ? rowp[0] + ko : X, 8 * nv);
+            } else {
+              cp8z(dst, nv > 0 ? rowp[0] + ko : X, nv > 0);
+              cp8z(dst + 1, nv > 1 ? rowp[1] + ko : X, nv > 1);
+            }
+          }
+        } else {
+          const int kk = 2 * (pl & 7);
+          const int kv = max(0, min(2, K - (kb + kk)));
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const int r = (pl >> 3) + 8 * q;
+            const int nv = (rv >> q) & 1 ? kv : 0;
+            double* dst = xs + r * PK + kk;
+            if (vec) {
+              cp16z(dst, nv ? rowp[q] + kb + kk : X, 8 * nv);
+            } else {
+              cp8z(dst, nv > 0 ? rowp[q] + kb + kk : X, nv > 0);
+              cp8z(dst + 1, nv > 1 ? rowp[q] + kb + kk + 1 : X, nv > 1);
+            }
+          }
+        }
+        cp_async_mbar_arrive(&full[st]);
+        if (++kc == KT) {
+          kc = 0;
+          if (++mt < mt0 + seg) set_rows(mt);
+        }
+      }
+    } else {
+      // ---------------- consumers ----------------
+      double acc[NF][4];
+      const int g8 = lane >> 2, t4 = lane & 3;
+      const int ar = warp * 16 + g8;
+      const double alpha = g.alpha, beta = g.beta;
+      auto zero_block = [&](int k_lo, int k_hi, int j) {
+        return (TRI == 1 && k_hi < 8 * j) || (TRI == 2 && k_lo > 8 * j + 7);
+      };
+      auto xa = [&](const double* xs, int rs, int k) -> double {
+        return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
+      };
+      for (int mt = mt0; mt < mt0 + seg; ++mt) {
+#pragma unroll
+        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+        for (int kc = 0; kc < KT; ++kc, ++gs) {
+          const int st = gs % SS2_STAGES;
+          mbar_wait(&full[st], (gs / SS2_STAGES) & 1);
+          const double* xs = Xs + st * XSTAGE;
+          const double* ss = Ss + kc * SBK * PS;
+          const int kv = K - kc * SBK;
+          const int kg = kc * SBK;
+          if (kv >= 12) {
+            double a[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+              double bq[4];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
+              if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
+            }
+          } else {
+            int k0 = 0;
+            if (kv > 4) {
+              double a[4], bq[2];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
+#pragma unroll
+              for (int j = 0; j < NF; ++j) {
+                bq[0] = ss[t4 * PS + j * 8 + g8];
+                bq[1] = ss[(t4 + 4) * PS + j * 8 + g8];
+                dmma_16x8x8(acc[j], a, bq);
+              }
+              k0 = 8;
+            }
+            if (kv > k0) {
+              double a[2], bq[1];
+              a[0] = xa(xs, 0, k0 + t4);
+              a[1] = xa(xs, 1, k0 + t4);
+#pragma unroll
+              for (int j = 0; j < NF; ++j) {
+                bq[0] = ss[(k0 + t4) * PS + j * 8 + g8];
+                dmma_16x8x4(acc[j], a, bq);
+              }
+            }
+          }
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&empty[st]);
+        }
+#pragma unroll
+        for (int f = 0; f < 2; ++f) {
+          const int m = mt * SBM + ar + 8 * f;
+          if (m < M) {
+            const int hi = m / M_lo, lo = m - hi * M_lo;
+            double* crow = C + hi * g.c_hi + lo * g.c_lo;
+            const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+              const int n = j * 8 + 2 * t4;
+              const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
+              if (pair && n + 1 < N) {
+                double2 r = make_double2(alpha * v0, alpha * v1);
+                double2* p = reinterpret_cast<double2*>(crow + n);
+                if (beta != 0.0) {
+                  const double2 o = *p;
+                  r.x += beta * o.x;
+                  r.y += beta * o.y;
+                }
+                *p = r;
+              } else {
+                if (n < N) {
+                  double* p = crow + (long long)n * g.c_n;
+                  *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
+                }
+                if (n + 1 < N) {
+                  double* p = crow + (long long)(n + 1) * g.c_n;
+                  *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+    t += seg;
+  }
+  asm volatile("cp.async.wait_all;\n" ::: "memory");
+}
+
+size_t ss2_smem(int nf, int kp) {
+  return sizeof(double) * ((size_t)SS2_STAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8));
+}
+
+// HT_SS_WS=0: the CTA-barrier cp.async pipeline (A/B comparisons)
+const int g_ss_ws = [] {
+  const char* e = std::getenv("HT_SS_WS");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
 size_t ss_smem(int nf, int kp) { return sizeof(double) * ((size_t)SSTAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8)); }
 
 template <int NF, int LAYOUT, int TRI>
@@ -298,11 +545,14 @@ int launch_ss(SsBatch& b, cudaStream_t s) {
   if (!attr) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF, LAYOUT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ss_smem(NF, kSsMaxK)));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(ss2_kernel<NF, LAYOUT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)ss2_smem(NF, kSsMaxK)));
     attr = true;
   }
   const int total = b.tile_begin[b.count];
   const int grid = std::min(total, kSMs);  // persistent: balanced contiguous tile ranges
-  ss_kernel<NF, LAYOUT, TRI><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
+  if (g_ss_ws) ss2_kernel<NF, LAYOUT, TRI><<<grid, SS2_T, ss2_smem(NF, b.kp), s>>>(b);
+  else ss_kernel<NF, LAYOUT, TRI><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
   HT_LAUNCH_CHECK();
   return kOk;
 }
