@@ -2,6 +2,8 @@
 // gemm.cu; this file holds the batched Cholesky / triangular-inverse kernel and
 // the launch sequence.
 #include <cmath>
+#include <cstdlib>
+#include <algorithm>
 
 #include "cholqr.cuh"
 #include "gemm.cuh"
@@ -220,6 +222,276 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
   if (tid == 0 && bad) atomicOr(cb.fail, 1);
 }
 
+
+// ---- blocked variant (default) --------------------------------------------------
+// One CTA of 8 warps per K x K Gram matrix, the matrix resident in shared memory
+// (padded to Kp = 16 * ceil(K / 16), pitch Kp + 4).  Right-looking blocked Cholesky
+// W = L L^T with 16-wide panels: the 16 x 16 diagonal block is factored by one warp
+// in registers (lane i owns row i; pivot by shuffle, rsqrt, rank-1 update), the panel
+// below by a row-per-thread triangular solve, the trailing matrix by DMMA m16n8k16
+// tiles.  Then X = L^{-1}: diagonal blocks per warp (column per lane), off-diagonal
+// blocks by block distance with DMMA (T = L_{I,*} X_{*,J}, X_{IJ} = -X_{II} T).  X is
+// kept transposed in the strict upper triangle (it is R^{-1} = L^{-T} there), its
+// diagonal in rinv.  Same outputs, flags and kappa estimate as chol_kernel; K
+// pivots cost one shuffle-rsqrt-update each instead of a CTA barrier each.
+constexpr int kC2Threads = 256;
+constexpr int kC2Warps = kC2Threads / 32;
+
+__host__ __device__ constexpr int c2_pitch(int kp) { return kp + 4; }
+size_t chol2_smem(int K) {
+  const int kp = (K + 15) / 16 * 16;
+  return sizeof(double) * ((size_t)kp * c2_pitch(kp) + 3 * (size_t)kp + (size_t)kC2Warps * 16 * 17);
+}
+
+__global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_constant__ CholBatch cb) {
+  int di = 0;
+  while (di + 1 < cb.count && (int)blockIdx.x >= cb.block_begin[di + 1]) ++di;
+  const CholDesc& c = cb.d[di];
+  if (c.active && *c.active == 0) return;
+  const int node = blockIdx.x - cb.block_begin[di];
+  const int K = c.K;
+  const int Kp = (K + 15) / 16 * 16, P = c2_pitch(Kp);
+  extern __shared__ __align__(16) double sm[];
+  double* A = sm;                       // [Kp][P]
+  double* d0 = A + (size_t)Kp * P;      // original diagonal
+  double* rinv = d0 + Kp;               // 1 / L_ii  (= diagonal of X = L^{-1})
+  double* scratch = rinv + 2 * Kp;      // per warp 16 x 17
+  __shared__ double red[kC2Warps][2];
+  __shared__ int bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const long long off = (long long)node * K * K;
+  const double* Wg = c.W + off;
+  if (tid == 0) bad = 0;
+
+  // load: A[r][cc] = W[cc][r] for r >= cc (the upper triangle of W), zero elsewhere
+  double dev = 0.0;
+  bool nonfinite = false;
+  for (int e = tid; e < Kp * Kp; e += kC2Threads) {
+    const int cc = e / Kp, r = e - cc * Kp;
+    double x = 0.0;
+    if (r < K && cc < K && r >= cc) {
+      x = Wg[(long long)cc * K + r];
+      dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
+      nonfinite |= !isfinite(x);
+      if (r == cc) d0[r] = x;
+    }
+    A[r * P + cc] = x;
+  }
+  const int any_nonfinite = __syncthreads_or(nonfinite);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
+  if (lane == 0) red[warp][0] = dev;
+  __syncthreads();
+  if (tid == 0) {
+    double m = 0.0;
+    for (int q = 0; q < kC2Warps; ++q) m = fmax(m, red[q][0]);
+    if (any_nonfinite || (c.check_identity && !(m <= kIdentityTol))) bad = 1;
+  }
+
+  const int nJ = Kp / 16;
+  for (int J = 0; J < nJ; ++J) {
+    const int j0 = 16 * J, jb = min(16, K - j0);
+    // (a) diagonal block, warp 0, lane i owns row j0 + i
+    if (warp == 0) {
+      double x[16];
+      const int i = lane & 15;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) x[k] = A[(j0 + i) * P + j0 + k];
+      bool flag = false;
+#pragma unroll
+      for (int p = 0; p < 16; ++p) {
+        if (p < jb) {
+          double d = __shfl_sync(0xffffffffu, x[p], p);
+          const double dd = d0[j0 + p];
+          const bool ok = dd > 1e-290 && isfinite(dd) && d > kPivotTol * dd && isfinite(d);
+          if (!ok) {
+            d = (dd > 1e-290 && isfinite(dd)) ? dd : 1.0;  // keep going; the node is flagged
+            flag = true;
+          }
+          const double rs = rsqrt(d);
+          if (i == p) {
+            x[p] = d * rs;
+            if (lane == p) rinv[j0 + p] = rs;
+          } else if (i > p) {
+            x[p] *= rs;
+          }
+#pragma unroll
+          for (int j = p + 1; j < 16; ++j) {
+            const double ljp = __shfl_sync(0xffffffffu, x[p], j);
+            if (i >= j) x[j] = fma(-x[p], ljp, x[j]);
+          }
+        }
+      }
+      if (lane < jb) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k <= i) A[(j0 + i) * P + j0 + k] = x[k];
+      }
+      if (flag && lane == 0) bad = 1;
+    }
+    __syncthreads();
+    // (b) panel: rows r >= j0 + 16 solve y L_JJ^T = a
+    {
+      const int r = j0 + 16 + tid;
+      if (r < K) {
+        double y[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) y[k] = A[r * P + j0 + k];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          y[k] *= rinv[j0 + k];
+#pragma unroll
+          for (int k2 = k + 1; k2 < 16; ++k2) y[k2] = fma(-y[k], A[(j0 + k2) * P + j0 + k], y[k2]);
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) A[r * P + j0 + k] = y[k];
+      }
+    }
+    __syncthreads();
+    // (c) trailing update A[I][cn] -= L[I][J] L[cn][J]^T on the lower tiles (DMMA)
+    if (j0 + 16 < K) {
+      int tile = warp;
+      for (int I = J + 1; I < nJ; ++I) {
+        const int ntl = 2 * (I - J);  // n8 tiles cn = 2(J+1) .. 2I+1
+        for (; tile < ntl; tile += kC2Warps) {
+          const int n0 = 16 * (J + 1) + 8 * tile, i0 = 16 * I;
+          double a[8], b[4], acc[4];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) a[q] = -A[(i0 + g8 + 8 * (q & 1)) * P + j0 + t4 + 4 * (q >> 1)];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b[q] = A[(n0 + g8) * P + j0 + t4 + 4 * q];
+          acc[0] = A[(i0 + g8) * P + n0 + 2 * t4];
+          acc[1] = A[(i0 + g8) * P + n0 + 2 * t4 + 1];
+          acc[2] = A[(i0 + g8 + 8) * P + n0 + 2 * t4];
+          acc[3] = A[(i0 + g8 + 8) * P + n0 + 2 * t4 + 1];
+          dmma_16x8x16(acc, a, b);
+          A[(i0 + g8) * P + n0 + 2 * t4] = acc[0];
+          A[(i0 + g8) * P + n0 + 2 * t4 + 1] = acc[1];
+          A[(i0 + g8 + 8) * P + n0 + 2 * t4] = acc[2];
+          A[(i0 + g8 + 8) * P + n0 + 2 * t4 + 1] = acc[3];
+        }
+        tile -= ntl;
+      }
+    }
+    __syncthreads();
+  }
+
+  // X = L^{-1}; X[r][cc] (r > cc) lives at A[cc][r], X[r][r] = rinv[r]
+  auto xat = [&](int r, int cc) -> double {  // X element (zero above the diagonal / padding)
+    return r >= K ? 0.0 : (r > cc ? A[cc * P + r] : (r == cc ? rinv[r] : 0.0));
+  };
+  // (d) diagonal blocks: warp w -> block w, lane cc -> column cc
+  for (int J = warp; J < nJ; J += kC2Warps) {
+    const int j0 = 16 * J;
+    const int cc = lane & 15;
+    double xc[16];
+#pragma unroll
+    for (int r = 0; r < 16; ++r) {
+      double v = 0.0;
+      if (r == cc) v = j0 + r < K ? rinv[j0 + r] : 0.0;
+      else if (r > cc && j0 + r < K) {
+        double sacc = 0.0;
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+          if (k >= cc && k < r) sacc = fma(A[(j0 + r) * P + j0 + k], xc[k], sacc);
+        v = -rinv[j0 + r] * sacc;
+      }
+      xc[r] = v;
+    }
+    if (lane < 16) {
+#pragma unroll
+      for (int r = 0; r < 16; ++r)
+        if (r > cc) A[(j0 + cc) * P + j0 + r] = xc[r];
+    }
+  }
+  __syncthreads();
+  // (e) off-diagonal blocks by block distance: X_IJ = -X_II (sum_k L_Ik X_kJ)
+  double* T = scratch + warp * 16 * 17;
+  for (int dlt = 1; dlt < nJ; ++dlt) {
+    for (int I = dlt + warp; I < nJ; I += kC2Warps) {
+      const int Jc = I - dlt, i0 = 16 * I, jc0 = 16 * Jc;
+      double acc[2][4] = {{0, 0, 0, 0}, {0, 0, 0, 0}};
+      for (int kb = Jc; kb < I; ++kb) {
+        const int k0 = 16 * kb;
+        double a[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) a[q] = A[(i0 + g8 + 8 * (q & 1)) * P + k0 + t4 + 4 * (q >> 1)];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double b[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) b[q] = xat(k0 + t4 + 4 * q, jc0 + 8 * h + g8);
+          dmma_16x8x16(acc[h], a, b);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        T[g8 * 17 + 8 * h + 2 * t4] = acc[h][0];
+        T[g8 * 17 + 8 * h + 2 * t4 + 1] = acc[h][1];
+        T[(g8 + 8) * 17 + 8 * h + 2 * t4] = acc[h][2];
+        T[(g8 + 8) * 17 + 8 * h + 2 * t4 + 1] = acc[h][3];
+      }
+      __syncwarp();
+      double a[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) a[q] = -xat(i0 + g8 + 8 * (q & 1), i0 + t4 + 4 * (q >> 1));
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        double b[4], o[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int q = 0; q < 4; ++q) b[q] = T[(t4 + 4 * q) * 17 + 8 * h + g8];
+        dmma_16x8x16(o, a, b);
+        // X[i0 + row][jc0 + col] -> A[jc0 + col][i0 + row]
+        A[(jc0 + 8 * h + 2 * t4) * P + i0 + g8] = o[0];
+        A[(jc0 + 8 * h + 2 * t4 + 1) * P + i0 + g8] = o[1];
+        A[(jc0 + 8 * h + 2 * t4) * P + i0 + g8 + 8] = o[2];
+        A[(jc0 + 8 * h + 2 * t4 + 1) * P + i0 + g8 + 8] = o[3];
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+  }
+
+  // outputs: R = L^T, R^{-1} = X^T (upper), zeros below; Frobenius norms for kappa
+  double* Rf = c.Rf + off;
+  double* Ri = c.Ri + off;
+  double* Ro = c.Rout ? c.Rout + (long long)node * c.r_node : nullptr;
+  double s0 = 0.0, s1 = 0.0;
+  for (int e = tid; e < K * K; e += kC2Threads) {
+    const int i = e / K, j = e - i * K;
+    const double rv = j >= i ? A[j * P + i] : 0.0;
+    const double iv = j > i ? A[i * P + j] : (j == i ? rinv[i] : 0.0);
+    Rf[e] = rv;
+    if (Ro) Ro[(long long)i * c.r_ld + j] = rv;
+    Ri[e] = iv;
+    s0 = fma(rv, rv, s0);
+    s1 = fma(iv, iv, s1);
+  }
+  if (c.need2) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    if (lane == 0) { red[warp][0] = s0; red[warp][1] = s1; }
+    __syncthreads();
+    if (tid == 0) {
+      double a0 = 0.0, a1 = 0.0;
+      for (int q = 0; q < kC2Warps; ++q) { a0 += red[q][0]; a1 += red[q][1]; }
+      if (!(sqrt(a0 * a1) <= c.kappa_max)) atomicOr(c.need2, 1);
+    }
+  }
+  __syncthreads();
+  if (tid == 0 && bad) atomicOr(cb.fail, 1);
+}
+
+// HT_CHOL_BLOCKED=0: the register-blocked elimination kernel (A/B comparisons)
+const int g_chol_blocked = [] {
+  const char* e = std::getenv("HT_CHOL_BLOCKED");
+  return e && e[0] == '0' ? 0 : 1;
+}();
+
 int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, const char* tag = "cholqr_factor") {
   size_t i = 0;
   while (i < ds.size()) {
@@ -237,7 +509,19 @@ int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, cons
     double flops = 0;
     for (int q = 0; q < b.count; ++q) flops += (double)b.d[q].nodes * b.d[q].K * b.d[q].K * b.d[q].K / 1.5;
     ProfToken tok = prof_begin(s);
-    chol_kernel<<<blocks, kCholThreads, 0, s>>>(b);
+    if (g_chol_blocked) {
+      static bool attr = false;
+      if (!attr) {
+        HT_CUDA_CHECK(cudaFuncSetAttribute(chol2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)chol2_smem(kCholMaxK)));
+        attr = true;
+      }
+      int kmax = 1;
+      for (int q = 0; q < b.count; ++q) kmax = std::max(kmax, b.d[q].K);
+      chol2_kernel<<<blocks, kC2Threads, chol2_smem(kmax), s>>>(b);
+    } else {
+      chol_kernel<<<blocks, kCholThreads, 0, s>>>(b);
+    }
     HT_LAUNCH_CHECK();
     prof_end(tok, tag, s, ds[0].active ? 0.0 : flops, 0.0);  // conditional launches: no flop claim
   }
