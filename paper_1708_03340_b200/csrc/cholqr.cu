@@ -264,19 +264,32 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   const double* Wg = c.W + off;
   if (tid == 0) bad = 0;
 
-  // load: A[r][cc] = W[cc][r] for r >= cc (the upper triangle of W), zero elsewhere
+  // load: A[r][cc] = W[cc][r] for r >= cc (the upper triangle of W), zero elsewhere;
+  // eight independent loads in flight per thread
   double dev = 0.0;
   bool nonfinite = false;
-  for (int e = tid; e < Kp * Kp; e += kC2Threads) {
-    const int cc = e / Kp, r = e - cc * Kp;
-    double x = 0.0;
-    if (r < K && cc < K && r >= cc) {
-      x = Wg[(long long)cc * K + r];
-      dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
-      nonfinite |= !isfinite(x);
-      if (r == cc) d0[r] = x;
+  for (int e0 = tid; e0 < Kp * Kp; e0 += 8 * kC2Threads) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kC2Threads;
+      const int cc = e / Kp, r = e - cc * Kp;
+      v[u] = (e < Kp * Kp && r < K && cc < K && r >= cc) ? Wg[(long long)cc * K + r] : 0.0;
     }
-    A[r * P + cc] = x;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * kC2Threads;
+      if (e < Kp * Kp) {
+        const int cc = e / Kp, r = e - cc * Kp;
+        const double x = v[u];
+        if (r < K && cc < K && r >= cc) {
+          dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
+          nonfinite |= !isfinite(x);
+          if (r == cc) d0[r] = x;
+        }
+        A[r * P + cc] = x;
+      }
+    }
   }
   const int any_nonfinite = __syncthreads_or(nonfinite);
 #pragma unroll
@@ -292,9 +305,11 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   const int nJ = Kp / 16;
   for (int J = 0; J < nJ; ++J) {
     const int j0 = 16 * J, jb = min(16, K - j0);
-    // (a) diagonal block, warp 0, lane i owns row j0 + i
+    // (a) diagonal block, warp 0, lane i owns row j0 + i; the scaled pivot column is
+    // broadcast through shared memory (one STS + LDS.128 reads instead of 15 shuffles)
     if (warp == 0) {
       double x[16];
+      double* colb = scratch;  // 16 doubles
       const int i = lane & 15;
 #pragma unroll
       for (int k = 0; k < 16; ++k) x[k] = A[(j0 + i) * P + j0 + k];
@@ -309,18 +324,20 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
             d = (dd > 1e-290 && isfinite(dd)) ? dd : 1.0;  // keep going; the node is flagged
             flag = true;
           }
-          const double rs = rsqrt(d);
-          if (i == p) {
-            x[p] = d * rs;
-            if (lane == p) rinv[j0 + p] = rs;
-          } else if (i > p) {
-            x[p] *= rs;
-          }
+          double rs;
+          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(d));
+          // two Newton steps from the ~2^-22 hardware approximation: full precision
+          rs = rs * fma(-0.5 * d * rs, rs, 1.5);
+          rs = rs * fma(-0.5 * d * rs, rs, 1.5);
+          const double l = i == p ? d * rs : x[p] * rs;
+          x[p] = l;
+          if (lane == p) rinv[j0 + p] = rs;
+          if (lane < 16 && i >= p) colb[i] = l;
+          __syncwarp();
 #pragma unroll
-          for (int j = p + 1; j < 16; ++j) {
-            const double ljp = __shfl_sync(0xffffffffu, x[p], j);
-            if (i >= j) x[j] = fma(-x[p], ljp, x[j]);
-          }
+          for (int j = p + 1; j < 16; ++j)
+            if (i >= j) x[j] = fma(-l, colb[j], x[j]);
+          __syncwarp();
         }
       }
       if (lane < jb) {
