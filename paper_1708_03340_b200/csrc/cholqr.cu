@@ -224,7 +224,7 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
 
 
 // ---- blocked variant (default) --------------------------------------------------
-// One CTA of 8 warps per K x K Gram matrix, the matrix resident in shared memory
+// One CTA of 8 warps per K x K Gram matrix (the lower triangle is read), the matrix resident in shared memory
 // (padded to Kp = 16 * ceil(K / 16), pitch Kp + 4).  Right-looking blocked Cholesky
 // W = L L^T with 16-wide panels: the 16 x 16 diagonal block is factored by one warp
 // in registers (lane i owns row i; pivot by shuffle, rsqrt, rank-1 update), the panel
@@ -264,8 +264,8 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   const double* Wg = c.W + off;
   if (tid == 0) bad = 0;
 
-  // load: A[r][cc] = W[cc][r] for r >= cc (the upper triangle of W), zero elsewhere;
-  // eight independent loads in flight per thread
+  // load: A[r][cc] = W[r][cc] for r >= cc, zero elsewhere (W is symmetric: the Gram
+  // GEMMs write both triangles), row-major on both sides; eight loads in flight per thread
   double dev = 0.0;
   bool nonfinite = false;
   for (int e0 = tid; e0 < Kp * Kp; e0 += 8 * kC2Threads) {
@@ -273,16 +273,16 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * kC2Threads;
-      const int cc = e / Kp, r = e - cc * Kp;
-      v[u] = (e < Kp * Kp && r < K && cc < K && r >= cc) ? Wg[(long long)cc * K + r] : 0.0;
+      const int r = e / Kp, cc = e - r * Kp;
+      v[u] = (e < Kp * Kp && r < K && cc <= r) ? Wg[(long long)r * K + cc] : 0.0;
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int e = e0 + u * kC2Threads;
       if (e < Kp * Kp) {
-        const int cc = e / Kp, r = e - cc * Kp;
+        const int r = e / Kp, cc = e - r * Kp;
         const double x = v[u];
-        if (r < K && cc < K && r >= cc) {
+        if (r < K && cc <= r) {
           dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
           nonfinite |= !isfinite(x);
           if (r == cc) d0[r] = x;
@@ -314,30 +314,41 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
 #pragma unroll
       for (int k = 0; k < 16; ++k) x[k] = A[(j0 + i) * P + j0 + k];
       bool flag = false;
+      // pivot d -> rsqrt, with the usual check (a failed pivot is replaced and flagged)
+      auto pivot = [&](double d, int p, double& dfix) -> double {
+        double rs = rsqrt(d);  // issued before the (warp-uniform, rarely taken) check
+        const double dd = d0[j0 + p];
+        const bool ok = dd > 1e-290 && isfinite(dd) && d > kPivotTol * dd && isfinite(d);
+        dfix = d;
+        if (!ok) {
+          dfix = (dd > 1e-290 && isfinite(dd)) ? dd : 1.0;  // keep going; the node is flagged
+          rs = rsqrt(dfix);
+          flag = true;
+        }
+        return rs;
+      };
+      // software-pipelined: pivot p + 1's diagonal (lane p + 1's own update) and its
+      // rsqrt are issued before pivot p's broadcast and rank-1 update of the block
+      double dcur, rs = pivot(__shfl_sync(0xffffffffu, x[0], 0), 0, dcur);
 #pragma unroll
       for (int p = 0; p < 16; ++p) {
         if (p < jb) {
-          double d = __shfl_sync(0xffffffffu, x[p], p);
-          const double dd = d0[j0 + p];
-          const bool ok = dd > 1e-290 && isfinite(dd) && d > kPivotTol * dd && isfinite(d);
-          if (!ok) {
-            d = (dd > 1e-290 && isfinite(dd)) ? dd : 1.0;  // keep going; the node is flagged
-            flag = true;
-          }
-          double rs;
-          asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(d));
-          // two Newton steps from the ~2^-22 hardware approximation: full precision
-          rs = rs * fma(-0.5 * d * rs, rs, 1.5);
-          rs = rs * fma(-0.5 * d * rs, rs, 1.5);
-          const double l = i == p ? d * rs : x[p] * rs;
+          const double l = i == p ? dcur * rs : x[p] * rs;
           x[p] = l;
           if (lane == p) rinv[j0 + p] = rs;
+          double dnext = 0.0, rsn = 0.0;
+          if (p + 1 < jb) {
+            const double own = fma(-l, l, x[p + 1]);
+            rsn = pivot(__shfl_sync(0xffffffffu, own, p + 1), p + 1, dnext);
+          }
           if (lane < 16 && i >= p) colb[i] = l;
           __syncwarp();
 #pragma unroll
           for (int j = p + 1; j < 16; ++j)
             if (i >= j) x[j] = fma(-l, colb[j], x[j]);
           __syncwarp();
+          dcur = dnext;
+          rs = rsn;
         }
       }
       if (lane < jb) {

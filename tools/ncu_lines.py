@@ -65,4 +65,4 @@ for r in b["rows"]:
 text = open(src).read().split("\n")
 print(b["name"][:80], "samples", tot, "function", cands[0][:60])
 for ln, n in sorted(agg.items(), key=lambda kv: -kv[1])[:30]:
-    print("%5.1f%%  %4d  %s" % (100 * n / max(tot, 1), ln, text[ln - 1].strip()[:100] if ln > 0 else "?"))
+    print("%5.1f%%  %4d  %s" % (100 * n / max(tot, 1), ln, text[ln - 1].strip()[:100] if 0 < ln <= len(text) else "(inlined header)"))
