@@ -168,6 +168,11 @@ int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws
                      double* result_dev, double* result_host, ht_stream_t stream);
 
 /* apply_operator (arith.py:378-395): out ranks are op.rank * x.rank. */
+/* Entry evaluation (reference arith.py:221-243, evaluate_entry): out[b] = X[idx[b, :]]
+ * for `count` 0-based multi-indices idx (device int64, count x d, row-major; the
+ * caller checks the bounds); one upward pass through the tree per entry. */
+int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, double* out, ht_stream_t stream);
+
 int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream);
 
 /* ---- node kernels (kernels.py primitives, batched) ------------------- */

@@ -12,6 +12,8 @@ from .arith import (
     add,
     apply_operator,
     compute_bhat,
+    evaluate_entries,
+    evaluate_entry,
     gemm,
     get_eig_mode,
     get_qr_mode,
@@ -34,6 +36,10 @@ from .format import (
     GeneralizedMatrix,
     HTensor,
     HTOperator,
+    ParseError,
+    deserialize,
+    serialize,
+    serialized_size,
     gaussian_factors,
     gaussian_htensor,
     identity_htoperator,
@@ -52,6 +58,12 @@ __all__ = [
     "apply_operator",
     "build_balanced_tree",
     "compute_bhat",
+    "evaluate_entries",
+    "evaluate_entry",
+    "deserialize",
+    "serialize",
+    "serialized_size",
+    "ParseError",
     "gaussian_factors",
     "gaussian_htensor",
     "gemm",

@@ -328,6 +328,34 @@ def get_eig_mode() -> str:
     return _eig_mode
 
 
+def evaluate_entries(a: HTensor, indices) -> torch.Tensor:
+    """X[i] for a batch of 0-based multi-indices (B x d, host or device), on the device.
+    Batched form of the reference's evaluate_entry (arith.py:221-243); IndexError on
+    an out-of-bounds index, as there."""
+    idx = torch.as_tensor(indices, dtype=torch.int64)
+    if idx.dim() == 1:
+        idx = idx[None, :]
+    if idx.dim() != 2 or idx.shape[1] != a.tree.d:
+        raise IndexError(f"indices must be B x {a.tree.d}")
+    shape = torch.tensor(a.shape, dtype=torch.int64, device=idx.device)
+    if idx.numel() and (bool((idx < 0).any()) or bool((idx >= shape).any())):
+        bad = idx[((idx < 0) | (idx >= shape)).any(dim=1)][0].tolist()
+        raise IndexError(f"index {tuple(bad)} out of bounds for shape {a.shape}")
+    idx = idx.to(a.device).contiguous()
+    out = torch.empty(idx.shape[0], dtype=F64, device=a.device)
+    _lib.check(_lib.load().ht_evaluate_entries(a._c(), idx.data_ptr(), idx.shape[0], out.data_ptr(), _stream()),
+               "evaluate_entries")
+    return out
+
+
+def evaluate_entry(a: HTensor, index) -> float:
+    """One tensor entry (reference arith.py:221-243)."""
+    index = tuple(int(i) for i in index)
+    if len(index) != a.tree.d or any(not 0 <= i < n for i, n in zip(index, a.shape)):
+        raise IndexError(f"index {index} out of bounds for shape {a.shape}")
+    return float(evaluate_entries(a, [index])[0].item())
+
+
 def set_graph_mode(on: bool) -> None:
     """CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on).
     Same kernels and arguments as the eager launches, so results are identical."""

@@ -1643,6 +1643,48 @@ int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws
   return kOk;
 }
 
+int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, double* out, ht_stream_t stream) {
+  View v;
+  HT_TRY(make_view(x, v));
+  const Tree& T = *v.T;
+  if (T.nn > kEvalMaxNodes) {
+    set_error("evaluate_entries: tree too large");
+    return kErrUnsupported;
+  }
+  if (count < 0 || (count > 0 && (!idx || !out))) {
+    set_error("evaluate_entries: null index or output buffer");
+    return kErrArgument;
+  }
+  EvalTree E{};
+  E.nn = T.nn;
+  E.d = T.d;
+  E.depth = T.depth;
+  E.kmax = 1;
+  for (int t = 0; t < T.nn; ++t) {
+    E.son1[t] = (short)T.son1[t];
+    E.son2[t] = (short)T.son2[t];
+    E.dim[t] = (short)(T.leaf(t) ? T.lo[t] - 1 : -1);
+    E.k[t] = (short)v.k[t];
+    E.p[t] = v.p[t];
+    E.kmax = std::max<int>(E.kmax, (int)v.k[t]);
+  }
+  // post-order: sons before their father, son1's subtree before son2's
+  int q = 0;
+  std::vector<std::pair<int, bool>> st{{0, false}};
+  while (!st.empty()) {
+    auto [t, expanded] = st.back();
+    st.pop_back();
+    if (T.leaf(t) || expanded) {
+      E.post[q++] = (short)t;
+      continue;
+    }
+    st.push_back({t, true});
+    st.push_back({T.son2[t], false});
+    st.push_back({T.son1[t], false});
+  }
+  return evaluate_entries(E, (const long long*)idx, count, out, (cudaStream_t)stream);
+}
+
 int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream) {
   View vx, vo;
   HT_TRY(make_view(x, vx));

@@ -234,3 +234,89 @@ int dot(const double* a, const double* b, long long n, double* out, cudaStream_t
 }
 
 }  // namespace ht
+
+namespace ht {
+namespace {
+constexpr int kEvalThreads = 256;
+
+__global__ void __launch_bounds__(kEvalThreads) evaluate_kernel(const __grid_constant__ EvalTree T,
+                                                                const long long* __restrict__ idx,
+                                                                double* __restrict__ out) {
+  extern __shared__ double stk[];  // [depth + 2][kmax]
+  const long long b = blockIdx.x;
+  const long long* ib = idx + b * T.d;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  int top = 0;  // number of rows on the stack
+  double result = 0.0;
+  for (int q = 0; q < T.nn; ++q) {
+    const int t = T.post[q];
+    if (T.son1[t] < 0) {  // leaf: row U[i_mu, :]
+      const long long i = ib[T.dim[t]];
+      const int k = T.k[t];
+      for (int j = tid; j < k; j += kEvalThreads) stk[top * T.kmax + j] = T.p[t][i * k + j];
+      ++top;
+      __syncthreads();
+      continue;
+    }
+    const int k1 = T.k[T.son1[t]], k2 = T.k[T.son2[t]];
+    const double* r1 = stk + (top - 2) * T.kmax;
+    const double* r2 = stk + (top - 1) * T.kmax;
+    const double* Bt = T.p[t];
+    if (t == 0) {  // root: r1^T B_D r2, one CTA-wide reduction
+      double acc = 0.0;
+      for (int e = tid; e < k1 * k2; e += kEvalThreads) acc = fma(r1[e / k2] * Bt[e], r2[e % k2], acc);
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      __shared__ double red[kEvalThreads / 32];
+      if (lane == 0) red[warp] = acc;
+      __syncthreads();
+      if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < kEvalThreads / 32; ++w) s += red[w];
+        result = s;
+      }
+      break;
+    }
+    // inner: row[i] = sum_{j,l} B[i,j,l] r1[j] r2[l]; warp per i, lanes along l (coalesced)
+    const int kt = T.k[t];
+    double* row = stk + top * T.kmax;  // written above the operands, then moved down
+    for (int i = warp; i < kt; i += kEvalThreads / 32) {
+      const double* Bi = Bt + (long long)i * k1 * k2;
+      double acc = 0.0;
+      for (int j = 0; j < k1; ++j) {
+        double s = 0.0;
+        for (int l = lane; l < k2; l += 32) s = fma(Bi[j * k2 + l], r2[l], s);
+        acc = fma(r1[j], s, acc);
+      }
+      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      if (lane == 0) row[i] = acc;
+    }
+    __syncthreads();
+    double* dst = stk + (top - 2) * T.kmax;
+    for (int i = tid; i < kt; i += kEvalThreads) dst[i] = row[i];
+    __syncthreads();
+    top -= 1;
+  }
+  if (tid == 0) out[b] = result;
+}
+}  // namespace
+
+int evaluate_entries(const EvalTree& T, const long long* idx, long long B, double* out, cudaStream_t s) {
+  if (B <= 0) return kOk;
+  const size_t smem = sizeof(double) * (size_t)(T.depth + 3) * T.kmax;
+  if (smem > 200 * 1024) {
+    set_error("evaluate_entries: ranks too large for the shared-memory row stack");
+    return kErrUnsupported;
+  }
+  static bool attr = false;
+  if (!attr) {
+    HT_CUDA_CHECK(cudaFuncSetAttribute(evaluate_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    attr = true;
+  }
+  ProfToken tok = prof_begin(s);
+  evaluate_kernel<<<(unsigned)B, kEvalThreads, smem, s>>>(T, idx, out);
+  HT_LAUNCH_CHECK();
+  double flops = 0;
+  prof_end(tok, "evaluate", s, flops, 0.0);
+  return kOk;
+}
+}  // namespace ht

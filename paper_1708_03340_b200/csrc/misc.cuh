@@ -60,3 +60,18 @@ int copy2d_batched(const std::vector<Copy2dDesc>& descs, cudaStream_t stream);
 int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream);
 
 }  // namespace ht
+
+namespace ht {
+// Entry evaluation (reference arith.py:221-243): for each multi-index b the leaf rows
+// U_mu[i_mu, :] are combined upward through the transfer tensors in post-order; one
+// CTA per entry, the rows of the open subtrees on a shared-memory stack.
+constexpr int kEvalMaxNodes = 1023;
+struct EvalTree {
+  int nn, d, kmax, depth;
+  short post[kEvalMaxNodes];  // node ids in post-order (root last)
+  short son1[kEvalMaxNodes], son2[kEvalMaxNodes], dim[kEvalMaxNodes];  // dim: 0-based (leaves)
+  short k[kEvalMaxNodes];
+  const double* p[kEvalMaxNodes];
+};
+int evaluate_entries(const EvalTree& T, const long long* idx, long long B, double* out, cudaStream_t s);
+}  // namespace ht

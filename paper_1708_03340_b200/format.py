@@ -256,6 +256,14 @@ def _upload(tree: DimensionTree, arrays: dict, dev: torch.device):
             a = a.detach().to("cpu", F64).numpy()
         host[t] = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
     total = sum(a.size for a in host.values())
+    if dev.type != "cuda":  # host-resident container (I/O, CPU tests); no kernel runs on it
+        arena = torch.from_numpy(np.concatenate([host[t].ravel() for t in range(len(tree.nodes))]
+                                                if host else np.zeros(0))).to(dev)
+        nodes, off = {}, 0
+        for t in range(len(tree.nodes)):
+            nodes[t] = arena[off:off + host[t].size].view(host[t].shape)
+            off += host[t].size
+        return nodes, arena
     pinned = torch.empty(total, dtype=F64, pin_memory=True)
     buf = pinned.numpy()
     off = 0
@@ -524,3 +532,94 @@ def storage_size(tensor: HTensor) -> int:
 __all__ = ["HTensor", "HTOperator", "GeneralizedMatrix", "random_htensor", "gaussian_htensor", "gaussian_factors",
            "identity_htoperator",
            "storage_size", "build_balanced_tree", "DimensionTree"]
+
+
+# ---------------------------------------------------------------------------
+# HT01 binary interchange (reference format.py:467-553): little-endian; magic
+# "HT01", u32 d, u64 reserved 0, d u64 leaf sizes in dimension order, 2d-1 u64
+# ranks in BFS node order (root 1), then every node array in id order as f64 with
+# the first index fastest (matrices column-major, transfer tensors mode 1 fastest).
+# Host-side packing of one device->host copy of the tensor's arena; deserialize
+# uploads the arrays as one arena.
+# ---------------------------------------------------------------------------
+
+HT01_MAGIC = b"HT01"
+
+
+class ParseError(ValueError):
+    """Malformed HT01 data; carries the byte offset of the first problem (format.py:37-42)."""
+
+    def __init__(self, message: str, offset: int):
+        super().__init__(f"{message} (byte offset {offset})")
+        self.offset = offset
+
+
+def serialized_size(tensor: HTensor) -> int:
+    """Exact byte length of :func:`serialize`: 16-byte header, the two index tables,
+    then 8 bytes per stored float."""
+    d = tensor.tree.d
+    return 16 + 8 * d + 8 * (2 * d - 1) + 8 * storage_size(tensor)
+
+
+def serialize(tensor: HTensor) -> bytes:
+    import struct
+
+    tree = tensor.tree
+    d = tree.d
+    leaves, transfer, root = tensor.to_numpy()
+    parts = [HT01_MAGIC, struct.pack("<IQ", d, 0)]
+    parts.append(np.array([leaves[tree.leaf_for_dim(mu).index].shape[0] for mu in range(1, d + 1)],
+                          dtype="<u8").tobytes())
+    parts.append(np.array([1] + [tensor.rank(t) for t in range(1, len(tree.nodes))], dtype="<u8").tobytes())
+    for node in tree.nodes:
+        arr = root if node.is_root else (leaves[node.index] if node.is_leaf else transfer[node.index])
+        parts.append(np.asarray(arr, dtype="<f8").ravel(order="F").tobytes())
+    return b"".join(parts)
+
+
+def deserialize(blob: bytes, device=None) -> HTensor:
+    """Inverse of :func:`serialize` (raises :class:`ParseError` with the byte offset)."""
+    import struct
+
+    blob = bytes(blob)
+    if len(blob) < 4 or blob[:4] != HT01_MAGIC:
+        raise ParseError("bad magic", 0)
+    if len(blob) < 16:
+        raise ParseError("truncated header", len(blob))
+    (d,) = struct.unpack_from("<I", blob, 4)
+    if d < 2:
+        raise ParseError(f"invalid dimension {d}", 4)
+    tree = build_balanced_tree(d)
+    off = 16
+    nn = 2 * d - 1
+    if len(blob) < off + 8 * (d + nn):
+        raise ParseError("truncated index tables", len(blob))
+    sizes = np.frombuffer(blob, dtype="<u8", count=d, offset=off).astype(np.int64)
+    off += 8 * d
+    ranks = np.frombuffer(blob, dtype="<u8", count=nn, offset=off).astype(np.int64)
+    if ranks[0] != 1:
+        raise ParseError(f"root rank must be 1, found {ranks[0]}", off)
+    off += 8 * nn
+    leaves, transfer, root = {}, {}, None
+    for node in tree.nodes:
+        t = node.index
+        if node.is_root:
+            shape = (int(ranks[node.sons[0]]), int(ranks[node.sons[1]]))
+        elif node.is_leaf:
+            shape = (int(sizes[node.dim - 1]), int(ranks[t]))
+        else:
+            shape = (int(ranks[t]), int(ranks[node.sons[0]]), int(ranks[node.sons[1]]))
+        count = math.prod(shape)
+        if len(blob) < off + 8 * count:
+            raise ParseError("truncated payload", len(blob))
+        arr = np.frombuffer(blob, dtype="<f8", count=count, offset=off).reshape(shape, order="F")
+        off += 8 * count
+        if node.is_root:
+            root = np.ascontiguousarray(arr)
+        elif node.is_leaf:
+            leaves[t] = np.ascontiguousarray(arr)
+        else:
+            transfer[t] = np.ascontiguousarray(arr)
+    if off != len(blob):
+        raise ParseError(f"{len(blob) - off} trailing bytes", off)
+    return HTensor(tree, leaves, transfer, root, device=device)

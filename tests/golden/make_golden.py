@@ -304,7 +304,34 @@ def golden_spec():
     np.savez_compressed(os.path.join(OUT, "spec.npz"), **out)
 
 
+def golden_io():
+    """HT01 bytes (format.py:467-553) and evaluate_entry values (arith.py:221-243) of
+    the reference on a ragged d=5 tree with mixed leaf sizes and ranks."""
+    tr = orc.balanced_tree(5)
+    ranks = {1: 3, 2: 4, 3: 2, 4: 3, 5: 2, 6: 3, 7: 2, 8: 3}
+    sizes = {1: 4, 2: 5, 3: 3, 4: 6, 5: 2}
+    rng = np.random.default_rng(np.random.PCG64(77))
+    rt = ref.build_balanced_tree(5)
+    U, B = {}, {}
+    for node in rt.nodes:
+        t = node.index
+        if node.is_root:
+            root = rng.standard_normal((ranks[node.sons[0]], ranks[node.sons[1]]))
+        elif node.is_leaf:
+            U[t] = rng.standard_normal((sizes[node.dim], ranks[t]))
+        else:
+            B[t] = rng.standard_normal((ranks[t], ranks[node.sons[0]], ranks[node.sons[1]]))
+    x = ref.HTensor(rt, U, B, root)
+    blob = ref.serialize(x)
+    idx = np.array([[0, 0, 0, 0, 0], [3, 4, 2, 5, 1], [1, 2, 0, 3, 1], [2, 0, 1, 4, 0]])
+    vals = np.array([ref_arith.evaluate_entry(x, tuple(i)) for i in idx])
+    out = {"meta": meta(), "blob": np.frombuffer(blob, dtype=np.uint8), "idx": idx, "vals": vals}
+    pack("x", x, out)
+    np.savez_compressed(os.path.join(OUT, "io.npz"), **out)
+
+
 if __name__ == "__main__":
+    golden_io()
     golden_spec()
     golden_small()
     golden_shrink()
