@@ -449,18 +449,16 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
           const int kv = K - kc * SBK;
           const int kg = kc * SBK;
           if (kv >= 12) {
-            // all fragments of the k16 step first (one LDS burst), then the MMAs: the
-            // DMMAs no longer wait on a just-issued LDS each
-            double a[8], bq[NF][4];
+            double a[8];
 #pragma unroll
             for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
 #pragma unroll
-            for (int j = 0; j < NF; ++j)
+            for (int j = 0; j < NF; ++j) {
+              double bq[4];
 #pragma unroll
-              for (int i = 0; i < 4; ++i) bq[j][i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
-#pragma unroll
-            for (int j = 0; j < NF; ++j)
-              if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq[j]);
+              for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
+              if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
+            }
           } else {
             int k0 = 0;
             if (kv > 4) {

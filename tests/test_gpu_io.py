@@ -28,7 +28,7 @@ def test_evaluate_entry_matches_reference(cuda_ok):
     assert htb.serialize(x) == z["blob"].tobytes()
 
 
-@pytest.mark.parametrize("d,n,k", [(8, 12, 5), (16, 6, 20), (4, 30, 100)])
+@pytest.mark.parametrize("d,n,k", [(8, 12, 5), (16, 24, 20), (4, 130, 100)])
 def test_evaluate_entries_vs_dense(cuda_ok, d, n, k):
     import paper_1708_03340_b200 as htb
 
