@@ -3,7 +3,8 @@
 //
 //   1. Householder tridiagonalisation A = Q T Q^T (lower, dsytd2 order): per column
 //      one reflector, the symmetric mat-vec p = tau A22 v by 4 threads per row, and
-//      the rank-2 update A22 -= v w^T + w v^T.  Reflectors stay in the lower triangle.
+//      the rank-2 update A22 -= v w^T + w v^T, on the lower triangle only.  Reflectors
+//      stay in the lower triangle.
 //   2. All K eigenvalues of T by multisection bisection: 4 threads per eigenvalue
 //      evaluate Sturm counts at 4 points per round (sign changes of the scaled
 //      leading-minor recurrence p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2}).
@@ -45,27 +46,35 @@ __device__ __forceinline__ double quad_sum(double v) {
   return v;
 }
 
-// Number of eigenvalues of T (d, e2 = e^2) strictly below x: sign changes of the
-// leading minors p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2} (T normalised to
-// ||T|| ~ 1).  Three FP64 ops per step; the sign test runs on the integer pipe and
-// the exact power-of-two rescale is checked every 8 steps (|p| changes by at most
-// 2^16 up / 2^-424 down in 8 steps: inside a block |e_k| > eps ||T||, and splits
-// restart the recurrence).  A zero minor counts as positive.
-__device__ __forceinline__ int sturm_count(const double* d, const double* e2, int K, double x) {
-  double pm2 = 1.0, pm1 = d[0] - x;
+// Number of eigenvalues of T strictly below x: sign changes of the leading minors
+// p_k = (d_k - x) p_{k-1} - e_{k-1}^2 p_{k-2} (T normalised to ||T|| ~ 1), with
+// de[k] = (d_k, e_{k-1}^2) read as one 16-byte word.  Three FP64 ops per step; the
+// sign test runs on the integer pipe and the exact power-of-two rescale is checked
+// every 8 steps (|p| changes by at most 2^16 up / 2^-424 down in 8 steps: inside a
+// block |e_k| > eps ||T||, and splits restart the recurrence).  A zero minor counts
+// as positive.  `splits`: some e_k = 0 (block-uniform; the common case has none and
+// runs the recurrence without the restart select).
+__device__ __forceinline__ int sturm_count(const double2* de, int K, double x, bool splits) {
+  double pm2 = 1.0, pm1 = de[0].x - x;
   int c = __double_as_longlong(pm1) < 0;
   int k = 1;
+  auto step = [&](int kk) {
+    const double2 t = de[kk];
+    // a split (e_{k-1} = 0) restarts the recurrence for the next block with
+    // p_{k-1} = 1: the count adds up over blocks and |p| cannot decay across it
+    const double q = (splits && t.y == 0.0) ? 1.0 : pm1;
+    const double p = fma(t.x - x, q, -t.y * pm2);
+    c += (int)((unsigned)(__double2hiint(p) ^ __double2hiint(q)) >> 31);
+    pm2 = q;
+    pm1 = p;
+  };
   while (k < K) {
-    const int kend = min(K, k + 8);
-    for (; k < kend; ++k) {
-      // a split (e_{k-1} = 0) restarts the recurrence for the next block with
-      // p_{k-1} = 1: the count adds up over blocks and |p| cannot decay across it
-      const double e2k = e2[k - 1];
-      const double q = e2k == 0.0 ? 1.0 : pm1;
-      const double p = fma(d[k] - x, q, -e2k * pm2);
-      c += (__double_as_longlong(p) ^ __double_as_longlong(q)) < 0;
-      pm2 = q;
-      pm1 = p;
+    if (k + 8 <= K) {
+#pragma unroll
+      for (int u = 0; u < 8; ++u) step(k + u);
+      k += 8;
+    } else {
+      for (; k < K; ++k) step(k);
     }
     const double a = fmax(fabs(pm1), fabs(pm2));
     if (a > 0x1p+300) {
@@ -77,6 +86,51 @@ __device__ __forceinline__ int sturm_count(const double* d, const double* e2, in
     }
   }
   return c;
+}
+
+// Back-transformation of one vector slice held in registers: thread `part` of an
+// 8-thread group owns rows part + 8q (q < kBtRQ).  Reflectors j of block JB
+// (8 JB <= j < 8 JB + 8) touch rows > j, i.e. register q = JB (rows with part >
+// j - 8 JB) and all q > JB: the block index is a template parameter so the register
+// window is resolved at compile time.  v_j = 1 at row j + 1, A[row][j] below.
+constexpr int kBtG = 8, kBtRQ = (kEigMaxK + kBtG - 1) / kBtG;
+template <int JB>
+__device__ __forceinline__ void bt_block(double (&zr)[kBtRQ], const double* A, const double* tau, int ap, int K,
+                                         int part) {
+  const int jhi = min(8 * JB + 7, K - 3);
+  for (int j = jhi; j >= 8 * JB; --j) {
+    const double tj = tau[j];
+    if (tj == 0.0) continue;
+    double av[kBtRQ];
+    double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+    for (int q = JB; q < kBtRQ; ++q) {
+      const int row = part + kBtG * q;
+      double a;
+      if (q == JB) a = row == j + 1 ? 1.0 : (row > j && row < K ? A[row * ap + j] : 0.0);
+      else if (q == JB + 1) a = row == j + 1 ? 1.0 : (row < K ? A[row * ap + j] : 0.0);
+      else a = row < K ? A[row * ap + j] : 0.0;
+      av[q] = a;
+      if ((q - JB) & 1) s1 = fma(a, zr[q], s1);
+      else s0 = fma(a, zr[q], s0);
+    }
+    double sj = s0 + s1;
+    sj += __shfl_xor_sync(0xffffffffu, sj, 1);
+    sj += __shfl_xor_sync(0xffffffffu, sj, 2);
+    sj += __shfl_xor_sync(0xffffffffu, sj, 4);
+    sj *= tj;
+#pragma unroll
+    for (int q = JB; q < kBtRQ; ++q) zr[q] = fma(-sj, av[q], zr[q]);
+  }
+}
+
+template <int JB>
+__device__ __forceinline__ void bt_dispatch(int jb, double (&zr)[kBtRQ], const double* A, const double* tau, int ap,
+                                            int K, int part) {
+  if constexpr (JB >= 0) {
+    if (jb == JB) bt_block<JB>(zr, A, tau, ap, K, part);
+    else bt_dispatch<JB - 1>(jb, zr, A, tau, ap, K, part);
+  }
 }
 
 __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ TriBatch b) {
@@ -169,17 +223,27 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     double* vn = vbuf + ((j + 1) & 1) * KM;
     const double tj = tau[j];
     if (tj != 0.0) {
-      // p = tau * A22 v (4 threads per row) and the per-warp partial of p.v
+      // p = tau * A22 v (4 threads per row) and the per-warp partial of p.v.  Only the
+      // lower triangle of A22 is kept current: S[i][k] is row i for k <= i, column i
+      // (odd pitch: conflict-free across rows) for k > i.
       {
         double pv = 0.0;
         for (int i0 = 0; i0 < m; i0 += TT / kGroup) {
           const int i = i0 + tid / kGroup, part = tid % kGroup;
-          double acc = 0.0;
+          double acc = 0.0, acc2 = 0.0;
           if (i < m) {
-            const double* row = A + (size_t)(j + 1 + i) * ap + (j + 1);
-            for (int k = part; k < m; k += kGroup) acc = fma(row[k], v[k], acc);
+            const double* rowi = A + (size_t)(j + 1 + i) * ap + (j + 1);
+            const double* coli = A + (size_t)(j + 1) * ap + (j + 1 + i);
+            // uniform trip count across the warp (rows differ in where they switch)
+            int k = part;
+            for (; k + kGroup < m; k += 2 * kGroup) {
+              const int k2 = k + kGroup;
+              acc = fma(k <= i ? rowi[k] : coli[(size_t)k * ap], v[k], acc);
+              acc2 = fma(k2 <= i ? rowi[k2] : coli[(size_t)k2 * ap], v[k2], acc2);
+            }
+            if (k < m) acc = fma(k <= i ? rowi[k] : coli[(size_t)k * ap], v[k], acc);
           }
-          acc = quad_sum(acc) * tj;
+          acc = quad_sum(acc + acc2) * tj;
           if (i < m && part == 0) {
             pv += acc * v[i];
             pb[i] = acc;
@@ -203,10 +267,27 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
         __syncwarp();
         if (j + 3 < K) reflector(j + 1, vn);
       } else {
-        for (int r = warp - 1; r < m; r += TT / 32 - 1) {
-          const double vr = v[r], wr = fma(c, vr, pb[r]);
-          double* ar = A + (j + 1 + r) * ap + (j + 1);
-          for (int cc = 1 + lane; cc < m; cc += 32) ar[cc] -= fma(vr, fma(c, v[cc], pb[cc]), wr * v[cc]);
+        // rank-2 update of the lower triangle (columns 1 .. r of row r); each lane keeps
+        // v and w of its columns in registers, 128 columns per pass
+        for (int cb = 1; cb < m; cb += 128) {
+          double vq[4], wq[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int cc = cb + lane + 32 * q;
+            vq[q] = cc < m ? v[cc] : 0.0;
+            wq[q] = cc < m ? fma(c, vq[q], pb[cc]) : 0.0;
+          }
+          int r = warp - 1;
+          if (r < cb) r += ((cb - r + TT / 32 - 2) / (TT / 32 - 1)) * (TT / 32 - 1);
+          for (; r < m; r += TT / 32 - 1) {
+            const double vr = v[r], wr = fma(c, vr, pb[r]);
+            double* ar = A + (size_t)(j + 1 + r) * ap + (j + 1);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const int cc = cb + lane + 32 * q;
+              if (cc <= r) ar[cc] -= fma(vr, wq[q], wr * vq[q]);
+            }
+          }
         }
       }
     } else if (warp == 0 && j + 3 < K) {
@@ -269,11 +350,18 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   // absolute accuracy of the reduction): graded Gramians leave long runs of tiny
   // e_k whose products would underflow the Sturm recurrence, and the twisted
   // vectors of eigenvalues shared by several blocks stay confined to their block
+  bool split = false;
   for (int k = tid; k + 1 < K; k += TT)
     if (fabs(ee[k]) <= 2.220446049250313e-16 * sh[3]) {
       ee[k] = 0.0;
       e2[k] = 0.0;
+      split = true;
     }
+  const bool splits = __syncthreads_or(split);
+  // (d_k, e_{k-1}^2) pairs for the Sturm recurrence, in the reflector / p buffers
+  // (free after the reduction; 16-byte aligned)
+  double2* de = reinterpret_cast<double2*>(vb + ((reinterpret_cast<uintptr_t>(vb) >> 3) & 1));
+  for (int k = tid; k < K; k += TT) de[k] = make_double2(dd[k], k > 0 ? e2[k - 1] : 0.0);
   __syncthreads();
 
   // ---- 2. eigenvalues: multisection bisection, 4 threads per eigenvalue ---------
@@ -288,7 +376,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       const bool done = !(w > 2.220446049250313e-16 * 2.0 * fmax(fabs(lo), fabs(hi)) + atol);
       if (__all_sync(0xffffffffu, done || !act)) break;
       const double x = lo + w * (double)(part + 1) / (double)(kGroup + 1);
-      const int c = act ? sturm_count(dd, e2, K, x) : 0;
+      const int c = act ? sturm_count(de, K, x, splits) : 0;
       // smallest point with count > i becomes hi; the point before it lo
       const unsigned base = (unsigned)(lane & ~(kGroup - 1));
       double nlo = lo, nhi = hi;
@@ -503,28 +591,51 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
   __syncthreads();
 
-  // ---- 4. back-transformation y = H_0 ... H_{K-3} z, G = 8 (r <= 64) or 4 threads per vector
-  {
-    const int G = r <= TT / 8 ? 8 : kGroup;
-    for (int v0 = 0; v0 < r; v0 += TT / G) {
-    const int v = v0 + tid / G, part = tid % G;
-    const bool act = v < r;
-    double* z = Z + (size_t)(act ? v : 0) * zp;
-    for (int j = K - 3; j >= 0; --j) {
-      const double tj = tau[j];
-      if (tj == 0.0) continue;
-      const int m = K - j - 1;
-      // v_j: 1 at row j+1, A[(j+1+k)*ap + j] below
-      double s = 0.0;
-      if (act)
-        for (int k = part; k < m; k += G) s = fma(k == 0 ? 1.0 : A[(j + 1 + k) * ap + j], z[j + 1 + k], s);
-      s += __shfl_xor_sync(0xffffffffu, s, 1);  // all lanes shuffle
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      if (G == 8) s += __shfl_xor_sync(0xffffffffu, s, 4);
-      s *= tj;
-      if (act)
-        for (int k = part; k < m; k += G) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(size_t)(j + 1 + k) * ap + j], z[j + 1 + k]);
+  // ---- 4. back-transformation y = H_0 ... H_{K-3} z --------------------------------
+  if (!big) {
+    // 8 threads per vector, the vector in registers (bt_block), so each reflector is
+    // one pass over its column (broadcast to the four vectors of a warp) instead of a
+    // read-modify-write of z in shared memory
+    for (int v0 = 0; v0 < r; v0 += TT / kBtG) {
+      const int v = v0 + tid / kBtG, part = tid % kBtG;
+      const bool act = v < r;
+      double* z = Z + (size_t)(act ? v : 0) * zp;
+      double zr[kBtRQ];
+#pragma unroll
+      for (int q = 0; q < kBtRQ; ++q) {
+        const int row = part + kBtG * q;
+        zr[q] = (act && row < K) ? z[row] : 0.0;
+      }
+      for (int jb = (K - 3) / 8; jb >= 0 && K >= 3; --jb) bt_dispatch<kBtRQ - 1>(jb, zr, A, tau, ap, K, part);
+      if (act) {
+#pragma unroll
+        for (int q = 0; q < kBtRQ; ++q) {
+          const int row = part + kBtG * q;
+          if (row < K) z[row] = zr[q];
+        }
+      }
     }
+  } else {
+    const int G = r <= TT / 8 ? 8 : kGroup;  // global-scratch matrices (K > kEigMaxK)
+    for (int v0 = 0; v0 < r; v0 += TT / G) {
+      const int v = v0 + tid / G, part = tid % G;
+      const bool act = v < r;
+      double* z = Z + (size_t)(act ? v : 0) * zp;
+      for (int j = K - 3; j >= 0; --j) {
+        const double tj = tau[j];
+        if (tj == 0.0) continue;
+        const int m = K - j - 1;
+        // v_j: 1 at row j+1, A[(j+1+k)*ap + j] below
+        double s = 0.0;
+        if (act)
+          for (int k = part; k < m; k += G) s = fma(k == 0 ? 1.0 : A[(size_t)(j + 1 + k) * ap + j], z[j + 1 + k], s);
+        s += __shfl_xor_sync(0xffffffffu, s, 1);  // all lanes shuffle
+        s += __shfl_xor_sync(0xffffffffu, s, 2);
+        if (G == 8) s += __shfl_xor_sync(0xffffffffu, s, 4);
+        s *= tj;
+        if (act)
+          for (int k = part; k < m; k += G) z[j + 1 + k] = fma(-s, k == 0 ? 1.0 : A[(size_t)(j + 1 + k) * ap + j], z[j + 1 + k]);
+      }
     }
   }
   __syncthreads();

@@ -56,13 +56,20 @@ for l in funcs[cands[0]]:
     if m and curl is not None:
         lines[int(m.group(1), 16)] = curl
 base = min(int(r[0], 16) for r in b["rows"])
-agg, tot = {}, 0
+stl = [(i, c) for i, c in enumerate(h) if c.startswith("stall_") and "Not Issued" not in c]
+agg, tot, why = {}, 0, {}
 for r in b["rows"]:
     n = int(r[iN] or 0)
     tot += n
     ln = lines.get(int(r[0], 16) - base, -1)
     agg[ln] = agg.get(ln, 0) + n
+    w = why.setdefault(ln, {})
+    for i, c in stl:
+        w[c[6:]] = w.get(c[6:], 0) + float(r[i] or 0)
 text = open(src).read().split("\n")
 print(b["name"][:80], "samples", tot, "function", cands[0][:60])
 for ln, n in sorted(agg.items(), key=lambda kv: -kv[1])[:30]:
-    print("%5.1f%%  %4d  %s" % (100 * n / max(tot, 1), ln, text[ln - 1].strip()[:100] if 0 < ln <= len(text) else "(inlined header)"))
+    top = sorted(why.get(ln, {}).items(), key=lambda kv: -kv[1])[:3]
+    ws = " ".join("%s:%d" % (k, v) for k, v in top if v > 0)
+    print("%5.1f%%  %4d  %-70s %s" % (100 * n / max(tot, 1), ln,
+                                      text[ln - 1].strip()[:70] if 0 < ln <= len(text) else "(inlined header)", ws))
