@@ -173,6 +173,14 @@ int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws
  * caller checks the bounds); one upward pass through the tree per entry. */
 int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, double* out, ht_stream_t stream);
 
+/* Weighted contraction readouts (reference cookie.py:362-426, extract_solution and
+ * parameter_mean): as ht_evaluate_entries, but whenever leaf_weights[mu] != NULL the
+ * leaf of 0-based dimension mu contributes the row w_mu^T U_mu (w_mu: device, length
+ * n_mu) and idx[b, mu] is ignored.  leaf_weights: host array of d device pointers, or
+ * NULL (plain entry evaluation). */
+int ht_evaluate_weighted(const ht_tensor* x, const double* const* leaf_weights, const int64_t* idx, int64_t count,
+                         double* out, ht_stream_t stream);
+
 int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream);
 
 /* ---- node kernels (kernels.py primitives, batched) ------------------- */

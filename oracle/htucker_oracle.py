@@ -487,6 +487,57 @@ def evaluate_entry(a: HT, index) -> float:
     raise AssertionError
 
 
+def _upward_spatial_pass(a: HT, leaf_values: dict) -> np.ndarray:
+    """cookie.py:362-380: parameter leaves contribute row vectors, the spatial (last)
+    leaf its full frame; nodes holding the spatial mode carry (n x k_t) matrices
+    (einsum "qjl,j,nl->nq"), the root returns v2 @ (B_D^T v1)."""
+    tr = a.tree
+    vals = dict(leaf_values)
+    for t in _bottom_up(tr):
+        if tr.is_leaf(t):
+            continue
+        s1, s2 = tr.sons[t]
+        v1, v2 = vals[s1], vals[s2]
+        if t == 0:
+            return v2 @ (a.root.T @ v1)
+        if tr.interval[t][1] == tr.d:
+            vals[t] = np.einsum("qjl,j,nl->nq", a.B[t], v1, v2)
+        else:
+            vals[t] = np.einsum("qjl,j,l->q", a.B[t], v1, v2)
+    raise AssertionError
+
+
+def extract_solution(a: HT, param_indices) -> np.ndarray:
+    """cookie.py:383-404: spatial vector at one parameter-index combination."""
+    tr = a.tree
+    param_indices = tuple(int(i) for i in param_indices)
+    if len(param_indices) != tr.d - 1:
+        raise ValueError(f"need {tr.d - 1} parameter indices")
+    vals = {}
+    for mu in range(1, tr.d):
+        f = a.U[tr.leaf_of_dim(mu)]
+        if not 0 <= param_indices[mu - 1] < f.shape[0]:
+            raise IndexError(f"parameter index {param_indices[mu - 1]} out of bounds")
+        vals[tr.leaf_of_dim(mu)] = f[param_indices[mu - 1], :]
+    vals[tr.leaf_of_dim(tr.d)] = a.U[tr.leaf_of_dim(tr.d)]
+    return _upward_spatial_pass(a, vals)
+
+
+def parameter_mean(a: HT, weights=None) -> np.ndarray:
+    """cookie.py:407-426: weighted contraction over all parameter grids (default
+    uniform)."""
+    tr = a.tree
+    vals = {}
+    for mu in range(1, tr.d):
+        f = a.U[tr.leaf_of_dim(mu)]
+        w = np.full(f.shape[0], 1.0 / f.shape[0]) if weights is None else np.asarray(weights[mu - 1], float)
+        if w.shape != (f.shape[0],):
+            raise ValueError(f"weight length {w.shape} mismatches dimension {mu}")
+        vals[tr.leaf_of_dim(mu)] = w @ f
+    vals[tr.leaf_of_dim(tr.d)] = a.U[tr.leaf_of_dim(tr.d)]
+    return _upward_spatial_pass(a, vals)
+
+
 def to_dense(a: HT) -> np.ndarray:
     """format.py:342-383: explicit frames bottom-up (desk-scale only)."""
     tr = a.tree

@@ -1644,10 +1644,15 @@ int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws
 }
 
 int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, double* out, ht_stream_t stream) {
+  return ht_evaluate_weighted(x, nullptr, idx, count, out, stream);
+}
+
+int ht_evaluate_weighted(const ht_tensor* x, const double* const* leaf_weights, const int64_t* idx, int64_t count,
+                         double* out, ht_stream_t stream) {
   View v;
   HT_TRY(make_view(x, v));
   const Tree& T = *v.T;
-  if (T.nn > kEvalMaxNodes) {
+  if (T.nn > kEvalMaxNodes || T.d > kEvalMaxDims) {
     set_error("evaluate_entries: tree too large");
     return kErrUnsupported;
   }
@@ -1667,6 +1672,11 @@ int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, d
     E.k[t] = (short)v.k[t];
     E.p[t] = v.p[t];
     E.kmax = std::max<int>(E.kmax, (int)v.k[t]);
+    if (T.leaf(t)) {
+      const int mu = T.lo[t] - 1;
+      E.n[mu] = (int)v.n[t];
+      E.w[mu] = leaf_weights ? leaf_weights[mu] : nullptr;
+    }
   }
   // post-order: sons before their father, son1's subtree before son2's
   int q = 0;

@@ -250,10 +250,22 @@ __global__ void __launch_bounds__(kEvalThreads) evaluate_kernel(const __grid_con
   double result = 0.0;
   for (int q = 0; q < T.nn; ++q) {
     const int t = T.post[q];
-    if (T.son1[t] < 0) {  // leaf: row U[i_mu, :]
-      const long long i = ib[T.dim[t]];
+    if (T.son1[t] < 0) {  // leaf: row U[i_mu, :], or the weighted row w_mu^T U
+      const int mu = T.dim[t];
       const int k = T.k[t];
-      for (int j = tid; j < k; j += kEvalThreads) stk[top * T.kmax + j] = T.p[t][i * k + j];
+      const double* w = T.w[mu];
+      if (w) {
+        const double* U = T.p[t];
+        const int n = T.n[mu];
+        for (int j = tid; j < k; j += kEvalThreads) {
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s = fma(w[i], U[(long long)i * k + j], s);
+          stk[top * T.kmax + j] = s;
+        }
+      } else {
+        const long long i = ib[mu];
+        for (int j = tid; j < k; j += kEvalThreads) stk[top * T.kmax + j] = T.p[t][i * k + j];
+      }
       ++top;
       __syncthreads();
       continue;

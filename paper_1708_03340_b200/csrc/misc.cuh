@@ -66,12 +66,17 @@ namespace ht {
 // U_mu[i_mu, :] are combined upward through the transfer tensors in post-order; one
 // CTA per entry, the rows of the open subtrees on a shared-memory stack.
 constexpr int kEvalMaxNodes = 1023;
+constexpr int kEvalMaxDims = 512;
 struct EvalTree {
   int nn, d, kmax, depth;
   short post[kEvalMaxNodes];  // node ids in post-order (root last)
   short son1[kEvalMaxNodes], son2[kEvalMaxNodes], dim[kEvalMaxNodes];  // dim: 0-based (leaves)
   short k[kEvalMaxNodes];
   const double* p[kEvalMaxNodes];
+  // optional per-dimension leaf weights: the leaf of dimension mu contributes the row
+  // w[mu]^T U (w[mu] of length n[mu]) instead of U[idx[mu], :]
+  const double* w[kEvalMaxDims];
+  int n[kEvalMaxDims];
 };
 int evaluate_entries(const EvalTree& T, const long long* idx, long long B, double* out, cudaStream_t s);
 }  // namespace ht

@@ -168,3 +168,68 @@ def laplace_sum_operator(tree, n: int, device=None) -> HTOperator:
     h[0, 0, 0] = h[1, 1, 0] = h[1, 0, 1] = 1.0
     transfer = {node.index: h.copy() for node in tree.nodes if not node.is_leaf and not node.is_root}
     return HTOperator(tree, leaves, transfer, np.array([[0.0, 1.0], [1.0, 0.0]]), device=device)
+
+
+# -- evaluation over the parameter directions (reference cookie.py:359-426) ----------
+
+
+def _spatial_readout(x: HTensor, leaf_weights: dict, param_rows: list) -> "torch.Tensor":
+    """X contracted over every parameter mode, the spatial (last) mode left open: one
+    device upward pass per spatial index (``ht_evaluate_weighted``); parameter leaves
+    contribute the weighted row w^T U (leaf_weights[mu]) or the frame row U[i, :]
+    (param_rows[mu]).  Same value as the reference's _upward_spatial_pass
+    (cookie.py:362-380), reassociated per spatial entry."""
+    import ctypes
+
+    import torch
+
+    from . import _lib
+    from .arith import _stream
+
+    d = x.tree.d
+    n_sp = x.shape[d - 1]
+    idx = torch.zeros((n_sp, d), dtype=torch.int64)
+    for mu, i in enumerate(param_rows):
+        if i is not None:
+            idx[:, mu] = int(i)
+    idx[:, d - 1] = torch.arange(n_sp, dtype=torch.int64)
+    idx = idx.to(x.device).contiguous()
+    ws = [None] * d
+    for mu, w in leaf_weights.items():
+        ws[mu] = torch.as_tensor(w, dtype=torch.float64).to(x.device).contiguous()
+    ptrs = (ctypes.c_void_p * d)(*[w.data_ptr() if w is not None else None for w in ws])
+    out = torch.empty(n_sp, dtype=torch.float64, device=x.device)
+    _lib.check(_lib.load().ht_evaluate_weighted(x._c(), ctypes.cast(ptrs, ctypes.c_void_p), idx.data_ptr(),
+                                                 n_sp, out.data_ptr(), _stream()), "evaluate_weighted")
+    return out
+
+
+def extract_solution(x: HTensor, param_indices) -> "torch.Tensor":
+    """Spatial vector at one parameter-index combination (0-based), on the device
+    (reference cookie.py:383-404): ValueError unless d-1 indices, IndexError when one
+    is out of bounds, as there."""
+    d = x.tree.d
+    param_indices = tuple(int(i) for i in param_indices)
+    if len(param_indices) != d - 1:
+        raise ValueError(f"need {d - 1} parameter indices")
+    shape = x.shape
+    for mu, i in enumerate(param_indices):
+        if not 0 <= i < shape[mu]:
+            raise IndexError(f"parameter index {i} out of bounds for dimension {mu + 1} of size {shape[mu]}")
+    return _spatial_readout(x, {}, list(param_indices))
+
+
+def parameter_mean(x: HTensor, weights=None) -> "torch.Tensor":
+    """Weighted contraction over all parameter grids (default uniform), on the device
+    (reference cookie.py:407-426): ValueError on a weight vector of the wrong length."""
+    d = x.tree.d
+    shape = x.shape
+    lw = {}
+    for mu in range(d - 1):
+        n = shape[mu]
+        w = np.full(n, 1.0 / n) if weights is None else np.asarray(
+            weights[mu].cpu() if hasattr(weights[mu], "cpu") else weights[mu], dtype=float)
+        if w.shape != (n,):
+            raise ValueError(f"weight length {w.shape} mismatches dimension {mu + 1} of size {n}")
+        lw[mu] = w
+    return _spatial_readout(x, lw, [None] * (d - 1))

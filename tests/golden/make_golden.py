@@ -291,6 +291,29 @@ def golden_c4_cg():
     np.savez_compressed(os.path.join(OUT, "c4_cg.npz"), **out)
 
 
+def golden_readouts():
+    """The reference's parameter-direction readouts (cookie.extract_solution /
+    parameter_mean) on a seeded Gaussian d=10 tensor of the cookie shape (nine
+    16-point parameter modes, spatial mode last): pins the oracle's restatement."""
+    from htucker import cookie
+
+    tree = orc.balanced_tree(10)
+    x = orc.gaussian_htensor(tree, [16] * 9 + [40], 6, seed=31)
+    xr = to_ref(x)
+    out = {"meta": meta()}
+    pack("X", x, out)
+    rng = np.random.default_rng(5)
+    idx = [tuple(int(v) for v in rng.integers(0, 16, 9)) for _ in range(3)]
+    out["idx"] = np.array(idx)
+    for q, ii in enumerate(idx):
+        out[f"sol/{q}"] = np.asarray(cookie.extract_solution(xr, ii))
+    out["mean"] = np.asarray(cookie.parameter_mean(xr))
+    ws = [rng.random(16) for _ in range(9)]
+    out["weights"] = np.array(ws)
+    out["wmean"] = np.asarray(cookie.parameter_mean(xr, ws))
+    np.savez_compressed(os.path.join(OUT, "readouts.npz"), **out)
+
+
 def golden_spec():
     """Known answers quoted in the SPEC."""
     q, r = ref_kernels.reduced_qr(np.array([[3.0], [4.0]]))
@@ -340,6 +363,7 @@ if __name__ == "__main__":
     golden_c2_d8()
     golden_cg()
     golden_c4_operator()
+    golden_readouts()
     if "--c4" in sys.argv:  # minutes of CPU time
         golden_c4_cg()
     print("golden fixtures written to", OUT)

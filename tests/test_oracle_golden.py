@@ -178,3 +178,26 @@ def test_oracle_cg_matches_reference_cg():
     assert [x.rank(t) for t in range(1, 7)] == list(z["ranks_X"])
     ref = unpack(z, "Xcg", tr)
     assert orc.orth_difference_norm(x, ref) <= 1e-12 * orc.norm(ref)
+
+
+def test_readouts_against_reference():
+    """Oracle extract_solution / parameter_mean vs the reference's cookie.py:383-426
+    on the fixture tensor (d=10, nine 16-point parameter modes, spatial mode last)."""
+    from tests.goldens import load, unpack
+
+    z = load("readouts.npz")
+    tree = orc.balanced_tree(10)
+    x = unpack(z, "X", tree)
+    gen = orc.gaussian_htensor(tree, [16] * 9 + [40], 6, seed=31)
+    for t in range(1, tree.n_nodes):
+        np.testing.assert_array_equal(x.rank(t), gen.rank(t))
+    for q, idx in enumerate(z["idx"]):
+        np.testing.assert_allclose(orc.extract_solution(x, idx), z[f"sol/{q}"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(orc.parameter_mean(x), z["mean"], rtol=1e-13, atol=0)
+    np.testing.assert_allclose(orc.parameter_mean(x, list(z["weights"])), z["wmean"], rtol=1e-13, atol=0)
+    with pytest.raises(ValueError):
+        orc.extract_solution(x, (0,) * 8)
+    with pytest.raises(IndexError):
+        orc.extract_solution(x, (0,) * 8 + (16,))
+    with pytest.raises(ValueError):
+        orc.parameter_mean(x, [np.ones(15)] * 9)
