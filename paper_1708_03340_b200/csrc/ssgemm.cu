@@ -487,6 +487,32 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
           __syncwarp();
           if (lane == 0) mbar_arrive(&empty[st]);
         }
+        // m-contiguous outputs (c_lo == 1, e.g. t1^T and the projections): lanes g8 and
+        // g8 ^ 1 swap one value per fragment so each stores a 16-byte (m, m + 1) pair
+        // (dense stationary operands only: the triangular instances are register-bound)
+        const bool mpair = TRI == 0 && beta == 0.0 && g.c_lo == 1 && g.c_n != 1 && !(M_lo & 1) && !(g.c_hi & 1) &&
+                           !(g.c_n & 1) && !(((uintptr_t)C) & 15);
+        if (mpair) {
+          const bool odd = g8 & 1;
+#pragma unroll
+          for (int f = 0; f < 2; ++f) {
+            const int m0 = mt * SBM + warp * 16 + 8 * f + (g8 & ~1);
+            const int hi = m0 / M_lo, lo = m0 - hi * M_lo;
+            double* crow = C + hi * g.c_hi + lo;
+#pragma unroll
+            for (int j = 0; j < NF; ++j) {
+              const double keep = odd ? acc[j][2 * f + 1] : acc[j][2 * f];
+              const double got = __shfl_xor_sync(0xffffffffu, odd ? acc[j][2 * f] : acc[j][2 * f + 1], 4);
+              const int col = j * 8 + 2 * t4 + (odd ? 1 : 0);
+              if (col < N && m0 < M) {
+                double* p = crow + (long long)col * g.c_n;
+                const double r0 = alpha * (odd ? got : keep), r1 = alpha * (odd ? keep : got);
+                if (m0 + 1 < M) *reinterpret_cast<double2*>(p) = make_double2(r0, r1);
+                else *p = r0;
+              }
+            }
+          }
+        } else
 #pragma unroll
         for (int f = 0; f < 2; ++f) {
           const int m = mt * SBM + ar + 8 * f;

@@ -46,6 +46,10 @@ for l in dis.split("\n"):
         funcs[name].append(l)
 want = re.sub(r"\(.*", "", b["name"]).split("::")[-1].split("<")[0]
 cands = [f for f in funcs if want in f]
+targs = re.findall(r"\(int\)(-?\d+)", b["name"].split("(ht::")[0]) or re.findall(r"<(.*)>", b["name"])
+if targs and all(re.fullmatch(r"-?\d+", a) for a in targs):  # template instance: match the mangled args
+    tag = "I" + "".join("Li%sE" % a.replace("-", "n") for a in targs) + "E"
+    cands = [f for f in cands if tag in f] or cands
 lines, curl = {}, None
 for l in funcs[cands[0]]:
     m = re.search(r"line (\d+)", l)
