@@ -217,6 +217,10 @@ int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha
 int ht_set_qr_mode(int mode);
 /* Number of Cholesky-QR2 sweeps that were re-run with Householder QR. */
 int64_t ht_qr_fallback_count(void);
+/* Graph replays re-run a flagged Cholesky-QR sweep on the Householder path through a
+ * device-side conditional node (no host round trip): 1 when in use, 0 when the
+ * driver lacks conditional nodes (host-side flag check), -1 before the first capture. */
+int ht_graph_device_fallback(void);
 
 /* Eigensolver policy of the truncation (process-wide).
  *   0 (default): Householder tridiagonalisation + multisection bisection +

@@ -494,6 +494,8 @@ struct OrthCheck {
   bool used = false;
   bool capture = false;  // inside a CUDA-graph capture: `host` is the graph's own pinned
                          // flag, only the copy is recorded (the caller owns the event)
+  bool device = false;   // inside a capture whose fallback is a device-side conditional
+                         // node: nothing is copied to the host
 };
 
 std::mutex g_check_mu;
@@ -545,6 +547,10 @@ int orth_sweep(const View& x, OrthPlan& op, const Arena& scratch_in, cudaStream_
     int n_chol = 0;
     HT_TRY(run_orthogonalize(x, op, a, a, s, true, true, fail, &n_chol));
     if (n_chol == 0) return kOk;
+    if (deferred && deferred->device) {
+      deferred->used = true;
+      return kOk;
+    }
     if (deferred) {
       if (!deferred->capture) HT_TRY(check_acquire(*deferred));
       HT_CUDA_CHECK(cudaMemcpyAsync(deferred->host, fail, sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -1048,6 +1054,7 @@ struct TruncGraph {
   int* flag = nullptr;  // pinned
   cudaEvent_t ev = nullptr;
   bool chol = false;    // the ORTH graph ran Cholesky-QR and wrote the flag
+  bool device = false;  // the Householder re-run is a conditional node of the REST graph
   long long n_orth = 0, n_rest = 0;
   unsigned long long used = 0;
   long long replays = 0;
@@ -1161,6 +1168,76 @@ cudaStream_t capture_stream() {
   return cs;
 }
 
+// Device-side Cholesky-QR fallback (graph replays): a one-thread kernel turns the red
+// flag into the condition of an IF node whose body is the whole truncation on the
+// Householder path, so a replay needs no host round trip.  Taken branches are counted
+// on the device (ht_qr_fallback_count adds them).
+__device__ unsigned long long g_dev_qr_fallbacks = 0;
+int g_dev_fallback = -1;  // -1 untried, 1 works, 0 unavailable (host check instead)
+
+__global__ void qr_fallback_cond_kernel(cudaGraphConditionalHandle h, const int* fail) {
+  const unsigned v = *fail != 0 ? 1u : 0u;
+  if (v) atomicAdd(&g_dev_qr_fallbacks, 1ull);
+  cudaGraphSetConditional(h, v);
+}
+
+cudaStream_t capture_stream2() {
+  static std::map<int, cudaStream_t> streams;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  streams[dev] = cs;
+  return cs;
+}
+
+// Appended to the REST capture on `s`: condition kernel + IF node (body captured on a
+// second stream).  `body_launches`: kernels recorded in the body (they run only when
+// the branch is taken).
+int capture_device_fallback(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
+                            const int* fail, cudaStream_t s, long long* body_launches) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  HT_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  qr_fallback_cond_kernel<<<1, 1, 0, s>>>(h, fail);
+  HT_LAUNCH_CHECK();
+  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  HT_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, nd, &cp));
+  HT_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t s2 = capture_stream2();
+  if (!s2) {
+    set_error("cannot create the second graph-capture stream");
+    return kErrCuda;
+  }
+  const long long l0 = prof_launches();
+  HT_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+  TruncPlan P2;
+  int rc = truncate_phase1(v, ctl, ws, ws_bytes, P2, s2, nullptr, true);
+  if (rc == kOk) rc = truncate_phase2(v, ctl, ws, o, s2);
+  cudaGraph_t body = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s2, &body);
+  *body_launches = prof_launches() - l0;
+  if (rc != kOk) return rc;
+  if (ce != cudaSuccess) {
+    set_error(std::string("fallback body capture: ") + cudaGetErrorString(ce));
+    return kErrCuda;
+  }
+  return kOk;
+}
+
 int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
                        cudaStream_t s_caller, TruncGraph* G) {
   (void)s_caller;
@@ -1180,17 +1257,39 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   OrthCheck chk;
   chk.host = G->flag;
   chk.capture = true;
+  chk.device = g_dev_fallback != 0;
   HT_TRY(capture_part(s, &G->orth, &G->n_orth, [&]() -> int {
     HT_TRY(plan_truncate(v, P, ws));
     HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
     return phase_orth(v, P, s, &chk);
   }));
   G->chol = chk.used;
-  HT_TRY(capture_part(s, &G->rest, &G->n_rest, [&]() -> int {
+  G->device = chk.used && chk.device;
+  long long body = 0;
+  const int rc = capture_part(s, &G->rest, &G->n_rest, [&]() -> int {
     HT_TRY(phase_gram(P, s));
     HT_TRY(phase_eig(v, ctl, P, s));
-    return truncate_phase2(v, ctl, ws, o, s);
-  }));
+    HT_TRY(truncate_phase2(v, ctl, ws, o, s));
+    if (!G->device) return kOk;
+    return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s, &body);
+  });
+  if (rc != kOk && G->device && g_dev_fallback < 0) {
+    // conditional nodes unavailable: recapture with the host-side flag check
+    g_dev_fallback = 0;
+    if (G->orth) cudaGraphExecDestroy(G->orth);
+    G->orth = nullptr;
+    g_graph_flags.push_back(G->flag);
+    G->flag = nullptr;
+    if (G->ev) cudaEventDestroy(G->ev);
+    G->ev = nullptr;
+    cudaGetLastError();
+    return capture_truncation(v, ctl, ws, ws_bytes, o, s_caller, G);
+  }
+  HT_TRY(rc);
+  if (G->device) {
+    g_dev_fallback = 1;
+    G->n_rest -= body;  // the Householder body runs only when the branch is taken
+  }
   return kOk;
 }
 
@@ -1234,13 +1333,13 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
   }
   G->used = ++g_graph_clock;
   HT_CUDA_CHECK(cudaGraphLaunch(G->orth, s));
-  if (G->chol) HT_CUDA_CHECK(cudaEventRecord(G->ev, s));
+  if (G->chol && !G->device) HT_CUDA_CHECK(cudaEventRecord(G->ev, s));
   HT_CUDA_CHECK(cudaGraphLaunch(G->rest, s));
   prof_add_launches(G->n_orth + G->n_rest);
   ++g_graph_replays;
   ++G->replays;
   ran = true;
-  if (G->chol) {
+  if (G->chol && !G->device) {
     HT_CUDA_CHECK(cudaEventSynchronize(G->ev));
     failed = *(volatile int*)G->flag != 0;
   }
@@ -1499,7 +1598,17 @@ int ht_set_qr_mode(int mode) {
   return kOk;
 }
 
-int64_t ht_qr_fallback_count(void) { return g_qr_fallbacks; }
+int ht_graph_device_fallback(void) { return g_dev_fallback; }
+
+int64_t ht_qr_fallback_count(void) {
+  unsigned long long dev = 0;
+  if (g_dev_fallback == 1) {  // branches taken inside graph replays (synchronises the device)
+    cudaDeviceSynchronize();
+    if (cudaMemcpyFromSymbol(&dev, g_dev_qr_fallbacks, sizeof(dev)) != cudaSuccess) dev = 0;
+    cudaGetLastError();
+  }
+  return g_qr_fallbacks + (int64_t)dev;
+}
 
 int ht_set_graph_mode(int on) {
   if (on != 0 && on != 1) {

@@ -59,6 +59,9 @@ def test_graph_replay_routes_rank_deficient_input_to_householder(cuda_ok):
     f0 = htb.qr_fallback_count()
     outs = _truncs(htb, x, ctl, 4)
     assert htb.qr_fallback_count() - f0 == 4
+    # replays take the Householder branch on the device (conditional node), no host check
+    from paper_1708_03340_b200 import _lib
+    assert _lib.load().ht_graph_device_fallback() == 1
     ref = orc.truncate(to_host(x), orc.Ctl(max_rank=12))
     leaves, transfer, root = htb.truncate(x, ctl).to_numpy()
     for o in outs[1:]:

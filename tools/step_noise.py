@@ -28,7 +28,22 @@ def timed(n=50):
     return e0.elapsed_time(e1) / n
 
 
+print("arena", hex(x.arena.data_ptr()) if hasattr(x, "arena") else "?", "graphs", htb.graph_stats())
+htb.set_graph_mode(False)
+print("eager  ", [round(timed(), 3) for _ in range(3)])
+htb.set_graph_mode(True)
 print("plain  ", [round(timed(), 3) for _ in range(6)])
 with bench.ClockSampler(0):
     print("sampler", [round(timed(), 3) for _ in range(6)])
 print("plain  ", [round(timed(), 3) for _ in range(6)])
+
+import time  # noqa: E402
+
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+for _ in range(50):
+    htb.truncate(x, ctl)
+t1 = time.perf_counter()
+torch.cuda.synchronize()
+t2 = time.perf_counter()
+print("host enqueue ms/step %.3f, wall ms/step %.3f" % ((t1 - t0) * 20, (t2 - t0) * 20))
