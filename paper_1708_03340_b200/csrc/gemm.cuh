@@ -55,7 +55,7 @@ int gemm_grouped(std::vector<GemmDesc>& descs, cudaStream_t stream, const char* 
 int gemm_tiles(int M, int N);
 int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, const char* tag = "reduce_partials");
 
-constexpr int kMaxGemmDescs = 48;
+constexpr int kMaxGemmDescs = 64;  // one launch for a d=64 level's 2 x 32 son Gramians (params < 32 KB)
 constexpr int kGemmBM = 64, kGemmBN = 64, kGemmBK = 16;
 
 // Host helper: a plain (single-batch, KO=1) GEMM descriptor with all strides.
