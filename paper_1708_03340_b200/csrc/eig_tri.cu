@@ -227,7 +227,6 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
       // lower triangle of A22 is kept current: S[i][k] is row i for k <= i, column i
       // (odd pitch: conflict-free across rows) for k > i.
       {
-        double pv = 0.0;
         for (int i0 = 0; i0 < m; i0 += TT / kGroup) {
           const int i = i0 + tid / kGroup, part = tid % kGroup;
           double acc = 0.0, acc2 = 0.0;
@@ -244,19 +243,15 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
             if (k < m) acc = fma(k <= i ? rowi[k] : coli[(size_t)k * ap], v[k], acc);
           }
           acc = quad_sum(acc + acc2) * tj;
-          if (i < m && part == 0) {
-            pv += acc * v[i];
-            pb[i] = acc;
-          }
+          if (i < m && part == 0) pb[i] = acc;
         }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) pv += __shfl_xor_sync(0xffffffffu, pv, o);
-        if (lane == 0) red[warp][0] = pv;
       }
       __syncthreads();
-      double sv = red[lane & (TT / 32 - 1)][0];  // same shuffle tree in every warp: deterministic
+      // p.v summed by every warp from pb (same order in each: deterministic)
+      double sv = 0.0;
+      for (int i = lane; i < m; i += 32) sv = fma(pb[i], v[i], sv);
 #pragma unroll
-      for (int o = TT / 64; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
+      for (int o = 16; o > 0; o >>= 1) sv += __shfl_xor_sync(0xffffffffu, sv, o);
       const double c = -0.5 * tj * sv;                     // w = p + c v
       if (warp == 0) {
         // column j+1 (A22 column 0), then the next reflector from it
@@ -443,8 +438,93 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   if (flags[1]) return;  // the Jacobi kernel takes this node
   const int r = rsel;
 
-  // ---- 3. eigenvectors of T (twisted factorisation), one thread per vector ----------
-  for (int v = tid; v < r; v += TT) {
+  // ---- 3. eigenvectors of T (twisted factorisation) --------------------------------
+  // Fast path (2r <= K, matrices in shared memory): two adjacent lanes per vector run
+  // the stationary (D+, lane 0) and progressive (D-, lane 1, into the spare row r + v
+  // of Z) recurrences at the same time; gamma / twist, L = e / D+ and U = e / D- are
+  // then element-wise, and the two product chains run down and up from the twist
+  // concurrently.  Same quantities as the serial passes below.
+  const bool pair2 = !big && K >= 2 && 2 * r <= K;
+  if (pair2) {
+    const int v = tid >> 1, role = tid & 1;
+    const bool act = v < r;
+    const double sig = act ? lam[K - 1 - v] : 0.0;
+    double* z = Z + (size_t)(act ? v : 0) * zp;
+    double* w = Z + (size_t)(act ? r + v : 0) * zp;
+    const double pivmin = sh[2];
+    if (act && role == 0) {  // D+_k (guarded) into z[k]
+      double dp = dd[0] - sig;
+      if (fabs(dp) < pivmin) dp = -pivmin;
+      z[0] = dp;
+      for (int k = 0; k + 1 < K; ++k) {
+        dp = (dd[k + 1] - sig) - e2[k] / dp;
+        if (fabs(dp) < pivmin) dp = -pivmin;
+        z[k + 1] = dp;
+      }
+    } else if (act) {  // guarded D-_k into w[k]
+      double dm = dd[K - 1] - sig;
+      if (fabs(dm) < pivmin) dm = -pivmin;
+      w[K - 1] = dm;
+      for (int k = K - 2; k >= 0; --k) {
+        const double u = ee[k] / dm;
+        const double dmk = (dd[k] - sig) - ee[k] * u;
+        dm = fabs(dmk) < pivmin ? -pivmin : dmk;
+        w[k] = dm;
+      }
+    }
+    __syncthreads();
+    // gamma_k = D+_k + D-_k - (d_k - sig), twist = argmin |gamma| (ties: larger k, as
+    // the serial descending scan); lane 0 takes k < K/2, lane 1 the rest
+    int twist = K - 1;
+    double gmin = INFINITY;
+    if (act) {
+      const int h = K / 2;
+      const int klo = role ? h : 0, khi = role ? K - 1 : h;  // k in [klo, khi)
+      if (role) gmin = fabs(z[K - 1]);
+      for (int k = khi - 1; k >= klo; --k) {
+        const double u = ee[k] / w[k + 1];
+        const double dmk = (dd[k] - sig) - ee[k] * u;
+        const double g = fabs(z[k] + dmk - (dd[k] - sig));
+        if (g < gmin) {
+          gmin = g;
+          twist = k;
+        }
+      }
+    }
+    {
+      const double og = __shfl_xor_sync(0xffffffffu, gmin, 1);
+      const int ot = __shfl_xor_sync(0xffffffffu, twist, 1);
+      if (og < gmin || (og == gmin && ot > twist)) {
+        gmin = og;
+        twist = ot;
+      }
+    }
+    __syncthreads();  // every gamma is read before z is overwritten
+    double part = 0.0;
+    if (act && role == 0) {  // z_k = -L_k z_{k+1}, L_k = e_k / D+_k, downward from the twist
+      double prev = 1.0;
+      for (int k = twist - 1; k >= 0; --k) {
+        prev = -(ee[k] / z[k]) * prev;
+        z[k] = prev;
+        part = fma(prev, prev, part);
+      }
+    } else if (act) {  // z_{k+1} = -U_k z_k, U_k = e_k / D-_{k+1}, upward from the twist
+      double prev = 1.0;
+      z[twist] = 1.0;
+      for (int k = twist; k + 1 < K; ++k) {
+        prev = -(ee[k] / w[k + 1]) * prev;
+        z[k + 1] = prev;
+        part = fma(prev, prev, part);
+      }
+    }
+    const double nrm = 1.0 + part + __shfl_xor_sync(0xffffffffu, part, 1);
+    __syncthreads();
+    if (act) {
+      const double inv = 1.0 / sqrt(nrm);
+      for (int k = role ? twist : 0; k < (role ? K : twist); ++k) z[k] *= inv;
+    }
+  }
+  for (int v = tid; v < r && !pair2; v += TT) {
     const double sig = lam[K - 1 - v];  // descending order: vector v <-> eigenvalue K-1-v
     double* z = Z + v * zp;
     const double pivmin = sh[2];
