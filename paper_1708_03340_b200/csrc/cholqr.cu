@@ -10,6 +10,7 @@
 #include "prof.cuh"
 #include "ssgemm.cuh"
 #include "misc.cuh"
+#include "cond.cuh"
 
 namespace ht {
 namespace {
@@ -643,49 +644,59 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   g.clear();
   sd.clear();
   // pass 2 (skipped on the device unless need2): W2 = Q1^T Q1, R2 = chol(W2),
-  // Q = Q1 R2^{-1}, R = R2 R1
-  for (size_t p = 0; p < cs.size(); ++p) {
-    const CholQr& c = cs[p];
-    if (c.q.K <= kCholInPlaceK) gram(g, r, c, c.q.Q, c.q.q_r, c.q.q_c, c.q.q_node, need2 + p);
-    else gram(g, r, c, c.Q1, c.q.K, 1, (long long)c.q.m * c.q.K, need2 + p);
-  }
-  HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_gram", false));
-  HT_TRY(reduce_partials(r, s));
-  for (size_t p = 0; p < cs.size(); ++p) {
-    const CholQr& c = cs[p];
-    CholDesc d{};
-    d.W = c.W; d.Rf = c.R2; d.Ri = c.Ri;
-    d.K = c.q.K; d.nodes = c.q.nodes;
-    d.check_identity = 1;
-    d.active = need2 + p;
-    ch.push_back(d);
-  }
-  HT_TRY(launch_chol(ch, fail, s, "cholqr2_factor"));
-  g.clear();
-  for (size_t p = 0; p < cs.size(); ++p) {
-    const CholQr& c = cs[p];
-    const int K = c.q.K, m = c.q.m;
-    if (K <= kCholInPlaceK) {  // Q <- Q R2^{-1} in place (each CTA owns whole rows)
-      SsDesc d = ss_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
-      d.jobs = c.q.nodes; d.x_job = c.q.q_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
-      d.s_tri = 2;
-      d.active = need2 + p;
-      sd.push_back(d);
-    } else {
-      GemmDesc d = gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
-      d.nb1 = c.q.nodes; d.a_b1 = (long long)m * K; d.b_b1 = (long long)K * K;
-      d.c_b1 = c.q.q_node;
-      d.active = need2 + p;
-      g.push_back(d);
+  // Q = Q1 R2^{-1}, R = R2 R1.  Inside the library's own graph captures the five
+  // launches sit in an IF node taken only when some need2 flag is set; elsewhere they
+  // are enqueued and exit on their device flags.
+  auto pass2 = [&](cudaStream_t s) -> int {
+    for (size_t p = 0; p < cs.size(); ++p) {
+      const CholQr& c = cs[p];
+      if (c.q.K <= kCholInPlaceK) gram(g, r, c, c.q.Q, c.q.q_r, c.q.q_c, c.q.q_node, need2 + p);
+      else gram(g, r, c, c.Q1, c.q.K, 1, (long long)c.q.m * c.q.K, need2 + p);
     }
-    GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
-    e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
-    e.active = need2 + p;
-    g.push_back(e);
+    HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_gram", false));
+    HT_TRY(reduce_partials(r, s));
+    for (size_t p = 0; p < cs.size(); ++p) {
+      const CholQr& c = cs[p];
+      CholDesc d{};
+      d.W = c.W; d.Rf = c.R2; d.Ri = c.Ri;
+      d.K = c.q.K; d.nodes = c.q.nodes;
+      d.check_identity = 1;
+      d.active = need2 + p;
+      ch.push_back(d);
+    }
+    HT_TRY(launch_chol(ch, fail, s, "cholqr2_factor"));
+    g.clear();
+    for (size_t p = 0; p < cs.size(); ++p) {
+      const CholQr& c = cs[p];
+      const int K = c.q.K, m = c.q.m;
+      if (K <= kCholInPlaceK) {  // Q <- Q R2^{-1} in place (each CTA owns whole rows)
+        SsDesc d = ss_desc(c.q.Q, c.q.q_r, c.q.q_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+        d.jobs = c.q.nodes; d.x_job = c.q.q_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+        d.s_tri = 2;
+        d.active = need2 + p;
+        sd.push_back(d);
+      } else {
+        GemmDesc d = gemm_desc(c.Q1, K, 1, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+        d.nb1 = c.q.nodes; d.a_b1 = (long long)m * K; d.b_b1 = (long long)K * K;
+        d.c_b1 = c.q.q_node;
+        d.active = need2 + p;
+        g.push_back(d);
+      }
+      GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
+      e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
+      e.active = need2 + p;
+      g.push_back(e);
+    }
+    HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
+    HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
+    return kOk;
+  };
+  if (g_own_capture && g_cond_nodes != 0) {
+    const int rc = capture_if_any(s, need2, (int)cs.size(), nullptr, pass2);
+    if (rc != kOk) g_cond_nodes = 0;  // the capture fails; later captures stay unconditional
+    return rc;
   }
-  HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
-  HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
-  return kOk;
+  return pass2(s);
 }
 
 // ---------------------------------------------------------------------------

@@ -13,6 +13,8 @@
 #include <vector>
 
 #include "cholqr.cuh"
+#include "cond.cuh"
+
 #include "qr_wide.cuh"
 #include "common.cuh"
 #include "eig.cuh"
@@ -22,6 +24,84 @@
 #include "misc.cuh"
 #include "qr.cuh"
 #include "prof.cuh"
+
+namespace ht {
+int g_cond_nodes = -1;
+long long g_cond_body_launches = 0;
+thread_local bool g_own_capture = false;
+
+bool stream_capturing(cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(s, &cs) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return cs == cudaStreamCaptureStatusActive;
+}
+
+namespace {
+__global__ void cond_any_kernel(cudaGraphConditionalHandle h, const int* flags, int n, unsigned long long* taken) {
+  unsigned v = 0;
+  for (int i = 0; i < n; ++i) v |= flags[i] != 0 ? 1u : 0u;
+  if (v && taken) atomicAdd(taken, 1ull);
+  cudaGraphSetConditional(h, v);
+}
+
+cudaStream_t body_stream() {  // IF bodies are captured on their own stream (per device)
+  static std::map<int, cudaStream_t> streams;
+  static std::mutex mu;
+  std::lock_guard<std::mutex> lk(mu);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = streams.find(dev);
+  if (it != streams.end()) return it->second;
+  cudaStream_t cs = nullptr;
+  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  streams[dev] = cs;
+  return cs;
+}
+}  // namespace
+
+int capture_if_any(cudaStream_t s, const int* flags, int n, unsigned long long* taken,
+                   const std::function<int(cudaStream_t)>& body) {
+  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+  cudaGraph_t graph = nullptr;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t nd = 0;
+  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
+  cudaGraphConditionalHandle h;
+  HT_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
+  cond_any_kernel<<<1, 1, 0, s>>>(h, flags, n, taken);
+  HT_LAUNCH_CHECK();
+  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
+  cudaGraphNodeParams cp = {};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeIf;
+  cp.conditional.size = 1;
+  cudaGraphNode_t node;
+  HT_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, nd, &cp));
+  HT_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
+  cudaStream_t s2 = body_stream();
+  if (!s2) {
+    set_error("cannot create the IF-body capture stream");
+    return kErrCuda;
+  }
+  const long long l0 = prof_launches();
+  HT_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
+                                              cudaStreamCaptureModeThreadLocal));
+  const int rc = body(s2);
+  cudaGraph_t out = nullptr;
+  const cudaError_t ce = cudaStreamEndCapture(s2, &out);
+  g_cond_body_launches += prof_launches() - l0;
+  if (rc != kOk) return rc;
+  if (ce != cudaSuccess) {
+    set_error(std::string("IF-body capture: ") + cudaGetErrorString(ce));
+    return kErrCuda;
+  }
+  return kOk;
+}
+}  // namespace ht
 
 namespace ht {
 
@@ -1130,9 +1210,11 @@ void destroy_graph(TruncGraph* g) {
 // Capture one part of the truncation on `s`; on error the capture is ended and discarded.
 template <class F>
 int capture_part(cudaStream_t s, cudaGraphExec_t* exec, long long* launches, F&& body) {
-  const long long l0 = prof_launches();
+  const long long l0 = prof_launches(), b0 = g_cond_body_launches;
   HT_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  g_own_capture = true;
   int rc = body();
+  g_own_capture = false;
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(s, &g);
   if (rc == kOk && ce != cudaSuccess) {
@@ -1148,9 +1230,11 @@ int capture_part(cudaStream_t s, cudaGraphExec_t* exec, long long* launches, F&&
   }
   if (g) cudaGraphDestroy(g);
   cudaGetLastError();
-  // the launches recorded during capture did not run; replays add them back
-  *launches = prof_launches() - l0;
-  prof_add_launches(-*launches);
+  // the launches recorded during capture did not run; replays add them back (except
+  // those inside IF bodies, which run only when their branch is taken)
+  const long long all = prof_launches() - l0;
+  prof_add_launches(-all);
+  *launches = all - (g_cond_body_launches - b0);
   return rc;
 }
 
@@ -1173,69 +1257,16 @@ cudaStream_t capture_stream() {
 // Householder path, so a replay needs no host round trip.  Taken branches are counted
 // on the device (ht_qr_fallback_count adds them).
 __device__ unsigned long long g_dev_qr_fallbacks = 0;
-int g_dev_fallback = -1;  // -1 untried, 1 works, 0 unavailable (host check instead)
 
-__global__ void qr_fallback_cond_kernel(cudaGraphConditionalHandle h, const int* fail) {
-  const unsigned v = *fail != 0 ? 1u : 0u;
-  if (v) atomicAdd(&g_dev_qr_fallbacks, 1ull);
-  cudaGraphSetConditional(h, v);
-}
-
-cudaStream_t capture_stream2() {
-  static std::map<int, cudaStream_t> streams;
-  int dev = 0;
-  cudaGetDevice(&dev);
-  auto it = streams.find(dev);
-  if (it != streams.end()) return it->second;
-  cudaStream_t cs = nullptr;
-  if (cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
-  streams[dev] = cs;
-  return cs;
-}
-
-// Appended to the REST capture on `s`: condition kernel + IF node (body captured on a
-// second stream).  `body_launches`: kernels recorded in the body (they run only when
-// the branch is taken).
 int capture_device_fallback(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
-                            const int* fail, cudaStream_t s, long long* body_launches) {
-  cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
-  cudaGraph_t graph = nullptr;
-  const cudaGraphNode_t* deps = nullptr;
-  size_t nd = 0;
-  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
-  cudaGraphConditionalHandle h;
-  HT_CUDA_CHECK(cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault));
-  qr_fallback_cond_kernel<<<1, 1, 0, s>>>(h, fail);
-  HT_LAUNCH_CHECK();
-  HT_CUDA_CHECK(cudaStreamGetCaptureInfo(s, &st, nullptr, &graph, &deps, &nd));
-  cudaGraphNodeParams cp = {};
-  cp.type = cudaGraphNodeTypeConditional;
-  cp.conditional.handle = h;
-  cp.conditional.type = cudaGraphCondTypeIf;
-  cp.conditional.size = 1;
-  cudaGraphNode_t node;
-  HT_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, nd, &cp));
-  HT_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
-  cudaStream_t s2 = capture_stream2();
-  if (!s2) {
-    set_error("cannot create the second graph-capture stream");
-    return kErrCuda;
-  }
-  const long long l0 = prof_launches();
-  HT_CUDA_CHECK(cudaStreamBeginCaptureToGraph(s2, cp.conditional.phGraph_out[0], nullptr, nullptr, 0,
-                                              cudaStreamCaptureModeThreadLocal));
-  TruncPlan P2;
-  int rc = truncate_phase1(v, ctl, ws, ws_bytes, P2, s2, nullptr, true);
-  if (rc == kOk) rc = truncate_phase2(v, ctl, ws, o, s2);
-  cudaGraph_t body = nullptr;
-  const cudaError_t ce = cudaStreamEndCapture(s2, &body);
-  *body_launches = prof_launches() - l0;
-  if (rc != kOk) return rc;
-  if (ce != cudaSuccess) {
-    set_error(std::string("fallback body capture: ") + cudaGetErrorString(ce));
-    return kErrCuda;
-  }
-  return kOk;
+                            const int* fail, cudaStream_t s) {
+  unsigned long long* taken = nullptr;
+  HT_CUDA_CHECK(cudaGetSymbolAddress((void**)&taken, g_dev_qr_fallbacks));
+  return capture_if_any(s, fail, 1, taken, [&](cudaStream_t s2) -> int {
+    TruncPlan P2;
+    HT_TRY(truncate_phase1(v, ctl, ws, ws_bytes, P2, s2, nullptr, true));
+    return truncate_phase2(v, ctl, ws, o, s2);
+  });
 }
 
 int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
@@ -1257,7 +1288,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   OrthCheck chk;
   chk.host = G->flag;
   chk.capture = true;
-  chk.device = g_dev_fallback != 0;
+  chk.device = g_cond_nodes != 0;
   HT_TRY(capture_part(s, &G->orth, &G->n_orth, [&]() -> int {
     HT_TRY(plan_truncate(v, P, ws));
     HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
@@ -1265,17 +1296,17 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   }));
   G->chol = chk.used;
   G->device = chk.used && chk.device;
-  long long body = 0;
   const int rc = capture_part(s, &G->rest, &G->n_rest, [&]() -> int {
     HT_TRY(phase_gram(P, s));
     HT_TRY(phase_eig(v, ctl, P, s));
     HT_TRY(truncate_phase2(v, ctl, ws, o, s));
     if (!G->device) return kOk;
-    return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s, &body);
+    return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s);
   });
-  if (rc != kOk && G->device && g_dev_fallback < 0) {
-    // conditional nodes unavailable: recapture with the host-side flag check
-    g_dev_fallback = 0;
+  if (rc != kOk && g_cond_nodes < 0) {
+    // conditional nodes unavailable: recapture with eager second passes and the
+    // host-side flag check
+    g_cond_nodes = 0;
     if (G->orth) cudaGraphExecDestroy(G->orth);
     G->orth = nullptr;
     g_graph_flags.push_back(G->flag);
@@ -1286,10 +1317,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
     return capture_truncation(v, ctl, ws, ws_bytes, o, s_caller, G);
   }
   HT_TRY(rc);
-  if (G->device) {
-    g_dev_fallback = 1;
-    G->n_rest -= body;  // the Householder body runs only when the branch is taken
-  }
+  if (G->device) g_cond_nodes = 1;
   return kOk;
 }
 
@@ -1598,11 +1626,11 @@ int ht_set_qr_mode(int mode) {
   return kOk;
 }
 
-int ht_graph_device_fallback(void) { return g_dev_fallback; }
+int ht_graph_device_fallback(void) { return g_cond_nodes; }
 
 int64_t ht_qr_fallback_count(void) {
   unsigned long long dev = 0;
-  if (g_dev_fallback == 1) {  // branches taken inside graph replays (synchronises the device)
+  if (g_cond_nodes == 1) {  // branches taken inside graph replays (synchronises the device)
     cudaDeviceSynchronize();
     if (cudaMemcpyFromSymbol(&dev, g_dev_qr_fallbacks, sizeof(dev)) != cudaSuccess) dev = 0;
     cudaGetLastError();
