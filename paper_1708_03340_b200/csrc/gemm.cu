@@ -881,6 +881,10 @@ struct CfgInfo {
 constexpr CfgInfo kCfg[kNumCfg] = {{64, 64}, {128, 104}, {104, 128}, {128, 56}, {56, 128}, {64, 104}, {104, 64}};
 
 Cfg pick_cfg(const GemmDesc& d) {
+  // a handful of rank-sized products (root / top-level GEMMs): latency-bound, so spread
+  // each over 64 x 64 tiles (four CTAs for 100 x 100) rather than one big tile
+  if (d.M <= 128 && d.N <= 128 && (long long)d.K * std::max(d.KO, 1) <= 256 && (long long)d.nb1 * d.nb2 <= 4)
+    return kC64;
   // half-height tiles only pay off for short reductions (the rank-sized K of the mode
   // products and Q = A R^-1); long (split-K) reductions keep the full tiles
   const bool half = g_half_tiles && (long long)d.K * std::max(d.KO, 1) <= 512;
