@@ -345,10 +345,19 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
     double* C = g.C + job * g.c_job;
     const bool vec = b.vec[di];
     __syncthreads();  // the previous segment is done with S (and the barriers are initialised)
-    for (int e = tid; e < KT * SBK * NP; e += SS2_T) {
-      const int k = e / NP, n = e - k * NP;
-      const bool ok = k < K && n < N;
-      cp8z(Ss + k * PS + n, ok ? S + k * g.s_k + n * g.s_n : S, ok);
+    if (g.s_n == 1 && !(g.s_k & 1) && !(((uintptr_t)S) & 15)) {
+      // rows of S contiguous along n: 16-byte copies of (n, n + 1) pairs
+      for (int e = tid; e < KT * SBK * (NP / 2); e += SS2_T) {
+        const int k = e / (NP / 2), n = 2 * (e - k * (NP / 2));
+        const int nv = k < K ? max(0, min(2, N - n)) : 0;
+        cp16z(Ss + k * PS + n, nv ? S + (long long)k * g.s_k + n : S, 8 * nv);
+      }
+    } else {
+      for (int e = tid; e < KT * SBK * NP; e += SS2_T) {
+        const int k = e / NP, n = e - k * NP;
+        const bool ok = k < K && n < N;
+        cp8z(Ss + k * PS + n, ok ? S + k * g.s_k + n * g.s_n : S, ok);
+      }
     }
     asm volatile("cp.async.wait_all;\n" ::: "memory");
     __syncthreads();
