@@ -34,25 +34,29 @@ __device__ __forceinline__ int find(const B& b) {
   return di;
 }
 
+// One warp per output row (i0, i1): the row's A segment, scaled C segment and zeros
+// are written with coalesced stores; index arithmetic once per row, not per element.
 __global__ void embed_kernel(const __grid_constant__ EmbedBatch b) {
   const int di = find(b);
   const EmbedDesc& e = b.d[di];
-  const long long total = (long long)e.D0 * e.D1 * e.D2;
-  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
-  for (long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x; x < total; x += stride) {
-    const int i2 = (int)(x % e.D2);
-    const long long r = x / e.D2;
-    const int i1 = (int)(r % e.D1);
-    const int i0 = (int)(r / e.D1);
-    double v = 0.0;
-    if (i0 < e.a0 && i1 < e.a1 && i2 < e.a2) {
-      v = e.A[((long long)i0 * e.a1 + i1) * e.a2 + i2];
-    } else {
-      const int j0 = i0 - e.o0, j1 = i1 - e.o1, j2 = i2 - e.o2;
-      if (j0 >= 0 && j1 >= 0 && j2 >= 0 && j0 < e.c0 && j1 < e.c1 && j2 < e.c2)
-        v = e.alpha_c * e.C[((long long)j0 * e.c1 + j1) * e.c2 + j2];
+  const long long rows = (long long)e.D0 * e.D1;
+  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
+  const long long nw = (long long)(b.begin[di + 1] - b.begin[di]) * wpb;
+  for (long long r = (long long)(blockIdx.x - b.begin[di]) * wpb + (threadIdx.x >> 5); r < rows; r += nw) {
+    const int i0 = (int)(r / e.D1), i1 = (int)(r - (long long)i0 * e.D1);
+    double* o = e.out + r * e.D2;
+    const bool ina = i0 < e.a0 && i1 < e.a1;
+    const double* arow = e.A + ((long long)i0 * e.a1 + i1) * e.a2;
+    const int j0 = i0 - e.o0, j1 = i1 - e.o1;
+    const bool inc = j0 >= 0 && j1 >= 0 && j0 < e.c0 && j1 < e.c1;
+    const double* crow = e.C + ((long long)j0 * e.c1 + j1) * e.c2;
+    for (int i2 = lane; i2 < e.D2; i2 += 32) {
+      double v = 0.0;
+      const int j2 = i2 - e.o2;
+      if (ina && i2 < e.a2) v = arow[i2];
+      else if (inc && j2 >= 0 && j2 < e.c2) v = e.alpha_c * crow[j2];
+      o[i2] = v;
     }
-    e.out[x] = v;
   }
 }
 
@@ -119,12 +123,14 @@ int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream) {
     EmbedBatch b;
     b.count = 0;
     int blocks = 0;
+    double bytes = 0.0;
     while (i < descs.size() && b.count < MAXD) {
       const EmbedDesc& d = descs[i++];
       const long long total = (long long)d.D0 * d.D1 * d.D2;
       if (total == 0) continue;
       b.begin[b.count] = blocks;
-      blocks += blocks_for(total);
+      blocks += (int)std::max<long long>(1, std::min<long long>(ceil_div((long long)d.D0 * d.D1, 8), 2048));
+      bytes += 8.0 * ((double)total + (double)d.a0 * d.a1 * d.a2 + (double)d.c0 * d.c1 * d.c2);
       b.d[b.count++] = d;
     }
     if (!b.count) continue;
@@ -132,7 +138,7 @@ int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream) {
     ProfToken tok = prof_begin(stream);
     embed_kernel<<<blocks, 256, 0, stream>>>(b);
     HT_LAUNCH_CHECK();
-    prof_end(tok, "embed", stream, 0.0, 0.0);
+    prof_end(tok, "embed", stream, 0.0, bytes);
   }
   return kOk;
 }
