@@ -42,6 +42,8 @@ __global__ void embed_kernel(const __grid_constant__ EmbedBatch b) {
   const long long rows = (long long)e.D0 * e.D1;
   const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
   const long long nw = (long long)(b.begin[di + 1] - b.begin[di]) * wpb;
+  const bool vec = !((e.D2 | e.a2 | e.c2 | e.o2) & 1) &&
+                   !((((uintptr_t)e.out) | ((uintptr_t)e.A) | ((uintptr_t)e.C)) & 15);
   for (long long r = (long long)(blockIdx.x - b.begin[di]) * wpb + (threadIdx.x >> 5); r < rows; r += nw) {
     const int i0 = (int)(r / e.D1), i1 = (int)(r - (long long)i0 * e.D1);
     double* o = e.out + r * e.D2;
@@ -50,6 +52,20 @@ __global__ void embed_kernel(const __grid_constant__ EmbedBatch b) {
     const int j0 = i0 - e.o0, j1 = i1 - e.o1;
     const bool inc = j0 >= 0 && j1 >= 0 && j0 < e.c0 && j1 < e.c1;
     const double* crow = e.C + ((long long)j0 * e.c1 + j1) * e.c2;
+    if (vec) {  // even extents and offsets: 16-byte pairs never straddle a segment edge
+      for (int p = lane; 2 * p < e.D2; p += 32) {
+        const int i2 = 2 * p, j2 = i2 - e.o2;
+        double2 v = make_double2(0.0, 0.0);
+        if (ina && i2 < e.a2) {
+          v = reinterpret_cast<const double2*>(arow)[p];
+        } else if (inc && j2 >= 0 && j2 < e.c2) {
+          const double2 c = reinterpret_cast<const double2*>(crow)[j2 >> 1];
+          v = make_double2(e.alpha_c * c.x, e.alpha_c * c.y);
+        }
+        reinterpret_cast<double2*>(o)[p] = v;
+      }
+      continue;
+    }
     for (int i2 = lane; i2 < e.D2; i2 += 32) {
       double v = 0.0;
       const int j2 = i2 - e.o2;
