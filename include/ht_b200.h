@@ -111,11 +111,24 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
                 const ht_tensor* out, ht_stream_t stream);
 /* CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on;
  * env HT_GRAPHS=0 turns it off at start-up).  The second ht_truncate call with the
- * same shapes, device pointers, control and kernel policies captures the truncation
- * as two graphs (ORTH; GRAM + EIG + PROJECT) and later calls replay them.  Results
- * are identical to the eager launches (same kernels, same arguments). */
+ * same shapes, control and kernel policies captures the truncation as two graphs
+ * (ORTH; GRAM + EIG + PROJECT) and later calls replay them.  Replays do not depend
+ * on the buffers' addresses: a call whose input / output / workspace moved relocates
+ * a cached graph of the same shapes (argument words shifted by each buffer's move)
+ * instead of capturing again.  Results are identical to the eager launches (same
+ * kernels, same arguments). */
 int ht_set_graph_mode(int on);
 int ht_graph_stats(int64_t* captures, int64_t* replays);
+int64_t ht_graph_relocations(void);
+
+/* Sticky error word of the queued (not host-checked) truncations on the current
+ * device: fixed-rank ht_truncate, graph replays and the sharded phases OR their
+ * eigensolver status into it.  Reads it behind `stream` (synchronising that stream),
+ * optionally clears it, and returns HT_ERR_NOT_SYMMETRIC (kernels.py:47-50) or
+ * HT_ERR_NONCONVERGED (non-finite Gramian / no convergence) when set.  The Python
+ * layer calls it at every host synchronisation point (to_numpy, inner_product,
+ * evaluate_entry, synchronize). */
+int ht_status(int32_t clear, int32_t* status, ht_stream_t stream);
 
 /* Sharded truncation (the paper's tree-parallel protocol, one subtree per GPU):
  * runs one phase restricted to the nodes with mask[t] != 0 (host array [2d-1]).

@@ -28,6 +28,8 @@ from .arith import (
     set_eig_mode,
     set_graph_mode,
     graph_stats,
+    graph_relocations,
+    synchronize,
     set_qr_mode,
     subtract,
     truncate,
@@ -83,6 +85,8 @@ __all__ = [
     "set_eig_mode",
     "set_graph_mode",
     "graph_stats",
+    "graph_relocations",
+    "synchronize",
     "set_qr_mode",
     "storage_size",
     "subtract",

@@ -38,7 +38,7 @@ EXPORTS = (
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
     "ht_launch_count", "ht_profile_enable", "ht_profile_report", "ht_profile_log",
     "ht_truncate_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_qr_fallback_count", "ht_set_eig_mode",
-    "ht_set_graph_mode", "ht_graph_stats", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
+    "ht_set_graph_mode", "ht_graph_stats", "ht_graph_relocations", "ht_status", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
 )
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -111,6 +111,8 @@ def _declare(lib):
         "ht_evaluate_entries": ([t, _vp, ctypes.c_int64, _vp, _vp], ctypes.c_int),
         "ht_evaluate_weighted": ([t, _vp, _vp, ctypes.c_int64, _vp, _vp], ctypes.c_int),
         "ht_graph_stats": ([_i64p, _i64p], ctypes.c_int),
+        "ht_graph_relocations": ([], ctypes.c_int64),
+        "ht_status": ([ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
         "ht_graph_device_fallback": ([], ctypes.c_int),
         "ht_profile_enable": ([ctypes.c_int], ctypes.c_int),
         "ht_profile_report": ([ctypes.c_char_p, ctypes.c_size_t], ctypes.c_int),
@@ -156,6 +158,11 @@ def check(rc: int, what: str = "") -> None:
     if rc == HT_ERR_UNSUPPORTED:
         raise NotImplementedError(msg)
     raise RuntimeError(msg)
+
+
+def check_status(stream=None) -> None:
+    """Raise the error a queued truncation left in the sticky status word (and clear it)."""
+    check(load().ht_status(1, None, stream_handle(stream)), "queued truncation")
 
 
 def profile_report() -> dict:

@@ -153,6 +153,7 @@ def inner_product(a: HTensor, c: HTensor) -> float:
     host = ctypes.c_double(0.0)
     _lib.check(lib.ht_inner_product(a._c(), c._c(), ws.data_ptr(), ws.numel(), res.data_ptr(),
                                     ctypes.byref(host), _stream()), "inner_product")
+    _lib.check_status()  # host synchronisation point: errors of queued truncations surface here
     return float(host.value)
 
 
@@ -353,13 +354,26 @@ def evaluate_entry(a: HTensor, index) -> float:
     index = tuple(int(i) for i in index)
     if len(index) != a.tree.d or any(not 0 <= i < n for i, n in zip(index, a.shape)):
         raise IndexError(f"index {index} out of bounds for shape {a.shape}")
-    return float(evaluate_entries(a, [index])[0].item())
+    v = float(evaluate_entries(a, [index])[0].item())
+    _lib.check_status()
+    return v
+
+
+def synchronize() -> None:
+    """Wait for the queued work of the current stream and raise any error a queued
+    truncation recorded (fixed-rank truncations do not read their status back)."""
+    _lib.check_status()
 
 
 def set_graph_mode(on: bool) -> None:
     """CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on).
     Same kernels and arguments as the eager launches, so results are identical."""
     _lib.check(_lib.load().ht_set_graph_mode(1 if on else 0), "set_graph_mode")
+
+
+def graph_relocations() -> int:
+    """How many cached truncation graphs were relocated to new buffer addresses."""
+    return int(_lib.load().ht_graph_relocations())
 
 
 def graph_stats() -> tuple:
@@ -406,4 +420,4 @@ def _check_all():
 
 __all__ = ["TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
            "orthogonalize", "compute_bhat", "truncate", "hierarchical_singular_values", "apply_operator",
-           "gemm", "leaf_map"]
+           "gemm", "leaf_map", "synchronize"]

@@ -24,6 +24,7 @@
 #include "misc.cuh"
 #include "qr.cuh"
 #include "prof.cuh"
+#include "reloc.cuh"
 
 namespace ht {
 int g_cond_nodes = -1;
@@ -81,6 +82,7 @@ int capture_if_any(cudaStream_t s, const int* flags, int n, unsigned long long* 
   cp.conditional.size = 1;
   cudaGraphNode_t node;
   HT_CUDA_CHECK(cudaGraphAddNode(&node, graph, deps, nd, &cp));
+  if (g_cond_sink) g_cond_sink->push_back(node);
   HT_CUDA_CHECK(cudaStreamUpdateCaptureDependencies(s, &node, 1, cudaStreamSetCaptureDependencies));
   cudaStream_t s2 = body_stream();
   if (!s2) {
@@ -93,6 +95,7 @@ int capture_if_any(cudaStream_t s, const int* flags, int n, unsigned long long* 
   const int rc = body(s2);
   cudaGraph_t out = nullptr;
   const cudaError_t ce = cudaStreamEndCapture(s2, &out);
+  if (g_body_sink && ce == cudaSuccess) g_body_sink->push_back(cp.conditional.phGraph_out[0]);
   g_cond_body_launches += prof_launches() - l0;
   if (rc != kOk) return rc;
   if (ce != cudaSuccess) {
@@ -817,7 +820,31 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   return kOk;
 }
 
+size_t truncate_ws_bytes_uncached(const View& x);
+
+// Workspace sizing replays the whole plan in measure mode (~0.1 ms of host time at
+// d=64); every truncation queries it twice, so it is cached per shape.
 size_t truncate_ws_bytes(const View& x) {
+  static std::mutex mu;
+  static std::map<std::vector<long long>, size_t> cache;
+  std::vector<long long> key{(long long)x.T->d, (long long)x.orth};
+  for (int t = 0; t < x.T->nn; ++t) {
+    key.push_back(x.n[t]);
+    key.push_back(x.k[t]);
+  }
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const size_t b = truncate_ws_bytes_uncached(x);
+  std::lock_guard<std::mutex> lk(mu);
+  if (cache.size() > 256) cache.clear();
+  cache[key] = b;
+  return b;
+}
+
+size_t truncate_ws_bytes_uncached(const View& x) {
   TruncPlan P;
   plan_truncate(x, P, nullptr);
   Arena sc = P.scratch;
@@ -870,7 +897,17 @@ int phase_gram(TruncPlan& P, cudaStream_t s) {
 }
 
 // batched eigendecomposition + select_rank of the (masked) non-root nodes
-int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t s) {
+// Sticky error word (per device): truncations whose status is not read back on the
+// host (fixed-rank ht_truncate, graph replays, the sharded phases) OR their eigensolver
+// status into it; ht_status() reads and clears it at the caller's next host sync.
+__device__ int g_sticky_status = 0;
+
+__global__ void sticky_or_kernel(const int* status) {
+  const int v = *status;
+  if (v) atomicOr(&g_sticky_status, v);
+}
+
+int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t s, bool sticky = false) {
   const Tree& T = *x.T;
   std::vector<EigProblem> eps;
   for (int t = 1; t < T.nn; ++t) {
@@ -906,18 +943,23 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     }
     eps.push_back(e);
   }
-  return eig_batched(eps, s);
+  HT_TRY(eig_batched(eps, s));
+  if (sticky) {
+    sticky_or_kernel<<<1, 1, 0, s>>>(P.status);
+    HT_LAUNCH_CHECK();
+  }
+  return kOk;
 }
 
 int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, TruncPlan& P, cudaStream_t s,
-                    OrthCheck* deferred = nullptr, bool force_hh = false) {
+                    OrthCheck* deferred = nullptr, bool force_hh = false, bool sticky = false) {
   HT_TRY(check_ctl(ctl));
   HT_TRY(check_ws(x, ws, ws_bytes));
   HT_TRY(plan_truncate(x, P, ws));
   HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
   HT_TRY(phase_orth(x, P, s, deferred, force_hh));
   HT_TRY(phase_gram(P, s));
-  return phase_eig(x, ctl, P, s);
+  return phase_eig(x, ctl, P, s, sticky);
 }
 
 std::vector<long long> static_ranks(const View& x, const ht_trunc_ctl* ctl, bool& ok) {
@@ -1121,16 +1163,27 @@ int check_compatible(const View& a, const View& c) {
 
 // ---------------------------------------------------------------------------
 // CUDA-graph replay of the fixed-rank truncation.  A truncation is ~90 launches whose
-// arguments depend only on the shapes, the device pointers, the control and the
-// kernel policies; the second call with the same key captures it as two graphs --
-// ORTH (ending with the copy of the Cholesky-QR red flag into the graph's own pinned
-// word) and GRAM + EIG + PROJECT -- and every later call replays them: two launches,
-// no per-kernel host cost, and the host waits only on the ORTH graph's completion
-// (as the eager path does) before reading the flag.
+// arguments depend only on the shapes, the device addresses, the control and the
+// kernel policies.  The second call with the same shapes captures it as two graphs --
+// ORTH and GRAM + EIG + PROJECT (with the device-side Householder fallback as a
+// conditional node) -- and later calls replay them: two launches, no per-kernel host
+// cost.  Replays do not depend on the caller's addresses: a call whose input, output
+// or workspace moved (caching allocators, rotating pipeline buffers) relocates a
+// cached graph of the same shapes (reloc.cuh: every argument word that pointed into
+// the captured input / output / workspace ranges is shifted by that buffer's move)
+// instead of capturing again.  Address combinations seen repeatedly get their own
+// graph (up to kMaxPerShape per shape), so alternating buffers replay without any
+// per-call relocation.
 // ---------------------------------------------------------------------------
 struct TruncGraph {
-  std::vector<long long> key;
+  std::vector<long long> skey;             // shapes, control, policies (no addresses)
+  std::vector<uintptr_t> cap_in, cap_out;  // node addresses at capture
+  uintptr_t cap_ws = 0;
+  std::vector<uintptr_t> cur_in, cur_out;  // addresses the executable graphs use now
+  uintptr_t cur_ws = 0;
+  cudaGraph_t g_orth = nullptr, g_rest = nullptr;
   cudaGraphExec_t orth = nullptr, rest = nullptr;
+  RelocTable r_orth, r_rest;
   int* flag = nullptr;  // pinned
   cudaEvent_t ev = nullptr;
   bool chol = false;    // the ORTH graph ran Cholesky-QR and wrote the flag
@@ -1138,19 +1191,22 @@ struct TruncGraph {
   long long n_orth = 0, n_rest = 0;
   unsigned long long used = 0;
   long long replays = 0;
+  bool relocatable() const { return r_orth.ok && r_rest.ok; }
+};
+
+struct Addrs {
+  std::vector<uintptr_t> in, out;
+  uintptr_t ws = 0;
 };
 
 std::mutex g_graph_mu;
 std::vector<TruncGraph*> g_graphs;
-std::map<std::vector<long long>, int> g_graph_seen;
+std::map<std::vector<long long>, int> g_graph_seen;  // shape keys and address keys seen
 unsigned long long g_graph_clock = 0;
 int g_graph_mode = -1;  // -1: from HT_GRAPHS (default on)
-long long g_graph_captures = 0, g_graph_replays = 0;
-// graphs evicted after fewer than two replays: the caller's buffers rotate faster than
-// the cache holds them, so capturing only adds host work -- stop capturing new ones
-long long g_graph_waste = 0;
+long long g_graph_captures = 0, g_graph_replays = 0, g_graph_relocations = 0;
 constexpr size_t kMaxGraphs = 16;
-constexpr long long kMaxGraphWaste = 8;
+constexpr size_t kMaxPerShape = 3;
 
 bool graphs_on() {
   if (g_graph_mode < 0) {
@@ -1160,27 +1216,56 @@ bool graphs_on() {
   return g_graph_mode == 1;
 }
 
-std::vector<long long> graph_key(const View& v, const View& o, const ht_trunc_ctl* ctl, const void* ws,
-                                 size_t ws_bytes) {
+std::vector<long long> shape_key(const View& v, const View& o, const ht_trunc_ctl* ctl, size_t ws_bytes) {
   std::vector<long long> k;
   const int nn = v.T->nn;
-  k.reserve(8 + 6 * nn);
+  k.reserve(12 + 4 * nn);
   int dev = 0;
   cudaGetDevice(&dev);
   long long eps_bits;
   memcpy(&eps_bits, &ctl->eps, sizeof(eps_bits));
-  k.insert(k.end(), {(long long)dev, (long long)v.T->d, (long long)v.orth, (long long)(uintptr_t)ws,
-                     (long long)ws_bytes, eps_bits, (long long)ctl->max_rank, (long long)ctl->flags,
-                     (long long)g_qr_mode, (long long)g_eig_mode});
+  k.insert(k.end(), {(long long)dev, (long long)v.T->d, (long long)v.orth, (long long)ws_bytes, eps_bits,
+                     (long long)ctl->max_rank, (long long)ctl->flags, (long long)g_qr_mode, (long long)g_eig_mode});
   for (int t = 0; t < nn; ++t) {
     k.push_back(v.n[t]);
     k.push_back(v.k[t]);
-    k.push_back((long long)(uintptr_t)v.p[t]);
     k.push_back(o.k[t]);
-    k.push_back((long long)(uintptr_t)o.p[t]);
     k.push_back(ctl->max_rank_per_node ? ctl->max_rank_per_node[t] : -1);
   }
   return k;
+}
+
+Addrs addresses(const View& v, const View& o, const void* ws) {
+  Addrs a;
+  for (int t = 0; t < v.T->nn; ++t) {
+    a.in.push_back((uintptr_t)v.p[t]);
+    a.out.push_back((uintptr_t)o.p[t]);
+  }
+  a.ws = (uintptr_t)ws;
+  return a;
+}
+
+std::vector<long long> address_key(const std::vector<long long>& skey, const Addrs& a) {
+  std::vector<long long> k = skey;
+  k.push_back(-7);  // separator: address keys never equal shape keys
+  for (auto p : a.in) k.push_back((long long)p);
+  for (auto p : a.out) k.push_back((long long)p);
+  k.push_back((long long)a.ws);
+  return k;
+}
+
+bool same_addrs(const TruncGraph* g, const Addrs& a) {
+  return g->cur_in == a.in && g->cur_out == a.out && g->cur_ws == a.ws;
+}
+
+// Relocation keeps the relative layout of each buffer: every node of the input (and of
+// the output) must have moved by the same amount (merged launch descriptors address
+// several nodes from one base pointer plus a fixed stride).
+bool uniform_move(const TruncGraph* g, const Addrs& a) {
+  const long long din = (long long)(a.in[0] - g->cap_in[0]), dout = (long long)(a.out[0] - g->cap_out[0]);
+  for (size_t t = 0; t < a.in.size(); ++t)
+    if ((long long)(a.in[t] - g->cap_in[t]) != din || (long long)(a.out[t] - g->cap_out[t]) != dout) return false;
+  return true;
 }
 
 // Pinned flag words of the graphs, recycled (never freed: cudaFreeHost would
@@ -1202,18 +1287,26 @@ void destroy_graph(TruncGraph* g) {
   // executable graphs and events still in flight are released by the driver on completion
   if (g->orth) cudaGraphExecDestroy(g->orth);
   if (g->rest) cudaGraphExecDestroy(g->rest);
+  if (g->g_orth) cudaGraphDestroy(g->g_orth);
+  if (g->g_rest) cudaGraphDestroy(g->g_rest);
   if (g->ev) cudaEventDestroy(g->ev);
   if (g->flag) g_graph_flags.push_back(g->flag);
   delete g;
 }
 
 // Capture one part of the truncation on `s`; on error the capture is ended and discarded.
+// The source graph is kept (`graph`) together with the conditional bodies it contains.
 template <class F>
-int capture_part(cudaStream_t s, cudaGraphExec_t* exec, long long* launches, F&& body) {
+int capture_part(cudaStream_t s, cudaGraph_t* graph, cudaGraphExec_t* exec, std::vector<cudaGraph_t>* bodies,
+                 std::vector<cudaGraphNode_t>* conds, long long* launches, F&& body) {
   const long long l0 = prof_launches(), b0 = g_cond_body_launches;
   HT_CUDA_CHECK(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
   g_own_capture = true;
+  g_body_sink = bodies;
+  g_cond_sink = conds;
   int rc = body();
+  g_body_sink = nullptr;
+  g_cond_sink = nullptr;
   g_own_capture = false;
   cudaGraph_t g = nullptr;
   cudaError_t ce = cudaStreamEndCapture(s, &g);
@@ -1228,7 +1321,11 @@ int capture_part(cudaStream_t s, cudaGraphExec_t* exec, long long* launches, F&&
       rc = kErrCuda;
     }
   }
-  if (g) cudaGraphDestroy(g);
+  if (rc == kOk) {
+    *graph = g;
+  } else if (g) {
+    cudaGraphDestroy(g);
+  }
   cudaGetLastError();
   // the launches recorded during capture did not run; replays add them back (except
   // those inside IF bodies, which run only when their branch is taken)
@@ -1264,14 +1361,13 @@ int capture_device_fallback(const View& v, const ht_trunc_ctl* ctl, char* ws, si
   HT_CUDA_CHECK(cudaGetSymbolAddress((void**)&taken, g_dev_qr_fallbacks));
   return capture_if_any(s, fail, 1, taken, [&](cudaStream_t s2) -> int {
     TruncPlan P2;
-    HT_TRY(truncate_phase1(v, ctl, ws, ws_bytes, P2, s2, nullptr, true));
+    HT_TRY(truncate_phase1(v, ctl, ws, ws_bytes, P2, s2, nullptr, true, true));
     return truncate_phase2(v, ctl, ws, o, s2);
   });
 }
 
 int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_bytes, const View& o,
-                       cudaStream_t s_caller, TruncGraph* G) {
-  (void)s_caller;
+                       TruncGraph* G) {
   cudaStream_t s = capture_stream();
   if (!s) {
     set_error("cannot create the graph-capture stream");
@@ -1289,16 +1385,18 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   chk.host = G->flag;
   chk.capture = true;
   chk.device = g_cond_nodes != 0;
-  HT_TRY(capture_part(s, &G->orth, &G->n_orth, [&]() -> int {
+  std::vector<cudaGraph_t> b_orth, b_rest;
+  std::vector<cudaGraphNode_t> c_orth, c_rest;
+  HT_TRY(capture_part(s, &G->g_orth, &G->orth, &b_orth, &c_orth, &G->n_orth, [&]() -> int {
     HT_TRY(plan_truncate(v, P, ws));
     HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
     return phase_orth(v, P, s, &chk);
   }));
   G->chol = chk.used;
   G->device = chk.used && chk.device;
-  const int rc = capture_part(s, &G->rest, &G->n_rest, [&]() -> int {
+  const int rc = capture_part(s, &G->g_rest, &G->rest, &b_rest, &c_rest, &G->n_rest, [&]() -> int {
     HT_TRY(phase_gram(P, s));
-    HT_TRY(phase_eig(v, ctl, P, s));
+    HT_TRY(phase_eig(v, ctl, P, s, true));
     HT_TRY(truncate_phase2(v, ctl, ws, o, s));
     if (!G->device) return kOk;
     return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s);
@@ -1308,17 +1406,50 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
     // host-side flag check
     g_cond_nodes = 0;
     if (G->orth) cudaGraphExecDestroy(G->orth);
+    if (G->g_orth) cudaGraphDestroy(G->g_orth);
     G->orth = nullptr;
+    G->g_orth = nullptr;
     g_graph_flags.push_back(G->flag);
     G->flag = nullptr;
     if (G->ev) cudaEventDestroy(G->ev);
     G->ev = nullptr;
     cudaGetLastError();
-    return capture_truncation(v, ctl, ws, ws_bytes, o, s_caller, G);
+    return capture_truncation(v, ctl, ws, ws_bytes, o, G);
   }
   HT_TRY(rc);
   if (G->device) g_cond_nodes = 1;
+  // relocation tables: argument words inside the input (group 0), output (1) and
+  // workspace (2) ranges
+  std::vector<RelocRange> ranges;
+  for (int t = 0; t < v.T->nn; ++t) {
+    ranges.push_back({(uintptr_t)v.p[t], (uintptr_t)(v.p[t] + v.elems(t)), 0});
+    ranges.push_back({(uintptr_t)o.p[t], (uintptr_t)(o.p[t] + o.elems(t)), 1});
+  }
+  ranges.push_back({(uintptr_t)ws, (uintptr_t)ws + ws_bytes, 2});
+  reloc_scan(G->g_orth, b_orth, c_orth, ranges, G->r_orth);
+  reloc_scan(G->g_rest, b_rest, c_rest, ranges, G->r_rest);
   return kOk;
+}
+
+int relocate(TruncGraph* G, const Addrs& a) {
+  const std::vector<long long> delta{(long long)(a.in[0] - G->cap_in[0]), (long long)(a.out[0] - G->cap_out[0]),
+                                     (long long)(a.ws - G->cap_ws)};
+  cudaError_t e = reloc_apply(G->orth, G->g_orth, G->r_orth, delta);
+  if (e == cudaSuccess) e = reloc_apply(G->rest, G->g_rest, G->r_rest, delta);
+  if (e != cudaSuccess) {
+    set_error(std::string("graph relocation: ") + cudaGetErrorString(e));
+    return kErrCuda;
+  }
+  G->cur_in = a.in;
+  G->cur_out = a.out;
+  G->cur_ws = a.ws;
+  ++g_graph_relocations;
+  return kOk;
+}
+
+void forget_graph(TruncGraph* G) {
+  g_graphs.erase(std::find(g_graphs.begin(), g_graphs.end(), G));
+  destroy_graph(G);
 }
 
 // ran = true when the graph path ran the truncation (else the caller runs it eagerly).
@@ -1333,31 +1464,51 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
     return kOk;  // the caller is capturing: record the eager launches into its graph
   }
   std::lock_guard<std::mutex> lk(g_graph_mu);
-  auto key = graph_key(v, o, ctl, ws, ws_bytes);
+  const auto skey = shape_key(v, o, ctl, ws_bytes);
+  const Addrs a = addresses(v, o, ws);
   TruncGraph* G = nullptr;
+  std::vector<TruncGraph*> same;
   for (auto* g : g_graphs)
-    if (g->key == key) G = g;
+    if (g->skey == skey) {
+      same.push_back(g);
+      if (same_addrs(g, a)) G = g;
+    }
   if (!G) {
-    if (g_graph_seen.size() > 1024) g_graph_seen.clear();
-    if (++g_graph_seen[key] < 2 || g_graph_waste > kMaxGraphWaste) return kOk;  // one-off keys stay eager
-    if (g_graphs.size() >= kMaxGraphs) {
-      auto it = std::min_element(g_graphs.begin(), g_graphs.end(),
-                                 [](TruncGraph* a, TruncGraph* b) { return a->used < b->used; });
-      if ((*it)->replays < 2) ++g_graph_waste;
-      // an in-flight executable graph is released by the driver when it completes
-      destroy_graph(*it);
-      g_graphs.erase(it);
+    if (g_graph_seen.size() > 4096) g_graph_seen.clear();
+    const int seen_shape = ++g_graph_seen[skey];
+    const int seen_addr = ++g_graph_seen[address_key(skey, a)];
+    TruncGraph* cand = nullptr;  // least recently used relocatable graph of these shapes
+    for (auto* g : same)
+      if (g->relocatable() && uniform_move(g, a) && (!cand || g->used < cand->used)) cand = g;
+    const bool capture = same.empty() ? seen_shape >= 2 : (seen_addr >= 2 && (same.size() < kMaxPerShape || !cand));
+    if (!capture && cand) {
+      if (relocate(cand, a) != kOk) {
+        forget_graph(cand);  // run eagerly; the shapes are captured again on a later call
+        cudaGetLastError();
+        return kOk;
+      }
+      G = cand;
+    } else if (capture) {
+      if (same.size() >= kMaxPerShape || g_graphs.size() >= kMaxGraphs) {
+        const auto& pool = same.size() >= kMaxPerShape ? same : g_graphs;
+        forget_graph(*std::min_element(pool.begin(), pool.end(),
+                                       [](TruncGraph* x, TruncGraph* y) { return x->used < y->used; }));
+      }
+      G = new TruncGraph;
+      G->skey = skey;
+      G->cap_in = G->cur_in = a.in;
+      G->cap_out = G->cur_out = a.out;
+      G->cap_ws = G->cur_ws = a.ws;
+      if (capture_truncation(v, ctl, ws, ws_bytes, o, G) != kOk) {
+        cudaGetLastError();
+        destroy_graph(G);
+        return kOk;  // fall back to the eager path (its own errors are authoritative)
+      }
+      g_graphs.push_back(G);
+      ++g_graph_captures;
+    } else {
+      return kOk;  // first sighting: eager
     }
-    G = new TruncGraph;
-    G->key = key;
-    if (capture_truncation(v, ctl, ws, ws_bytes, o, s, G) != kOk) {
-      cudaGetLastError();
-      destroy_graph(G);
-      g_graph_seen.erase(key);
-      return kOk;  // fall back to the eager path (its own errors are authoritative)
-    }
-    g_graphs.push_back(G);
-    ++g_graph_captures;
   }
   G->used = ++g_graph_clock;
   HT_CUDA_CHECK(cudaGraphLaunch(G->orth, s));
@@ -1470,7 +1621,7 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
   HT_TRY(truncate_graph(v, ctl, (char*)ws, ws_bytes, o, s, ran, failed));
   if (!ran) {
     OrthCheck chk;
-    HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk));
+    HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk, false, true));
     HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s));
     // the speculative result stands unless the Cholesky-QR flag was raised; then the
     // whole truncation is recomputed on the Householder path (stream order overwrites)
@@ -1478,7 +1629,7 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
   }
   if (!failed) return kOk;
   ++g_qr_fallbacks;
-  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, nullptr, true));
+  HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, nullptr, true, true));
   return truncate_phase2(v, ctl, (char*)ws, o, s);
 }
 
@@ -1502,7 +1653,7 @@ int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
       HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
       return phase_orth(v, P, s);
     case kPhaseGram: return phase_gram(P, s);
-    case kPhaseEig: return phase_eig(v, ctl, P, s);
+    case kPhaseEig: return phase_eig(v, ctl, P, s, true);
     default: break;
   }
   set_error("unknown truncate phase");
@@ -1650,7 +1801,6 @@ int ht_set_graph_mode(int on) {
     for (auto* g : g_graphs) destroy_graph(g);
     g_graphs.clear();
     g_graph_seen.clear();
-    g_graph_waste = 0;
   }
   return kOk;
 }
@@ -1658,6 +1808,29 @@ int ht_set_graph_mode(int on) {
 int ht_graph_stats(int64_t* captures, int64_t* replays) {
   if (captures) *captures = g_graph_captures;
   if (replays) *replays = g_graph_replays;
+  return kOk;
+}
+
+int64_t ht_graph_relocations(void) { return g_graph_relocations; }
+
+int ht_status(int32_t clear, int32_t* status, ht_stream_t stream) {
+  // ordered behind the caller's stream (errors queued on other streams surface at a later check)
+  cudaStream_t s = (cudaStream_t)stream;
+  int* d = nullptr;
+  HT_CUDA_CHECK(cudaGetSymbolAddress((void**)&d, g_sticky_status));
+  int h = 0;
+  HT_CUDA_CHECK(cudaMemcpyAsync(&h, d, sizeof(int), cudaMemcpyDeviceToHost, s));
+  HT_CUDA_CHECK(cudaStreamSynchronize(s));
+  if (clear && h) HT_CUDA_CHECK(cudaMemsetAsync(d, 0, sizeof(int), s));
+  if (status) *status = h;
+  if (h & kEigStatusNotSymmetric) {
+    set_error("matrix is not symmetric within tolerance (queued truncation)");
+    return kErrNotSymmetric;
+  }
+  if (h & kEigStatusNonConverged) {
+    set_error("eigensolver did not converge or the Gramian is not finite (queued truncation)");
+    return kErrNonConverged;
+  }
   return kOk;
 }
 

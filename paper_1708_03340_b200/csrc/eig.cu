@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
     const int i = x / K, j = x - i * K;
     asym = fmax(asym, fabs(A[i * ap + j] - A[j * ap + i]));
     amax = fmax(amax, fabs(A[i * ap + j]));
+    if (!isfinite(A[i * ap + j])) amax = INFINITY;  // fmax drops NaN: make it visible
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   }
   __syncthreads();
   if (tid == 0 && e.status && red[0] > 1e-12 * fmax(1.0, red[1])) atomicOr(e.status, kEigStatusNotSymmetric);
+  if (tid == 0 && e.status && !isfinite(red[1])) atomicOr(e.status, kEigStatusNonConverged);
   for (int x = tid; x < K * K; x += blockDim.x) {
     const int i = x / K, j = x - i * K;
     if (i < j) {

@@ -168,6 +168,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     const double a = S[x], at = S[j * K + i];
     asym = fmax(asym, fabs(a - at));
     amax = fmax(amax, fabs(a));
+    if (!isfinite(a)) amax = INFINITY;  // fmax drops NaN: make it visible
     A[i * ap + j] = 0.5 * (a + at);
   }
 #pragma unroll
@@ -181,7 +182,19 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
     double s0 = 0.0, s1 = 0.0;
     for (int w = 0; w < TT / 32; ++w) { s0 = fmax(s0, red[w][0]); s1 = fmax(s1, red[w][1]); }
     if (e.status && s0 > 1e-12 * fmax(1.0, s1)) atomicOr(e.status, kEigStatusNotSymmetric);
+    if (e.status && !isfinite(s1)) atomicOr(e.status, kEigStatusNonConverged);
     flags[0] = 0;
+    flags[1] = isfinite(s1) ? 0 : 1;
+  }
+  __syncthreads();
+  if (flags[1]) {  // non-finite Gramian: flagged above; NaN results, no Jacobi redo
+    for (int x = tid; x < K * K; x += TT) e.V[nd * e.v_node + x] = __longlong_as_double(0x7ff8000000000000ll);
+    for (int x = tid; x < K; x += TT) e.lam[nd * e.l_node + x] = __longlong_as_double(0x7ff8000000000000ll);
+    if (tid == 0) {
+      if (e.rank) e.rank[nd] = e.cap > 0 ? min(e.cap, K) : K;
+      if (e.fallback) e.fallback[nd] = 0;
+    }
+    return;
   }
 
   // ---- 1. tridiagonalisation --------------------------------------------------

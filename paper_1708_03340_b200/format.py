@@ -14,6 +14,7 @@ from __future__ import annotations
 import ctypes
 import math
 import os
+from collections.abc import Mapping
 
 import numpy as np
 import torch
@@ -43,6 +44,53 @@ def node_shape(tree: DimensionTree, t: int, sizes: dict, ranks: dict) -> tuple:
     if node.is_root:
         return (ranks[s1], ranks[s2])
     return (ranks[t], ranks[s1], ranks[s2])
+
+
+class _ArenaViews(Mapping):
+    """Node arrays of an arena-backed tensor, built as views on first access.
+
+    Outputs of add / truncate / apply are arena-backed; building all 2d-1 views
+    eagerly cost ~0.6 ms of host time per d=64 call, so only the arena, the offsets
+    and the shapes are kept until a node array is actually asked for.
+    """
+
+    __slots__ = ("arena", "offsets", "shapes", "_views")
+
+    def __init__(self, arena: torch.Tensor, offsets: list, shapes: list):
+        self.arena, self.offsets, self.shapes = arena, offsets, shapes
+        self._views = [None] * len(shapes)
+
+    def __getitem__(self, t):
+        v = self._views[t]
+        if v is None:
+            o, s = self.offsets[t], self.shapes[t]
+            v = self.arena[o:o + math.prod(s)].view(s)
+            self._views[t] = v
+        return v
+
+    def __iter__(self):
+        return iter(range(len(self.shapes)))
+
+    def __len__(self):
+        return len(self.shapes)
+
+    def __contains__(self, t):
+        return isinstance(t, int) and 0 <= t < len(self.shapes)
+
+    def get(self, t, default=None):
+        return self[t] if t in self else default
+
+    def pointers(self) -> list:
+        base = self.arena.data_ptr()
+        return [base + 8 * o for o in self.offsets]
+
+
+def _arena_views(arena: torch.Tensor, shapes: list) -> _ArenaViews:
+    offsets, off = [], 0
+    for s in shapes:
+        offsets.append(off)
+        off += math.prod(s)
+    return _ArenaViews(arena, offsets, shapes)
 
 
 class HTensor:
@@ -88,17 +136,12 @@ class HTensor:
               device=None) -> "HTensor":
         """Allocate an uninitialised tensor (one arena) with the given leaf sizes / ranks."""
         dev = _device(device)
-        shapes = {t: node_shape(tree, t, sizes_by_node, ranks) for t in range(len(tree.nodes))}
-        total = sum(math.prod(s) for s in shapes.values())
+        shapes = [node_shape(tree, t, sizes_by_node, ranks) for t in range(len(tree.nodes))]
+        total = sum(math.prod(s) for s in shapes)
         arena = torch.empty(total, dtype=F64, device=dev)
         if _POISON:  # debugging aid (HT_POISON_WORKSPACE=1): outputs start as NaN
             arena.fill_(float("nan"))
-        nodes, off = {}, 0
-        for t in range(len(tree.nodes)):
-            n = math.prod(shapes[t])
-            nodes[t] = arena[off:off + n].view(shapes[t])
-            off += n
-        return cls._wrap(tree, nodes, orthogonal, arena)
+        return cls._wrap(tree, _arena_views(arena, shapes), orthogonal, arena)
 
     @classmethod
     def from_numpy(cls, tree, leaves, transfer, root_matrix, orthogonal=False, device=None) -> "HTensor":
@@ -121,13 +164,17 @@ class HTensor:
     def node_array(self, t: int) -> torch.Tensor:
         return self._nodes[t]
 
+    def _shape(self, t: int) -> tuple:
+        n = self._nodes
+        return n.shapes[t] if isinstance(n, _ArenaViews) else tuple(n[t].shape)
+
     def rank(self, node_id: int) -> int:
         node = self.tree.node(node_id)
         if node.is_root:
             return 1
         if node.is_leaf:
-            return int(self._nodes[node_id].shape[1])
-        return int(self._nodes[node_id].shape[0])
+            return int(self._shape(node_id)[1])
+        return int(self._shape(node_id)[0])
 
     @property
     def ranks(self) -> dict:
@@ -139,11 +186,12 @@ class HTensor:
 
     @property
     def shape(self) -> tuple:
-        return tuple(int(self._nodes[self.tree.leaf_for_dim(mu).index].shape[0])
-                     for mu in range(1, self.tree.d + 1))
+        return tuple(int(self._shape(self.tree.leaf_for_dim(mu).index)[0]) for mu in range(1, self.tree.d + 1))
 
     @property
     def device(self) -> torch.device:
+        if self._arena is not None:
+            return self._arena.device
         return self._nodes[0].device
 
     def validate(self) -> None:
@@ -176,8 +224,17 @@ class HTensor:
     # -- host transfer ---------------------------------------------------------
 
     def to_numpy(self):
-        """(leaves, transfer, root_matrix) as numpy dicts -- one D2H copy when arena-backed."""
-        if self._arena is not None:
+        """(leaves, transfer, root_matrix) as numpy dicts -- one D2H copy when arena-backed.
+        A host synchronisation point: errors left by queued truncations are raised here."""
+        if self.device.type == "cuda":
+            with torch.cuda.device(self.device):
+                _lib.check_status()
+        if isinstance(self._nodes, _ArenaViews):
+            host = self._arena.cpu().numpy()
+            out = {}
+            for t, (o, s) in enumerate(zip(self._nodes.offsets, self._nodes.shapes)):
+                out[t] = host[o:o + math.prod(s)].reshape(s)
+        elif self._arena is not None:
             host = self._arena.cpu().numpy()
             out, off = {}, 0
             for t in range(len(self.tree.nodes)):
@@ -224,21 +281,44 @@ class HTensor:
 
     def host_layout(self):
         """(sizes_by_node, ranks) needed to rebuild this tensor from a host arena."""
-        return ({leaf.index: int(self._nodes[leaf.index].shape[0]) for leaf in self.tree.leaves},
+        return ({leaf.index: int(self._shape(leaf.index)[0]) for leaf in self.tree.leaves},
                 {t: self.rank(t) for t in range(1, len(self.tree.nodes))})
 
     # -- C ABI -----------------------------------------------------------------
 
+    def _check_resident(self) -> torch.device:
+        """Every node array must be a float64 CUDA tensor on one device (the C ABI takes
+        raw device pointers); host-resident tensors are rejected instead of faulting."""
+        if isinstance(self._nodes, _ArenaViews):
+            arrays = [self._arena]
+        else:
+            arrays = [self._nodes[t] for t in range(len(self.tree.nodes))]
+        dev = arrays[0].device
+        for a in arrays:
+            if not a.is_cuda or a.dtype != F64 or a.device != dev:
+                raise ValueError(f"HTensor node arrays must be float64 CUDA tensors on one device; got "
+                                 f"{a.dtype} on {a.device} (host-resident tensors cannot be passed to the kernels)")
+            if not a.is_contiguous():
+                raise ValueError("HTensor node arrays must be contiguous (C-order)")
+        return dev
+
     def _c(self) -> _lib.CTensor:
         if self._cstruct is None:
+            dev = self._check_resident()
             tree = self.tree
             n = _lib.i64_array(self.shape)
             ranks = _lib.i64_array([1] + [self.rank(t) for t in range(1, len(tree.nodes))])
-            ptrs = _lib.ptr_array([self._nodes[t].data_ptr() for t in range(len(tree.nodes))])
+            if isinstance(self._nodes, _ArenaViews):
+                ptrs = _lib.ptr_array(self._nodes.pointers())
+            else:
+                ptrs = _lib.ptr_array([self._nodes[t].data_ptr() for t in range(len(tree.nodes))])
             cs = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
                               ctypes.cast(ranks, ctypes.POINTER(ctypes.c_int64)),
                               ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), int(self.orthogonal))
-            self._cstruct = (cs, n, ranks, ptrs)
+            self._cstruct = (cs, n, ranks, ptrs, dev.index)
+        if self._cstruct[4] != torch.cuda.current_device():
+            raise ValueError(f"HTensor lives on cuda:{self._cstruct[4]} but the current device is "
+                             f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device(...)")
         cs = self._cstruct[0]
         cs.orthogonal = int(self.orthogonal)
         return cs

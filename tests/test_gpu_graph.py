@@ -70,3 +70,107 @@ def test_graph_replay_routes_rank_deficient_input_to_householder(cuda_ok):
     got = orc.HT(orc.balanced_tree(8), {t: np.array(v) for t, v in leaves.items()},
                  {t: np.array(v) for t, v in transfer.items()}, np.array(root))
     assert orc.orth_difference_norm(got, ref) / orc.norm(ref) <= 1e-10
+
+
+def _fresh_copy(htb, x):
+    """The same values in a new arena (new addresses, same layout)."""
+    sizes, ranks = x.host_layout()
+    y = htb.HTensor.empty(x.tree, sizes, ranks, orthogonal=x.orthogonal)
+    y._arena.copy_(x._arena)
+    return y
+
+
+@pytest.mark.parametrize("deficient", [False, True])
+def test_graph_relocation_bitwise_equals_eager(cuda_ok, deficient):
+    """Replays on moved buffers (new input, output and workspace addresses) relocate the
+    cached graph instead of capturing again, and still reproduce the eager launches bit
+    for bit -- including the device-side Householder branch (conditional body)."""
+    import paper_1708_03340_b200 as htb
+
+    tree = htb.build_balanced_tree(8)
+    a = htb.gaussian_htensor(tree, 150, 14, 11)
+    c = a if deficient else htb.gaussian_htensor(tree, 150, 14, 12)
+    x = htb.add(a, c)
+    ctl = htb.TruncationControl.fixed_rank(13)
+    htb.set_graph_mode(False)
+    try:
+        eager = _arrays(htb.truncate(x, ctl))
+    finally:
+        htb.set_graph_mode(True)
+    for _ in range(3):  # capture + replay on x
+        htb.truncate(x, ctl)
+    c0, _ = htb.graph_stats()
+    m0 = htb.graph_relocations()
+    keep = []
+    for i in range(6):
+        y = _fresh_copy(htb, x)
+        keep.append(y)  # keep the buffers alive: every call sees new addresses
+        got = _arrays(htb.truncate(y, ctl))
+        for p, q in zip(got, eager):
+            assert np.array_equal(p, q), f"relocated replay {i} differs from the eager truncation"
+    c1, _ = htb.graph_stats()
+    assert htb.graph_relocations() - m0 >= 4, "moved buffers should relocate the cached graph"
+    assert c1 - c0 <= 1
+
+
+def test_graph_relocation_whole_graph_update_path(cuda_ok):
+    """Same check with relocation forced through cudaGraphExecUpdate (HT_RELOC_UPDATE=1),
+    the path used where the driver refuses per-node updates inside conditional bodies."""
+    import os
+    import subprocess
+    import sys
+
+    code = (
+        "import numpy as np, paper_1708_03340_b200 as htb\n"
+        "from tests.test_gpu_graph import _arrays, _fresh_copy\n"
+        "tree = htb.build_balanced_tree(8)\n"
+        "a = htb.gaussian_htensor(tree, 120, 12, 5)\n"
+        "for c in (htb.gaussian_htensor(tree, 120, 12, 6), a):\n"
+        "    x = htb.add(a, c); ctl = htb.TruncationControl.fixed_rank(11)\n"
+        "    htb.set_graph_mode(False); ref = _arrays(htb.truncate(x, ctl)); htb.set_graph_mode(True)\n"
+        "    [htb.truncate(x, ctl) for _ in range(3)]\n"
+        "    m0 = htb.graph_relocations(); keep = []\n"
+        "    for i in range(4):\n"
+        "        y = _fresh_copy(htb, x); keep.append(y)\n"
+        "        assert all(np.array_equal(p, q) for p, q in zip(_arrays(htb.truncate(y, ctl)), ref))\n"
+        "    assert htb.graph_relocations() - m0 >= 3\n"
+        "print('ok')\n")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, HT_RELOC_UPDATE="1", PYTHONPATH=root)
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_fixed_rank_truncate_raises_on_non_finite_input(cuda_ok):
+    """Fixed-rank truncate is asynchronous; a non-finite Gramian recorded by a queued
+    (eager or graph-replayed) truncation is raised at the next host synchronisation."""
+    import paper_1708_03340_b200 as htb
+
+    tree = htb.build_balanced_tree(8)
+    x = htb.add(htb.gaussian_htensor(tree, 100, 10, 1), htb.gaussian_htensor(tree, 100, 10, 2))
+    ctl = htb.TruncationControl.fixed_rank(10)
+    for _ in range(3):  # capture the graph on these buffers
+        htb.truncate(x, ctl)
+    htb.synchronize()
+    x._arena[5] = float("nan")  # poison a leaf entry in place: the replay sees it
+    t = htb.truncate(x, ctl)
+    with pytest.raises(RuntimeError, match="not finite|converge"):
+        t.to_numpy()
+    htb.synchronize()  # the sticky word was cleared by the raise
+    htb.set_graph_mode(False)
+    try:
+        htb.truncate(x, ctl)
+        with pytest.raises(RuntimeError):
+            htb.synchronize()
+    finally:
+        htb.set_graph_mode(True)
+
+
+def test_host_resident_tensor_rejected(cuda_ok):
+    import paper_1708_03340_b200 as htb
+
+    tree = htb.build_balanced_tree(4)
+    f = htb.gaussian_factors(tree, 20, 3, 0)
+    xh = htb.HTensor(tree, *f, device="cpu")
+    with pytest.raises(ValueError, match="CUDA"):
+        htb.truncate(xh, htb.TruncationControl.fixed_rank(2))
