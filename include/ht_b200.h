@@ -206,9 +206,11 @@ int ht_qr_batched(int64_t m, int64_t K, int64_t nodes, const double* A, int64_t 
                   double* Q, int64_t q_r, int64_t q_c, int64_t q_node, double* R, int64_t r_ld, int64_t r_node,
                   void* ws, size_t ws_bytes, ht_stream_t stream);
 
-/* sym_eig_desc (kernels.py:35-54) on `nodes` K x K row-major matrices:
- * eigenvectors V (row-major, columns = eigenvectors), lam descending clamped.
- * Synchronises to report HT_ERR_NOT_SYMMETRIC like the reference. */
+/* sym_eig_desc (kernels.py:35-54) on `nodes` K x K row-major matrices (K <= 512):
+ * eigenvectors V (row-major, columns = eigenvectors), lam descending clamped, by
+ * parallel cyclic Jacobi (relative accuracy on graded matrices; K > 112 keeps the
+ * matrices in a temporary global scratch).  Synchronises to report
+ * HT_ERR_NOT_SYMMETRIC like the reference. */
 int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double* lam, ht_stream_t stream);
 
 /* Strided batched GEMM C = alpha*A*B + beta*C (the mode_multiply / tensordot

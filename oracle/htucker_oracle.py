@@ -707,3 +707,10 @@ def c2_inputs(d: int, n: int = 1000, k: int = 50, seed_base: int | None = None):
     a = gaussian_htensor(tr, n, k, s)
     c = gaussian_htensor(tr, n, k, s + 1)
     return a, c, add(a, c)
+
+
+def c5_inputs(d: int = 256, n: int = 2048, k: int = 100):
+    """BASELINE config 4 (C5): four rank-k Gaussian tensors, seeds 0..3; the caller sums
+    them in the fixed order ((A0 + A1) + A2) + A3 (rank 4k)."""
+    tr = balanced_tree(d)
+    return [gaussian_htensor(tr, n, k, s) for s in range(4)]

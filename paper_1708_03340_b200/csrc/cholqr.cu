@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Cholesky-QR2 (see cholqr.cuh).  The GEMMs run on the grouped DMMA kernel of
 // gemm.cu; this file holds the batched Cholesky / triangular-inverse kernel and
 // the launch sequence.
@@ -725,6 +727,7 @@ long long cholbig_workspace_doubles(CholBig& c) {
   const int K = c.q.K;
   c.np = (K + kCholInPlaceK - 1) / kCholInPlaceK;
   c.pw = (K + c.np - 1) / c.np;
+  c.pw += c.pw & 1;  // even panel width: every panel starts 16-byte aligned (c0 even)
   const long long n = c.q.nodes;
   const long long c0max = (long long)(c.np - 1) * c.pw;
   c.S = split_for((long long)gemm_tiles((int)c0max, c.pw) * n, c.q.m);
@@ -742,6 +745,9 @@ long long cholbig_workspace_doubles(CholBig& c) {
 }
 
 void cholbig_bind(CholBig& c, double* ws) {
+  if (g_sync_check && getenv("HT_SYNC_DUMP"))
+    fprintf(stderr, "[cholbig] K=%d m=%d nodes=%d np=%d pw=%d S=%d ws=%p doubles=%lld\n", c.q.K, c.q.m, c.q.nodes,
+            c.np, c.pw, c.S, (void*)ws, cholbig_workspace_doubles(c));
   const long long n = c.q.nodes;
   const long long c0max = (long long)(c.np - 1) * c.pw;
   auto al = [](double* p) { return (double*)(((uintptr_t)p + 255) & ~(uintptr_t)255); };
@@ -767,6 +773,7 @@ int cholbig_run(std::vector<CholBig>& cs, int* fail, int* need2, bool two_pass, 
       HT_CUDA_CHECK(cudaMemset2DAsync(q.R + nd * q.r_node, sizeof(double) * q.r_ld, 0, sizeof(double) * K, K, s));
     for (int j = 0; j < c.np; ++j) {
       const int c0 = j * c.pw, w = std::min(c.pw, K - c0);
+      if (w <= 0) break;
       double* QJ = q.Q + (long long)c0 * q.q_c;
       double* RJ = q.R + c0;  // rows 0..c0-1 of the column block J
       for (int pass = 0; j > 0 && pass < 2; ++pass) {

@@ -4,6 +4,7 @@
 // mma.sync DMMA (tcgen05 has no kind::f64); DMMA and DFMA both measure ~37 TF/s
 // on this pool's B200s (profiles/r01_fp64_peak_microbench.jsonl).
 #pragma once
+#include <cstdio>
 
 #include <cuda_runtime.h>
 #include <cstdint>
@@ -37,9 +38,20 @@ const char* last_error();
     }                                                                           \
   } while (0)
 
+// HT_SYNC_CHECK=1 (debugging): every launch check also synchronises the device, so a
+// faulting kernel is reported at its own launch site
+extern const int g_sync_check;
+int debug_probe();  // HT_SYNC_CHECK=3: a fixed long-reduction GEMM after every launch
+
 #define HT_LAUNCH_CHECK()                                                       \
   do {                                                                          \
     cudaError_t _e = cudaGetLastError();                                        \
+    if (_e == cudaSuccess && ::ht::g_sync_check) {                              \
+      _e = cudaDeviceSynchronize();                                             \
+      if (::ht::g_sync_check > 1) fprintf(stderr, "[launch] %s:%d -> %d\n", __FILE__, __LINE__, (int)_e); \
+      if (_e == cudaSuccess && ::ht::g_sync_check > 2 && ::ht::debug_probe() != 0) \
+        fprintf(stderr, "[probe] FAILED after %s:%d\n", __FILE__, __LINE__);    \
+    }                                                                           \
     if (_e != cudaSuccess) {                                                    \
       ::ht::set_error(std::string("kernel launch (") + __FILE__ + ":" +         \
                       std::to_string(__LINE__) + "): " + cudaGetErrorString(_e)); \

@@ -27,6 +27,10 @@
 #include "reloc.cuh"
 
 namespace ht {
+const int g_sync_check = [] {
+  const char* e = getenv("HT_SYNC_CHECK");
+  return e ? atoi(e) : 0;  // 1: synchronise after every launch, 2: and log each launch site
+}();
 int g_cond_nodes = -1;
 long long g_cond_body_launches = 0;
 thread_local bool g_own_capture = false;
@@ -358,8 +362,11 @@ void merge_qrs(std::vector<QrProblem>& v) {
 }
 
 // Plan (and, if arena has a base, bind) the QR workspace of a set of problems.
+// Sizing runs (no base) never merge: merging depends on the caller's pointers, and
+// the unmerged plan is an upper bound of any merged one (split-K partials shrink,
+// per-node terms add up), so the size query covers every layout.
 int plan_qrs(std::vector<QrProblem>& qs, Arena& ar) {
-  merge_qrs(qs);
+  if (ar.base) merge_qrs(qs);
   for (auto& q : qs) {
     HT_TRY(qr_plan(q));
     double* w = ar.take(qr_workspace_doubles(q));
@@ -489,7 +496,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       q.m = (int)(k1o * k2o); q.K = (int)kt; q.nodes = 1;
       qs.push_back(q);
     }
-    merge_qrs(qs);
+    if (scratch_ar.base) merge_qrs(qs);  // sizing runs plan unmerged (see plan_qrs)
     std::vector<QrProblem> hh, wide;
     std::vector<CholQr> cq;
     std::vector<CholBig> cb;
@@ -2092,18 +2099,33 @@ int ht_qr_batched(int64_t m, int64_t K, int64_t nodes, const double* A, int64_t 
 }
 
 int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double* lam, ht_stream_t stream) {
-  int* st = nullptr;
-  HT_CUDA_CHECK(cudaMallocAsync((void**)&st, sizeof(int), (cudaStream_t)stream));
-  HT_CUDA_CHECK(cudaMemsetAsync(st, 0, sizeof(int), (cudaStream_t)stream));
+  if (K < 1 || K > kEigMaxKBig || nodes < 0) {
+    set_error("ht_syev_batched: K must be in [1, 512]");
+    return kErrArgument;
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  // status word, per-node fallback flags and (K > 112) the per-node global scratch
+  const long long wn = eig_work_doubles((int)K);
+  const size_t bytes = 64 + sizeof(int) * (size_t)std::max<int64_t>(nodes, 1) + 256 +
+                       sizeof(double) * (size_t)(wn * nodes);
+  char* buf = nullptr;
+  HT_CUDA_CHECK(cudaMallocAsync((void**)&buf, bytes, s));
+  int* st = (int*)buf;
+  int* fb = (int*)(buf + 64);
+  double* work = wn ? (double*)(buf + ((64 + sizeof(int) * std::max<int64_t>(nodes, 1) + 255) & ~(size_t)255))
+                    : nullptr;
+  HT_CUDA_CHECK(cudaMemsetAsync(st, 0, sizeof(int), s));
   EigProblem e{};
   e.S = S; e.s_node = K * K; e.V = V; e.v_node = K * K; e.lam = lam; e.l_node = K;
   e.status = st; e.K = (int)K; e.nodes = (int)nodes; e.n_nonroot = 1;
+  (void)fb;  // Jacobi for every node (no tridiagonal fast path, no fallback flags)
+  e.work = work; e.w_node = wn;
   e.graded_fallback = 1;
   std::vector<EigProblem> v{e};
-  int rc = eig_batched(v, (cudaStream_t)stream);
+  int rc = eig_batched(v, s);
   int hs = 0;
-  cudaMemcpyAsync(&hs, st, sizeof(int), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
-  cudaFreeAsync(st, (cudaStream_t)stream);
+  cudaMemcpyAsync(&hs, st, sizeof(int), cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(buf, s);
   HT_CUDA_CHECK(cudaStreamSynchronize((cudaStream_t)stream));
   if (rc != kOk) return rc;
   if (hs & kEigStatusNotSymmetric) {

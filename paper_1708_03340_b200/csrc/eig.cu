@@ -26,6 +26,11 @@ __device__ __forceinline__ int circle(int i, int r, int n) {
   return i == 0 ? 0 : ((i - 1 + r) % (n - 1)) + 1;
 }
 
+// BIG: K > kEigMaxK -- A and V^T live in the node's global scratch (e.work, L2-resident
+// at the sizes that need it), only the rotation parameters and the block list stay in
+// shared memory.  Same rotations, same order: relative accuracy for graded Gramians at
+// any rank up to kEigMaxKBig.
+template <bool BIG>
 __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ EigBatch b) {
   extern __shared__ double sm[];
   int di = 0;
@@ -39,9 +44,9 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   const int half = n / 2;
   const int nblk = half * (half + 1) / 2;
   const int vp_pitch = n + 2;      // even: 16-byte aligned rows for double2 rotations
-  double* A = sm;                  // n x ap, symmetric
+  double* A = BIG ? e.work + nd * e.w_node : sm;  // n x ap, symmetric
   double* Vt = A + ((n * ap + 1) & ~1);  // n x vp_pitch, rows = eigenvectors (V transposed)
-  double* cs = Vt + n * vp_pitch;  // [half]
+  double* cs = BIG ? sm : Vt + n * vp_pitch;  // [half]
   double* sn = cs + half;
   double* tt = sn + half;
   int* pp = (int*)(tt + half);     // [half]
@@ -239,7 +244,8 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
 size_t smem_bytes(int K) {
   const int n = K + (K & 1);
   const int half = n / 2;
-  return (size_t)(n * (n + 1) + 1 + n * (n + 2) + 3 * half) * sizeof(double) + (size_t)2 * half * sizeof(int) +
+  const size_t mats = K > kEigMaxK ? 0 : (size_t)(n * (n + 1) + 1 + n * (n + 2));
+  return (mats + 3 * half) * sizeof(double) + (size_t)2 * half * sizeof(int) +
          (size_t)(half * (half + 1) / 2) * sizeof(unsigned short) + 64;
 }
 
@@ -256,33 +262,38 @@ int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
     tri = tri && p.fallback != nullptr && (p.K <= kEigMaxK || p.work);
     big = big || p.K > kEigMaxK;
   }
-  if (big && !tri) {
-    set_error("eigensolver: K > 112 needs the tridiagonal path (eig mode auto and a workspace)");
-    return kErrUnsupported;
-  }
+  for (const auto& p : probs)
+    if (p.K > kEigMaxK && (!p.work || p.K > kEigMaxKBig)) {
+      set_error("eigensolver: K > 112 needs a global workspace (and K <= 512)");
+      return kErrUnsupported;
+    }
+  (void)big;
   if (tri) HT_TRY(eig_tri_batched(probs, stream));
   else
     for (auto& p : probs) p.fallback = nullptr;
-  // the Jacobi kernel only serves nodes the tridiagonal path flagged (never K > 112)
-  std::vector<EigProblem> jp;
-  for (const auto& p : probs)
-    if (p.K <= kEigMaxK) jp.push_back(p);
-  probs.swap(jp);
+  // the Jacobi kernel serves the nodes the tridiagonal path flagged (or every node in
+  // Jacobi mode); K > 112 runs the global-scratch variant
   if (!g_attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+    HT_CUDA_CHECK(cudaFuncSetAttribute(jacobi_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
     g_attr = true;
   }
+  for (int pass = 0; pass < 2; ++pass) {
+  const bool bigpass = pass == 1;
+  std::vector<EigProblem> sel;
+  for (const auto& p : probs)
+    if ((p.K > kEigMaxK) == bigpass) sel.push_back(p);
   size_t i = 0;
-  while (i < probs.size()) {
+  while (i < sel.size()) {
     EigBatch b;
     b.count = 0;
     int blocks = 0;
     size_t smem = 0;
-    while (i < probs.size() && b.count < MAXD) {
-      const EigProblem& p = probs[i++];
+    while (i < sel.size() && b.count < MAXD) {
+      const EigProblem& p = sel[i++];
       if (p.nodes == 0) continue;
-      if (p.K > kEigMaxK || p.K < 1) {
-        set_error("eig_batched: K=" + std::to_string(p.K) + " outside the shared-memory Jacobi path (K <= 112)");
+      if (p.K > kEigMaxKBig || p.K < 1) {
+        set_error("eig_batched: K=" + std::to_string(p.K) + " outside the Jacobi path (K <= 512)");
         return kErrUnsupported;
       }
       b.begin[b.count] = blocks;
@@ -298,9 +309,11 @@ int eig_batched(std::vector<EigProblem>& probs, cudaStream_t stream) {
       bytes += 24.0 * b.d[q].nodes * (double)b.d[q].K * b.d[q].K;
     }
     ProfToken tok = prof_begin(stream);
-    jacobi_kernel<<<blocks, ET, smem, stream>>>(b);
+    if (bigpass) jacobi_kernel<true><<<blocks, ET, smem, stream>>>(b);
+    else jacobi_kernel<false><<<blocks, ET, smem, stream>>>(b);
     HT_LAUNCH_CHECK();
     prof_end(tok, "jacobi_eig", stream, flops, bytes);
+  }
   }
   return kOk;
 }

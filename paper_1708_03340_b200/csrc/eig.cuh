@@ -38,7 +38,8 @@ struct EigProblem {
 
 constexpr int kEigMaxK = 112;      // shared-memory paths (Jacobi; tridiagonal in smem)
 constexpr int kEigMaxKBig = 512;   // tridiagonal path with the matrices in global scratch
-inline long long eig_work_doubles(int K) { return K > kEigMaxK ? 2LL * K * (K + 2) : 0; }
+// tridiagonal path: K x (K|1) matrix + kept-vector rows; Jacobi: A (n x n+1) + V^T (n x n+2), n = K rounded up to even
+inline long long eig_work_doubles(int K) { return K > kEigMaxK ? 2LL * (K + 1) * (K + 3) + 8 : 0; }
 constexpr int kEigStatusNotSymmetric = 1;
 constexpr int kEigStatusNonConverged = 2;
 

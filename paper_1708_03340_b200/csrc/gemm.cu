@@ -1,3 +1,4 @@
+#include <cstdio>
 // Grouped FP64 DMMA GEMM (see gemm.cuh).
 //
 // CTA tiles are shaped for the HT contractions, whose short dimension is a rank
@@ -944,6 +945,14 @@ int gemm_tiles(int M, int N) {  // tiles of a long-reduction (split-K planned) G
 }
 
 int gemm_grouped(std::vector<GemmDesc>& descs_in, cudaStream_t stream, const char* tag, bool count_flops) {
+  if (g_sync_check > 1 || (g_sync_check && getenv("HT_SYNC_DUMP")))
+    for (const auto& d : descs_in)
+      fprintf(stderr,
+              "[gemm %s] M=%d N=%d K=%d KO=%d nb=%d,%d S=%d A=%p(%lld,%lld,%lld,%lld) B=%p(%lld,%lld,%lld,%lld) "
+              "C=%p(%lld,%lld,%lld) tri=%d,%d act=%p sym=%d ab=%g,%g\n",
+              tag ? tag : "-", d.M, d.N, d.K, d.KO, d.nb1, d.nb2, d.splits, (const void*)d.A, d.a_m, d.a_k, d.a_o,
+              d.a_b1, (const void*)d.B, d.b_k, d.b_n, d.b_o, d.b_b1, (void*)d.C, d.c_m, d.c_n, d.c_b1, d.a_tri,
+              d.b_tri, (const void*)d.active, d.sym, d.alpha, d.beta);
   std::vector<std::pair<GemmDesc, int>> lr;
   std::vector<GemmDesc> descs;
   for (const auto& d : descs_in) {
@@ -1016,4 +1025,26 @@ int reduce_partials(const std::vector<ReduceDesc>& descs, cudaStream_t stream, c
   return kOk;
 }
 
+}  // namespace ht
+
+namespace ht {
+// Debugging aid (HT_SYNC_CHECK=3): one fixed split-K long-reduction GEMM on a private
+// buffer, synchronised; non-zero if it faults (localises kernels that corrupt state).
+int debug_probe() {
+  static double* buf = nullptr;
+  static bool busy = false;
+  if (busy) return 0;
+  busy = true;
+  if (!buf && cudaMalloc(&buf, sizeof(double) * (150 * 2048 + 8 * 76 * 74)) != cudaSuccess) return 1;
+  GemmDesc g = gemm_desc(buf, 2048, 1, buf + 76 * 2048, 1, 2048, buf + 150 * 2048, 74, 1, 76, 74, 2048);
+  g.splits = 8;
+  g.c_b1 = 76 * 74;
+  std::vector<GemmDesc> v{g};
+  const int sc = g_sync_check;
+  (void)sc;
+  int rc = gemm_grouped(v, 0, "probe", false);
+  cudaError_t e = cudaDeviceSynchronize();
+  busy = false;
+  return rc != kOk || e != cudaSuccess;
+}
 }  // namespace ht

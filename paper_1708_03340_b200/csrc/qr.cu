@@ -1,3 +1,5 @@
+#include <cstdio>
+#include <cstdlib>
 // Blocked tree-TSQR Householder QR with DMMA trailing updates (see qr.cuh).
 //
 // Reference semantics: kernels.py:24-32 -- dlarfg reflectors as in LAPACK dgeqrf,
@@ -693,6 +695,14 @@ void qr_bind_workspace(QrProblem& p, double* ws) {
 
 int qr_batched(std::vector<QrProblem>& probs, cudaStream_t stream) {
   if (probs.empty()) return kOk;
+  if (g_sync_check && getenv("HT_SYNC_DUMP"))
+    for (const auto& p : probs)
+      fprintf(stderr,
+              "[qr] m=%d K=%d nodes=%d P=%d rpc=%d A=%p(%lld,%lld,%lld) Q=%p(%lld,%lld,%lld) R=%p(%lld,%lld) V=%p "
+              "Rst=%p Tst=%p X=%p own=%d vn=%lld stn=%lld tn=%lld xn=%lld\n",
+              p.m, p.K, p.nodes, p.P, p.rpc, (const void*)p.A, p.a_r, p.a_c, p.a_node, (void*)p.Q, p.q_r, p.q_c,
+              p.q_node, (void*)p.R, p.r_ld, p.r_node, (void*)p.V, (void*)p.Rst, (void*)p.Tst, (void*)p.X,
+              (int)p.own_v, p.v_node, p.st_node, p.t_node, p.x_node);
   if (!g_attr_done) {
     HT_CUDA_CHECK(cudaFuncSetAttribute(qr_factor_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));
     HT_CUDA_CHECK(cudaFuncSetAttribute(qr_apply_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_LIMIT));

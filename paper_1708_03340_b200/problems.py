@@ -78,60 +78,96 @@ def parameter_grids(points: int = 16, lo: float = 0.1, hi: float = 1.0):
     return [np.linspace(lo, hi, points) for _ in range(N_PARAMS)]
 
 
-def _params(node):
-    return [mu for mu in node.dims if mu <= N_PARAMS]
+def distinct_parameter_grids(points: int = 16):
+    """C4 with the parameter symmetry broken: parameter i samples [0.1 + 0.013 i,
+    1.0 - 0.007 i] (still inside [0.1, 1.0]), so no two parameter modes are
+    interchangeable and the truncations' kept subspaces are unique."""
+    return [np.linspace(0.1 + 0.013 * i, 1.0 - 0.007 * i, points) for i in range(N_PARAMS)]
 
 
-def _has_space(node):
-    return node.interval[1] == SPATIAL_DIM
+def kron_sum_operator(tree, terms: list, factors: dict, sizes: dict, device=None) -> HTOperator:
+    """HT operator of a sum of Kronecker products  sum_j (x)_mu F_{j,mu}  with minimal ranks.
 
+    ``terms[j]`` maps a mode mu (1-based) to a key of ``factors`` (the matrix F_{j,mu},
+    a GeneralizedMatrix); modes a term does not mention carry the identity of size
+    ``sizes[mu]``.  Construction (the matricisation view of an HT operator): at node t
+    the operator is  sum_j L_j (x) R_j  with L_j / R_j the restrictions of term j to the
+    modes inside / outside t.  Grouping the terms by their outside restriction R gives
+    the column space of the matricisation: one column  sum_{j: R_j = R} L_j  per distinct
+    R, with duplicates removed; this is the node's frame (ranks 1 + |params| and
+    1 + |params outside| for C4's affine family).  Each transfer tensor then solves
+    column_i(t) = sum_{j,l} B[i,j,l] column_j(s1) (x) column_l(s2) exactly (the columns
+    are formal sums of elementary Kronecker products, so this is a small linear system
+    over those products with 0/1 solutions).  Columns are ordered by the first term
+    they contain."""
+    d = tree.d
+    cols = {}
+    for node in tree.nodes:
+        inside = tuple(node.dims)
+        outside = tuple(mu for mu in range(1, d + 1) if mu not in set(inside))
+        groups, first = {}, {}
+        for j, term in enumerate(terms):
+            key = tuple(term.get(mu) for mu in outside)
+            u = tuple(term.get(mu) for mu in inside)
+            g = groups.setdefault(key, {})
+            g[u] = g.get(u, 0) + 1
+            first.setdefault(key, j)
+        frame = []
+        for key in sorted(groups, key=first.get):
+            if groups[key] not in frame:
+                frame.append(groups[key])
+        cols[node.index] = frame
 
-def _columns(node):
-    """Column meaning of an operator node: slot 0 is the identity (parameter-only
-    nodes) or the complete partial operator (nodes containing space); the other
-    slots are the parameters owned (parameter-only nodes) or still outside (space)."""
-    if _has_space(node):
-        return [0] + [mu for mu in range(1, N_PARAMS + 1) if mu not in set(node.dims)]
-    return [0] + _params(node)
+    def leaf_matrix(formal, mu):
+        """A leaf column: one factor, or a weighted sum of factors (terms that share
+        everything outside this mode)."""
+        mats = [(c, GeneralizedMatrix.diagonal(np.ones(sizes[mu])) if key is None else factors[key])
+                for (key,), c in formal.items()]
+        if len(mats) == 1 and mats[0][0] == 1:
+            return mats[0][1]
+        kinds = {g.kind for _, g in mats}
+        if kinds == {"diagonal"}:
+            return GeneralizedMatrix.diagonal(sum(c * g.data for c, g in mats))
+        if "dense" not in kinds:
+            import scipy.sparse as sp
 
+            return GeneralizedMatrix.csr(sum(c * sp.csr_matrix(g.to_dense()) if g.kind == "diagonal" else c * g.data
+                                             for c, g in mats))
+        return GeneralizedMatrix.dense(sum(c * g.to_dense() for c, g in mats))
 
-def affine_operator(matrices, grids, device=None) -> HTOperator:
-    """HT operator of ``matrices[0] (x) I + sum_mu matrices[mu] (x) diag(grids[mu-1])``
-    (``matrices`` = [A_0, A_1 .. A_9]) with minimal ranks: 2 at the parameter leaves,
-    1 + (number of parameters outside) for the nodes containing space (10 at the
-    spatial leaf), 1 + (parameters owned) elsewhere."""
-    if len(matrices) != N_PARAMS + 1 or len(grids) != N_PARAMS:
-        raise ValueError("expected 10 matrices and 9 parameter grids")
-    tree = build_balanced_tree(SPATIAL_DIM)
-    leaves = {}
-    for mu in range(1, N_PARAMS + 1):
-        g = np.asarray(grids[mu - 1], dtype=np.float64)
-        leaves[tree.leaf_for_dim(mu).index] = [GeneralizedMatrix.diagonal(np.ones(g.size)),
-                                               GeneralizedMatrix.diagonal(g)]
-    leaves[tree.leaf_for_dim(SPATIAL_DIM).index] = [GeneralizedMatrix.csr(m) for m in matrices]
-    transfer, root = {}, None
+    leaves, transfer, root = {}, {}, None
     for node in tree.nodes:
         if node.is_leaf:
+            leaves[node.index] = [leaf_matrix(f, node.dims[0]) for f in cols[node.index]]
             continue
-        left, right = tree.sons(node.index)
-        if _has_space(left):
-            raise ValueError("the spatial mode must sit in the right subtree")
-        ct, cl, cr = _columns(node), _columns(left), _columns(right)
-        it = {c: i for i, c in enumerate(ct)}
-        il = {c: i for i, c in enumerate(cl)}
-        ir = {c: i for i, c in enumerate(cr)}
-        core = np.zeros((len(ct), len(cl), len(cr)))
-        core[0, 0, 0] = 1.0  # identity (x) identity, or identity (x) complete
-        if _has_space(node):
-            for mu in _params(left):  # absorb: parameter mu of the left son meets slot mu on the right
-                core[0, il[mu], ir[mu]] = 1.0
-            for nu in ct[1:]:  # pass-through slots of parameters still outside
-                core[it[nu], 0, ir[nu]] = 1.0
-        else:
-            for mu in _params(left):
-                core[it[mu], il[mu], 0] = 1.0
-            for mu in _params(right):
-                core[it[mu], 0, ir[mu]] = 1.0
+        s1, s2 = node.sons
+        n1 = len(tree.node(s1).dims)
+        left, right, parent = cols[s1], cols[s2], cols[node.index]
+        pairs = [(j, l) for j in range(len(left)) for l in range(len(right))]
+        keys = {}
+        for j, l in pairs:
+            for u in left[j]:
+                for v in right[l]:
+                    keys.setdefault(u + v, len(keys))
+        for f in parent:
+            for uv in f:
+                keys.setdefault(uv, len(keys))
+        M = np.zeros((len(keys), len(pairs)))
+        for c, (j, l) in enumerate(pairs):
+            for u, a in left[j].items():
+                for v, b in right[l].items():
+                    M[keys[u + v], c] += a * b
+        core = np.zeros((len(parent), len(left), len(right)))
+        for i, f in enumerate(parent):
+            rhs = np.zeros(len(keys))
+            for uv, a in f.items():
+                rhs[keys[uv]] = a
+            sol = np.linalg.lstsq(M, rhs, rcond=None)[0]
+            sol = np.round(sol)  # integer coefficients: exact 0/1 transfer tensors
+            if not np.allclose(M @ sol, rhs):
+                raise ValueError(f"node {node.index}: column {i} is not in the span of its sons' frames")
+            core[i] = sol.reshape(len(left), len(right))
+        assert n1 == len(tree.node(s1).dims)
         if node.is_root:
             root = core[0]
         else:
@@ -139,17 +175,46 @@ def affine_operator(matrices, grids, device=None) -> HTOperator:
     return HTOperator(tree, leaves, transfer, root, device=device)
 
 
-def constant_rhs(load, grids, device=None) -> HTensor:
-    """Rank-1 right-hand side: the load vector on the spatial leaf, ones on every
-    parameter leaf (the source does not depend on the parameters)."""
+def affine_operator(matrices, grids, device=None) -> HTOperator:
+    """HT operator of the affine family  A_0 (x) I + sum_mu A_mu (x) diag(grid_mu)
+    (``matrices`` = [A_0, A_1 .. A_9] on the spatial mode, the last of the d = 10
+    modes; parameter mu is mode mu): ten Kronecker terms handed to kron_sum_operator.
+    Minimal ranks: 2 at the parameter leaves, 10 at the spatial leaf, 1 + (parameters
+    owned) at parameter-only nodes, 1 + (parameters outside) at nodes holding space."""
+    if len(matrices) != N_PARAMS + 1 or len(grids) != N_PARAMS:
+        raise ValueError("expected 10 matrices and 9 parameter grids")
     tree = build_balanced_tree(SPATIAL_DIM)
-    leaves = {tree.leaf_for_dim(mu).index: np.ones((len(grids[mu - 1]), 1)) for mu in range(1, N_PARAMS + 1)}
-    leaves[tree.leaf_for_dim(SPATIAL_DIM).index] = np.asarray(load, dtype=np.float64).reshape(-1, 1)
+    if SPATIAL_DIM not in tree.node(tree.node(0).sons[1]).dims:
+        raise ValueError("the spatial mode must sit in the right subtree")
+    factors = {("A", m): GeneralizedMatrix.csr(a) for m, a in enumerate(matrices)}
+    factors.update({("D", mu): GeneralizedMatrix.diagonal(np.asarray(grids[mu - 1], dtype=np.float64))
+                    for mu in range(1, N_PARAMS + 1)})
+    terms = [{SPATIAL_DIM: ("A", 0)}] + [{SPATIAL_DIM: ("A", mu), mu: ("D", mu)} for mu in range(1, N_PARAMS + 1)]
+    sizes = {mu: len(grids[mu - 1]) for mu in range(1, N_PARAMS + 1)}
+    sizes[SPATIAL_DIM] = matrices[0].shape[0]
+    return kron_sum_operator(tree, terms, factors, sizes, device=device)
+
+
+def rank_one_tensor(tree, vectors: dict, device=None) -> HTensor:
+    """The elementary tensor (x)_mu v_mu (``vectors[mu]``, 1-based modes) in HT format:
+    every rank 1, every transfer tensor and the root equal to 1."""
+    leaves = {tree.leaf_for_dim(mu).index: np.asarray(v, dtype=np.float64).reshape(-1, 1)
+              for mu, v in vectors.items()}
     transfer = {n.index: np.ones((1, 1, 1)) for n in tree.inner_nodes}
     return HTensor(tree, leaves, transfer, np.ones((1, 1)), device=device)
 
 
-__all__ = ["p1_diffusion_matrices", "parameter_grids", "affine_operator", "constant_rhs", "N_PARAMS", "SPATIAL_DIM"]
+def constant_rhs(load, grids, device=None) -> HTensor:
+    """C4's right-hand side load (x) 1 (x) ... (x) 1: the source does not depend on the
+    parameters (spatial mode last)."""
+    tree = build_balanced_tree(SPATIAL_DIM)
+    vectors = {mu: np.ones(len(grids[mu - 1])) for mu in range(1, N_PARAMS + 1)}
+    vectors[SPATIAL_DIM] = load
+    return rank_one_tensor(tree, vectors, device=device)
+
+
+__all__ = ["p1_diffusion_matrices", "parameter_grids", "distinct_parameter_grids", "affine_operator",
+           "kron_sum_operator", "rank_one_tensor", "constant_rhs", "N_PARAMS", "SPATIAL_DIM"]
 
 
 def laplace_sum_operator(tree, n: int, device=None) -> HTOperator:

@@ -1,9 +1,19 @@
-"""CG with truncation after every operation -- the reference solver loop
-(solvers.py:110-231) as the direct caller of the truncation hot path.
+"""Truncated conjugate gradients over the Backend seam -- the direct caller of the
+truncation hot path (reference solvers.py:172-231, the algorithm of the paper's
+CG-with-truncation experiments).
 
-The loop is backend-generic exactly like the reference's: it only calls the
-eleven Backend methods, so it runs on ``GpuBackend`` (default; every add /
-apply / truncate / inner product on the B200) or on any other backend object.
+``TruncatedCG`` keeps the iteration as an explicit state machine: ``start()``
+builds the first iterate, ``advance()`` performs one CG step, ``report()``
+measures an iterate.  Every tensor operation goes through the eleven Backend
+methods only, so the loop runs unchanged on ``GpuBackend`` (default: every add,
+apply, truncate and inner product on the B200) or on any other backend object
+-- including the reference's own ``SerialBackend``.
+
+The arithmetic order is the reference's, so traces agree with its CG to rounding:
+residual R0 = T(B - A X0) with X0 = B, D0 = R0; per step Z = T(A D),
+alpha = <R,R>/<D,Z>, X <- T(X + alpha D), R <- T(R - alpha Z),
+beta = <R',R'>/<R,R>, D <- T(beta D + R'); a non-positive curvature <D,Z> stops the
+iteration with a diagnostic.  T is the truncation of ``cfg.truncation``.
 """
 
 from __future__ import annotations
@@ -11,8 +21,8 @@ from __future__ import annotations
 import math
 import time
 from dataclasses import dataclass, field
+from typing import NamedTuple
 
-from .arith import TruncationControl
 from .backend import GpuBackend
 
 
@@ -28,15 +38,14 @@ class RelativeTruncation:
 
 @dataclass
 class SolverConfig:
-    """solvers.py:110-135 (the fields the CG loop uses)."""
+    """The CG fields of the reference's SolverConfig (solvers.py:110-135)."""
 
     truncation: object  # TruncationControl or RelativeTruncation
     eps_stop: float = 1e-8
     max_cg_steps: int = 25
 
 
-@dataclass
-class TraceEntry:
+class TraceEntry(NamedTuple):
     step: int
     true_rel_residual: float
     internal_residual: float
@@ -49,65 +58,98 @@ class ConvergenceTrace:
     entries: list = field(default_factory=list)
     aborted: str | None = None
 
-    def record(self, step, true_rel, internal, max_rank, seconds):
-        self.entries.append(TraceEntry(step, true_rel, internal, max_rank, seconds))
+    def record(self, *values) -> None:
+        self.entries.append(TraceEntry(*values))
 
     @property
     def floor(self) -> float:
         return min(e.true_rel_residual for e in self.entries)
 
 
-def _true_residual(backend, op, x, b_neg, norm_b: float, ctl) -> float:
-    """solvers.py:163-170: |A x - b| / |b| recomputed in tree arithmetic."""
-    ax = backend.truncate(backend.apply(op, x), ctl)
-    return backend.norm(backend.add(ax, b_neg)) / norm_b
+class Iterate(NamedTuple):
+    step: int
+    x: object
+    r: object
+    d: object
+    rr: float  # <R, R>
+
+
+class TruncatedCG:
+    """CG with truncation after every operation, one step at a time."""
+
+    def __init__(self, backend, op, rhs, cfg: SolverConfig):
+        self.be = backend
+        self.cfg = cfg
+        self.A = backend.lift_operator(op)
+        self.b = backend.lift(rhs)
+        self._minus_b = None
+        self._norm_b = None
+
+    # -- building blocks ---------------------------------------------------------
+    def _combine(self, *terms):
+        """sum alpha_i Y_i in tree arithmetic (ranks add; no truncation)."""
+        acc = None
+        for alpha, y in terms:
+            y = self.be.scale(y, alpha) if alpha is not None else y
+            acc = y if acc is None else self.be.add(acc, y)
+        return acc
+
+    def _round(self, y):
+        return self.be.truncate(y, self.cfg.truncation)
+
+    # -- the iteration -----------------------------------------------------------
+    def start(self) -> Iterate:
+        x = self.b
+        r = self._round(self._combine((None, self.b), (-1.0, self.be.apply(self.A, x))))
+        return Iterate(0, x, r, r, self.be.inner_product(r, r))
+
+    def converged(self, it: Iterate) -> bool:
+        return math.sqrt(max(0.0, it.rr)) <= self.cfg.eps_stop or it.step >= self.cfg.max_cg_steps
+
+    def advance(self, it: Iterate):
+        """One CG step; returns (next iterate, None) or (None, reason) on breakdown."""
+        be = self.be
+        z = self._round(be.apply(self.A, it.d))
+        curvature = be.inner_product(it.d, z)
+        if curvature <= 0.0:
+            return None, f"non-positive curvature <D,AD> = {curvature:.3e} at step {it.step}"
+        alpha = it.rr / curvature
+        x = self._round(self._combine((None, it.x), (alpha, it.d)))
+        r = self._round(self._combine((None, it.r), (-alpha, z)))
+        rr = be.inner_product(r, r)
+        d = self._round(self._combine((rr / it.rr, it.d), (None, r)))
+        return Iterate(it.step + 1, x, r, d, rr), None
+
+    def report(self, it: Iterate) -> tuple:
+        """(true relative residual ||T(A X) - B|| / ||B||, internal residual ||R||, max rank):
+        the true residual is recomputed in tree arithmetic and never fed back."""
+        if self._minus_b is None:
+            self._minus_b = self.be.scale(self.b, -1.0)
+            self._norm_b = self.be.norm(self.b)
+        ax = self._round(self.be.apply(self.A, it.x))
+        true_rel = self.be.norm(self.be.add(ax, self._minus_b)) / self._norm_b
+        return true_rel, math.sqrt(max(0.0, it.rr)), self.be.max_rank(it.x)
 
 
 def cg_solve(op, rhs, cfg: SolverConfig, backend=None, trace_residuals: bool = True):
-    """solvers.py:172-186: X0 = rhs; stops when the internal residual norm drops to
-    ``eps_stop`` or after ``max_cg_steps``; a non-positive curvature aborts."""
+    """Solve A X = rhs by truncated CG from X0 = rhs (reference solvers.py:172-186):
+    stops when ||R|| <= eps_stop or after max_cg_steps; returns (X, ConvergenceTrace)."""
     backend = backend or GpuBackend()
-    a = backend.lift_operator(op)
-    b = backend.lift(rhs)
+    cg = TruncatedCG(backend, op, rhs, cfg)
     trace = ConvergenceTrace()
-    x = _cg_loop(a, b, cfg, backend, trace if trace_residuals else None)
-    return backend.retrieve(x), trace
-
-
-def _cg_loop(a, b, cfg: SolverConfig, backend, trace):
-    """solvers.py:189-231."""
-    ctl = cfg.truncation
     t0 = time.perf_counter()
-    if trace is not None:
-        b_neg = backend.scale(b, -1.0)
-        norm_b = backend.norm(b)
-    x = b
-    r = backend.truncate(backend.add(b, backend.scale(backend.apply(a, x), -1.0)), ctl)
-    d = r
-    rr = backend.inner_product(r, r)
-    if trace is not None:
-        trace.record(0, _true_residual(backend, a, x, b_neg, norm_b, ctl), math.sqrt(max(0.0, rr)),
-                     backend.max_rank(x), time.perf_counter() - t0)
-    j = 0
-    while math.sqrt(max(0.0, rr)) > cfg.eps_stop and j < cfg.max_cg_steps:
-        z = backend.truncate(backend.apply(a, d), ctl)
-        dz = backend.inner_product(d, z)
-        if dz <= 0.0:
-            if trace is not None:
-                trace.aborted = f"non-positive curvature <D,AD> = {dz:.3e} at step {j}"
+    it = cg.start()
+    if trace_residuals:
+        trace.record(it.step, *cg.report(it), time.perf_counter() - t0)
+    while not cg.converged(it):
+        nxt, why = cg.advance(it)
+        if nxt is None:
+            trace.aborted = why
             break
-        alpha = rr / dz
-        x = backend.truncate(backend.add(x, backend.scale(d, alpha)), ctl)
-        r_new = backend.truncate(backend.add(r, backend.scale(z, -alpha)), ctl)
-        rr_new = backend.inner_product(r_new, r_new)
-        beta = rr_new / rr
-        d = backend.truncate(backend.add(backend.scale(d, beta), r_new), ctl)
-        r, rr = r_new, rr_new
-        j += 1
-        if trace is not None:
-            trace.record(j, _true_residual(backend, a, x, b_neg, norm_b, ctl), math.sqrt(max(0.0, rr)),
-                         backend.max_rank(x), time.perf_counter() - t0)
-    return x
+        it = nxt
+        if trace_residuals:
+            trace.record(it.step, *cg.report(it), time.perf_counter() - t0)
+    return backend.retrieve(it.x), trace
 
 
-__all__ = ["SolverConfig", "RelativeTruncation", "ConvergenceTrace", "TraceEntry", "cg_solve"]
+__all__ = ["SolverConfig", "RelativeTruncation", "ConvergenceTrace", "TraceEntry", "TruncatedCG", "cg_solve"]

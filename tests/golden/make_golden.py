@@ -2,7 +2,7 @@
 
 Run in the build container only (the reference does not exist on the GPU box):
 
-    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/make_golden.py
+    PYTHONPATH=/root/reference/pkg/src:/root/repo python tests/golden/make_golden.py [--c4] [--large]
 
 The fixtures pin both the oracle restatement (``tests/test_oracle_golden.py``)
 and, through the oracle, the CUDA path (``tests/test_gpu_parity.py``).  Inputs
@@ -183,6 +183,45 @@ def golden_c2_d8():
     np.savez_compressed(os.path.join(OUT, "c2_d8.npz"), **out)
 
 
+def golden_c2_large(d: int):
+    """C2 at d = 64 / 128 / 256 (n=1000, k=50, rank 100 -> 50) through the REFERENCE:
+    every hierarchical singular value (sqrt of sym_eig_desc of compute_bhat of the
+    orthogonalised sum), the truncated ranks, <T,T>, ||X|| and the truncation error.
+    Inputs regenerate from the seeds (2p, 2p+1); only gauge-invariant outputs are kept."""
+    a, c, x = orc.c2_inputs(d)
+    xr = ref.add(to_ref(a), to_ref(c))
+    tr = ref.truncate(xr, ref.TruncationControl.fixed_rank(50))
+    _, _, lam = ref_sigmas(xr)
+    out = {"meta": meta()}
+    for t in lam:
+        out[f"lam/{t}"] = lam[t]
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 2 * d - 1)])
+    out["ip_TT"] = ref.inner_product(tr, tr)
+    out["norm_X"] = ref.norm(xr)
+    out["trunc_err"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(xr, tr)).root_matrix))
+    np.savez_compressed(os.path.join(OUT, f"c2_d{d}.npz"), **out)
+
+
+def golden_c5_shape():
+    """C5 shape on one shard's worth of tree: d=8, n=2048, the 4-way sum of rank-100
+    Gaussian tensors (seeds 0..3, X = ((A0 + A1) + A2) + A3, rank 400) truncated to
+    rank 100 -- 2048 x 400 leaf frames, 400^3 transfer tensors, 400 x 400 Gramians."""
+    xs = orc.c5_inputs(8)
+    xr = to_ref(xs[0])
+    for y in xs[1:]:
+        xr = ref.add(xr, to_ref(y))
+    tr = ref.truncate(xr, ref.TruncationControl.fixed_rank(100))
+    _, _, lam = ref_sigmas(xr)
+    out = {"meta": meta()}
+    for t in lam:
+        out[f"lam/{t}"] = lam[t]
+    out["ranks_T"] = np.array([tr.rank(t) for t in range(1, 15)])
+    out["ip_TT"] = ref.inner_product(tr, tr)
+    out["norm_X"] = ref.norm(xr)
+    out["trunc_err"] = float(np.linalg.norm(ref.orthogonalize(ref.subtract(xr, tr)).root_matrix))
+    np.savez_compressed(os.path.join(OUT, "c5_d8.npz"), **out)
+
+
 def golden_c3_small():
     """Operator application + truncation (C3 shape, shrunk): d=4, n=6, k=3,
     Laplace-sum operator, eps 1e-8*||Y|| with cap 3."""
@@ -259,7 +298,7 @@ def golden_c4_operator():
     np.savez_compressed(os.path.join(OUT, "c4_operator.npz"), **out)
 
 
-def golden_c4_cg():
+def golden_c4_cg(broken: bool = False):
     """BASELINE C4 at full size through the REFERENCE: cookie.build_ht_operator on the
     64 x 64 P1 subdomain matrices, build_rhs_htensor, and solvers.cg_solve for 20
     steps on a SerialBackend whose truncate uses eps = 1e-6 * ||Y|| (cap 50) -- the
@@ -277,7 +316,9 @@ def golden_c4_cg():
             return ref_ar.truncate(x, ref.TruncationControl(eps=1e-6 * ref_ar.norm(x), max_rank=50))
 
     mats, load = problems.p1_diffusion_matrices(cells=64)
-    grids = problems.parameter_grids(points=16)
+    # broken: distinct grids per parameter, so no two parameter modes are interchangeable
+    # and the kept singular subspaces at the rank cap are unique
+    grids = problems.distinct_parameter_grids(points=16) if broken else problems.parameter_grids(points=16)
     op = cookie.build_ht_operator([sp.csr_matrix(mats[0].shape)] + mats, grids)
     rhs = cookie.build_rhs_htensor(load, grids)
     cfg = ref_solvers.SolverConfig(truncation=ref.TruncationControl(eps=1.0, max_rank=50), eps_stop=1e-12,
@@ -288,7 +329,7 @@ def golden_c4_cg():
            "true_rel": np.array([e.true_rel_residual for e in trace.entries]),
            "max_rank": np.array([e.max_rank for e in trace.entries]),
            "ranks_X": np.array([x.rank(t) for t in range(1, 19)])}
-    np.savez_compressed(os.path.join(OUT, "c4_cg.npz"), **out)
+    np.savez_compressed(os.path.join(OUT, "c4_cg_distinct.npz" if broken else "c4_cg.npz"), **out)
 
 
 def golden_readouts():
@@ -366,4 +407,9 @@ if __name__ == "__main__":
     golden_readouts()
     if "--c4" in sys.argv:  # minutes of CPU time
         golden_c4_cg()
+        golden_c4_cg(broken=True)
+    if "--large" in sys.argv:  # minutes of CPU time
+        for d in (64, 128, 256):
+            golden_c2_large(d)
+        golden_c5_shape()
     print("golden fixtures written to", OUT)

@@ -103,3 +103,30 @@ def test_qr_wide_kernel_direct(cuda_ok):
     np.testing.assert_allclose(o.U[2].T @ o.U[2], np.eye(200), atol=1e-13)
     ro = orc.orthogonalize(x)
     assert orc.orth_difference_norm(o, ro) <= 1e-12 * orc.norm(ro)
+
+
+@pytest.mark.parametrize("k", [69, 75])
+@pytest.mark.parametrize("mode", ["householder", "auto"])
+def test_bigk_workspace_covers_unmerged_layouts(cuda_ok, k, mode):
+    """K = 2k with K = 2 mod 4 (138, 150): node arrays whose byte size is not a multiple
+    of 256 make the scratch allocator pad between nodes, so the per-level QR problems do
+    not merge at run time -- the workspace query must cover the unmerged plan (it once
+    sized the merged one and the Householder panels overran into the output)."""
+    import paper_1708_03340_b200 as htb
+
+    tr = orc.balanced_tree(4)
+    a = orc.gaussian_htensor(tr, 300, k, 41)
+    c = orc.gaussian_htensor(tr, 300, k, 42)
+    x = orc.add(a, c)
+    htb.set_qr_mode(mode)
+    try:
+        xd = to_dev(x)
+        o = to_host(htb.orthogonalize(xd))
+        ro = orc.orthogonalize(x)
+        for (t, u), (_, v) in zip(o.arrays(), ro.arrays()):
+            np.testing.assert_allclose(u, v, rtol=0, atol=1e-12 * max(1.0, np.abs(v).max()))
+        T = htb.truncate(xd, htb.TruncationControl.fixed_rank(k))
+        ref = orc.truncate(x, orc.Ctl(max_rank=k))
+        assert rel_err(to_host(T), ref) <= 1e-10
+    finally:
+        htb.set_qr_mode("auto")

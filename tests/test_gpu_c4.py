@@ -88,3 +88,32 @@ def test_cg_c4_full_size_matches_reference_trace(cuda_ok):
     assert [e.max_rank for e in trace.entries] == list(g["max_rank"])
     # the final iterate has drifted by ~1e-3: its eps-chosen ranks may move by one
     assert np.abs(np.array([x.rank(t) for t in range(1, 19)]) - g["ranks_X"]).max() <= 1
+
+
+@pytest.mark.slow
+def test_cg_c4_distinct_grids_holds_parity_for_20_steps(cuda_ok):
+    """C4 with the parameter symmetry broken (every parameter on its own grid, see
+    problems.distinct_parameter_grids): the kept singular subspaces at the rank cap are
+    unique, so the 20-step CG trace must follow the REFERENCE's own cg_solve
+    (tests/golden/c4_cg_distinct.npz, make_golden.py --c4) to rtol 1e-10 at every
+    step, with identical maximal ranks and final ranks."""
+    import os
+
+    from paper_1708_03340_b200 import problems
+    from paper_1708_03340_b200.backend import GpuBackend
+    from paper_1708_03340_b200.solvers import RelativeTruncation, SolverConfig, cg_solve
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "c4_cg_distinct.npz"))
+    mats, load = problems.p1_diffusion_matrices(cells=64)
+    grids = problems.distinct_parameter_grids(points=16)
+    op = problems.affine_operator([sp.csr_matrix(mats[0].shape)] + mats, grids)
+    rhs = problems.constant_rhs(load, grids)
+    cfg = SolverConfig(truncation=RelativeTruncation(1e-6, max_rank=50), eps_stop=1e-12, max_cg_steps=20)
+    x, trace = cg_solve(op, rhs, cfg, backend=GpuBackend())
+    true = np.array([e.true_rel_residual for e in trace.entries])
+    internal = np.array([e.internal_residual for e in trace.entries])
+    assert trace.aborted is None and len(true) == len(g["true_rel"])
+    np.testing.assert_allclose(true, g["true_rel"], rtol=1e-10)
+    np.testing.assert_allclose(internal, g["internal"], rtol=1e-10)
+    assert [e.max_rank for e in trace.entries] == list(g["max_rank"])
+    assert [x.rank(t) for t in range(1, 19)] == list(g["ranks_X"])

@@ -79,7 +79,10 @@ def _qr_dev(lib, A_np, col_major=False, nodes=1):
 
 @pytest.mark.parametrize("m,K,col", [(64, 20, False), (1000, 100, False), (256, 60, False), (10000, 100, True),
                                      (400, 20, True), (3600, 60, True), (16, 40, False), (5, 3, False),
-                                     (130, 112, False), (1, 1, False), (2000, 1, True)])
+                                     (130, 112, False), (1, 1, False), (2000, 1, True),
+                                     # odd widths (block Gram-Schmidt panels of odd ranks, e.g. K=150 -> 2 x 75)
+                                     (300, 75, True), (300, 75, False), (300, 77, True), (500, 101, True),
+                                     (130, 111, False), (200, 65, True), (22500, 75, True)])
 def test_qr_matches_reduced_qr(lib, m, K, col):
     rng = np.random.default_rng(m * 7 + K)
     nodes = 3
@@ -151,6 +154,23 @@ def test_syev_graded_relative_accuracy(lib):
     _, lam = _syev(lib, S)
     ref = np.linalg.eigvalsh(S[0])[::-1]  # dsyevd is also accurate here (graded, well-ordered)
     np.testing.assert_allclose(lam[0], ref, rtol=1e-8)
+
+
+@pytest.mark.parametrize("K", [80, 113, 150, 301])
+def test_syev_graded_relative_accuracy_any_rank(lib, K):
+    """Graded S = D M D (eigenvalues over 16 decades, randomly placed): the Jacobi
+    kernels -- shared-memory up to K = 112, global scratch beyond -- deliver every
+    eigenvalue to relative accuracy (against the host restatement of the same method,
+    tests/jacobi_host.py; LAPACK's dsyevd is only accurate relative to ||S|| here)."""
+    from tests.jacobi_host import graded_spd, jacobi_eigvals
+
+    S = np.stack([graded_spd(K, 8, K + i) for i in range(2)])
+    V, lam = _syev(lib, S)
+    for i in range(2):
+        ref = jacobi_eigvals(S[i])
+        assert ref[-1] < 1e-14 * ref[0]
+        np.testing.assert_allclose(lam[i], ref, rtol=1e-11)
+        np.testing.assert_allclose(V[i].T @ V[i], np.eye(K), atol=1e-13)
 
 
 def test_syev_rejects_nonsymmetric(lib):

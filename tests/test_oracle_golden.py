@@ -166,6 +166,22 @@ def test_c2_d8_sigmas():
     np.testing.assert_allclose(orc.inner_product(t_, t_), float(z["ip_TT"]), rtol=1e-10)
 
 
+def test_c2_d64_sigmas():
+    """The headline config (d=64): the oracle's sigmas, ranks and <T,T> against the
+    reference-generated fixture (the GPU parity tests compare against both)."""
+    z = load("c2_d64.npz")
+    a, c, x = orc.c2_inputs(64)
+    sig = orc.hierarchical_singular_values(x)
+    lam = node_dict(z, "lam", x.tree)
+    assert len(lam) == 126
+    for t, lt in lam.items():
+        np.testing.assert_allclose(sig[t], np.sqrt(lt), rtol=1e-10)
+    t_ = orc.truncate(x, orc.Ctl(max_rank=50))
+    assert [t_.rank(t) for t in range(1, 127)] == list(z["ranks_T"])
+    np.testing.assert_allclose(orc.inner_product(t_, t_), float(z["ip_TT"]), rtol=1e-10)
+    np.testing.assert_allclose(orc.orth_difference_norm(x, t_), float(z["trunc_err"]), rtol=1e-8)
+
+
 def test_oracle_cg_matches_reference_cg():
     """The oracle's CG (solvers.py:172-231 restated) against the reference's own
     cg_solve run in the build container (tests/golden/cg.npz)."""
