@@ -139,13 +139,24 @@ int ht_status(int32_t clear, int32_t* status, ht_stream_t stream);
  *   phase 2 EIG    : eigendecomposition + rank choice of masked non-root nodes
  *   phase 3 PROJECT: projection of masked nodes into `out` (unmasked sons' eigen-
  *                    vectors must be in their slots)
- * Node arrays of unowned nodes are never touched (any non-null pointer). */
+ * `owned` (host [2d-1], or NULL = every node) is the node set this shard owns for the
+ * whole truncation: the workspace then holds the orthogonalised arrays, R factors,
+ * Gramians and eigenpairs of the owned nodes and of their sons (the message slots)
+ * only, and phase scratch sized for the owned nodes -- ht_truncate_workspace_size_
+ * sharded gives its size (C5, d = 256 on 8 GPUs: ~1/8 of the whole-tree plan).  Every
+ * phase mask must lie inside `owned`; the same `owned` must be passed to every phase
+ * and slot query of one truncation.
+ * Node arrays of unowned nodes are never touched (any non-null pointer).
+ * Replaces the node-worker protocol of dist.py:239-333 (_cmd_orth / _cmd_truncate). */
+int ht_truncate_workspace_size_sharded(const ht_tensor* x, const uint8_t* owned, size_t* bytes);
 int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int32_t phase,
-                        const uint8_t* mask, const ht_tensor* out, ht_stream_t stream);
+                        const uint8_t* mask, const uint8_t* owned, const ht_tensor* out, ht_stream_t stream);
 /* Device pointer + element count of a per-node workspace slot of the truncation:
  * kind 0 R factor, 1 Gramian, 2 eigenvectors, 3 eigenvalues, 4 ranks (int32,
- * all nodes + status word), 5 orthogonalised node array.  Host-only query. */
-int ht_truncate_slot(const ht_tensor* x, void* ws, int32_t kind, int32_t node, void** ptr, int64_t* count);
+ * all nodes + status word), 5 orthogonalised node array.  Host-only query; with
+ * `owned`, only owned nodes and their sons have slots. */
+int ht_truncate_slot(const ht_tensor* x, void* ws, const uint8_t* owned, int32_t kind, int32_t node, void** ptr,
+                     int64_t* count);
 
 /* Hierarchical singular values: after ht_truncate_ranks, copy the descending,
  * clamped eigenvalues lambda_t of every non-root node's reduced Gramian
@@ -179,6 +190,14 @@ int ht_scale(const double* x, double* y, int64_t count, double alpha, ht_stream_
 int ht_inner_product_workspace_size(const ht_tensor* a, const ht_tensor* c, size_t* bytes);
 int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws_bytes,
                      double* result_dev, double* result_host, ht_stream_t stream);
+/* Sharded inner product (reference dist.py:239-254 GRAM_UP wave, 516-524): the Phi
+ * recursion of the nodes with mask[t] != 0 only (levels bottom-up); Phi of unmasked
+ * sons must already sit in their slots (received from the shard that owns them).
+ * If the root is masked the result lands in result_dev.  Same workspace size as
+ * ht_inner_product; ht_inner_product_slot gives Phi_t's slot (k_a x k_c, row-major). */
+int ht_inner_product_sharded(const ht_tensor* a, const ht_tensor* c, const uint8_t* mask, void* ws, size_t ws_bytes,
+                             double* result_dev, ht_stream_t stream);
+int ht_inner_product_slot(const ht_tensor* a, const ht_tensor* c, void* ws, int32_t node, void** ptr, int64_t* count);
 
 /* apply_operator (arith.py:378-395): out ranks are op.rank * x.rank. */
 /* Entry evaluation (reference arith.py:221-243, evaluate_entry): out[b] = X[idx[b, :]]
@@ -195,6 +214,10 @@ int ht_evaluate_weighted(const ht_tensor* x, const double* const* leaf_weights, 
                          double* out, ht_stream_t stream);
 
 int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream);
+/* apply_operator restricted to mask[t] != 0: node-local, so the sharded form
+ * (reference dist.py:324-333 _cmd_apply, 557-566) needs no communication. */
+int ht_apply_operator_sharded(const ht_operator* op, const ht_tensor* x, const uint8_t* mask, const ht_tensor* out,
+                              ht_stream_t stream);
 
 /* ---- node kernels (kernels.py primitives, batched) ------------------- */
 

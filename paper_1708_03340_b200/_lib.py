@@ -34,10 +34,10 @@ EXPORTS = (
     "ht_gramians_workspace_size", "ht_gramians",
     "ht_add", "ht_add_sharded", "ht_scale",
     "ht_inner_product_workspace_size", "ht_inner_product",
-    "ht_apply_operator",
+    "ht_apply_operator", "ht_apply_operator_sharded", "ht_inner_product_sharded", "ht_inner_product_slot",
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
     "ht_launch_count", "ht_profile_enable", "ht_profile_report", "ht_profile_log",
-    "ht_truncate_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_qr_fallback_count", "ht_set_eig_mode",
+    "ht_truncate_sharded", "ht_truncate_workspace_size_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_qr_fallback_count", "ht_set_eig_mode",
     "ht_set_graph_mode", "ht_graph_stats", "ht_graph_relocations", "ht_status", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
 )
 
@@ -98,11 +98,15 @@ def _declare(lib):
         "ht_inner_product_workspace_size": ([t, t, sz], ctypes.c_int),
         "ht_inner_product": ([t, t, _vp, ctypes.c_size_t, _vp, P(ctypes.c_double), _vp], ctypes.c_int),
         "ht_apply_operator": ([P(COperator), t, t, _vp], ctypes.c_int),
+        "ht_apply_operator_sharded": ([P(COperator), t, _vp, t, _vp], ctypes.c_int),
+        "ht_inner_product_sharded": ([t, t, _vp, _vp, ctypes.c_size_t, _vp, _vp], ctypes.c_int),
+        "ht_inner_product_slot": ([t, t, _vp, ctypes.c_int32, P(ctypes.c_void_p), _i64p], ctypes.c_int),
         "ht_qr_workspace_size": ([ctypes.c_int64] * 3 + [sz], ctypes.c_int),
         "ht_qr_batched": ([ctypes.c_int64] * 3 + [_vp] + [ctypes.c_int64] * 3 + [_vp] + [ctypes.c_int64] * 3
                           + [_vp] + [ctypes.c_int64] * 2 + [_vp, ctypes.c_size_t, _vp], ctypes.c_int),
-        "ht_truncate_sharded": ([t, ctl, _vp, ctypes.c_size_t, ctypes.c_int32, _vp, t, _vp], ctypes.c_int),
-        "ht_truncate_slot": ([t, _vp, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_void_p), _i64p], ctypes.c_int),
+        "ht_truncate_sharded": ([t, ctl, _vp, ctypes.c_size_t, ctypes.c_int32, _vp, _vp, t, _vp], ctypes.c_int),
+        "ht_truncate_workspace_size_sharded": ([t, _vp, sz], ctypes.c_int),
+        "ht_truncate_slot": ([t, _vp, _vp, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_void_p), _i64p], ctypes.c_int),
         "ht_launch_count": ([], ctypes.c_int64),
         "ht_set_qr_mode": ([ctypes.c_int], ctypes.c_int),
         "ht_qr_fallback_count": ([], ctypes.c_int64),

@@ -181,7 +181,13 @@ struct View {
   std::vector<double*> p;
   bool orth = false;
   std::vector<unsigned char> mask;  // empty: every node (else: nodes this shard processes)
+  // empty: every node; else the nodes this shard owns -- the truncate workspace then
+  // holds state only for owned nodes and their sons (the message slots), sized for them
+  std::vector<unsigned char> owned;
   bool on(int t) const { return mask.empty() || mask[t] != 0; }
+  bool needed(int t) const {
+    return owned.empty() || owned[t] != 0 || (t > 0 && owned[T->father[t]] != 0);
+  }
   long long k1(int t) const { return k[T->son1[t]]; }
   long long k2(int t) const { return k[T->son2[t]]; }
   long long elems(int t) const {
@@ -433,6 +439,29 @@ void orth_slots(const View& x, OrthPlan& op, Arena& ar) {
   }
 }
 
+// Nodes of one tree level (masked), split into consecutive groups whose per-phase
+// scratch stays under kChunkBytes: at C5 (400^3 transfer tensors) a level's absorb /
+// Gramian / projection temporaries would otherwise take tens of GB; at the C2 sizes
+// every level is one group (one launch per level, as before).
+constexpr double kChunkBytes = 4.0 * (1 << 30);
+
+template <class F>
+std::vector<std::vector<int>> level_chunks(const std::vector<int>& level, const View& x, F&& bytes) {
+  std::vector<std::vector<int>> out(1);
+  double acc = 0;
+  for (int t : level) {
+    if (!x.on(t)) continue;
+    const double b = bytes(t);
+    if (!out.back().empty() && acc + b > kChunkBytes) {
+      out.emplace_back();
+      acc = 0;
+    }
+    out.back().push_back(t);
+    acc += b;
+  }
+  return out;
+}
+
 int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar, cudaStream_t s, bool exec,
                       bool chol = false, int* fail = nullptr, int* n_chol = nullptr) {
   const Tree& T = *x.T;
@@ -443,16 +472,21 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   const size_t scratch_base = scratch_ar.off;
   size_t scratch_max = scratch_base;
   for (int l = T.depth; l >= 1; --l) {
+   const auto chunks = level_chunks(T.levels[l], x, [&](int t) {
+     if (T.leaf(t)) return 16.0 * x.n[t] * x.k[t];
+     return 24.0 * x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]];  // T1 + Bp + QR scratch
+   });
+   for (const auto& chunk : chunks) {
     scratch_ar.off = scratch_base;
     std::vector<GemmDesc> g2, g3;
     std::vector<SsDesc> sa2, sa3;
     std::vector<QrProblem> qs;
     std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
-    for (int t : T.levels[l])
+    for (int t : chunk)
       if (!T.leaf(t) && x.on(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
-    for (int t : T.levels[l])
+    for (int t : chunk)
       if (!T.leaf(t) && x.on(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
-    for (int t : T.levels[l]) {
+    for (int t : chunk) {
       if (!x.on(t)) continue;
       if (T.leaf(t)) {
         QrProblem q{};
@@ -556,6 +590,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       HT_TRY(qr_wide_batched(wide, s));
       HT_TRY(qr_batched(hh, s));
     }
+   }
   }
   // root: B_D <- R1 B_D R2^T (arith.py:144-145)
   scratch_ar.off = scratch_base;
@@ -698,10 +733,16 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     }
   }
   for (int l = 1; l < T.depth; ++l) {
+   std::vector<int> lev;
+   for (int t : T.levels[l])
+     if (!T.leaf(t)) lev.push_back(t);
+   // t1 (kt k1 k2) + split-K partials of the son Gramians (<= 4 (k1^2 + k2^2) for the
+   // split counts these shapes get) per node
+   for (const auto& inner : level_chunks(lev, o, [&](int t) {
+          const double k1 = (double)o.k[T.son1[t]], k2 = (double)o.k[T.son2[t]];
+          return 8.0 * o.k[t] * k1 * k2 + 8.0 * 160.0 * (k1 * k1 + k2 * k2);
+        })) {
     scratch_ar.off = base;
-    std::vector<int> inner;
-    for (int t : T.levels[l])
-      if (!T.leaf(t) && o.on(t)) inner.push_back(t);
     if (inner.empty()) continue;
     std::vector<GemmDesc> g1s, g2s;
     std::vector<SsDesc> s1s;
@@ -748,6 +789,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       HT_TRY(gemm_grouped(g2s, s, "gemm_gram_g"));
       HT_TRY(reduce_partials(rs, s));
     }
+   }
   }
   scratch_ar.off = mx;
   return kOk;
@@ -797,6 +839,7 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
     P.op.out.assign(T.nn, nullptr);
     const auto& ko = P.op.ko;
     for (int t = 0; t < T.nn; ++t) {
+      if (!x.needed(t)) continue;
       long long e;
       if (T.leaf(t)) e = x.n[t] * ko[t];
       else if (t == 0) e = ko[T.son1[t]] * ko[T.son2[t]];
@@ -804,7 +847,8 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
       P.op.out[t] = ar.take(e);
     }
     P.op.R.assign(T.nn, nullptr);
-    for (int t = 1; t < T.nn; ++t) P.op.R[t] = ar.take(ko[t] * x.k[t]);
+    for (int t = 1; t < T.nn; ++t)
+      if (x.needed(t)) P.op.R[t] = ar.take(ko[t] * x.k[t]);
     P.o.k = ko;
     P.o.p = P.op.out;
     P.o.orth = true;
@@ -813,18 +857,30 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   P.EV.assign(T.nn, nullptr);
   P.lam.assign(T.nn, nullptr);
   // G / EV / lam of all non-root nodes are contiguous so same-K nodes batch
-  for (int t = 1; t < T.nn; ++t) P.G[t] = ar.take(P.o.k[t] * P.o.k[t]);
-  for (int t = 1; t < T.nn; ++t) P.EV[t] = ar.take(P.o.k[t] * P.o.k[t]);
-  for (int t = 1; t < T.nn; ++t) P.lam[t] = ar.take(P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t)
+    if (x.needed(t)) P.G[t] = ar.take(P.o.k[t] * P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t)
+    if (x.needed(t)) P.EV[t] = ar.take(P.o.k[t] * P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t)
+    if (x.needed(t)) P.lam[t] = ar.take(P.o.k[t]);
   P.ranks = ar.take_int(T.nn + 2);
   P.status = P.ranks + T.nn;
   P.qr_fail = P.ranks + T.nn + 1;
   P.eigflag = ar.take_int(T.nn);
   P.eigwork.assign(T.nn, nullptr);
   for (int t = 1; t < T.nn; ++t)
-    if (P.o.k[t] > kEigMaxK) P.eigwork[t] = ar.take(eig_work_doubles((int)P.o.k[t]));
+    if (P.o.k[t] > kEigMaxK && (x.owned.empty() || x.owned[t]))
+      P.eigwork[t] = ar.take(eig_work_doubles((int)P.o.k[t]));
   P.scratch = ar;  // everything after this point is phase scratch
   return kOk;
+}
+
+// projection temporaries of node t (mode-1 and mode-2 results; the root's R1^T B_D)
+double proj_scratch_bytes(const Tree& T, const View& o, const View& out, int t) {
+  if (t == 0) return 8.0 * out.k[T.son1[0]] * o.k[T.son2[0]] + 256;
+  if (T.leaf(t)) return 0.0;
+  const double k1 = (double)o.k[T.son1[t]], k2 = (double)o.k[T.son2[t]];
+  return 8.0 * out.k[t] * k1 * k2 + 8.0 * out.k[t] * out.k[T.son1[t]] * k2 + 512;
 }
 
 size_t truncate_ws_bytes_uncached(const View& x);
@@ -838,6 +894,7 @@ size_t truncate_ws_bytes(const View& x) {
   for (int t = 0; t < x.T->nn; ++t) {
     key.push_back(x.n[t]);
     key.push_back(x.k[t]);
+    key.push_back(x.owned.empty() ? 2 : x.owned[t]);
   }
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -851,7 +908,9 @@ size_t truncate_ws_bytes(const View& x) {
   return b;
 }
 
-size_t truncate_ws_bytes_uncached(const View& x) {
+size_t truncate_ws_bytes_uncached(const View& x_in) {
+  View x = x_in;
+  x.mask = x.owned;  // phase scratch is sized for the owned nodes (every phase mask is a subset)
   TruncPlan P;
   plan_truncate(x, P, nullptr);
   Arena sc = P.scratch;
@@ -864,17 +923,17 @@ size_t truncate_ws_bytes_uncached(const View& x) {
     need = std::max(need, a3.off);
   }
   {
-    // projection temporaries with the (upper-bound) ranks ko
+    // projection temporaries with the (upper-bound) ranks ko: any chunk of them holds
+    // at most kChunkBytes + one node's bytes (and never more than all of them)
     const Tree& T = *x.T;
-    Arena a4 = sc;
-    for (int t = 1; t < T.nn; ++t) {
-      if (T.leaf(t)) continue;
-      const long long kt = P.o.k[t], k1 = P.o.k[T.son1[t]], k2 = P.o.k[T.son2[t]];
-      a4.take(kt * k1 * k2);
-      a4.take(kt * k1 * k2);
+    double total = 0, biggest = 0;
+    for (int t = 0; t < T.nn; ++t) {
+      if (!x.on(t)) continue;
+      const double b = proj_scratch_bytes(T, P.o, P.o, t);
+      total += b;
+      biggest = std::max(biggest, b);
     }
-    a4.take(P.o.k[T.son1[0]] * P.o.k[T.son2[0]]);
-    need = std::max(need, a4.off);
+    need = std::max(need, sc.off + (size_t)std::min(total, kChunkBytes + biggest) + 4096);
   }
   // every Arena::take may pad by up to 255 bytes; planning merges differ between
   // measure and execute mode, so reserve the worst case per node
@@ -994,16 +1053,26 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
       set_error("output rank exceeds the orthogonalised rank at node " + std::to_string(t));
       return kErrShape;
     }
+  // every node is independent: one group of launches for all nodes,
+  // or several when the mode-1/2 temporaries of the inner nodes exceed kChunkBytes
+  std::vector<int> all;
+  for (int t = 1; t < T.nn; ++t) all.push_back(t);
+  all.push_back(0);
+  for (const auto& chunk : level_chunks(all, x, [&](int t) { return proj_scratch_bytes(T, o, out, t); })) {
   Arena sc = P.scratch;
   std::vector<GemmDesc> st1, st2, st3;
   std::vector<SsDesc> ss1, ss2, ss3;
   std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
-  for (int t = 1; t < T.nn; ++t)
-    if (!T.leaf(t) && x.on(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
-  for (int t = 1; t < T.nn; ++t)
-    if (!T.leaf(t) && x.on(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
-  for (int t = 1; t < T.nn; ++t) {
-    if (!x.on(t)) continue;
+  for (int t : chunk)
+    if (t != 0 && !T.leaf(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+  for (int t : chunk)
+    if (t != 0 && !T.leaf(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
+  bool root = false;
+  for (int t : chunk) {
+    if (t == 0) {
+      root = true;
+      continue;
+    }
     const long long kt = o.k[t], rt = out.k[t];
     if (T.leaf(t)) {
       // U_new (n x r) = Q (n x k) * EV[:, :r]   (arith.py:344)
@@ -1037,7 +1106,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     else
       st3.push_back(gemm_desc(C2[t], k2, 1, P.EV[s2], k2, 1, out.p[t], r2, 1, (int)(rt * r1), (int)r2, (int)k2));
   }
-  if (x.on(0)) {
+  if (root) {
     // root: Q1^T B_D Q2   (arith.py:350-351)
     const int s1 = T.son1[0], s2 = T.son2[0];
     const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
@@ -1057,6 +1126,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   HT_TRY(ss_gemm(ss2, s, "ss_project"));
   HT_TRY(gemm_grouped(st3, s, "gemm_project"));
   HT_TRY(ss_gemm(ss3, s, "ss_project"));
+  }
   return kOk;
 }
 
@@ -1088,13 +1158,15 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
     std::vector<GemmDesc> gl, g1, g2, g3;
     std::vector<ReduceDesc> rs;
     long long tiles = 0;
-    for (int t : T.levels[l]) tiles += (long long)gemm_tiles((int)a.k[t], (int)c.k[t]);
+    for (int t : T.levels[l])
+      if (a.on(t)) tiles += (long long)gemm_tiles((int)a.k[t], (int)c.k[t]);
     std::vector<double*> S1s(T.nn, nullptr), S2s(T.nn, nullptr);
     for (int t : T.levels[l])
-      if (!T.leaf(t)) S1s[t] = ar.take(a.k[t] * a.k[T.son2[t]] * c.k[T.son1[t]]);
+      if (!T.leaf(t) && a.on(t)) S1s[t] = ar.take(a.k[t] * a.k[T.son2[t]] * c.k[T.son1[t]]);
     for (int t : T.levels[l])
-      if (!T.leaf(t)) S2s[t] = ar.take(a.k[t] * c.k[T.son1[t]] * c.k[T.son2[t]]);
+      if (!T.leaf(t) && a.on(t)) S2s[t] = ar.take(a.k[t] * c.k[T.son1[t]] * c.k[T.son2[t]]);
     for (int t : T.levels[l]) {
+      if (!a.on(t)) continue;  // sharded: Phi of unmasked nodes arrive in their slots
       const long long ka = a.k[t], kc = c.k[t];
       if (T.leaf(t)) {
         // Phi = U_a^T U_c   (arith.py:105-106)
@@ -1139,6 +1211,10 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
   }
   // root: sum((Phi1^T A Phi2) * C)   (arith.py:121-123)
   ar.off = base;
+  if (!a.on(0)) {
+    ar.off = mx;
+    return kOk;
+  }
   const int s1 = T.son1[0], s2 = T.son2[0];
   const long long ka1 = a.k[s1], ka2 = a.k[s2], kc1 = c.k[s1], kc2 = c.k[s2];
   double* T1 = ar.take(kc1 * ka2);
@@ -1535,6 +1611,11 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
 }  // namespace
 }  // namespace ht
 
+namespace ht {
+int apply_operator_masked(const ht_operator* op, const ht_tensor* x, const uint8_t* mask, const ht_tensor* out,
+                          cudaStream_t s);
+}
+
 using namespace ht;
 
 extern "C" {
@@ -1640,13 +1721,29 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
   return truncate_phase2(v, ctl, (char*)ws, o, s);
 }
 
+int ht_truncate_workspace_size_sharded(const ht_tensor* x, const uint8_t* owned, size_t* bytes) {
+  View v;
+  HT_TRY(make_view(x, v, false));
+  if (owned) v.owned.assign(owned, owned + v.T->nn);
+  *bytes = truncate_ws_bytes(v);
+  return kOk;
+}
+
 int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int32_t phase,
-                        const uint8_t* mask, const ht_tensor* out, ht_stream_t stream) {
+                        const uint8_t* mask, const uint8_t* owned, const ht_tensor* out, ht_stream_t stream) {
   View v;
   HT_TRY(make_view(x, v));
   HT_TRY(check_ctl(ctl));
+  if (owned) v.owned.assign(owned, owned + v.T->nn);
   HT_TRY(check_ws(v, (char*)ws, ws_bytes));
-  if (mask) v.mask.assign(mask, mask + v.T->nn);
+  if (mask) {
+    v.mask.assign(mask, mask + v.T->nn);
+    for (int t = 0; t < v.T->nn; ++t)
+      if (v.mask[t] && !v.owned.empty() && !v.owned[t]) {
+        set_error("phase mask names node " + std::to_string(t) + " outside the owned set");
+        return kErrArgument;
+      }
+  }
   cudaStream_t s = (cudaStream_t)stream;
   if (phase == kPhaseProject) {
     View o;
@@ -1667,11 +1764,17 @@ int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
   return kErrArgument;
 }
 
-int ht_truncate_slot(const ht_tensor* x, void* ws, int32_t kind, int32_t node, void** ptr, int64_t* count) {
+int ht_truncate_slot(const ht_tensor* x, void* ws, const uint8_t* owned, int32_t kind, int32_t node, void** ptr,
+                     int64_t* count) {
   View v;
   HT_TRY(make_view(x, v, false));
   if (node < 0 || node >= v.T->nn) {
     set_error("node id out of range");
+    return kErrArgument;
+  }
+  if (owned) v.owned.assign(owned, owned + v.T->nn);
+  if (kind != 4 && !v.needed(node)) {
+    set_error("node " + std::to_string(node) + " has no slot in this shard's workspace plan");
     return kErrArgument;
   }
   TruncPlan P;
@@ -1960,6 +2063,48 @@ int ht_inner_product(const ht_tensor* a, const ht_tensor* c, void* ws, size_t ws
   return kOk;
 }
 
+int ht_inner_product_sharded(const ht_tensor* a, const ht_tensor* c, const uint8_t* mask, void* ws, size_t ws_bytes,
+                             double* result_dev, ht_stream_t stream) {
+  View va, vc;
+  HT_TRY(make_view(a, va));
+  HT_TRY(make_view(c, vc));
+  HT_TRY(check_compatible(va, vc));
+  size_t need = 0;
+  HT_TRY(ht_inner_product_workspace_size(a, c, &need));
+  if (ws_bytes < need || (mask && mask[0] && !result_dev)) {
+    set_error("inner product workspace too small or no result buffer");
+    return kErrArgument;
+  }
+  if (mask) va.mask.assign(mask, mask + va.T->nn);
+  Arena ar;
+  ar.base = (char*)ws;
+  return run_inner_product(va, vc, ar, result_dev, (cudaStream_t)stream, true);
+}
+
+int ht_inner_product_slot(const ht_tensor* a, const ht_tensor* c, void* ws, int32_t node, void** ptr, int64_t* count) {
+  View va, vc;
+  HT_TRY(make_view(a, va, false));
+  HT_TRY(make_view(c, vc, false));
+  if (node < 1 || node >= va.T->nn) {
+    set_error("inner product slots exist for non-root nodes only");
+    return kErrArgument;
+  }
+  // Phi_t (k_a x k_c) of every non-root node sits at the start of the workspace, in
+  // node order (run_inner_product's first allocations)
+  Arena ar;
+  ar.base = (char*)ws;
+  double* p = nullptr;
+  for (int t = 1; t <= node; ++t) p = ar.take(va.k[t] * vc.k[t]);
+  *ptr = p;
+  *count = va.k[node] * vc.k[node];
+  return kOk;
+}
+
+int ht_apply_operator_sharded(const ht_operator* op, const ht_tensor* x, const uint8_t* mask, const ht_tensor* out,
+                              ht_stream_t stream) {
+  return apply_operator_masked(op, x, mask, out, (cudaStream_t)stream);
+}
+
 int ht_evaluate_entries(const ht_tensor* x, const int64_t* idx, int64_t count, double* out, ht_stream_t stream) {
   return ht_evaluate_weighted(x, nullptr, idx, count, out, stream);
 }
@@ -2013,6 +2158,16 @@ int ht_evaluate_weighted(const ht_tensor* x, const double* const* leaf_weights, 
 }
 
 int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor* out, ht_stream_t stream) {
+  return apply_operator_masked(op, x, nullptr, out, (cudaStream_t)stream);
+}
+
+}  // extern "C"
+
+namespace ht {
+// apply_operator (arith.py:378-395) restricted to mask[t] != 0 (NULL: every node);
+// node-local, so the sharded form needs no communication (reference dist.py:324-333)
+int apply_operator_masked(const ht_operator* op, const ht_tensor* x, const uint8_t* mask, const ht_tensor* out,
+                          cudaStream_t s) {
   View vx, vo;
   HT_TRY(make_view(x, vx));
   if (!op || op->d != x->d) {
@@ -2021,11 +2176,11 @@ int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor
   }
   const Tree& T = *vx.T;
   HT_TRY(make_view(out, vo));
-  cudaStream_t s = (cudaStream_t)stream;
   std::vector<KronDesc> kd;
   std::vector<LeafApplyDesc> ld;
   std::vector<GemmDesc> gd;
   for (int t = 0; t < T.nn; ++t) {
+    if (mask && !mask[t]) continue;
     const long long R = t == 0 ? 1 : op->rank[t];
     if (t > 0 && vo.k[t] != R * vx.k[t]) {
       set_error("apply output ranks must be operator rank * tensor rank");
@@ -2070,6 +2225,9 @@ int ht_apply_operator(const ht_operator* op, const ht_tensor* x, const ht_tensor
   HT_TRY(gemm_grouped(gd, s));
   return kOk;
 }
+}  // namespace ht
+
+extern "C" {
 
 int ht_qr_workspace_size(int64_t m, int64_t K, int64_t nodes, size_t* bytes) {
   QrProblem q{};

@@ -103,3 +103,34 @@ class NumpyShardEngine:
         o = Out()
         o.ranks, o.arrays = ranks, arrays
         return o
+
+
+class NumpyInnerEngine:
+    """Phase / slot interface of dist.GpuInnerEngine with the oracle's Phi kernels."""
+
+    def __init__(self, a: "orc.HT", c: "orc.HT"):
+        self.a, self.c, self.tr = a, c, a.tree
+        nn = self.tr.n_nodes
+        self.phi = {t: np.zeros((a.rank(t), c.rank(t))) for t in range(1, nn)}
+        self.res = torch.zeros(1, dtype=torch.float64)
+
+    def phase(self, nodes):
+        tr, s = self.tr, set(nodes)
+        for lev in reversed(tr.levels()):
+            for t in lev:
+                if t not in s:
+                    continue
+                if tr.is_leaf(t):
+                    self.phi[t][...] = self.a.U[t].T @ self.c.U[t]
+                elif t == 0:
+                    s1, s2 = tr.sons[0]
+                    self.res[0] = float(np.sum((self.phi[s1].T @ self.a.root @ self.phi[s2]) * self.c.root))
+                else:
+                    s1, s2 = tr.sons[t]
+                    self.phi[t][...] = orc.node_phi_inner(self.a.B[t], self.c.B[t], self.phi[s1], self.phi[s2])
+
+    def slot(self, node):
+        return torch.from_numpy(self.phi[node]).view(-1)
+
+    def result(self):
+        return self.res

@@ -87,6 +87,59 @@ def test_sharded_truncate_matches_serial(world, d, cap, eps_rel):
     assert err <= 1e-12
 
 
+def _ip_worker(rank, world, port, d, n, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist_.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_1708_03340_b200 import build_balanced_tree, dist
+        from tests.np_engine import NumpyInnerEngine
+
+        tr = orc.balanced_tree(d)
+        a = orc.gaussian_htensor(tr, n, 3, 5)
+        c = orc.add(orc.gaussian_htensor(tr, n, 2, 6), a)  # different ranks on every node
+        smap = dist.ShardMap.build(build_balanced_tree(d), world)
+        v = dist.sharded_inner_product(NumpyInnerEngine(a, c), dist.TorchComm(), smap)
+        q.put((rank, v, orc.inner_product(a, c)))
+    finally:
+        dist_.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,d", [(2, 8), (4, 8), (4, 16), (2, 10), (4, 10)])
+def test_sharded_inner_product_matches_serial(world, d):
+    """The GRAM_UP wave (reference dist.py:239-254): Phi of the shard roots up, rank 0
+    finishes the top levels, every rank returns the same value."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_ip_worker, args=(r, world, port, d, 7, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    for _, v, ref in got:
+        np.testing.assert_allclose(v, ref, rtol=1e-12)
+
+
+def test_c5_shard_workspace_fits():
+    """C5 (d=256, n=2048, rank 400 -> 100) on 8 GPUs: each rank's truncate workspace is
+    planned for its 32-leaf subtree (+ the top nodes on rank 0) and their message slots,
+    not the whole tree -- host-only query, no device needed."""
+    from paper_1708_03340_b200 import build_balanced_tree, dist
+
+    tree = build_balanced_tree(256)
+    sizes = {leaf.index: 2048 for leaf in tree.leaves}
+    ranks = {t: 400 for t in range(1, len(tree.nodes))}
+    whole = dist.shard_workspace_bytes(tree, sizes, ranks, None)
+    smap = dist.ShardMap.build(tree, 8)
+    per = [dist.shard_workspace_bytes(tree, sizes, ranks, smap.owned(g)) for g in range(8)]
+    assert whole > 100e9  # the whole-tree plan cannot fit one B200
+    assert max(per) < 40e9, [f"{b / 1e9:.1f} GB" for b in per]
+    assert max(per) < whole / 4
+
+
 def test_shard_map_layout():
     from paper_1708_03340_b200 import build_balanced_tree, dist
 
