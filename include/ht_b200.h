@@ -253,6 +253,13 @@ int ht_gemm_strided(int64_t M, int64_t N, int64_t K, int64_t batch, double alpha
  *   2: as 0 but both Cholesky-QR passes always run (CholeskyQR2).
  * Both give the unique QR with diag(R) >= 0 of kernels.py:24-32 up to rounding. */
 int ht_set_qr_mode(int mode);
+/* Implicit Q in truncation (process-wide; default 1, env HT_IMPLICIT_Q).  With 1 the
+ * Cholesky-QR sweep of a truncation does not form the orthogonal transfer tensors
+ * Q_t = M23(Bp_t) R_t^{-1}: it keeps the absorbed tensor Bp_t and R_t^{-1}, and the
+ * Gramian and projection phases fold R_t^{-1} into their small operands
+ * (G~ = R^-1 G R^-T, R^-1 Q_t).  Mathematically identical to reference
+ * arith.py:325-352; 0 forms Q explicitly (A/B comparisons, tests). */
+int ht_set_implicit_q(int on);
 /* Number of Cholesky-QR2 sweeps that were re-run with Householder QR. */
 int64_t ht_qr_fallback_count(void);
 /* Graph replays re-run a flagged Cholesky-QR sweep on the Householder path through a

@@ -27,6 +27,7 @@ from .arith import (
     scale,
     set_eig_mode,
     set_graph_mode,
+    set_implicit_q,
     graph_stats,
     graph_relocations,
     synchronize,
@@ -84,6 +85,7 @@ __all__ = [
     "scale",
     "set_eig_mode",
     "set_graph_mode",
+    "set_implicit_q",
     "graph_stats",
     "graph_relocations",
     "synchronize",

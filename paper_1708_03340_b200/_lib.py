@@ -37,7 +37,7 @@ EXPORTS = (
     "ht_apply_operator", "ht_apply_operator_sharded", "ht_inner_product_sharded", "ht_inner_product_slot",
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
     "ht_launch_count", "ht_profile_enable", "ht_profile_report", "ht_profile_log",
-    "ht_truncate_sharded", "ht_truncate_workspace_size_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_qr_fallback_count", "ht_set_eig_mode",
+    "ht_truncate_sharded", "ht_truncate_workspace_size_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_set_implicit_q", "ht_qr_fallback_count", "ht_set_eig_mode",
     "ht_set_graph_mode", "ht_graph_stats", "ht_graph_relocations", "ht_status", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
 )
 
@@ -109,6 +109,7 @@ def _declare(lib):
         "ht_truncate_slot": ([t, _vp, _vp, ctypes.c_int32, ctypes.c_int32, P(ctypes.c_void_p), _i64p], ctypes.c_int),
         "ht_launch_count": ([], ctypes.c_int64),
         "ht_set_qr_mode": ([ctypes.c_int], ctypes.c_int),
+        "ht_set_implicit_q": ([ctypes.c_int], ctypes.c_int),
         "ht_qr_fallback_count": ([], ctypes.c_int64),
         "ht_set_eig_mode": ([ctypes.c_int], ctypes.c_int),
         "ht_set_graph_mode": ([ctypes.c_int], ctypes.c_int),

@@ -310,6 +310,14 @@ def get_qr_mode() -> str:
     return _qr_mode
 
 
+def set_implicit_q(on: bool) -> None:
+    """Implicit-Q truncation (process-wide, default on): the Cholesky-QR sweep keeps the
+    absorbed transfer tensors and R^-1 instead of forming Q = M23(B') R^-1, and the
+    Gramian / projection phases fold R^-1 into their small operands.  Off forms Q
+    explicitly; both compute reference arith.py:325-352."""
+    _lib.check(_lib.load().ht_set_implicit_q(1 if on else 0), "set_implicit_q")
+
+
 _EIG_MODES = {"auto": 0, "jacobi": 1}
 _eig_mode = "auto"
 

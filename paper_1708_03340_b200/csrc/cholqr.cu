@@ -616,7 +616,8 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   for (size_t p = 0; p < cs.size(); ++p) {
     const CholQr& c = cs[p];
     CholDesc d{};
-    d.W = c.W; d.Rf = c.R1; d.Ri = c.Ri; d.Rout = c.q.R; d.r_ld = c.q.r_ld; d.r_node = c.q.r_node;
+    d.W = c.W; d.Rf = c.R1; d.Ri = c.q.rinv ? c.q.rinv : c.Ri; d.Rout = c.q.R; d.r_ld = c.q.r_ld;
+    d.r_node = c.q.r_node;
     d.K = c.q.K; d.nodes = c.q.nodes;
     d.need2 = need2 + p;
     d.kappa_max = (c.q.K <= kCholInPlaceK && !two_pass) ? kKappaOnePass : 0.0;
@@ -630,6 +631,7 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   std::vector<SsDesc> sd;
   for (auto& c : cs) {
     const int K = c.q.K, m = c.q.m;
+    if (c.q.rinv) continue;  // implicit Q: A and R^{-1} stand for Q
     if (K <= kCholInPlaceK) {
       SsDesc d = ss_desc(c.q.A, c.q.a_r, c.q.a_c, c.Ri, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
       d.jobs = c.q.nodes; d.x_job = c.q.a_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
@@ -650,6 +652,29 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   // launches sit in an IF node taken only when some need2 flag is set; elsewhere they
   // are enqueued and exit on their device flags.
   auto pass2 = [&](cudaStream_t s) -> int {
+    // implicit-Q problems form their first-pass Q1 = A R1^{-1} only now (in place when
+    // one CTA owns whole rows, else into scratch)
+    for (size_t p = 0; p < cs.size(); ++p) {
+      const CholQr& c = cs[p];
+      if (!c.q.rinv) continue;
+      const int K = c.q.K, m = c.q.m;
+      if (K <= kCholInPlaceK) {
+        SsDesc d = ss_desc(c.q.A, c.q.a_r, c.q.a_c, c.q.rinv, K, 1, c.q.Q, c.q.q_r, c.q.q_c, m, K, K);
+        d.jobs = c.q.nodes; d.x_job = c.q.a_node; d.s_job = (long long)K * K; d.c_job = c.q.q_node;
+        d.s_tri = 2;
+        d.active = need2 + p;
+        sd.push_back(d);
+      } else {
+        GemmDesc d = gemm_desc(c.q.A, c.q.a_r, c.q.a_c, c.q.rinv, K, 1, c.Q1, K, 1, m, K, K);
+        d.nb1 = c.q.nodes; d.a_b1 = c.q.a_node; d.b_b1 = (long long)K * K; d.c_b1 = (long long)m * K;
+        d.active = need2 + p;
+        g.push_back(d);
+      }
+    }
+    HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
+    HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
+    sd.clear();
+    g.clear();
     for (size_t p = 0; p < cs.size(); ++p) {
       const CholQr& c = cs[p];
       if (c.q.K <= kCholInPlaceK) gram(g, r, c, c.q.Q, c.q.q_r, c.q.q_c, c.q.q_node, need2 + p);
@@ -691,6 +716,11 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
     }
     HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
     HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
+    // the Q of an implicit problem is explicit now: its R^{-1} stand-in becomes I
+    for (size_t p = 0; p < cs.size(); ++p) {
+      const CholQr& c = cs[p];
+      if (c.q.rinv) HT_TRY(identity_batched(c.q.rinv, (long long)c.q.K * c.q.K, c.q.K, c.q.nodes, need2 + p, s));
+    }
     return kOk;
   };
   if (g_own_capture && g_cond_nodes != 0) {

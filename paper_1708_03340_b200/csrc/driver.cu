@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "eig.cuh"
 #include "gemm.cuh"
+#include "gramfin.cuh"
 #include "ssgemm.cuh"
 #include "ht_b200.h"
 #include "misc.cuh"
@@ -348,7 +349,9 @@ void merge_qrs(std::vector<QrProblem>& v) {
         bool same = e.m == d.m && e.K == d.K && e.a_r == d.a_r && e.a_c == d.a_c && e.q_r == d.q_r &&
                     e.q_c == d.q_c && e.r_ld == d.r_ld && e.A - d.A == c * dA && e.Q - d.Q == c * dQ &&
                     e.R - d.R == c * dR && (e.V == nullptr) == (d.V == nullptr) &&
-                    (d.V == nullptr || e.V - d.V == c * (long long)d.m * d.K);
+                    (d.V == nullptr || e.V - d.V == c * (long long)d.m * d.K) &&
+                    (e.rinv == nullptr) == (d.rinv == nullptr) &&
+                    (d.rinv == nullptr || e.rinv - d.rinv == c * (long long)d.K * d.K);
         if (!same) break;
         ++j;
       }
@@ -408,7 +411,37 @@ struct OrthPlan {
   std::vector<long long> ko;
   std::vector<double*> out;  // orthogonalised node arrays
   std::vector<double*> R;    // R factors (ko[t] x k[t], row-major)
+  // Implicit Q (truncation only).  For an inner node with imp[t] the Cholesky-QR sweep
+  // leaves out[t] = Bp, the absorbed transfer tensor (I, R1, R2) o B, and rinv[t] =
+  // R^{-1} (K x K row-major), and never forms Q = M23(Bp) R^{-1}: the orthogonalised
+  // tensor is out[t] x_1 R^{-T}.  Its consumers fold R^{-1} into their small operand
+  // (Gramian: G~ = R^{-1} G R^{-T}; projection: R^{-1} Q_t), which removes the Q GEMM
+  // (K^4 flop + one read and write of every transfer tensor).  Paths that produce an
+  // explicit Q (second Cholesky-QR pass, Householder) set rinv[t] = I.
+  std::vector<unsigned char> imp;
+  std::vector<double*> rinv;
 };
+
+#ifndef HT_IMPLICIT_Q_DEFAULT
+#define HT_IMPLICIT_Q_DEFAULT 1
+#endif
+int g_implicit_q = -1;  // -1: from HT_IMPLICIT_Q (default on)
+bool implicit_q_enabled() {
+  if (g_implicit_q < 0) {
+    const char* e = std::getenv("HT_IMPLICIT_Q");
+    g_implicit_q = e ? (e[0] != '0') : HT_IMPLICIT_Q_DEFAULT;
+  }
+  return g_implicit_q != 0;
+}
+
+// Static eligibility of node t for the implicit-Q form: an inner non-root node whose
+// QR problem ((ko1 ko2) x k_t) takes the Cholesky-QR path.
+bool implicit_q_node(const View& x, const std::vector<long long>& ko, int t) {
+  const Tree& T = *x.T;
+  if (t == 0 || T.leaf(t) || x.orth || !implicit_q_enabled()) return false;
+  const long long m = ko[T.son1[t]] * ko[T.son2[t]], K = x.k[t];
+  return K >= 1 && K <= kCholMaxK && m >= 2 * K;
+}
 
 // Runs (or, in measure mode, sizes) the bottom-up sweep.  `out` pointers may be
 // supplied (ht_orthogonalize) or carved from the arena (truncate).
@@ -484,8 +517,11 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
     for (int t : chunk)
       if (!T.leaf(t) && x.on(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
+    // implicit Q (Cholesky-QR sweep only): the absorbed tensor goes straight into the
+    // node's slot and stays there
+    auto imp = [&](int t) { return chol && !op.imp.empty() && op.imp[t]; };
     for (int t : chunk)
-      if (!T.leaf(t) && x.on(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
+      if (!T.leaf(t) && x.on(t) && !imp(t)) Bps[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * ko[T.son2[t]]);
     for (int t : chunk) {
       if (!x.on(t)) continue;
       if (T.leaf(t)) {
@@ -500,7 +536,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       const int s1 = T.son1[t], s2 = T.son2[t];
       const long long kt = x.k[t], k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
       double* T1 = T1s[t];
-      double* Bp = Bps[t];
+      double* Bp = imp(t) ? op.out[t] : Bps[t];
       // mode-2 absorb, per slice i: T1_i (k1o x k2) = R1 (k1o x k1) * B_i (k1 x k2)
       if (ss_fits(k1o, k1)) {
         // streamed as T1_i^T = B_i^T R1^T over the rows (i, l): R1^T stays in shared memory
@@ -524,7 +560,8 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       // QR of M23(Bp): (k1o k2o) x kt column-major, in place as reflector storage
       QrProblem q{};
       q.A = Bp; q.a_r = 1; q.a_c = k1o * k2o;
-      q.V = Bp;
+      q.V = imp(t) ? nullptr : Bp;
+      q.rinv = imp(t) ? op.rinv[t] : nullptr;
       q.Q = op.out[t]; q.q_r = 1; q.q_c = k1o * k2o;
       q.R = op.R[t]; q.r_ld = kt;
       q.m = (int)(k1o * k2o); q.K = (int)kt; q.nodes = 1;
@@ -589,6 +626,11 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       HT_TRY(cholbig_run(cb, fail ? fail : bfail, bflags, g_qr_mode == 2, s, !chol));
       HT_TRY(qr_wide_batched(wide, s));
       HT_TRY(qr_batched(hh, s));
+      // explicit Q for a node that has an implicit-Q slot (Householder sweep): R^{-1} := I
+      if (!chol && !op.imp.empty())
+        for (int t : chunk)
+          if (op.imp[t] && op.rinv[t])
+            HT_TRY(identity_batched(op.rinv[t], 0, (int)x.k[t], 1, nullptr, s));
     }
    }
   }
@@ -706,8 +748,23 @@ size_t orth_scratch_need(const View& x, OrthPlan op, const Arena& scratch_in) {
 // ---------------------------------------------------------------------------
 // reduced Gramians, top-down (arith.py:148-158, 299-322)
 // ---------------------------------------------------------------------------
-int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar, cudaStream_t s, bool exec) {
+// With an implicit-Q orthogonalisation (OrthPlan::imp / rinv), o.p[t] holds Bp and the
+// orthogonal tensor is Bp x_1 R^{-T}: the node's Gramian is then applied as
+// G~ = R^{-1} G R^{-T} to Bp (sum_{i1,i2} Q[i1,.] G[i1,i2] Q[i2,.] with Q[i,.] =
+// sum_m R^{-1}[m,i] Bp[m,.]), and the son Gramians come out in the same bases.
+int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar, cudaStream_t s, bool exec,
+                 const OrthPlan* imp = nullptr, const std::vector<double*>* Gt = nullptr) {
   const Tree& T = *o.T;
+  // finish of son s's Gramian: sum the partials; implicit-Q sons also get G~_s
+  auto finish = [&](const double* P, int S, int son) {
+    GramFinDesc f{};
+    f.P = P; f.G = G[son]; f.S = S; f.K = (int)o.k[son];
+    if (imp && !imp->imp.empty() && imp->imp[son] && Gt && (*Gt)[son]) {
+      f.Rinv = imp->rinv[son];
+      f.Gt = (*Gt)[son];
+    }
+    return f;
+  };
   const size_t base = scratch_ar.off;
   size_t mx = base;
   // root: G_s1 = B_D B_D^T, G_s2 = B_D^T B_D
@@ -717,6 +774,8 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     const long long k1 = o.k[s1], k2 = o.k[s2];
     double* P1 = scratch_ar.take(k1 * k1);
     double* P2 = scratch_ar.take(k2 * k2);
+    double* P1s = scratch_ar.take(k1 * k1);
+    double* P2s = scratch_ar.take(k2 * k2);
     mx = std::max(mx, scratch_ar.off);
     if (exec) {
       std::vector<GemmDesc> g;
@@ -726,10 +785,14 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       g.push_back(a);
       g.push_back(b);
       HT_TRY(gemm_grouped(g, s));
+      // B_D B_D^T is not computed by the symmetric kernel: symmetrise on the host side
+      // of the finish (gram_finish sums partials only), via a 1-partial reduce
       std::vector<ReduceDesc> r(2);
-      r[0] = ReduceDesc{P1, G[s1], k1, 1, 0, 0, 1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0};
-      r[1] = ReduceDesc{P2, G[s2], k2, 1, 0, 0, 1, (int)k2, (int)k2, 1, 1, 1, 1.0, 0.0};
+      r[0] = ReduceDesc{P1, P1s, k1, 1, 0, 0, 1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0};
+      r[1] = ReduceDesc{P2, P2s, k2, 1, 0, 0, 1, (int)k2, (int)k2, 1, 1, 1, 1.0, 0.0};
       HT_TRY(reduce_partials(r, s));
+      std::vector<GramFinDesc> f{finish(P1s, 1, s1), finish(P2s, 1, s2)};
+      HT_TRY(gram_finish(f, s));
     }
   }
   for (int l = 1; l < T.depth; ++l) {
@@ -746,7 +809,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     if (inner.empty()) continue;
     std::vector<GemmDesc> g1s, g2s;
     std::vector<SsDesc> s1s;
-    std::vector<ReduceDesc> rs;
+    std::vector<GramFinDesc> rs;
     long long tiles = 0;
     for (int t : inner) {
       const long long k1 = o.k[T.son1[t]], k2 = o.k[T.son2[t]];
@@ -754,6 +817,18 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     }
     std::vector<double*> t1s(T.nn, nullptr);
     for (int t : inner) t1s[t] = scratch_ar.take(o.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+    // implicit Q: the level applies G~_t = R_t^{-1} G_t R_t^{-T} (formed by the previous
+    // level's gram_finish) to the absorbed tensor
+    auto gop = [&](int t) { return (Gt && (*Gt)[t]) ? (*Gt)[t] : G[t]; };
+    // a node whose father another shard processes received G_t as a message: form its
+    // G~_t here
+    std::vector<GramFinDesc> pre;
+    for (int t : inner)
+      if (!o.on(T.father[t]) && imp && !imp->imp.empty() && imp->imp[t] && Gt && (*Gt)[t]) {
+        GramFinDesc f = finish(G[t], 1, t);
+        f.G = nullptr;
+        pre.push_back(f);
+      }
     for (int t : inner) {
       const int s1 = T.son1[t], s2 = T.son2[t];
       const long long kt = o.k[t], k1 = o.k[s1], k2 = o.k[s2];
@@ -762,9 +837,9 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       // t1 (kt x k1k2) = G_t (kt x kt) * M1(B)   (arith.py:155); streamed as
       // t1^T = M1(B)^T G_t^T with G_t resident in shared memory
       if (ss_fits(kt, kt))
-        s1s.push_back(ss_desc(o.p[t], 1, f, G[t], 1, kt, t1, 1, f, (int)f, (int)kt, (int)kt));
+        s1s.push_back(ss_desc(o.p[t], 1, f, gop(t), 1, kt, t1, 1, f, (int)f, (int)kt, (int)kt));
       else
-        g1s.push_back(gemm_desc(G[t], kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
+        g1s.push_back(gemm_desc(gop(t), kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
       const int S1 = pick_splits(tiles, kt * k2);
       const int S2 = pick_splits(tiles, kt * k1);
       double* P1 = scratch_ar.take(S1 * k1 * k1);
@@ -777,17 +852,18 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       b.splits = S2; b.sym = 1;
       g2s.push_back(a);
       g2s.push_back(b);
-      rs.push_back(ReduceDesc{P1, G[s1], k1, 1, 0, 0, S1, (int)k1, (int)k1, 1, 1, 1, 1.0, 0.0});
-      rs.push_back(ReduceDesc{P2, G[s2], k2, 1, 0, 0, S2, (int)k2, (int)k2, 1, 1, 1, 1.0, 0.0});
+      rs.push_back(finish(P1, S1, s1));
+      rs.push_back(finish(P2, S2, s2));
     }
     mx = std::max(mx, scratch_ar.off);
     if (exec) {
+      HT_TRY(gram_finish(pre, s));
       merge_gemms(g1s);
       merge_ss(s1s);
       HT_TRY(gemm_grouped(g1s, s, "gemm_gram_t1"));
       HT_TRY(ss_gemm(s1s, s, "ss_gram_t1"));
       HT_TRY(gemm_grouped(g2s, s, "gemm_gram_g"));
-      HT_TRY(reduce_partials(rs, s));
+      HT_TRY(gram_finish(rs, s));
     }
    }
   }
@@ -802,6 +878,7 @@ struct TruncPlan {
   OrthPlan op;
   View o;                       // orthogonal tensor (x itself or op.out)
   std::vector<double*> G, EV, lam;
+  std::vector<double*> Gt;  // implicit-Q nodes: R^{-1} G R^{-T}
   int* ranks = nullptr;
   int* status = nullptr;
   int* qr_fail = nullptr;
@@ -849,16 +926,38 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
     P.op.R.assign(T.nn, nullptr);
     for (int t = 1; t < T.nn; ++t)
       if (x.needed(t)) P.op.R[t] = ar.take(ko[t] * x.k[t]);
+    // R^{-1} of the implicit-Q nodes this rank owns, packed (node stride K*K within a
+    // run of same-K nodes, as the batched Cholesky kernel writes them)
+    P.op.imp.assign(T.nn, 0);
+    P.op.rinv.assign(T.nn, nullptr);
+    long long rtot = 0;
+    for (int t = 1; t < T.nn; ++t)
+      if ((x.owned.empty() || x.owned[t]) && implicit_q_node(x, ko, t)) {
+        P.op.imp[t] = 1;
+        rtot += x.k[t] * x.k[t];
+      }
+    if (rtot > 0) {
+      double* rb = ar.take(rtot);
+      long long off = 0;
+      for (int t = 1; t < T.nn; ++t)
+        if (P.op.imp[t]) {
+          P.op.rinv[t] = rb ? rb + off : nullptr;
+          off += x.k[t] * x.k[t];
+        }
+    }
     P.o.k = ko;
     P.o.p = P.op.out;
     P.o.orth = true;
   }
   P.G.assign(T.nn, nullptr);
+  P.Gt.assign(T.nn, nullptr);
   P.EV.assign(T.nn, nullptr);
   P.lam.assign(T.nn, nullptr);
   // G / EV / lam of all non-root nodes are contiguous so same-K nodes batch
   for (int t = 1; t < T.nn; ++t)
     if (x.needed(t)) P.G[t] = ar.take(P.o.k[t] * P.o.k[t]);
+  for (int t = 1; t < T.nn; ++t)
+    if (!P.op.imp.empty() && P.op.imp[t]) P.Gt[t] = ar.take(P.o.k[t] * P.o.k[t]);
   for (int t = 1; t < T.nn; ++t)
     if (x.needed(t)) P.EV[t] = ar.take(P.o.k[t] * P.o.k[t]);
   for (int t = 1; t < T.nn; ++t)
@@ -880,7 +979,7 @@ double proj_scratch_bytes(const Tree& T, const View& o, const View& out, int t) 
   if (t == 0) return 8.0 * out.k[T.son1[0]] * o.k[T.son2[0]] + 256;
   if (T.leaf(t)) return 0.0;
   const double k1 = (double)o.k[T.son1[t]], k2 = (double)o.k[T.son2[t]];
-  return 8.0 * out.k[t] * k1 * k2 + 8.0 * out.k[t] * out.k[T.son1[t]] * k2 + 512;
+  return 8.0 * out.k[t] * k1 * k2 + 8.0 * out.k[t] * out.k[T.son1[t]] * k2 + 8.0 * o.k[t] * out.k[t] + 768;
 }
 
 size_t truncate_ws_bytes_uncached(const View& x);
@@ -890,7 +989,7 @@ size_t truncate_ws_bytes_uncached(const View& x);
 size_t truncate_ws_bytes(const View& x) {
   static std::mutex mu;
   static std::map<std::vector<long long>, size_t> cache;
-  std::vector<long long> key{(long long)x.T->d, (long long)x.orth};
+  std::vector<long long> key{(long long)x.T->d, (long long)x.orth, (long long)implicit_q_enabled()};
   for (int t = 0; t < x.T->nn; ++t) {
     key.push_back(x.n[t]);
     key.push_back(x.k[t]);
@@ -919,7 +1018,7 @@ size_t truncate_ws_bytes_uncached(const View& x_in) {
   if (!x.orth) need = std::max(need, orth_scratch_need(x, P.op, sc));
   {
     Arena a3 = sc;
-    run_gramians(P.o, P.G, a3, nullptr, false);
+    run_gramians(P.o, P.G, a3, nullptr, false, &P.op, &P.Gt);
     need = std::max(need, a3.off);
   }
   {
@@ -959,7 +1058,7 @@ int phase_orth(const View& x, TruncPlan& P, cudaStream_t s, OrthCheck* deferred 
 
 int phase_gram(TruncPlan& P, cudaStream_t s) {
   Arena sc = P.scratch;
-  return run_gramians(P.o, P.G, sc, s, true);
+  return run_gramians(P.o, P.G, sc, s, true, &P.op, &P.Gt);
 }
 
 // batched eigendecomposition + select_rank of the (masked) non-root nodes
@@ -1065,6 +1164,17 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
   for (int t : chunk)
     if (t != 0 && !T.leaf(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
+  // implicit Q: the mode-1 operand of node t is R^{-1} EV_t[:, :r_t] (k_t x r_t)
+  std::vector<double*> PEV(P.EV);
+  std::vector<long long> pev_ld(T.nn, 0);
+  std::vector<GemmDesc> gpe;
+  for (int t : chunk) {
+    if (t == 0 || P.op.imp.empty() || !P.op.imp[t]) continue;
+    const long long kt = o.k[t], rt = out.k[t];
+    PEV[t] = sc.take(kt * rt);
+    pev_ld[t] = rt;
+    gpe.push_back(gemm_desc(P.op.rinv[t], kt, 1, P.EV[t], kt, 1, PEV[t], rt, 1, (int)kt, (int)rt, (int)kt));
+  }
   for (int t : chunk)
     if (t != 0 && !T.leaf(t)) C2[t] = sc.take(out.k[t] * out.k[T.son1[t]] * o.k[T.son2[t]]);
   bool root = false;
@@ -1085,10 +1195,11 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     const int s1 = T.son1[t], s2 = T.son2[t];
     const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
     // mode 1: C1 (rt x k1k2) = EV_t^T[:rt] * M1(B)   (arith.py:168); streamed as C1^T = M1(B)^T EV_t
+    const long long ev_ld = pev_ld[t] ? pev_ld[t] : kt;
     if (ss_fits(rt, kt))
-      ss1.push_back(ss_desc(o.p[t], 1, k1 * k2, P.EV[t], kt, 1, C1[t], 1, k1 * k2, (int)(k1 * k2), (int)rt, (int)kt));
+      ss1.push_back(ss_desc(o.p[t], 1, k1 * k2, PEV[t], ev_ld, 1, C1[t], 1, k1 * k2, (int)(k1 * k2), (int)rt, (int)kt));
     else
-      st1.push_back(gemm_desc(P.EV[t], 1, kt, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
+      st1.push_back(gemm_desc(PEV[t], 1, ev_ld, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
     // mode 2, per slice i: C2_i (r1 x k2) = EV_s1^T[:r1] * C1_i   (arith.py:169);
     // streamed as C2_i^T = C1_i^T EV_s1 over the rows (i, l)
     if (ss_fits(r1, k1)) {
@@ -1114,6 +1225,8 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     st1.push_back(gemm_desc(P.EV[s1], 1, k1, o.p[0], k2, 1, tmp, k2, 1, (int)r1, (int)k2, (int)k1));
     st3.push_back(gemm_desc(tmp, k2, 1, P.EV[s2], k2, 1, out.p[0], r2, 1, (int)r1, (int)r2, (int)k2));
   }
+  merge_gemms(gpe);
+  HT_TRY(gemm_grouped(gpe, s, "gemm_project_rinv"));
   merge_gemms(st1);
   merge_gemms(st2);
   merge_gemms(st3);
@@ -1308,7 +1421,8 @@ std::vector<long long> shape_key(const View& v, const View& o, const ht_trunc_ct
   long long eps_bits;
   memcpy(&eps_bits, &ctl->eps, sizeof(eps_bits));
   k.insert(k.end(), {(long long)dev, (long long)v.T->d, (long long)v.orth, (long long)ws_bytes, eps_bits,
-                     (long long)ctl->max_rank, (long long)ctl->flags, (long long)g_qr_mode, (long long)g_eig_mode});
+                     (long long)ctl->max_rank, (long long)ctl->flags, (long long)g_qr_mode, (long long)g_eig_mode,
+                     (long long)implicit_q_enabled()});
   for (int t = 0; t < nn; ++t) {
     k.push_back(v.n[t]);
     k.push_back(v.k[t]);
@@ -1897,6 +2011,15 @@ int64_t ht_qr_fallback_count(void) {
     cudaGetLastError();
   }
   return g_qr_fallbacks + (int64_t)dev;
+}
+
+int ht_set_implicit_q(int on) {
+  if (on != 0 && on != 1) {
+    set_error("implicit-Q mode must be 0 (explicit Q = A R^-1) or 1 (R^-1 folded into the consumers)");
+    return kErrArgument;
+  }
+  g_implicit_q = on;
+  return kOk;
 }
 
 int ht_set_graph_mode(int on) {

@@ -247,6 +247,20 @@ int scale_copy(const double* x, double* y, long long n, double alpha, cudaStream
   return kOk;
 }
 
+__global__ void identity_kernel(double* p, long long node_stride, int K, const int* active) {
+  if (active && *active == 0) return;
+  double* q = p + (long long)blockIdx.y * node_stride;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < K * K; e += gridDim.x * blockDim.x)
+    q[e] = (e / K == e % K) ? 1.0 : 0.0;
+}
+
+int identity_batched(double* p, long long node_stride, int K, int nodes, const int* active, cudaStream_t stream) {
+  if (nodes <= 0 || K <= 0) return kOk;
+  identity_kernel<<<dim3((K * K + 255) / 256, nodes), 256, 0, stream>>>(p, node_stride, K, active);
+  HT_LAUNCH_CHECK();
+  return kOk;
+}
+
 int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream) {
   ProfToken tok = prof_begin(stream);
   dot_kernel<<<1, 1024, 0, stream>>>(a, b, n, out);

@@ -56,6 +56,8 @@ struct Copy2dDesc {
   int rows, cols, nodes;
 };
 int copy2d_batched(const std::vector<Copy2dDesc>& descs, cudaStream_t stream);
+// p[node * node_stride + i * K + j] = (i == j) for nodes x K x K (skipped when *active == 0)
+int identity_batched(double* p, long long node_stride, int K, int nodes, const int* active, cudaStream_t stream);
 // out[0] = sum_i a[i] * b[i]   (single CTA, deterministic order)
 int dot(const double* a, const double* b, long long n, double* out, cudaStream_t stream);
 

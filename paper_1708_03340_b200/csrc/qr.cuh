@@ -39,6 +39,12 @@ struct QrProblem {
   // A when A is itself column-major scratch (a_r == 1, a_c == m): the kernel reads
   // a block into registers before writing its reflectors back.
   double* V;
+  // optional (Cholesky-QR path only): implicit Q.  The factor kernel writes R^{-1}
+  // (K x K row-major, node stride K*K) here and the first-pass Q = A R^{-1} is NOT
+  // formed: the caller keeps A and folds R^{-1} into its next small operand (see
+  // driver.cu, "implicit Q").  A node that needs the second pass gets an explicit Q
+  // (written to Q, which then aliases A) and R^{-1} := I.
+  double* rinv = nullptr;
 
   // --- filled by qr_plan() ---
   int P, rpc;

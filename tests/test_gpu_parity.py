@@ -16,18 +16,22 @@ SIGMA_RTOL = 1e-10
 ERR_TOL = 1e-10
 
 
-@pytest.fixture(scope="module", params=[("auto", "auto"), ("cholqr2", "auto"), ("householder", "jacobi")],
-                ids=["fast", "cholqr2", "fallback"])
+@pytest.fixture(scope="module", params=[("auto", "auto", True), ("auto", "auto", False), ("cholqr2", "auto", True),
+                                        ("householder", "jacobi", True)],
+                ids=["fast", "explicit_q", "cholqr2", "fallback"])
 def htb(cuda_ok, request):
-    """Every parity test runs under both kernel policies: the fast paths (Cholesky-QR2,
-    tridiagonal eigensolver; default) and their fallbacks (Householder QR, Jacobi)."""
+    """Every parity test runs under each kernel policy: the fast paths (Cholesky-QR with
+    implicit Q, tridiagonal eigensolver; default), the same with Q formed explicitly, both
+    Cholesky-QR passes, and the fallbacks (Householder QR, Jacobi)."""
     import paper_1708_03340_b200 as m
 
     m.set_qr_mode(request.param[0])
     m.set_eig_mode(request.param[1])
+    m.set_implicit_q(request.param[2])
     yield m
     m.set_qr_mode("auto")
     m.set_eig_mode("auto")
+    m.set_implicit_q(True)
 
 
 def _sig_host(sig):
