@@ -260,7 +260,9 @@ class _Single:
 
     # end to end: the user's workflow T = truncate(add(A, C)) from pinned host A, C to a
     # pinned host T, every step; consecutive steps are pipelined over a copy stream, the
-    # compute stream and a read-back stream (double-buffered device inputs).
+    # compute stream and a read-back stream (double-buffered device inputs, sums and
+    # results: add(..., out=) / truncate(..., out=) write into the slot's buffers, so the
+    # truncation replays its captured graphs as they are).
     def prepare_e2e(self):
         import torch
 
@@ -268,9 +270,15 @@ class _Single:
         self.host_a, self.host_c = self.a.to_host_arena(), self.c.to_host_arena()
         la, lc = self.a.host_layout(), self.c.host_layout()
         self.dev = [(htb.HTensor.empty(self.tree, *la), htb.HTensor.empty(self.tree, *lc)) for _ in range(2)]
+        lx = self.x.host_layout()
+        self.xbuf = [htb.HTensor.empty(self.tree, *lx) for _ in range(2)]
+        T = self.step()
+        self.tbuf = [htb.HTensor.empty(self.tree, *T.host_layout()) for _ in range(2)]
         self.copy_stream, self.d2h_stream = torch.cuda.Stream(), torch.cuda.Stream()
-        self.out_host = [None, None]
-        self.keep = [None, None]
+        self.out_host = [T.to_host_arena() for _ in range(2)]
+        for h in self.out_host:
+            h.fill_(0.0)  # touch the pinned pages (a first DMA into fresh pinned memory is slow)
+        self.d2h_ev = [None, None]
         torch.cuda.synchronize()
 
     def e2e_run(self, n, start_event):
@@ -298,16 +306,18 @@ class _Single:
             if i + 1 < n:
                 issue_h2d(i + 1)
             comp.wait_event(h2d_ev[slot])
-            t = htb.truncate(htb.add(*self.dev[slot]), self.ctl)
+            x = htb.add(*self.dev[slot], out=self.xbuf[slot])
+            if self.d2h_ev[slot] is not None:  # the read-back of this slot's last result is done
+                comp.wait_event(self.d2h_ev[slot])
+            t = htb.truncate(x, self.ctl, out=self.tbuf[slot])
             comp_ev[slot] = torch.cuda.Event()
             comp_ev[slot].record(comp)
             with torch.cuda.stream(self.d2h_stream):
                 self.d2h_stream.wait_event(comp_ev[slot])
-                t._arena.record_stream(self.d2h_stream)
                 self.out_host[slot] = t.to_host_arena(self.out_host[slot])
                 last = torch.cuda.Event()
                 last.record(self.d2h_stream)
-            self.keep[slot] = t
+            self.d2h_ev[slot] = last
         comp.wait_event(last)
 
     def e2e_bytes(self):

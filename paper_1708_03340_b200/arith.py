@@ -111,9 +111,12 @@ def _stream():
 # ---------------------------------------------------------------------------
 
 
-def add(a: HTensor, c: HTensor) -> HTensor:
-    """arith.py:355-365: frames concatenate, transfers embed block-diagonally."""
-    return _add(a, c, 1.0)
+def add(a: HTensor, c: HTensor, out: HTensor | None = None) -> HTensor:
+    """arith.py:355-365: frames concatenate, transfers embed block-diagonally.  ``out``
+    (optional, an extension of the reference API): an existing tensor of the sum's
+    shapes to write into (pipelines reuse device buffers; fixed buffers also let the
+    truncation replay its captured CUDA graphs without re-pointing them)."""
+    return _add(a, c, 1.0, out)
 
 
 def subtract(a: HTensor, c: HTensor) -> HTensor:
@@ -121,12 +124,22 @@ def subtract(a: HTensor, c: HTensor) -> HTensor:
     return _add(a, c, -1.0)
 
 
-def _add(a: HTensor, c: HTensor, alpha_c: float) -> HTensor:
+def _check_out(out: HTensor, tree, sizes: dict, ranks: dict) -> None:
+    if out.tree.d != tree.d or _sizes_by_node(out) != sizes or \
+            any(out.rank(t) != ranks[t] for t in range(1, len(tree.nodes))):
+        raise ValueError("out tensor has the wrong shapes for this result")
+
+
+def _add(a: HTensor, c: HTensor, alpha_c: float, out: HTensor | None = None) -> HTensor:
     _check_compatible(a, c)
     lib = _lib.load()
     tree = a.tree
     ranks = {t: a.rank(t) + c.rank(t) for t in range(1, len(tree.nodes))}
-    out = HTensor.empty(tree, _sizes_by_node(a), ranks, device=a.device)
+    if out is None:
+        out = HTensor.empty(tree, _sizes_by_node(a), ranks, device=a.device)
+    else:
+        _check_out(out, tree, _sizes_by_node(a), ranks)
+        out.orthogonal = False
     _lib.check(lib.ht_add(a._c(), c._c(), float(alpha_c), out._c(), _stream()), "add")
     return out
 
@@ -234,13 +247,22 @@ class _TruncState:
         self.phase1_done = True
 
 
-def truncate(a: HTensor, ctl: TruncationControl) -> HTensor:
+def truncate(a: HTensor, ctl: TruncationControl, out: HTensor | None = None) -> HTensor:
     """arith.py:325-352: orthogonalize if needed, reduced Gramians, batched
-    eigendecompositions + rank choice, projection.  Result not orthogonal."""
+    eigendecompositions + rank choice, projection.  Result not orthogonal.  ``out``
+    (optional, an extension of the reference API): an existing tensor of the result's
+    shapes to write into -- only when the ranks follow from the control and the shapes
+    (fixed-rank control), as they do not depend on the data then."""
     lib = _lib.load()
     st = _TruncState(a, ctl)
+    if out is not None:
+        if not st.static:
+            raise ValueError("truncate(out=...) needs a control whose ranks follow from the shapes (max_rank only)")
+        _check_out(out, a.tree, _sizes_by_node(a), st.ranks)
+        out.orthogonal = False
     if st.static:
-        out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
+        if out is None:
+            out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
         _lib.check(lib.ht_truncate(a._c(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
                                    _stream()), "truncate")
         return out

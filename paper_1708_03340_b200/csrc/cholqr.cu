@@ -17,7 +17,6 @@
 namespace ht {
 namespace {
 
-constexpr int kCholThreads = 1024;
 constexpr int kCholMaxDescs = 48;
 // pivot / column-norm^2 below this => kappa(A) ~> 1e5: leave it to Householder
 constexpr double kPivotTol = 1e-10;
@@ -48,185 +47,7 @@ struct CholBatch {
   int* fail;
 };
 
-// One CTA per K x K Gram matrix (K <= 128).  Symmetric Gaussian elimination
-// (W = L D L^T, U = D L^T) with L^{-1} carried in the strictly lower triangle:
-// at step j every row i > j does
-//   U[i][c]    -= m_i U[j][c]     (c >= i)          m_i = U[j][i] / U[j][j]
-//   Linv[i][c] -= m_i Linv[j][c]  (c <  j),  Linv[i][j] = -m_i
-// Then R = D^{-1/2} U and R^{-1} = L^{-T} D^{-1/2}.  (U[j][i] is the Schur
-// complement's (i, j) entry by symmetry, so only row j is ever broadcast.)
-// Register-resident 2-D blocks: warp bi, lane bc keeps W[4bi .. 4bi+3][4bc .. 4bc+3]
-// in registers, so a warp owns four whole rows.  Pivots are eliminated four at a
-// time: warp J factors its own 4-row panel (pivot and multipliers by shuffles from
-// the diagonal-block lane; row values are lane-local), publishes it to a
-// double-buffered shared panel, and after ONE barrier every lower warp applies the
-// four eliminations from the panel -- K/4 barriers instead of K.
-constexpr int kCholB = 4;                      // block edge
-constexpr int kCholGrid = kCholMaxK / kCholB;  // 32 x 32 thread grid
-static_assert(kCholGrid * kCholGrid == kCholThreads && kCholGrid == kWarp, "one warp per 4-row block");
-
-__global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_constant__ CholBatch cb) {
-  int di = 0;
-  while (di + 1 < cb.count && (int)blockIdx.x >= cb.block_begin[di + 1]) ++di;
-  const CholDesc& c = cb.d[di];
-  if (c.active && *c.active == 0) return;
-  const int node = blockIdx.x - cb.block_begin[di];
-  const int K = c.K;
-  __shared__ __align__(16) double panel[2][kCholB][kCholMaxK];
-  __shared__ double dorig[kCholMaxK];
-  __shared__ double sqd[kCholMaxK];
-  __shared__ double red[kCholThreads / kWarp][2];
-  __shared__ int bad;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int bi = warp, bc = lane;
-  const int i0 = kCholB * bi, c0 = kCholB * bc;
-  const bool act = i0 < K;  // the warp has rows
-  const long long off = (long long)node * K * K;
-  const double* Wg = c.W + off;
-
-  double w[kCholB][kCholB];
-  double dev = 0.0;
-  bool nonfinite = false;
-#pragma unroll
-  for (int u = 0; u < kCholB; ++u)
-#pragma unroll
-    for (int v = 0; v < kCholB; ++v) {
-      const int i = i0 + u, cc = c0 + v;
-      double x = 0.0;
-      if (i < K && cc < K) {
-        x = Wg[(long long)i * K + cc];
-        if (cc >= i) {
-          dev = fmax(dev, fabs(x - (cc == i ? 1.0 : 0.0)));
-          nonfinite |= !isfinite(x);
-        }
-        if (cc == i) dorig[i] = x;
-      }
-      w[u][v] = x;
-    }
-  const int any_nonfinite = __syncthreads_or(nonfinite);
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
-  if (lane == 0) red[warp][0] = dev;
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0.0;
-    for (int q = 0; q < kCholThreads / kWarp; ++q) m = fmax(m, red[q][0]);
-    bad = any_nonfinite || (c.check_identity && !(m <= kIdentityTol)) ? 1 : 0;
-  }
-
-  const int nblk = (K + kCholB - 1) / kCholB;
-  for (int J = 0; J < nblk; ++J) {
-    const int j0 = kCholB * J;
-    double(*P)[kCholMaxK] = panel[J & 1];
-    if (warp == J) {
-      // factor the panel: rows j0 .. j0+3 against pivots j0 .. j0+3 (lane J holds the
-      // diagonal block)
-      bool flag = false;
-#pragma unroll
-      for (int u = 0; u < kCholB; ++u) {
-        const int r = j0 + u;
-        if (r >= K) break;
-        double p = __shfl_sync(0xffffffffu, w[u][u], J);
-        const double d0 = dorig[r];
-        const bool ok = d0 > 1e-290 && isfinite(d0) && p > kPivotTol * d0 && isfinite(p);
-        if (!ok) {
-          p = (d0 > 1e-290 && isfinite(d0)) ? d0 : 1.0;  // keep going; the node is flagged
-          flag = true;
-        }
-        if (lane == 0) sqd[r] = p;
-        const double rp = __drcp_rn(p);
-#pragma unroll
-        for (int u2 = u + 1; u2 < kCholB; ++u2) {
-          const double mi = __shfl_sync(0xffffffffu, w[u][u2], J) * rp;  // U[r][r2] / p
-#pragma unroll
-          for (int v = 0; v < kCholB; ++v) {
-            const double t = fma(-mi, w[u][v], w[u2][v]);
-            w[u2][v] = c0 + v == r ? -mi : t;
-          }
-        }
-      }
-      if (flag && lane == 0) bad = 1;
-#pragma unroll
-      for (int u = 0; u < kCholB; ++u) {
-        *reinterpret_cast<double2*>(&P[u][c0]) = make_double2(w[u][0], w[u][1]);
-        *reinterpret_cast<double2*>(&P[u][c0 + 2]) = make_double2(w[u][2], w[u][3]);
-      }
-    }
-    __syncthreads();
-    if (act && warp > J) {
-#pragma unroll
-      for (int u = 0; u < kCholB; ++u) {
-        const int r = j0 + u;
-        if (r >= K) break;
-        const double rp = __drcp_rn(sqd[r]);
-        const double2 r01 = *reinterpret_cast<const double2*>(&P[u][c0]);
-        const double2 r23 = *reinterpret_cast<const double2*>(&P[u][c0 + 2]);
-        const double2 m01 = *reinterpret_cast<const double2*>(&P[u][i0]);
-        const double2 m23 = *reinterpret_cast<const double2*>(&P[u][i0 + 2]);
-        const double rr[4] = {r01.x, r01.y, r23.x, r23.y};
-        const double mr[4] = {m01.x, m01.y, m23.x, m23.y};
-#pragma unroll
-        for (int uu = 0; uu < kCholB; ++uu) {
-          const double mi = mr[uu] * rp;
-#pragma unroll
-          for (int v = 0; v < kCholB; ++v) {
-            const double t = fma(-mi, rr[v], w[uu][v]);
-            w[uu][v] = c0 + v == r ? -mi : t;
-          }
-        }
-      }
-    }
-  }
-  __syncthreads();
-  for (int j = tid; j < K; j += kCholThreads) sqd[j] = sqrt(sqd[j]);
-  __syncthreads();
-  double* Rf = c.Rf + off;
-  double* Ri = c.Ri + off;
-  double* Ro = c.Rout ? c.Rout + (long long)node * c.r_node : nullptr;
-  double s0 = 0.0, s1 = 0.0;  // ||R||_F^2, ||R^{-1}||_F^2
-  if (act) {
-#pragma unroll
-    for (int u = 0; u < kCholB; ++u) {
-      const int i = i0 + u;
-      if (i >= K) continue;
-      const double isi = 1.0 / sqd[i];
-#pragma unroll
-      for (int v = 0; v < kCholB; ++v) {
-        const int cc = c0 + v;
-        if (cc >= K) continue;
-        const double x = w[u][v] * isi;
-        // R[i][cc] = U[i][cc] / sqrt(D_i) (cc >= i)
-        const double rv = cc >= i ? x : 0.0;
-        Rf[(long long)i * K + cc] = rv;
-        if (Ro) Ro[(long long)i * c.r_ld + cc] = rv;
-        // R^{-1}(cc, i) = Linv[i][cc] / sqrt(D_i) for cc <= i; zeros below the diagonal
-        const double iv = cc < i ? x : (cc == i ? isi : 0.0);
-        Ri[(long long)cc * K + i] = iv;
-        s0 = fma(rv, rv, s0);
-        s1 = fma(iv, iv, s1);
-      }
-    }
-  }
-  if (c.need2) {
-    // kappa_2(R) <= ||R||_F ||R^{-1}||_F: one block reduction of the two sums of squares
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    if (lane == 0) { red[warp][0] = s0; red[warp][1] = s1; }
-    __syncthreads();
-    if (tid == 0) {
-      double a0 = 0.0, a1 = 0.0;
-      for (int q = 0; q < kCholThreads / kWarp; ++q) { a0 += red[q][0]; a1 += red[q][1]; }
-      if (!(sqrt(a0 * a1) <= c.kappa_max)) atomicOr(c.need2, 1);
-    }
-  }
-  if (tid == 0 && bad) atomicOr(cb.fail, 1);
-}
-
-
-// ---- blocked variant (default) --------------------------------------------------
+// ---- batched blocked Cholesky ---------------------------------------------------
 // One CTA of 8 warps per K x K Gram matrix (the lower triangle is read), the matrix resident in shared memory
 // (padded to Kp = 16 * ceil(K / 16), pitch Kp + 4).  Right-looking blocked Cholesky
 // W = L L^T with 16-wide panels: the 16 x 16 diagonal block is factored by one warp
@@ -235,8 +56,9 @@ __global__ void __launch_bounds__(kCholThreads, 1) chol_kernel(const __grid_cons
 // tiles.  Then X = L^{-1}: diagonal blocks per warp (column per lane), off-diagonal
 // blocks by block distance with DMMA (T = L_{I,*} X_{*,J}, X_{IJ} = -X_{II} T).  X is
 // kept transposed in the strict upper triangle (it is R^{-1} = L^{-T} there), its
-// diagonal in rinv.  Same outputs, flags and kappa estimate as chol_kernel; K
-// pivots cost one shuffle-rsqrt-update each instead of a CTA barrier each.
+// diagonal in rinv.  Outputs: R, R^{-1}, the red flag (a pivot loses more than 10
+// digits against its column norm, anything non-finite, or -- second pass -- W not
+// within 0.1 of I) and the ||R||_F ||R^{-1}||_F estimate that decides the second pass.
 constexpr int kC2Threads = 256;
 constexpr int kC2Warps = kC2Threads / 32;
 
@@ -517,12 +339,6 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   if (tid == 0 && bad) atomicOr(cb.fail, 1);
 }
 
-// HT_CHOL_BLOCKED=0: the register-blocked elimination kernel (A/B comparisons)
-const int g_chol_blocked = [] {
-  const char* e = std::getenv("HT_CHOL_BLOCKED");
-  return e && e[0] == '0' ? 0 : 1;
-}();
-
 int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, const char* tag = "cholqr_factor") {
   size_t i = 0;
   while (i < ds.size()) {
@@ -540,19 +356,15 @@ int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, cons
     double flops = 0;
     for (int q = 0; q < b.count; ++q) flops += (double)b.d[q].nodes * b.d[q].K * b.d[q].K * b.d[q].K / 1.5;
     ProfToken tok = prof_begin(s);
-    if (g_chol_blocked) {
-      static bool attr = false;
-      if (!attr) {
-        HT_CUDA_CHECK(cudaFuncSetAttribute(chol2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           (int)chol2_smem(kCholMaxK)));
-        attr = true;
-      }
-      int kmax = 1;
-      for (int q = 0; q < b.count; ++q) kmax = std::max(kmax, b.d[q].K);
-      chol2_kernel<<<blocks, kC2Threads, chol2_smem(kmax), s>>>(b);
-    } else {
-      chol_kernel<<<blocks, kCholThreads, 0, s>>>(b);
+    static bool attr = false;
+    if (!attr) {
+      HT_CUDA_CHECK(cudaFuncSetAttribute(chol2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)chol2_smem(kCholMaxK)));
+      attr = true;
     }
+    int kmax = 1;
+    for (int q = 0; q < b.count; ++q) kmax = std::max(kmax, b.d[q].K);
+    chol2_kernel<<<blocks, kC2Threads, chol2_smem(kmax), s>>>(b);
     HT_LAUNCH_CHECK();
     prof_end(tok, tag, s, ds[0].active ? 0.0 : flops, 0.0);  // conditional launches: no flop claim
   }

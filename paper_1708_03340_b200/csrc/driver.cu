@@ -2392,14 +2392,13 @@ int ht_syev_batched(int64_t K, int64_t nodes, const double* S, double* V, double
   char* buf = nullptr;
   HT_CUDA_CHECK(cudaMallocAsync((void**)&buf, bytes, s));
   int* st = (int*)buf;
-  int* fb = (int*)(buf + 64);
   double* work = wn ? (double*)(buf + ((64 + sizeof(int) * std::max<int64_t>(nodes, 1) + 255) & ~(size_t)255))
                     : nullptr;
   HT_CUDA_CHECK(cudaMemsetAsync(st, 0, sizeof(int), s));
   EigProblem e{};
   e.S = S; e.s_node = K * K; e.V = V; e.v_node = K * K; e.lam = lam; e.l_node = K;
   e.status = st; e.K = (int)K; e.nodes = (int)nodes; e.n_nonroot = 1;
-  (void)fb;  // Jacobi for every node (no tridiagonal fast path, no fallback flags)
+  // Jacobi for every node (no tridiagonal fast path, no fallback flags)
   e.work = work; e.w_node = wn;
   e.graded_fallback = 1;
   std::vector<EigProblem> v{e};

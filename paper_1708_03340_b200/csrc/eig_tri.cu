@@ -27,6 +27,9 @@ namespace ht {
 namespace {
 
 constexpr int TT = 512;
+#ifndef HT_EIG_TIMING
+#define HT_EIG_TIMING 0  // 1: blocks 0-1 print their phase times (clock64) -- experiments only
+#endif
 constexpr int MAXD = 48;
 constexpr int kGroup = 4;  // threads per eigenvalue / eigenvector / mat-vec row
 constexpr double kGradedTol = 1e-6;
@@ -161,6 +164,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
   // ---- load, symmetry check (kernels.py:46-50), symmetrise -------------------
+  long long clk[6] = {clock64(), 0, 0, 0, 0, 0};
   const double* S = e.S + nd * e.s_node;
   double asym = 0.0, amax = 0.0;
   for (int x = tid; x < K * K; x += TT) {
@@ -198,6 +202,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   }
 
   // ---- 1. tridiagonalisation --------------------------------------------------
+  if (HT_EIG_TIMING) clk[1] = clock64();
   // Reflector j from column j (rows j+1..K-1), computed by warp 0 into vbuf[j & 1]
   // while the other warps finish the previous rank-2 update: two barriers per column.
   double* vbuf = vb;
@@ -373,6 +378,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   __syncthreads();
 
   // ---- 2. eigenvalues: multisection bisection, 4 threads per eigenvalue ---------
+  if (HT_EIG_TIMING) clk[2] = clock64();
   for (int i0 = 0; i0 < K; i0 += TT / kGroup) {
     const int i = i0 + tid / kGroup, part = tid % kGroup;
     const double pivmin = sh[2];
@@ -456,6 +462,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   const int r = rsel;
 
   // ---- 3. eigenvectors of T (twisted factorisation) --------------------------------
+  if (HT_EIG_TIMING) clk[3] = clock64();
   // Fast path (2r <= K, matrices in shared memory): two adjacent lanes per vector run
   // the stationary (D+, lane 0) and progressive (D-, lane 1, into the spare row r + v
   // of Z) recurrences at the same time; gamma / twist, L = e / D+ and U = e / D- are
@@ -689,6 +696,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   __syncthreads();
 
   // ---- 4. back-transformation y = H_0 ... H_{K-3} z --------------------------------
+  if (HT_EIG_TIMING) clk[4] = clock64();
   if (!big) {
     // 8 threads per vector, the vector in registers (bt_block), so each reflector is
     // one pass over its column (broadcast to the four vectors of a warp) instead of a
@@ -740,6 +748,11 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   for (int x = tid; x < K * r; x += TT) {
     const int row = x / r, c = x - row * r;
     Vo[(long long)row * K + c] = Z[c * zp + row];
+  }
+  if (HT_EIG_TIMING && tid == 0 && blockIdx.x < 2) {
+    clk[5] = clock64();
+    printf("tri_eig block %d K=%d r=%d: load %lld tridiag %lld bisect+select %lld eigvec %lld backtr+out %lld cycles\n",
+           blockIdx.x, K, r, clk[1] - clk[0], clk[2] - clk[1], clk[3] - clk[2], clk[4] - clk[3], clk[5] - clk[4]);
   }
 }
 

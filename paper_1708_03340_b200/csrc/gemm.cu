@@ -400,14 +400,12 @@ __global__ void reduce_partials_kernel(const __grid_constant__ ReduceBatch rb) {
 // descriptor either along m/n (lm = 1: a_m == b_n == 1, staged [k][m]) or along k
 // (lm = 0: a_k == b_k == 1, staged [m][k]); both layouts share one launch so a level's
 // two son Gramians fill the machine together.
-constexpr int LR_THREADS = 448;
 constexpr int LR_T = 112;        // tile edge
 constexpr int LR_BK = 32;
 constexpr int LR_STAGES = 3;
 constexpr int LR_PM = LR_T + 4;  // [k][m] pitch (4 mod 16 doubles: conflict-free fragments)
 constexpr int LR_PK = LR_BK + 4; // [m][k] pitch
 constexpr int LR_OPD = (LR_BK * LR_PM > LR_T * LR_PK) ? LR_BK * LR_PM : LR_T * LR_PK;  // doubles per operand-stage
-constexpr int LR_Q = LR_T * LR_BK / 2 / LR_THREADS;  // 16-byte pairs per thread per operand-stage (4)
 
 struct LrBatch {
   int count;
@@ -420,156 +418,8 @@ __device__ __forceinline__ void cp16z(double* smem, const double* gmem, int vali
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid_bytes));
 }
 
-template <int LM>
-__device__ __forceinline__ void lr_body(const GemmDesc& g, int local, double* smem) {
-  const int split = local % g.splits;
-  const int b = local / g.splits;
-  const int b1 = b % g.nb1, b2 = b / g.nb1;
-  const double* A = g.A + b1 * g.a_b1 + b2 * g.a_b2;
-  const double* B = g.B + b1 * g.b_b1 + b2 * g.b_b2;
-  const int M = g.M, N = g.N, K = g.K;
-  const long long L = (long long)K * g.KO;
-  const long long per_split = ((L + g.splits - 1) / g.splits + LR_BK - 1) / LR_BK * LR_BK;
-  const long long f_begin = split * per_split;
-  const long long f_end = min(L, f_begin + per_split);
-  const int nst = f_end > f_begin ? (int)((f_end - f_begin + LR_BK - 1) / LR_BK) : 0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-
-  // loader slots, LR_Q 16-byte pairs per operand per stage:
-  //   LM = 1: pair p = tid + 448 q -> k row p / 56 (= tid / 56 + 8 q), m pair 2 (tid % 56)
-  //   LM = 0: pair p = tid + 448 q -> row p / 16 (= tid / 16 + 28 q), k pair 2 (tid % 16)
-  const double* arow[LM ? 1 : LR_Q];
-  const double* brow[LM ? 1 : LR_Q];
-  int avb[LM ? 1 : LR_Q], bvb[LM ? 1 : LR_Q];  // valid bytes (rows beyond M / N read nothing)
-  if (LM) {
-    const int m = 2 * (tid % 56);
-    avb[0] = 8 * max(0, min(2, M - m));
-    bvb[0] = 8 * max(0, min(2, N - m));
-    arow[0] = A + (long long)min(m, M - 1) * g.a_m;
-    brow[0] = B + (long long)min(m, N - 1) * g.b_n;
-  } else {
-#pragma unroll
-    for (int q = 0; q < LR_Q; ++q) {
-      const int r = tid / 16 + 28 * q;
-      avb[q] = r < M ? 16 : 0;
-      bvb[q] = r < N ? 16 : 0;
-      arow[q] = A + (long long)min(r, M - 1) * g.a_m;
-      brow[q] = B + (long long)min(r, N - 1) * g.b_n;
-    }
-  }
-  auto kk_of = [&](int q) { return LM ? tid / 56 + 8 * q : 2 * (tid % 16); };
-  const long long a_wrap = g.a_o - (long long)K * g.a_k, b_wrap = g.b_o - (long long)K * g.b_k;
-  // loader cursor: stage start f = (o, k), advanced by LR_BK (K >= LR_BK or KO == 1)
-  long long ld_o = f_begin / K;
-  int ld_k = (int)(f_begin - ld_o * K);
-  int ld_s = 0, ld_st = 0;
-  auto issue = [&]() {
-    if (ld_s < nst) {
-      double* as = smem + ld_st * 2 * LR_OPD;
-      double* bs = as + LR_OPD;
-      const long long f0 = f_begin + (long long)ld_s * LR_BK;
-      const long long abase = ld_o * g.a_o + (long long)ld_k * g.a_k;
-      const long long bbase = ld_o * g.b_o + (long long)ld_k * g.b_k;
-#pragma unroll
-      for (int q = 0; q < LR_Q; ++q) {
-        const int kk = kk_of(q);
-        const bool fin = f0 + kk < f_end;
-        const bool wrap = ld_k + kk >= K;  // slot crosses into the next outer index
-        const long long ao = abase + (long long)kk * g.a_k + (wrap ? a_wrap : 0);
-        const long long bo = bbase + (long long)kk * g.b_k + (wrap ? b_wrap : 0);
-        const int av = fin ? avb[LM ? 0 : q] : 0, bv = fin ? bvb[LM ? 0 : q] : 0;
-        double* ad = LM ? as + kk * LR_PM + 2 * (tid % 56) : as + (tid / 16 + 28 * q) * LR_PK + kk;
-        double* bd = LM ? bs + kk * LR_PM + 2 * (tid % 56) : bs + (tid / 16 + 28 * q) * LR_PK + kk;
-        cp16z(ad, av ? arow[LM ? 0 : q] + ao : A, av);
-        cp16z(bd, bv ? brow[LM ? 0 : q] + bo : B, bv);
-      }
-    }
-    cp_commit();
-    ++ld_s;
-    ld_k += LR_BK;
-    while (ld_k >= K) {
-      ld_k -= K;
-      ++ld_o;
-    }
-    if (++ld_st == LR_STAGES) ld_st = 0;
-  };
-#pragma unroll
-  for (int st = 0; st < LR_STAGES - 1; ++st) issue();
-
-  const int wm = warp >> 1, wn = warp & 1;
-  const int g8 = lane >> 2, t4 = lane & 3;
-  const int ar = wm * 16 + g8, bc = wn * 56 + g8;
-  double acc[7][4];
-#pragma unroll
-  for (int j = 0; j < 7; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-  int st = 0;
-  for (int s = 0; s < nst; ++s) {
-    cp_wait<LR_STAGES - 2>();
-    __syncthreads();
-    issue();
-    const double* as = smem + st * 2 * LR_OPD;
-    const double* bs = as + LR_OPD;
-    if (++st == LR_STAGES) st = 0;
-#pragma unroll
-    for (int k16 = 0; k16 < LR_BK; k16 += 16) {
-      double a[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int m = ar + 8 * (i & 1), k = k16 + t4 + 4 * (i >> 1);
-        a[i] = LM ? as[k * LR_PM + m] : as[m * LR_PK + k];
-      }
-#pragma unroll
-      for (int j = 0; j < 7; ++j) {
-        double bq[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int n = bc + 8 * j, k = k16 + t4 + 4 * i;
-          bq[i] = LM ? bs[k * LR_PM + n] : bs[n * LR_PK + k];
-        }
-        dmma_16x8x16(acc[j], a, bq);
-      }
-    }
-  }
-  cp_wait<0>();
-
-  const long long nbatch = (long long)g.nb1 * g.nb2;
-#pragma unroll
-  for (int f = 0; f < 2; ++f) {
-    const int m = ar + 8 * f;
-    if (m >= M) continue;
-#pragma unroll
-    for (int j = 0; j < 7; ++j) {
-#pragma unroll
-      for (int v = 0; v < 2; ++v) {
-        const int n = wn * 56 + 8 * j + 2 * t4 + v;
-        if (n >= N) continue;
-        const double r = acc[j][2 * f + v];
-        if (g.splits == 1) {
-          double* p = g.C + b1 * g.c_b1 + b2 * g.c_b2 + (long long)m * g.c_m + (long long)n * g.c_n;
-          *p = g.beta != 0.0 ? g.alpha * r + g.beta * *p : g.alpha * r;
-        } else {
-          g.C[((long long)split * nbatch + b) * M * N + (long long)m * N + n] = r;
-        }
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(LR_THREADS, 1) lr_kernel(const __grid_constant__ LrBatch batch) {
-  extern __shared__ __align__(16) double smem[];
-  int di = 0;
-  while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
-  const GemmDesc& g = batch.d[di];
-  if (g.active && *g.active == 0) return;
-  const int local = blockIdx.x - g.block_begin;
-  if (batch.lm[di]) lr_body<1>(g, local, smem);
-  else lr_body<0>(g, local, smem);
-}
-
-
 // ---- long-reduction kernel, warp-specialised mbarrier pipeline -----------------
-// Same tile and MMA schedule as lr_body (14 consumer warps, 112 x 112, m16n8k16),
-// but one producer warp stages the operands (16-byte cp.async, completion counted on
+// 14 consumer warps, 112 x 112 tiles, m16n8k16; producer warps stage the operands (16-byte cp.async, completion counted on
 // a per-stage `full` mbarrier) and the consumers release each stage on an `empty`
 // mbarrier: no CTA-wide barrier per k-chunk, consumer warps drift independently and
 // the producer runs up to LR_STAGES chunks ahead.
@@ -783,7 +633,7 @@ __device__ __forceinline__ void lrt_body(const GemmDesc& g, int local, double* s
 }
 
 __global__ void __launch_bounds__(LRT_THREADS, 1) lrt_kernel(const __grid_constant__ LrBatch batch) {
-  extern __shared__ __align__(128) double smem[];
+  extern __shared__ __align__(16) double smem[];
   __shared__ unsigned long long full[LR_STAGES], empty[LR_STAGES];
   int di = 0;
   while (di + 1 < batch.count && (int)blockIdx.x >= batch.d[di + 1].block_begin) ++di;
@@ -801,12 +651,6 @@ __global__ void __launch_bounds__(LRT_THREADS, 1) lrt_kernel(const __grid_consta
   if (batch.lm[di]) lrt_body<1>(g, local, smem, full, empty);
   else lrt_body<0>(g, local, smem, full, empty);
 }
-
-// HT_LR_TMA=0: the cp.async / __syncthreads pipeline (A/B comparisons)
-const int g_lr_tma = [] {
-  const char* e = std::getenv("HT_LR_TMA");
-  return e && e[0] == '0' ? 0 : 1;
-}();
 
 // descriptors the long-reduction kernel takes: plain operands, M, N <= 112 (not both
 // <= 56), reduction >= 256, and 16-byte pairs: layout 1 (a_m == b_n == 1) or 0
@@ -829,7 +673,6 @@ size_t lr_smem() { return sizeof(double) * (size_t)LR_STAGES * 2 * LR_OPD; }
 int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream, const char* tag, bool count_flops) {
   static bool attr = false;
   if (!attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(lr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
     HT_CUDA_CHECK(cudaFuncSetAttribute(lrt_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lr_smem()));
     attr = true;
   }
@@ -845,7 +688,7 @@ int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream
       ++i;
       if (d.splits < 1) d.splits = 1;
       if (d.KO < 1) d.KO = 1;
-      if (d.M != d.N || !g_lr_tma) d.sym = 0;
+      if (d.M != d.N) d.sym = 0;
       d.tiles_m = d.tiles_n = 1;
       d.block_begin = blocks;
       blocks += d.splits * d.nb1 * d.nb2;
@@ -857,8 +700,7 @@ int lr_grouped(std::vector<std::pair<GemmDesc, int>>& descs, cudaStream_t stream
     }
     if (batch.count == 0) continue;
     ProfToken tok = prof_begin(stream);
-    if (g_lr_tma) lrt_kernel<<<blocks, LRT_THREADS, lr_smem(), stream>>>(batch);
-    else lr_kernel<<<blocks, LR_THREADS, lr_smem(), stream>>>(batch);
+    lrt_kernel<<<blocks, LRT_THREADS, lr_smem(), stream>>>(batch);
     HT_LAUNCH_CHECK();
     prof_end(tok, tag, stream, count_flops ? flops : 0.0, count_flops ? bytes : 0.0);
   }

@@ -8,10 +8,23 @@
 namespace ht {
 namespace {
 
-constexpr int SST = 256;     // 8 warps
-constexpr int SBM = 128;     // rows per output tile (16 per warp: two m8 fragments)
-constexpr int SBK = 16;      // k-chunk per pipeline stage
-constexpr int SSTAGES = 4;
+#ifndef HT_SS2_DEBUG_NOLOAD
+#define HT_SS2_DEBUG_NOLOAD 0
+#endif
+#ifndef HT_SS2_DEBUG_SMALLC
+#define HT_SS2_DEBUG_SMALLC 0
+#endif
+#ifndef HT_SS2_DEBUG_NOSTORE
+#define HT_SS2_DEBUG_NOSTORE 0
+#endif
+#ifndef HT_SS2_CONS
+#define HT_SS2_CONS 8
+#endif
+#ifndef HT_SS2_STAGES
+#define HT_SS2_STAGES 5
+#endif
+constexpr int SBM = 16 * HT_SS2_CONS;  // rows per output tile (16 per consumer warp: two m8 fragments)
+constexpr int SBK = 16;                // k-chunk per pipeline stage
 constexpr int kSsMaxDescs = 32;
 constexpr int kSMs = 148;
 #ifndef SS_DEBUG_NO_EPILOGUE
@@ -37,11 +50,6 @@ __device__ __forceinline__ void cp8z(double* smem, const double* gmem, bool vali
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gmem), "r"(valid ? 8 : 0));
 }
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
-}
 
 __device__ __forceinline__ void cp16z(double* smem, const double* gmem, int valid_bytes) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
@@ -51,258 +59,198 @@ __device__ __forceinline__ void cp16z(double* smem, const double* gmem, int vali
 constexpr int PK = SBK + 4;  // [m][k] layout pitch (4 mod 16 doubles: conflict-free fragments)
 constexpr int XSTAGE = (SBK * PX > SBM * PK) ? SBK * PX : SBM * PK;  // doubles per stage
 
-// LAYOUT 0: X m-contiguous (x_lo == 1), staged [k][m]; copies are row pairs (m, m+1).
-// LAYOUT 1: X k-contiguous (x_k == 1), staged [m][k]; copies are k pairs.
-// VEC: pairs are 16-byte aligned and never straddle an M_lo boundary -> one 16-byte
-// cp.async per pair, else two 8-byte ones.
-template <int NF, int LAYOUT, int TRI>
-__global__ void __launch_bounds__(SST, 1) ss_kernel(const __grid_constant__ SsBatch b) {
-  constexpr int NP = NF * 8;
-  constexpr int PS = ss_pitch(NP);
-  extern __shared__ __align__(16) double smem[];
-  double* Xs = smem;                    // [SSTAGES][XSTAGE]
-  double* Ss = smem + SSTAGES * XSTAGE;  // [kp][PS]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int total = b.tile_begin[b.count];
-  const int G = gridDim.x;
-  int t = (int)((long long)blockIdx.x * total / G);
-  const int t_end = (int)((long long)(blockIdx.x + 1) * total / G);
+// X staging.  LAYOUT 0: X m-contiguous (x_lo == 1), staged [k][m]; copies are row
+// pairs (m, m+1).  LAYOUT 1: X k-contiguous (x_k == 1), staged [m][k]; copies are k
+// pairs.  VEC: pairs are 16-byte aligned and never straddle an M_lo boundary -> one
+// 16-byte cp.async per pair, else two 8-byte ones.
 
-  while (t < t_end) {
-    int di = 0;
-    while (di + 1 < b.count && t >= b.tile_begin[di + 1]) ++di;
-    const SsDesc& g = b.d[di];
-    const int tm = b.tiles_m[di];
-    const int local = t - b.tile_begin[di];
-    const int job = local / tm, mt0 = local - job * tm;
-    const int seg = min(t_end - t, tm - mt0);  // tiles of this (desc, job) in this CTA
-    if (g.active && *g.active == 0) {
-      t += seg;
-      continue;
-    }
-    const int K = g.K, N = g.N, M = g.M, M_lo = g.M_lo;
-    const int KT = (K + SBK - 1) / SBK;
-    const double* X = g.X + job * g.x_job;
-    const double* S = g.S + job * g.s_job;
-    double* C = g.C + job * g.c_job;
-    const bool vec = b.vec[di];
-    __syncthreads();  // the previous segment is done with the shared buffers
-
-    // stationary operand: S(k, n) for k < KT*SBK, n < NP (zero padded)
-    for (int e = tid; e < KT * SBK * NP; e += SST) {
-      const int k = e / NP, n = e - k * NP;
-      const bool ok = k < K && n < N;
-      cp8z(Ss + k * PS + n, ok ? S + k * g.s_k + n * g.s_n : S, ok);
-    }
-
-    // loader: LAYOUT 0 -> pair of rows (2*mp, 2*mp+1) with mp = tid%64, kk = tid/64 + 4q
-    //         LAYOUT 1 -> rows tid/8 + 32q, k pair (2*(tid%8), +1)
-    constexpr int NR = LAYOUT == 0 ? 2 : 4;
-    int ld_tile = -1;
-    const double* rowp[NR];
-    int rowv[NR];  // LAYOUT 0: valid rows of the pair (0..2); LAYOUT 1: row valid (0/1)
-    auto set_rows = [&](int mt) {
-      ld_tile = mt;
-      if (LAYOUT == 0) {
-        const int m = mt * SBM + 2 * (tid & 63);
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int mm = min(m + u, M - 1);
-          const int hi = mm / M_lo, lo = mm - hi * M_lo;
-          rowp[u] = X + hi * g.x_hi + lo * g.x_lo;
-        }
-        rowv[0] = max(0, min(2, M - m));
-      } else {
-#pragma unroll
-        for (int q = 0; q < NR; ++q) {
-          const int m = mt * SBM + (tid >> 3) + 32 * q;
-          rowv[q] = m < M;
-          const int mm = rowv[q] ? m : 0;
-          const int hi = mm / M_lo, lo = mm - hi * M_lo;
-          rowp[q] = X + hi * g.x_hi + lo * g.x_lo;
-        }
-      }
-    };
-    const int nsteps = seg * KT;
-    // loader cursor (step ld_s = (tile ld_mt, chunk ld_kc) into stage ld_st), advanced
-    // incrementally: no divisions in the steady state
-    int ld_s = 0, ld_mt = mt0, ld_kc = 0, ld_st = 0;
-    long long ld_koff = 0;  // LAYOUT 0: ld_kc * SBK * x_k
-    long long qoff[4];      // LAYOUT 0: k offset of each of the thread's four k rows
-#pragma unroll
-    for (int q = 0; q < 4; ++q) qoff[q] = (long long)((tid >> 6) + 4 * q) * g.x_k;
-    auto issue = [&]() {
-      if (ld_s < nsteps && !(SS_DEBUG_NO_XLOAD && ld_s >= SSTAGES)) {
-        if (ld_mt != ld_tile) set_rows(ld_mt);
-        double* xs = Xs + ld_st * XSTAGE;
-        const int kb = ld_kc * SBK;
-        if (LAYOUT == 0) {
-          const int r = 2 * (tid & 63);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const int kk = (tid >> 6) + 4 * q;
-            const int nv = kb + kk < K ? rowv[0] : 0;
-            double* dst = xs + kk * PX + r;
-            const long long ko = ld_koff + qoff[q];
-            if (vec) {
-              cp16z(dst, nv ? rowp[0] + ko : X, 8 * nv);
-            } else {
-              cp8z(dst, nv > 0 ? rowp[0] + ko : X, nv > 0);
-              cp8z(dst + 1, nv > 1 ? rowp[1] + ko : X, nv > 1);
-            }
-          }
-        } else {
-          const int kk = 2 * (tid & 7);
-          const int kv = max(0, min(2, K - (kb + kk)));
-#pragma unroll
-          for (int q = 0; q < NR; ++q) {
-            const int r = (tid >> 3) + 32 * q;
-            const int nv = rowv[q] ? kv : 0;
-            double* dst = xs + r * PK + kk;
-            if (vec) {
-              cp16z(dst, nv ? rowp[q] + kb + kk : X, 8 * nv);
-            } else {
-              cp8z(dst, nv > 0 ? rowp[q] + kb + kk : X, nv > 0);
-              cp8z(dst + 1, nv > 1 ? rowp[q] + kb + kk + 1 : X, nv > 1);
-            }
-          }
-        }
-      }
-      cp_commit();
-      ++ld_s;
-      ld_koff += (long long)SBK * g.x_k;
-      if (++ld_kc == KT) {
-        ld_kc = 0;
-        ld_koff = 0;
-        ++ld_mt;
-      }
-      if (++ld_st == SSTAGES) ld_st = 0;
-    };
-#pragma unroll
-    for (int s = 0; s < SSTAGES - 1; ++s) issue();  // S travels with the first group
-
-    double acc[NF][4];  // m16n8 accumulators: rows g, g+8 of the warp's 16, cols 2t, 2t+1
-    const int g8 = lane >> 2, t4 = lane & 3;
-    const int ar = warp * 16 + g8;
-    const double alpha = g.alpha, beta = g.beta;
-    // the (k-range [k_lo, k_hi], fragment j) MMA block is structurally zero (TRI is the
-    // batch's triangular pattern of S, a template parameter: dense batches have no branches)
-    auto zero_block = [&](int k_lo, int k_hi, int j) {
-      return (TRI == 1 && k_hi < 8 * j) || (TRI == 2 && k_lo > 8 * j + 7);
-    };
-    // fragment element (row ar + 8*rs, k) of the current stage
-    auto xa = [&](const double* xs, int rs, int k) -> double {
-      return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
-    };
-    // tiles outer, k-chunks inner: the accumulators live in fixed registers through the
-    // chunk loop (no epilogue branch inside it) while the loader cursor runs ahead
-    // across tile boundaries
-    int st = 0;
-    for (int mt = mt0; mt < mt0 + seg; ++mt) {
-#pragma unroll
-      for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-      for (int kc = 0; kc < KT; ++kc) {
-        cp_wait<SSTAGES - 2>();
-        __syncthreads();
-        issue();
-        const double* xs = Xs + st * XSTAGE;
-        const double* ss = Ss + kc * SBK * PS;
-        if (++st == SSTAGES) st = 0;
-        const int kv = K - kc * SBK;  // valid k of this chunk (zero-filled beyond)
-        const int kg = kc * SBK;      // global k of the chunk
-        if (kv >= 12) {  // m16n8k16 (k rows beyond K are zero in shared memory)
-          double a[8];
-#pragma unroll
-          for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
-#pragma unroll
-          for (int j = 0; j < NF; ++j) {
-            double bq[4];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
-            if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
-          }
-        } else {  // tail: k8 and/or k4 steps
-          int k0 = 0;
-          if (kv > 4) {
-            double a[4], bq[2];
-#pragma unroll
-            for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              bq[0] = ss[t4 * PS + j * 8 + g8];
-              bq[1] = ss[(t4 + 4) * PS + j * 8 + g8];
-              dmma_16x8x8(acc[j], a, bq);
-            }
-            k0 = 8;
-          }
-          if (kv > k0) {
-            double a[2], bq[1];
-            a[0] = xa(xs, 0, k0 + t4);
-            a[1] = xa(xs, 1, k0 + t4);
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              bq[0] = ss[(k0 + t4) * PS + j * 8 + g8];
-              dmma_16x8x4(acc[j], a, bq);
-            }
-          }
-        }
-      }
-      if (SS_DEBUG_NO_EPILOGUE) {
-        if (alpha == 12345.0)  // keep the MMAs alive
-          for (int j = 0; j < NF; ++j) C[j] = acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
-        continue;
-      }
-#pragma unroll
-      for (int f = 0; f < 2; ++f) {
-        const int m = mt * SBM + ar + 8 * f;
-        if (m < M) {
-          const int hi = m / M_lo, lo = m - hi * M_lo;
-          double* crow = C + hi * g.c_hi + lo * g.c_lo;
-          const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
-#pragma unroll
-          for (int j = 0; j < NF; ++j) {
-            const int n = j * 8 + 2 * t4;
-            const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
-            if (pair && n + 1 < N) {
-              double2 r = make_double2(alpha * v0, alpha * v1);
-              double2* p = reinterpret_cast<double2*>(crow + n);
-              if (beta != 0.0) {
-                const double2 o = *p;
-                r.x += beta * o.x;
-                r.y += beta * o.y;
-              }
-              *p = r;
-            } else {
-              if (n < N) {
-                double* p = crow + (long long)n * g.c_n;
-                *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
-              }
-              if (n + 1 < N) {
-                double* p = crow + (long long)(n + 1) * g.c_n;
-                *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
-              }
-            }
-          }
-        }
-      }
-    }
-    cp_wait<0>();
-    t += seg;
-  }
-}
-
-
-// ---- warp-specialised variant --------------------------------------------------
-// Same tiles and MMA schedule as ss_kernel (8 consumer warps x 16 rows, S resident),
-// but two producer warps stage the X chunks (cp.async, completion counted on a
+// ---- warp-specialised pipeline ------------------------------------------------
+// 8 consumer warps x 16 rows with S resident in shared memory; two producer warps
+// stage the X chunks (cp.async, completion counted on a
 // per-stage `full` mbarrier) and the consumers release each stage on an `empty`
 // mbarrier: no CTA-wide barrier per 16-deep k-chunk, so consumer warps drift and the
 // producers run up to SS2_STAGES chunks ahead, across tile boundaries.  The only CTA
 // barriers left are at job (segment) boundaries, where S is reloaded.
-constexpr int SS2_CONS = 8;
+// Triangular stationary operands: the MMA fragments j of k-chunk kc that are not
+// structurally zero form one contiguous range [lo, hi) (TRI 1: S(k, n) = 0 for k < n ->
+// j < 2 kc + 2; TRI 2: S(k, n) = 0 for k > n -> j >= 2 kc).  Each chunk index gets its
+// own fully unrolled, branch-free MMA sequence (a per-fragment skip branch kept ptxas
+// from interleaving the fragments' dependent DMMA chains).
+template <int NF, int TRI, int KC>
+struct TriRange {
+  static constexpr int lo = TRI == 2 ? (2 * KC < NF ? 2 * KC : NF) : 0;
+  static constexpr int hi = TRI == 1 ? (2 * KC + 2 < NF ? 2 * KC + 2 : NF) : NF;
+};
+
+template <int LO, int HI, int J0, int NJ, int PS>
+__device__ __forceinline__ void ss_mma_range(double (&acc)[NJ][4], const double (&a)[8], const double* ss, int t4,
+                                             int g8) {
+  constexpr int lo = LO > J0 ? LO : J0;
+  constexpr int hi = HI < J0 + NJ ? HI : J0 + NJ;
+#pragma unroll
+  for (int j = lo; j < hi; ++j) {
+    double bq[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
+    dmma_16x8x16(acc[j - J0], a, bq);
+  }
+}
+
+template <int NF, int TRI, int PS, int J0, int NJ>
+__device__ __forceinline__ void ss_mma_chunk(int kc, double (&acc)[NJ][4], const double (&a)[8], const double* ss,
+                                             int t4, int g8) {
+  if (TRI == 0) {
+    ss_mma_range<0, NF, J0, NJ, PS>(acc, a, ss, t4, g8);
+    return;
+  }
+  switch (kc) {
+#define HT_SS_CASE(c)                                                                                          \
+  case c:                                                                                                     \
+    ss_mma_range<TriRange<NF, TRI, c>::lo, TriRange<NF, TRI, c>::hi, J0, NJ, PS>(acc, a, ss, t4, g8);        \
+    break;
+    HT_SS_CASE(0) HT_SS_CASE(1) HT_SS_CASE(2) HT_SS_CASE(3) HT_SS_CASE(4) HT_SS_CASE(5) HT_SS_CASE(6)
+#undef HT_SS_CASE
+    default:  // kc >= 7 (K > 112): every fragment of a TRI 1 chunk, j >= 14 of TRI 2 (none when NF <= 13)
+      ss_mma_range<TriRange<NF, TRI, 7>::lo, TriRange<NF, TRI, 7>::hi, J0, NJ, PS>(acc, a, ss, t4, g8);
+      break;
+  }
+}
+
+// consumer warps: HT_SS2_CONS row groups of 16 rows, each split over HT_SS2_NSPLIT
+// warps along n (more warps per scheduler to hide the DMMA / shared-memory latency)
+#ifndef HT_SS2_NSPLIT
+#define HT_SS2_NSPLIT 1
+#endif
+constexpr int SS2_NSPLIT = HT_SS2_NSPLIT;
+constexpr int SS2_CONS = HT_SS2_CONS * SS2_NSPLIT;
 constexpr int SS2_PROD = 2;
 constexpr int SS2_T = (SS2_CONS + SS2_PROD) * 32;
-constexpr int SS2_STAGES = 5;
+constexpr int SS2_STAGES = HT_SS2_STAGES;
+
+// Consumer warp: 16 rows (row group rg) x fragments [J0, J0 + NJ) of every tile of the
+// CTA's segment; X chunks from the `full` ring, released on `empty`.
+template <int NF, int LAYOUT, int TRI, int PS, int J0, int NJ>
+__device__ __forceinline__ void ss2_consume(const SsDesc& g, const double* Xs, const double* Ss,
+                                            unsigned long long* full, unsigned long long* empty, unsigned& gs,
+                                            int mt0, int seg, int KT, double* C, int rg, int lane) {
+  const int K = g.K, N = g.N, M = g.M, M_lo = g.M_lo;
+  double acc[NJ][4];
+  const int g8 = lane >> 2, t4 = lane & 3;
+  const int ar = rg * 16 + g8;
+  const double alpha = g.alpha, beta = g.beta;
+  auto xa = [&](const double* xs, int rs, int k) -> double {
+    return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
+  };
+  for (int mt = mt0; mt < mt0 + seg; ++mt) {
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
+    for (int kc = 0; kc < KT; ++kc, ++gs) {
+      const int st = gs % SS2_STAGES;
+      mbar_wait(&full[st], (gs / SS2_STAGES) & 1);
+      const double* xs = Xs + st * XSTAGE;
+      const double* ss = Ss + kc * SBK * PS;
+      const int kv = K - kc * SBK;
+      if (kv >= 12) {
+        double a[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
+        ss_mma_chunk<NF, TRI, PS, J0, NJ>(kc, acc, a, ss, t4, g8);
+      } else {
+        int k0 = 0;
+        if (kv > 4) {
+          double a[4], bq[2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
+#pragma unroll
+          for (int j = J0; j < J0 + NJ; ++j) {
+            bq[0] = ss[t4 * PS + j * 8 + g8];
+            bq[1] = ss[(t4 + 4) * PS + j * 8 + g8];
+            dmma_16x8x8(acc[j - J0], a, bq);
+          }
+          k0 = 8;
+        }
+        if (kv > k0) {
+          double a[2], bq[1];
+          a[0] = xa(xs, 0, k0 + t4);
+          a[1] = xa(xs, 1, k0 + t4);
+#pragma unroll
+          for (int j = J0; j < J0 + NJ; ++j) {
+            bq[0] = ss[(k0 + t4) * PS + j * 8 + g8];
+            dmma_16x8x4(acc[j - J0], a, bq);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+    if (HT_SS2_DEBUG_NOSTORE) {  // timing experiments: keep the MMAs alive, store nothing
+      double z = 0.0;
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) z += acc[j][0] + acc[j][1] + acc[j][2] + acc[j][3];
+      if (alpha == 12345.0) C[lane] = z;
+      continue;
+    }
+    // m-contiguous outputs (c_lo == 1, e.g. t1^T and the projections): lanes g8 and
+    // g8 ^ 1 swap one value per fragment so each stores a 16-byte (m, m + 1) pair
+    // (dense stationary operands only: the triangular instances are register-bound)
+    const bool mpair = TRI == 0 && beta == 0.0 && g.c_lo == 1 && g.c_n != 1 && !(M_lo & 1) && !(g.c_hi & 1) &&
+                       !(g.c_n & 1) && !(((uintptr_t)C) & 15);
+    if (mpair) {
+      const bool odd = g8 & 1;
+#pragma unroll
+      for (int f = 0; f < 2; ++f) {
+        const int m0 = (HT_SS2_DEBUG_SMALLC ? 0 : mt * SBM) + rg * 16 + 8 * f + (g8 & ~1);
+        const int hi = m0 / M_lo, lo = m0 - hi * M_lo;
+        double* crow = C + hi * g.c_hi + lo;
+#pragma unroll
+        for (int j = J0; j < J0 + NJ; ++j) {
+          const double keep = odd ? acc[j - J0][2 * f + 1] : acc[j - J0][2 * f];
+          const double got = __shfl_xor_sync(0xffffffffu, odd ? acc[j - J0][2 * f] : acc[j - J0][2 * f + 1], 4);
+          const int col = j * 8 + 2 * t4 + (odd ? 1 : 0);
+          if (col < N && m0 < M) {
+            double* p = crow + (long long)col * g.c_n;
+            const double r0 = alpha * (odd ? got : keep), r1 = alpha * (odd ? keep : got);
+            if (m0 + 1 < M) *reinterpret_cast<double2*>(p) = make_double2(r0, r1);
+            else *p = r0;
+          }
+        }
+      }
+    } else
+#pragma unroll
+    for (int f = 0; f < 2; ++f) {
+      const int m = (HT_SS2_DEBUG_SMALLC ? 0 : mt * SBM) + ar + 8 * f;
+      if (m < M) {
+        const int hi = m / M_lo, lo = m - hi * M_lo;
+        double* crow = C + hi * g.c_hi + lo * g.c_lo;
+        const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
+#pragma unroll
+        for (int j = J0; j < J0 + NJ; ++j) {
+          const int n = j * 8 + 2 * t4;
+          const double v0 = acc[j - J0][2 * f], v1 = acc[j - J0][2 * f + 1];
+          if (pair && n + 1 < N) {
+            double2 r = make_double2(alpha * v0, alpha * v1);
+            double2* p = reinterpret_cast<double2*>(crow + n);
+            if (beta != 0.0) {
+              const double2 o = *p;
+              r.x += beta * o.x;
+              r.y += beta * o.y;
+            }
+            *p = r;
+          } else {
+            if (n < N) {
+              double* p = crow + (long long)n * g.c_n;
+              *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
+            }
+            if (n + 1 < N) {
+              double* p = crow + (long long)(n + 1) * g.c_n;
+              *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
+            }
+          }
+        }
+      }
+    }
+  }
+}
 
 template <int NF, int LAYOUT, int TRI>
 __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ SsBatch b) {
@@ -399,7 +347,8 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
         mbar_wait(&empty[st], ((gs / SS2_STAGES) & 1) ^ 1);
         double* xs = Xs + st * XSTAGE;
         const int kb = kc * SBK;
-        if (LAYOUT == 0) {
+        if (HT_SS2_DEBUG_NOLOAD && s >= SS2_STAGES) {
+        } else if (LAYOUT == 0) {
           const int r = 2 * pl;
 #pragma unroll
           for (int kk = 0; kk < SBK; ++kk) {
@@ -437,124 +386,15 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
       }
     } else {
       // ---------------- consumers ----------------
-      double acc[NF][4];
-      const int g8 = lane >> 2, t4 = lane & 3;
-      const int ar = warp * 16 + g8;
-      const double alpha = g.alpha, beta = g.beta;
-      auto zero_block = [&](int k_lo, int k_hi, int j) {
-        return (TRI == 1 && k_hi < 8 * j) || (TRI == 2 && k_lo > 8 * j + 7);
-      };
-      auto xa = [&](const double* xs, int rs, int k) -> double {
-        return LAYOUT == 0 ? xs[k * PX + ar + 8 * rs] : xs[(ar + 8 * rs) * PK + k];
-      };
-      for (int mt = mt0; mt < mt0 + seg; ++mt) {
-#pragma unroll
-        for (int j = 0; j < NF; ++j) acc[j][0] = acc[j][1] = acc[j][2] = acc[j][3] = 0.0;
-        for (int kc = 0; kc < KT; ++kc, ++gs) {
-          const int st = gs % SS2_STAGES;
-          mbar_wait(&full[st], (gs / SS2_STAGES) & 1);
-          const double* xs = Xs + st * XSTAGE;
-          const double* ss = Ss + kc * SBK * PS;
-          const int kv = K - kc * SBK;
-          const int kg = kc * SBK;
-          if (kv >= 12) {
-            double a[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              double bq[4];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) bq[i] = ss[(t4 + 4 * i) * PS + j * 8 + g8];
-              if (!zero_block(kg, kg + 15, j)) dmma_16x8x16(acc[j], a, bq);
-            }
-          } else {
-            int k0 = 0;
-            if (kv > 4) {
-              double a[4], bq[2];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) a[i] = xa(xs, i & 1, t4 + 4 * (i >> 1));
-#pragma unroll
-              for (int j = 0; j < NF; ++j) {
-                bq[0] = ss[t4 * PS + j * 8 + g8];
-                bq[1] = ss[(t4 + 4) * PS + j * 8 + g8];
-                dmma_16x8x8(acc[j], a, bq);
-              }
-              k0 = 8;
-            }
-            if (kv > k0) {
-              double a[2], bq[1];
-              a[0] = xa(xs, 0, k0 + t4);
-              a[1] = xa(xs, 1, k0 + t4);
-#pragma unroll
-              for (int j = 0; j < NF; ++j) {
-                bq[0] = ss[(k0 + t4) * PS + j * 8 + g8];
-                dmma_16x8x4(acc[j], a, bq);
-              }
-            }
-          }
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&empty[st]);
-        }
-        // m-contiguous outputs (c_lo == 1, e.g. t1^T and the projections): lanes g8 and
-        // g8 ^ 1 swap one value per fragment so each stores a 16-byte (m, m + 1) pair
-        // (dense stationary operands only: the triangular instances are register-bound)
-        const bool mpair = TRI == 0 && beta == 0.0 && g.c_lo == 1 && g.c_n != 1 && !(M_lo & 1) && !(g.c_hi & 1) &&
-                           !(g.c_n & 1) && !(((uintptr_t)C) & 15);
-        if (mpair) {
-          const bool odd = g8 & 1;
-#pragma unroll
-          for (int f = 0; f < 2; ++f) {
-            const int m0 = mt * SBM + warp * 16 + 8 * f + (g8 & ~1);
-            const int hi = m0 / M_lo, lo = m0 - hi * M_lo;
-            double* crow = C + hi * g.c_hi + lo;
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              const double keep = odd ? acc[j][2 * f + 1] : acc[j][2 * f];
-              const double got = __shfl_xor_sync(0xffffffffu, odd ? acc[j][2 * f] : acc[j][2 * f + 1], 4);
-              const int col = j * 8 + 2 * t4 + (odd ? 1 : 0);
-              if (col < N && m0 < M) {
-                double* p = crow + (long long)col * g.c_n;
-                const double r0 = alpha * (odd ? got : keep), r1 = alpha * (odd ? keep : got);
-                if (m0 + 1 < M) *reinterpret_cast<double2*>(p) = make_double2(r0, r1);
-                else *p = r0;
-              }
-            }
-          }
-        } else
-#pragma unroll
-        for (int f = 0; f < 2; ++f) {
-          const int m = mt * SBM + ar + 8 * f;
-          if (m < M) {
-            const int hi = m / M_lo, lo = m - hi * M_lo;
-            double* crow = C + hi * g.c_hi + lo * g.c_lo;
-            const bool pair = g.c_n == 1 && ((((uintptr_t)crow) & 15) == 0);
-#pragma unroll
-            for (int j = 0; j < NF; ++j) {
-              const int n = j * 8 + 2 * t4;
-              const double v0 = acc[j][2 * f], v1 = acc[j][2 * f + 1];
-              if (pair && n + 1 < N) {
-                double2 r = make_double2(alpha * v0, alpha * v1);
-                double2* p = reinterpret_cast<double2*>(crow + n);
-                if (beta != 0.0) {
-                  const double2 o = *p;
-                  r.x += beta * o.x;
-                  r.y += beta * o.y;
-                }
-                *p = r;
-              } else {
-                if (n < N) {
-                  double* p = crow + (long long)n * g.c_n;
-                  *p = beta != 0.0 ? alpha * v0 + beta * *p : alpha * v0;
-                }
-                if (n + 1 < N) {
-                  double* p = crow + (long long)(n + 1) * g.c_n;
-                  *p = beta != 0.0 ? alpha * v1 + beta * *p : alpha * v1;
-                }
-              }
-            }
-          }
-        }
+      constexpr int NFA = SS2_NSPLIT == 1 ? NF : (NF + 1) / 2;
+      const int rg = warp / SS2_NSPLIT;
+      if constexpr (SS2_NSPLIT == 1) {
+        ss2_consume<NF, LAYOUT, TRI, PS, 0, NF>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
+      } else {
+        if (warp % SS2_NSPLIT == 0)
+          ss2_consume<NF, LAYOUT, TRI, PS, 0, NFA>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
+        else
+          ss2_consume<NF, LAYOUT, TRI, PS, NFA, NF - NFA>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
       }
     }
     t += seg;
@@ -566,28 +406,17 @@ size_t ss2_smem(int nf, int kp) {
   return sizeof(double) * ((size_t)SS2_STAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8));
 }
 
-// HT_SS_WS=0: the CTA-barrier cp.async pipeline (A/B comparisons)
-const int g_ss_ws = [] {
-  const char* e = std::getenv("HT_SS_WS");
-  return e && e[0] == '0' ? 0 : 1;
-}();
-
-size_t ss_smem(int nf, int kp) { return sizeof(double) * ((size_t)SSTAGES * XSTAGE + (size_t)kp * ss_pitch(nf * 8)); }
-
 template <int NF, int LAYOUT, int TRI>
 int launch_ss(SsBatch& b, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    HT_CUDA_CHECK(cudaFuncSetAttribute(ss_kernel<NF, LAYOUT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)ss_smem(NF, kSsMaxK)));
     HT_CUDA_CHECK(cudaFuncSetAttribute(ss2_kernel<NF, LAYOUT, TRI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)ss2_smem(NF, kSsMaxK)));
     attr = true;
   }
   const int total = b.tile_begin[b.count];
   const int grid = std::min(total, kSMs);  // persistent: balanced contiguous tile ranges
-  if (g_ss_ws) ss2_kernel<NF, LAYOUT, TRI><<<grid, SS2_T, ss2_smem(NF, b.kp), s>>>(b);
-  else ss_kernel<NF, LAYOUT, TRI><<<grid, SST, ss_smem(NF, b.kp), s>>>(b);
+  ss2_kernel<NF, LAYOUT, TRI><<<grid, SS2_T, ss2_smem(NF, b.kp), s>>>(b);
   HT_LAUNCH_CHECK();
   return kOk;
 }

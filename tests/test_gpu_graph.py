@@ -174,3 +174,35 @@ def test_host_resident_tensor_rejected(cuda_ok):
     xh = htb.HTensor(tree, *f, device="cpu")
     with pytest.raises(ValueError, match="CUDA"):
         htb.truncate(xh, htb.TruncationControl.fixed_rank(2))
+
+
+def test_out_buffers_replay_without_relocation(cuda_ok):
+    """add(..., out=) / truncate(..., out=) write into fixed buffers: the results equal the
+    allocating calls bit for bit, alternating buffer pairs replay their own captured graphs
+    (no relocation), and wrong shapes / data-dependent ranks are rejected."""
+    import paper_1708_03340_b200 as htb
+
+    tree = htb.build_balanced_tree(8)
+    a, c = htb.gaussian_htensor(tree, 150, 16, 5), htb.gaussian_htensor(tree, 150, 16, 6)
+    ctl = htb.TruncationControl.fixed_rank(16)
+    ref = _arrays(htb.truncate(htb.add(a, c), ctl))
+    x0 = htb.add(a, c)
+    xb = [htb.HTensor.empty(tree, *x0.host_layout()) for _ in range(2)]
+    t0 = htb.truncate(x0, ctl)
+    tb = [htb.HTensor.empty(tree, *t0.host_layout()) for _ in range(2)]
+    for i in range(6):
+        x = htb.add(a, c, out=xb[i % 2])
+        t = htb.truncate(x, ctl, out=tb[i % 2])
+        assert t is tb[i % 2]
+        for u, v in zip(_arrays(t), ref):
+            np.testing.assert_array_equal(u, v)
+    r0 = htb.graph_relocations()
+    for i in range(4):
+        htb.truncate(htb.add(a, c, out=xb[i % 2]), ctl, out=tb[i % 2])
+    assert htb.graph_relocations() == r0
+    with pytest.raises(ValueError):
+        htb.truncate(x0, htb.TruncationControl.fixed_rank(8), out=tb[0])
+    with pytest.raises(ValueError):
+        htb.truncate(x0, htb.TruncationControl.accuracy(1e-3), out=tb[0])
+    with pytest.raises(ValueError):
+        htb.add(a, a, out=tb[0])

@@ -1,4 +1,7 @@
-// Stand-alone timing of the streaming GEMM on the truncation's shapes (experiments).
+// Stand-alone timing of the streaming GEMM on the truncation's C2 d=64 level-5 shapes
+// (32 nodes, K = 100): the Gramian t1 product (dense), the two absorb mode products
+// (triangular R^T) and the first projection mode product (N = 50).  Build variants
+// with -DHT_SS2_CONS=.. -DHT_SS2_STAGES=.. (experiments only).
 #include <cstdio>
 #include <vector>
 #include "../paper_1708_03340_b200/csrc/ssgemm.cu"
@@ -6,37 +9,55 @@ namespace ht {
 ProfToken prof_begin(cudaStream_t) { return ProfToken{}; }
 void prof_end(const ProfToken&, const char*, cudaStream_t, double, double) {}
 void set_error(const std::string& m) { fprintf(stderr, "%s\n", m.c_str()); }
+extern const int g_sync_check = 0;
+int debug_probe() { return 0; }
 }  // namespace ht
 using namespace ht;
 
 int main() {
-  const int K = 100, N = 100, nodes = 32, kt = 100, k1 = 100, k2 = 100;
+  const int K = 100, nodes = 32;
+  const long long K3 = (long long)K * K * K;
   double *X, *S, *C;
-  const size_t big = (size_t)nodes * kt * k1 * k2;
-  cudaMalloc(&X, big * 8); cudaMalloc(&C, big * 8); cudaMalloc(&S, (size_t)nodes * K * N * 8);
-  cudaMemset(X, 0, big * 8); cudaMemset(S, 0, (size_t)nodes * K * N * 8);
+  cudaMalloc(&X, nodes * K3 * 8); cudaMalloc(&C, nodes * K3 * 8); cudaMalloc(&S, (size_t)nodes * K * K * 8);
+  cudaMemset(X, 0, nodes * K3 * 8); cudaMemset(S, 0, (size_t)nodes * K * K * 8);
   cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-  for (int variant = 0; variant < 2; ++variant) {
+  const char* names[] = {"t1 (dense, N=100)", "absorb mode-2 (tri)", "absorb mode-3 (tri)", "project mode-1 (N=50)"};
+  for (int variant = 0; variant < 4; ++variant) {
     std::vector<SsDesc> v;
-    if (variant == 0) {  // mode-3 absorb: X row-major (k-contiguous)
-      SsDesc d = ss_desc(X, k2, 1, S, 1, k2, C, N, 1, kt * k1, N, k2);
-      d.jobs = nodes; d.x_job = (long long)kt * k1 * k2; d.s_job = K * N; d.c_job = (long long)kt * k1 * N;
+    double frac = 1.0;
+    int N = K;
+    if (variant == 0) {  // t1^T = M1(B)^T G^T: rows (j,l) contiguous, k = i
+      SsDesc d = ss_desc(X, 1, (long long)K * K, S, 1, K, C, 1, (long long)K * K, K * K, K, K);
+      d.jobs = nodes; d.x_job = K3; d.s_job = K * K; d.c_job = K3;
       v.push_back(d);
-    } else {  // mode-2 absorb: two-level rows, m-contiguous X, column-major C
-      SsDesc d = ss_desc(X, 1, k2, S, 1, k1, C, 1, k2, kt * k2, N, k1);
-      d.M_lo = k2; d.x_hi = (long long)k1 * k2; d.c_hi = (long long)N * k2;
-      d.jobs = nodes; d.x_job = (long long)kt * k1 * k2; d.s_job = K * N; d.c_job = (long long)kt * N * k2;
+    } else if (variant == 1) {  // T1_i^T = B_i^T R1^T over rows (i, l)
+      SsDesc d = ss_desc(X, 1, K, S, 1, K, C, 1, K, K * K, K, K);
+      d.M_lo = K; d.x_hi = (long long)K * K; d.c_hi = (long long)K * K; d.s_tri = 1;
+      d.jobs = nodes; d.x_job = K3; d.s_job = K * K; d.c_job = K3;
+      v.push_back(d); frac = 0.5;
+    } else if (variant == 2) {  // Bp = T1 R2^T, rows (i, j) k-contiguous
+      SsDesc d = ss_desc(X, K, 1, S, 1, K, C, K, 1, K * K, K, K);
+      d.s_tri = 1;
+      d.jobs = nodes; d.x_job = K3; d.s_job = K * K; d.c_job = K3;
+      v.push_back(d); frac = 0.5;
+    } else {  // C1^T = M1(B)^T PEV (N = 50)
+      N = 50;
+      SsDesc d = ss_desc(X, 1, (long long)K * K, S, N, 1, C, 1, (long long)K * K, K * K, N, K);
+      d.jobs = nodes; d.x_job = K3; d.s_job = K * N; d.c_job = (long long)K * K * N;
       v.push_back(d);
     }
     ss_gemm(v, 0, "x");
     cudaEventRecord(e0);
-    for (int r = 0; r < 10; ++r) ss_gemm(v, 0, "x");
+    const int reps = 20;
+    for (int r = 0; r < reps; ++r) ss_gemm(v, 0, "x");
     cudaEventRecord(e1);
     cudaEventSynchronize(e1);
-    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 10;
-    const double fl = 2.0 * nodes * (double)kt * k1 * k2 * N;
-    printf("variant %d (%s): %.1f us  %.2f TF/s  (err %s)\n", variant, variant ? "mode-2" : "mode-3", ms * 1e3,
-           fl / ms / 1e9, cudaGetErrorString(cudaGetLastError()));
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= reps;
+    const double fl = 2.0 * nodes * (double)K * K * K * N;
+    const double by = 8.0 * nodes * ((double)K * K * K + (double)K * K * N);
+    printf("CONS=%d STAGES=%d %-24s %7.1f us  alg %5.2f TF/s  exec %5.2f TF/s  %5.2f TB/s  (%s)\n", HT_SS2_CONS,
+           HT_SS2_STAGES, names[variant], ms * 1e3, fl / ms / 1e9, frac * fl / ms / 1e9, by / ms / 1e9,
+           cudaGetErrorString(cudaGetLastError()));
   }
   return 0;
 }
