@@ -59,6 +59,9 @@ struct CholBatch {
 // diagonal in rinv.  Outputs: R, R^{-1}, the red flag (a pivot loses more than 10
 // digits against its column norm, anything non-finite, or -- second pass -- W not
 // within 0.1 of I) and the ||R||_F ||R^{-1}||_F estimate that decides the second pass.
+#ifndef HT_CHOL_TIMING
+#define HT_CHOL_TIMING 0  // 1: block 0 prints its phase times (clock64) -- experiments only
+#endif
 constexpr int kC2Threads = 256;
 constexpr int kC2Warps = kC2Threads / 32;
 
@@ -88,34 +91,37 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   const long long off = (long long)node * K * K;
   const double* Wg = c.W + off;
   if (tid == 0) bad = 0;
+  long long clk[6] = {clock64(), 0, 0, 0, 0, 0};
 
-  // load: A[r][cc] = W[r][cc] for r >= cc, zero elsewhere (W is symmetric: the Gram
-  // GEMMs write both triangles), row-major on both sides; eight loads in flight per thread
+  // load: the whole K x K block into A (zero-filled padding) with every copy in flight
+  // at once (cp.async, 16-byte pairs when the rows allow); the factorisation reads the
+  // lower triangle only (W is symmetric: the Gram GEMMs write both triangles) and the
+  // strict upper triangle is overwritten by X = L^{-1} later
+  {
+    const bool v16 = !(K & 1) && !(((uintptr_t)Wg) & 15);
+    const int rw = v16 ? Kp / 2 : Kp;  // copies per row
+    for (int e = tid; e < Kp * rw; e += kC2Threads) {
+      const int r = e / rw, cc = (e - r * rw) * (v16 ? 2 : 1);
+      const unsigned sa = (unsigned)__cvta_generic_to_shared(A + r * P + cc);
+      const bool ok = r < K && cc < K;
+      const double* src = ok ? Wg + (long long)r * K + cc : Wg;
+      if (v16)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 16 : 0));
+      else
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(src), "r"(ok ? 8 : 0));
+    }
+    asm volatile("cp.async.wait_all;\n" ::: "memory");
+    __syncthreads();
+  }
   double dev = 0.0;
   bool nonfinite = false;
-  for (int e0 = tid; e0 < Kp * Kp; e0 += 8 * kC2Threads) {
-    double v[8];
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * kC2Threads;
-      const int r = e / Kp, cc = e - r * Kp;
-      v[u] = (e < Kp * Kp && r < K && cc <= r) ? Wg[(long long)r * K + cc] : 0.0;
+  for (int r = warp; r < K; r += kC2Warps)
+    for (int cc = lane; cc <= r; cc += 32) {
+      const double x = A[r * P + cc];
+      dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
+      nonfinite |= !isfinite(x);
+      if (r == cc) d0[r] = x;
     }
-#pragma unroll
-    for (int u = 0; u < 8; ++u) {
-      const int e = e0 + u * kC2Threads;
-      if (e < Kp * Kp) {
-        const int r = e / Kp, cc = e - r * Kp;
-        const double x = v[u];
-        if (r < K && cc <= r) {
-          dev = fmax(dev, fabs(x - (r == cc ? 1.0 : 0.0)));
-          nonfinite |= !isfinite(x);
-          if (r == cc) d0[r] = x;
-        }
-        A[r * P + cc] = x;
-      }
-    }
-  }
   const int any_nonfinite = __syncthreads_or(nonfinite);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dev = fmax(dev, __shfl_xor_sync(0xffffffffu, dev, o));
@@ -128,6 +134,7 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   }
 
   const int nJ = Kp / 16;
+  if (HT_CHOL_TIMING) clk[1] = clock64();
   for (int J = 0; J < nJ; ++J) {
     const int j0 = 16 * J, jb = min(16, K - j0);
     // (a) diagonal block, warp 0, lane i owns row j0 + i; the scaled pivot column is
@@ -234,6 +241,7 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   auto xat = [&](int r, int cc) -> double {  // X element (zero above the diagonal / padding)
     return r >= K ? 0.0 : (r > cc ? A[cc * P + r] : (r == cc ? rinv[r] : 0.0));
   };
+  if (HT_CHOL_TIMING) clk[2] = clock64();
   // (d) diagonal blocks: warp w -> block w, lane cc -> column cc
   for (int J = warp; J < nJ; J += kC2Warps) {
     const int j0 = 16 * J;
@@ -259,6 +267,7 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
     }
   }
   __syncthreads();
+  if (HT_CHOL_TIMING) clk[3] = clock64();
   // (e) off-diagonal blocks by block distance: X_IJ = -X_II (sum_k L_Ik X_kJ)
   double* T = scratch + warp * 16 * 17;
   for (int dlt = 1; dlt < nJ; ++dlt) {
@@ -306,8 +315,9 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
     __syncthreads();
   }
 
+  if (HT_CHOL_TIMING) clk[4] = clock64();
   // outputs: R = L^T, R^{-1} = X^T (upper), zeros below; Frobenius norms for kappa
-  double* Rf = c.Rf + off;
+  double* Rf = c.Rf ? c.Rf + off : nullptr;
   double* Ri = c.Ri + off;
   double* Ro = c.Rout ? c.Rout + (long long)node * c.r_node : nullptr;
   double s0 = 0.0, s1 = 0.0;
@@ -315,7 +325,7 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
     const int i = e / K, j = e - i * K;
     const double rv = j >= i ? A[j * P + i] : 0.0;
     const double iv = j > i ? A[i * P + j] : (j == i ? rinv[i] : 0.0);
-    Rf[e] = rv;
+    if (Rf) Rf[e] = rv;
     if (Ro) Ro[(long long)i * c.r_ld + j] = rv;
     Ri[e] = iv;
     s0 = fma(rv, rv, s0);
@@ -337,6 +347,11 @@ __global__ void __launch_bounds__(kC2Threads, 1) chol2_kernel(const __grid_const
   }
   __syncthreads();
   if (tid == 0 && bad) atomicOr(cb.fail, 1);
+  if (HT_CHOL_TIMING && tid == 0 && blockIdx.x == 0) {
+    clk[5] = clock64();
+    printf("chol2 K=%d: load %lld factor %lld inv-diag %lld inv-offdiag %lld out %lld cycles\n", K, clk[1] - clk[0],
+           clk[2] - clk[1], clk[3] - clk[2], clk[4] - clk[3], clk[5] - clk[4]);
+  }
 }
 
 int launch_chol(const std::vector<CholDesc>& ds, int* fail, cudaStream_t s, const char* tag = "cholqr_factor") {
@@ -428,7 +443,9 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
   for (size_t p = 0; p < cs.size(); ++p) {
     const CholQr& c = cs[p];
     CholDesc d{};
-    d.W = c.W; d.Rf = c.R1; d.Ri = c.q.rinv ? c.q.rinv : c.Ri; d.Rout = c.q.R; d.r_ld = c.q.r_ld;
+    // R1 goes to the output R only (the rarely taken second pass copies it back into
+    // c.R1 first): one fewer K x K store per node on the critical path
+    d.W = c.W; d.Rf = nullptr; d.Ri = c.q.rinv ? c.q.rinv : c.Ri; d.Rout = c.q.R; d.r_ld = c.q.r_ld;
     d.r_node = c.q.r_node;
     d.K = c.q.K; d.nodes = c.q.nodes;
     d.need2 = need2 + p;
@@ -505,6 +522,7 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
     }
     HT_TRY(launch_chol(ch, fail, s, "cholqr2_factor"));
     g.clear();
+    std::vector<GemmDesc> rcopy;
     for (size_t p = 0; p < cs.size(); ++p) {
       const CholQr& c = cs[p];
       const int K = c.q.K, m = c.q.m;
@@ -521,11 +539,17 @@ int cholqr_run(std::vector<CholQr>& cs, int* fail, int* need2, bool two_pass, cu
         d.active = need2 + p;
         g.push_back(d);
       }
+      GemmDesc cp = gemm_desc(nullptr, K, 1, c.q.R, c.q.r_ld, 1, c.R1, K, 1, K, K, K);  // R1 = copy of R
+      cp.a_tri = 3;
+      cp.nb1 = c.q.nodes; cp.b_b1 = c.q.r_node; cp.c_b1 = (long long)K * K;
+      cp.active = need2 + p;
+      rcopy.push_back(cp);
       GemmDesc e = gemm_desc(c.R2, K, 1, c.R1, K, 1, c.q.R, c.q.r_ld, 1, K, K, K);
       e.nb1 = c.q.nodes; e.a_b1 = (long long)K * K; e.b_b1 = (long long)K * K; e.c_b1 = c.q.r_node;
       e.active = need2 + p;
       g.push_back(e);
     }
+    HT_TRY(gemm_grouped(rcopy, s, "gemm_cholqr2_q", false));  // before R is overwritten by R2 R1
     HT_TRY(ss_gemm(sd, s, "ss_cholqr2_q", false));
     HT_TRY(gemm_grouped(g, s, "gemm_cholqr2_q", false));
     // the Q of an implicit problem is explicit now: its R^{-1} stand-in becomes I

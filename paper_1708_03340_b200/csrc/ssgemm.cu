@@ -116,13 +116,10 @@ __device__ __forceinline__ void ss_mma_chunk(int kc, double (&acc)[NJ][4], const
   }
 }
 
-// consumer warps: HT_SS2_CONS row groups of 16 rows, each split over HT_SS2_NSPLIT
-// warps along n (more warps per scheduler to hide the DMMA / shared-memory latency)
-#ifndef HT_SS2_NSPLIT
-#define HT_SS2_NSPLIT 1
-#endif
-constexpr int SS2_NSPLIT = HT_SS2_NSPLIT;
-constexpr int SS2_CONS = HT_SS2_CONS * SS2_NSPLIT;
+// (Measured alternatives that lost: n-split consumer warps, 16 warps x half the
+// fragments; two consumer groups on alternate tiles half a tile out of phase, to overlap
+// one group's epilogue with the other's MMAs: +5 % dense, -5 % triangular.)
+constexpr int SS2_CONS = HT_SS2_CONS;
 constexpr int SS2_PROD = 2;
 constexpr int SS2_T = (SS2_CONS + SS2_PROD) * 32;
 constexpr int SS2_STAGES = HT_SS2_STAGES;
@@ -386,16 +383,7 @@ __global__ void __launch_bounds__(SS2_T, 1) ss2_kernel(const __grid_constant__ S
       }
     } else {
       // ---------------- consumers ----------------
-      constexpr int NFA = SS2_NSPLIT == 1 ? NF : (NF + 1) / 2;
-      const int rg = warp / SS2_NSPLIT;
-      if constexpr (SS2_NSPLIT == 1) {
-        ss2_consume<NF, LAYOUT, TRI, PS, 0, NF>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
-      } else {
-        if (warp % SS2_NSPLIT == 0)
-          ss2_consume<NF, LAYOUT, TRI, PS, 0, NFA>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
-        else
-          ss2_consume<NF, LAYOUT, TRI, PS, NFA, NF - NFA>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, rg, lane);
-      }
+      ss2_consume<NF, LAYOUT, TRI, PS, 0, NF>(g, Xs, Ss, full, empty, gs, mt0, seg, KT, C, warp, lane);
     }
     t += seg;
   }
