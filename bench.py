@@ -48,6 +48,81 @@ def storage(d, n, k):
     return d * n * k + (d - 2) * k**3 + k**2
 
 
+def device_ms(fn, reps, warm=2):
+    """Mean device time of fn() over reps calls (CUDA events on the current stream)."""
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def fit_log2_model(d_values, times):
+    """t = a + b log2(d), least squares (reference bench.py:190-200); returns (a, b, r^2)."""
+    x = np.log2(np.asarray(d_values, float))
+    y = np.asarray(times, float)
+    b, a = np.polyfit(x, y, 1)
+    pred = a + b * x
+    ss_res, ss_tot = float(np.sum((y - pred) ** 2)), float(np.sum((y - y.mean()) ** 2))
+    return float(a), float(b), 1.0 if ss_tot == 0 else 1.0 - ss_res / ss_tot
+
+
+def secondary(htb, work, args):
+    """Secondary device timings on the bench tensors (1 GPU): the add that forms X
+    (HBM-bound block embedding), <T,T> (a14), the truncation of the
+    orthogonalised X (the paper's Fig. 5d number), and the truncation under the
+    Householder QR policy (the north star's QR; the default Cholesky-QR re-runs on it)."""
+    out = {}
+    x = work.x
+    ms = device_ms(lambda: htb.add(work.a, work.c, out=x), 10)
+    nbytes = 8 * (work.a.arena_numel() + work.c.arena_numel() + x.arena_numel())
+    out["add"] = {"ms": ms, "GB/s": nbytes / (ms * 1e-3) / 1e9, "bytes": nbytes,
+                  "hbm_frac": nbytes / (ms * 1e-3) / 1e9 / measured_peaks().get("hbm_gbs", 6521.1)}
+    T = work.step()
+    out["inner_product_TT"] = {"ms": device_ms(lambda: htb.inner_product_device(T, T), 10)}
+    xo = htb.orthogonalize(x)
+    out["truncate_orthogonal_input"] = {"ms": device_ms(lambda: htb.truncate(xo, work.ctl), 10)}
+    htb.set_qr_mode("householder")
+    try:
+        ms = device_ms(lambda: htb.truncate(x, work.ctl), 5)
+    finally:
+        htb.set_qr_mode("auto")
+    out["truncate_householder_qr"] = {"ms": ms, "truncations_per_s": 1e3 / ms}
+    return out
+
+
+def sweep(htb, args, world):
+    """C2 weak-scaling study: d = 8 .. 256 at n, k of the run; per d the
+    device time of add + truncate + <T,T> and the fit t = a + b log2 d (1 GPU: the
+    tree levels run one launch each, so time grows with the per-level work)."""
+    rows = []
+    for p in range(3, 9):
+        d = 2 ** p
+        tree = htb.build_balanced_tree(d)
+        a = htb.HTensor(tree, *htb.gaussian_factors(tree, args.n, args.k, 2 * p))
+        c = htb.HTensor(tree, *htb.gaussian_factors(tree, args.n, args.k, 2 * p + 1))
+        ctl = htb.TruncationControl.fixed_rank(args.k)
+        x = htb.add(a, c)
+        T = htb.truncate(x, ctl)
+        ms_add = device_ms(lambda: htb.add(a, c, out=x), 5)
+        ms_tr = device_ms(lambda: htb.truncate(x, ctl), 5)
+        ms_ip = device_ms(lambda: htb.inner_product_device(T, T), 5)
+        rows.append({"d": d, "log2_d": p, "add_ms": ms_add, "truncate_ms": ms_tr, "inner_product_ms": ms_ip,
+                     "total_ms": ms_add + ms_tr + ms_ip,
+                     "truncate_tflops": algorithmic_flops(d, args.n, 2 * args.k, args.k) / (ms_tr * 1e-3) / 1e12})
+        del a, c, x, T
+    a_, b_, r2 = fit_log2_model([r["d"] for r in rows], [r["total_ms"] for r in rows])
+    return {"rows": rows, "fit_total_ms": {"a": a_, "b": b_, "r2": r2, "model": "t = a + b log2 d"},
+            "n_gpus": world}
+
+
 class ClockSampler:
     """nvidia-smi-equivalent NVML sampling of SM clocks and throttle reasons during the timed region."""
 
@@ -432,6 +507,8 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.synchronize()
     prof = _lib.profile_report()
     lib.ht_profile_enable(0)
+    extra = secondary(htb, work, args) if world == 1 else None
+    sweep_res = sweep(htb, args, world) if (world == 1 and args.sweep) else None
 
     # end-to-end through the public API: pinned host A, C -> H2D -> add -> truncate -> D2H of T
     work.prepare_e2e()
@@ -507,6 +584,10 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if extra is not None:
+        line["secondary"] = extra
+    if sweep_res is not None:
+        line["sweep"] = sweep_res
     if world == 1 and not args.no_cpu_baseline:
         from oracle import htucker_oracle as orc  # checker / CPU baseline only
 
@@ -530,6 +611,8 @@ def main():
     ap.add_argument("--n", type=int, default=1000)
     ap.add_argument("--k", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sweep", action="store_true",
+                    help="also run the C2 weak-scaling study d = 8..256 (time vs log2 d, fit a + b log2 d)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replica tensors per GPU instead of one tree-sharded tensor")
     args = ap.parse_args()

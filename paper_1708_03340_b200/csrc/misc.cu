@@ -11,7 +11,8 @@ constexpr int MAXD = 64;
 
 struct EmbedBatch {
   int count;
-  int begin[MAXD + 1];
+  long long row_begin[MAXD + 1];  // prefix sums of the descriptors' output rows
+  unsigned char vec[MAXD];        // even extents / offsets, 16-byte aligned: pair copies
   EmbedDesc d[MAXD];
 };
 
@@ -34,45 +35,127 @@ __device__ __forceinline__ int find(const B& b) {
   return di;
 }
 
-// One warp per output row (i0, i1): the row's A segment, scaled C segment and zeros
-// are written with coalesced stores; index arithmetic once per row, not per element.
-__global__ void embed_kernel(const __grid_constant__ EmbedBatch b) {
-  const int di = find(b);
-  const EmbedDesc& e = b.d[di];
-  const long long rows = (long long)e.D0 * e.D1;
-  const int lane = threadIdx.x & 31, wpb = blockDim.x >> 5;
-  const long long nw = (long long)(b.begin[di + 1] - b.begin[di]) * wpb;
-  const bool vec = !((e.D2 | e.a2 | e.c2 | e.o2) & 1) &&
-                   !((((uintptr_t)e.out) | ((uintptr_t)e.A) | ((uintptr_t)e.C)) & 15);
-  for (long long r = (long long)(blockIdx.x - b.begin[di]) * wpb + (threadIdx.x >> 5); r < rows; r += nw) {
-    const int i0 = (int)(r / e.D1), i1 = (int)(r - (long long)i0 * e.D1);
-    double* o = e.out + r * e.D2;
-    const bool ina = i0 < e.a0 && i1 < e.a1;
-    const double* arow = e.A + ((long long)i0 * e.a1 + i1) * e.a2;
-    const int j0 = i0 - e.o0, j1 = i1 - e.o1;
-    const bool inc = j0 >= 0 && j1 >= 0 && j0 < e.c0 && j1 < e.c1;
-    const double* crow = e.C + ((long long)j0 * e.c1 + j1) * e.c2;
-    if (vec) {  // even extents and offsets: 16-byte pairs never straddle a segment edge
-      for (int p = lane; 2 * p < e.D2; p += 32) {
-        const int i2 = 2 * p, j2 = i2 - e.o2;
-        double2 v = make_double2(0.0, 0.0);
-        if (ina && i2 < e.a2) {
-          v = reinterpret_cast<const double2*>(arow)[p];
-        } else if (inc && j2 >= 0 && j2 < e.c2) {
-          const double2 c = reinterpret_cast<const double2*>(crow)[j2 >> 1];
-          v = make_double2(e.alpha_c * c.x, e.alpha_c * c.y);
-        }
-        reinterpret_cast<double2*>(o)[p] = v;
+// Block embedding of add.  Output rows (i0, i1) of D2 values, all descriptors' rows in
+// one global row space; each warp owns a contiguous run of rows (descriptor lookup once
+// per run) and works on four rows at a time: every lane issues the loads of all four
+// rows (A or scaled C segments; pure-zero rows -- half of every inner node -- load
+// nothing) before any store, so ~8 16-byte loads per lane are in flight.
+constexpr int kEmbedThreads = 256;
+constexpr int kEmbedU = 4;  // rows per warp step
+
+struct RowSrc {
+  const double* a;  // A row segment -> output [0, ahi), or null
+  const double* c;  // C row segment (indexed from clo) -> output [clo, chi), or null
+  int ahi, clo, chi;
+  // value pair (i2, i2 + 1) of the output row: exactly one source or zero
+  __device__ __forceinline__ bool from_a(int i2) const { return a && i2 < ahi; }
+  __device__ __forceinline__ bool from_c(int i2) const { return c && i2 >= clo && i2 < chi; }
+};
+
+// (a leaf row has both: U = [U_a, U_c]; an inner row at most one block)
+__device__ __forceinline__ RowSrc row_src(const EmbedDesc& e, int i0, int i1) {
+  RowSrc s{nullptr, nullptr, 0, 0, 0};
+  if (i0 < e.a0 && i1 < e.a1) {
+    s.a = e.A + ((long long)i0 * e.a1 + i1) * e.a2;
+    s.ahi = e.a2;
+  }
+  const int j0 = i0 - e.o0, j1 = i1 - e.o1;
+  if (j0 >= 0 && j1 >= 0 && j0 < e.c0 && j1 < e.c1) {
+    s.c = e.C + ((long long)j0 * e.c1 + j1) * e.c2 - e.o2;
+    s.clo = e.o2;
+    s.chi = e.o2 + e.c2;
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(kEmbedThreads, 4) embed_kernel(const __grid_constant__ EmbedBatch b) {
+  const int lane = threadIdx.x & 31;
+  const long long gw = (long long)blockIdx.x * (kEmbedThreads / 32) + (threadIdx.x >> 5);
+  const long long nwarps = (long long)gridDim.x * (kEmbedThreads / 32);
+  const long long total = b.row_begin[b.count];
+  long long r = total * gw / nwarps;
+  const long long r_end = total * (gw + 1) / nwarps;
+  int di = 0;
+  while (di + 1 < b.count && r >= b.row_begin[di + 1]) ++di;
+  while (r < r_end) {
+    const EmbedDesc& e = b.d[di];
+    const long long rd_end = min(r_end, b.row_begin[di + 1]);  // this descriptor's part of the run
+    const long long base = b.row_begin[di];
+    const bool vec = b.vec[di];
+    const int D2 = e.D2;
+    // (i0, i1) of the run's first row (one division per run), then stepped per row
+    int i0 = (int)((r - base) / e.D1), i1 = (int)((r - base) - (long long)i0 * e.D1);
+    auto step = [&]() {
+      if (++i1 == e.D1) {
+        i1 = 0;
+        ++i0;
       }
-      continue;
+    };
+    if (vec) {
+      const int P2 = D2 >> 1;  // 16-byte pairs per row
+      for (; r < rd_end; r += kEmbedU) {
+        double2 v[kEmbedU][2];  // only the loaded pairs stay live into the store phase
+        const double sc = e.alpha_c;
+        const int s0 = i0, s1 = i1;  // first row of this step (the long-row path restarts from it)
+#pragma unroll
+        for (int u = 0; u < kEmbedU; ++u) {
+          const RowSrc src = r + u < rd_end ? row_src(e, i0, i1) : RowSrc{nullptr, nullptr, 0, 0, 0};
+          step();
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pr = lane + 32 * h, i2 = 2 * pr;
+            v[u][h] = make_double2(0.0, 0.0);
+            if (pr < P2) {
+              if (src.from_a(i2)) {
+                v[u][h] = *reinterpret_cast<const double2*>(src.a + i2);
+              } else if (src.from_c(i2)) {
+                const double2 w = *reinterpret_cast<const double2*>(src.c + i2);
+                v[u][h] = make_double2(sc * w.x, sc * w.y);
+              }
+            }
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kEmbedU; ++u) {
+          if (r + u >= rd_end) break;
+          double2* o = reinterpret_cast<double2*>(e.out + (r + u - base) * D2);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int pr = lane + 32 * h;
+            if (pr < P2) o[pr] = v[u][h];
+          }
+          if (P2 > 64) {  // rows longer than 128 values
+            int q0 = s0, q1 = s1 + u;
+            while (q1 >= e.D1) {
+              q1 -= e.D1;
+              ++q0;
+            }
+            const RowSrc src = row_src(e, q0, q1);
+            for (int pr = lane + 64; pr < P2; pr += 32) {
+              const int i2 = 2 * pr;
+              double2 w = make_double2(0.0, 0.0);
+              if (src.from_a(i2)) {
+                w = *reinterpret_cast<const double2*>(src.a + i2);
+              } else if (src.from_c(i2)) {
+                w = *reinterpret_cast<const double2*>(src.c + i2);
+                w.x *= sc;
+                w.y *= sc;
+              }
+              o[pr] = w;
+            }
+          }
+        }
+      }
+    } else {
+      for (; r < rd_end; ++r, step()) {
+        const RowSrc sr = row_src(e, i0, i1);
+        double* o = e.out + (r - base) * D2;
+        for (int i2 = lane; i2 < D2; i2 += 32)
+          o[i2] = sr.from_a(i2) ? sr.a[i2] : (sr.from_c(i2) ? e.alpha_c * sr.c[i2] : 0.0);
+      }
     }
-    for (int i2 = lane; i2 < e.D2; i2 += 32) {
-      double v = 0.0;
-      const int j2 = i2 - e.o2;
-      if (ina && i2 < e.a2) v = arow[i2];
-      else if (inc && j2 >= 0 && j2 < e.c2) v = e.alpha_c * crow[j2];
-      o[i2] = v;
-    }
+    r = rd_end;  // (the four-row steps may overshoot the descriptor's last row)
+    ++di;
   }
 }
 
@@ -138,21 +221,24 @@ int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream) {
   while (i < descs.size()) {
     EmbedBatch b;
     b.count = 0;
-    int blocks = 0;
+    b.row_begin[0] = 0;
     double bytes = 0.0;
     while (i < descs.size() && b.count < MAXD) {
       const EmbedDesc& d = descs[i++];
-      const long long total = (long long)d.D0 * d.D1 * d.D2;
-      if (total == 0) continue;
-      b.begin[b.count] = blocks;
-      blocks += (int)std::max<long long>(1, std::min<long long>(ceil_div((long long)d.D0 * d.D1, 8), 2048));
-      bytes += 8.0 * ((double)total + (double)d.a0 * d.a1 * d.a2 + (double)d.c0 * d.c1 * d.c2);
+      const long long rows = (long long)d.D0 * d.D1;
+      if (rows * d.D2 == 0) continue;
+      b.vec[b.count] = !((d.D2 | d.a2 | d.c2 | d.o2) & 1) &&
+                       !((((uintptr_t)d.out) | ((uintptr_t)d.A) | ((uintptr_t)d.C)) & 15);
+      b.row_begin[b.count + 1] = b.row_begin[b.count] + rows;
+      bytes += 8.0 * ((double)rows * d.D2 + (double)d.a0 * d.a1 * d.a2 + (double)d.c0 * d.c1 * d.c2);
       b.d[b.count++] = d;
     }
     if (!b.count) continue;
-    b.begin[b.count] = blocks;
+    // enough warps to keep ~8 loads per lane in flight on every SM, not more than rows / 4
+    const long long rows = b.row_begin[b.count];
+    const int blocks = (int)std::max<long long>(1, std::min<long long>(148LL * 8, ceil_div(rows, 4 * 8)));
     ProfToken tok = prof_begin(stream);
-    embed_kernel<<<blocks, 256, 0, stream>>>(b);
+    embed_kernel<<<blocks, kEmbedThreads, 0, stream>>>(b);
     HT_LAUNCH_CHECK();
     prof_end(tok, "embed", stream, 0.0, bytes);
   }

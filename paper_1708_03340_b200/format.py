@@ -279,6 +279,12 @@ class HTensor:
         host.copy_(flat, non_blocking=True)
         return host
 
+    def arena_numel(self) -> int:
+        """Number of float64 values of the tensor (all node arrays)."""
+        if self._arena is not None:
+            return int(self._arena.numel())
+        return sum(int(self._nodes[t].numel()) for t in range(len(self.tree.nodes)))
+
     def host_layout(self):
         """(sizes_by_node, ranks) needed to rebuild this tensor from a host arena."""
         return ({leaf.index: int(self._shape(leaf.index)[0]) for leaf in self.tree.leaves},
