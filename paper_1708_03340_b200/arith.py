@@ -91,7 +91,11 @@ def _ws(nbytes: int, dev) -> torch.Tensor:
 
 
 def _sizes_by_node(x: HTensor) -> dict:
-    return {leaf.index: int(x.node_array(leaf.index).shape[0]) for leaf in x.tree.leaves}
+    sz = x.__dict__.get("_sizes_cached")
+    if sz is None:
+        sz = {leaf.index: int(x.node_array(leaf.index).shape[0]) for leaf in x.tree.leaves}
+        x._sizes_cached = sz
+    return dict(sz)
 
 
 def _check_compatible(a: HTensor, c: HTensor) -> None:
@@ -125,8 +129,9 @@ def subtract(a: HTensor, c: HTensor) -> HTensor:
 
 
 def _check_out(out: HTensor, tree, sizes: dict, ranks: dict) -> None:
+    rl = out._rank_list()
     if out.tree.d != tree.d or _sizes_by_node(out) != sizes or \
-            any(out.rank(t) != ranks[t] for t in range(1, len(tree.nodes))):
+            any(rl[t] != ranks[t] for t in range(1, len(tree.nodes))):
         raise ValueError("out tensor has the wrong shapes for this result")
 
 
@@ -134,7 +139,8 @@ def _add(a: HTensor, c: HTensor, alpha_c: float, out: HTensor | None = None) -> 
     _check_compatible(a, c)
     lib = _lib.load()
     tree = a.tree
-    ranks = {t: a.rank(t) + c.rank(t) for t in range(1, len(tree.nodes))}
+    ra, rc = a._rank_list(), c._rank_list()
+    ranks = {t: ra[t] + rc[t] for t in range(1, len(tree.nodes))}
     if out is None:
         out = HTensor.empty(tree, _sizes_by_node(a), ranks, device=a.device)
     else:

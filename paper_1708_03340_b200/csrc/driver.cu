@@ -1269,6 +1269,7 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
   for (int l = T.depth; l >= 1; --l) {
     ar.off = base;
     std::vector<GemmDesc> gl, g1, g2, g3;
+    std::vector<SsDesc> s1v, s2v;
     std::vector<ReduceDesc> rs;
     long long tiles = 0;
     for (int t : T.levels[l])
@@ -1295,14 +1296,27 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
       const long long ja = a.k[s1], la = a.k[s2], jc = c.k[s1], lc = c.k[s2];
       double* S1 = S1s[t];
       double* S2 = S2s[t];
-      // s1[i,l,j'] = sum_j B_a[i,j,l] Phi1[j,j']   (arith.py:116)
-      GemmDesc x1 = gemm_desc(a.p[t], 1, la, phi[s1], jc, 1, S1, jc, 1, (int)la, (int)jc, (int)ja);
-      x1.nb1 = (int)ka; x1.a_b1 = ja * la; x1.b_b1 = 0; x1.c_b1 = la * jc;
-      g1.push_back(x1);
-      // s2[i,j',l'] = sum_l s1[i,l,j'] Phi2[l,l']   (arith.py:117)
-      GemmDesc x2 = gemm_desc(S1, 1, jc, phi[s2], lc, 1, S2, lc, 1, (int)jc, (int)lc, (int)la);
-      x2.nb1 = (int)ka; x2.a_b1 = la * jc; x2.b_b1 = 0; x2.c_b1 = jc * lc;
-      g2.push_back(x2);
+      // s1[i,l,j'] = sum_j B_a[i,j,l] Phi1[j,j']   (arith.py:116): streamed over the rows
+      // (i, l) of B_a with Phi1 resident (one job per node)
+      if (ss_fits(jc, ja)) {
+        SsDesc d = ss_desc(a.p[t], 1, la, phi[s1], jc, 1, S1, jc, 1, (int)(ka * la), (int)jc, (int)ja);
+        d.M_lo = (int)la; d.x_hi = ja * la; d.c_hi = la * jc;
+        s1v.push_back(d);
+      } else {
+        GemmDesc x1 = gemm_desc(a.p[t], 1, la, phi[s1], jc, 1, S1, jc, 1, (int)la, (int)jc, (int)ja);
+        x1.nb1 = (int)ka; x1.a_b1 = ja * la; x1.b_b1 = 0; x1.c_b1 = la * jc;
+        g1.push_back(x1);
+      }
+      // s2[i,j',l'] = sum_l s1[i,l,j'] Phi2[l,l']   (arith.py:117): rows (i, j') of s1
+      if (ss_fits(lc, la)) {
+        SsDesc d = ss_desc(S1, 1, jc, phi[s2], lc, 1, S2, lc, 1, (int)(ka * jc), (int)lc, (int)la);
+        d.M_lo = (int)jc; d.x_hi = la * jc; d.c_hi = jc * lc;
+        s2v.push_back(d);
+      } else {
+        GemmDesc x2 = gemm_desc(S1, 1, jc, phi[s2], lc, 1, S2, lc, 1, (int)jc, (int)lc, (int)la);
+        x2.nb1 = (int)ka; x2.a_b1 = la * jc; x2.b_b1 = 0; x2.c_b1 = jc * lc;
+        g2.push_back(x2);
+      }
       // Phi_t[i,i'] = sum_{j',l'} s2[i,j',l'] B_c[i',j',l']   (arith.py:118)
       const int S = pick_splits(tiles, jc * lc);
       double* Pp = ar.take(S * ka * kc);
@@ -1315,10 +1329,14 @@ int run_inner_product(const View& a, const View& c, Arena& ar, double* result, c
     if (exec) {
       merge_gemms(g1);
       merge_gemms(g2);
-      HT_TRY(gemm_grouped(gl, s));
-      HT_TRY(gemm_grouped(g1, s));
-      HT_TRY(gemm_grouped(g2, s));
-      HT_TRY(gemm_grouped(g3, s));
+      merge_ss(s1v);
+      merge_ss(s2v);
+      HT_TRY(gemm_grouped(gl, s, "gemm_phi_leaf"));
+      HT_TRY(gemm_grouped(g1, s, "gemm_phi"));
+      HT_TRY(ss_gemm(s1v, s, "ss_phi"));
+      HT_TRY(gemm_grouped(g2, s, "gemm_phi"));
+      HT_TRY(ss_gemm(s2v, s, "ss_phi"));
+      HT_TRY(gemm_grouped(g3, s, "gemm_phi"));
       HT_TRY(reduce_partials(rs, s));
     }
   }

@@ -168,13 +168,25 @@ class HTensor:
         n = self._nodes
         return n.shapes[t] if isinstance(n, _ArenaViews) else tuple(n[t].shape)
 
+    def _rank_list(self) -> list:
+        """Ranks by node id, computed once (node shapes never change: HTensors are
+        immutable by convention, format.py:19)."""
+        rl = self.__dict__.get("_ranks_cached")
+        if rl is None:
+            rl = []
+            for t in range(len(self.tree.nodes)):
+                node = self.tree.node(t)
+                if node.is_root:
+                    rl.append(1)
+                elif node.is_leaf:
+                    rl.append(int(self._shape(t)[1]))
+                else:
+                    rl.append(int(self._shape(t)[0]))
+            self._ranks_cached = rl
+        return rl
+
     def rank(self, node_id: int) -> int:
-        node = self.tree.node(node_id)
-        if node.is_root:
-            return 1
-        if node.is_leaf:
-            return int(self._shape(node_id)[1])
-        return int(self._shape(node_id)[0])
+        return self._rank_list()[node_id]
 
     @property
     def ranks(self) -> dict:
@@ -186,7 +198,11 @@ class HTensor:
 
     @property
     def shape(self) -> tuple:
-        return tuple(int(self._shape(self.tree.leaf_for_dim(mu).index)[0]) for mu in range(1, self.tree.d + 1))
+        sh = self.__dict__.get("_shape_cached")
+        if sh is None:
+            sh = tuple(int(self._shape(self.tree.leaf_for_dim(mu).index)[0]) for mu in range(1, self.tree.d + 1))
+            self._shape_cached = sh
+        return sh
 
     @property
     def device(self) -> torch.device:
