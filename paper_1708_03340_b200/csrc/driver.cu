@@ -1110,8 +1110,10 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
   }
   HT_TRY(eig_batched(eps, s));
   if (sticky) {
+    ProfToken tok = prof_begin(s);
     sticky_or_kernel<<<1, 1, 0, s>>>(P.status);
     HT_LAUNCH_CHECK();
+    prof_end(tok, "sticky_status", s, 0.0, 0.0);
   }
   return kOk;
 }

@@ -342,8 +342,10 @@ __global__ void identity_kernel(double* p, long long node_stride, int K, const i
 
 int identity_batched(double* p, long long node_stride, int K, int nodes, const int* active, cudaStream_t stream) {
   if (nodes <= 0 || K <= 0) return kOk;
+  ProfToken tok = prof_begin(stream);
   identity_kernel<<<dim3((K * K + 255) / 256, nodes), 256, 0, stream>>>(p, node_stride, K, active);
   HT_LAUNCH_CHECK();
+  prof_end(tok, "identity", stream, 0.0, 0.0);
   return kOk;
 }
 
