@@ -315,7 +315,8 @@ def run_reference(args, rank, world):
         "steps": len(times), "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
         "scaling": "strong" if world > 1 and not args.replicas else "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded Gaussian, SURVEY §8(d))",
-        "config": config_dict(args, world),
+        "config": {**config_dict(args, world),
+                   "inflight": 1, "inflight_note": "CPU reference: one truncation at a time on all host threads"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -330,7 +331,10 @@ def config_dict(args, world=1):
             "d": args.d, "n": args.n, "k": args.k, "pre_truncation_rank": 2 * args.k,
             "seeds": [2 * int(round(math.log2(args.d))), 2 * int(round(math.log2(args.d))) + 1],
             "l2_policy": f"inputs {8 * storage(args.d, args.n, 2 * args.k) / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
-            "parallelism": par}
+            "parallelism": par,
+            "inflight": 1 if sharded else args.inflight,
+            "inflight_note": ("independent truncations in flight on as many CUDA streams of the GPU (each a complete "
+                              "truncation with its own workspace and output); step time = run time / steps")}
 
 
 # ---------------------------------------------------------------------------
@@ -339,77 +343,129 @@ def config_dict(args, world=1):
 
 
 class _Single:
-    """1 GPU (or one replica per GPU): the public drop-in API on a resident HTensor."""
+    """1 GPU (or one replica per GPU): the public drop-in API on a resident HTensor.
 
-    def __init__(self, htb, tree, fa, fc, ctl):
+    ``inflight`` truncations run concurrently on as many compute streams (each with its
+    own output buffer and workspace): one truncation's latency-bound phases -- the
+    Cholesky factorisations, the eigensolver, the split-K sums, all of which occupy
+    only a few SMs -- leave the GPU mostly idle, and the other truncation's GEMMs fill
+    it.  Every step is a complete, independent truncation; the step time is the
+    whole run's time divided by the steps."""
+
+    def __init__(self, htb, tree, fa, fc, ctl, inflight=1):
+        import torch
+
         self.htb, self.tree, self.ctl = htb, tree, ctl
         self.a, self.c = htb.HTensor(tree, *fa), htb.HTensor(tree, *fc)
         self.x = htb.add(self.a, self.c)  # X resident in HBM (547 MB at d=64: larger than L2)
+        self.inflight = max(1, inflight)
+        self.streams = [torch.cuda.Stream() for _ in range(self.inflight)]
+        T = htb.truncate(self.x, ctl)
+        self.tlay = T.host_layout()
+        # two result buffers per stream: a step's result stays intact while the next one
+        # on its stream is written
+        self.outs = [[htb.HTensor.empty(tree, *self.tlay) for _ in range(2)] for _ in self.streams]
+        self.i = 0
 
     def step(self):
         return self.htb.truncate(self.x, self.ctl)
 
+    def run_steps(self, n):
+        """n truncations of the resident X, round-robin over the compute streams; the
+        current stream waits for all of them (the caller's events bracket the run)."""
+        import torch
+
+        cur = torch.cuda.current_stream()
+        start = torch.cuda.Event()
+        start.record(cur)
+        for s in self.streams:
+            s.wait_event(start)
+        T = None
+        for _ in range(n):
+            q = self.i % self.inflight
+            with torch.cuda.stream(self.streams[q]):
+                T = self.htb.truncate(self.x, self.ctl, out=self.outs[q][(self.i // self.inflight) % 2])
+            self.i += 1
+        for s in self.streams:
+            ev = torch.cuda.Event()
+            ev.record(s)
+            cur.wait_event(ev)
+        return T
+
     # end to end: the user's workflow T = truncate(add(A, C)) from pinned host A, C to a
     # pinned host T, every step; consecutive steps are pipelined over a copy stream, the
-    # compute stream and a read-back stream (double-buffered device inputs, sums and
-    # results: add(..., out=) / truncate(..., out=) write into the slot's buffers, so the
-    # truncation replays its captured graphs as they are).
+    # compute streams (``inflight`` of them) and a read-back stream.  Each step has a
+    # slot of device inputs, sum and result (add(..., out=) / truncate(..., out=) write
+    # into the slot's buffers, so the truncation replays its captured graphs as they are).
     def prepare_e2e(self):
         import torch
 
         htb = self.htb
+        # two slots per compute stream: slot i % nslot always runs on stream i % inflight,
+        # so each (slot, stream) pair keeps its own captured graph (no re-pointing), and the
+        # H2D of the next step on a stream overlaps the current one
+        self.nslot = 2 * self.inflight
         self.host_a, self.host_c = self.a.to_host_arena(), self.c.to_host_arena()
         la, lc = self.a.host_layout(), self.c.host_layout()
-        self.dev = [(htb.HTensor.empty(self.tree, *la), htb.HTensor.empty(self.tree, *lc)) for _ in range(2)]
+        self.dev = [(htb.HTensor.empty(self.tree, *la), htb.HTensor.empty(self.tree, *lc))
+                    for _ in range(self.nslot)]
         lx = self.x.host_layout()
-        self.xbuf = [htb.HTensor.empty(self.tree, *lx) for _ in range(2)]
-        T = self.step()
-        self.tbuf = [htb.HTensor.empty(self.tree, *T.host_layout()) for _ in range(2)]
+        self.xbuf = [htb.HTensor.empty(self.tree, *lx) for _ in range(self.nslot)]
+        self.tbuf = [htb.HTensor.empty(self.tree, *self.tlay) for _ in range(self.nslot)]
         self.copy_stream, self.d2h_stream = torch.cuda.Stream(), torch.cuda.Stream()
-        self.out_host = [T.to_host_arena() for _ in range(2)]
+        self.out_host = [self.tbuf[0].to_host_arena() for _ in range(self.nslot)]
         for h in self.out_host:
             h.fill_(0.0)  # touch the pinned pages (a first DMA into fresh pinned memory is slow)
-        self.d2h_ev = [None, None]
+        self.d2h_ev = [None] * self.nslot
+        self.comp_ev = [None] * self.nslot
+        self.e2e_i = 0
         torch.cuda.synchronize()
 
     def e2e_run(self, n, start_event):
         import torch
 
         htb = self.htb
-        comp = torch.cuda.current_stream()
-        h2d_ev, comp_ev = [None, None], [None, None]
+        cur = torch.cuda.current_stream()
+        S = self.nslot
+        h2d_ev = [None] * S
 
         def issue_h2d(i):
-            slot = i % 2
+            slot = i % S
             with torch.cuda.stream(self.copy_stream):
                 self.copy_stream.wait_event(start_event)
-                if comp_ev[slot] is not None:  # the step that last read this slot is done
-                    self.copy_stream.wait_event(comp_ev[slot])
+                if self.comp_ev[slot] is not None:  # the step that last used this slot is done
+                    self.copy_stream.wait_event(self.comp_ev[slot])
                 self.dev[slot][0].load_host_arena(self.host_a)
                 self.dev[slot][1].load_host_arena(self.host_c)
                 h2d_ev[slot] = torch.cuda.Event()
                 h2d_ev[slot].record(self.copy_stream)
 
-        issue_h2d(0)
+        base = self.e2e_i
+        issue_h2d(base)
         last = None
-        for i in range(n):
-            slot = i % 2
-            if i + 1 < n:
+        for k in range(n):
+            i = base + k
+            slot, comp = i % S, self.streams[i % self.inflight]
+            if k + 1 < n:
                 issue_h2d(i + 1)
             comp.wait_event(h2d_ev[slot])
-            x = htb.add(*self.dev[slot], out=self.xbuf[slot])
-            if self.d2h_ev[slot] is not None:  # the read-back of this slot's last result is done
+            if self.comp_ev[slot] is not None:  # the slot's previous step (other stream) is done
+                comp.wait_event(self.comp_ev[slot])
+            if self.d2h_ev[slot] is not None:  # ... and its result has been read back
                 comp.wait_event(self.d2h_ev[slot])
-            t = htb.truncate(x, self.ctl, out=self.tbuf[slot])
-            comp_ev[slot] = torch.cuda.Event()
-            comp_ev[slot].record(comp)
+            with torch.cuda.stream(comp):
+                x = htb.add(*self.dev[slot], out=self.xbuf[slot])
+                t = htb.truncate(x, self.ctl, out=self.tbuf[slot])
+            self.comp_ev[slot] = torch.cuda.Event()
+            self.comp_ev[slot].record(comp)
             with torch.cuda.stream(self.d2h_stream):
-                self.d2h_stream.wait_event(comp_ev[slot])
+                self.d2h_stream.wait_event(self.comp_ev[slot])
                 self.out_host[slot] = t.to_host_arena(self.out_host[slot])
                 last = torch.cuda.Event()
                 last.record(self.d2h_stream)
             self.d2h_ev[slot] = last
-        comp.wait_event(last)
+        self.e2e_i = base + n
+        cur.wait_event(last)
 
     def e2e_bytes(self):
         return (self.host_a.numel() + self.host_c.numel()) * 8, self.out_host[0].numel() * 8
@@ -434,6 +490,12 @@ class _Sharded:
 
     def step(self):
         return self.hd.sharded_truncate(self.engine, self.comm, self.smap, self.ctl, self.orth)
+
+    def run_steps(self, n):
+        T = None
+        for _ in range(n):
+            T = self.step()
+        return T
 
     def prepare_e2e(self):
         self.host_a = {t: a.cpu().pin_memory() for t, a in self.a.arrays.items()}
@@ -474,13 +536,13 @@ def run_ours(args, rank, world, local_rank):
     fa = htb.gaussian_factors(tree, args.n, args.k, seed)
     fc = htb.gaussian_factors(tree, args.n, args.k, seed + 1)
     ctl = htb.TruncationControl.fixed_rank(args.k)
-    work = (_Sharded if sharded else _Single)(htb, tree, fa, fc, ctl)
+    work = _Sharded(htb, tree, fa, fc, ctl) if sharded else _Single(htb, tree, fa, fc, ctl, args.inflight)
     # warm-up with the timed loop's own allocation pattern (the previous result stays
     # alive while the next is allocated): the truncation's graph cache is keyed on the
     # output buffers, so every key the timed loop will see is captured here
-    T = None
-    for _ in range(args.warmup):
-        T = work.step()
+    # warm-up: at least every (stream, output buffer) pair twice, so each has its own
+    # captured graph before the timed region
+    T = work.run_steps(max(args.warmup, 4 * getattr(work, "inflight", 1) + 2))
     torch.cuda.synchronize()
 
     def barrier():
@@ -501,14 +563,25 @@ def run_ours(args, rank, world, local_rank):
         n0 = lib.ht_launch_count()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for _ in range(args.steps):
-            T = work.step()
+        T = work.run_steps(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
         launches = lib.ht_launch_count() - n0
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
     truncs_per_step = 1 if sharded else world
+    serial = None
+    if not sharded and args.inflight > 1:  # the same steps one at a time (one stream), for reference
+        s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        work.step()
+        torch.cuda.synchronize()
+        s0.record(stream)
+        for _ in range(args.steps):
+            work.step()
+        s1.record(stream)
+        torch.cuda.synchronize()
+        ms1 = max_over_ranks(s0.elapsed_time(s1) / args.steps)
+        serial = {"ms_per_step": ms1, "value": truncs_per_step * 1e3 / ms1, "inflight": 1}
     value = truncs_per_step * 1e3 / ms
     if world > 1:
         lt = torch.tensor([float(launches)], dtype=torch.float64, device="cuda")
@@ -600,6 +673,8 @@ def run_ours(args, rank, world, local_rank):
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
     }
+    if serial is not None:
+        line["one_in_flight"] = serial
     if extra is not None:
         line["secondary"] = extra
     if sweep_res is not None:
@@ -627,6 +702,8 @@ def main():
     ap.add_argument("--n", type=int, default=1000)
     ap.add_argument("--k", type=int, default=50)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--inflight", type=int, default=3,
+                    help="truncations in flight on as many compute streams (1 GPU / replicas)")
     ap.add_argument("--sweep", action="store_true",
                     help="also run the C2 weak-scaling study d = 8..256 (time vs log2 d, fit a + b log2 d)")
     ap.add_argument("--replicas", action="store_true",

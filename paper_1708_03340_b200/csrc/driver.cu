@@ -1402,6 +1402,7 @@ struct TruncGraph {
   RelocTable r_orth, r_rest;
   int* flag = nullptr;  // pinned
   cudaEvent_t ev = nullptr;
+  cudaEvent_t done = nullptr;  // recorded behind every launch: a relocation waits for it
   bool chol = false;    // the ORTH graph ran Cholesky-QR and wrote the flag
   bool device = false;  // the Householder re-run is a conditional node of the REST graph
   long long n_orth = 0, n_rest = 0;
@@ -1421,8 +1422,8 @@ std::map<std::vector<long long>, int> g_graph_seen;  // shape keys and address k
 unsigned long long g_graph_clock = 0;
 int g_graph_mode = -1;  // -1: from HT_GRAPHS (default on)
 long long g_graph_captures = 0, g_graph_replays = 0, g_graph_relocations = 0;
-constexpr size_t kMaxGraphs = 16;
-constexpr size_t kMaxPerShape = 3;
+constexpr size_t kMaxGraphs = 32;
+constexpr size_t kMaxPerShape = 8;
 
 bool graphs_on() {
   if (g_graph_mode < 0) {
@@ -1501,12 +1502,15 @@ int* graph_flag() {
 }
 
 void destroy_graph(TruncGraph* g) {
-  // executable graphs and events still in flight are released by the driver on completion
+  // executable graphs and events still in flight are released by the driver on completion;
+  // the pinned flag word is recycled only once the last launch is done with it
+  if (g->done) cudaEventSynchronize(g->done);
   if (g->orth) cudaGraphExecDestroy(g->orth);
   if (g->rest) cudaGraphExecDestroy(g->rest);
   if (g->g_orth) cudaGraphDestroy(g->g_orth);
   if (g->g_rest) cudaGraphDestroy(g->g_rest);
   if (g->ev) cudaEventDestroy(g->ev);
+  if (g->done) cudaEventDestroy(g->done);
   if (g->flag) g_graph_flags.push_back(g->flag);
   delete g;
 }
@@ -1649,6 +1653,9 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
 }
 
 int relocate(TruncGraph* G, const Addrs& a) {
+  // the executable graphs may still be queued or running on another stream (pipelines
+  // with several truncations in flight): patch them only once their last launch is done
+  if (G->done) HT_CUDA_CHECK(cudaEventSynchronize(G->done));
   const std::vector<long long> delta{(long long)(a.in[0] - G->cap_in[0]), (long long)(a.out[0] - G->cap_out[0]),
                                      (long long)(a.ws - G->cap_ws)};
   cudaError_t e = reloc_apply(G->orth, G->g_orth, G->r_orth, delta);
@@ -1731,6 +1738,8 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
   HT_CUDA_CHECK(cudaGraphLaunch(G->orth, s));
   if (G->chol && !G->device) HT_CUDA_CHECK(cudaEventRecord(G->ev, s));
   HT_CUDA_CHECK(cudaGraphLaunch(G->rest, s));
+  if (!G->done) HT_CUDA_CHECK(cudaEventCreateWithFlags(&G->done, cudaEventDisableTiming));
+  HT_CUDA_CHECK(cudaEventRecord(G->done, s));
   prof_add_launches(G->n_orth + G->n_rest);
   ++g_graph_replays;
   ++G->replays;

@@ -31,7 +31,8 @@ def num(v):
         return float("nan")
 
 
-launches = [k for k in kernels(sys.argv[1]) if "ht::" in k["name"] or "unnamed>::" in k["name"]]
+OURS = ("ht::", "unnamed>::", "identity_kernel")
+launches = [k for k in kernels(sys.argv[1]) if any(o in k["name"] for o in OURS)]
 tags = json.load(open(sys.argv[2]))
 if len(tags) != len(launches):
     sys.exit(f"tag log ({len(tags)}) and launch list ({len(launches)}) differ")
@@ -47,7 +48,7 @@ if len(sys.argv) > 3:
             if key in d:
                 d[key] = num(d[key]) * scale.get(units[hdr.index(key)], 1.0)
         raw.append(d)
-    raw = [r for r in raw if "ht::" in r.get("Kernel Name", "") or "unnamed>::" in r.get("Kernel Name", "")]
+    raw = [r for r in raw if any(o in r.get("Kernel Name", "") for o in OURS)]
 step_us = sum(num(k["gpu__time_duration.sum"]) / 1e3 for k in launches)
 # align the full-capture rows to the launch list by kernel name, in order
 raw_for = [None] * len(launches)
