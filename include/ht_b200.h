@@ -283,7 +283,8 @@ int ht_set_eig_mode(int mode);
 int64_t ht_launch_count(void);
 /* Bit 0: record a CUDA event pair on the launching stream around every kernel
  * launch and attribute algorithmic flops/bytes per kernel; bit 1: keep a
- * launch-order log of kernel tags (no events; for matching ncu launch lists).
+ * launch-order log of kernel tags (no events; for matching ncu launch lists);
+ * bit 2 (with bit 0): one report entry per launch, keyed "tag#seq".
  * Clears the tally and the log. */
 int ht_profile_enable(int on);
 /* The launch-order log as JSON [["tag", flops, bytes], ...]; returns its length. */

@@ -1,4 +1,5 @@
 #include <algorithm>
+#include <type_traits>
 
 #include "misc.cuh"
 #include "prof.cuh"
@@ -9,11 +10,19 @@ namespace {
 
 constexpr int MAXD = 64;
 
+constexpr int kEmbedMaxD = 128;
+
+// Unsigned division by a per-descriptor constant (n < 2^31): q = (umulhi(n, m) + n) >> s.
+struct FastDiv {
+  unsigned m, s, d;
+};
+
 struct EmbedBatch {
   int count;
-  long long row_begin[MAXD + 1];  // prefix sums of the descriptors' output rows
-  unsigned char vec[MAXD];        // even extents / offsets, 16-byte aligned: pair copies
-  EmbedDesc d[MAXD];
+  int begin[kEmbedMaxD + 1];  // prefix sums of the descriptors' CTA counts
+  FastDiv row[kEmbedMaxD];    // units per output row (D2 / W)
+  FastDiv d1[kEmbedMaxD];     // D1
+  EmbedDesc d[kEmbedMaxD];
 };
 
 struct KronBatch {
@@ -35,127 +44,61 @@ __device__ __forceinline__ int find(const B& b) {
   return di;
 }
 
-// Block embedding of add.  Output rows (i0, i1) of D2 values, all descriptors' rows in
-// one global row space; each warp owns a contiguous run of rows (descriptor lookup once
-// per run) and works on four rows at a time: every lane issues the loads of all four
-// rows (A or scaled C segments; pure-zero rows -- half of every inner node -- load
-// nothing) before any store, so ~8 16-byte loads per lane are in flight.
+// Block embedding of add (arith.py:173-192).  The output of a node is one flat run of
+// W-double units (W = 2: 16-byte pairs when every extent / offset is even and the bases
+// are 16-byte aligned; W = 1 otherwise); each CTA owns a contiguous chunk of one
+// descriptor's units and every thread issues the loads of kEmbedU units (A or scaled C
+// segment, nothing for the structural zeros -- three quarters of an inner node) before
+// any store, so stores are fully coalesced and ~kEmbedU loads per thread are in flight.
 constexpr int kEmbedThreads = 256;
-constexpr int kEmbedU = 4;  // rows per warp step
+constexpr int kEmbedU = 8;  // units per thread per CTA chunk
+constexpr int kEmbedChunk = kEmbedThreads * kEmbedU;
 
-struct RowSrc {
-  const double* a;  // A row segment -> output [0, ahi), or null
-  const double* c;  // C row segment (indexed from clo) -> output [clo, chi), or null
-  int ahi, clo, chi;
-  // value pair (i2, i2 + 1) of the output row: exactly one source or zero
-  __device__ __forceinline__ bool from_a(int i2) const { return a && i2 < ahi; }
-  __device__ __forceinline__ bool from_c(int i2) const { return c && i2 >= clo && i2 < chi; }
-};
-
-// (a leaf row has both: U = [U_a, U_c]; an inner row at most one block)
-__device__ __forceinline__ RowSrc row_src(const EmbedDesc& e, int i0, int i1) {
-  RowSrc s{nullptr, nullptr, 0, 0, 0};
-  if (i0 < e.a0 && i1 < e.a1) {
-    s.a = e.A + ((long long)i0 * e.a1 + i1) * e.a2;
-    s.ahi = e.a2;
-  }
-  const int j0 = i0 - e.o0, j1 = i1 - e.o1;
-  if (j0 >= 0 && j1 >= 0 && j0 < e.c0 && j1 < e.c1) {
-    s.c = e.C + ((long long)j0 * e.c1 + j1) * e.c2 - e.o2;
-    s.clo = e.o2;
-    s.chi = e.o2 + e.c2;
-  }
-  return s;
+__device__ __forceinline__ unsigned fdiv(unsigned n, const FastDiv& f) {
+  return (__umulhi(n, f.m) + n) >> f.s;
 }
 
-__global__ void __launch_bounds__(kEmbedThreads, 4) embed_kernel(const __grid_constant__ EmbedBatch b) {
-  const int lane = threadIdx.x & 31;
-  const long long gw = (long long)blockIdx.x * (kEmbedThreads / 32) + (threadIdx.x >> 5);
-  const long long nwarps = (long long)gridDim.x * (kEmbedThreads / 32);
-  const long long total = b.row_begin[b.count];
-  long long r = total * gw / nwarps;
-  const long long r_end = total * (gw + 1) / nwarps;
-  int di = 0;
-  while (di + 1 < b.count && r >= b.row_begin[di + 1]) ++di;
-  while (r < r_end) {
-    const EmbedDesc& e = b.d[di];
-    const long long rd_end = min(r_end, b.row_begin[di + 1]);  // this descriptor's part of the run
-    const long long base = b.row_begin[di];
-    const bool vec = b.vec[di];
-    const int D2 = e.D2;
-    // (i0, i1) of the run's first row (one division per run), then stepped per row
-    int i0 = (int)((r - base) / e.D1), i1 = (int)((r - base) - (long long)i0 * e.D1);
-    auto step = [&]() {
-      if (++i1 == e.D1) {
-        i1 = 0;
-        ++i0;
-      }
-    };
-    if (vec) {
-      const int P2 = D2 >> 1;  // 16-byte pairs per row
-      for (; r < rd_end; r += kEmbedU) {
-        double2 v[kEmbedU][2];  // only the loaded pairs stay live into the store phase
-        const double sc = e.alpha_c;
-        const int s0 = i0, s1 = i1;  // first row of this step (the long-row path restarts from it)
+template <int W>
+__global__ void __launch_bounds__(kEmbedThreads) embed_kernel(const __grid_constant__ EmbedBatch b) {
+  using V = typename std::conditional<W == 2, double2, double>::type;
+  int lo = 0, hi = b.count - 1;  // descriptor of this CTA: begin[lo] <= blockIdx.x < begin[lo + 1]
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if ((int)blockIdx.x >= b.begin[mid]) lo = mid;
+    else hi = mid - 1;
+  }
+  const EmbedDesc& e = b.d[lo];
+  const FastDiv fr = b.row[lo], f1 = b.d1[lo];
+  const unsigned units = (unsigned)(((long long)e.D0 * e.D1 * e.D2) / W);
+  const unsigned u0 = (unsigned)(blockIdx.x - b.begin[lo]) * kEmbedChunk + threadIdx.x;
+  const double sc = e.alpha_c;
+  V v[kEmbedU];
 #pragma unroll
-        for (int u = 0; u < kEmbedU; ++u) {
-          const RowSrc src = r + u < rd_end ? row_src(e, i0, i1) : RowSrc{nullptr, nullptr, 0, 0, 0};
-          step();
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int pr = lane + 32 * h, i2 = 2 * pr;
-            v[u][h] = make_double2(0.0, 0.0);
-            if (pr < P2) {
-              if (src.from_a(i2)) {
-                v[u][h] = *reinterpret_cast<const double2*>(src.a + i2);
-              } else if (src.from_c(i2)) {
-                const double2 w = *reinterpret_cast<const double2*>(src.c + i2);
-                v[u][h] = make_double2(sc * w.x, sc * w.y);
-              }
-            }
-          }
+  for (int k = 0; k < kEmbedU; ++k) {
+    const unsigned u = u0 + k * kEmbedThreads;
+    if constexpr (W == 2) v[k] = make_double2(0.0, 0.0);
+    else v[k] = 0.0;
+    if (u < units) {
+      const unsigned row = fdiv(u, fr);
+      const int i2 = (int)(u - row * fr.d) * W;
+      const int i0 = (int)fdiv(row, f1), i1 = (int)(row - (unsigned)i0 * f1.d);
+      if (i0 < e.a0 && i1 < e.a1 && i2 < e.a2) {
+        v[k] = *reinterpret_cast<const V*>(e.A + ((long long)i0 * e.a1 + i1) * e.a2 + i2);
+      } else {
+        const int j0 = i0 - e.o0, j1 = i1 - e.o1, j2 = i2 - e.o2;
+        if (j0 >= 0 && j1 >= 0 && j2 >= 0 && j0 < e.c0 && j1 < e.c1 && j2 < e.c2) {
+          const V w = *reinterpret_cast<const V*>(e.C + ((long long)j0 * e.c1 + j1) * e.c2 + j2);
+          if constexpr (W == 2) v[k] = make_double2(sc * w.x, sc * w.y);
+          else v[k] = sc * w;
         }
-#pragma unroll
-        for (int u = 0; u < kEmbedU; ++u) {
-          if (r + u >= rd_end) break;
-          double2* o = reinterpret_cast<double2*>(e.out + (r + u - base) * D2);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int pr = lane + 32 * h;
-            if (pr < P2) o[pr] = v[u][h];
-          }
-          if (P2 > 64) {  // rows longer than 128 values
-            int q0 = s0, q1 = s1 + u;
-            while (q1 >= e.D1) {
-              q1 -= e.D1;
-              ++q0;
-            }
-            const RowSrc src = row_src(e, q0, q1);
-            for (int pr = lane + 64; pr < P2; pr += 32) {
-              const int i2 = 2 * pr;
-              double2 w = make_double2(0.0, 0.0);
-              if (src.from_a(i2)) {
-                w = *reinterpret_cast<const double2*>(src.a + i2);
-              } else if (src.from_c(i2)) {
-                w = *reinterpret_cast<const double2*>(src.c + i2);
-                w.x *= sc;
-                w.y *= sc;
-              }
-              o[pr] = w;
-            }
-          }
-        }
-      }
-    } else {
-      for (; r < rd_end; ++r, step()) {
-        const RowSrc sr = row_src(e, i0, i1);
-        double* o = e.out + (r - base) * D2;
-        for (int i2 = lane; i2 < D2; i2 += 32)
-          o[i2] = sr.from_a(i2) ? sr.a[i2] : (sr.from_c(i2) ? e.alpha_c * sr.c[i2] : 0.0);
       }
     }
-    r = rd_end;  // (the four-row steps may overshoot the descriptor's last row)
-    ++di;
+  }
+  V* out = reinterpret_cast<V*>(e.out);
+#pragma unroll
+  for (int k = 0; k < kEmbedU; ++k) {
+    const unsigned u = u0 + k * kEmbedThreads;
+    if (u < units) __stcs(out + u, v[k]);
   }
 }
 
@@ -216,31 +159,51 @@ int blocks_for(long long total) { return (int)std::max<long long>(1, std::min<lo
 
 }  // namespace
 
+namespace {
+FastDiv make_fastdiv(unsigned d) {
+  FastDiv f;
+  f.d = d;
+  unsigned s = 0;
+  while ((1ull << s) < d) ++s;
+  f.s = s;
+  f.m = (unsigned)(((1ull << 32) * ((1ull << s) - d)) / d + 1);
+  return f;
+}
+}  // namespace
+
 int embed_batched(const std::vector<EmbedDesc>& descs, cudaStream_t stream) {
-  size_t i = 0;
-  while (i < descs.size()) {
-    EmbedBatch b;
-    b.count = 0;
-    b.row_begin[0] = 0;
-    double bytes = 0.0;
-    while (i < descs.size() && b.count < MAXD) {
-      const EmbedDesc& d = descs[i++];
-      const long long rows = (long long)d.D0 * d.D1;
-      if (rows * d.D2 == 0) continue;
-      b.vec[b.count] = !((d.D2 | d.a2 | d.c2 | d.o2) & 1) &&
-                       !((((uintptr_t)d.out) | ((uintptr_t)d.A) | ((uintptr_t)d.C)) & 15);
-      b.row_begin[b.count + 1] = b.row_begin[b.count] + rows;
-      bytes += 8.0 * ((double)rows * d.D2 + (double)d.a0 * d.a1 * d.a2 + (double)d.c0 * d.c1 * d.c2);
-      b.d[b.count++] = d;
+  // W = 2 launches for the 16-byte-pair descriptors, W = 1 for the rest
+  for (int W : {2, 1}) {
+    size_t i = 0;
+    while (i < descs.size()) {
+      EmbedBatch b;
+      b.count = 0;
+      b.begin[0] = 0;
+      double bytes = 0.0;
+      while (i < descs.size() && b.count < kEmbedMaxD) {
+        const EmbedDesc& d = descs[i++];
+        const long long n = (long long)d.D0 * d.D1 * d.D2;
+        if (n == 0) continue;
+        const bool vec = !((d.D2 | d.a2 | d.c2 | d.o2) & 1) &&
+                         !((((uintptr_t)d.out) | ((uintptr_t)d.A) | ((uintptr_t)d.C)) & 15);
+        if ((W == 2) != vec) continue;
+        if (n / W >= (1ll << 31)) {
+          set_error("add: node array too large for the embedding kernel");
+          return kErrShape;
+        }
+        b.row[b.count] = make_fastdiv((unsigned)(d.D2 / W));
+        b.d1[b.count] = make_fastdiv((unsigned)d.D1);
+        b.begin[b.count + 1] = b.begin[b.count] + ceil_div(n / W, kEmbedChunk);
+        bytes += 8.0 * ((double)n + (double)d.a0 * d.a1 * d.a2 + (double)d.c0 * d.c1 * d.c2);
+        b.d[b.count++] = d;
+      }
+      if (!b.count) continue;
+      ProfToken tok = prof_begin(stream);
+      if (W == 2) embed_kernel<2><<<b.begin[b.count], kEmbedThreads, 0, stream>>>(b);
+      else embed_kernel<1><<<b.begin[b.count], kEmbedThreads, 0, stream>>>(b);
+      HT_LAUNCH_CHECK();
+      prof_end(tok, "embed", stream, 0.0, bytes);
     }
-    if (!b.count) continue;
-    // enough warps to keep ~8 loads per lane in flight on every SM, not more than rows / 4
-    const long long rows = b.row_begin[b.count];
-    const int blocks = (int)std::max<long long>(1, std::min<long long>(148LL * 8, ceil_div(rows, 4 * 8)));
-    ProfToken tok = prof_begin(stream);
-    embed_kernel<<<blocks, kEmbedThreads, 0, stream>>>(b);
-    HT_LAUNCH_CHECK();
-    prof_end(tok, "embed", stream, 0.0, bytes);
   }
   return kOk;
 }

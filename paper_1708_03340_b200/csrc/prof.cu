@@ -30,6 +30,8 @@ std::vector<Pending> g_pending;
 std::vector<cudaEvent_t> g_pool;
 std::map<std::string, Entry> g_acc;
 bool g_log_on = false;
+bool g_per_launch = false;  // bit 2: one report entry per launch ("tag#seq")
+long long g_seq = 0;
 struct LogEntry {
   std::string name;
   double flops, bytes;
@@ -85,7 +87,13 @@ void prof_end(const ProfToken& tok, const char* name, cudaStream_t s, double flo
   std::lock_guard<std::mutex> g(g_mu);
   cudaEvent_t b = get_event();
   cudaEventRecord(b, s);
-  g_pending.push_back({name, tok.a, b, flops, bytes});
+  if (g_per_launch) {
+    char key[160];
+    snprintf(key, sizeof key, "%s#%03lld", name, g_seq++);
+    g_pending.push_back({key, tok.a, b, flops, bytes});
+  } else {
+    g_pending.push_back({name, tok.a, b, flops, bytes});
+  }
   if (g_pending.size() > 4096) drain_locked();
 }
 
@@ -111,6 +119,8 @@ int ht_profile_enable(int on) {
   ht::g_log.clear();
   ht::g_on = (on & 1) != 0;
   ht::g_log_on = (on & 2) != 0;
+  ht::g_per_launch = (on & 4) != 0;
+  ht::g_seq = 0;
   return 0;
 }
 
