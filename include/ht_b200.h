@@ -44,12 +44,20 @@ enum {
   HT_ERR_UNSUPPORTED = 7
 };
 
-typedef struct {
+struct ht_kron_src;
+typedef struct ht_tensor {
   int32_t d;              /* tensor dimension, >= 2 */
   const int64_t* n;       /* [d] host: leaf sizes by mode (mode mu -> n[mu-1]) */
   const int64_t* rank;    /* [2d-1] host: rank per node id, rank[0] == 1 */
   double* const* node;    /* [2d-1] host array of device pointers, BFS node id order */
   int32_t orthogonal;     /* HTensor.orthogonal (format.py:76) */
+  /* NULL for an ordinary tensor.  Otherwise the tensor is y = apply_operator(op, x)
+   * (arith.py:378-395) whose transfer tensors and root matrix F_t = H_t (x) B_t
+   * (arith.py:204-213) are NOT materialised: node[t] is NULL for every inner node and
+   * the root (leaf frames are ordinary device arrays), and rank[t] = op.rank[t] *
+   * x.rank[t].  Accepted by the truncation entry points only (ht_truncate*), whose
+   * orthogonalisation sweep consumes H_t and B_t in place. */
+  const struct ht_kron_src* kron;
 } ht_tensor;
 
 /* TruncationControl (arith.py:32-66). eps <= 0 means "no accuracy bound";
@@ -67,6 +75,12 @@ typedef struct {
  * eigenpairs and the tail sums, which the tridiagonal path delivers to the
  * reference's (LAPACK dsyevd) absolute accuracy. */
 #define HT_CTL_RELATIVE_SIGMA 1
+/* eps is RELATIVE to the norm of the tensor being truncated: the per-node budget is
+ * (eps ||x||)^2 / (2d-2) with ||x|| = ||B_D||_F of the orthogonalised root, taken on
+ * the device after the orthogonalisation sweep -- the C3 / C4 controls "rel. tol of
+ * every truncate's own input" without a separate inner product (and without
+ * materialising a Kronecker-form input).  Not available in ht_truncate_sharded. */
+#define HT_CTL_RELATIVE_EPS 2
 
 /* GeneralizedMatrix (format.py:135-180). kind: 0 dense (row-major rows x cols),
  * 1 diagonal (values[rows]), 2 CSR (int32 indptr[rows+1], indices[nnz]). */
@@ -86,6 +100,12 @@ typedef struct {
   const ht_gmat* const* leaf_cols;/* [2d-1] host (NULL entries for non-leaves) */
   double* const* node;            /* [2d-1] device pointers (leaf entries unused) */
 } ht_operator;
+
+/* The factors of an unmaterialised y = apply_operator(op, x) (see ht_tensor.kron). */
+typedef struct ht_kron_src {
+  const ht_operator* op;
+  const ht_tensor* x;     /* ordinary tensor (x->kron == NULL) */
+} ht_kron_src;
 
 const char* ht_last_error(void);
 const char* ht_version(void);

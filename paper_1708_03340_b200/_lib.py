@@ -46,8 +46,10 @@ _vp = ctypes.c_void_p
 
 
 class CTensor(ctypes.Structure):
+    # `kron`: ht_kron_src* (NULL for an ordinary tensor; see include/ht_b200.h)
     _fields_ = [("d", ctypes.c_int32), ("n", _i64p), ("rank", _i64p),
-                ("node", ctypes.POINTER(ctypes.c_void_p)), ("orthogonal", ctypes.c_int32)]
+                ("node", ctypes.POINTER(ctypes.c_void_p)), ("orthogonal", ctypes.c_int32),
+                ("kron", ctypes.c_void_p)]
 
 
 class CTruncCtl(ctypes.Structure):
@@ -56,6 +58,7 @@ class CTruncCtl(ctypes.Structure):
 
 
 CTL_RELATIVE_SIGMA = 1
+CTL_RELATIVE_EPS = 2
 
 
 class CGmat(ctypes.Structure):
@@ -67,6 +70,10 @@ class COperator(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("rank", _i64p),
                 ("leaf_cols", ctypes.POINTER(ctypes.POINTER(CGmat))),
                 ("node", ctypes.POINTER(ctypes.c_void_p))]
+
+
+class CKronSrc(ctypes.Structure):
+    _fields_ = [("op", ctypes.POINTER(COperator)), ("x", ctypes.POINTER(CTensor))]
 
 
 _lock = threading.Lock()

@@ -34,6 +34,10 @@ class TruncationControl:
 
     eps: float | None = None
     max_rank: int | dict | None = None
+    # eps is relative to the norm of the tensor being truncated (HT_CTL_RELATIVE_EPS:
+    # ||x|| is read off the orthogonalised root on the device; an extension of the
+    # reference control, which only has an absolute eps)
+    eps_is_relative: bool = False
 
     def __post_init__(self):
         if self.eps is None and self.max_rank is None:
@@ -54,6 +58,12 @@ class TruncationControl:
         """Relative accuracy rel*||Y|| (C3/C4 configs); the reference only has absolute eps."""
         return TruncationControl(eps=rel * norm_value, max_rank=max_rank)
 
+    @staticmethod
+    def relative_accuracy(rel: float, max_rank=None) -> "TruncationControl":
+        """eps = rel * ||x|| for whatever tensor x the control is applied to; the norm is
+        taken on the device inside the truncation (no separate inner product)."""
+        return TruncationControl(eps=rel, max_rank=max_rank, eps_is_relative=True)
+
     def cap_for(self, node_id: int):
         if self.max_rank is None:
             return None
@@ -72,6 +82,8 @@ class TruncationControl:
                 cap = 1  # select_rank keeps at least one column (arith.py:88)
         c = _lib.CTruncCtl(float(self.eps) if self.eps is not None else 0.0, cap,
                            ctypes.cast(per, ctypes.POINTER(ctypes.c_int64)) if per is not None else None)
+        if self.eps_is_relative and self.eps is not None:
+            c.flags = _lib.CTL_RELATIVE_EPS
         return c, per
 
 
@@ -236,10 +248,10 @@ class _TruncState:
         nn = len(a.tree.nodes)
         self.cctl, self._keep = ctl._c(nn)
         nbytes = ctypes.c_size_t(0)
-        _lib.check(lib.ht_truncate_workspace_size(a._c(), ctypes.byref(nbytes)), "truncate")
+        _lib.check(lib.ht_truncate_workspace_size(a._c_trunc(), ctypes.byref(nbytes)), "truncate")
         self.ws = _ws(nbytes.value, a.device)
         rbuf = (ctypes.c_int64 * nn)()
-        self.static = lib.ht_truncate_static_ranks(a._c(), ctypes.byref(self.cctl), rbuf) == 1
+        self.static = lib.ht_truncate_static_ranks(a._c_trunc(), ctypes.byref(self.cctl), rbuf) == 1
         self.ranks = {t: int(rbuf[t]) for t in range(1, nn)}
         self.phase1_done = False
 
@@ -247,7 +259,7 @@ class _TruncState:
         lib = _lib.load()
         nn = len(self.a.tree.nodes)
         rbuf = (ctypes.c_int64 * nn)()
-        _lib.check(lib.ht_truncate_ranks(self.a._c(), ctypes.byref(self.cctl), self.ws.data_ptr(), self.ws.numel(),
+        _lib.check(lib.ht_truncate_ranks(self.a._c_trunc(), ctypes.byref(self.cctl), self.ws.data_ptr(), self.ws.numel(),
                                          rbuf, _stream()), "truncate")
         self.ranks = {t: int(rbuf[t]) for t in range(1, nn)}
         self.phase1_done = True
@@ -269,12 +281,12 @@ def truncate(a: HTensor, ctl: TruncationControl, out: HTensor | None = None) -> 
     if st.static:
         if out is None:
             out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
-        _lib.check(lib.ht_truncate(a._c(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
+        _lib.check(lib.ht_truncate(a._c_trunc(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
                                    _stream()), "truncate")
         return out
     st.run_phase1()
     out = HTensor.empty(a.tree, _sizes_by_node(a), st.ranks, device=a.device)
-    _lib.check(lib.ht_truncate_project(a._c(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
+    _lib.check(lib.ht_truncate_project(a._c_trunc(), ctypes.byref(st.cctl), st.ws.data_ptr(), st.ws.numel(), out._c(),
                                        _stream()), "truncate")
     return out
 
@@ -288,11 +300,11 @@ def hierarchical_singular_values(a: HTensor) -> dict:
     st.run_phase1()
     nn = len(a.tree.nodes)
     rbuf = (ctypes.c_int64 * nn)()
-    _lib.check(lib.ht_orth_ranks(a._c(), rbuf), "orth ranks")
+    _lib.check(lib.ht_orth_ranks(a._c_trunc(), rbuf), "orth ranks")
     ko = {t: (int(rbuf[t]) if not a.orthogonal else a.rank(t)) for t in range(1, nn)}
     total = sum(ko.values())
     lam = torch.empty(total, dtype=F64, device=a.device)
-    _lib.check(lib.ht_truncate_eigenvalues(a._c(), st.ws.data_ptr(), st.ws.numel(), lam.data_ptr(), _stream()),
+    _lib.check(lib.ht_truncate_eigenvalues(a._c_trunc(), st.ws.data_ptr(), st.ws.numel(), lam.data_ptr(), _stream()),
                "eigenvalues")
     out, off = {}, 0
     for t in range(1, nn):
@@ -301,13 +313,133 @@ def hierarchical_singular_values(a: HTensor) -> dict:
     return out
 
 
-def apply_operator(op: HTOperator, a: HTensor) -> HTensor:
-    """arith.py:378-395 (Lemma 4): ranks multiply, operator index slow."""
+class AppliedHTensor(HTensor):
+    """``apply_operator(op, x)`` with its transfer tensors kept in Kronecker form.
+
+    The leaf frames V_t = [W_r U_t]_r are computed at once; the transfer tensors and
+    the root F_t = H_t (x) B_t (reference arith.py:204-213) are NOT written to memory.
+    ``truncate`` / ``hierarchical_singular_values`` consume H_t and B_t in place (the
+    orthogonalisation sweep's first mode product runs against the small B_t; SURVEY
+    K10b, ``ht_tensor.kron`` in include/ht_b200.h).  Anything else that reads the
+    tensor (``transfer``, ``to_numpy``, ``add``, ``inner_product`` ...) materialises it
+    first and from then on it is an ordinary ``HTensor``: the values are those of the
+    eager ``apply_operator`` either way.  ``op`` and ``x`` are referenced (not copied)
+    until then, so they must not be overwritten in place (``truncate(..., out=x)``).
+    """
+
+    @classmethod
+    def _build(cls, op: HTOperator, x: HTensor) -> "AppliedHTensor":
+        lib = _lib.load()
+        tree = x.tree
+        nn = len(tree.nodes)
+        ranks = {t: op.rank(t) * x.rank(t) for t in range(1, nn)}
+        sizes = {leaf.index: int(op.leaf_shape(leaf.index)[0]) for leaf in tree.leaves}
+        obj = cls.__new__(cls)
+        obj.tree = tree
+        obj.orthogonal = False
+        obj._cstruct = None
+        obj._op, obj._x = op, x
+        obj._dense = None
+        obj._ranks_cached = [1] + [ranks[t] for t in range(1, nn)]
+        obj._sizes_cached = dict(sizes)
+        obj._shape_cached = tuple(sizes[tree.leaf_for_dim(mu).index] for mu in range(1, tree.d + 1))
+        dev = x.device
+        leaf_ids = [leaf.index for leaf in tree.leaves]
+        offs, total = {}, 0
+        for t in leaf_ids:
+            offs[t] = total
+            total += sizes[t] * ranks[t]
+        arena = torch.empty(total, dtype=F64, device=dev)
+        base = arena.data_ptr()
+        n = _lib.i64_array(obj._shape_cached)
+        rk = _lib.i64_array(obj._ranks_cached)
+        cop, cx = op._c(), x._c()
+        # leaf frames through the node-masked apply (inner nodes masked off: their
+        # pointers are placeholders the call never dereferences)
+        mask = (ctypes.c_uint8 * nn)(*[1 if tree.node(t).is_leaf else 0 for t in range(nn)])
+        tmp_ptrs = _lib.ptr_array([base + 8 * offs[t] if t in offs else base for t in range(nn)])
+        tmp = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
+                           ctypes.cast(rk, ctypes.POINTER(ctypes.c_int64)),
+                           ctypes.cast(tmp_ptrs, ctypes.POINTER(ctypes.c_void_p)), 0)
+        _lib.check(lib.ht_apply_operator_sharded(ctypes.byref(cop), cx, mask, tmp, _stream()), "apply_operator")
+        ptrs = _lib.ptr_array([base + 8 * offs[t] if t in offs else 0 for t in range(nn)])
+        src = _lib.CKronSrc(ctypes.pointer(cop), ctypes.pointer(cx))
+        cs = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.cast(rk, ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), 0,
+                          ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
+        obj._kron = (cs, n, rk, ptrs, src, cop, cx, arena, dev.index)
+        return obj
+
+    # -- lazily materialised storage ---------------------------------------------
+    @property
+    def is_materialized(self) -> bool:
+        return self._dense is not None
+
+    def _materialize(self) -> HTensor:
+        if self._dense is None:
+            lib = _lib.load()
+            ranks = {t: self._ranks_cached[t] for t in range(1, len(self.tree.nodes))}
+            out = HTensor.empty(self.tree, self._sizes_cached, ranks, device=self._x.device)
+            _lib.check(lib.ht_apply_operator(ctypes.byref(self._op._c()), self._x._c(), out._c(), _stream()),
+                       "apply_operator")
+            self._dense = out
+            self._kron = None
+            self._op = self._x = None
+        return self._dense
+
+    @property
+    def _nodes(self):
+        return self._materialize()._nodes
+
+    @property
+    def _arena(self):
+        return self._materialize()._arena
+
+    @property
+    def device(self) -> torch.device:
+        return self._dense.device if self._dense is not None else self._x.device
+
+    def _shape(self, t: int) -> tuple:
+        if self._dense is not None:
+            return self._dense._shape(t)
+        node = self.tree.node(t)
+        rl = self._ranks_cached
+        if node.is_leaf:
+            return (self._sizes_cached[t], rl[t])
+        s1, s2 = node.sons
+        return (rl[s1], rl[s2]) if node.is_root else (rl[t], rl[s1], rl[s2])
+
+    def _c_trunc(self) -> _lib.CTensor:
+        if self._dense is not None:
+            return self._c()
+        if self._kron[8] != torch.cuda.current_device():
+            raise ValueError(f"HTensor lives on cuda:{self._kron[8]} but the current device is "
+                             f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device(...)")
+        return self._kron[0]
+
+
+_lazy_apply = os.environ.get("HT_LAZY_APPLY", "1") != "0"
+
+
+def set_lazy_apply(on: bool) -> None:
+    """``apply_operator`` returns an ``AppliedHTensor`` (Kronecker-form transfer tensors,
+    consumed in place by ``truncate``; default) or materialises every F_t at once."""
+    global _lazy_apply
+    _lazy_apply = bool(on)
+
+
+def apply_operator(op: HTOperator, a: HTensor, lazy: bool | None = None) -> HTensor:
+    """arith.py:378-395 (Lemma 4): ranks multiply, operator index slow.  ``lazy`` (default:
+    ``set_lazy_apply``, on) keeps the transfer tensors H_t (x) B_t unmaterialised until
+    something other than ``truncate`` reads them (``AppliedHTensor``)."""
     tree = a.tree
     if op.tree.d != tree.d:
         raise ValueError(f"operator dimension {op.tree.d} != tensor dimension {tree.d}")
     if op.col_sizes != a.shape:
         raise ValueError(f"operator column sizes {op.col_sizes} do not match tensor shape {a.shape}")
+    if _lazy_apply if lazy is None else lazy:
+        return AppliedHTensor._build(op, a)
     lib = _lib.load()
     ranks = {t: op.rank(t) * a.rank(t) for t in range(1, len(tree.nodes))}
     sizes = {leaf.index: int(op.leaf_shape(leaf.index)[0]) for leaf in tree.leaves}
@@ -454,6 +586,6 @@ def _check_all():
     return _lib.load()
 
 
-__all__ = ["TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
+__all__ = ["AppliedHTensor", "set_lazy_apply", "TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
            "orthogonalize", "compute_bhat", "truncate", "hierarchical_singular_values", "apply_operator",
            "gemm", "leaf_map", "synchronize"]

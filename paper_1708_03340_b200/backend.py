@@ -91,8 +91,8 @@ class GpuBackend:
 
     def truncate(self, x, ctl):
         rel = getattr(ctl, "rel", None)
-        if rel is not None:  # relative accuracy: eps = rel * ||x|| for this input
-            return arith.truncate(x, TruncationControl(eps=rel * arith.norm(x), max_rank=ctl.max_rank))
+        if rel is not None:  # relative accuracy: eps = rel * ||x|| for this input, ||x|| taken on the device
+            return arith.truncate(x, TruncationControl.relative_accuracy(rel, max_rank=ctl.max_rank))
         return arith.truncate(x, _ctl(ctl))
 
     def inner_product(self, x, y) -> float:

@@ -185,6 +185,15 @@ struct View {
   // empty: every node; else the nodes this shard owns -- the truncate workspace then
   // holds state only for owned nodes and their sons (the message slots), sized for them
   std::vector<unsigned char> owned;
+  // Kronecker-form transfer tensors (ht_tensor.kron): F_t = H_t (x) B_t of
+  // y = apply_operator(op, x), not materialised (p[t] == nullptr for inner nodes and the
+  // root).  Empty for an ordinary tensor.
+  struct KronNode {
+    const double* H = nullptr;  // (rt, r1, r2) operator transfer tensor (root: rt = 1)
+    const double* B = nullptr;  // (kt, k1, k2) tensor transfer tensor (root: kt = 1)
+    int rt = 1, r1 = 1, r2 = 1, kt = 1, k1 = 1, k2 = 1;
+  };
+  std::vector<KronNode> kron;
   bool on(int t) const { return mask.empty() || mask[t] != 0; }
   bool needed(int t) const {
     return owned.empty() || owned[t] != 0 || (t > 0 && owned[T->father[t]] != 0);
@@ -198,16 +207,26 @@ struct View {
   }
 };
 
-int make_view(const ht_tensor* x, View& v, bool need_ptrs = true) {
+int make_view(const ht_tensor* x, View& v, bool need_ptrs = true, bool allow_kron = false) {
   if (!x || x->d < 2) {
     set_error("tensor dimension must be >= 2");
     return kErrShape;
+  }
+  const ht_kron_src* ks = x->kron;
+  if (ks && !allow_kron) {
+    set_error("a Kronecker-form tensor (unmaterialised apply_operator result) is accepted by truncate only");
+    return kErrUnsupported;
+  }
+  if (ks && (!ks->op || !ks->x || ks->x->kron || ks->op->d != x->d || ks->x->d != x->d || x->orthogonal)) {
+    set_error("malformed Kronecker-form tensor");
+    return kErrArgument;
   }
   const Tree& T = tree_for(x->d);
   v.T = &T;
   v.n.assign(T.nn, 0);
   v.k.assign(T.nn, 1);
   v.p.assign(T.nn, nullptr);
+  v.kron.clear();
   v.orth = x->orthogonal != 0;
   for (int t = 0; t < T.nn; ++t) {
     v.k[t] = t == 0 ? 1 : x->rank[t];
@@ -221,6 +240,31 @@ int make_view(const ht_tensor* x, View& v, bool need_ptrs = true) {
         set_error("leaf size must be >= 1");
         return kErrShape;
       }
+    }
+    if (ks && !T.leaf(t)) {
+      View::KronNode kn;
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      kn.rt = t == 0 ? 1 : (int)ks->op->rank[t];
+      kn.r1 = (int)ks->op->rank[s1]; kn.r2 = (int)ks->op->rank[s2];
+      kn.kt = t == 0 ? 1 : (int)ks->x->rank[t];
+      kn.k1 = (int)ks->x->rank[s1]; kn.k2 = (int)ks->x->rank[s2];
+      if (kn.rt < 1 || kn.r1 < 1 || kn.r2 < 1 || kn.kt < 1 || kn.k1 < 1 || kn.k2 < 1 ||
+          (t > 0 && x->rank[t] != (long long)kn.rt * kn.kt) || x->rank[s1] != (long long)kn.r1 * kn.k1 ||
+          x->rank[s2] != (long long)kn.r2 * kn.k2) {
+        set_error("Kronecker-form ranks must be operator rank * tensor rank");
+        return kErrShape;
+      }
+      if (need_ptrs) {
+        if (!ks->op->node || !ks->op->node[t] || !ks->x->node || !ks->x->node[t]) {
+          set_error("missing device pointer for Kronecker factor of node " + std::to_string(t));
+          return kErrArgument;
+        }
+        kn.H = ks->op->node[t];
+        kn.B = ks->x->node[t];
+      }
+      if (v.kron.empty()) v.kron.assign(T.nn, View::KronNode{});
+      v.kron[t] = kn;
+      continue;
     }
     if (need_ptrs) {
       if (!x->node || !x->node[t]) {
@@ -505,18 +549,26 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
   const size_t scratch_base = scratch_ar.off;
   size_t scratch_max = scratch_base;
   for (int l = T.depth; l >= 1; --l) {
+   const bool kr = !x.kron.empty();
    const auto chunks = level_chunks(T.levels[l], x, [&](int t) {
      if (T.leaf(t)) return 16.0 * x.n[t] * x.k[t];
-     return 24.0 * x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]];  // T1 + Bp + QR scratch
+     double b = 24.0 * x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]];  // T1 + Bp + QR scratch
+     if (kr) b += 8.0 * x.kron[t].rt * x.kron[t].r2 * ko[T.son1[t]] * x.kron[t].k1;  // E
+     return b;
    });
    for (const auto& chunk : chunks) {
     scratch_ar.off = scratch_base;
     std::vector<GemmDesc> g2, g3;
     std::vector<SsDesc> sa2, sa3;
     std::vector<QrProblem> qs;
-    std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr);
+    std::vector<KronFactorDesc> kf;
+    std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr), Es(T.nn, nullptr);
     for (int t : chunk)
       if (!T.leaf(t) && x.on(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
+    if (kr)
+      for (int t : chunk)
+        if (!T.leaf(t) && x.on(t))
+          Es[t] = scratch_ar.take((long long)x.kron[t].rt * x.kron[t].r2 * ko[T.son1[t]] * x.kron[t].k1);
     // implicit Q (Cholesky-QR sweep only): the absorbed tensor goes straight into the
     // node's slot and stays there
     auto imp = [&](int t) { return chol && !op.imp.empty() && op.imp[t]; };
@@ -537,6 +589,31 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       const long long kt = x.k[t], k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
       double* T1 = T1s[t];
       double* Bp = imp(t) ? op.out[t] : Bps[t];
+      if (kr) {
+        // Kronecker-form node F = H (x) B (arith.py:204-213), never materialised:
+        //   T1[(a,i), J, (c,l)] = sum_j E_ac[J, j] B[i, j, l],  E_ac = sum_b H[a,b,c] R1[:, (b,:)]
+        // -- rt*r2 products against the small tensor B, 1/r1 of the dense mode product's
+        // flops and no read of the (rt r1 r2)-fold larger F.
+        const View::KronNode& kn = x.kron[t];
+        const long long kts = kn.kt, k1s = kn.k1, k2s = kn.k2;
+        double* E = Es[t];
+        kf.push_back(KronFactorDesc{kn.H, op.R[s1], E, kn.rt, kn.r1, kn.r2, (int)k1s, (int)k1o, (int)k1});
+        for (int a = 0; a < kn.rt; ++a) {
+          const double* Ea = E ? E + (long long)a * kn.r2 * k1o * k1s : nullptr;
+          double* Ta = T1 ? T1 + (long long)a * kts * k1o * k2 : nullptr;
+          if (ss_fits(k1o, k1s)) {
+            SsDesc d = ss_desc(kn.B, 1, k2s, Ea, 1, k1s, Ta, 1, k2, (int)(kts * k2s), (int)k1o, (int)k1s);
+            d.M_lo = (int)k2s; d.x_hi = k1s * k2s; d.c_hi = k1o * k2;
+            d.jobs = kn.r2; d.x_job = 0; d.s_job = k1o * k1s; d.c_job = k2s;
+            sa2.push_back(d);
+          } else {
+            GemmDesc g = gemm_desc(Ea, k1s, 1, kn.B, k2s, 1, Ta, k2, 1, (int)k1o, (int)k2s, (int)k1s);
+            g.nb1 = (int)kts; g.a_b1 = 0; g.b_b1 = k1s * k2s; g.c_b1 = k1o * k2;
+            g.nb2 = kn.r2; g.a_b2 = k1o * k1s; g.b_b2 = 0; g.c_b2 = k2s;
+            g2.push_back(g);
+          }
+        }
+      } else
       // mode-2 absorb, per slice i: T1_i (k1o x k2) = R1 (k1o x k1) * B_i (k1 x k2)
       if (ss_fits(k1o, k1)) {
         // streamed as T1_i^T = B_i^T R1^T over the rows (i, l): R1^T stays in shared memory
@@ -616,6 +693,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       merge_gemms(g3);
       merge_ss(sa2);
       merge_ss(sa3);
+      HT_TRY(kron_factor_batched(kf, s));
       HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
       HT_TRY(ss_gemm(sa2, s, "ss_absorb"));
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
@@ -640,9 +718,16 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     const int s1 = T.son1[0], s2 = T.son2[0];
     const long long k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
     double* tmp = scratch_ar.take(k1o * k2);
+    // Kronecker-form root H_D (x) B_D (arith.py:212-213): a k1 x k2 matrix, materialised here
+    double* xroot = x.kron.empty() ? x.p[0] : scratch_ar.take(k1 * k2);
     scratch_max = std::max(scratch_max, scratch_ar.off);
     if (exec) {
-      std::vector<GemmDesc> g{gemm_desc(op.R[s1], k1, 1, x.p[0], k2, 1, tmp, k2, 1, (int)k1o, (int)k2, (int)k1)};
+      if (!x.kron.empty()) {
+        const View::KronNode& kn = x.kron[0];
+        std::vector<KronDesc> kd{KronDesc{xroot, kn.H, kn.B, 1, kn.r1, kn.r2, 1, kn.k1, kn.k2}};
+        HT_TRY(kron_batched(kd, s));
+      }
+      std::vector<GemmDesc> g{gemm_desc(op.R[s1], k1, 1, xroot, k2, 1, tmp, k2, 1, (int)k1o, (int)k2, (int)k1)};
       HT_TRY(gemm_grouped(g, s));
       std::vector<GemmDesc> g4{gemm_desc(tmp, k2, 1, op.R[s2], 1, k2, op.out[0], k2o, 1, (int)k1o, (int)k2o, (int)k2)};
       HT_TRY(gemm_grouped(g4, s));
@@ -883,6 +968,7 @@ struct TruncPlan {
   int* status = nullptr;
   int* qr_fail = nullptr;
   int* eigflag = nullptr;  // per node: redo with Jacobi (set by the tridiagonal fast path)
+  double* norm2 = nullptr;  // ||x||^2 = ||root of the orthogonalised tensor||_F^2 (HT_CTL_RELATIVE_EPS)
   std::vector<double*> eigwork;  // per node: eigensolver scratch when K > kEigMaxK
   Arena scratch;
 };
@@ -966,6 +1052,7 @@ int plan_truncate(const View& x, TruncPlan& P, char* base) {
   P.status = P.ranks + T.nn;
   P.qr_fail = P.ranks + T.nn + 1;
   P.eigflag = ar.take_int(T.nn);
+  P.norm2 = ar.take(1);
   P.eigwork.assign(T.nn, nullptr);
   for (int t = 1; t < T.nn; ++t)
     if (P.o.k[t] > kEigMaxK && (x.owned.empty() || x.owned[t]))
@@ -994,6 +1081,7 @@ size_t truncate_ws_bytes(const View& x) {
     key.push_back(x.n[t]);
     key.push_back(x.k[t]);
     key.push_back(x.owned.empty() ? 2 : x.owned[t]);
+    if (!x.kron.empty()) key.push_back(((long long)x.kron[t].rt << 40) | ((long long)x.kron[t].r1 << 20) | x.kron[t].r2);
   }
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -1084,13 +1172,14 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
     e.work = P.eigwork[t];
     e.K = (int)P.o.k[t]; e.nodes = 1;
     e.eps = ctl->eps > 0 ? ctl->eps : 0.0;
+    e.eps_scale2 = (e.eps > 0 && (ctl->flags & HT_CTL_RELATIVE_EPS)) ? P.norm2 : nullptr;
     e.n_nonroot = T.nn - 1;
     e.cap = eig_caps(ctl, t);
     e.graded_fallback = (ctl->flags & HT_CTL_RELATIVE_SIGMA) ? 1 : 0;
     e.s_node = 0; e.v_node = 0; e.l_node = 0;
     if (!eps.empty()) {
       EigProblem& b = eps.back();
-      if (b.K == e.K && b.cap == e.cap && b.graded_fallback == e.graded_fallback && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback &&
+      if (b.K == e.K && b.cap == e.cap && b.graded_fallback == e.graded_fallback && b.eps_scale2 == e.eps_scale2 && b.rank + b.nodes == e.rank && b.fallback + b.nodes == e.fallback &&
           (b.work == nullptr) == (e.work == nullptr)) {
         if (b.nodes == 1) {
           b.s_node = e.S - b.S; b.v_node = e.V - b.V; b.l_node = e.lam - b.lam;
@@ -1107,6 +1196,13 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
       }
     }
     eps.push_back(e);
+  }
+  if (ctl->eps > 0 && (ctl->flags & HT_CTL_RELATIVE_EPS)) {
+    if (!x.on(0) || !P.o.p[0]) {
+      set_error("HT_CTL_RELATIVE_EPS needs the root on this rank (not available in the sharded phases)");
+      return kErrUnsupported;
+    }
+    HT_TRY(dot(P.o.p[0], P.o.p[0], P.o.k[T.son1[0]] * P.o.k[T.son2[0]], P.norm2, s));
   }
   HT_TRY(eig_batched(eps, s));
   if (sticky) {
@@ -1682,6 +1778,7 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
   ran = false;
   failed = false;
   if (!graphs_on() || g_qr_mode == 1 || prof_active()) return kOk;
+  if (!v.kron.empty()) return kOk;  // Kronecker-form input: eager (its factors' addresses are not tracked)
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(s, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) {
     cudaGetLastError();
@@ -1768,14 +1865,14 @@ const char* ht_version(void) { return "ht_b200 0.1.0 (sm_100a, fp64 DMMA)"; }
 
 int ht_truncate_workspace_size(const ht_tensor* x, size_t* bytes) {
   View v;
-  HT_TRY(make_view(x, v, false));
+  HT_TRY(make_view(x, v, false, true));
   *bytes = truncate_ws_bytes(v);
   return kOk;
 }
 
 int ht_truncate_static_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, int64_t* out_rank) {
   View v;
-  HT_TRY(make_view(x, v, false));
+  HT_TRY(make_view(x, v, false, true));
   HT_TRY(check_ctl(ctl));
   bool ok = false;
   auto r = static_ranks(v, ctl, ok);
@@ -1787,7 +1884,7 @@ int ht_truncate_static_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, int64_
 int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, int64_t* out_rank,
                       ht_stream_t stream) {
   View v;
-  HT_TRY(make_view(x, v));
+  HT_TRY(make_view(x, v, true, true));
   cudaStream_t s = (cudaStream_t)stream;
   TruncPlan P;
   OrthCheck chk;
@@ -1818,7 +1915,7 @@ int ht_truncate_ranks(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, siz
 int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, const ht_tensor* out,
                         ht_stream_t stream) {
   View v, o;
-  HT_TRY(make_view(x, v));
+  HT_TRY(make_view(x, v, true, true));
   HT_TRY(out_view(out, v, o));
   (void)ctl;
   if (ws_bytes < truncate_ws_bytes(v)) {
@@ -1831,7 +1928,7 @@ int ht_truncate_project(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
 int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws_bytes, const ht_tensor* out,
                 ht_stream_t stream) {
   View v, o;
-  HT_TRY(make_view(x, v));
+  HT_TRY(make_view(x, v, true, true));
   HT_TRY(check_ctl(ctl));
   bool ok = false;
   auto r = static_ranks(v, ctl, ok);
@@ -1877,6 +1974,10 @@ int ht_truncate_sharded(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, s
   View v;
   HT_TRY(make_view(x, v));
   HT_TRY(check_ctl(ctl));
+  if (ctl->flags & HT_CTL_RELATIVE_EPS) {
+    set_error("HT_CTL_RELATIVE_EPS is not available in the sharded phases (pass eps * dist norm)");
+    return kErrUnsupported;
+  }
   if (owned) v.owned.assign(owned, owned + v.T->nn);
   HT_TRY(check_ws(v, (char*)ws, ws_bytes));
   if (mask) {
@@ -1961,7 +2062,7 @@ int ht_truncate_slot(const ht_tensor* x, void* ws, const uint8_t* owned, int32_t
 
 int ht_truncate_eigenvalues(const ht_tensor* x, void* ws, size_t ws_bytes, double* lam, ht_stream_t stream) {
   View v;
-  HT_TRY(make_view(x, v));
+  HT_TRY(make_view(x, v, true, true));
   if (ws_bytes < truncate_ws_bytes(v)) {
     set_error("truncate workspace too small");
     return kErrArgument;
@@ -1979,7 +2080,7 @@ int ht_truncate_eigenvalues(const ht_tensor* x, void* ws, size_t ws_bytes, doubl
 
 int ht_orth_ranks(const ht_tensor* x, int64_t* out_rank) {
   View v;
-  HT_TRY(make_view(x, v, false));
+  HT_TRY(make_view(x, v, false, true));
   auto ko = orth_ranks(v);
   for (int t = 0; t < v.T->nn; ++t) out_rank[t] = ko[t];
   return kOk;

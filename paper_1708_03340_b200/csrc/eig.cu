@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(ET, 1) jacobi_kernel(const __grid_constant__ E
   if (tid == 0 && e.rank) {
     int r = K;
     if (e.eps > 0.0) {
-      const double budget = e.eps * e.eps / e.n_nonroot;
+      const double budget = e.eps * e.eps * (e.eps_scale2 ? *e.eps_scale2 : 1.0) / e.n_nonroot;
       // tails[r] = sum_{i >= r} lam[i], accumulated from the end like numpy's cumsum (arith.py:83-84)
       double tail = 0.0;
       r = K;

@@ -27,6 +27,8 @@ struct EigProblem {
   int* status;      // device int, OR-ed with error bits (may be null)
   int K, nodes;
   double eps;       // absolute truncation accuracy; <= 0: none
+  const double* eps_scale2;  // optional device scalar: the budget uses eps^2 * *eps_scale2
+                             // (HT_CTL_RELATIVE_EPS: ||x||^2)
   int n_nonroot;    // 2d - 2
   int cap;          // rank cap; <= 0: none
   int* fallback;    // per-node flags (node stride 1): set by the tridiagonal fast path for

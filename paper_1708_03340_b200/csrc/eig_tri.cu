@@ -425,7 +425,7 @@ __global__ void __launch_bounds__(TT, 1) tri_eig_kernel(const __grid_constant__ 
   if (tid == 0) {
     int r = K;
     if (e.eps > 0.0) {
-      const double budget = e.eps * e.eps / e.n_nonroot;
+      const double budget = e.eps * e.eps * (e.eps_scale2 ? *e.eps_scale2 : 1.0) / e.n_nonroot;
       double tail = 0.0;
       for (int k = K - 1; k >= 0; --k) {  // descending index k <-> ascending K-1-k
         tail += fmax(lam[K - 1 - k] * unscale, 0.0);

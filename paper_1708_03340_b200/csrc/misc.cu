@@ -118,6 +118,31 @@ __global__ void kron_kernel(const __grid_constant__ KronBatch b) {
   }
 }
 
+struct KronFactorBatch {
+  int count;
+  int begin[MAXD + 1];
+  KronFactorDesc d[MAXD];
+};
+
+__global__ void kron_factor_kernel(const __grid_constant__ KronFactorBatch b) {
+  const int di = find(b);
+  const KronFactorDesc& k = b.d[di];
+  const long long total = (long long)k.ra * k.rc * k.ko * k.ks;
+  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
+  for (long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x; x < total; x += stride) {
+    const int j = (int)(x % k.ks);
+    long long r = x / k.ks;
+    const int J = (int)(r % k.ko);
+    r /= k.ko;
+    const int c = (int)(r % k.rc), a = (int)(r / k.rc);
+    const double* h = k.H + ((long long)a * k.rb) * k.rc + c;
+    const double* row = k.R + (long long)J * k.ldr + j;
+    double v = 0.0;
+    for (int q = 0; q < k.rb; ++q) v = fma(h[(long long)q * k.rc], row[(long long)q * k.ks], v);
+    k.E[x] = v;
+  }
+}
+
 __global__ void leaf_apply_kernel(const __grid_constant__ LeafBatch b) {
   const int di = find(b);
   const LeafApplyDesc& e = b.d[di];
@@ -228,6 +253,30 @@ int kron_batched(const std::vector<KronDesc>& descs, cudaStream_t stream) {
     kron_kernel<<<blocks, 256, 0, stream>>>(b);
     HT_LAUNCH_CHECK();
     prof_end(tok, "kron", stream, 0.0, 0.0);
+  }
+  return kOk;
+}
+
+int kron_factor_batched(const std::vector<KronFactorDesc>& descs, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    KronFactorBatch b;
+    b.count = 0;
+    int blocks = 0;
+    while (i < descs.size() && b.count < MAXD) {
+      const KronFactorDesc& d = descs[i++];
+      const long long total = (long long)d.ra * d.rc * d.ko * d.ks;
+      if (total == 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += blocks_for(total);
+      b.d[b.count++] = d;
+    }
+    if (!b.count) continue;
+    b.begin[b.count] = blocks;
+    ProfToken tok = prof_begin(stream);
+    kron_factor_kernel<<<blocks, 256, 0, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "kron_factor", stream, 0.0, 0.0);
   }
   return kOk;
 }

@@ -33,6 +33,19 @@ struct KronDesc {
 };
 int kron_batched(const std::vector<KronDesc>& descs, cudaStream_t stream);
 
+// Stationary operands of a mode product applied to an unmaterialised Kronecker product
+// F = H (x) B (arith.py:204-213 consumed in place): with R (ko x rb*ks row-major, ld ldr)
+// the factor absorbed into the mode whose operator index is b,
+//   E[a][c][J][j] = sum_b H[a,b,c] R[J, b*ks + j]        (ra x rc matrices of ko x ks)
+// so that (F x_2 R)[(a,i), J, (c,l)] = sum_j E[a][c][J][j] B[i,j,l].
+struct KronFactorDesc {
+  const double* H;
+  const double* R;
+  double* E;
+  int ra, rb, rc, ks, ko, ldr;
+};
+int kron_factor_batched(const std::vector<KronFactorDesc>& descs, cudaStream_t stream);
+
 // Leaf operator column applied to U (n_in x k row-major), written into columns
 // [col0, col0+k) of V (n_out x ldv row-major).  kind 1: diagonal, kind 2: CSR.
 struct LeafApplyDesc {

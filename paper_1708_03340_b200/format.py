@@ -345,6 +345,11 @@ class HTensor:
         cs.orthogonal = int(self.orthogonal)
         return cs
 
+    def _c_trunc(self) -> _lib.CTensor:
+        """The C view the truncation entry points take (``AppliedHTensor`` overrides it
+        with its Kronecker form)."""
+        return self._c()
+
     def __repr__(self) -> str:
         return (f"HTensor(d={self.tree.d}, shape={self.shape}, max_rank={self.max_rank}, "
                 f"orthogonal={self.orthogonal}, device={self.device})")

@@ -72,13 +72,21 @@ def c3(reps):
     y = htb.apply_operator(op, x)
     ny = htb.norm(y)
     ctl = htb.TruncationControl(eps=1e-8 * ny, max_rank=30)
-    ms_apply = timed(lambda: htb.apply_operator(op, x), reps)
+    y = htb.apply_operator(op, x, lazy=False)
+    ms_apply = timed(lambda: htb.apply_operator(op, x, lazy=False), reps)
     ms_norm = timed(lambda: htb.norm(y), reps)
     ms_tr = timed(lambda: htb.truncate(y, ctl), reps)
     t = htb.truncate(y, ctl)
+    # Kronecker-fused workflow: F_t never materialised, ||Y|| taken on the device inside
+    # the truncation (HT_CTL_RELATIVE_EPS)
+    rctl = htb.TruncationControl.relative_accuracy(1e-8, max_rank=30)
+    ms_fused = timed(lambda: htb.truncate(htb.apply_operator(op, x), rctl), reps)
+    ms_lazy_apply = timed(lambda: htb.apply_operator(op, x), reps)
+    tf = htb.truncate(htb.apply_operator(op, x), rctl)
     return {"config": "C3", "d": 16, "n": 256, "K": 60, "r": 30, "apply_ms": ms_apply, "norm_ms": ms_norm,
             "truncate_ms": ms_tr, "apply_norm_truncate_ms": ms_apply + ms_norm + ms_tr,
-            "ranks_out": sorted(set(t.ranks.values()))}
+            "fused_apply_truncate_ms": ms_fused, "lazy_apply_ms": ms_lazy_apply,
+            "ranks_out": sorted(set(t.ranks.values())), "ranks_out_fused": sorted(set(tf.ranks.values()))}
 
 
 def c5_shard(reps):
