@@ -313,7 +313,8 @@ def run_reference(args, rank, world):
     return {
         "metric": METRIC, "value": value, "unit": UNIT, "impl": "reference", "n_gpus": world,
         "steps": len(times), "warmup": warm, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-        "scaling": "strong" if world > 1 and not args.replicas else "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if (world > 1 and not args.replicas and not args.weak) else "weak", "vs_baseline": None,
+        "dtype": "f64",
         "data": "synthetic (seeded Gaussian, SURVEY §8(d))",
         "config": {**config_dict(args, world),
                    "inflight": 1, "inflight_note": "CPU reference: one truncation at a time on all host threads"},
@@ -332,6 +333,9 @@ def config_dict(args, world=1):
             "seeds": [2 * int(round(math.log2(args.d))), 2 * int(round(math.log2(args.d))) + 1],
             "l2_policy": f"inputs {8 * storage(args.d, args.n, 2 * args.k) / 1e6:.0f} MB > 126 MB L2 (no flush needed)",
             "parallelism": par,
+            **({"weak_scaling": {"leaves_per_gpu": args.leaves_per_gpu, "log2_d": math.log2(args.d),
+                                 "note": "d grows with the GPU count; plot ms_per_step against log2_d"}}
+               if getattr(args, "weak", False) and sharded else {}),
             "inflight": 1 if sharded else args.inflight,
             "inflight_note": ("independent truncations in flight on as many CUDA streams of the GPU (each a complete "
                               "truncation with its own workspace and output); step time = run time / steps")}
@@ -657,7 +661,7 @@ def run_ours(args, rank, world, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
-        "scaling": "strong" if sharded else "weak",
+        "scaling": "strong" if (sharded and not args.weak) else "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded Gaussian factors, SURVEY §8(d))",
         "config": config_dict(args, world),
         "roofline": roof,
@@ -708,11 +712,17 @@ def main():
                     help="also run the C2 weak-scaling study d = 8..256 (time vs log2 d, fit a + b log2 d)")
     ap.add_argument("--replicas", action="store_true",
                     help="N>1: independent replica tensors per GPU instead of one tree-sharded tensor")
+    ap.add_argument("--weak", action="store_true",
+                    help="N>1: weak scaling of the tree-sharded truncation -- d = D * N leaves (every GPU owns a "
+                         "D-leaf subtree), the paper's runtime-vs-log2(d) study (reference bench.py:184-204)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    args.leaves_per_gpu = args.d
+    if args.weak and world > 1 and not args.replicas:
+        args.d *= world
     if args.impl == "reference":
         line = run_reference(args, rank, world)
     else:
