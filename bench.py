@@ -361,7 +361,9 @@ class _Single:
 
         self.htb, self.tree, self.ctl = htb, tree, ctl
         self.a, self.c = htb.HTensor(tree, *fa), htb.HTensor(tree, *fc)
-        self.x = htb.add(self.a, self.c)  # X resident in HBM (547 MB at d=64: larger than L2)
+        # X resident in HBM, materialised (547 MB at d=64: larger than L2); the block-form
+        # (lazy) sum is what the end-to-end workflow below truncates
+        self.x = htb.add(self.a, self.c, lazy=False)
         self.inflight = max(1, inflight)
         self.streams = [torch.cuda.Stream() for _ in range(self.inflight)]
         T = htb.truncate(self.x, ctl)

@@ -45,6 +45,7 @@ enum {
 };
 
 struct ht_kron_src;
+struct ht_sum_src;
 typedef struct ht_tensor {
   int32_t d;              /* tensor dimension, >= 2 */
   const int64_t* n;       /* [d] host: leaf sizes by mode (mode mu -> n[mu-1]) */
@@ -58,6 +59,15 @@ typedef struct ht_tensor {
    * x.rank[t].  Accepted by the truncation entry points only (ht_truncate*), whose
    * orthogonalisation sweep consumes H_t and B_t in place. */
   const struct ht_kron_src* kron;
+  /* NULL for an ordinary tensor.  Otherwise the tensor is the block-form sum
+   * y = sum_q alpha[q] * term[q] (arith.py:173-192: leaf frames concatenated, transfer
+   * tensors and root block-diagonal, alpha on the root blocks) whose block-diagonal
+   * transfer tensors and root are NOT materialised: node[t] is NULL for every inner
+   * node and the root, the leaf frames [U_1 .. U_p] are ordinary device arrays, and
+   * rank[t] = sum_q term[q].rank[t].  Accepted by the truncation entry points only:
+   * the orthogonalisation sweep's mode products run on the diagonal blocks (SURVEY
+   * K9 / 7.4.7: 1 - 1/p^2 of an inner node is structural zeros). */
+  const struct ht_sum_src* sum;
 } ht_tensor;
 
 /* TruncationControl (arith.py:32-66). eps <= 0 means "no accuracy bound";
@@ -100,6 +110,13 @@ typedef struct {
   const ht_gmat* const* leaf_cols;/* [2d-1] host (NULL entries for non-leaves) */
   double* const* node;            /* [2d-1] device pointers (leaf entries unused) */
 } ht_operator;
+
+/* The terms of an unmaterialised block-form sum (see ht_tensor.sum). */
+typedef struct ht_sum_src {
+  int32_t count;                   /* p >= 2 terms */
+  const ht_tensor* const* term;    /* [p] ordinary tensors (kron == sum == NULL), same d and n */
+  const double* alpha;             /* [p] host: coefficient of each term (applied to its root block) */
+} ht_sum_src;
 
 /* The factors of an unmaterialised y = apply_operator(op, x) (see ht_tensor.kron). */
 typedef struct ht_kron_src {

@@ -49,7 +49,7 @@ class CTensor(ctypes.Structure):
     # `kron`: ht_kron_src* (NULL for an ordinary tensor; see include/ht_b200.h)
     _fields_ = [("d", ctypes.c_int32), ("n", _i64p), ("rank", _i64p),
                 ("node", ctypes.POINTER(ctypes.c_void_p)), ("orthogonal", ctypes.c_int32),
-                ("kron", ctypes.c_void_p)]
+                ("kron", ctypes.c_void_p), ("sum", ctypes.c_void_p)]
 
 
 class CTruncCtl(ctypes.Structure):
@@ -70,6 +70,11 @@ class COperator(ctypes.Structure):
     _fields_ = [("d", ctypes.c_int32), ("rank", _i64p),
                 ("leaf_cols", ctypes.POINTER(ctypes.POINTER(CGmat))),
                 ("node", ctypes.POINTER(ctypes.c_void_p))]
+
+
+class CSumSrc(ctypes.Structure):
+    _fields_ = [("count", ctypes.c_int32), ("term", ctypes.POINTER(ctypes.POINTER(CTensor))),
+                ("alpha", ctypes.POINTER(ctypes.c_double))]
 
 
 class CKronSrc(ctypes.Structure):

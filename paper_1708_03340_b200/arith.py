@@ -127,12 +127,16 @@ def _stream():
 # ---------------------------------------------------------------------------
 
 
-def add(a: HTensor, c: HTensor, out: HTensor | None = None) -> HTensor:
-    """arith.py:355-365: frames concatenate, transfers embed block-diagonally.  ``out``
+def add(a: HTensor, c: HTensor, out: HTensor | None = None, lazy: bool | None = None) -> HTensor:
+    """arith.py:355-365: frames concatenate, transfers embed block-diagonally.  By
+    default (``set_lazy_add``) the result is a ``SumHTensor``: the block-diagonal transfer
+    tensors are not written until something other than ``truncate`` reads them.  ``out``
     (optional, an extension of the reference API): an existing tensor of the sum's
-    shapes to write into (pipelines reuse device buffers; fixed buffers also let the
-    truncation replay its captured CUDA graphs without re-pointing them)."""
-    return _add(a, c, 1.0, out)
+    shapes to write into -- an ordinary ``HTensor`` (materialised sum; pipelines reuse
+    device buffers, and fixed buffers let the truncation replay its captured CUDA graphs
+    without re-pointing them) or a ``SumHTensor`` returned by an earlier ``add`` of
+    tensors of these shapes (its leaf arena is reused)."""
+    return _add(a, c, 1.0, out, lazy)
 
 
 def subtract(a: HTensor, c: HTensor) -> HTensor:
@@ -147,8 +151,26 @@ def _check_out(out: HTensor, tree, sizes: dict, ranks: dict) -> None:
         raise ValueError("out tensor has the wrong shapes for this result")
 
 
-def _add(a: HTensor, c: HTensor, alpha_c: float, out: HTensor | None = None) -> HTensor:
+_lazy_add = os.environ.get("HT_LAZY_ADD", "1") != "0"
+
+
+def set_lazy_add(on: bool) -> None:
+    """``add`` / ``subtract`` return a ``SumHTensor`` (block-form sum, consumed in place by
+    ``truncate``; default) or materialise the block-diagonal embedding at once."""
+    global _lazy_add
+    _lazy_add = bool(on)
+
+
+def _add(a: HTensor, c: HTensor, alpha_c: float, out: HTensor | None = None, lazy: bool | None = None) -> HTensor:
     _check_compatible(a, c)
+    if lazy is None:
+        lazy = _lazy_add if out is None else (isinstance(out, SumHTensor) and out._dense is None)
+    if lazy:
+        terms = _sum_terms(a, 1.0) + _sum_terms(c, float(alpha_c))
+        assert terms[0][0] == 1.0  # the first block carries no coefficient (as in the eager embedding)
+        return SumHTensor._build(terms, a, c, out if isinstance(out, SumHTensor) else None)
+    if isinstance(out, _LazyHTensor) and out._dense is None:
+        raise ValueError("out tensor has the wrong shapes for this result")
     lib = _lib.load()
     tree = a.tree
     ra, rc = a._rank_list(), c._rank_list()
@@ -212,13 +234,13 @@ def orthogonalize(a: HTensor) -> HTensor:
     tree = a.tree
     nn = len(tree.nodes)
     rbuf = (ctypes.c_int64 * nn)()
-    _lib.check(lib.ht_orth_ranks(a._c(), rbuf), "orthogonalize")
+    _lib.check(lib.ht_orth_ranks(a._c_trunc(), rbuf), "orthogonalize")
     ranks = {t: int(rbuf[t]) for t in range(1, nn)}
     out = HTensor.empty(tree, _sizes_by_node(a), ranks, orthogonal=True, device=a.device)
     nbytes = ctypes.c_size_t(0)
-    _lib.check(lib.ht_orthogonalize_workspace_size(a._c(), ctypes.byref(nbytes)), "orthogonalize")
+    _lib.check(lib.ht_orthogonalize_workspace_size(a._c_trunc(), ctypes.byref(nbytes)), "orthogonalize")
     ws = _ws(nbytes.value, a.device)
-    _lib.check(lib.ht_orthogonalize(a._c(), ws.data_ptr(), ws.numel(), out._c(), _stream()), "orthogonalize")
+    _lib.check(lib.ht_orthogonalize(a._c_trunc(), ws.data_ptr(), ws.numel(), out._c(), _stream()), "orthogonalize")
     return out
 
 
@@ -313,7 +335,93 @@ def hierarchical_singular_values(a: HTensor) -> dict:
     return out
 
 
-class AppliedHTensor(HTensor):
+class _LazyHTensor(HTensor):
+    """An ``HTensor`` whose transfer tensors and root are held in a structured form
+    (Kronecker products / diagonal blocks) until something other than ``truncate`` /
+    ``hierarchical_singular_values`` reads them.  Leaf frames are ordinary arrays in
+    ``_leaf_arena``; ``_lazy`` keeps the C structs (and everything they point to) alive.
+    Subclasses provide ``_materialize_now() -> HTensor``."""
+
+    def _init_lazy(self, tree, sizes: dict, ranks: dict, dev, leaf_arena=None):
+        nn = len(tree.nodes)
+        self.tree = tree
+        self.orthogonal = False
+        self._cstruct = None
+        self._dense = None
+        self._ranks_cached = [1] + [ranks[t] for t in range(1, nn)]
+        self._sizes_cached = dict(sizes)
+        self._shape_cached = tuple(sizes[tree.leaf_for_dim(mu).index] for mu in range(1, tree.d + 1))
+        self._lazy_dev = dev
+        offs, total = {}, 0
+        for t in sorted(leaf.index for leaf in tree.leaves):  # node-id order, 256-byte aligned frames
+            offs[t] = total
+            total += (sizes[t] * ranks[t] + 31) // 32 * 32
+        if leaf_arena is None:
+            leaf_arena = torch.empty(total, dtype=F64, device=dev)
+        self._leaf_arena = leaf_arena
+        base = leaf_arena.data_ptr()
+        self._n_arr = _lib.i64_array(self._shape_cached)
+        self._rk_arr = _lib.i64_array(self._ranks_cached)
+        # leaf pointers; inner nodes get a placeholder (`base`) in the struct handed to the
+        # node-masked kernels that fill the leaves, and NULL in the lazy struct
+        self._leaf_ptrs = [base + 8 * offs[t] if t in offs else None for t in range(nn)]
+        self._leaf_mask = (ctypes.c_uint8 * nn)(*[1 if t in offs else 0 for t in range(nn)])
+        ph = _lib.ptr_array([p if p is not None else base for p in self._leaf_ptrs])
+        self._leaf_cs = (_lib.CTensor(tree.d, ctypes.cast(self._n_arr, ctypes.POINTER(ctypes.c_int64)),
+                                      ctypes.cast(self._rk_arr, ctypes.POINTER(ctypes.c_int64)),
+                                      ctypes.cast(ph, ctypes.POINTER(ctypes.c_void_p)), 0), ph)
+
+    def _lazy_struct(self, kron=None, sum_=None) -> _lib.CTensor:
+        ptrs = _lib.ptr_array([p if p is not None else 0 for p in self._leaf_ptrs])
+        cs = _lib.CTensor(self.tree.d, ctypes.cast(self._n_arr, ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.cast(self._rk_arr, ctypes.POINTER(ctypes.c_int64)),
+                          ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), 0,
+                          ctypes.cast(ctypes.pointer(kron), ctypes.c_void_p) if kron is not None else None,
+                          ctypes.cast(ctypes.pointer(sum_), ctypes.c_void_p) if sum_ is not None else None)
+        return cs, ptrs
+
+    @property
+    def is_materialized(self) -> bool:
+        return self._dense is not None
+
+    def _materialize(self) -> HTensor:
+        if self._dense is None:
+            self._dense = self._materialize_now()
+            self._lazy = None
+        return self._dense
+
+    @property
+    def _nodes(self):
+        return self._materialize()._nodes
+
+    @property
+    def _arena(self):
+        return self._materialize()._arena
+
+    @property
+    def device(self) -> torch.device:
+        return self._dense.device if self._dense is not None else self._lazy_dev
+
+    def _shape(self, t: int) -> tuple:
+        if self._dense is not None:
+            return self._dense._shape(t)
+        node = self.tree.node(t)
+        rl = self._ranks_cached
+        if node.is_leaf:
+            return (self._sizes_cached[t], rl[t])
+        s1, s2 = node.sons
+        return (rl[s1], rl[s2]) if node.is_root else (rl[t], rl[s1], rl[s2])
+
+    def _c_trunc(self) -> _lib.CTensor:
+        if self._dense is not None:
+            return self._c()
+        if self._lazy_dev.index != torch.cuda.current_device():
+            raise ValueError(f"HTensor lives on cuda:{self._lazy_dev.index} but the current device is "
+                             f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device(...)")
+        return self._lazy[0]
+
+
+class AppliedHTensor(_LazyHTensor):
     """``apply_operator(op, x)`` with its transfer tensors kept in Kronecker form.
 
     The leaf frames V_t = [W_r U_t]_r are computed at once; the transfer tensors and
@@ -335,88 +443,85 @@ class AppliedHTensor(HTensor):
         ranks = {t: op.rank(t) * x.rank(t) for t in range(1, nn)}
         sizes = {leaf.index: int(op.leaf_shape(leaf.index)[0]) for leaf in tree.leaves}
         obj = cls.__new__(cls)
-        obj.tree = tree
-        obj.orthogonal = False
-        obj._cstruct = None
-        obj._op, obj._x = op, x
-        obj._dense = None
-        obj._ranks_cached = [1] + [ranks[t] for t in range(1, nn)]
-        obj._sizes_cached = dict(sizes)
-        obj._shape_cached = tuple(sizes[tree.leaf_for_dim(mu).index] for mu in range(1, tree.d + 1))
-        dev = x.device
-        leaf_ids = [leaf.index for leaf in tree.leaves]
-        offs, total = {}, 0
-        for t in leaf_ids:
-            offs[t] = total
-            total += sizes[t] * ranks[t]
-        arena = torch.empty(total, dtype=F64, device=dev)
-        base = arena.data_ptr()
-        n = _lib.i64_array(obj._shape_cached)
-        rk = _lib.i64_array(obj._ranks_cached)
         cop, cx = op._c(), x._c()
-        # leaf frames through the node-masked apply (inner nodes masked off: their
-        # pointers are placeholders the call never dereferences)
-        mask = (ctypes.c_uint8 * nn)(*[1 if tree.node(t).is_leaf else 0 for t in range(nn)])
-        tmp_ptrs = _lib.ptr_array([base + 8 * offs[t] if t in offs else base for t in range(nn)])
-        tmp = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
-                           ctypes.cast(rk, ctypes.POINTER(ctypes.c_int64)),
-                           ctypes.cast(tmp_ptrs, ctypes.POINTER(ctypes.c_void_p)), 0)
-        _lib.check(lib.ht_apply_operator_sharded(ctypes.byref(cop), cx, mask, tmp, _stream()), "apply_operator")
-        ptrs = _lib.ptr_array([base + 8 * offs[t] if t in offs else 0 for t in range(nn)])
+        obj._init_lazy(tree, sizes, ranks, x.device)
+        obj._op, obj._x = op, x
+        # leaf frames through the node-masked apply (inner nodes masked off)
+        _lib.check(lib.ht_apply_operator_sharded(ctypes.byref(cop), cx, obj._leaf_mask, obj._leaf_cs[0], _stream()),
+                   "apply_operator")
         src = _lib.CKronSrc(ctypes.pointer(cop), ctypes.pointer(cx))
-        cs = _lib.CTensor(tree.d, ctypes.cast(n, ctypes.POINTER(ctypes.c_int64)),
-                          ctypes.cast(rk, ctypes.POINTER(ctypes.c_int64)),
-                          ctypes.cast(ptrs, ctypes.POINTER(ctypes.c_void_p)), 0,
-                          ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
-        obj._kron = (cs, n, rk, ptrs, src, cop, cx, arena, dev.index)
+        cs, ptrs = obj._lazy_struct(kron=src)
+        obj._lazy = (cs, ptrs, src, cop, cx)
         return obj
 
-    # -- lazily materialised storage ---------------------------------------------
-    @property
-    def is_materialized(self) -> bool:
-        return self._dense is not None
+    def _materialize_now(self) -> HTensor:
+        lib = _lib.load()
+        ranks = {t: self._ranks_cached[t] for t in range(1, len(self.tree.nodes))}
+        out = HTensor.empty(self.tree, self._sizes_cached, ranks, device=self._lazy_dev)
+        _lib.check(lib.ht_apply_operator(ctypes.byref(self._op._c()), self._x._c(), out._c(), _stream()),
+                   "apply_operator")
+        self._op = self._x = None
+        return out
 
-    def _materialize(self) -> HTensor:
-        if self._dense is None:
-            lib = _lib.load()
-            ranks = {t: self._ranks_cached[t] for t in range(1, len(self.tree.nodes))}
-            out = HTensor.empty(self.tree, self._sizes_cached, ranks, device=self._x.device)
-            _lib.check(lib.ht_apply_operator(ctypes.byref(self._op._c()), self._x._c(), out._c(), _stream()),
-                       "apply_operator")
-            self._dense = out
-            self._kron = None
-            self._op = self._x = None
-        return self._dense
 
-    @property
-    def _nodes(self):
-        return self._materialize()._nodes
+class SumHTensor(_LazyHTensor):
+    """``add(a, c)`` (and sums of sums) held in block form: the leaf frames
+    [U_1 .. U_p] are concatenated at once, the block-diagonal transfer tensors and root
+    (reference arith.py:173-192) are NOT written to memory -- 1 - 1/p^2 of every inner
+    node would be structural zeros.  ``truncate`` / ``hierarchical_singular_values``
+    run the orthogonalisation sweep's mode products on the diagonal blocks
+    (``ht_tensor.sum`` in include/ht_b200.h); anything else
+    materialises the sum with the ordinary embedding kernel (same values as the eager
+    ``add``).  The terms are referenced, not copied: overwrite them only after the
+    sum has been consumed."""
 
-    @property
-    def _arena(self):
-        return self._materialize()._arena
+    @classmethod
+    def _build(cls, terms: list, a, c, out: "SumHTensor | None" = None) -> "SumHTensor":
+        """terms: [(alpha, ordinary HTensor)]; a, c: the two operands of this add (ordinary
+        tensors or unmaterialised sums), whose leaf frames are concatenated."""
+        lib = _lib.load()
+        tree = terms[0][1].tree
+        nn = len(tree.nodes)
+        ranks = {t: sum(x.rank(t) for _, x in terms) for t in range(1, nn)}
+        sizes = _sizes_by_node(terms[0][1])
+        if out is not None and out._dense is None and out._ranks_cached[1:] == [ranks[t] for t in range(1, nn)] \
+                and out._sizes_cached == sizes and out._lazy_dev == terms[0][1].device:
+            obj, arena = out, out._leaf_arena
+        else:
+            obj, arena = cls.__new__(cls), None
+        obj._init_lazy(tree, sizes, ranks, terms[0][1].device, arena)
+        obj._terms = list(terms)
+        _lib.check(lib.ht_add_sharded(_leaf_view(a), _leaf_view(c), 1.0, obj._leaf_mask, obj._leaf_cs[0], _stream()),
+                   "add")
+        structs = [x._c() for _, x in terms]
+        tarr = (ctypes.POINTER(_lib.CTensor) * len(terms))(*[ctypes.pointer(cs) for cs in structs])
+        alphas = (ctypes.c_double * len(terms))(*[float(al) for al, _ in terms])
+        src = _lib.CSumSrc(len(terms), tarr, alphas)
+        cs, ptrs = obj._lazy_struct(sum_=src)
+        obj._lazy = (cs, ptrs, src, tarr, alphas, structs)
+        return obj
 
-    @property
-    def device(self) -> torch.device:
-        return self._dense.device if self._dense is not None else self._x.device
+    def _materialize_now(self) -> HTensor:
+        acc = None
+        for alpha, x in self._terms:
+            acc = x if acc is None else _add(acc, x, alpha, lazy=False)
+        self._terms = None
+        return acc
 
-    def _shape(self, t: int) -> tuple:
-        if self._dense is not None:
-            return self._dense._shape(t)
-        node = self.tree.node(t)
-        rl = self._ranks_cached
-        if node.is_leaf:
-            return (self._sizes_cached[t], rl[t])
-        s1, s2 = node.sons
-        return (rl[s1], rl[s2]) if node.is_root else (rl[t], rl[s1], rl[s2])
 
-    def _c_trunc(self) -> _lib.CTensor:
-        if self._dense is not None:
-            return self._c()
-        if self._kron[8] != torch.cuda.current_device():
-            raise ValueError(f"HTensor lives on cuda:{self._kron[8]} but the current device is "
-                             f"cuda:{torch.cuda.current_device()}; call under torch.cuda.device(...)")
-        return self._kron[0]
+def _leaf_view(x: HTensor) -> _lib.CTensor:
+    """C view good for the leaf frames of x (what the node-masked add reads)."""
+    if isinstance(x, _LazyHTensor) and x._dense is None:
+        return x._leaf_cs[0]
+    return x._c()
+
+
+def _sum_terms(x: HTensor, alpha: float) -> list:
+    if isinstance(x, SumHTensor) and x._dense is None and alpha in (1.0, -1.0):
+        return [(alpha * al, t) for al, t in x._terms]
+    if isinstance(x, _LazyHTensor):
+        x = x._materialize()
+    return [(alpha, x)]
 
 
 _lazy_apply = os.environ.get("HT_LAZY_APPLY", "1") != "0"
@@ -586,6 +691,6 @@ def _check_all():
     return _lib.load()
 
 
-__all__ = ["AppliedHTensor", "set_lazy_apply", "TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
+__all__ = ["AppliedHTensor", "SumHTensor", "set_lazy_apply", "set_lazy_add", "TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
            "orthogonalize", "compute_bhat", "truncate", "hierarchical_singular_values", "apply_operator",
            "gemm", "leaf_map", "synchronize"]

@@ -194,6 +194,16 @@ struct View {
     int rt = 1, r1 = 1, r2 = 1, kt = 1, k1 = 1, k2 = 1;
   };
   std::vector<KronNode> kron;
+  // Block-form sum (ht_tensor.sum): the diagonal blocks of every inner node and the root,
+  // not materialised (p[t] == nullptr there).  Empty for an ordinary tensor.
+  struct SumBlock {
+    const double* B = nullptr;  // term's (kt, k1, k2) transfer tensor / (k1, k2) root
+    double alpha = 1.0;         // root blocks only
+    int kt = 1, k1 = 1, k2 = 1;  // block extents (root: kt = 1)
+    int ot = 0, o1 = 0, o2 = 0;  // block offsets in the node's (k_t, k_1, k_2)
+  };
+  std::vector<std::vector<SumBlock>> sum;
+  bool lazy() const { return !kron.empty() || !sum.empty(); }
   bool on(int t) const { return mask.empty() || mask[t] != 0; }
   bool needed(int t) const {
     return owned.empty() || owned[t] != 0 || (t > 0 && owned[T->father[t]] != 0);
@@ -213,6 +223,23 @@ int make_view(const ht_tensor* x, View& v, bool need_ptrs = true, bool allow_kro
     return kErrShape;
   }
   const ht_kron_src* ks = x->kron;
+  const ht_sum_src* ss = x->sum;
+  if (ss && (!allow_kron || ks)) {
+    set_error("a block-form sum (unmaterialised add result) is accepted by truncate only");
+    return kErrUnsupported;
+  }
+  if (ss) {
+    bool ok = ss->count >= 2 && ss->term && ss->alpha && !x->orthogonal;
+    for (int q = 0; ok && q < ss->count; ++q) {
+      const ht_tensor* tq = ss->term[q];
+      ok = tq && !tq->kron && !tq->sum && tq->d == x->d && tq->rank && tq->n;
+      for (int mu = 0; ok && mu < x->d; ++mu) ok = tq->n[mu] == x->n[mu];
+    }
+    if (!ok) {
+      set_error("malformed block-form sum");
+      return kErrArgument;
+    }
+  }
   if (ks && !allow_kron) {
     set_error("a Kronecker-form tensor (unmaterialised apply_operator result) is accepted by truncate only");
     return kErrUnsupported;
@@ -227,6 +254,8 @@ int make_view(const ht_tensor* x, View& v, bool need_ptrs = true, bool allow_kro
   v.k.assign(T.nn, 1);
   v.p.assign(T.nn, nullptr);
   v.kron.clear();
+  v.sum.clear();
+  if (ss) v.sum.assign(T.nn, {});
   v.orth = x->orthogonal != 0;
   for (int t = 0; t < T.nn; ++t) {
     v.k[t] = t == 0 ? 1 : x->rank[t];
@@ -240,6 +269,41 @@ int make_view(const ht_tensor* x, View& v, bool need_ptrs = true, bool allow_kro
         set_error("leaf size must be >= 1");
         return kErrShape;
       }
+    }
+    if (ss) {
+      long long tot = 0;
+      for (int q = 0; q < ss->count; ++q) tot += t == 0 ? 0 : ss->term[q]->rank[t];
+      if (t > 0 && tot != x->rank[t]) {
+        set_error("block-form sum: rank of node " + std::to_string(t) + " must be the sum of the terms' ranks");
+        return kErrShape;
+      }
+    }
+    if (ss && !T.leaf(t)) {
+      const int s1 = T.son1[t], s2 = T.son2[t];
+      int ot = 0, o1 = 0, o2 = 0;
+      for (int q = 0; q < ss->count; ++q) {
+        const ht_tensor* tq = ss->term[q];
+        View::SumBlock b;
+        b.kt = t == 0 ? 1 : (int)tq->rank[t];
+        b.k1 = (int)tq->rank[s1]; b.k2 = (int)tq->rank[s2];
+        b.ot = ot; b.o1 = o1; b.o2 = o2;
+        b.alpha = t == 0 ? ss->alpha[q] : 1.0;
+        if (b.kt < 1 || b.k1 < 1 || b.k2 < 1) {
+          set_error("block-form sum: term ranks must be >= 1");
+          return kErrShape;
+        }
+        if (need_ptrs) {
+          if (!tq->node || !tq->node[t]) {
+            set_error("missing device pointer for term " + std::to_string(q) + " of node " + std::to_string(t));
+            return kErrArgument;
+          }
+          b.B = tq->node[t];
+        }
+        if (t > 0) ot += b.kt;
+        o1 += b.k1; o2 += b.k2;
+        v.sum[t].push_back(b);
+      }
+      continue;
     }
     if (ks && !T.leaf(t)) {
       View::KronNode kn;
@@ -562,6 +626,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     std::vector<SsDesc> sa2, sa3;
     std::vector<QrProblem> qs;
     std::vector<KronFactorDesc> kf;
+    std::vector<ZeroDesc> zs;
     std::vector<double*> T1s(T.nn, nullptr), Bps(T.nn, nullptr), Es(T.nn, nullptr);
     for (int t : chunk)
       if (!T.leaf(t) && x.on(t)) T1s[t] = scratch_ar.take(x.k[t] * ko[T.son1[t]] * x.k[T.son2[t]]);
@@ -589,6 +654,64 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       const long long kt = x.k[t], k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
       double* T1 = T1s[t];
       double* Bp = imp(t) ? op.out[t] : Bps[t];
+      if (!x.sum.empty()) {
+        // Block-form sum (arith.py:173-192, never materialised): both mode products run on
+        // the diagonal blocks only.  Block q (extents kq x k1q x k2q at offsets ot, o1, o2)
+        // sees the columns [o1, o1 + k1q) of R1: rows J < o1 dense, rows [o1, o1 + k1q)
+        // upper triangular, nothing below -- so its slab of T1 is written for J < lim1 and
+        // l in the block, and its slab of Bp for J < lim1, L < lim2; the rest of the slab is
+        // structurally zero (zero-filled once, before the products).
+        for (const View::SumBlock& b : x.sum[t]) {
+          const long long kq = b.kt, k1q = b.k1, k2q = b.k2;
+          const long long lim1 = std::min<long long>(b.o1 + k1q, k1o), lim2 = std::min<long long>(b.o2 + k2q, k2o);
+          double* Tq = T1 ? T1 + (long long)b.ot * k1o * k2 + b.o2 : nullptr;   // T1[(ot+i), J, (o2+l)]
+          double* Bq = Bp ? Bp + (long long)b.ot * k1o * k2o : nullptr;          // Bp[(ot+i), J, L]
+          if (lim1 < k1o || lim2 < k2o) zs.push_back(ZeroDesc{Bq, kq * k1o * k2o});
+          if (lim1 <= 0 || lim2 <= 0) continue;
+          const double* R1q = op.R[s1] ? op.R[s1] + b.o1 : nullptr;  // R1[J, o1 + j]
+          const double* R2q = op.R[s2] ? op.R[s2] + b.o2 : nullptr;  // R2[L, o2 + l]
+          const long long d1 = std::min<long long>(b.o1, lim1), t1n = lim1 - d1;  // dense / triangular rows of R1's block
+          const long long d2 = std::min<long long>(b.o2, lim2), t2n = lim2 - d2;
+          // mode 2: T1_q[i, J, l] = sum_j R1[J, o1 + j] B_q[i, j, l]
+          if (ss_fits(std::max<long long>(d1, t1n), k1q)) {
+            if (d1 > 0) {
+              SsDesc d = ss_desc(b.B, 1, k2q, R1q, 1, k1, Tq, 1, k2, (int)(kq * k2q), (int)d1, (int)k1q);
+              d.M_lo = (int)k2q; d.x_hi = k1q * k2q; d.c_hi = k1o * k2;
+              sa2.push_back(d);
+            }
+            if (t1n > 0) {
+              SsDesc d = ss_desc(b.B, 1, k2q, R1q ? R1q + d1 * k1 : nullptr, 1, k1, Tq ? Tq + d1 * k2 : nullptr, 1, k2,
+                                 (int)(kq * k2q), (int)t1n, (int)k1q);
+              d.M_lo = (int)k2q; d.x_hi = k1q * k2q; d.c_hi = k1o * k2;
+              d.s_tri = 1;  // S(j, n) = R1[o1 + n, o1 + j] = 0 for j < n
+              sa2.push_back(d);
+            }
+          } else {
+            GemmDesc g = gemm_desc(R1q, k1, 1, b.B, k2q, 1, Tq, k2, 1, (int)lim1, (int)k2q, (int)k1q);
+            g.nb1 = (int)kq; g.a_b1 = 0; g.b_b1 = k1q * k2q; g.c_b1 = k1o * k2;
+            g2.push_back(g);
+          }
+          // mode 3: Bp_q[i, J, L] = sum_l T1_q[i, J, l] R2[L, o2 + l]   (J < lim1)
+          if (ss_fits(std::max<long long>(d2, t2n), k2q)) {
+            if (d2 > 0) {
+              SsDesc d = ss_desc(Tq, k2, 1, R2q, 1, k2, Bq, k2o, 1, (int)(kq * lim1), (int)d2, (int)k2q);
+              d.M_lo = (int)lim1; d.x_hi = k1o * k2; d.c_hi = k1o * k2o;
+              sa3.push_back(d);
+            }
+            if (t2n > 0) {
+              SsDesc d = ss_desc(Tq, k2, 1, R2q ? R2q + d2 * k2 : nullptr, 1, k2, Bq ? Bq + d2 : nullptr, k2o, 1,
+                                 (int)(kq * lim1), (int)t2n, (int)k2q);
+              d.M_lo = (int)lim1; d.x_hi = k1o * k2; d.c_hi = k1o * k2o;
+              d.s_tri = 1;
+              sa3.push_back(d);
+            }
+          } else {
+            GemmDesc g = gemm_desc(Tq, k2, 1, R2q, 1, k2, Bq, k2o, 1, (int)lim1, (int)lim2, (int)k2q);
+            g.nb1 = (int)kq; g.a_b1 = k1o * k2; g.b_b1 = 0; g.c_b1 = k1o * k2o;
+            g3.push_back(g);
+          }
+        }
+      } else {
       if (kr) {
         // Kronecker-form node F = H (x) B (arith.py:204-213), never materialised:
         //   T1[(a,i), J, (c,l)] = sum_j E_ac[J, j] B[i, j, l],  E_ac = sum_b H[a,b,c] R1[:, (b,:)]
@@ -634,6 +757,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       }
       else
         g3.push_back(gemm_desc(T1, k2, 1, op.R[s2], 1, k2, Bp, k2o, 1, (int)(kt * k1o), (int)k2o, (int)k2));
+      }
       // QR of M23(Bp): (k1o k2o) x kt column-major, in place as reflector storage
       QrProblem q{};
       q.A = Bp; q.a_r = 1; q.a_c = k1o * k2o;
@@ -694,6 +818,7 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
       merge_ss(sa2);
       merge_ss(sa3);
       HT_TRY(kron_factor_batched(kf, s));
+      HT_TRY(zero_batched(zs, s));
       HT_TRY(gemm_grouped(g2, s, "gemm_absorb"));
       HT_TRY(ss_gemm(sa2, s, "ss_absorb"));
       HT_TRY(gemm_grouped(g3, s, "gemm_absorb"));
@@ -719,13 +844,20 @@ int run_orthogonalize(const View& x, OrthPlan& op, Arena& ar, Arena& scratch_ar,
     const long long k1 = x.k[s1], k2 = x.k[s2], k1o = ko[s1], k2o = ko[s2];
     double* tmp = scratch_ar.take(k1o * k2);
     // Kronecker-form root H_D (x) B_D (arith.py:212-213): a k1 x k2 matrix, materialised here
-    double* xroot = x.kron.empty() ? x.p[0] : scratch_ar.take(k1 * k2);
+    double* xroot = !x.lazy() ? x.p[0] : scratch_ar.take(k1 * k2);
     scratch_max = std::max(scratch_max, scratch_ar.off);
     if (exec) {
       if (!x.kron.empty()) {
         const View::KronNode& kn = x.kron[0];
         std::vector<KronDesc> kd{KronDesc{xroot, kn.H, kn.B, 1, kn.r1, kn.r2, 1, kn.k1, kn.k2}};
         HT_TRY(kron_batched(kd, s));
+      }
+      if (!x.sum.empty()) {  // block-diagonal root with the terms' coefficients (arith.py:189-191)
+        std::vector<ZeroDesc> z{ZeroDesc{xroot, k1 * k2}};
+        HT_TRY(zero_batched(z, s));
+        std::vector<RootBlockDesc> rb;
+        for (const View::SumBlock& b : x.sum[0]) rb.push_back(RootBlockDesc{b.B, b.alpha, b.k1, b.k2, b.o1, b.o2});
+        HT_TRY(root_blocks(xroot, (int)k2, rb, s));
       }
       std::vector<GemmDesc> g{gemm_desc(op.R[s1], k1, 1, xroot, k2, 1, tmp, k2, 1, (int)k1o, (int)k2, (int)k1)};
       HT_TRY(gemm_grouped(g, s));
@@ -1082,6 +1214,10 @@ size_t truncate_ws_bytes(const View& x) {
     key.push_back(x.k[t]);
     key.push_back(x.owned.empty() ? 2 : x.owned[t]);
     if (!x.kron.empty()) key.push_back(((long long)x.kron[t].rt << 40) | ((long long)x.kron[t].r1 << 20) | x.kron[t].r2);
+    if (!x.sum.empty()) {
+      key.push_back(-11);
+      for (const auto& b : x.sum[t]) key.push_back(((long long)b.kt << 40) | ((long long)b.k1 << 20) | b.k2);
+    }
   }
   {
     std::lock_guard<std::mutex> lk(mu);
@@ -1155,12 +1291,17 @@ int phase_gram(TruncPlan& P, cudaStream_t s) {
 // status into it; ht_status() reads and clears it at the caller's next host sync.
 __device__ int g_sticky_status = 0;
 
-__global__ void sticky_or_kernel(const int* status) {
+// `skip`: the Cholesky-QR red flag of a speculative sweep -- when it is raised the whole
+// truncation is recomputed on the Householder path (which reports its own status), so
+// the garbage eigenproblems of the failed sweep must not leave an error behind
+__global__ void sticky_or_kernel(const int* status, const int* skip) {
+  if (skip && *skip) return;
   const int v = *status;
   if (v) atomicOr(&g_sticky_status, v);
 }
 
-int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t s, bool sticky = false) {
+int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t s, bool sticky = false,
+              const int* sticky_skip = nullptr) {
   const Tree& T = *x.T;
   std::vector<EigProblem> eps;
   for (int t = 1; t < T.nn; ++t) {
@@ -1207,7 +1348,7 @@ int phase_eig(const View& x, const ht_trunc_ctl* ctl, TruncPlan& P, cudaStream_t
   HT_TRY(eig_batched(eps, s));
   if (sticky) {
     ProfToken tok = prof_begin(s);
-    sticky_or_kernel<<<1, 1, 0, s>>>(P.status);
+    sticky_or_kernel<<<1, 1, 0, s>>>(P.status, sticky_skip);
     HT_LAUNCH_CHECK();
     prof_end(tok, "sticky_status", s, 0.0, 0.0);
   }
@@ -1222,7 +1363,9 @@ int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_
   HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
   HT_TRY(phase_orth(x, P, s, deferred, force_hh));
   HT_TRY(phase_gram(P, s));
-  return phase_eig(x, ctl, P, s, sticky);
+  // speculative Cholesky-QR sweep: its red flag voids the status of this pass
+  const bool spec = !force_hh && !x.orth && (g_qr_mode == 0 || g_qr_mode == 2);
+  return phase_eig(x, ctl, P, s, sticky, spec ? P.qr_fail : nullptr);
 }
 
 std::vector<long long> static_ranks(const View& x, const ht_trunc_ctl* ctl, bool& ok) {
@@ -1546,6 +1689,15 @@ std::vector<long long> shape_key(const View& v, const View& o, const ht_trunc_ct
     k.push_back(o.k[t]);
     k.push_back(ctl->max_rank_per_node ? ctl->max_rank_per_node[t] : -1);
   }
+  if (!v.sum.empty()) {  // block-form sum: block extents and the coefficients baked into the root expansion
+    k.push_back(-11);
+    for (int t = 0; t < nn; ++t)
+      for (const auto& b : v.sum[t]) {
+        long long abits;
+        memcpy(&abits, &b.alpha, sizeof(abits));
+        k.insert(k.end(), {(long long)t, (long long)b.kt, (long long)b.k1, (long long)b.k2, abits});
+      }
+  }
   return k;
 }
 
@@ -1555,6 +1707,9 @@ Addrs addresses(const View& v, const View& o, const void* ws) {
     a.in.push_back((uintptr_t)v.p[t]);
     a.out.push_back((uintptr_t)o.p[t]);
   }
+  if (!v.sum.empty())
+    for (int t = 0; t < v.T->nn; ++t)
+      for (const auto& b : v.sum[t]) a.in.push_back((uintptr_t)b.B);
   a.ws = (uintptr_t)ws;
   return a;
 }
@@ -1713,7 +1868,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   G->device = chk.used && chk.device;
   const int rc = capture_part(s, &G->g_rest, &G->rest, &b_rest, &c_rest, &G->n_rest, [&]() -> int {
     HT_TRY(phase_gram(P, s));
-    HT_TRY(phase_eig(v, ctl, P, s, true));
+    HT_TRY(phase_eig(v, ctl, P, s, true, G->chol ? P.qr_fail : nullptr));
     HT_TRY(truncate_phase2(v, ctl, ws, o, s));
     if (!G->device) return kOk;
     return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s);
@@ -1739,7 +1894,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   // workspace (2) ranges
   std::vector<RelocRange> ranges;
   for (int t = 0; t < v.T->nn; ++t) {
-    ranges.push_back({(uintptr_t)v.p[t], (uintptr_t)(v.p[t] + v.elems(t)), 0});
+    if (v.p[t]) ranges.push_back({(uintptr_t)v.p[t], (uintptr_t)(v.p[t] + v.elems(t)), 0});
     ranges.push_back({(uintptr_t)o.p[t], (uintptr_t)(o.p[t] + o.elems(t)), 1});
   }
   ranges.push_back({(uintptr_t)ws, (uintptr_t)ws + ws_bytes, 2});
@@ -1800,7 +1955,7 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
     const int seen_addr = ++g_graph_seen[address_key(skey, a)];
     TruncGraph* cand = nullptr;  // least recently used relocatable graph of these shapes
     for (auto* g : same)
-      if (g->relocatable() && uniform_move(g, a) && (!cand || g->used < cand->used)) cand = g;
+      if (!v.lazy() && g->relocatable() && uniform_move(g, a) && (!cand || g->used < cand->used)) cand = g;
     const bool capture = same.empty() ? seen_shape >= 2 : (seen_addr >= 2 && (same.size() < kMaxPerShape || !cand));
     if (!capture && cand) {
       if (relocate(cand, a) != kOk) {
@@ -2088,7 +2243,7 @@ int ht_orth_ranks(const ht_tensor* x, int64_t* out_rank) {
 
 int ht_orthogonalize_workspace_size(const ht_tensor* x, size_t* bytes) {
   View v;
-  HT_TRY(make_view(x, v, false));
+  HT_TRY(make_view(x, v, false, true));
   OrthPlan op;
   op.out.assign(v.T->nn, nullptr);
   Arena ar;
@@ -2099,7 +2254,7 @@ int ht_orthogonalize_workspace_size(const ht_tensor* x, size_t* bytes) {
 
 int ht_orthogonalize(const ht_tensor* x, void* ws, size_t ws_bytes, const ht_tensor* out, ht_stream_t stream) {
   View v, o;
-  HT_TRY(make_view(x, v));
+  HT_TRY(make_view(x, v, true, true));
   HT_TRY(out_view(out, v, o));
   auto ko = orth_ranks(v);
   for (int t = 1; t < v.T->nn; ++t)

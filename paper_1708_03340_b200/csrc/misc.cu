@@ -257,6 +257,84 @@ int kron_batched(const std::vector<KronDesc>& descs, cudaStream_t stream) {
   return kOk;
 }
 
+struct ZeroBatch {
+  int count;
+  int begin[MAXD + 1];
+  ZeroDesc d[MAXD];
+};
+
+__global__ void zero_kernel(const __grid_constant__ ZeroBatch b) {
+  const int di = find(b);
+  const ZeroDesc& z = b.d[di];
+  const long long stride = (long long)(b.begin[di + 1] - b.begin[di]) * blockDim.x;
+  long long x = (long long)(blockIdx.x - b.begin[di]) * blockDim.x + threadIdx.x;
+  if (!(reinterpret_cast<uintptr_t>(z.p) & 15)) {  // 16-byte stores over the aligned body
+    double2* p2 = reinterpret_cast<double2*>(z.p);
+    const long long n2 = z.count / 2;
+    for (long long i = x; i < n2; i += stride) p2[i] = make_double2(0.0, 0.0);
+    if ((z.count & 1) && x == 0) z.p[z.count - 1] = 0.0;
+  } else {
+    for (long long i = x; i < z.count; i += stride) z.p[i] = 0.0;
+  }
+}
+
+int zero_batched(const std::vector<ZeroDesc>& descs, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < descs.size()) {
+    ZeroBatch b;
+    b.count = 0;
+    int blocks = 0;
+    double bytes = 0;
+    while (i < descs.size() && b.count < MAXD) {
+      const ZeroDesc& d = descs[i++];
+      if (d.count <= 0) continue;
+      b.begin[b.count] = blocks;
+      blocks += blocks_for(d.count / 8);
+      b.d[b.count++] = d;
+      bytes += 8.0 * d.count;
+    }
+    if (!b.count) continue;
+    b.begin[b.count] = blocks;
+    ProfToken tok = prof_begin(stream);
+    zero_kernel<<<blocks, 256, 0, stream>>>(b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "zero_fill", stream, 0.0, bytes);
+  }
+  return kOk;
+}
+
+struct RootBlocks {
+  int count;
+  RootBlockDesc d[16];
+};
+
+__global__ void root_blocks_kernel(double* out, int cols, const __grid_constant__ RootBlocks b) {
+  const RootBlockDesc& q = b.d[blockIdx.y];
+  const int total = q.r * q.c;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
+    const int i = e / q.c, j = e - i * q.c;
+    out[(long long)(q.ro + i) * cols + q.co + j] = q.alpha * q.B[e];
+  }
+}
+
+int root_blocks(double* out, int cols, const std::vector<RootBlockDesc>& blocks, cudaStream_t stream) {
+  size_t i = 0;
+  while (i < blocks.size()) {
+    RootBlocks b;
+    b.count = 0;
+    int mx = 1;
+    while (i < blocks.size() && b.count < 16) {
+      mx = std::max(mx, blocks[i].r * blocks[i].c);
+      b.d[b.count++] = blocks[i++];
+    }
+    ProfToken tok = prof_begin(stream);
+    root_blocks_kernel<<<dim3(std::min((mx + 255) / 256, 64), b.count), 256, 0, stream>>>(out, cols, b);
+    HT_LAUNCH_CHECK();
+    prof_end(tok, "root_blocks", stream, 0.0, 0.0);
+  }
+  return kOk;
+}
+
 int kron_factor_batched(const std::vector<KronFactorDesc>& descs, cudaStream_t stream) {
   size_t i = 0;
   while (i < descs.size()) {

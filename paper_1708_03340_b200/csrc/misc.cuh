@@ -46,6 +46,23 @@ struct KronFactorDesc {
 };
 int kron_factor_batched(const std::vector<KronFactorDesc>& descs, cudaStream_t stream);
 
+// Zero-fill of contiguous runs (the structurally zero slabs of a block-form sum's
+// absorbed transfer tensors).
+struct ZeroDesc {
+  double* p;
+  long long count;
+};
+int zero_batched(const std::vector<ZeroDesc>& descs, cudaStream_t stream);
+
+// out (rows x cols row-major) = blockdiag_q(alpha_q * B_q), B_q (r_q x c_q) at (ro_q, co_q);
+// `out` must be zero-filled first.
+struct RootBlockDesc {
+  const double* B;
+  double alpha;
+  int r, c, ro, co;
+};
+int root_blocks(double* out, int cols, const std::vector<RootBlockDesc>& blocks, cudaStream_t stream);
+
 // Leaf operator column applied to U (n_in x k row-major), written into columns
 // [col0, col0+k) of V (n_out x ldv row-major).  kind 1: diagonal, kind 2: CSR.
 struct LeafApplyDesc {

@@ -131,3 +131,53 @@ def test_gaussian_factors_match_oracle_generator():
         assert all(np.array_equal(lv[t], o.U[t]) for t in o.U)
         assert all(np.array_equal(tf[t], o.B[t]) for t in o.B)
         assert np.array_equal(root, o.root)
+
+
+def test_kronecker_form_shape_queries_without_gpu():
+    """ht_tensor.kron (an unmaterialised apply_operator result, DESIGN 3.4): the
+    truncation's shape-only queries accept it, check rank = operator rank * tensor rank,
+    and every other entry point rejects it."""
+    import ctypes
+
+    from paper_1708_03340_b200 import _lib
+
+    lib = _lib.load()
+    d, nn = 4, 7
+    n = _lib.i64_array([64] * d)
+    xr = _lib.i64_array([1] + [30] * (nn - 1))
+    opr = _lib.i64_array([1] + [2] * (nn - 1))
+    yr = _lib.i64_array([1] + [60] * (nn - 1))
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    x = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(xr, i64p), None, 0)
+    op = _lib.COperator(d, ctypes.cast(opr, i64p), None, None)
+    src = _lib.CKronSrc(ctypes.pointer(op), ctypes.pointer(x))
+    y = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(yr, i64p), None, 0,
+                     ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
+    dense = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(yr, i64p), None, 0)
+    nb, nb_dense = ctypes.c_size_t(0), ctypes.c_size_t(0)
+    assert lib.ht_truncate_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == 0
+    assert lib.ht_truncate_workspace_size(ctypes.byref(dense), ctypes.byref(nb_dense)) == 0
+    assert nb.value >= nb_dense.value  # the E_ac operands live in the sweep's scratch
+    ctl = _lib.CTruncCtl(0.0, 30, None)
+    out = (ctypes.c_int64 * nn)()
+    assert lib.ht_truncate_static_ranks(ctypes.byref(y), ctypes.byref(ctl), out) == 1
+    assert list(out)[1:] == [30] * (nn - 1)
+    # rank chain of the Kronecker form
+    bad_r = _lib.i64_array([1] + [61] * (nn - 1))
+    ybad = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(bad_r, i64p), None, 0,
+                        ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
+    assert lib.ht_truncate_workspace_size(ctypes.byref(ybad), ctypes.byref(nb)) == _lib.HT_ERR_SHAPE
+    assert "operator rank" in _lib.last_error()
+    # not a truncation entry point
+    assert lib.ht_inner_product_workspace_size(ctypes.byref(y), ctypes.byref(y), ctypes.byref(nb)) \
+        == _lib.HT_ERR_UNSUPPORTED
+    assert lib.ht_orthogonalize_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == _lib.HT_ERR_UNSUPPORTED
+
+
+def test_relative_accuracy_control_sets_the_flag():
+    from paper_1708_03340_b200 import TruncationControl, _lib
+
+    c, _ = TruncationControl.relative_accuracy(1e-6, 50)._c(7)
+    assert c.flags == _lib.CTL_RELATIVE_EPS and c.eps == 1e-6 and c.max_rank == 50
+    c2, _ = TruncationControl.accuracy(1e-6)._c(7)
+    assert c2.flags == 0

@@ -126,7 +126,7 @@ def test_graph_relocation_whole_graph_update_path(cuda_ok):
         "tree = htb.build_balanced_tree(8)\n"
         "a = htb.gaussian_htensor(tree, 120, 12, 5)\n"
         "for c in (htb.gaussian_htensor(tree, 120, 12, 6), a):\n"
-        "    x = htb.add(a, c); ctl = htb.TruncationControl.fixed_rank(11)\n"
+        "    x = htb.add(a, c, lazy=False); ctl = htb.TruncationControl.fixed_rank(11)\n"
         "    htb.set_graph_mode(False); ref = _arrays(htb.truncate(x, ctl)); htb.set_graph_mode(True)\n"
         "    [htb.truncate(x, ctl) for _ in range(3)]\n"
         "    m0 = htb.graph_relocations(); keep = []\n"
