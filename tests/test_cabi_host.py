@@ -171,7 +171,44 @@ def test_kronecker_form_shape_queries_without_gpu():
     # not a truncation entry point
     assert lib.ht_inner_product_workspace_size(ctypes.byref(y), ctypes.byref(y), ctypes.byref(nb)) \
         == _lib.HT_ERR_UNSUPPORTED
-    assert lib.ht_orthogonalize_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == _lib.HT_ERR_UNSUPPORTED
+    assert lib.ht_gramians_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == _lib.HT_ERR_UNSUPPORTED
+    # the orthogonalisation sweep itself takes the structured form
+    assert lib.ht_orthogonalize_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == 0
+
+
+def test_block_form_sum_shape_queries_without_gpu():
+    """ht_tensor.sum (an unmaterialised add result, DESIGN 3.5): rank = sum of the terms'
+    ranks, accepted by the truncation / orthogonalisation queries only."""
+    import ctypes
+
+    from paper_1708_03340_b200 import _lib
+
+    lib = _lib.load()
+    d, nn = 8, 15
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    n = _lib.i64_array([200] * d)
+    ra, rc = _lib.i64_array([1] + [30] * (nn - 1)), _lib.i64_array([1] + [20] * (nn - 1))
+    ry = _lib.i64_array([1] + [50] * (nn - 1))
+    a = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(ra, i64p), None, 0)
+    c = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(rc, i64p), None, 0)
+    terms = (ctypes.POINTER(_lib.CTensor) * 2)(ctypes.pointer(a), ctypes.pointer(c))
+    alphas = (ctypes.c_double * 2)(1.0, -0.5)
+    src = _lib.CSumSrc(2, terms, alphas)
+    y = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(ry, i64p), None, 0, None,
+                     ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
+    nb = ctypes.c_size_t(0)
+    assert lib.ht_truncate_workspace_size(ctypes.byref(y), ctypes.byref(nb)) == 0 and nb.value > 0
+    ctl = _lib.CTruncCtl(0.0, 25, None)
+    out = (ctypes.c_int64 * nn)()
+    assert lib.ht_truncate_static_ranks(ctypes.byref(y), ctypes.byref(ctl), out) == 1
+    assert list(out)[1:] == [25] * (nn - 1)
+    bad = _lib.i64_array([1] + [51] * (nn - 1))
+    ybad = _lib.CTensor(d, ctypes.cast(n, i64p), ctypes.cast(bad, i64p), None, 0, None,
+                        ctypes.cast(ctypes.pointer(src), ctypes.c_void_p))
+    assert lib.ht_truncate_workspace_size(ctypes.byref(ybad), ctypes.byref(nb)) == _lib.HT_ERR_SHAPE
+    assert "sum of the terms" in _lib.last_error()
+    assert lib.ht_inner_product_workspace_size(ctypes.byref(y), ctypes.byref(y), ctypes.byref(nb)) \
+        == _lib.HT_ERR_UNSUPPORTED
 
 
 def test_relative_accuracy_control_sets_the_flag():
