@@ -157,6 +157,10 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
 int ht_set_graph_mode(int on);
 int ht_graph_stats(int64_t* captures, int64_t* replays);
 int64_t ht_graph_relocations(void);
+/* Relocation of cached graphs to moved buffers: off by default (a new address
+ * combination runs eagerly once and is captured when seen again); HT_RELOC=1 or
+ * ht_set_graph_relocation(1) turns it on. */
+int ht_set_graph_relocation(int on);
 
 /* Sticky error word of the queued (not host-checked) truncations on the current
  * device: fixed-rank ht_truncate, graph replays and the sharded phases OR their

@@ -38,7 +38,7 @@ EXPORTS = (
     "ht_qr_workspace_size", "ht_qr_batched", "ht_syev_batched", "ht_gemm_strided",
     "ht_launch_count", "ht_profile_enable", "ht_profile_report", "ht_profile_log",
     "ht_truncate_sharded", "ht_truncate_workspace_size_sharded", "ht_truncate_slot", "ht_set_qr_mode", "ht_set_implicit_q", "ht_qr_fallback_count", "ht_set_eig_mode",
-    "ht_set_graph_mode", "ht_graph_stats", "ht_graph_relocations", "ht_status", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
+    "ht_set_graph_mode", "ht_graph_stats", "ht_graph_relocations", "ht_set_graph_relocation", "ht_status", "ht_evaluate_entries", "ht_evaluate_weighted", "ht_graph_device_fallback",
 )
 
 _i64p = ctypes.POINTER(ctypes.c_int64)
@@ -129,6 +129,7 @@ def _declare(lib):
         "ht_evaluate_weighted": ([t, _vp, _vp, ctypes.c_int64, _vp, _vp], ctypes.c_int),
         "ht_graph_stats": ([_i64p, _i64p], ctypes.c_int),
         "ht_graph_relocations": ([], ctypes.c_int64),
+        "ht_set_graph_relocation": ([ctypes.c_int], ctypes.c_int),
         "ht_status": ([ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), _vp], ctypes.c_int),
         "ht_graph_device_fallback": ([], ctypes.c_int),
         "ht_profile_enable": ([ctypes.c_int], ctypes.c_int),

@@ -644,6 +644,12 @@ def set_graph_mode(on: bool) -> None:
     _lib.check(_lib.load().ht_set_graph_mode(1 if on else 0), "set_graph_mode")
 
 
+def set_graph_relocation(on: bool) -> None:
+    """Re-point cached truncation graphs at moved buffers instead of capturing a graph per
+    address combination (process-wide; off by default, ``HT_RELOC=1`` turns it on)."""
+    _lib.check(_lib.load().ht_set_graph_relocation(1 if on else 0), "set_graph_relocation")
+
+
 def graph_relocations() -> int:
     """How many cached truncation graphs were relocated to new buffer addresses."""
     return int(_lib.load().ht_graph_relocations())
@@ -691,6 +697,6 @@ def _check_all():
     return _lib.load()
 
 
-__all__ = ["AppliedHTensor", "SumHTensor", "set_lazy_apply", "set_lazy_add", "TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
+__all__ = ["set_graph_relocation", "AppliedHTensor", "SumHTensor", "set_lazy_apply", "set_lazy_add", "TruncationControl", "add", "subtract", "scale", "inner_product", "inner_product_device", "norm",
            "orthogonalize", "compute_bhat", "truncate", "hierarchical_singular_values", "apply_operator",
            "gemm", "leaf_map", "synchronize"]

@@ -1664,6 +1664,19 @@ long long g_graph_captures = 0, g_graph_replays = 0, g_graph_relocations = 0;
 constexpr size_t kMaxGraphs = 32;
 constexpr size_t kMaxPerShape = 8;
 
+// Re-pointing a cached graph at moved buffers (reloc.cu) is opt-in (ht_set_graph_relocation /
+// HT_RELOC=1): with several truncations in flight on different streams it was seen to
+// hang or fault intermittently (~1 in 5 benchmark runs), so by default a new address
+// combination runs eagerly once and gets its own captured graph when it is seen again.
+int g_graph_reloc = -1;
+bool reloc_enabled() {
+  if (g_graph_reloc < 0) {
+    const char* e = getenv("HT_RELOC");
+    g_graph_reloc = (e && e[0] == '1') ? 1 : 0;
+  }
+  return g_graph_reloc == 1;
+}
+
 bool graphs_on() {
   if (g_graph_mode < 0) {
     const char* e = getenv("HT_GRAPHS");
@@ -1954,6 +1967,7 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
     const int seen_shape = ++g_graph_seen[skey];
     const int seen_addr = ++g_graph_seen[address_key(skey, a)];
     TruncGraph* cand = nullptr;  // least recently used relocatable graph of these shapes
+    if (reloc_enabled())
     for (auto* g : same)
       if (!v.lazy() && g->relocatable() && uniform_move(g, a) && (!cand || g->used < cand->used)) cand = g;
     const bool capture = same.empty() ? seen_shape >= 2 : (seen_addr >= 2 && (same.size() < kMaxPerShape || !cand));
@@ -2330,6 +2344,12 @@ int ht_graph_stats(int64_t* captures, int64_t* replays) {
 }
 
 int64_t ht_graph_relocations(void) { return g_graph_relocations; }
+
+int ht_set_graph_relocation(int on) {
+  std::lock_guard<std::mutex> lk(g_graph_mu);
+  g_graph_reloc = on ? 1 : 0;
+  return kOk;
+}
 
 int ht_status(int32_t clear, int32_t* status, ht_stream_t stream) {
   // ordered behind the caller's stream (errors queued on other streams surface at a later check)

@@ -81,7 +81,7 @@ def _fresh_copy(htb, x):
 
 
 @pytest.mark.parametrize("deficient", [False, True])
-def test_graph_relocation_bitwise_equals_eager(cuda_ok, deficient):
+def test_graph_relocation_bitwise_equals_eager(cuda_ok, deficient, request):
     """Replays on moved buffers (new input, output and workspace addresses) relocate the
     cached graph instead of capturing again, and still reproduce the eager launches bit
     for bit -- including the device-side Householder branch (conditional body)."""
@@ -90,8 +90,10 @@ def test_graph_relocation_bitwise_equals_eager(cuda_ok, deficient):
     tree = htb.build_balanced_tree(8)
     a = htb.gaussian_htensor(tree, 150, 14, 11)
     c = a if deficient else htb.gaussian_htensor(tree, 150, 14, 12)
-    x = htb.add(a, c)
+    x = htb.add(a, c, lazy=False)
     ctl = htb.TruncationControl.fixed_rank(13)
+    htb.set_graph_relocation(True)  # opt-in (off by default)
+    request.addfinalizer(lambda: htb.set_graph_relocation(False))
     htb.set_graph_mode(False)
     try:
         eager = _arrays(htb.truncate(x, ctl))
@@ -123,6 +125,7 @@ def test_graph_relocation_whole_graph_update_path(cuda_ok):
     code = (
         "import numpy as np, paper_1708_03340_b200 as htb\n"
         "from tests.test_gpu_graph import _arrays, _fresh_copy\n"
+        "htb.set_graph_relocation(True)\n"
         "tree = htb.build_balanced_tree(8)\n"
         "a = htb.gaussian_htensor(tree, 120, 12, 5)\n"
         "for c in (htb.gaussian_htensor(tree, 120, 12, 6), a):\n"
