@@ -19,7 +19,9 @@ def htb(cuda_ok, request):
 
     m.set_qr_mode(request.param[0])
     m.set_implicit_q(request.param[1])
+    m.set_lazy_add(True, min_values=0)  # block form for the small test tensors too
     yield m
+    m.set_lazy_add(True, min_values=1 << 20)
     m.set_qr_mode("auto")
     m.set_implicit_q(True)
 

@@ -1,0 +1,70 @@
+"""BASELINE config C5 (d=256, n=2048, four rank-100 Gaussian tensors summed -> rank 400 ->
+truncated to rank 100) on ONE B200.  The materialised sum is 131.7 GB and the truncation
+workspace 140 GB, which is why the config is specified 8-way sharded; with the block-form
+sum (DESIGN 3.5) X is never written, so inputs (9.8 GB) + workspace fit in 180 GB.
+
+Checks (size-independent properties; the CPU oracle needs ~90 min for this config):
+  * ranks == 100 everywhere;
+  * err^2 = ||X - T||^2 from bilinear inner products of the TERMS (16 + 4 + 1 rank-100
+    inner products; X itself is never formed) against the hierarchical singular values of
+    X:  max_t tail_t <= err^2 <= sum_t tail_t  (quasi-optimality of the hierarchical SVD),
+    tail_t = sum_{i >= 100} sigma_{t,i}^2.
+
+python tools/c5_single_gpu.py [d] [n] [k]      (defaults 256 2048 100)"""
+import json
+import os
+import sys
+import time
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_1708_03340_b200 as htb  # noqa: E402
+
+d = int(sys.argv[1]) if len(sys.argv) > 1 else 256
+n = int(sys.argv[2]) if len(sys.argv) > 2 else 2048
+k = int(sys.argv[3]) if len(sys.argv) > 3 else 100
+free, total = torch.cuda.mem_get_info()
+need = 8 * (4 * (d * n * k + (d - 2) * k ** 3) + d * n * 4 * k + (d - 2) * (4 * k) ** 3 * 1.08 + (d - 2) * k ** 3)
+print(f"free {free / 1e9:.1f} GB of {total / 1e9:.1f}; estimated need {need / 1e9:.1f} GB", flush=True)
+if need > 0.97 * free:
+    print(json.dumps({"config": "C5 single GPU", "skipped": "not enough free device memory"}))
+    sys.exit(0)
+tree = htb.build_balanced_tree(d)
+t0 = time.time()
+parts = [htb.HTensor(tree, *htb.gaussian_factors(tree, n, k, 40 + s)) for s in range(4)]
+print(f"inputs on device after {time.time() - t0:.1f} s", flush=True)
+x = htb.add(htb.add(htb.add(parts[0], parts[1]), parts[2]), parts[3])
+assert isinstance(x, htb.SumHTensor) and not x.is_materialized and x.max_rank == 4 * k
+ctl = htb.TruncationControl.fixed_rank(k)
+
+
+def timed(fn):
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return r, e0.elapsed_time(e1)
+
+
+T, ms_first = timed(lambda: htb.truncate(x, ctl))
+T, ms = timed(lambda: htb.truncate(x, ctl))
+htb.synchronize()
+assert not x.is_materialized
+ranks = sorted(set(T.ranks.values()))
+xx = sum(htb.inner_product(p, q) for p in parts for q in parts)
+tx = sum(htb.inner_product(T, p) for p in parts)
+tt = htb.inner_product(T, T)
+err2 = xx - 2.0 * tx + tt
+del T
+torch.cuda.empty_cache()
+sig, ms_sig = timed(lambda: htb.hierarchical_singular_values(x))
+tails = [float((s[k:] ** 2).sum()) for s in sig.values()]
+out = {"config": "C5 on one B200 (block-form sum)", "d": d, "n": n, "K": 4 * k, "r": k, "truncate_ms": ms,
+       "first_call_ms": ms_first, "sigma_ms": ms_sig, "ranks_out": ranks, "norm2_X": xx, "err2": err2,
+       "rel_err": (max(err2, 0.0) / xx) ** 0.5, "max_tail": max(tails), "sum_tails": sum(tails),
+       "quasi_optimal": bool(max(tails) * (1 - 1e-8) <= err2 <= sum(tails) * (1 + 1e-8)),
+       "peak_device_GB": torch.cuda.max_memory_allocated() / 1e9, "gpu": torch.cuda.get_device_name(0)}
+print(json.dumps(out), flush=True)
