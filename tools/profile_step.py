@@ -2,7 +2,7 @@
 (--profile-from-start off).  Also writes the launch-order kernel tags of that step
 to gpurun_out/tags.json so ncu launch lists can be attributed to pipeline stages.
 
-    python tools/profile_step.py [d]"""
+    python tools/profile_step.py [d] [dense|block]      (block: the block-form sum, DESIGN 3.5)"""
 import json
 import os
 import sys
@@ -16,8 +16,9 @@ from paper_1708_03340_b200 import _lib  # noqa: E402
 d = int(sys.argv[1]) if len(sys.argv) > 1 else 64
 tree = htb.build_balanced_tree(d)
 p = d.bit_length() - 1
+block = len(sys.argv) > 2 and sys.argv[2] == "block"
 x = htb.add(htb.HTensor(tree, *htb.gaussian_factors(tree, 1000, 50, 2 * p)),
-            htb.HTensor(tree, *htb.gaussian_factors(tree, 1000, 50, 2 * p + 1)))
+            htb.HTensor(tree, *htb.gaussian_factors(tree, 1000, 50, 2 * p + 1)), lazy=block)
 ctl = htb.TruncationControl.fixed_rank(50)
 for _ in range(2):
     htb.truncate(x, ctl)
