@@ -215,9 +215,42 @@ def scale(a: HTensor, alpha: float) -> HTensor:
     return HTensor._wrap(a.tree, nodes, a.orthogonal)
 
 
+def _bilinear_terms(x: HTensor) -> list | None:
+    """[(alpha, term)] of an unmaterialised block-form sum, else None."""
+    if "SumHTensor" in globals() and isinstance(x, SumHTensor) and x._dense is None:
+        return list(x._terms)
+    return None
+
+
+def _inner_product_bilinear(a: HTensor, c: HTensor) -> torch.Tensor | None:
+    """<sum_i a_i A_i, sum_j c_j C_j> = sum_ij a_i c_j <A_i, C_j> for block-form sums: the
+    terms' (smaller-rank) inner products instead of a materialisation plus one inner
+    product at the summed ranks.  None when neither operand is an unmaterialised sum."""
+    ta, tc = _bilinear_terms(a), _bilinear_terms(c)
+    if ta is None and tc is None:
+        return None
+    same = a is c
+    ta = ta if ta is not None else [(1.0, a)]
+    tc = tc if tc is not None else [(1.0, c)]
+    acc = None
+    for i, (al, x) in enumerate(ta):
+        for j, (be, y) in enumerate(tc):
+            if same and j < i:
+                continue  # <A_i, A_j> = <A_j, A_i>
+            w = al * be * (2.0 if same and j > i else 1.0)
+            v = inner_product_device(x, y) * w
+            acc = v if acc is None else acc + v
+    return acc
+
+
 def inner_product(a: HTensor, c: HTensor) -> float:
     """arith.py:246-265 (returns a host float; one device->host read)."""
     _check_compatible(a, c)
+    bil = _inner_product_bilinear(a, c)
+    if bil is not None:
+        v = float(bil.item())
+        _lib.check_status()
+        return v
     lib = _lib.load()
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.ht_inner_product_workspace_size(a._c(), c._c(), ctypes.byref(nbytes)), "inner_product")
@@ -233,6 +266,9 @@ def inner_product(a: HTensor, c: HTensor) -> float:
 def inner_product_device(a: HTensor, c: HTensor) -> torch.Tensor:
     """Asynchronous variant: the inner product as a 1-element device tensor."""
     _check_compatible(a, c)
+    bil = _inner_product_bilinear(a, c)
+    if bil is not None:
+        return bil
     lib = _lib.load()
     nbytes = ctypes.c_size_t(0)
     _lib.check(lib.ht_inner_product_workspace_size(a._c(), c._c(), ctypes.byref(nbytes)), "inner_product")

@@ -169,3 +169,18 @@ def test_c4_rank_pattern_with_cholqr_fallback(htb, lazy):
     refe = orc.truncate(x, orc.Ctl(eps=eps, max_rank=20))
     assert to_host(Te).ranks == refe.ranks
     assert rel_err(to_host(Te), refe) <= 1e-10
+
+
+def test_inner_product_of_block_form_sums_is_bilinear(htb):
+    """<X, Y> for unmaterialised sums runs on the terms (no materialisation) and agrees
+    with the oracle's inner product of the materialised sums."""
+    tr = orc.balanced_tree(8)
+    a, c, e = (orc.gaussian_htensor(tr, 40, k, s) for k, s in ((6, 1), (5, 2), (4, 3)))
+    da, dc, de = to_dev(a), to_dev(c), to_dev(e)
+    x, xr = htb.subtract(htb.add(da, dc), de), orc.add(orc.add(a, c), orc.scale(e, -1.0))
+    y, yr = htb.add(de, da), orc.add(e, a)
+    np.testing.assert_allclose(htb.inner_product(x, x), orc.inner_product(xr, xr), rtol=1e-12)
+    np.testing.assert_allclose(htb.inner_product(x, y), orc.inner_product(xr, yr), rtol=1e-11)
+    np.testing.assert_allclose(htb.inner_product(x, dc), orc.inner_product(xr, c), rtol=1e-11)
+    np.testing.assert_allclose(htb.norm(x), orc.norm(xr), rtol=1e-12)
+    assert not x.is_materialized and not y.is_materialized
