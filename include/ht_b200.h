@@ -149,11 +149,11 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
 /* CUDA-graph replay of repeated fixed-rank truncations (process-wide, default on;
  * env HT_GRAPHS=0 turns it off at start-up).  The second ht_truncate call with the
  * same shapes, control and kernel policies captures the truncation as two graphs
- * (ORTH; GRAM + EIG + PROJECT) and later calls replay them.  Replays do not depend
- * on the buffers' addresses: a call whose input / output / workspace moved relocates
- * a cached graph of the same shapes (argument words shifted by each buffer's move)
- * instead of capturing again.  Results are identical to the eager launches (same
- * kernels, same arguments). */
+ * (ORTH; GRAM + EIG + PROJECT) and later calls with the same input / output /
+ * workspace addresses replay them; a new address combination runs eagerly once and gets
+ * its own graph when it is seen again (up to eight per shape), unless relocation is
+ * switched on (below).  Results are identical to the eager launches (same kernels, same
+ * arguments). */
 int ht_set_graph_mode(int on);
 int ht_graph_stats(int64_t* captures, int64_t* replays);
 int64_t ht_graph_relocations(void);
