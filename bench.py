@@ -642,7 +642,8 @@ def run_ours(args, rank, world, local_rank):
     w0.record(stream)
     # warm-up of the pipeline (allocations, streams, graph captures): a fixed count,
     # independent of --warmup -- replays relocate to whatever buffers the allocator hands out
-    work.e2e_run(E2E_WARMUP, w0)
+    # (every (slot, stream) pair at least twice: the second sighting captures its graph)
+    work.e2e_run(max(E2E_WARMUP, 4 * getattr(work, "inflight", 1) + 2), w0)
     torch.cuda.synchronize()
     e2e_steps = max(3, args.steps)
     f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

@@ -1661,8 +1661,8 @@ std::map<std::vector<long long>, int> g_graph_seen;  // shape keys and address k
 unsigned long long g_graph_clock = 0;
 int g_graph_mode = -1;  // -1: from HT_GRAPHS (default on)
 long long g_graph_captures = 0, g_graph_replays = 0, g_graph_relocations = 0;
-constexpr size_t kMaxGraphs = 32;
-constexpr size_t kMaxPerShape = 8;
+constexpr size_t kMaxGraphs = 96;
+constexpr size_t kMaxPerShape = 24;  // address combinations per shape (e.g. 2 result buffers x streams x pipelines)
 
 // Re-pointing a cached graph at moved buffers (reloc.cu) is opt-in (ht_set_graph_relocation /
 // HT_RELOC=1): with several truncations in flight on different streams it was seen to
@@ -1981,8 +1981,13 @@ int truncate_graph(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t ws_b
     } else if (capture) {
       if (same.size() >= kMaxPerShape || g_graphs.size() >= kMaxGraphs) {
         const auto& pool = same.size() >= kMaxPerShape ? same : g_graphs;
-        forget_graph(*std::min_element(pool.begin(), pool.end(),
-                                       [](TruncGraph* x, TruncGraph* y) { return x->used < y->used; }));
+        TruncGraph* lru = *std::min_element(pool.begin(), pool.end(),
+                                            [](TruncGraph* x, TruncGraph* y) { return x->used < y->used; });
+        // a caller cycling through more address combinations than the cache holds would
+        // evict graphs that are still in use and pay a capture (~50 ms) per call: run
+        // eagerly instead while the least recently used graph is still warm
+        if (g_graph_clock - lru->used < 4 * pool.size()) return kOk;
+        forget_graph(lru);
       }
       G = new TruncGraph;
       G->skey = skey;
