@@ -449,12 +449,15 @@ void merge_qrs(std::vector<QrProblem>& v) {
   while (i < v.size()) {
     QrProblem d = v[i];
     size_t j = i + 1;
-    if (j < v.size()) {
+    // only single-node problems merge: the list is merged twice (by the sweep and again by
+    // plan_qrs), and merging an already merged run with a same-shape neighbour would
+    // re-stride it and drop its inner nodes
+    if (j < v.size() && d.nodes == 1) {
       const long long dA = v[j].A - d.A, dQ = v[j].Q - d.Q, dR = v[j].R - d.R;
       while (j < v.size()) {
         const QrProblem& e = v[j];
         const long long c = (long long)(j - i);
-        bool same = e.m == d.m && e.K == d.K && e.a_r == d.a_r && e.a_c == d.a_c && e.q_r == d.q_r &&
+        bool same = e.nodes == 1 && e.m == d.m && e.K == d.K && e.a_r == d.a_r && e.a_c == d.a_c && e.q_r == d.q_r &&
                     e.q_c == d.q_c && e.r_ld == d.r_ld && e.A - d.A == c * dA && e.Q - d.Q == c * dQ &&
                     e.R - d.R == c * dR && (e.V == nullptr) == (d.V == nullptr) &&
                     (d.V == nullptr || e.V - d.V == c * (long long)d.m * d.K) &&

@@ -177,3 +177,37 @@ def test_syev_rejects_nonsymmetric(lib):
     S = np.array([[[1.0, 2.0], [0.0, 1.0]]])
     with pytest.raises(ValueError):
         _syev(lib, S)
+
+
+def test_qr_merge_keeps_every_node_of_irregularly_spaced_leaves(cuda_ok):
+    """Leaf frames of one shape at irregular spacing (pairs 12 doubles apart, the pairs 96 /
+    104 apart): the sweep merges each pair into a two-node QR problem, and the second
+    merge pass (plan_qrs) must not fuse the two pairs into one re-strided problem that
+    would drop a node of each (regression: NaN leaf frames)."""
+    import torch
+
+    import paper_1708_03340_b200 as htb
+    from oracle import htucker_oracle as orc
+    from tests.htconv import to_host
+
+    tr = orc.balanced_tree(4)
+    x = orc.gaussian_htensor(tr, 4, 3, 7)
+    buf = torch.full((512,), float("nan"), dtype=torch.float64, device="cuda")
+    offs = {3: 0, 4: 12, 5: 96, 6: 200}
+    leaves = {}
+    for t, o in offs.items():
+        leaves[t] = buf[o:o + 12].view(4, 3)
+        leaves[t].copy_(torch.from_numpy(x.U[t]))
+    tree = htb.build_balanced_tree(4)
+    dev = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()  # noqa: E731
+    xd = htb.HTensor(tree, leaves, {t: dev(b) for t, b in x.B.items()}, dev(x.root))
+    for mode in ("householder", "auto"):
+        htb.set_qr_mode(mode)
+        try:
+            o = to_host(htb.orthogonalize(xd))
+        finally:
+            htb.set_qr_mode("auto")
+        ref = orc.orthogonalize(x)
+        for (t, u), (_, v) in zip(o.arrays(), ref.arrays()):
+            assert np.all(np.isfinite(u)), f"node {t} not written ({mode})"
+            np.testing.assert_allclose(u, v, rtol=1e-10, atol=1e-12)
