@@ -242,3 +242,28 @@ def test_concurrent_truncations_on_streams_match_serial(cuda_ok):
     for o in outs:
         for u, v in zip(_arrays(o), ref):
             np.testing.assert_array_equal(u, v)
+
+
+def test_more_address_combinations_than_the_cache_run_eagerly(cuda_ok):
+    """A caller cycling through more result buffers than the graph cache holds (24 per
+    shape) must not pay a capture per call: warm graphs are never evicted, the overflow
+    runs eagerly, and every result equals the eager one."""
+    import paper_1708_03340_b200 as htb
+
+    tree = htb.build_balanced_tree(4)
+    x = htb.add(htb.gaussian_htensor(tree, 60, 7, 1), htb.gaussian_htensor(tree, 60, 7, 2), lazy=False)
+    ctl = htb.TruncationControl.fixed_rank(6)
+    htb.set_graph_mode(False)
+    try:
+        ref = _arrays(htb.truncate(x, ctl))
+    finally:
+        htb.set_graph_mode(True)
+    first = htb.truncate(x, ctl)
+    outs = [htb.HTensor.empty(tree, *first.host_layout()) for _ in range(30)]
+    c0, _ = htb.graph_stats()
+    for rnd in range(4):
+        for o in outs:
+            got = _arrays(htb.truncate(x, ctl, out=o))
+            assert all(np.array_equal(p, q) for p, q in zip(got, ref))
+    c1, r1 = htb.graph_stats()
+    assert c1 - c0 <= 26, f"{c1 - c0} captures for 30 rotating buffers: the cache is thrashing"
