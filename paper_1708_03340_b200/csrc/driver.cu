@@ -972,8 +972,12 @@ size_t orth_scratch_need(const View& x, OrthPlan op, const Arena& scratch_in) {
 // orthogonal tensor is Bp x_1 R^{-T}: the node's Gramian is then applied as
 // G~ = R^{-1} G R^{-T} to Bp (sum_{i1,i2} Q[i1,.] G[i1,i2] Q[i2,.] with Q[i,.] =
 // sum_m R^{-1}[m,i] Bp[m,.]), and the son Gramians come out in the same bases.
+// `blocks`: o.p[t] of the implicit-Q nodes are the absorbed tensors of a block-form sum as
+// the Cholesky-QR sweep left them (View::sum of the input, staircase zero pattern): row i of
+// block q vanishes outside the corner J < lim1_q, L < lim2_q, so the columns (J, L) of the
+// shell between two corners only see the rows i >= ot_q.
 int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar, cudaStream_t s, bool exec,
-                 const OrthPlan* imp = nullptr, const std::vector<double*>* Gt = nullptr) {
+                 const OrthPlan* imp = nullptr, const std::vector<double*>* Gt = nullptr, bool blocks = false) {
   const Tree& T = *o.T;
   // finish of son s's Gramian: sum the partials; implicit-Q sons also get G~_s
   auto finish = [&](const double* P, int S, int son) {
@@ -1056,7 +1060,29 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
       double* t1 = t1s[t];
       // t1 (kt x k1k2) = G_t (kt x kt) * M1(B)   (arith.py:155); streamed as
       // t1^T = M1(B)^T G_t^T with G_t resident in shared memory
-      if (ss_fits(kt, kt))
+      const bool staircase = blocks && ss_fits(kt, kt) && imp && !imp->imp.empty() && imp->imp[t] && Gt &&
+                             (*Gt)[t] && !o.sum.empty() && o.sum[t].size() >= 2;
+      if (staircase) {
+        long long prev1 = 0, prev2 = 0;
+        for (const View::SumBlock& b : o.sum[t]) {
+          const long long lim1 = std::min<long long>(b.o1 + b.k1, k1), lim2 = std::min<long long>(b.o2 + b.k2, k2);
+          const long long kc = kt - b.ot;  // rows i >= ot_q contribute to this shell
+          const double* Xq = o.p[t] ? o.p[t] + (long long)b.ot * f : nullptr;
+          const double* Sq = gop(t) ? gop(t) + b.ot : nullptr;
+          auto rect = [&](long long j0, long long j1, long long l0, long long l1) {
+            if (j1 <= j0 || l1 <= l0 || kc <= 0) return;
+            const long long base = j0 * k2 + l0;
+            SsDesc d = ss_desc(Xq ? Xq + base : nullptr, 1, f, Sq, 1, kt, t1 ? t1 + base : nullptr, 1, f,
+                               (int)((j1 - j0) * (l1 - l0)), (int)kt, (int)kc);
+            d.M_lo = (int)(l1 - l0); d.x_hi = k2; d.c_hi = k2;
+            s1s.push_back(d);
+          };
+          rect(prev1, lim1, 0, lim2);      // J in [prev1, lim1), L < lim2
+          rect(0, prev1, prev2, lim2);     // J < prev1, L in [prev2, lim2)
+          prev1 = std::max(prev1, lim1);
+          prev2 = std::max(prev2, lim2);
+        }
+      } else if (ss_fits(kt, kt))
         s1s.push_back(ss_desc(o.p[t], 1, f, gop(t), 1, kt, t1, 1, f, (int)f, (int)kt, (int)kt));
       else
         g1s.push_back(gemm_desc(gop(t), kt, 1, o.p[t], f, 1, t1, f, 1, (int)kt, (int)f, (int)kt));
@@ -1283,9 +1309,9 @@ int phase_orth(const View& x, TruncPlan& P, cudaStream_t s, OrthCheck* deferred 
   return orth_sweep(x, P.op, P.scratch, s, P.qr_fail, deferred, force_hh);
 }
 
-int phase_gram(TruncPlan& P, cudaStream_t s) {
+int phase_gram(TruncPlan& P, cudaStream_t s, bool blocks = false) {
   Arena sc = P.scratch;
-  return run_gramians(P.o, P.G, sc, s, true, &P.op, &P.Gt);
+  return run_gramians(P.o, P.G, sc, s, true, &P.op, &P.Gt, blocks);
 }
 
 // batched eigendecomposition + select_rank of the (masked) non-root nodes
@@ -1365,9 +1391,9 @@ int truncate_phase1(const View& x, const ht_trunc_ctl* ctl, char* ws, size_t ws_
   HT_TRY(plan_truncate(x, P, ws));
   HT_CUDA_CHECK(cudaMemsetAsync(P.status, 0, sizeof(int), s));
   HT_TRY(phase_orth(x, P, s, deferred, force_hh));
-  HT_TRY(phase_gram(P, s));
   // speculative Cholesky-QR sweep: its red flag voids the status of this pass
   const bool spec = !force_hh && !x.orth && (g_qr_mode == 0 || g_qr_mode == 2);
+  HT_TRY(phase_gram(P, s, spec));
   return phase_eig(x, ctl, P, s, sticky, spec ? P.qr_fail : nullptr);
 }
 
@@ -1883,7 +1909,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   G->chol = chk.used;
   G->device = chk.used && chk.device;
   const int rc = capture_part(s, &G->g_rest, &G->rest, &b_rest, &c_rest, &G->n_rest, [&]() -> int {
-    HT_TRY(phase_gram(P, s));
+    HT_TRY(phase_gram(P, s, G->chol));
     HT_TRY(phase_eig(v, ctl, P, s, true, G->chol ? P.qr_fail : nullptr));
     HT_TRY(truncate_phase2(v, ctl, ws, o, s));
     if (!G->device) return kOk;
