@@ -1411,7 +1411,10 @@ std::vector<long long> static_ranks(const View& x, const ht_trunc_ctl* ctl, bool
   return r;
 }
 
-int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View& out, cudaStream_t s) {
+// `blocks`: as in run_gramians -- the workspace holds the result of a Cholesky-QR sweep over
+// a block-form sum, so the mode-1 products of its implicit-Q nodes follow the staircase.
+int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View& out, cudaStream_t s,
+                    bool blocks = false) {
   TruncPlan P;
   HT_TRY(plan_truncate(x, P, ws));
   const Tree& T = *x.T;
@@ -1466,7 +1469,28 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
     const long long k1 = o.k[s1], k2 = o.k[s2], r1 = out.k[s1], r2 = out.k[s2];
     // mode 1: C1 (rt x k1k2) = EV_t^T[:rt] * M1(B)   (arith.py:168); streamed as C1^T = M1(B)^T EV_t
     const long long ev_ld = pev_ld[t] ? pev_ld[t] : kt;
-    if (ss_fits(rt, kt))
+    const bool staircase = blocks && ss_fits(rt, kt) && !P.op.imp.empty() && P.op.imp[t] && !o.sum.empty() &&
+                           o.sum[t].size() >= 2;
+    if (staircase) {
+      const long long f = k1 * k2;
+      long long prev1 = 0, prev2 = 0;
+      for (const View::SumBlock& b : o.sum[t]) {
+        const long long lim1 = std::min<long long>(b.o1 + b.k1, k1), lim2 = std::min<long long>(b.o2 + b.k2, k2);
+        const long long kc = kt - b.ot;  // rows i >= ot_q reach this shell of columns (J, L)
+        auto rect = [&](long long j0, long long j1, long long l0, long long l1) {
+          if (j1 <= j0 || l1 <= l0 || kc <= 0) return;
+          const long long base = j0 * k2 + l0;
+          SsDesc d = ss_desc(o.p[t] + (long long)b.ot * f + base, 1, f, PEV[t] + (long long)b.ot * ev_ld, ev_ld, 1,
+                             C1[t] + base, 1, f, (int)((j1 - j0) * (l1 - l0)), (int)rt, (int)kc);
+          d.M_lo = (int)(l1 - l0); d.x_hi = k2; d.c_hi = k2;
+          ss1.push_back(d);
+        };
+        rect(prev1, lim1, 0, lim2);
+        rect(0, prev1, prev2, lim2);
+        prev1 = std::max(prev1, lim1);
+        prev2 = std::max(prev2, lim2);
+      }
+    } else if (ss_fits(rt, kt))
       ss1.push_back(ss_desc(o.p[t], 1, k1 * k2, PEV[t], ev_ld, 1, C1[t], 1, k1 * k2, (int)(k1 * k2), (int)rt, (int)kt));
     else
       st1.push_back(gemm_desc(PEV[t], 1, ev_ld, o.p[t], k1 * k2, 1, C1[t], k1 * k2, 1, (int)rt, (int)(k1 * k2), (int)kt));
@@ -1911,7 +1935,7 @@ int capture_truncation(const View& v, const ht_trunc_ctl* ctl, char* ws, size_t 
   const int rc = capture_part(s, &G->g_rest, &G->rest, &b_rest, &c_rest, &G->n_rest, [&]() -> int {
     HT_TRY(phase_gram(P, s, G->chol));
     HT_TRY(phase_eig(v, ctl, P, s, true, G->chol ? P.qr_fail : nullptr));
-    HT_TRY(truncate_phase2(v, ctl, ws, o, s));
+    HT_TRY(truncate_phase2(v, ctl, ws, o, s, G->chol));
     if (!G->device) return kOk;
     return capture_device_fallback(v, ctl, ws, ws_bytes, o, P.qr_fail, s);
   });
@@ -2153,7 +2177,7 @@ int ht_truncate(const ht_tensor* x, const ht_trunc_ctl* ctl, void* ws, size_t ws
   if (!ran) {
     OrthCheck chk;
     HT_TRY(truncate_phase1(v, ctl, (char*)ws, ws_bytes, P, s, &chk, false, true));
-    HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s));
+    HT_TRY(truncate_phase2(v, ctl, (char*)ws, o, s, !v.orth && (g_qr_mode == 0 || g_qr_mode == 2)));
     // the speculative result stands unless the Cholesky-QR flag was raised; then the
     // whole truncation is recomputed on the Householder path (stream order overwrites)
     HT_TRY(check_result(chk, failed));
