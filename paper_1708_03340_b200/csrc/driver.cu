@@ -1033,6 +1033,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     if (inner.empty()) continue;
     std::vector<GemmDesc> g1s, g2s;
     std::vector<SsDesc> s1s;
+    std::vector<std::vector<SsDesc>> s1k;  // staircase descriptors by kind
     std::vector<GramFinDesc> rs;
     long long tiles = 0;
     for (int t : inner) {
@@ -1069,16 +1070,20 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
           const long long kc = kt - b.ot;  // rows i >= ot_q contribute to this shell
           const double* Xq = o.p[t] ? o.p[t] + (long long)b.ot * f : nullptr;
           const double* Sq = gop(t) ? gop(t) + b.ot : nullptr;
-          auto rect = [&](long long j0, long long j1, long long l0, long long l1) {
+          const size_t q = (size_t)(&b - o.sum[t].data());
+          // descriptors of one kind (block, rectangle) are kept together across the level's
+          // nodes so that merge_ss turns each kind into one multi-job descriptor
+          auto rect = [&](size_t kind, long long j0, long long j1, long long l0, long long l1) {
             if (j1 <= j0 || l1 <= l0 || kc <= 0) return;
             const long long base = j0 * k2 + l0;
             SsDesc d = ss_desc(Xq ? Xq + base : nullptr, 1, f, Sq, 1, kt, t1 ? t1 + base : nullptr, 1, f,
                                (int)((j1 - j0) * (l1 - l0)), (int)kt, (int)kc);
             d.M_lo = (int)(l1 - l0); d.x_hi = k2; d.c_hi = k2;
-            s1s.push_back(d);
+            if (s1k.size() <= kind) s1k.resize(kind + 1);
+            s1k[kind].push_back(d);
           };
-          rect(prev1, lim1, 0, lim2);      // J in [prev1, lim1), L < lim2
-          rect(0, prev1, prev2, lim2);     // J < prev1, L in [prev2, lim2)
+          rect(2 * q, prev1, lim1, 0, lim2);          // J in [prev1, lim1), L < lim2
+          rect(2 * q + 1, 0, prev1, prev2, lim2);     // J < prev1, L in [prev2, lim2)
           prev1 = std::max(prev1, lim1);
           prev2 = std::max(prev2, lim2);
         }
@@ -1104,6 +1109,7 @@ int run_gramians(const View& o, const std::vector<double*>& G, Arena& scratch_ar
     mx = std::max(mx, scratch_ar.off);
     if (exec) {
       HT_TRY(gram_finish(pre, s));
+      for (auto& k : s1k) s1s.insert(s1s.end(), k.begin(), k.end());
       merge_gemms(g1s);
       merge_ss(s1s);
       HT_TRY(gemm_grouped(g1s, s, "gemm_gram_t1"));
@@ -1434,6 +1440,7 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   Arena sc = P.scratch;
   std::vector<GemmDesc> st1, st2, st3;
   std::vector<SsDesc> ss1, ss2, ss3;
+  std::vector<std::vector<SsDesc>> ss1k;  // staircase mode-1 descriptors by kind (merged across nodes)
   std::vector<double*> C1(T.nn, nullptr), C2(T.nn, nullptr);
   for (int t : chunk)
     if (t != 0 && !T.leaf(t)) C1[t] = sc.take(out.k[t] * o.k[T.son1[t]] * o.k[T.son2[t]]);
@@ -1477,16 +1484,18 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
       for (const View::SumBlock& b : o.sum[t]) {
         const long long lim1 = std::min<long long>(b.o1 + b.k1, k1), lim2 = std::min<long long>(b.o2 + b.k2, k2);
         const long long kc = kt - b.ot;  // rows i >= ot_q reach this shell of columns (J, L)
-        auto rect = [&](long long j0, long long j1, long long l0, long long l1) {
+        const size_t q = (size_t)(&b - o.sum[t].data());
+        auto rect = [&](size_t kind, long long j0, long long j1, long long l0, long long l1) {
           if (j1 <= j0 || l1 <= l0 || kc <= 0) return;
           const long long base = j0 * k2 + l0;
           SsDesc d = ss_desc(o.p[t] + (long long)b.ot * f + base, 1, f, PEV[t] + (long long)b.ot * ev_ld, ev_ld, 1,
                              C1[t] + base, 1, f, (int)((j1 - j0) * (l1 - l0)), (int)rt, (int)kc);
           d.M_lo = (int)(l1 - l0); d.x_hi = k2; d.c_hi = k2;
-          ss1.push_back(d);
+          if (ss1k.size() <= kind) ss1k.resize(kind + 1);
+          ss1k[kind].push_back(d);
         };
-        rect(prev1, lim1, 0, lim2);
-        rect(0, prev1, prev2, lim2);
+        rect(2 * q, prev1, lim1, 0, lim2);
+        rect(2 * q + 1, 0, prev1, prev2, lim2);
         prev1 = std::max(prev1, lim1);
         prev2 = std::max(prev2, lim2);
       }
@@ -1521,6 +1530,8 @@ int truncate_phase2(const View& x, const ht_trunc_ctl* ctl, char* ws, const View
   }
   merge_gemms(gpe);
   HT_TRY(gemm_grouped(gpe, s, "gemm_project_rinv"));
+  for (auto& k : ss1k) ss1.insert(ss1.end(), k.begin(), k.end());
+  ss1k.clear();
   merge_gemms(st1);
   merge_gemms(st2);
   merge_gemms(st3);
