@@ -184,3 +184,27 @@ def test_inner_product_of_block_form_sums_is_bilinear(htb):
     np.testing.assert_allclose(htb.inner_product(x, dc), orc.inner_product(xr, c), rtol=1e-11)
     np.testing.assert_allclose(htb.norm(x), orc.norm(xr), rtol=1e-12)
     assert not x.is_materialized and not y.is_materialized
+
+
+def test_three_unequal_terms_staircase(htb):
+    """Three terms of unequal, node-dependent ranks (the staircase of corners has three
+    steps of different sizes), fixed-rank (graph-captured on repeat) and accuracy control."""
+    tr = orc.balanced_tree(8)
+    rk = lambda base: {t: base + (t % 3) for t in range(1, 15)}  # noqa: E731
+    a = orc.gaussian_htensor(tr, 60, rk(4), 21)
+    c = orc.gaussian_htensor(tr, 60, rk(3), 22)
+    e = orc.gaussian_htensor(tr, 60, rk(5), 23)
+    x = orc.add(orc.add(a, orc.scale(c, -1.0)), e)
+    xd = htb.add(htb.subtract(to_dev(a), to_dev(c)), to_dev(e))
+    assert isinstance(xd, htb.SumHTensor) and len(xd._terms) == 3
+    ref = orc.truncate(x, orc.Ctl(max_rank=6))
+    for _ in range(3):  # eager, capture, replay
+        T = htb.truncate(xd, htb.TruncationControl.fixed_rank(6))
+        assert to_host(T).ranks == ref.ranks
+        assert rel_err(to_host(T), ref) <= 1e-10
+    eps = 0.2 * orc.norm(x)
+    Te = htb.truncate(xd, htb.TruncationControl.accuracy(eps))
+    refe = orc.truncate(x, orc.Ctl(eps=eps))
+    assert to_host(Te).ranks == refe.ranks
+    assert rel_err(to_host(Te), refe) <= 1e-10
+    assert not xd.is_materialized
